@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""bench.py — candidate allocations scored per second (and time-to-optimal-plan) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1; one rank per GPU)
+
+A step is one pass of the whole planning path over one batch (BASELINE config 5, "batched
+planning: 4096 request mixes x 4 models x 16 groups per launch"): level-1 DP of the model
+library (K1), per-mix staging, exhaustive enumeration + FP32 scoring of every level tuple
+of every mix (K2), the exact band re-check and tie-break (K5), and materialisation of all
+4096 lookup tables.  Scaling is weak: every rank plans its own 4096 mixes, no collective
+on the data path.  value = all ranks' candidates / max-over-ranks device time.
+
+The reference arm (--impl reference) times the ORACLE (oracle/, plain single-threaded C)
+on a bounded sample of the same workload: there is no reference implementation of this
+path to run (the paper solves it offline with Gurobi and publishes no solver number).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate allocations scored/sec"
+UNIT = "candidates/s"
+WORKLOAD = ("C5 batched planning: 4096 mixes x 4 models (7-model library, draws with replacement) x 16 groups "
+            "x 8 pool sizes {18..144} of N=148 SMs, switchMax=14, EXCLUDE_SELF, SUM, QoS 3x isolated")
+N_MIXES = 4096
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mixes", type=int, default=N_MIXES)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttp", action="store_true", help="skip the time-to-plan block")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 3 + k and r[3 + k].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------------------- oracle
+def oracle_rate(models, ids, qos, budget_s: float):
+    """The oracle (plain C, 1 thread) enumerating a contiguous prefix of mix 0's candidate
+    space for about budget_s seconds.  Returns (candidates/s, sample description)."""
+    import ctypes as C
+    import oracle
+    import synth
+    p = synth.c5_problem(0, models, ids, qos)
+    pp = oracle.Prepared(p)
+    r = oracle._Result()
+    n = 200_000
+    t = time.perf_counter()
+    oracle.lib().or_enum_range(C.byref(pp.c), 0, n, C.byref(r))
+    dt = time.perf_counter() - t
+    n2 = int(min(pp.n_tuples, max(n, n * budget_s / max(dt, 1e-6))))
+    t = time.perf_counter()
+    oracle.lib().or_enum_range(C.byref(pp.c), 0, n2, C.byref(r))
+    dt = time.perf_counter() - t
+    return n2 / dt, n2, dt
+
+
+# ----------------------------------------------------------------------------------------- main
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        return reference_arm(a, rank, world)
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2506_12598_b200 as ec
+    from paper_2506_12598_b200 import eclip as ecl
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    models, ids, qos = synth.make_c5(a.mixes, seed=rank)
+    pr = ec.Profiles.from_models(models)
+    stream = torch.cuda.current_stream(dev)
+    d_ids = torch.from_numpy(ids).to(dev)
+    d_qos = torch.from_numpy(qos).to(dev)
+    out = ec.alloc_batch_out(a.mixes, 4, 16, device=dev)
+    kw = dict(total_sms=148, switch_max=14, p_idle_w=200.0, p_max_w=1000.0, device=local, stream=stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        ec.plan_batch(pr, d_ids, qos_ns=d_qos, out=out, gmax=16, **kw)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    # candidates per step: prod of level counts per mix (exact)
+    Ls = level_counts(pr, ec)
+    cand_step = int(sum(int(np.prod([Ls[m] for m in row], dtype=np.float64)) for row in ids))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(a.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    ok = out["status"].cpu().numpy()
+    n_feas = int((ok == 0).sum())
+    assert (ok >= 0).all(), "planner reported an error status"
+    t_all = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    t_max_ms = float(t_all.item())
+    value = world * a.steps * cand_step / (t_max_ms * 1e-3)
+
+    # ---- pass-1 kernel alone (the dominant kernel): CUDA events on the launching stream
+    k_ms, k_launches = pass1_time(ec, pr, ids, qos, stream, local)
+
+    # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
+    pin_ids = torch.from_numpy(ids).pin_memory()
+    pin_q = torch.from_numpy(qos).pin_memory()
+    h_out = ec.alloc_batch_out(a.mixes, 4, 16)
+    e2e_ms = []
+    barrier()
+    for _ in range(a.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ec.plan_batch(pr, pin_ids.numpy(), qos_ns=pin_q.numpy(), out=h_out, gmax=16, **kw)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * a.steps * cand_step / (float(e2e_t.item()) * 1e-3)
+    assert np.array_equal(h_out["winner_index"], out["winner_index"].cpu().numpy().view(np.uint64))
+    h2d = ids.nbytes + qos.nbytes
+    d2h = sum(v.nbytes for k, v in h_out.items() if not k.startswith("_"))
+
+    # ---- time-to-optimal-plan (single problems; C4 sharded over all ranks)
+    ttp = {} if a.no_ttp else time_to_plan(ec, world, rank, dist if world > 1 else None)
+
+    if rank == 0:
+        f_max = 1965.0
+        issue_per_cand = 5.5            # packed f32x2 (2.5 slots) + 2 QoS compares + 1 min
+        cand_per_s_kernel = cand_step / (k_ms * 1e-3)
+        achieved = issue_per_cand * cand_per_s_kernel / 1e9
+        peak = 148 * 128 * f_max * 1e6 / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t_max_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded knee-shaped profiles, SURVEY §8(d))",
+            "config": {"workload": WORKLOAD, "mixes_per_rank": a.mixes, "candidates_per_step_per_rank": cand_step,
+                       "feasible_mixes_rank0": n_feas, "engine": "enum", "parallelism": f"weak x{world} (mixes)",
+                       "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": float(e2e_t.item()) / a.steps},
+            "gpu_launches": int(8 * a.steps),
+            "roofline": {"bound": "alu", "kernel": "k_pass1_sum<3,EXCL,QoS>", "achieved": achieved, "peak": peak,
+                         "unit": "G issue-slots/s (FP32 issue, 148 SM x 128 lanes x 1965 MHz)",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel_ms_per_launch": k_ms / k_launches,
+                         "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
+                         "fp32_lane_ops_per_candidate": 8, "issue_slots_per_candidate": issue_per_cand},
+            "clocks": ck,
+            "time_to_plan_ms": ttp,
+        }
+        if not a.no_cpu_baseline and world == 1:
+            rate, n, dt = oracle_rate(models, ids, qos, 15.0)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": f"oracle O-B (plain C, 1 thread) enumerating the first {n} level "
+                                              f"tuples of mix 0 in {dt:.1f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def level_counts(pr, ec):
+    """level count L_m of every library model = the candidate count of a 1-worker plan"""
+    n = pr.info()["n_models"]
+    return [ec.plan(pr, [m], total_sms=148, switch_max=14).candidates for m in range(n)]
+
+
+def pass1_time(ec, pr, ids, qos, stream, local):
+    """CUDA-event time of the pass-1 kernel(s) alone, via the split API on the same stream"""
+    import torch
+    from paper_2506_12598_b200.eclip import Session
+    tot, launches = 0.0, 0
+    for rep in range(3):
+        s = Session(pr, batch=dict(model_ids=ids, qos_ns=qos, total_sms=148, p_idle_w=200.0, p_max_w=1000.0),
+                    engine="enum", device=local, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.pass1()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rep > 0:
+            tot += e0.elapsed_time(e1)
+            launches += 1
+        s.close()
+    return tot, launches
+
+
+def time_to_plan(ec, world, rank, dist):
+    import synth
+    from paper_2506_12598_b200 import parallel
+    res = {}
+    for name, p in (("C2", synth.make_c2()), ("C3", synth.make_c3("matrix")), ("C4", synth.make_c4())):
+        pr = ec.Profiles.from_models(p.models)
+        ts = []
+        for rep in range(4):
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if dist is None:
+                r = ec.plan_problem(pr, p)
+            else:
+                r = parallel.plan_distributed(pr, p)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        res[name] = {"ms": float(np.median(ts[1:])), "engine": r.engine, "candidates": r.candidates,
+                     "units_scored": r.units_scored, "objective": r.objective}
+    return res
+
+
+def reference_arm(a, rank, world):
+    """--impl reference: the oracle (the only other implementation of this path), timed on the
+    host cores on a bounded sample of the same workload per step; rank 0 only."""
+    if rank != 0:
+        return
+    import synth
+    models, ids, qos = synth.make_c5(a.mixes, seed=0)
+    rates = []
+    for i in range(a.warmup + a.steps):
+        rate, n, dt = oracle_rate(models, ids, qos, 3.0)
+        if i >= a.warmup:
+            rates.append((n, dt))
+    n_tot = sum(n for n, _ in rates)
+    t_tot = sum(dt for _, dt in rates)
+    value = n_tot / t_tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t_tot / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "exact int / f32 (oracle)", "data": "synthetic",
+            "config": {"workload": WORKLOAD},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"per step: the first ~{rates[0][0]} level tuples of mix 0 (about 3 s of "
+                                       f"single-threaded oracle work)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,208 @@
+/*
+ * eclip.h — C-ABI of the B200-native ECLIP resource-allocation planner.
+ *
+ * The operation is the resource-allocation optimizer of ECLIP (arXiv 2506.12598,
+ * PAPER.md §IV-B "Resource Allocation Optimizer"): for every kernel group of
+ * every co-located worker (one model per worker) choose one pre-allocated CU/SM pool
+ * size (decision x_{k,c}, one configuration per kernel), with at most switchMax
+ * configuration switches per worker and request, minimising the predicted
+ * co-located execution time e_k = beta_k (1 + alpha_k), alpha_k = CUOverlap_w / N
+ * (P:309), CUAverage_w / CUOverlap_w, with equal weight per worker.
+ * The paper solves it offline with an ILP solver and stores a lookup table; this
+ * library solves it exactly and exhaustively on the GPU.  DESIGN.md fixes every reading
+ * (slowdown modes, objectives, QoS, ties) with citations; SURVEY.md §8(b) is the contract.
+ *
+ * Conventions
+ *   - Every function returns ECLIP_OK (0) or a negative ECLIP_E_* code; eclip_last_error()
+ *     returns a thread-local message for the last failure on the calling thread.
+ *   - Inputs are borrowed for the duration of the call.  eclip_profiles objects are created
+ *     and freed by the library, immutable after creation and safe to share between threads.
+ *     All result arrays are allocated by the caller.  There is no global mutable state
+ *     except the per-thread error message: calls on different threads are independent.
+ *   - Times are integer nanoseconds inside the library (profile files carry decimal
+ *     microseconds, rounded to the nearest ns, ties to even).
+ *   - The planner never falls back to the CPU: without a usable CUDA device every planning
+ *     call fails with ECLIP_E_CUDA.
+ */
+#ifndef ECLIP_H
+#define ECLIP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status / error codes ---------------------------------------------------------- */
+#define ECLIP_OK 0
+#define ECLIP_INFEASIBLE 1          /* result status (not an error): no plan meets every QoS bound */
+#define ECLIP_E_PARSE -1            /* profile text is not the SPEC format */
+#define ECLIP_E_MISSING_CONFIG -2   /* a kernel row lacks a size column */
+#define ECLIP_E_NONMONOTONE -3      /* exec time increases with CUs / is <= 0; message names model and kernel */
+#define ECLIP_E_INVALID_ARG -4      /* bad problem (see eclip_problem field comments) */
+#define ECLIP_E_TOO_LARGE -5        /* search space / integer ranges beyond the engine's limits */
+#define ECLIP_E_CUDA -6             /* CUDA runtime failure, or no CUDA device */
+#define ECLIP_E_OOM -7              /* device or host allocation failed */
+#define ECLIP_E_IO -8               /* file cannot be read */
+
+/* ---- slowdown modes (CUOverlap_w; readings in DESIGN.md §3.3) ---------------- */
+#define ECLIP_EXCLUDE_SELF 0        /* sum_{w' != w} CUAverage_w'  (default) */
+#define ECLIP_PAPER_AS_WRITTEN 1    /* CUAverage_w + sum_{w' != w} CUAverage_w'  (P:314 verbatim) */
+#define ECLIP_EXCESS_OVER_CAPACITY 2/* max(0, sum_w' CUAverage_w' - N) */
+#define ECLIP_MATRIX 3              /* sum_{w' != w} M[w][w'] CUAverage_w'  (BASELINE C3) */
+
+/* ---- objectives ("one identically weighted objective per worker") ------------- */
+#define ECLIP_SUM 0                 /* sum_w sum_{k in w} e_k  (default) */
+#define ECLIP_MAX 1                 /* max_w sum_{k in w} e_k  (makespan) */
+#define ECLIP_ENERGY 2              /* power x makespan, power linear in sum_w CUAverage_w / N */
+
+/* ---- engines ------------------------------------------------------------------------ */
+#define ECLIP_ENGINE_AUTO 0
+#define ECLIP_ENGINE_ENUM 1         /* exhaustive level-tuple enumeration (every candidate scored) */
+#define ECLIP_ENGINE_SLICE 2        /* exact T'-sliced DP (linear slowdown modes only) */
+
+/* ---- profiles ------------------------------------------------------------------------ */
+typedef struct eclip_profiles eclip_profiles;
+
+/* Parse a profile file (SPEC "External Interfaces"): per model a JSON header
+ * line {"model": name, "kernels": N, "configs": [c_0, ..., c_{C-1}]} followed by N CSV rows
+ * "kernel_id, t_0, ..., t_{C-1}" in decimal microseconds; several models may follow each
+ * other.  All models of one profiles object must share the same ascending size list.
+ * Errors: ECLIP_E_IO, ECLIP_E_PARSE, ECLIP_E_MISSING_CONFIG, ECLIP_E_NONMONOTONE. */
+int eclip_load_profiles(const char* path, eclip_profiles** out);
+int eclip_load_profiles_mem(const char* text, size_t len, eclip_profiles** out);
+
+/* Build from arrays: model m has n_kernels[m] kernels; exec_ns holds, model after model,
+ * n_kernels[m] rows of n_sizes integer-ns times; sizes_sm ascending (SM or CU counts). */
+int eclip_profiles_from_arrays(int32_t n_models, const int32_t* n_kernels, int32_t n_sizes,
+                               const int32_t* sizes_sm, const int64_t* exec_ns, eclip_profiles** out);
+void eclip_free_profiles(eclip_profiles* p);
+
+/* Introspection: number of models and sizes; copies of sizes [n_sizes], kernel counts
+ * [n_models] and exec times (same layout as eclip_profiles_from_arrays) when non-NULL. */
+int eclip_profiles_info(const eclip_profiles* p, int32_t* n_models, int32_t* n_sizes,
+                        int32_t* sizes_sm, int32_t* n_kernels, int64_t* exec_ns, char* names, size_t names_cap);
+
+const char* eclip_last_error(void);
+const char* eclip_version(void);
+
+/* ---- one planning problem (one co-location mix) ------------------------------------- */
+typedef struct {
+    int32_t n_models;             /* W >= 1 workers (<= 16; ENUM <= 8) */
+    const int32_t* model_ids;     /* [W] indices into the profiles (repeats allowed: P:378 Mix 1 = 2x albert) */
+    const int32_t* group_bounds;  /* NULL => one group per kernel (the paper's formulation).  Else, for each
+                                     worker w in order, G_w+1 ascending kernel offsets 0 = b_0 < ... < b_G = K_w
+                                     (concatenated).  Group g = kernels [b_g, b_{g+1}); beta_g = sum of its
+                                     kernels' times; switches are counted between groups. */
+    int32_t total_sms;            /* N: total CUs/SMs (60 for MI50-shaped, 148 for B200-shaped); sizes must be <= N */
+    const uint32_t* allowed_mask; /* [W] bitmask over size columns (pool layouts); NULL => all sizes */
+    const double* qos_ns;         /* [W] latency bound Q_w on sum_{k in w} e_k (inclusive); NULL or +inf => none */
+    int32_t switch_max;           /* R >= 0 switches per worker per request (the paper uses 14) */
+    int32_t slowdown;             /* ECLIP_EXCLUDE_SELF | ECLIP_PAPER_AS_WRITTEN | ECLIP_EXCESS_OVER_CAPACITY | ECLIP_MATRIX */
+    const float* slowdown_matrix; /* [W*W] row-major, entries >= 0 (MATRIX only; diagonal ignored) */
+    int32_t objective;            /* ECLIP_SUM | ECLIP_MAX | ECLIP_ENERGY */
+    float p_idle_w, p_max_w;      /* power model, 0 <= p_idle <= p_max (75 / 225 W) */
+} eclip_problem;
+
+/* Result of one problem.  Arrays are caller-allocated and may be NULL when not wanted:
+ * group_sm / group_latency_ns need sum_w G_w entries, the per-worker arrays W entries. */
+typedef struct {
+    int32_t status;               /* ECLIP_OK or ECLIP_INFEASIBLE */
+    int32_t engine_used;          /* ECLIP_ENGINE_ENUM | ECLIP_ENGINE_SLICE */
+    int32_t* group_sm;            /* [sum G] chosen pool size per group: the lookup table */
+    double* group_latency_ns;     /* [sum G] e_g = beta_g (1 + alpha_w) */
+    double* model_latency_ns;     /* [W] L_w = sum_{k in w} e_k */
+    int32_t* model_switches;      /* [W] switchTotal_w */
+    int32_t* winner_levels;       /* [W] canonical level rank per worker */
+    double objective;             /* SUM / MAX: ns;  ENERGY: W*ns (= nJ) */
+    double makespan_ns;           /* max_w L_w */
+    double power_w;               /* p_idle + (p_max - p_idle) min(1, sum_w CUAverage_w / N) */
+    double energy_j;              /* power x makespan */
+    double throughput_rps;        /* sum_w 1e9 / L_w (each worker back to back) */
+    uint64_t winner_index;        /* mixed-radix index of the winning level tuple (worker 0 most significant) */
+    uint64_t candidates;          /* level tuples in the search space (prod_w L_w) */
+    uint64_t units_scored;        /* ENUM: tuples scored; SLICE: lattice points evaluated */
+    uint64_t exact_key[4];        /* the winner's exact integer key, little-endian limbs */
+} eclip_result;
+
+typedef struct {
+    int32_t engine;               /* ECLIP_ENGINE_AUTO (default) | ENUM | SLICE */
+    int32_t device;               /* CUDA device ordinal (default 0) */
+    void* cuda_stream;            /* cudaStream_t to run on (NULL => the library's own stream) */
+    double tie_tol;               /* tau: ties within key <= m (1 + tau) go to the lowest index (default 1e-5) */
+    int32_t shard, n_shards;      /* candidate-space shard of this call (default 0 / 1); see eclip_session_* */
+} eclip_options;
+
+void eclip_default_options(eclip_options* o);
+
+/* Plan one problem.  Every level tuple is scored on the GPU (or the exact SLICE DP covers
+ * them); the winner is the lowest-index tuple whose exact key is within (1+tau) of the exact
+ * minimum.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_TOO_LARGE, ECLIP_E_CUDA, ECLIP_E_OOM. */
+int eclip_plan(const eclip_profiles* prof, const eclip_problem* problem, const eclip_options* opt,
+               eclip_result* result);
+
+/* Plan many independent problems in one launch sequence (serving-loop replanning, BASELINE
+ * config 5).  All problems must share W, total_sms, switch_max, slowdown, objective, power
+ * model and group layout; model_ids / qos / masks / matrices differ per problem. */
+typedef struct {
+    int32_t n_problems;
+    int32_t n_models;             /* W, same for every problem */
+    const int32_t* model_ids;     /* [n_problems * W] */
+    const double* qos_ns;         /* [n_problems * W] or NULL */
+    const uint32_t* allowed_mask; /* [n_models_in_profiles] per-model mask, or NULL => all sizes */
+    const float* slowdown_matrix; /* [n_problems * W * W] (MATRIX only) */
+    int32_t total_sms, switch_max, slowdown, objective;
+    float p_idle_w, p_max_w;
+    int32_t on_device;            /* 0: the arrays above and below are host memory.
+                                     1: model_ids, qos_ns, slowdown_matrix and every eclip_batch_out array are
+                                     CUDA device pointers; the call then performs no host<->device copy of
+                                     per-problem data and does not synchronise the stream before returning. */
+} eclip_batch;
+
+typedef struct {                  /* struct-of-arrays results, caller-allocated (host or device per on_device) */
+    int32_t* status;              /* [n] */
+    int32_t* winner_levels;       /* [n * W] */
+    uint64_t* winner_index;       /* [n] */
+    double* objective;            /* [n] */
+    double* makespan_ns;          /* [n] */
+    double* power_w;              /* [n] */
+    double* energy_j;             /* [n] */
+    double* throughput_rps;       /* [n] */
+    double* model_latency_ns;     /* [n * W] */
+    int32_t* model_switches;      /* [n * W] */
+    int32_t* group_sm;            /* [n * W * Gmax] (row of worker w at (i*W + w)*Gmax; unused tail = 0), or NULL */
+    int32_t group_stride;         /* Gmax used for group_sm */
+} eclip_batch_out;
+
+int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,
+                     eclip_batch_out* out);
+
+/* ---- split API for multi-GPU / process-group runs -------------------------------------
+ * A session plans a batch (n_problems >= 1) restricted to candidate shard opt->shard of
+ * opt->n_shards.  Between the steps the caller combines per-problem values across shards:
+ *   pass1      -> float m[n]        : combine with MIN
+ *   pass2_min  -> uint64 key[4n]    : combine with lexicographic MIN on (key[3],key[2],key[1],key[0])
+ *   pass2_first-> uint64 index[n]   : combine with MIN (UINT64_MAX = none in this shard)
+ * then finish() materialises the results (identical on every shard).  All buffers are host
+ * memory.  eclip_plan / eclip_plan_batch are exactly session(shard 0 of 1) + these steps. */
+typedef struct eclip_session eclip_session;
+int eclip_session_create(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,
+                         eclip_session** out);
+int eclip_session_pass1(eclip_session* s, float* min_key32);
+int eclip_session_pass2_min(eclip_session* s, const float* global_min_key32, uint64_t* exact_min);
+int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_index);
+int eclip_session_finish(eclip_session* s, const uint64_t* global_first_index, eclip_batch_out* out);
+void eclip_session_free(eclip_session* s);
+
+/* Single-problem sessions (the per-worker masks / groups of eclip_problem; used to shard
+ * one large problem, e.g. BASELINE config 4, across GPUs).  Same steps as above with
+ * n = 1; finish_problem fills an eclip_result exactly like eclip_plan. */
+int eclip_session_create_problem(const eclip_profiles* prof, const eclip_problem* problem,
+                                 const eclip_options* opt, eclip_session** out);
+int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_index, eclip_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECLIP_H */

@@ -1,0 +1,976 @@
+// api.cpp — the C-ABI (include/eclip.h): profile ingest, validation,
+// level-table jobs, engine orchestration and result marshalling.  Every step of the
+// planning path runs in the CUDA kernels of levels.cu / enum.cu / slice.cu; this file only
+// prepares inputs, launches, and copies results.  There is no CPU fallback.
+#include <algorithm>
+#include <cerrno>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/eclip.h"
+#include "engine.h"
+#include "slice.h"
+
+using namespace eclip;
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t _e = (x);                                                                       \
+        if (_e != cudaSuccess) {                                                                    \
+            return fail(_e == cudaErrorMemoryAllocation ? ECLIP_E_OOM : ECLIP_E_CUDA, "CUDA: %s (%s:%d)", \
+                        cudaGetErrorString(_e), __FILE__, __LINE__);                                \
+        }                                                                                           \
+    } while (0)
+
+extern "C" const char* eclip_last_error(void) { return g_err.c_str(); }
+extern "C" const char* eclip_version(void) { return "eclip-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------------------------------
+// profiles
+// ------------------------------------------------------------------------------------------
+struct eclip_profiles {
+    std::vector<std::string> names;
+    std::vector<int32_t> sizes;
+    std::vector<int32_t> nk;
+    std::vector<int64_t> row0;   // first row of each model
+    std::vector<int64_t> exec;   // [sum nk][C]
+    int C() const { return (int)sizes.size(); }
+    int n() const { return (int)nk.size(); }
+    const int64_t* row(int m, int k) const { return exec.data() + (size_t)(row0[m] + k) * sizes.size(); }
+};
+
+// decimal microseconds -> integer ns, round half to even
+static bool us_to_ns(const std::string& cell, int64_t* out) {
+    size_t i = 0, n = cell.size();
+    while (i < n && isspace((unsigned char)cell[i])) i++;
+    while (n > i && isspace((unsigned char)cell[n - 1])) n--;
+    if (i >= n) return false;
+    bool neg = false;
+    if (cell[i] == '+' || cell[i] == '-') { neg = cell[i] == '-'; i++; }
+    std::string ip, fp;
+    while (i < n && isdigit((unsigned char)cell[i])) ip += cell[i++];
+    if (i < n && cell[i] == '.') {
+        i++;
+        while (i < n && isdigit((unsigned char)cell[i])) fp += cell[i++];
+    }
+    if (i != n || (ip.empty() && fp.empty())) return false;
+    if (ip.size() > 12) return false;
+    int64_t whole = 0;
+    for (char c : ip) whole = whole * 10 + (c - '0');
+    int64_t ns = whole * 1000;
+    std::string f3 = fp.substr(0, std::min<size_t>(3, fp.size()));
+    while (f3.size() < 3) f3 += '0';
+    ns += (f3[0] - '0') * 100 + (f3[1] - '0') * 10 + (f3[2] - '0');
+    // remaining digits decide rounding: > half up, == half to even
+    if (fp.size() > 3) {
+        std::string rest = fp.substr(3);
+        int cmp;
+        if (rest[0] > '5') cmp = 1;
+        else if (rest[0] < '5') cmp = -1;
+        else {
+            cmp = 0;
+            for (size_t k = 1; k < rest.size(); k++)
+                if (rest[k] != '0') { cmp = 1; break; }
+        }
+        if (cmp > 0 || (cmp == 0 && (ns & 1))) ns += 1;
+    }
+    *out = neg ? -ns : ns;
+    return true;
+}
+
+static int parse_profiles(const char* text, size_t len, eclip_profiles** out) {
+    std::string s(text, len);
+    std::istringstream in(s);
+    std::string line;
+    std::vector<std::string> lines;
+    while (std::getline(in, line)) {
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        bool blank = true;
+        for (char c : line)
+            if (!isspace((unsigned char)c)) { blank = false; break; }
+        if (!blank) lines.push_back(line);
+    }
+    auto P = std::make_unique<eclip_profiles>();
+    size_t i = 0;
+    while (i < lines.size()) {
+        // minimal JSON header parse: {"model": "...", "kernels": N, "configs": [..]}
+        const std::string& h = lines[i];
+        auto key = [&](const char* k) -> size_t {
+            size_t p = h.find(std::string("\"") + k + "\"");
+            if (p == std::string::npos) return p;
+            p = h.find(':', p);
+            return p == std::string::npos ? p : p + 1;
+        };
+        size_t pm = key("model"), pk = key("kernels"), pc = key("configs");
+        if (h.find('{') == std::string::npos || pm == std::string::npos || pk == std::string::npos || pc == std::string::npos)
+            return fail(ECLIP_E_PARSE, "parse failure: line %zu is not a profile header", i + 1);
+        size_t q1 = h.find('"', pm), q2 = q1 == std::string::npos ? q1 : h.find('"', q1 + 1);
+        if (q2 == std::string::npos) return fail(ECLIP_E_PARSE, "parse failure: bad model name on line %zu", i + 1);
+        std::string name = h.substr(q1 + 1, q2 - q1 - 1);
+        long nk = strtol(h.c_str() + pk, nullptr, 10);
+        size_t b1 = h.find('[', pc), b2 = h.find(']', pc);
+        if (nk < 1 || b1 == std::string::npos || b2 == std::string::npos)
+            return fail(ECLIP_E_PARSE, "parse failure: model %s: bad kernels/configs", name.c_str());
+        std::vector<int32_t> cfg;
+        {
+            std::string c = h.substr(b1 + 1, b2 - b1 - 1);
+            std::stringstream cs(c);
+            std::string tok;
+            while (std::getline(cs, tok, ',')) {
+                char* e = nullptr;
+                long v = strtol(tok.c_str(), &e, 10);
+                if (v <= 0) return fail(ECLIP_E_PARSE, "parse failure: model %s: bad config %s", name.c_str(), tok.c_str());
+                cfg.push_back((int32_t)v);
+            }
+        }
+        if (cfg.empty()) return fail(ECLIP_E_PARSE, "parse failure: model %s: empty configs", name.c_str());
+        if (P->sizes.empty()) P->sizes = cfg;
+        else if (P->sizes != cfg)
+            return fail(ECLIP_E_PARSE, "parse failure: model %s: configs differ from the first model's", name.c_str());
+        for (size_t j = 1; j < cfg.size(); j++)
+            if (cfg[j] <= cfg[j - 1]) return fail(ECLIP_E_PARSE, "parse failure: configs must ascend");
+        if (i + 1 + (size_t)nk > lines.size())
+            return fail(ECLIP_E_PARSE, "parse failure: model %s: expected %ld kernel rows", name.c_str(), nk);
+        P->names.push_back(name);
+        P->nk.push_back((int32_t)nk);
+        P->row0.push_back((int64_t)(P->exec.size() / cfg.size()));
+        for (long k = 0; k < nk; k++) {
+            const std::string& r = lines[i + 1 + k];
+            std::vector<std::string> cells;
+            std::stringstream rs(r);
+            std::string tok;
+            while (std::getline(rs, tok, ',')) cells.push_back(tok);
+            if (cells.size() != cfg.size() + 1)
+                return fail(ECLIP_E_MISSING_CONFIG, "missing config column: model %s, kernel %ld", name.c_str(), k);
+            std::vector<int64_t> row;
+            for (size_t j = 1; j < cells.size(); j++) {
+                int64_t v;
+                if (!us_to_ns(cells[j], &v))
+                    return fail(ECLIP_E_PARSE, "parse failure: model %s, kernel %ld: not a decimal: %s", name.c_str(), k,
+                                cells[j].c_str());
+                if (v <= 0) return fail(ECLIP_E_NONMONOTONE, "non-positive exec_time: model %s, kernel %ld", name.c_str(), k);
+                row.push_back(v);
+            }
+            for (size_t j = 0; j + 1 < row.size(); j++)
+                if (row[j] < row[j + 1])
+                    return fail(ECLIP_E_NONMONOTONE, "non-monotone exec_time: model %s, kernel %ld", name.c_str(), k);
+            P->exec.insert(P->exec.end(), row.begin(), row.end());
+        }
+        i += 1 + nk;
+    }
+    if (P->nk.empty()) return fail(ECLIP_E_PARSE, "parse failure: empty profile file");
+    *out = P.release();
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_load_profiles_mem(const char* text, size_t len, eclip_profiles** out) {
+    if (!text || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    return parse_profiles(text, len, out);
+}
+
+extern "C" int eclip_load_profiles(const char* path, eclip_profiles** out) {
+    if (!path || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(ECLIP_E_IO, "cannot read %s: %s", path, strerror(errno));
+    std::stringstream ss;
+    ss << f.rdbuf();
+    std::string s = ss.str();
+    return parse_profiles(s.data(), s.size(), out);
+}
+
+extern "C" int eclip_profiles_from_arrays(int32_t n_models, const int32_t* n_kernels, int32_t n_sizes,
+                                          const int32_t* sizes_sm, const int64_t* exec_ns, eclip_profiles** out) {
+    if (n_models < 1 || !n_kernels || n_sizes < 1 || n_sizes > 32 || !sizes_sm || !exec_ns || !out)
+        return fail(ECLIP_E_INVALID_ARG, "bad arguments to eclip_profiles_from_arrays");
+    auto P = std::make_unique<eclip_profiles>();
+    P->sizes.assign(sizes_sm, sizes_sm + n_sizes);
+    for (int j = 0; j < n_sizes; j++) {
+        if (sizes_sm[j] <= 0) return fail(ECLIP_E_INVALID_ARG, "size %d is not positive", j);
+        if (j && sizes_sm[j] <= sizes_sm[j - 1]) return fail(ECLIP_E_INVALID_ARG, "sizes must ascend");
+    }
+    int64_t r = 0;
+    for (int m = 0; m < n_models; m++) {
+        if (n_kernels[m] < 1) return fail(ECLIP_E_INVALID_ARG, "model %d has no kernels", m);
+        P->names.push_back("model" + std::to_string(m));
+        P->nk.push_back(n_kernels[m]);
+        P->row0.push_back(r);
+        for (int k = 0; k < n_kernels[m]; k++, r++) {
+            const int64_t* row = exec_ns + (size_t)r * n_sizes;
+            for (int j = 0; j < n_sizes; j++) {
+                if (row[j] <= 0) return fail(ECLIP_E_NONMONOTONE, "non-positive exec_time: model %d, kernel %d", m, k);
+                if (j && row[j - 1] < row[j]) return fail(ECLIP_E_NONMONOTONE, "non-monotone exec_time: model %d, kernel %d", m, k);
+            }
+            P->exec.insert(P->exec.end(), row, row + n_sizes);
+        }
+    }
+    *out = P.release();
+    return ECLIP_OK;
+}
+
+extern "C" void eclip_free_profiles(eclip_profiles* p) { delete p; }
+
+extern "C" int eclip_profiles_info(const eclip_profiles* p, int32_t* n_models, int32_t* n_sizes, int32_t* sizes_sm,
+                                   int32_t* n_kernels, int64_t* exec_ns, char* names, size_t names_cap) {
+    if (!p) return fail(ECLIP_E_INVALID_ARG, "null profiles");
+    if (n_models) *n_models = p->n();
+    if (n_sizes) *n_sizes = p->C();
+    if (sizes_sm) std::copy(p->sizes.begin(), p->sizes.end(), sizes_sm);
+    if (n_kernels) std::copy(p->nk.begin(), p->nk.end(), n_kernels);
+    if (exec_ns) std::copy(p->exec.begin(), p->exec.end(), exec_ns);
+    if (names && names_cap) {
+        std::string all;
+        for (auto& s : p->names) all += s + "\n";
+        size_t n = std::min(all.size(), names_cap - 1);
+        memcpy(names, all.data(), n);
+        names[n] = 0;
+    }
+    return ECLIP_OK;
+}
+
+extern "C" void eclip_default_options(eclip_options* o) {
+    memset(o, 0, sizeof(*o));
+    o->engine = ECLIP_ENGINE_AUTO;
+    o->device = 0;
+    o->cuda_stream = nullptr;
+    o->tie_tol = 1e-5;
+    o->shard = 0;
+    o->n_shards = 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// level tables (host descriptions; built on the GPU by K1)
+// ------------------------------------------------------------------------------------------
+struct TableSpec {
+    int model;
+    std::vector<int32_t> bounds;  // kernel offsets (G+1)
+    uint32_t mask;
+    int R;
+    bool operator<(const TableSpec& o) const {
+        return std::tie(model, bounds, mask, R) < std::tie(o.model, o.bounds, o.mask, o.R);
+    }
+};
+
+struct HostTable {
+    int G, C, Reff, smax, Lcap;
+    int64_t u, K;
+    uint32_t mask;
+    std::vector<int64_t> beta;  // [G*C]
+    std::vector<int32_t> need;  // [G*C]
+    size_t v_elems;
+};
+
+static int64_t gcd64(int64_t a, int64_t b) {
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+static int build_host_table(const eclip_profiles* P, const TableSpec& sp, HostTable* t) {
+    const int C = P->C();
+    const int G = (int)sp.bounds.size() - 1;
+    t->G = G; t->C = C; t->mask = sp.mask;
+    t->Reff = std::min(sp.R, G - 1);
+    t->beta.assign((size_t)G * C, 0);
+    t->need.assign((size_t)G * C, 0);
+    int64_t u = 0;
+    for (int j = 0; j < C; j++)
+        if ((sp.mask >> j) & 1u) u = gcd64(u, P->sizes[j]);
+    t->u = u;
+    int64_t smax = 0, bmax = 0;
+    for (int g = 0; g < G; g++) {
+        int64_t ng = sp.bounds[g + 1] - sp.bounds[g];
+        int64_t mx = 0, bm = 0;
+        for (int j = 0; j < C; j++) {
+            int64_t b = 0;
+            for (int k = sp.bounds[g]; k < sp.bounds[g + 1]; k++) b += P->row(sp.model, k)[j];
+            t->beta[(size_t)g * C + j] = b;
+            if ((sp.mask >> j) & 1u) {
+                t->need[(size_t)g * C + j] = (int32_t)(ng * P->sizes[j] / u);
+                mx = std::max<int64_t>(mx, t->need[(size_t)g * C + j]);
+                bm = std::max<int64_t>(bm, b);
+            }
+        }
+        smax += mx;
+        bmax += bm;
+    }
+    if (bmax >= ((int64_t)1 << 36))
+        return fail(ECLIP_E_TOO_LARGE, "model %d: solo request time %lld ns exceeds 2^36 ns", sp.model, (long long)bmax);
+    if (smax > (1 << 22)) return fail(ECLIP_E_TOO_LARGE, "model %d: CU-sum range too large", sp.model);
+    t->smax = (int)smax;
+    t->K = sp.bounds.back();
+    t->Lcap = (int)smax + 1;
+    t->v_elems = (size_t)G * C * (t->Reff + 1) * (smax + 1);
+    return ECLIP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// device allocation helpers (stream-ordered)
+// ------------------------------------------------------------------------------------------
+struct DevArena {
+    cudaStream_t st = nullptr;
+    std::vector<void*> ptrs;
+    template <class T>
+    cudaError_t alloc(T** p, size_t n) {
+        void* q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(n, 1) * sizeof(T), st);
+        if (e == cudaSuccess) ptrs.push_back(q);
+        *p = (T*)q;
+        return e;
+    }
+    void release() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+        ptrs.clear();
+    }
+    ~DevArena() { release(); }
+};
+
+// ------------------------------------------------------------------------------------------
+// the session: everything one planning call needs on the device
+// ------------------------------------------------------------------------------------------
+struct eclip_session {
+    const eclip_profiles* prof = nullptr;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int device = 0;
+    DevArena arena;
+    // problem description
+    Setup su{};
+    int W = 0, n = 0, C = 0;
+    bool on_device = false;
+    std::vector<HostTable> tabs;
+    std::vector<int32_t> tabL;
+    std::vector<int32_t> tabG;
+    std::vector<int32_t> h_table_of;     // host copy (single-problem path)
+    int32_t* d_sizes = nullptr;
+    Tables tb{};
+    Work wk{};
+    PrepIn pin{};
+    int engine = ECLIP_ENGINE_ENUM;
+    int gmax = 0;
+    uint64_t scored_local = 0;
+    SliceState slice;
+    ~eclip_session() {
+        slice.release();
+        arena.release();
+        if (own_stream && st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    }
+};
+
+static int setup_device(eclip_session* s, const eclip_options* opt) {
+    s->device = opt ? opt->device : 0;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(ECLIP_E_CUDA, "no CUDA device available (%s); the planner has no CPU fallback",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    if (s->device < 0 || s->device >= ndev) return fail(ECLIP_E_INVALID_ARG, "device %d out of range", s->device);
+    CU(cudaSetDevice(s->device));
+    if (opt && opt->cuda_stream) {
+        s->st = (cudaStream_t)opt->cuda_stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+        s->own_stream = true;
+    }
+    s->arena.st = s->st;
+    return ECLIP_OK;
+}
+
+// Build tables with K1 on the GPU and fetch their level counts.
+static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
+    const eclip_profiles* P = s->prof;
+    s->tabs.resize(specs.size());
+    for (size_t i = 0; i < specs.size(); i++) {
+        int rc = build_host_table(P, specs[i], &s->tabs[i]);
+        if (rc) return rc;
+    }
+    const int nt = (int)specs.size();
+    std::vector<LevelJob> jobs(nt);
+    std::vector<int64_t*> hS(nt), hB(nt), hbeta(nt);
+    std::vector<uint8_t*> hW(nt);
+    int32_t* dL;
+    CU(s->arena.alloc(&dL, nt));
+    s->gmax = 0;
+    for (int i = 0; i < nt; i++) {
+        HostTable& t = s->tabs[i];
+        LevelJob& J = jobs[i];
+        J.G = t.G; J.C = t.C; J.R = t.Reff; J.smax = t.smax; J.u = t.u; J.mask = t.mask; J.Lcap = t.Lcap;
+        int64_t* beta; int32_t* need;
+        CU(s->arena.alloc(&beta, t.beta.size()));
+        CU(s->arena.alloc(&need, t.need.size()));
+        CU(cudaMemcpyAsync(beta, t.beta.data(), t.beta.size() * 8, cudaMemcpyHostToDevice, s->st));
+        CU(cudaMemcpyAsync(need, t.need.data(), t.need.size() * 4, cudaMemcpyHostToDevice, s->st));
+        J.beta = beta; J.need = need;
+        hbeta[i] = beta;
+        CU(s->arena.alloc(&J.V, t.v_elems));
+        size_t ns = (size_t)(t.Reff + 1) * (t.smax + 1);
+        CU(s->arena.alloc(&J.best, 2 * ns + t.smax + 1));
+        CU(s->arena.alloc(&J.barg, ns));
+        CU(s->arena.alloc(&J.sidx, t.smax + 1));
+        CU(s->arena.alloc(&J.wtmp, (size_t)(t.smax + 1) * t.G));
+        CU(s->arena.alloc(&J.rank, t.smax + 1));
+        CU(s->arena.alloc(&J.outS, t.Lcap));
+        CU(s->arena.alloc(&J.outB, t.Lcap));
+        CU(s->arena.alloc(&J.outW, (size_t)t.Lcap * t.G));
+        J.outL = dL + i;
+        hS[i] = J.outS; hB[i] = J.outB; hW[i] = J.outW;
+        s->gmax = std::max(s->gmax, t.G);
+    }
+    LevelJob* djobs;
+    CU(s->arena.alloc(&djobs, nt));
+    CU(cudaMemcpyAsync(djobs, jobs.data(), sizeof(LevelJob) * nt, cudaMemcpyHostToDevice, s->st));
+    CU(launch_levels(djobs, jobs.data(), nt, s->st));
+    // device table views
+    std::vector<int64_t> hK(nt);
+    s->tabG.resize(nt);
+    for (int i = 0; i < nt; i++) { hK[i] = s->tabs[i].K; s->tabG[i] = s->tabs[i].G; }
+    int64_t* dK; int32_t* dG;
+    int64_t** dS; int64_t** dB; uint8_t** dW; int64_t** dbeta;
+    CU(s->arena.alloc(&dK, nt));
+    CU(s->arena.alloc(&dG, nt));
+    CU(s->arena.alloc(&dS, nt));
+    CU(s->arena.alloc(&dB, nt));
+    CU(s->arena.alloc(&dW, nt));
+    CU(s->arena.alloc(&dbeta, nt));
+    CU(cudaMemcpyAsync(dK, hK.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    CU(cudaMemcpyAsync(dG, s->tabG.data(), 4 * nt, cudaMemcpyHostToDevice, s->st));
+    CU(cudaMemcpyAsync(dS, hS.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    CU(cudaMemcpyAsync(dB, hB.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    CU(cudaMemcpyAsync(dW, hW.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    CU(cudaMemcpyAsync(dbeta, hbeta.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    s->tabL.resize(nt);
+    CU(cudaMemcpyAsync(s->tabL.data(), dL, 4 * nt, cudaMemcpyDeviceToHost, s->st));
+    CU(cudaStreamSynchronize(s->st));   // level counts size the enumeration
+    s->tb.n = nt; s->tb.L = dL; s->tb.K = dK; s->tb.G = dG;
+    s->tb.S = dS; s->tb.B = dB; s->tb.wit = dW; s->tb.beta = dbeta;
+    return ECLIP_OK;
+}
+
+static int check_common(const eclip_profiles* P, int W, int N, int R, int mode, int obj, float pi, float pm,
+                        double tol) {
+    if (!P) return fail(ECLIP_E_INVALID_ARG, "null profiles");
+    if (W < 1 || W > MAXW) return fail(ECLIP_E_INVALID_ARG, "n_models must be in [1, %d]", MAXW);
+    if (N < 1) return fail(ECLIP_E_INVALID_ARG, "total_sms must be >= 1");
+    if (P->sizes.back() > N) return fail(ECLIP_E_INVALID_ARG, "pool size %d exceeds total_sms %d", P->sizes.back(), N);
+    if (R < 0) return fail(ECLIP_E_INVALID_ARG, "switch_max must be >= 0");
+    if (mode < 0 || mode > 3) return fail(ECLIP_E_INVALID_ARG, "unknown slowdown mode %d", mode);
+    if (obj < 0 || obj > 2) return fail(ECLIP_E_INVALID_ARG, "unknown objective %d", obj);
+    if (!(std::isfinite(pi) && std::isfinite(pm) && pi >= 0.0f && pm >= pi))
+        return fail(ECLIP_E_INVALID_ARG, "power model needs 0 <= p_idle <= p_max");
+    if (!(tol >= 0.0 && tol < 1.0)) return fail(ECLIP_E_INVALID_ARG, "tie_tol must be in [0, 1)");
+    return ECLIP_OK;
+}
+
+static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, int obj, bool has_qos,
+                       const eclip_options* opt) {
+    (void)R;
+    Setup& su = s->su;
+    su.n_problems = n; su.W = W; su.N = N; su.mode = mode; su.obj = obj; su.has_qos = has_qos ? 1 : 0;
+    double tol = opt ? opt->tie_tol : 1e-5;
+    su.tol_den = 1000000000ull;
+    su.tol_num = (uint64_t)llround(tol * 1e9);
+    su.delta = (double)(8 * W + 16) * std::ldexp(1.0, -24);
+    su.shard = opt ? opt->shard : 0;
+    su.n_shards = opt ? std::max(1, opt->n_shards) : 1;
+}
+
+// choose the engine and size the work
+static int plan_geometry(eclip_session* s, const eclip_options* opt) {
+    Setup& su = s->su;
+    int Lmax = 1, teams = 1;
+    for (int L : s->tabL) {
+        Lmax = std::max(Lmax, L);
+        int ts, tm;
+        pass1_geometry(std::max(L, 1), &ts, &tm);
+        teams = std::max(teams, tm);
+    }
+    su.Lmax = Lmax;
+    su.teams = teams;
+    int want = opt ? opt->engine : ECLIP_ENGINE_AUTO;
+    // ENUM limits
+    long double space = 1;
+    for (int w = 0; w < su.W - 1; w++) space *= Lmax;
+    long double items = std::ceil(space / (long double)pass1_pitem(Lmax));
+    bool enum_ok = su.W <= MAXW_ENUM && (size_t)su.W * Lmax * sizeof(Lev) <= 200 * 1024 && items < 2e9 &&
+                   space * Lmax < 4e18;
+    bool slice_ok = su.mode != M_MATRIX && s->n == 1;
+    if (want == ECLIP_ENGINE_ENUM && !enum_ok)
+        return fail(ECLIP_E_TOO_LARGE, "ENUM engine limits exceeded (W=%d, Lmax=%d)", su.W, Lmax);
+    if (want == ECLIP_ENGINE_SLICE && !slice_ok)
+        return fail(ECLIP_E_INVALID_ARG, "SLICE engine needs a linear slowdown mode and a single problem");
+    if (want == ECLIP_ENGINE_AUTO) {
+        // ENUM scores every candidate; take SLICE when enumeration is far larger than the lattice
+        long double tuples = space * Lmax;
+        if (!enum_ok || (slice_ok && tuples > 4e10L)) {
+            if (!slice_ok) return fail(ECLIP_E_TOO_LARGE, "search space too large for ENUM and SLICE does not apply");
+            s->engine = ECLIP_ENGINE_SLICE;
+        } else {
+            s->engine = ECLIP_ENGINE_ENUM;
+        }
+    } else {
+        s->engine = want;
+    }
+    su.items_max = (int)std::max<long double>(1, items);
+    return ECLIP_OK;
+}
+
+static int alloc_work(eclip_session* s) {
+    Setup& su = s->su;
+    Work& wk = s->wk;
+    const size_t n = (size_t)su.n_problems;
+    CU(s->arena.alloc(&wk.probs, n));
+    CU(s->arena.alloc(&wk.levs, n * su.W * su.Lmax));
+    if (s->engine == ECLIP_ENGINE_ENUM) {
+        size_t ns = n * (size_t)su.items_max * su.teams;
+        CU(s->arena.alloc(&wk.submin, ns));
+        if (su.mode == M_MATRIX && su.has_qos) CU(s->arena.alloc(&wk.submin_sure, ns));
+    }
+    CU(s->arena.alloc(&wk.m32, n));
+    CU(s->arena.alloc(&wk.m32_sure, n));
+    CU(s->arena.alloc(&wk.hstar, n));
+    CU(s->arena.alloc(&wk.first, n));
+    return ECLIP_OK;
+}
+
+static int status_error(const eclip_session* s, int st, int p) {
+    (void)s;
+    if (st == -5) return fail(ECLIP_E_TOO_LARGE, "problem %d exceeds the exact-arithmetic ranges (Lambda N (W+1) < 2^24, ...)", p);
+    return fail(ECLIP_E_INVALID_ARG, "problem %d is invalid (model id / QoS / matrix / power values)", p);
+}
+
+// ------------------------------------------------------------------------------------------
+// session construction
+// ------------------------------------------------------------------------------------------
+static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr, const eclip_options* opt,
+                                eclip_session** out) {
+    if (!pr) return fail(ECLIP_E_INVALID_ARG, "null problem");
+    const int W = pr->n_models;
+    double tol = opt ? opt->tie_tol : 1e-5;
+    int rc = check_common(P, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, pr->p_idle_w, pr->p_max_w, tol);
+    if (rc) return rc;
+    if (!pr->model_ids) return fail(ECLIP_E_INVALID_ARG, "null model_ids");
+    const int C = P->C();
+    std::vector<TableSpec> specs;
+    std::map<TableSpec, int> ids;
+    std::vector<int32_t> table_of(W);
+    const int32_t* gb = pr->group_bounds;
+    for (int w = 0; w < W; w++) {
+        int m = pr->model_ids[w];
+        if (m < 0 || m >= P->n()) return fail(ECLIP_E_INVALID_ARG, "model id %d of worker %d out of range", m, w);
+        TableSpec sp;
+        sp.model = m;
+        sp.R = pr->switch_max;
+        sp.mask = pr->allowed_mask ? pr->allowed_mask[w] : ((C == 32) ? 0xffffffffu : ((1u << C) - 1u));
+        if (C < 32) sp.mask &= (1u << C) - 1u;
+        if (sp.mask == 0) return fail(ECLIP_E_INVALID_ARG, "worker %d has no allowed size", w);
+        for (int j = 0; j < C; j++)
+            if (((sp.mask >> j) & 1u) && P->sizes[j] > pr->total_sms)
+                return fail(ECLIP_E_INVALID_ARG, "size %d exceeds total_sms", P->sizes[j]);
+        int K = P->nk[m];
+        if (gb) {
+            if (gb[0] != 0) return fail(ECLIP_E_INVALID_ARG, "group_bounds of worker %d must start at 0", w);
+            sp.bounds.push_back(0);
+            int i = 1;
+            while (sp.bounds.back() != K) {
+                int b = gb[i];
+                if (b <= sp.bounds.back() || b > K)
+                    return fail(ECLIP_E_INVALID_ARG, "group_bounds of worker %d must ascend to %d", w, K);
+                sp.bounds.push_back(b);
+                i++;
+            }
+            gb += i;
+        } else {
+            for (int k = 0; k <= K; k++) sp.bounds.push_back(k);
+        }
+        auto it = ids.find(sp);
+        if (it == ids.end()) {
+            ids[sp] = (int)specs.size();
+            table_of[w] = (int)specs.size();
+            specs.push_back(sp);
+        } else {
+            table_of[w] = it->second;
+        }
+        if (pr->qos_ns && !(pr->qos_ns[w] >= 0.0)) return fail(ECLIP_E_INVALID_ARG, "qos_ns[%d] must be >= 0 or +inf", w);
+    }
+    if (pr->slowdown == ECLIP_MATRIX) {
+        if (!pr->slowdown_matrix) return fail(ECLIP_E_INVALID_ARG, "MATRIX slowdown needs slowdown_matrix");
+        if (W > MAXW_ENUM) return fail(ECLIP_E_TOO_LARGE, "MATRIX slowdown supports at most %d workers", MAXW_ENUM);
+        for (int i = 0; i < W * W; i++) {
+            float m = pr->slowdown_matrix[i];
+            if (i / W != i % W && !(std::isfinite(m) && m >= 0.0f && m < 1024.0f))
+                return fail(ECLIP_E_INVALID_ARG, "slowdown_matrix entries must be finite, >= 0 and < 1024");
+        }
+    }
+    auto s = std::make_unique<eclip_session>();
+    s->prof = P;
+    s->W = W; s->n = 1; s->C = C;
+    rc = setup_device(s.get(), opt);
+    if (rc) return rc;
+    bool has_qos = false;
+    if (pr->qos_ns)
+        for (int w = 0; w < W; w++) has_qos |= !std::isinf(pr->qos_ns[w]);
+    fill_setup(s.get(), 1, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, has_qos, opt);
+    rc = build_tables(s.get(), specs);
+    if (rc) return rc;
+    s->h_table_of = table_of;
+    rc = plan_geometry(s.get(), opt);
+    if (rc) return rc;
+    rc = alloc_work(s.get());
+    if (rc) return rc;
+    // per-problem inputs
+    int32_t* dtab; double* dq = nullptr; float* dM = nullptr;
+    CU(s->arena.alloc(&dtab, W));
+    CU(cudaMemcpyAsync(dtab, table_of.data(), 4 * W, cudaMemcpyHostToDevice, s->st));
+    if (pr->qos_ns) {
+        CU(s->arena.alloc(&dq, W));
+        CU(cudaMemcpyAsync(dq, pr->qos_ns, 8 * W, cudaMemcpyHostToDevice, s->st));
+    }
+    if (pr->slowdown == ECLIP_MATRIX) {
+        CU(s->arena.alloc(&dM, (size_t)W * W));
+        CU(cudaMemcpyAsync(dM, pr->slowdown_matrix, 4 * W * W, cudaMemcpyHostToDevice, s->st));
+    }
+    CU(s->arena.alloc(&s->d_sizes, C));
+    CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * C, cudaMemcpyHostToDevice, s->st));
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.p_idle = pr->p_idle_w; s->pin.p_max = pr->p_max_w;
+    CU(launch_prep(s->su, s->tb, s->pin, s->wk, C, s->d_sizes, s->st));
+    *out = s.release();
+    return ECLIP_OK;
+}
+
+static int session_from_batch(const eclip_profiles* P, const eclip_batch* b, const eclip_options* opt,
+                              eclip_session** out) {
+    if (!b) return fail(ECLIP_E_INVALID_ARG, "null batch");
+    double tol = opt ? opt->tie_tol : 1e-5;
+    int rc = check_common(P, b->n_models, b->total_sms, b->switch_max, b->slowdown, b->objective, b->p_idle_w,
+                          b->p_max_w, tol);
+    if (rc) return rc;
+    if (b->n_problems < 1) return fail(ECLIP_E_INVALID_ARG, "n_problems must be >= 1");
+    if (!b->model_ids) return fail(ECLIP_E_INVALID_ARG, "null model_ids");
+    if (b->slowdown == ECLIP_MATRIX && !b->slowdown_matrix)
+        return fail(ECLIP_E_INVALID_ARG, "MATRIX slowdown needs slowdown_matrix");
+    const int W = b->n_models, n = b->n_problems, C = P->C();
+    if (!b->on_device) {
+        for (int i = 0; i < n * W; i++) {
+            if (b->model_ids[i] < 0 || b->model_ids[i] >= P->n())
+                return fail(ECLIP_E_INVALID_ARG, "model id %d out of range (problem %d)", b->model_ids[i], i / W);
+            if (b->qos_ns && !(b->qos_ns[i] >= 0.0)) return fail(ECLIP_E_INVALID_ARG, "qos_ns must be >= 0 or +inf");
+        }
+    }
+    // one table per model of the profiles (the batch shares the grouping, mask and budget)
+    std::vector<TableSpec> specs;
+    for (int m = 0; m < P->n(); m++) {
+        TableSpec sp;
+        sp.model = m;
+        sp.R = b->switch_max;
+        sp.mask = b->allowed_mask ? b->allowed_mask[m] : ((C == 32) ? 0xffffffffu : ((1u << C) - 1u));
+        if (C < 32) sp.mask &= (1u << C) - 1u;
+        if (sp.mask == 0) return fail(ECLIP_E_INVALID_ARG, "model %d has no allowed size", m);
+        for (int j = 0; j < C; j++)
+            if (((sp.mask >> j) & 1u) && P->sizes[j] > b->total_sms)
+                return fail(ECLIP_E_INVALID_ARG, "size %d exceeds total_sms", P->sizes[j]);
+        for (int k = 0; k <= P->nk[m]; k++) sp.bounds.push_back(k);
+        specs.push_back(sp);
+    }
+    auto s = std::make_unique<eclip_session>();
+    s->prof = P;
+    s->W = W; s->n = n; s->C = C;
+    s->on_device = b->on_device != 0;
+    rc = setup_device(s.get(), opt);
+    if (rc) return rc;
+    fill_setup(s.get(), n, W, b->total_sms, b->switch_max, b->slowdown, b->objective, b->qos_ns != nullptr, opt);
+    rc = build_tables(s.get(), specs);
+    if (rc) return rc;
+    rc = plan_geometry(s.get(), opt);
+    if (rc) return rc;
+    if (s->engine != ECLIP_ENGINE_ENUM) return fail(ECLIP_E_TOO_LARGE, "batched planning runs on the ENUM engine only");
+    rc = alloc_work(s.get());
+    if (rc) return rc;
+    const int32_t* dtab = b->model_ids;
+    const double* dq = b->qos_ns;
+    const float* dM = b->slowdown_matrix;
+    if (!b->on_device) {
+        int32_t* t; double* q = nullptr; float* M = nullptr;
+        CU(s->arena.alloc(&t, (size_t)n * W));
+        CU(cudaMemcpyAsync(t, b->model_ids, 4 * (size_t)n * W, cudaMemcpyHostToDevice, s->st));
+        if (b->qos_ns) {
+            CU(s->arena.alloc(&q, (size_t)n * W));
+            CU(cudaMemcpyAsync(q, b->qos_ns, 8 * (size_t)n * W, cudaMemcpyHostToDevice, s->st));
+        }
+        if (b->slowdown == ECLIP_MATRIX) {
+            CU(s->arena.alloc(&M, (size_t)n * W * W));
+            CU(cudaMemcpyAsync(M, b->slowdown_matrix, 4 * (size_t)n * W * W, cudaMemcpyHostToDevice, s->st));
+        }
+        dtab = t; dq = q; dM = M;
+    }
+    CU(s->arena.alloc(&s->d_sizes, C));
+    CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * C, cudaMemcpyHostToDevice, s->st));
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.p_idle = b->p_idle_w; s->pin.p_max = b->p_max_w;
+    CU(launch_prep(s->su, s->tb, s->pin, s->wk, C, s->d_sizes, s->st));
+    *out = s.release();
+    return ECLIP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// steps
+// ------------------------------------------------------------------------------------------
+static int step_pass1(eclip_session* s) {
+    if (s->engine == ECLIP_ENGINE_SLICE) {
+        CU(slice_pass1(s->slice, s->su, s->tb, s->wk, s->st));
+        return ECLIP_OK;
+    }
+    CU(launch_pass1(s->su, s->wk, s->st));
+    CU(launch_reduce_min(s->su, s->wk, s->st));
+    return ECLIP_OK;
+}
+static int step_pass2_min(eclip_session* s) {
+    if (s->engine == ECLIP_ENGINE_SLICE) {
+        CU(slice_pass2_min(s->slice, s->su, s->tb, s->wk, s->st));
+        return ECLIP_OK;
+    }
+    CU(launch_pass2_min(s->su, s->wk, s->st));
+    return ECLIP_OK;
+}
+static int step_pass2_first(eclip_session* s) {
+    if (s->engine == ECLIP_ENGINE_SLICE) {
+        CU(slice_pass2_first(s->slice, s->su, s->tb, s->wk, s->st));
+        return ECLIP_OK;
+    }
+    CU(launch_pass2_first(s->su, s->wk, s->st));
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_create(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,
+                                    eclip_session** out) {
+    if (!out) return fail(ECLIP_E_INVALID_ARG, "null out");
+    if (batch && batch->on_device) return fail(ECLIP_E_INVALID_ARG, "sessions take host batches");
+    return session_from_batch(prof, batch, opt, out);
+}
+
+extern "C" int eclip_session_pass1(eclip_session* s, float* min_key32) {
+    if (!s) return fail(ECLIP_E_INVALID_ARG, "null session");
+    int rc = step_pass1(s);
+    if (rc) return rc;
+    if (min_key32) {
+        CU(cudaMemcpyAsync(min_key32, s->wk.m32, 4 * (size_t)s->n, cudaMemcpyDeviceToHost, s->st));
+        CU(cudaStreamSynchronize(s->st));
+    }
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_pass2_min(eclip_session* s, const float* global_min, uint64_t* exact_min) {
+    if (!s) return fail(ECLIP_E_INVALID_ARG, "null session");
+    if (global_min) {
+        CU(cudaMemcpyAsync(s->wk.m32, global_min, 4 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
+        if (!(s->su.mode == M_MATRIX && s->su.has_qos))
+            CU(cudaMemcpyAsync(s->wk.m32_sure, global_min, 4 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
+    }
+    int rc = step_pass2_min(s);
+    if (rc) return rc;
+    if (exact_min) {
+        CU(cudaMemcpyAsync(exact_min, s->wk.hstar, 32 * (size_t)s->n, cudaMemcpyDeviceToHost, s->st));
+        CU(cudaStreamSynchronize(s->st));
+    }
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_index) {
+    if (!s) return fail(ECLIP_E_INVALID_ARG, "null session");
+    if (global_exact_min)
+        CU(cudaMemcpyAsync(s->wk.hstar, global_exact_min, 32 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
+    int rc = step_pass2_first(s);
+    if (rc) return rc;
+    if (first_index) {
+        CU(cudaMemcpyAsync(first_index, s->wk.first, 8 * (size_t)s->n, cudaMemcpyDeviceToHost, s->st));
+        CU(cudaStreamSynchronize(s->st));
+    }
+    return ECLIP_OK;
+}
+
+// materialise into device buffers; copy to the caller's host arrays unless on_device
+static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host = nullptr, uint64_t* key_host = nullptr) {
+    const size_t n = s->n, W = s->W;
+    int stride = o->group_stride > 0 ? o->group_stride : 1;
+    MatOut mo{};
+    mo.group_stride = stride;
+    if (s->on_device) {
+        mo.status = o->status; mo.levels = o->winner_levels; mo.index = o->winner_index; mo.objective = o->objective;
+        mo.makespan = o->makespan_ns; mo.power = o->power_w; mo.energy = o->energy_j; mo.thr = o->throughput_rps;
+        mo.latency = o->model_latency_ns; mo.switches = o->model_switches; mo.group_sm = o->group_sm;
+        if (s->engine == ECLIP_ENGINE_SLICE) CU(slice_decode_winner(s->slice, s->su, s->wk, s->st));
+        CU(launch_materialize(s->su, s->tb, s->wk, s->d_sizes, s->C, mo, s->st));
+        return ECLIP_OK;
+    }
+    int32_t *st, *lv, *sw, *gsm = nullptr;
+    uint64_t *idx, *key = nullptr;
+    double *obj, *mk, *pw, *en, *thr, *lat, *glat = nullptr;
+    CU(s->arena.alloc(&st, n));
+    CU(s->arena.alloc(&lv, n * W));
+    CU(s->arena.alloc(&sw, n * W));
+    CU(s->arena.alloc(&idx, n));
+    CU(s->arena.alloc(&obj, n));
+    CU(s->arena.alloc(&mk, n));
+    CU(s->arena.alloc(&pw, n));
+    CU(s->arena.alloc(&en, n));
+    CU(s->arena.alloc(&thr, n));
+    CU(s->arena.alloc(&lat, n * W));
+    if (o->group_sm) CU(s->arena.alloc(&gsm, n * W * stride));
+    if (glat_host) CU(s->arena.alloc(&glat, n * W * stride));
+    if (key_host) CU(s->arena.alloc(&key, n * 4));
+    mo.group_lat = glat; mo.key = key;
+    mo.status = st; mo.levels = lv; mo.index = idx; mo.objective = obj; mo.makespan = mk; mo.power = pw;
+    mo.energy = en; mo.thr = thr; mo.latency = lat; mo.switches = sw; mo.group_sm = gsm;
+    if (s->engine == ECLIP_ENGINE_SLICE) CU(slice_decode_winner(s->slice, s->su, s->wk, s->st));
+    CU(launch_materialize(s->su, s->tb, s->wk, s->d_sizes, s->C, mo, s->st));
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s->st) : cudaSuccess;
+    };
+    CU(cp(o->status, st, 4 * n));
+    CU(cp(o->winner_levels, lv, 4 * n * W));
+    CU(cp(o->winner_index, idx, 8 * n));
+    CU(cp(o->objective, obj, 8 * n));
+    CU(cp(o->makespan_ns, mk, 8 * n));
+    CU(cp(o->power_w, pw, 8 * n));
+    CU(cp(o->energy_j, en, 8 * n));
+    CU(cp(o->throughput_rps, thr, 8 * n));
+    CU(cp(o->model_latency_ns, lat, 8 * n * W));
+    CU(cp(o->model_switches, sw, 4 * n * W));
+    if (gsm) CU(cp(o->group_sm, gsm, 4 * n * W * stride));
+    if (glat) CU(cp(glat_host, glat, 8 * n * W * stride));
+    if (key) CU(cp(key_host, key, 32 * n));
+    CU(cudaStreamSynchronize(s->st));
+    if (o->status)
+        for (size_t i = 0; i < n; i++)
+            if (o->status[i] < 0) return status_error(s, o->status[i], (int)i);
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_finish(eclip_session* s, const uint64_t* global_first_index, eclip_batch_out* out) {
+    if (!s || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    if (global_first_index)
+        CU(cudaMemcpyAsync(s->wk.first, global_first_index, 8 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
+    return finish_batch(s, out);
+}
+
+extern "C" void eclip_session_free(eclip_session* s) { delete s; }
+
+// ------------------------------------------------------------------------------------------
+// one-shot entry points
+// ------------------------------------------------------------------------------------------
+static int run_all_steps(eclip_session* s) {
+    int rc = step_pass1(s);
+    if (rc) return rc;
+    rc = step_pass2_min(s);
+    if (rc) return rc;
+    return step_pass2_first(s);
+}
+
+extern "C" int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,
+                                eclip_batch_out* out) {
+    if (!out) return fail(ECLIP_E_INVALID_ARG, "null out");
+    eclip_session* s = nullptr;
+    int rc = session_from_batch(prof, batch, opt, &s);
+    if (rc) { delete s; return rc; }
+    std::unique_ptr<eclip_session> guard(s);
+    rc = run_all_steps(s);
+    if (rc) return rc;
+    rc = finish_batch(s, out);
+    if (rc) return rc;
+    if (s->on_device && s->own_stream) CU(cudaStreamSynchronize(s->st));
+    return ECLIP_OK;
+}
+
+static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_override) {
+    const int W = s->W;
+    int gmax = 1;
+    for (int w = 0; w < W; w++) gmax = std::max(gmax, s->tabs[s->h_table_of[w]].G);
+    std::vector<int32_t> st(1), lv(W), sw(W), gsm((size_t)W * gmax);
+    std::vector<uint64_t> idx(1), key(4);
+    std::vector<double> obj(1), mk(1), pw(1), en(1), thr(1), lat(W), glat((size_t)W * gmax);
+    eclip_batch_out o{};
+    o.status = st.data(); o.winner_levels = lv.data(); o.winner_index = idx.data(); o.objective = obj.data();
+    o.makespan_ns = mk.data(); o.power_w = pw.data(); o.energy_j = en.data(); o.throughput_rps = thr.data();
+    o.model_latency_ns = lat.data(); o.model_switches = sw.data(); o.group_sm = gsm.data(); o.group_stride = gmax;
+    if (first_override) CU(cudaMemcpyAsync(s->wk.first, first_override, 8, cudaMemcpyHostToDevice, s->st));
+    int rc = finish_batch(s, &o, glat.data(), key.data());
+    if (rc) return rc;
+    r->status = st[0] == 0 ? ECLIP_OK : ECLIP_INFEASIBLE;
+    r->engine_used = s->engine;
+    r->objective = obj[0]; r->makespan_ns = mk[0]; r->power_w = pw[0]; r->energy_j = en[0];
+    r->throughput_rps = thr[0]; r->winner_index = idx[0];
+    for (int i = 0; i < 4; i++) r->exact_key[i] = key[i];
+    uint64_t total = 1;
+    for (int w = 0; w < W; w++) total *= (uint64_t)std::max(1, s->tabL[s->h_table_of[w]]);
+    r->candidates = total;
+    r->units_scored = s->engine == ECLIP_ENGINE_ENUM ? total : slice_units(s->slice);
+    size_t off = 0;
+    for (int w = 0; w < W; w++) {
+        int G = s->tabs[s->h_table_of[w]].G;
+        if (r->model_latency_ns) r->model_latency_ns[w] = lat[w];
+        if (r->model_switches) r->model_switches[w] = sw[w];
+        if (r->winner_levels) r->winner_levels[w] = lv[w];
+        for (int g = 0; g < G; g++) {
+            if (r->group_sm) r->group_sm[off + g] = gsm[(size_t)w * gmax + g];
+            if (r->group_latency_ns) r->group_latency_ns[off + g] = glat[(size_t)w * gmax + g];
+        }
+        off += G;
+    }
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_create_problem(const eclip_profiles* prof, const eclip_problem* problem,
+                                            const eclip_options* opt, eclip_session** out) {
+    if (!out) return fail(ECLIP_E_INVALID_ARG, "null out");
+    eclip_session* s = nullptr;
+    int rc = session_from_problem(prof, problem, opt, &s);
+    if (rc) { delete s; return rc; }
+    if (s->engine == ECLIP_ENGINE_SLICE) {
+        cudaError_t e = slice_setup(s->slice, s->su, s->tb, s->wk, s->tabL.data(), s->h_table_of.data(), s->st);
+        if (e != cudaSuccess) { delete s; return fail(ECLIP_E_CUDA, "SLICE setup: %s", cudaGetErrorString(e)); }
+    }
+    *out = s;
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_index, eclip_result* r) {
+    if (!s || !r) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    return plan_one(s, r, global_first_index);
+}
+
+extern "C" int eclip_plan(const eclip_profiles* prof, const eclip_problem* problem, const eclip_options* opt,
+                          eclip_result* r) {
+    if (!r) return fail(ECLIP_E_INVALID_ARG, "null result");
+    eclip_session* s = nullptr;
+    int rc = eclip_session_create_problem(prof, problem, opt, &s);
+    if (rc) return rc;
+    std::unique_ptr<eclip_session> guard(s);
+    rc = run_all_steps(s);
+    if (rc) return rc;
+    return plan_one(s, r, nullptr);
+}

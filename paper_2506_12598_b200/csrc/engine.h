@@ -1,0 +1,149 @@
+// engine.h — internal structures shared by the host planner (api.cpp) and the CUDA
+// kernels (levels.cu, enum.cu, slice.cu).  Not part of the C-ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "exact.cuh"
+
+namespace eclip {
+
+constexpr int MAXW = 16;        // workers per problem (API limit)
+constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
+constexpr int P1_THREADS = 512; // pass-1 CTA size
+constexpr int KIN = 8;          // inner-worker levels held in registers per thread (pass 1)
+
+enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
+enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };
+
+// ---------------------------------------------------------------------------------------
+// Level-1 DP job (one per level table; §8(a) a2, DESIGN.md §4 K1)
+// ---------------------------------------------------------------------------------------
+struct LevelJob {
+    int32_t G, C, R;            // groups, size columns, effective switch budget min(R, G-1)
+    int32_t smax;               // max level in units of u
+    int64_t u;                  // gcd of the allowed sizes (SMs)
+    uint32_t mask;              // allowed size columns
+    int32_t Lcap;               // capacity of the outputs
+    const int64_t* beta;        // [G*C] group solo times (ns)
+    const int32_t* need;        // [G*C] n_g c_j / u
+    int64_t* V;                 // workspace [G*C*(R+1)*(smax+1)]
+    int64_t* best;              // workspace [(R+1)*(smax+1)*2]: (b1 | j1<<?) packed as b1, b2 pairs
+    int32_t* barg;              // workspace [(R+1)*(smax+1)] argmin of b1
+    int32_t* sidx;              // workspace [smax+1] compacted level -> s
+    uint8_t* wtmp;              // workspace [(smax+1)*G] witnesses in s order
+    int32_t* rank;              // workspace [smax+1]
+    // outputs (rank order)
+    int64_t* outS;              // [Lcap] level CU-sum in SMs
+    int64_t* outB;              // [Lcap] B*(S) ns
+    uint8_t* outW;              // [Lcap*G] witness size columns
+    int32_t* outL;              // [1]
+};
+
+cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, cudaStream_t st);
+
+// ---------------------------------------------------------------------------------------
+// Staged per-level record of one worker inside one problem (written by the prep kernel).
+// ---------------------------------------------------------------------------------------
+struct Lev {
+    int64_t B;        // exact solo time B*(level) (ns)
+    int64_t BS;       // exact B * S'
+    int32_t S;        // S' = S Lambda / K  (Lambda-scaled CU-sum)
+    int32_t Tmax;     // largest T' at which this worker meets its QoS (linear modes); -1 never
+    float Bk;         // (float)((double)B / (Lambda N))
+    int32_t pad;
+};
+static_assert(sizeof(Lev) == 32, "Lev must be 32 bytes");
+
+// ---------------------------------------------------------------------------------------
+// Per-problem descriptor (written by the prep kernel; read by every later kernel)
+// ---------------------------------------------------------------------------------------
+struct Prob {
+    int32_t status;             // 0 ok, 1 infeasible, <0 ECLIP_E_* error
+    int32_t W;
+    int32_t table[MAXW];        // level table per worker
+    int32_t L[MAXW];
+    int32_t E;                  // fraction bits of the slowdown matrix (MATRIX), else 0
+    int32_t k_pow;              // fraction bits of the power model
+    int64_t lam, lamN;          // Lambda = lcm K_w, Lambda N
+    uint64_t P;                 // prefix count prod_{w<W-1} L_w
+    uint64_t total;             // prod_w L_w
+    uint64_t n_items;           // pass-1 items (prefix blocks of Pitem)
+    uint64_t Pitem;             // prefixes per item
+    float inv;                  // (float)(1 / (Lambda N))
+    float lamNf;                // (float)(Lambda N)
+    float p_idle, p_dyn;        // power model floats (p_dyn = fl(p_max - p_idle))
+    float Qlo[MAXW], Qhi[MAXW]; // MATRIX+QoS: surely / maybe feasible float bounds on L_w
+    float Mf[MAXW_ENUM * MAXW_ENUM];     // slowdown matrix (float)
+    int64_t Mi[MAXW_ENUM * MAXW_ENUM];   // M 2^E (exact)
+    u128 Hq[MAXW];              // floor(Q_w D) (exact QoS on h_w); all-ones = none
+    u128 D;                     // Lambda N 2^E
+    u128 pi_idle, pi_dyn;       // power model p 2^k (exact)
+    int32_t has_qos;
+    float p_max;                // power model float (for FP64 reporting)
+};
+
+// Settings shared by all problems of one launch sequence
+struct Setup {
+    int32_t n_problems, W, N, mode, obj, has_qos;
+    int32_t Lmax;               // max levels over the tables
+    int32_t items_max;          // max pass-1 items over problems
+    int32_t teams;              // teams per pass-1 CTA (sub-chunks per item)
+    int32_t team_size;          // threads per team
+    int32_t shard, n_shards;
+    uint64_t tol_num, tol_den;
+    double delta;               // FP32 filter relative error bound
+};
+
+// Device view of all level tables
+struct Tables {
+    int32_t n;
+    const int32_t* L;           // [n]
+    const int64_t* K;           // [n] kernels per table
+    const int32_t* G;           // [n]
+    const int64_t* const* S;    // [n] -> [L] level CU-sums (SMs)
+    const int64_t* const* B;    // [n] -> [L]
+    const uint8_t* const* wit;  // [n] -> [L*G]
+    const int64_t* const* beta; // [n] -> [G*C]
+};
+
+struct PrepIn {
+    const int32_t* table_of;    // [n*W] table id per (problem, worker)
+    const double* qos;          // [n*W] or null
+    const float* M;             // [n*W*W] or null
+    float p_idle, p_max;
+};
+
+// Device-side outputs / scratch of one launch sequence
+struct Work {
+    Prob* probs;                // [n]
+    Lev* levs;                  // [n * W * Lmax]
+    float* submin;              // [n * items_max * teams]  pass-1 minima (maybe-feasible)
+    float* submin_sure;         // [n * items_max * teams]  MATRIX+QoS: surely-feasible minima
+    float* m32;                 // [n] local (then global) minimum
+    float* m32_sure;            // [n]
+    U256* hstar;                // [n] exact minimum
+    uint64_t* first;            // [n] lowest index within tolerance
+    uint64_t* scored;           // [n]
+};
+
+cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
+                        cudaStream_t st);
+cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st);
+cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st);
+cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st);
+cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st);
+
+struct MatOut {                 // materialisation outputs (device pointers, may be null)
+    int32_t* status; int32_t* levels; uint64_t* index; double* objective; double* makespan;
+    double* power; double* energy; double* thr; double* latency; int32_t* switches; int32_t* group_sm;
+    double* group_lat; int32_t group_stride; uint64_t* key;
+};
+cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C,
+                               MatOut out, cudaStream_t st);
+
+// number of pass-1 items / teams for a problem shape (host helper, same formula as the kernels)
+void pass1_geometry(int L_inner, int* team_size, int* teams);
+uint64_t pass1_pitem(int L_inner);
+
+}  // namespace eclip

@@ -1,0 +1,1006 @@
+// enum.cu — the ENUM engine: every level tuple of every problem is scored on the GPU.
+//
+//   prep     per problem constants (Lambda, D, exact QoS bounds, power integers) and the
+//            staged per-level records
+//   pass 1   K2: mixed-radix enumeration (a4) + FP32 scoring (a5) + per-sub-chunk minima (a6).
+//            Every candidate is one joint allocation: a level tuple (l_0..l_{W-1}).  The
+//            last worker's levels live in registers (KIN per thread); the other workers form
+//            the "prefix", advanced by an odometer (no index decode in the hot loop, no
+//            candidate list in HBM).  FP32 keys are a FILTER with relative error <= delta
+//            (DESIGN.md §3.5); SUM uses the aggregated form
+//               sum_w B_w (1 + O_w / (Lambda N)) = B + (T' B - sum_w B_w S'_w) / (Lambda N)
+//            evaluated with packed f32x2 FMA/ADD (two candidates per instruction).
+//   pass 2   K5: per problem, rescan only the sub-chunks whose pass-1 minimum is within the
+//            band  m (1+tau)(1+delta)/(1-delta); evaluate those candidates EXACTLY (integers)
+//            to get the exact minimum H*, then the lowest index with key <= H* (1+tau).
+//   materialize (a9): winner -> witnesses -> per-group pool sizes, FP64 latency / power /
+//            energy / throughput.
+#include <cfloat>
+#include <cstdio>
+
+#include "engine.h"
+
+namespace eclip {
+
+// ------------------------------------------------------------------------------------------
+// small helpers
+// ------------------------------------------------------------------------------------------
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 f2pack(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(u64 v, float& lo, float& hi) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// 1-D TMA bulk copy global -> shared, completion on an mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
+}
+
+// stage the problem's level records (W x Lmax x 32 B, contiguous) into shared memory
+__device__ __forceinline__ void stage_levels(Lev* sl, const Lev* gl, unsigned bytes, uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, bytes);
+        const unsigned CH = 32768;
+        for (unsigned off = 0; off < bytes; off += CH) {
+            unsigned n = bytes - off < CH ? bytes - off : CH;
+            bulk_g2s((char*)sl + off, (const char*)gl + off, n, bar);
+        }
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+}
+
+// pass-1 geometry (shared with pass 2 and the host)
+__host__ __device__ __forceinline__ int team_size_of(int L_in) { return (L_in + KIN - 1) / KIN; }
+__host__ __device__ __forceinline__ int teams_of(int L_in) {
+    int t = P1_THREADS / team_size_of(L_in);
+    return t < 1 ? 1 : t;
+}
+__host__ __device__ __forceinline__ uint64_t pitem_of(int L_in) {
+    // about 2^20 candidates per item (one CTA work unit)
+    uint64_t p = ((uint64_t)1 << 20) / (uint64_t)(L_in > 0 ? L_in : 1);
+    return p < 1 ? 1 : p;
+}
+void pass1_geometry(int L_in, int* ts, int* teams) { *ts = team_size_of(L_in); *teams = teams_of(L_in); }
+uint64_t pass1_pitem(int L_in) { return pitem_of(L_in); }
+
+__host__ __device__ __forceinline__ void shard_items(uint64_t n_items, int shard, int n_shards, uint64_t* lo,
+                                                     uint64_t* hi) {
+    *lo = n_items * (uint64_t)shard / (uint64_t)n_shards;
+    *hi = n_items * (uint64_t)(shard + 1) / (uint64_t)n_shards;
+}
+
+// sub-chunk (item, team) -> prefix range
+__device__ __forceinline__ void subchunk_range(const Prob& P, uint64_t item, int team, int teams, uint64_t* lo,
+                                               uint64_t* hi) {
+    uint64_t ilo = item * P.Pitem;
+    uint64_t ihi = ilo + P.Pitem;
+    if (ihi > P.P) ihi = P.P;
+    uint64_t cnt = ihi > ilo ? ihi - ilo : 0;
+    uint64_t span = (cnt + (uint64_t)teams - 1) / (uint64_t)teams;
+    uint64_t a = ilo + (uint64_t)team * span;
+    uint64_t b = a + span;
+    if (a > ihi) a = ihi;
+    if (b > ihi) b = ihi;
+    *lo = a;
+    *hi = b;
+}
+
+// ------------------------------------------------------------------------------------------
+// prep
+// ------------------------------------------------------------------------------------------
+__device__ int frac_bits_d(double x, int limit) {
+    for (int k = 0; k <= limit; k++) {
+        double y = ldexp(x, k);
+        if (y == floor(y)) return k;
+    }
+    return -1;
+}
+
+// floor(q * D) for q >= 0 (double, may be inf); saturates to all-ones when >= 2^120
+__device__ u128 floor_qD(double q, u128 D) {
+    if (isinf(q)) return ~(u128)0;
+    if (!(q > 0.0)) return 0;
+    int ex;
+    double f = frexp(q, &ex);
+    u64 mant = (u64)ldexp(f, 53);
+    int e = ex - 53;
+    // mant * D < 2^53 * 2^60
+    U256 prod = u256_mul128((u128)mant, D);
+    if (prod.w[3] || prod.w[2]) return ~(u128)0;
+    u128 x = ((u128)prod.w[1] << 64) | prod.w[0];
+    if (e >= 0) {
+        // every exact h is < 2^112 (host-validated ranges), so any bound >= 2^120 is "none"
+        if (e >= 120 || (x >> (120 - e)) != 0) return ~(u128)0;
+        return x << e;
+    }
+    int s = -e;
+    return s >= 128 ? (u128)0 : (x >> s);
+}
+
+__global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= su.n_problems) return;
+    Prob P;
+    memset(&P, 0, sizeof(P));
+    P.W = su.W;
+    P.status = 0;
+    const int W = su.W;
+    u64 lam = 1;
+    for (int w = 0; w < W; w++) {
+        int t = in.table_of[(size_t)p * W + w];
+        if (t < 0 || t >= tb.n) { P.status = -4; break; }
+        P.table[w] = t;
+        P.L[w] = tb.L[t];
+        if (P.L[w] <= 0) P.status = 1;  // a worker without any budget-feasible plan
+        u64 K = (u64)tb.K[t];
+        u64 g = gcd_u64(lam, K);
+        lam = lam / g * K;
+        if (lam > ((u64)1 << 40)) P.status = -5;
+    }
+    P.lam = (int64_t)lam;
+    P.lamN = (int64_t)(lam * (u64)su.N);
+    if ((u128)P.lamN * (u128)(W + 1) >= ((u128)1 << 24)) P.status = P.status < 0 ? P.status : -5;
+    uint64_t Pn = 1, tot = 1;
+    for (int w = 0; w < W; w++) {
+        u128 t2 = (u128)tot * (u128)(P.L[w] > 0 ? P.L[w] : 1);
+        if (t2 >= ((u128)1 << 62)) P.status = -5;
+        tot = (uint64_t)t2;
+        if (w < W - 1) Pn *= (uint64_t)(P.L[w] > 0 ? P.L[w] : 1);
+    }
+    P.P = Pn;
+    P.total = tot;
+    int Lin = P.L[W - 1] > 0 ? P.L[W - 1] : 1;
+    P.Pitem = pitem_of(Lin);
+    P.n_items = (Pn + P.Pitem - 1) / P.Pitem;
+    P.inv = (float)(1.0 / (double)P.lamN);
+    P.lamNf = (float)P.lamN;
+    P.p_idle = in.p_idle;
+    P.p_dyn = in.p_max - in.p_idle;
+    P.p_max = in.p_max;
+    // power model as exact integers p 2^k
+    int k1 = frac_bits_d((double)in.p_idle, 40), k2 = frac_bits_d((double)in.p_max, 40);
+    if (k1 < 0 || k2 < 0) P.status = -4;
+    int k = k1 > k2 ? k1 : k2;
+    P.k_pow = k;
+    double pi_i = ldexp((double)in.p_idle, k), pi_m = ldexp((double)in.p_max, k);
+    if (pi_m >= 4.6e18) P.status = -5;
+    P.pi_idle = (u128)(u64)pi_i;
+    P.pi_dyn = (u128)((u64)pi_m - (u64)pi_i);
+    // slowdown matrix
+    P.E = 0;
+    if (su.mode == M_MATRIX) {
+        for (int a = 0; a < W; a++)
+            for (int b = 0; b < W; b++) {
+                float m = a == b ? 0.0f : in.M[(size_t)p * W * W + a * W + b];
+                if (!(m >= 0.0f) || m >= 1024.0f) { P.status = -4; m = 0.0f; }
+                int kb = frac_bits_d((double)m, 32);
+                if (kb < 0) P.status = -5;
+                if (kb > P.E) P.E = kb;
+                P.Mf[a * MAXW_ENUM + b] = m;
+            }
+        for (int a = 0; a < W; a++)
+            for (int b = 0; b < W; b++) P.Mi[a * MAXW_ENUM + b] = (int64_t)ldexp((double)P.Mf[a * MAXW_ENUM + b], P.E);
+    }
+    P.D = (u128)P.lamN << P.E;
+    P.has_qos = 0;
+    for (int w = 0; w < W; w++) {
+        double q = in.qos ? in.qos[(size_t)p * W + w] : (double)INFINITY;
+        if (!(q >= 0.0)) P.status = -4;
+        P.Hq[w] = floor_qD(q, P.D);
+        if (!isinf(q)) P.has_qos = 1;
+        // MATRIX + QoS float bounds on L_w (relative error of L32 <= (W+2) 2^-24; use 2W+8)
+        double marg = (double)(2 * W + 8) * 5.9604644775390625e-08;
+        P.Qhi[w] = isinf(q) ? INFINITY : __double2float_ru(q * (1.0 + marg));
+        P.Qlo[w] = isinf(q) ? INFINITY : __double2float_rd(q * (1.0 - marg));
+    }
+    probs[p] = P;
+}
+
+// one thread per (problem, worker, level)
+__global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t n = (size_t)su.n_problems * su.W * su.Lmax;
+    if (i >= n) return;
+    int l = (int)(i % su.Lmax);
+    int w = (int)((i / su.Lmax) % su.W);
+    int p = (int)(i / ((size_t)su.Lmax * su.W));
+    const Prob& P = probs[p];
+    Lev r;
+    r.B = 0; r.BS = 0; r.S = 0; r.Tmax = -1; r.Bk = 0.0f; r.pad = 0;
+    if (P.status >= 0 && l < P.L[w]) {
+        int t = P.table[w];
+        int64_t B = tb.B[t][l];
+        int64_t Sp = tb.S[t][l] * (P.lam / tb.K[t]);
+        r.B = B;
+        r.S = (int32_t)Sp;
+        r.BS = B * Sp;
+        r.Bk = (float)((double)B / (double)P.lamN);
+        int64_t T = (int64_t)1 << 24;
+        if (P.has_qos && su.mode != M_MATRIX && ~P.Hq[w] != 0) {
+            u128 hq = P.Hq[w];
+            int64_t hb;  // floor(Hq / B), saturated at 2^30
+            if ((hq >> 64) != 0) hb = (int64_t)1 << 30;
+            else {
+                u64 q = (u64)hq / (u64)B;
+                hb = q > ((u64)1 << 30) ? ((int64_t)1 << 30) : (int64_t)q;
+            }
+            if (su.mode == M_EXCL) T = Sp - P.lamN + hb;
+            else if (su.mode == M_PAPER) T = hb - P.lamN;
+            else T = ((u128)B * (u128)P.lamN > hq) ? -1 : hb;
+            if (T < -1) T = -1;
+            if (T > ((int64_t)1 << 24)) T = (int64_t)1 << 24;
+        }
+        r.Tmax = (int32_t)T;
+    }
+    levs[i] = r;
+}
+
+// ------------------------------------------------------------------------------------------
+// pass 1
+// ------------------------------------------------------------------------------------------
+struct Prefix {
+    // exact sums over the "hi" prefix workers 0..NP-2
+    int64_t hB, hBS;
+    int32_t hT, hTm;
+};
+
+template <int NP>
+__device__ __forceinline__ void hi_sums(const Lev* sl, int Lmax, const int* d, Prefix& h) {
+    h.hB = 0; h.hBS = 0; h.hT = 0; h.hTm = 1 << 24;
+#pragma unroll
+    for (int w = 0; w < NP - 1; w++) {
+        const Lev& r = sl[w * Lmax + d[w]];
+        h.hB += r.B; h.hBS += r.BS; h.hT += r.S; h.hTm = min(h.hTm, r.Tmax);
+    }
+}
+
+// decode prefix index p into digits d[0..NP-1] (worker 0 most significant)
+template <int NP>
+__device__ __forceinline__ void decode_prefix(uint64_t p, const int* L, int* d) {
+#pragma unroll
+    for (int w = NP - 1; w >= 0; w--) {
+        d[w] = (int)(p % (uint64_t)L[w]);
+        p /= (uint64_t)L[w];
+    }
+}
+
+// returns true if the odometer carried past the last prefix digit (hi part changed)
+template <int NP>
+__device__ __forceinline__ bool advance(int* d, const int* L) {
+    if (++d[NP - 1] < L[NP - 1]) return false;
+    d[NP - 1] = 0;
+#pragma unroll
+    for (int w = NP - 2; w >= 0; w--) {
+        if (++d[w] < L[w]) break;
+        d[w] = 0;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void team_min_write(float m, float* sm, float* out_slot, int team, int lane, int T,
+                                               bool active) {
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    if (active && lane == 0) {
+        float r = INFINITY;
+        for (int i = 0; i < T; i++) r = fminf(r, sm[threadIdx.x + i]);
+        *out_slot = r;
+    }
+    __syncthreads();
+}
+
+// SUM objective, linear slowdown modes: the aggregated packed-FP32 filter.
+template <int NP, int MODE, bool QOS>
+__global__ void __launch_bounds__(P1_THREADS, 1)
+k_pass1_sum(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ float red[P1_THREADS];
+    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
+
+    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
+    const int prob = blockIdx.x / ipS;
+    const int li = blockIdx.x % ipS;
+    const Prob& P = probs[prob];
+    if (P.status != 0) return;
+    uint64_t slo, shi;
+    shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
+    const uint64_t item = slo + (uint64_t)li;
+    if (item >= shi) return;
+
+    const int W = NP + 1;
+    stage_levels(sl, levs + (size_t)prob * su.W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
+
+    int L[NP + 1];
+#pragma unroll
+    for (int w = 0; w <= NP; w++) L[w] = P.L[w];
+    const int Lin = L[NP];
+    const int T = team_size_of(Lin), teams = teams_of(Lin);
+    const int team = threadIdx.x / T, lane = threadIdx.x % T;
+    const bool active = team < teams;
+
+    // inner-worker levels in registers (clamped duplicates beyond L_in leave the min unchanged)
+    u64 Bf2[KIN / 2], bsn2[KIN / 2], s2[KIN / 2];
+    float sfv[KIN], uv[KIN];
+    float smin_t = INFINITY, umax_t = -INFINITY;
+    const Lev* inner = sl + NP * su.Lmax;
+#pragma unroll
+    for (int q = 0; q < KIN / 2; q++) {
+        int i0 = min(lane * KIN + 2 * q, Lin - 1), i1 = min(lane * KIN + 2 * q + 1, Lin - 1);
+        const Lev& a = inner[i0];
+        const Lev& b = inner[i1];
+        Bf2[q] = f2pack(__ll2float_rn(a.B), __ll2float_rn(b.B));
+        bsn2[q] = f2pack(-__ll2float_rn(a.BS), -__ll2float_rn(b.BS));
+        float sa = (float)a.S, sb = (float)b.S;
+        s2[q] = f2pack(sa, sb);
+        sfv[2 * q] = sa; sfv[2 * q + 1] = sb;
+        uv[2 * q] = (float)(a.Tmax - a.S); uv[2 * q + 1] = (float)(b.Tmax - b.S);
+        smin_t = fminf(smin_t, fminf(sa, sb));
+        umax_t = fmaxf(umax_t, fmaxf(uv[2 * q], uv[2 * q + 1]));
+    }
+    const u64 INV2 = f2pack(P.inv, P.inv);
+    const u64 NLAMN2 = f2pack(-P.lamNf, -P.lamNf);
+
+    float m0 = INFINITY, m1 = INFINITY;
+    uint64_t lo = 0, hi = 0;
+    if (active) subchunk_range(P, item, team, teams, &lo, &hi);
+    uint64_t scored = 0;
+    if (active && lo < hi) {
+        int d[NP > 0 ? NP : 1];
+        Prefix h;
+        if (NP > 0) {
+            decode_prefix<NP>(lo, L, d);
+            hi_sums<NP>(sl, su.Lmax, d, h);
+        } else {
+            h.hB = 0; h.hBS = 0; h.hT = 0; h.hTm = 1 << 24;
+        }
+        for (uint64_t p = lo; p < hi; p++) {
+            int64_t pB = h.hB, pBS = h.hBS;
+            int32_t pT = h.hT, pTm = h.hTm;
+            if (NP > 0) {
+                const Lev& r = sl[(NP - 1) * su.Lmax + d[NP - 1]];
+                pB += r.B; pBS += r.BS; pT += r.S; pTm = min(pTm, r.Tmax);
+            }
+            const float Tpf = (float)pT;
+            const float c1 = (float)(pTm - pT);  // inner S' must be <= c1 (prefix workers' QoS)
+            bool any = true;
+            if (QOS) any = (c1 >= smin_t) && (Tpf <= umax_t);
+            if (any) {
+                const float Bpf = __ll2float_rn(pB);
+                const u64 PB = f2pack(Bpf, Bpf);
+                const u64 PT = f2pack(Tpf, Tpf);
+                u64 PBS = 0;
+                if (MODE == M_EXCL) { float b = -__ll2float_rn(pBS); PBS = f2pack(b, b); }
+#pragma unroll
+                for (int q = 0; q < KIN / 2; q++) {
+                    const u64 bsum = add2(PB, Bf2[q]);
+                    const u64 t = add2(PT, s2[q]);
+                    u64 num;
+                    if (MODE == M_EXCL) {
+                        num = fma2(t, bsum, add2(PBS, bsn2[q]));       // T' B - sum B S'
+                    } else if (MODE == M_PAPER) {
+                        num = mul2(t, bsum);                           // T' B
+                    } else {
+                        float e0, e1;
+                        f2unpack(add2(t, NLAMN2), e0, e1);
+                        num = mul2(f2pack(fmaxf(e0, 0.0f), fmaxf(e1, 0.0f)), bsum);  // max(0,T'-LN) B
+                    }
+                    const u64 key = fma2(num, INV2, bsum);
+                    float k0, k1;
+                    f2unpack(key, k0, k1);
+                    if (QOS) {
+                        if (sfv[2 * q] <= c1 && Tpf <= uv[2 * q]) m0 = fminf(m0, k0);
+                        if (sfv[2 * q + 1] <= c1 && Tpf <= uv[2 * q + 1]) m1 = fminf(m1, k1);
+                    } else {
+                        m0 = fminf(m0, k0);
+                        m1 = fminf(m1, k1);
+                    }
+                }
+            }
+            if (NP > 0) {
+                if (advance<NP>(d, L)) hi_sums<NP>(sl, su.Lmax, d, h);
+            }
+        }
+        scored = hi - lo;
+    }
+    (void)scored;
+    float* slot = submin + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
+    team_min_write(fminf(m0, m1), red, slot, team, lane, T, active);
+}
+
+// Generic (unpacked) filter: MAX / ENERGY objectives, and MATRIX slowdown (any objective).
+template <int NP, int MODE, int OBJ, bool QOS>
+__global__ void __launch_bounds__(P1_THREADS, 2)
+k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
+            float* __restrict__ submin_sure) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ float red[P1_THREADS];
+    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
+
+    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
+    const int prob = blockIdx.x / ipS;
+    const int li = blockIdx.x % ipS;
+    const Prob& P = probs[prob];
+    if (P.status != 0) return;
+    uint64_t slo, shi;
+    shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
+    const uint64_t item = slo + (uint64_t)li;
+    if (item >= shi) return;
+
+    constexpr int W = NP + 1;
+    stage_levels(sl, levs + (size_t)prob * su.W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
+
+    int L[W];
+#pragma unroll
+    for (int w = 0; w < W; w++) L[w] = P.L[w];
+    const int Lin = L[NP];
+    const int T = team_size_of(Lin), teams = teams_of(Lin);
+    const int team = threadIdx.x / T, lane = threadIdx.x % T;
+    const bool active = team < teams;
+
+    float iBf[KIN], iBk[KIN], isf[KIN], iu[KIN];
+    const Lev* inner = sl + NP * su.Lmax;
+#pragma unroll
+    for (int j = 0; j < KIN; j++) {
+        const Lev& a = inner[min(lane * KIN + j, Lin - 1)];
+        iBf[j] = __ll2float_rn(a.B);
+        iBk[j] = a.Bk;
+        isf[j] = (float)a.S;
+        iu[j] = (float)(a.Tmax - a.S);
+    }
+    float Mcol[W], Mrow_in[W];  // M[w][inner], M[inner][w]
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+        Mcol[w] = P.Mf[w * MAXW_ENUM + NP];
+        Mrow_in[w] = P.Mf[NP * MAXW_ENUM + w];
+    }
+
+    float m = INFINITY, ms = INFINITY;
+    uint64_t lo = 0, hi = 0;
+    if (active) subchunk_range(P, item, team, teams, &lo, &hi);
+    if (active && lo < hi) {
+        int d[NP > 0 ? NP : 1];
+        if (NP > 0) decode_prefix<NP>(lo, L, d);
+        for (uint64_t p = lo; p < hi; p++) {
+            // prefix workers' values
+            float pBf[W], pBk[W], psf[W];
+            int64_t pB = 0;
+            int32_t pT = 0, pTm = 1 << 24;
+#pragma unroll
+            for (int w = 0; w < NP; w++) {
+                const Lev& r = sl[w * su.Lmax + d[w]];
+                pBf[w] = __ll2float_rn(r.B);
+                pBk[w] = r.Bk;
+                psf[w] = (float)r.S;
+                pB += r.B; pT += r.S; pTm = min(pTm, r.Tmax);
+            }
+            const float Tpf = (float)pT;
+            const float c1 = (float)(pTm - pT);
+            // MATRIX: prefix part of every overlap (chain over prefix workers)
+            float Opre[W];
+            if (MODE == M_MATRIX) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    float o = 0.0f;
+#pragma unroll
+                    for (int v = 0; v < NP; v++)
+                        if (v != w) o = fmaf(P.Mf[w * MAXW_ENUM + v], psf[v], o);
+                    Opre[w] = o;
+                }
+            }
+            const float Bpf = __ll2float_rn(pB);
+#pragma unroll
+            for (int j = 0; j < KIN; j++) {
+                const float Tf = Tpf + isf[j];
+                float Lw[W];
+                float num = 0.0f;
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    const float bf = (w == NP) ? iBf[j] : pBf[w];
+                    const float bk = (w == NP) ? iBk[j] : pBk[w];
+                    float O;
+                    if (MODE == M_EXCL) O = (w == NP) ? Tpf : (Tf - psf[w]);
+                    else if (MODE == M_PAPER) O = Tf;
+                    else if (MODE == M_EXCESS) O = fmaxf(Tf - P.lamNf, 0.0f);
+                    else O = (w == NP) ? Opre[w] : fmaf(Mcol[w], isf[j], Opre[w]);
+                    Lw[w] = fmaf(O, bk, bf);
+                    if (OBJ == O_SUM) num = fmaf(bf, O, num);
+                }
+                float key;
+                if (OBJ == O_SUM) {
+                    key = fmaf(num, P.inv, Bpf + iBf[j]);
+                } else {
+                    float mx = Lw[0];
+#pragma unroll
+                    for (int w = 1; w < W; w++) mx = fmaxf(mx, Lw[w]);
+                    if (OBJ == O_MAX) key = mx;
+                    else key = fmaf(P.p_dyn, fminf(1.0f, Tf * P.inv), P.p_idle) * mx;
+                }
+                if (QOS) {
+                    if (MODE == M_MATRIX) {
+                        bool maybe = true, sure = true;
+#pragma unroll
+                        for (int w = 0; w < W; w++) {
+                            maybe = maybe && (Lw[w] <= P.Qhi[w]);
+                            sure = sure && (Lw[w] <= P.Qlo[w]);
+                        }
+                        if (maybe) m = fminf(m, key);
+                        if (sure) ms = fminf(ms, key);
+                    } else {
+                        if (isf[j] <= c1 && Tpf <= iu[j]) m = fminf(m, key);
+                    }
+                } else {
+                    m = fminf(m, key);
+                }
+            }
+            if (NP > 0) (void)advance<NP>(d, L);
+        }
+    }
+    (void)Mrow_in;
+    float* slot = submin + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
+    team_min_write(m, red, slot, team, lane, T, active);
+    if (MODE == M_MATRIX && QOS) {
+        float* slot2 = submin_sure + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
+        team_min_write(ms, red, slot2, team, lane, T, active);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// pass-1 dispatch
+// ------------------------------------------------------------------------------------------
+typedef void (*P1Sum)(Setup, const Prob*, const Lev*, float*);
+typedef void (*P1Gen)(Setup, const Prob*, const Lev*, float*, float*);
+
+template <int NP>
+static P1Sum pick_sum(int mode, bool qos) {
+    if (mode == M_EXCL) return qos ? k_pass1_sum<NP, M_EXCL, true> : k_pass1_sum<NP, M_EXCL, false>;
+    if (mode == M_PAPER) return qos ? k_pass1_sum<NP, M_PAPER, true> : k_pass1_sum<NP, M_PAPER, false>;
+    return qos ? k_pass1_sum<NP, M_EXCESS, true> : k_pass1_sum<NP, M_EXCESS, false>;
+}
+template <int NP, int MODE>
+static P1Gen pick_gen_m(int obj, bool qos) {
+    if (obj == O_SUM) return qos ? k_pass1_gen<NP, MODE, O_SUM, true> : k_pass1_gen<NP, MODE, O_SUM, false>;
+    if (obj == O_MAX) return qos ? k_pass1_gen<NP, MODE, O_MAX, true> : k_pass1_gen<NP, MODE, O_MAX, false>;
+    return qos ? k_pass1_gen<NP, MODE, O_ENERGY, true> : k_pass1_gen<NP, MODE, O_ENERGY, false>;
+}
+template <int NP>
+static P1Gen pick_gen(int mode, int obj, bool qos) {
+    if (mode == M_EXCL) return pick_gen_m<NP, M_EXCL>(obj, qos);
+    if (mode == M_PAPER) return pick_gen_m<NP, M_PAPER>(obj, qos);
+    if (mode == M_EXCESS) return pick_gen_m<NP, M_EXCESS>(obj, qos);
+    return pick_gen_m<NP, M_MATRIX>(obj, qos);
+}
+
+cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
+    const int NP = su.W - 1;
+    const bool qos = su.has_qos != 0;
+    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
+    const size_t grid = (size_t)su.n_problems * ipS;
+    const size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
+    if (grid == 0) return cudaSuccess;
+    if (su.obj == O_SUM && su.mode != M_MATRIX) {
+        P1Sum f = nullptr;
+        switch (NP) {
+            case 0: f = pick_sum<0>(su.mode, qos); break;
+            case 1: f = pick_sum<1>(su.mode, qos); break;
+            case 2: f = pick_sum<2>(su.mode, qos); break;
+            case 3: f = pick_sum<3>(su.mode, qos); break;
+            case 4: f = pick_sum<4>(su.mode, qos); break;
+            case 5: f = pick_sum<5>(su.mode, qos); break;
+            case 6: f = pick_sum<6>(su.mode, qos); break;
+            case 7: f = pick_sum<7>(su.mode, qos); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin);
+    } else {
+        P1Gen f = nullptr;
+        switch (NP) {
+            case 0: f = pick_gen<0>(su.mode, su.obj, qos); break;
+            case 1: f = pick_gen<1>(su.mode, su.obj, qos); break;
+            case 2: f = pick_gen<2>(su.mode, su.obj, qos); break;
+            case 3: f = pick_gen<3>(su.mode, su.obj, qos); break;
+            case 4: f = pick_gen<4>(su.mode, su.obj, qos); break;
+            case 5: f = pick_gen<5>(su.mode, su.obj, qos); break;
+            case 6: f = pick_gen<6>(su.mode, su.obj, qos); break;
+            case 7: f = pick_gen<7>(su.mode, su.obj, qos); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.submin_sure);
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// local minimum per problem over this shard's sub-chunks (one warp per problem)
+// ------------------------------------------------------------------------------------------
+__global__ void k_reduce_min(Setup su, const Prob* probs, const float* submin, const float* submin_sure, float* m32,
+                             float* m32_sure) {
+    int p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (p >= su.n_problems) return;
+    const Prob& P = probs[p];
+    float m = INFINITY, ms = INFINITY;
+    if (P.status == 0) {
+        uint64_t slo, shi;
+        shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
+        const int teams = teams_of(P.L[su.W - 1]);
+        for (uint64_t it = slo; it < shi; it++) {
+            for (int t = lane; t < teams; t += 32) {
+                size_t s = ((size_t)p * su.items_max + it) * su.teams + t;
+                m = fminf(m, submin[s]);
+                if (submin_sure) ms = fminf(ms, submin_sure[s]);
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        ms = fminf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+    }
+    if (lane == 0) {
+        m32[p] = m;
+        if (m32_sure) m32_sure[p] = submin_sure ? ms : m;
+    }
+}
+
+cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
+    const bool two = su.mode == M_MATRIX && su.has_qos;
+    int wpb = 8;
+    k_reduce_min<<<(su.n_problems + wpb - 1) / wpb, 32 * wpb, 0, st>>>(su, wk.probs, wk.submin,
+                                                                       two ? wk.submin_sure : nullptr, wk.m32,
+                                                                       wk.m32_sure);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// exact evaluation (pass 2)
+// ------------------------------------------------------------------------------------------
+// exact key of tuple lv (staged records sl); returns false if a QoS bound fails
+__device__ bool exact_key(const Setup& su, const Prob& P, const Lev* sl, const int* lv, U256& key) {
+    const int W = su.W;
+    int64_t Tp = 0;
+    for (int w = 0; w < W; w++) Tp += sl[w * su.Lmax + lv[w]].S;
+    u128 sum = 0, mx = 0;
+    for (int w = 0; w < W; w++) {
+        const Lev& r = sl[w * su.Lmax + lv[w]];
+        u128 O;
+        if (su.mode == M_EXCL) O = (u128)(Tp - r.S);
+        else if (su.mode == M_PAPER) O = (u128)Tp;
+        else if (su.mode == M_EXCESS) O = Tp > P.lamN ? (u128)(Tp - P.lamN) : (u128)0;
+        else {
+            O = 0;
+            for (int v = 0; v < W; v++)
+                if (v != w) O += (u128)P.Mi[w * MAXW_ENUM + v] * (u128)sl[v * su.Lmax + lv[v]].S;
+        }
+        u128 h = (u128)r.B * (P.D + O);
+        if (h > P.Hq[w]) return false;
+        sum += h;
+        if (h > mx) mx = h;
+    }
+    if (su.obj == O_SUM) key = u256_of(sum);
+    else if (su.obj == O_MAX) key = u256_of(mx);
+    else {
+        int64_t occ = Tp < P.lamN ? Tp : P.lamN;
+        u128 pn = P.pi_idle * (u128)P.lamN + P.pi_dyn * (u128)occ;
+        key = u256_mul128(pn, mx);
+    }
+    return true;
+}
+
+// scalar FP32 filter key (error <= delta) and maybe-feasibility, for pass 2
+__device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, const int* lv, float& key) {
+    const int W = su.W;
+    int64_t Tp = 0, SB = 0, SBS = 0;
+    for (int w = 0; w < W; w++) {
+        const Lev& r = sl[w * su.Lmax + lv[w]];
+        Tp += r.S; SB += r.B; SBS += r.BS;
+    }
+    const float Tf = (float)Tp;
+    float Lw[MAXW_ENUM];
+    float num = 0.0f;
+    bool feas = true;
+    for (int w = 0; w < W; w++) {
+        const Lev& r = sl[w * su.Lmax + lv[w]];
+        const float bf = __ll2float_rn(r.B);
+        float O;
+        if (su.mode == M_EXCL) O = Tf - (float)r.S;
+        else if (su.mode == M_PAPER) O = Tf;
+        else if (su.mode == M_EXCESS) O = fmaxf(Tf - P.lamNf, 0.0f);
+        else {
+            O = 0.0f;
+            for (int v = 0; v < W; v++)
+                if (v != w) O = fmaf(P.Mf[w * MAXW_ENUM + v], (float)sl[v * su.Lmax + lv[v]].S, O);
+        }
+        Lw[w] = fmaf(O, r.Bk, bf);
+        num = fmaf(bf, O, num);
+        if (su.has_qos) {
+            if (su.mode == M_MATRIX) feas = feas && (Lw[w] <= P.Qhi[w]);
+            else feas = feas && (Tp <= (int64_t)r.Tmax);
+        }
+    }
+    if (su.obj == O_SUM) {
+        if (su.mode == M_EXCL) {
+            const float bsum = __ll2float_rn(SB);
+            key = fmaf(fmaf(Tf, bsum, -__ll2float_rn(SBS)), P.inv, bsum);
+        } else {
+            key = fmaf(num, P.inv, __ll2float_rn(SB));
+        }
+    } else {
+        float mx = Lw[0];
+        for (int w = 1; w < W; w++) mx = fmaxf(mx, Lw[w]);
+        key = (su.obj == O_MAX) ? mx : fmaf(P.p_dyn, fminf(1.0f, Tf * P.inv), P.p_idle) * mx;
+    }
+    return feas;
+}
+
+__device__ float band_bound(const Setup& su, float m, float ms) {
+    // every candidate with exact key <= H*(1+tau) has key32 <= bound; H* <= ms / (1 - delta)
+    double base = (su.mode == M_MATRIX && su.has_qos) ? (double)ms : (double)m;
+    if (isinf(base)) return INFINITY;
+    double tau = (double)su.tol_num / (double)su.tol_den;
+    double b = base * (1.0 + tau) * (1.0 + su.delta) / (1.0 - su.delta) * (1.0 + 1e-12);
+    return __double2float_ru(b);
+}
+
+// one CTA per problem.  mode 0: exact minimum over the band.  mode 1: lowest index within tol.
+template <int PASS>
+__global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
+                                               const float* __restrict__ submin, const float* m32,
+                                               const float* m32_sure, U256* hstar, uint64_t* first) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ U256 red[512];
+    __shared__ uint64_t redi[512];
+    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
+    const int prob = blockIdx.x;
+    Prob& P = probs[prob];
+    if (P.status != 0) return;
+    if (isinf(m32[prob])) {  // nothing feasible anywhere (global minimum is +inf)
+        if (threadIdx.x == 0) {
+            if (PASS == 0) hstar[prob] = u256_max();
+            else first[prob] = ~0ull;
+        }
+        return;
+    }
+    const int W = su.W;
+    stage_levels(sl, levs + (size_t)prob * W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
+    const float bound = band_bound(su, m32[prob], m32_sure ? m32_sure[prob] : m32[prob]);
+    const int Lin = P.L[W - 1];
+    const int teams = teams_of(Lin);
+    uint64_t slo, shi;
+    shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
+    U256 best = u256_max();
+    uint64_t besti = ~0ull;
+    U256 hs = (PASS == 1) ? hstar[prob] : u256_zero();
+    if (PASS == 1 && u256_is_max(hs)) {  // no exactly-feasible candidate
+        if (threadIdx.x == 0) first[prob] = ~0ull;
+        return;
+    }
+    for (uint64_t it = slo; it < shi; it++) {
+        for (int t = 0; t < teams; t++) {
+            if (!(submin[((size_t)prob * su.items_max + it) * su.teams + t] <= bound)) continue;
+            uint64_t lo, hi;
+            subchunk_range(P, it, t, teams, &lo, &hi);
+            uint64_t ncand = (hi - lo) * (uint64_t)Lin;
+            for (uint64_t c = threadIdx.x; c < ncand; c += blockDim.x) {
+                uint64_t pre = lo + c / (uint64_t)Lin;
+                int lv[MAXW_ENUM];
+                lv[W - 1] = (int)(c % (uint64_t)Lin);
+                uint64_t q = pre;
+                for (int w = W - 2; w >= 0; w--) {
+                    lv[w] = (int)(q % (uint64_t)P.L[w]);
+                    q /= (uint64_t)P.L[w];
+                }
+                float k32;
+                if (!key32_scalar(su, P, sl, lv, k32)) continue;
+                if (!(k32 <= bound)) continue;
+                U256 k;
+                if (!exact_key(su, P, sl, lv, k)) continue;
+                if (PASS == 0) {
+                    if (u256_cmp(k, best) < 0) best = k;
+                } else {
+                    if (within_tol(k, hs, su.tol_num, su.tol_den)) {
+                        uint64_t idx = pre * (uint64_t)Lin + (uint64_t)lv[W - 1];
+                        if (idx < besti) besti = idx;
+                    }
+                }
+            }
+        }
+        if (PASS == 1) {
+            // items are in index order: stop at the first item holding a hit
+            if (__syncthreads_or(besti != ~0ull)) break;
+        }
+    }
+    if (PASS == 0) {
+        red[threadIdx.x] = best;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s && u256_cmp(red[threadIdx.x + s], red[threadIdx.x]) < 0) red[threadIdx.x] = red[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) hstar[prob] = red[0];
+    } else {
+        redi[threadIdx.x] = besti;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s && redi[threadIdx.x + s] < redi[threadIdx.x]) redi[threadIdx.x] = redi[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) first[prob] = redi[0];
+    }
+}
+
+cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
+    size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_pass2<0><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 wk.hstar, wk.first);
+    return cudaGetLastError();
+}
+cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
+    size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_pass2<1><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 wk.hstar, wk.first);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// materialisation (a9): one thread per problem
+// ------------------------------------------------------------------------------------------
+__global__ void k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs, const U256* hstar,
+                              const uint64_t* first, const int32_t* sizes, int C, MatOut o) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= su.n_problems) return;
+    const Prob& P = probs[p];
+    const int W = su.W;
+    int status = P.status;
+    if (status == 0 && (first[p] == ~0ull || u256_is_max(hstar[p]))) status = 1;  // infeasible
+    if (o.status) o.status[p] = status;
+    if (status != 0) {
+        if (o.index) o.index[p] = 0;
+        if (o.objective) o.objective[p] = 0.0;
+        if (o.makespan) o.makespan[p] = 0.0;
+        if (o.power) o.power[p] = 0.0;
+        if (o.energy) o.energy[p] = 0.0;
+        if (o.thr) o.thr[p] = 0.0;
+        for (int w = 0; w < W; w++) {
+            if (o.levels) o.levels[(size_t)p * W + w] = -1;
+            if (o.latency) o.latency[(size_t)p * W + w] = 0.0;
+            if (o.switches) o.switches[(size_t)p * W + w] = 0;
+            if (o.group_sm)
+                for (int g = 0; g < o.group_stride; g++) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = 0;
+        }
+        return;
+    }
+    uint64_t idx = first[p];
+    int lv[MAXW_ENUM];
+    uint64_t q = idx;
+    for (int w = W - 1; w >= 0; w--) {
+        lv[w] = (int)(q % (uint64_t)P.L[w]);
+        q /= (uint64_t)P.L[w];
+    }
+    // FP64 values from exact integers
+    double avg[MAXW_ENUM], Bw[MAXW_ENUM], sum_avg = 0.0;
+    for (int w = 0; w < W; w++) {
+        int t = P.table[w];
+        avg[w] = (double)tb.S[t][lv[w]] / (double)tb.K[t];
+        Bw[w] = (double)tb.B[t][lv[w]];
+        sum_avg += avg[w];
+    }
+    const double N = (double)su.N;
+    double mk = 0.0, obj = 0.0, thr = 0.0;
+    for (int w = 0; w < W; w++) {
+        double ov;
+        if (su.mode == M_EXCL) ov = sum_avg - avg[w];
+        else if (su.mode == M_PAPER) ov = sum_avg;
+        else if (su.mode == M_EXCESS) ov = sum_avg - N > 0.0 ? sum_avg - N : 0.0;
+        else {
+            ov = 0.0;
+            for (int v = 0; v < W; v++)
+                if (v != w) ov += (double)P.Mf[w * MAXW_ENUM + v] * avg[v];
+        }
+        double alpha = ov / N;
+        double Lw = Bw[w] * (1.0 + alpha);
+        mk = Lw > mk ? Lw : mk;
+        obj += Lw;
+        thr += 1e9 / Lw;
+        int t = P.table[w];
+        int G = tb.G[t];
+        const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
+        int sw = 0;
+        for (int g = 0; g < G; g++) {
+            if (g > 0 && wit[g] != wit[g - 1]) sw++;
+            if (o.group_sm && g < o.group_stride) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = sizes[wit[g]];
+            if (o.group_lat) o.group_lat[((size_t)p * W + w) * o.group_stride + g] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha);
+        }
+        if (o.group_sm)
+            for (int g = G; g < o.group_stride; g++) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = 0;
+        if (o.latency) o.latency[(size_t)p * W + w] = Lw;
+        if (o.switches) o.switches[(size_t)p * W + w] = sw;
+        if (o.levels) o.levels[(size_t)p * W + w] = lv[w];
+    }
+    double frac = sum_avg / N;
+    if (frac > 1.0) frac = 1.0;
+    double pw = (double)P.p_idle + ((double)P.p_max - (double)P.p_idle) * frac;
+    if (su.obj == O_MAX) obj = mk;
+    else if (su.obj == O_ENERGY) obj = pw * mk;
+    if (o.index) o.index[p] = idx;
+    if (o.objective) o.objective[p] = obj;
+    if (o.makespan) o.makespan[p] = mk;
+    if (o.power) o.power[p] = pw;
+    if (o.energy) o.energy[p] = pw * mk * 1e-9;
+    if (o.thr) o.thr[p] = thr;
+    if (o.key) {
+        U256 k;
+        exact_key(su, P, levs + (size_t)p * W * su.Lmax, lv, k);
+        for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
+    }
+}
+
+cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C, MatOut out,
+                               cudaStream_t st) {
+    k_materialize<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes,
+                                                               C, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
+                        cudaStream_t st) {
+    (void)C; (void)sizes;
+    k_prep_prob<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, in, wk.probs);
+    size_t n = (size_t)su.n_problems * su.W * su.Lmax;
+    k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
+    return cudaGetLastError();
+}
+
+}  // namespace eclip

@@ -1,0 +1,454 @@
+// slice.cu — SLICE engine kernels (K3 FP32 slice DP, exact slice DP, K4 lexicographic walk).
+// See slice.h and DESIGN.md §4.  Derivation (App. A.2 of SURVEY.md): in
+// the linear modes (EXCLUDE_SELF, PAPER_AS_WRITTEN, EXCESS) O_w depends on the tuple only
+// through (T', S'_w), so with T' fixed the SUM objective separates into per-worker terms.
+#include <algorithm>
+#include <cstdio>
+#include <numeric>
+#include <vector>
+
+#include "slice.h"
+
+namespace eclip {
+
+static constexpr uint64_t UINF = ~0ull;
+static constexpr int SL_THREADS = 256;
+
+SliceState::~SliceState() { release(); }
+void SliceState::release() {
+    for (void* p : allocs) cudaFreeAsync(p, st);
+    allocs.clear();
+}
+
+uint64_t slice_units(const SliceState& s) {
+    unsigned long long u = 0;
+    if (s.d_units) cudaMemcpy(&u, s.d_units, sizeof u, cudaMemcpyDeviceToHost);
+    return u;
+}
+
+// per-slice D range of worker w (w >= 1): P values reachable from T with workers w..W-1
+__device__ __forceinline__ void drange(const SliceDev& S, int64_t T, int w, int64_t* lo, int64_t* hi) {
+    int64_t a = T - S.phi[w], b = T - S.plo[w];
+    *lo = a > S.slo[w] ? a : S.slo[w];
+    *hi = b < S.shi[w] ? b : S.shi[w];
+}
+
+__device__ __forceinline__ int64_t overlap_exact(int mode, int64_t Tp, int64_t Sp, int64_t lamN) {
+    if (mode == M_EXCL) return Tp - Sp;
+    if (mode == M_PAPER) return Tp;
+    return Tp > lamN ? Tp - lamN : 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// K3: FP32 filter DP, one CTA per slice (interleaved over shards)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob* probs, const Lev* __restrict__ levs,
+                                                          const int16_t* __restrict__ dense, float* J32,
+                                                          unsigned long long* units) {
+    unsigned long long cnt = 0;
+    extern __shared__ float sm[];
+    const Prob& P = probs[0];
+    int64_t T = S.Tlo + S.shard + (int64_t)S.n_shards * blockIdx.x;
+    if (T > S.Thi) return;
+    const int W = S.W;
+    float* g = sm;                       // [gtot]
+    float* Da = g + S.gtot;              // [maxrange]
+    float* Db = Da + S.maxrange;         // [maxrange]
+    const int64_t Tp = T * S.gS;
+    const float Tpf = (float)Tp;
+    for (int i = threadIdx.x; i < S.gtot; i += blockDim.x) {
+        int w = 0;
+        while (w + 1 < W && S.doff[w + 1] <= i) w++;
+        int l = dense[i];
+        float v = INFINITY;
+        if (l >= 0) {
+            const Lev& r = levs[w * S.Lmax + l];
+            if (Tp <= (int64_t)r.Tmax) {
+                float O = (float)overlap_exact(S.mode, Tp, r.S, P.lamN);
+                v = fmaf(O, r.Bk, __ll2float_rn(r.B));
+            }
+        }
+        g[i] = v;
+    }
+    __syncthreads();
+    float* Dn = Da;   // D_{w+1}
+    float* Dc = Db;   // D_w
+    int64_t nlo = 0, nhi = -1;
+    if (W >= 2) {
+        drange(S, T, W - 1, &nlo, &nhi);
+        const float* gw = g + S.doff[W - 1];
+        for (int64_t p = nlo + threadIdx.x; p <= nhi; p += blockDim.x) Dn[p - nlo] = gw[p - S.smin[W - 1]];
+        __syncthreads();
+        for (int w = W - 2; w >= 1; w--) {
+            int64_t lo, hi;
+            drange(S, T, w, &lo, &hi);
+            const float* gw2 = g + S.doff[w];
+            const int nk = S.smax[w] - S.smin[w] + 1;
+            for (int64_t p = lo + threadIdx.x; p <= hi; p += blockDim.x) {
+                float best = INFINITY;
+                // rest = p - smin_w - k must lie in [nlo, nhi]
+                int64_t k0 = p - S.smin[w] - nhi, k1 = p - S.smin[w] - nlo;
+                int ka = (int)(k0 > 0 ? k0 : 0), kb = (int)(k1 < nk - 1 ? k1 : nk - 1);
+                const float* dn = Dn + (p - S.smin[w] - nlo);
+                if (kb >= ka) cnt += (unsigned long long)(kb - ka + 1);
+                for (int k = ka; k <= kb; k++) {
+                    float v = (S.obj == O_SUM) ? gw2[k] + dn[-k] : fmaxf(gw2[k], dn[-k]);
+                    best = fminf(best, v);
+                }
+                Dc[p - lo] = best;
+            }
+            __syncthreads();
+            float* t = Dn; Dn = Dc; Dc = t;
+            nlo = lo; nhi = hi;
+        }
+    }
+    // J = min_k g_0[k] (+) D_1[T - smin_0 - k]
+    float J = INFINITY;
+    const int nk0 = S.smax[0] - S.smin[0] + 1;
+    for (int k = threadIdx.x; k < nk0; k += blockDim.x) {
+        int64_t rest = T - S.smin[0] - k;
+        float v;
+        if (W == 1) {
+            if (rest != 0) continue;
+            v = g[k];
+        } else {
+            if (rest < nlo || rest > nhi) continue;
+            float d = Dn[rest - nlo];
+            v = (S.obj == O_SUM) ? g[k] + d : fmaxf(g[k], d);
+        }
+        J = fminf(J, v);
+        cnt++;
+    }
+    if (cnt) atomicAdd(units, cnt);
+    __shared__ float red[SL_THREADS];
+    red[threadIdx.x] = J;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fminf(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        float j = red[0];
+        if (S.obj == O_ENERGY && j < INFINITY) j = fmaf(P.p_dyn, fminf(1.0f, Tpf * P.inv), P.p_idle) * j;
+        J32[T - S.Tlo] = j;
+    }
+}
+
+// min over this shard's slices -> m32[0]; and the band list
+__global__ void k_slice_min(SliceDev S, const float* J32, float* m32) {
+    __shared__ float red[1024];
+    float m = INFINITY;
+    for (int64_t i = S.shard + (int64_t)S.n_shards * threadIdx.x; i < S.n_slices; i += (int64_t)S.n_shards * blockDim.x)
+        m = fminf(m, J32[i]);
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fminf(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) m32[0] = red[0];
+}
+
+__global__ void k_slice_band(SliceDev S, const float* J32, const float* m32, int32_t* band, int32_t* nband) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    float m = m32[0];
+    float bound = INFINITY;
+    if (!isinf(m)) {
+        double tau = (double)S.tol_num / (double)S.tol_den;
+        bound = __double2float_ru((double)m * (1.0 + tau) * (1.0 + S.delta) / (1.0 - S.delta) * (1.0 + 1e-12));
+    }
+    for (int64_t i = S.shard + (int64_t)S.n_shards * threadIdx.x; i < S.n_slices; i += (int64_t)S.n_shards * blockDim.x) {
+        if (!isinf(m) && J32[i] <= bound) {
+            int pos = atomicAdd(&cnt, 1);
+            band[pos] = (int32_t)i;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *nband = cnt;
+}
+
+// ------------------------------------------------------------------------------------------
+// exact DP of one slice into scratch (u64 per entry, UINF = infeasible); returns J via smem
+// layout of scratch: [g: gtot][D_1 .. D_{W-1}: maxrange each]
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t comb_u(int obj, uint64_t a, uint64_t b) {
+    if (a == UINF || b == UINF) return UINF;
+    return obj == O_SUM ? a + b : (a > b ? a : b);
+}
+
+__device__ void slice_exact_dp(const SliceDev& S, const Prob& P, const Lev* levs, const int16_t* dense, int64_t T,
+                               uint64_t* scr, int64_t* dlo, int64_t* dhi) {
+    const int W = S.W;
+    uint64_t* h = scr;
+    const int64_t Tp = T * S.gS;
+    for (int i = threadIdx.x; i < S.gtot; i += blockDim.x) {
+        int w = 0;
+        while (w + 1 < W && S.doff[w + 1] <= i) w++;
+        int l = dense[i];
+        uint64_t v = UINF;
+        if (l >= 0) {
+            const Lev& r = levs[w * S.Lmax + l];
+            if (Tp <= (int64_t)r.Tmax) v = (uint64_t)r.B * (uint64_t)(P.lamN + overlap_exact(S.mode, Tp, r.S, P.lamN));
+        }
+        h[i] = v;
+    }
+    if (threadIdx.x == 0)
+        for (int w = 1; w < W; w++) drange(S, T, w, &dlo[w], &dhi[w]);
+    __syncthreads();
+    if (W >= 2) {
+        uint64_t* D = scr + S.gtot + (size_t)(W - 1 - 1) * S.maxrange;
+        const uint64_t* hw = h + S.doff[W - 1];
+        for (int64_t p = dlo[W - 1] + threadIdx.x; p <= dhi[W - 1]; p += blockDim.x) D[p - dlo[W - 1]] = hw[p - S.smin[W - 1]];
+        __syncthreads();
+        for (int w = W - 2; w >= 1; w--) {
+            uint64_t* Dc = scr + S.gtot + (size_t)(w - 1) * S.maxrange;
+            const uint64_t* Dn = scr + S.gtot + (size_t)w * S.maxrange;
+            const uint64_t* hw2 = h + S.doff[w];
+            const int nk = S.smax[w] - S.smin[w] + 1;
+            for (int64_t p = dlo[w] + threadIdx.x; p <= dhi[w]; p += blockDim.x) {
+                uint64_t best = UINF;
+                for (int k = 0; k < nk; k++) {
+                    int64_t rest = p - S.smin[w] - k;
+                    if (rest < dlo[w + 1] || rest > dhi[w + 1]) continue;
+                    uint64_t v = comb_u(S.obj, hw2[k], Dn[rest - dlo[w + 1]]);
+                    if (v < best) best = v;
+                }
+                Dc[p - dlo[w]] = best;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__device__ U256 slice_key(const SliceDev& S, const Prob& P, int64_t Tp, uint64_t v) {
+    if (S.obj != O_ENERGY) return u256_of((u128)v);
+    int64_t occ = Tp < P.lamN ? Tp : P.lamN;
+    u128 pn = P.pi_idle * (u128)P.lamN + P.pi_dyn * (u128)occ;
+    return u256_mul128(pn, (u128)v);
+}
+
+// pass 2a: exact J for every band slice
+__global__ void __launch_bounds__(SL_THREADS) k_slice_exact(SliceDev S, const Prob* probs, const Lev* levs,
+                                                            const int16_t* dense, const int32_t* band,
+                                                            const int32_t* nband, uint64_t* scratch, U256* Jex) {
+    const Prob& P = probs[0];
+    __shared__ int64_t dlo[MAXW + 1], dhi[MAXW + 1];
+    __shared__ uint64_t red[SL_THREADS];
+    uint64_t* scr = scratch + (size_t)blockIdx.x * (S.gtot + (size_t)(S.W) * S.maxrange);
+    for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x) {
+        int64_t T = S.Tlo + band[bi];
+        slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
+        const int W = S.W;
+        const uint64_t* h = scr;
+        uint64_t J = UINF;
+        const int nk0 = S.smax[0] - S.smin[0] + 1;
+        for (int k = threadIdx.x; k < nk0; k += blockDim.x) {
+            int64_t rest = T - S.smin[0] - k;
+            uint64_t v;
+            if (W == 1) {
+                if (rest != 0) continue;
+                v = h[k];
+            } else {
+                if (rest < dlo[1] || rest > dhi[1]) continue;
+                v = comb_u(S.obj, h[k], scr[S.gtot + (rest - dlo[1])]);
+            }
+            if (v < J) J = v;
+        }
+        red[threadIdx.x] = J;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s && red[threadIdx.x + s] < red[threadIdx.x]) red[threadIdx.x] = red[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) Jex[band[bi]] = red[0] == UINF ? u256_max() : slice_key(S, P, T * S.gS, red[0]);
+        __syncthreads();
+    }
+}
+
+__global__ void k_slice_hstar(const int32_t* band, const int32_t* nband, const U256* Jex, U256* hstar) {
+    if (threadIdx.x != 0) return;
+    U256 m = u256_max();
+    for (int i = 0; i < *nband; i++)
+        if (u256_cmp(Jex[band[i]], m) < 0) m = Jex[band[i]];
+    hstar[0] = m;
+}
+
+// pass 2b: exact DP + lexicographic walk in every slice whose exact J is within tolerance
+__global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Prob* probs, const Lev* levs,
+                                                           const int16_t* dense, const int32_t* band,
+                                                           const int32_t* nband, uint64_t* scratch, const U256* Jex,
+                                                           const U256* hstar, unsigned long long* first) {
+    const Prob& P = probs[0];
+    __shared__ int64_t dlo[MAXW + 1], dhi[MAXW + 1];
+    uint64_t* scr = scratch + (size_t)blockIdx.x * (S.gtot + (size_t)(S.W) * S.maxrange);
+    const U256 hs = hstar[0];
+    if (u256_is_max(hs)) return;
+    for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x) {
+        if (u256_is_max(Jex[band[bi]]) || !within_tol(Jex[band[bi]], hs, S.tol_num, S.tol_den)) continue;
+        int64_t T = S.Tlo + band[bi];
+        slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
+        if (threadIdx.x == 0) {
+            const int W = S.W;
+            const int64_t Tp = T * S.gS;
+            int64_t rem = T;
+            uint64_t hp[MAXW];
+            int lv[MAXW];
+            bool ok = true;
+            for (int w = 0; w < W && ok; w++) {
+                bool found = false;
+                int L = P.L[w];
+                for (int l = 0; l < L; l++) {
+                    const Lev& r = levs[w * S.Lmax + l];
+                    int64_t s = r.S / S.gS;
+                    int64_t rest = rem - s;
+                    uint64_t hw = scr[S.doff[w] + (s - S.smin[w])];
+                    if (hw == UINF) continue;
+                    uint64_t v;
+                    if (w == W - 1) {
+                        if (rest != 0) continue;
+                        v = hw;
+                    } else {
+                        if (rest < dlo[w + 1] || rest > dhi[w + 1]) continue;
+                        v = comb_u(S.obj, hw, scr[S.gtot + (size_t)w * S.maxrange + (rest - dlo[w + 1])]);
+                    }
+                    for (int u = 0; u < w; u++) v = comb_u(S.obj, hp[u], v);
+                    if (v == UINF) continue;
+                    if (within_tol(slice_key(S, P, Tp, v), hs, S.tol_num, S.tol_den)) {
+                        lv[w] = l; hp[w] = hw; rem = rest; found = true;
+                        break;
+                    }
+                }
+                ok = found;
+            }
+            if (ok) {
+                uint64_t idx = 0;
+                for (int w = 0; w < W; w++) idx = idx * (uint64_t)P.L[w] + (uint64_t)lv[w];
+                atomicMin(first, (unsigned long long)idx);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+template <class T>
+static cudaError_t salloc(SliceState& s, T** p, size_t n) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(n, 1) * sizeof(T), s.st);
+    if (e == cudaSuccess) s.allocs.push_back(q);
+    *p = (T*)q;
+    return e;
+}
+
+#define CK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
+
+cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& wk, const int32_t* tabL,
+                        const int32_t* table_of, cudaStream_t st) {
+    (void)tb; (void)tabL; (void)table_of;
+    s.st = st;
+    const int W = su.W;
+    Prob P;
+    std::vector<Lev> lev((size_t)W * su.Lmax);
+    CK(cudaMemcpyAsync(&P, wk.probs, sizeof(Prob), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lev.data(), wk.levs, lev.size() * sizeof(Lev), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    SliceDev& S = s.h;
+    S.W = W; S.Lmax = su.Lmax; S.mode = su.mode; S.obj = su.obj;
+    S.shard = su.shard; S.n_shards = su.n_shards;
+    S.tol_num = su.tol_num; S.tol_den = su.tol_den;
+    S.delta = (double)(4 * W + 16) * std::ldexp(1.0, -24);
+    if (P.status != 0) {  // nothing to slice; the kernels see n_slices = 0
+        S.n_slices = 0; S.gtot = 1; S.maxrange = 1; S.gS = 1; S.Tlo = 0; S.Thi = -1;
+        CK(salloc(s, &s.dense, 1)); CK(salloc(s, &s.J32, 1)); CK(salloc(s, &s.Jex, 1));
+        CK(salloc(s, &s.band, 1)); CK(salloc(s, &s.nband, 1)); CK(salloc(s, &s.scratch, 1));
+        CK(salloc(s, &s.d_units, 1));
+        CK(cudaMemsetAsync(s.nband, 0, 4, st));
+        s.slots = 1;
+        return cudaSuccess;
+    }
+    int64_t g = 0;
+    for (int w = 0; w < W; w++)
+        for (int l = 0; l < P.L[w]; l++) g = std::gcd(g, (int64_t)lev[(size_t)w * su.Lmax + l].S);
+    if (g == 0) g = 1;
+    S.gS = g;
+    std::vector<int16_t> dense;
+    for (int w = 0; w < W; w++) {
+        int mn = INT32_MAX, mx = 0;
+        for (int l = 0; l < P.L[w]; l++) {
+            int v = (int)(lev[(size_t)w * su.Lmax + l].S / g);
+            mn = std::min(mn, v); mx = std::max(mx, v);
+        }
+        S.smin[w] = mn; S.smax[w] = mx;
+        S.doff[w] = (int32_t)dense.size();
+        size_t base = dense.size();
+        dense.resize(base + (mx - mn + 1), -1);
+        for (int l = 0; l < P.L[w]; l++) dense[base + lev[(size_t)w * su.Lmax + l].S / g - mn] = (int16_t)l;
+    }
+    if (su.Lmax > 32767) return cudaErrorInvalidValue;
+    S.gtot = (int32_t)dense.size();
+    S.plo[0] = 0; S.phi[0] = 0;
+    for (int w = 0; w < W; w++) { S.plo[w + 1] = S.plo[w] + S.smin[w]; S.phi[w + 1] = S.phi[w] + S.smax[w]; }
+    S.slo[W] = 0; S.shi[W] = 0;
+    for (int w = W - 1; w >= 0; w--) { S.slo[w] = S.slo[w + 1] + S.smin[w]; S.shi[w] = S.shi[w + 1] + S.smax[w]; }
+    S.Tlo = S.slo[0]; S.Thi = S.shi[0];
+    S.n_slices = S.Thi - S.Tlo + 1;
+    int64_t mr = 1;
+    for (int64_t T = S.Tlo; T <= S.Thi; T++)
+        for (int w = 1; w < W; w++) {
+            int64_t lo = std::max(S.slo[w], T - S.phi[w]), hi = std::min(S.shi[w], T - S.plo[w]);
+            mr = std::max<int64_t>(mr, hi - lo + 1);
+        }
+    S.maxrange = (int32_t)mr;
+    CK(salloc(s, &s.d_units, 1));
+    CK(salloc(s, &s.dense, dense.size()));
+    CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
+    CK(salloc(s, &s.J32, (size_t)S.n_slices));
+    CK(salloc(s, &s.Jex, (size_t)S.n_slices));
+    CK(salloc(s, &s.band, (size_t)S.n_slices));
+    CK(salloc(s, &s.nband, 1));
+    s.slots = 148 * 2;
+    CK(salloc(s, &s.scratch, (size_t)s.slots * (S.gtot + (size_t)W * S.maxrange)));
+    return cudaSuccess;
+}
+
+cudaError_t slice_pass1(SliceState& s, const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
+    (void)su; (void)tb;
+    const SliceDev& S = s.h;
+    int64_t mine = S.n_slices > S.shard ? (S.n_slices - S.shard + S.n_shards - 1) / S.n_shards : 0;
+    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * (size_t)S.maxrange);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    CK(cudaFuncSetAttribute((const void*)k_slice_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaMemsetAsync(s.d_units, 0, sizeof(unsigned long long), st));
+    if (mine > 0) k_slice_f32<<<(unsigned)mine, SL_THREADS, smem, st>>>(S, wk.probs, wk.levs, s.dense, s.J32, s.d_units);
+    k_slice_min<<<1, 1024, 0, st>>>(S, s.J32, wk.m32);
+    return cudaGetLastError();
+}
+
+cudaError_t slice_pass2_min(SliceState& s, const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
+    (void)su; (void)tb;
+    const SliceDev& S = s.h;
+    k_slice_band<<<1, 1024, 0, st>>>(S, s.J32, wk.m32, s.band, s.nband);
+    k_slice_exact<<<s.slots, SL_THREADS, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex);
+    k_slice_hstar<<<1, 32, 0, st>>>(s.band, s.nband, s.Jex, wk.hstar);
+    return cudaGetLastError();
+}
+
+cudaError_t slice_pass2_first(SliceState& s, const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
+    (void)su; (void)tb;
+    const SliceDev& S = s.h;
+    CK(cudaMemsetAsync(wk.first, 0xff, sizeof(uint64_t), st));
+    k_slice_walk<<<s.slots, SL_THREADS, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex,
+                                                 wk.hstar, (unsigned long long*)wk.first);
+    return cudaGetLastError();
+}
+
+cudaError_t slice_decode_winner(SliceState& s, const Setup& su, Work& wk, cudaStream_t st) {
+    (void)s; (void)su; (void)wk; (void)st;
+    return cudaSuccess;
+}
+
+}  // namespace eclip

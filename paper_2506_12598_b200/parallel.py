@@ -1,0 +1,87 @@
+"""Multi-GPU planning: shard the candidate space over ranks, one exchange per pass
+(DESIGN.md §5).
+
+One process per GPU.  Each rank runs a Session on its shard (ENUM: a contiguous range of
+pass-1 items of every problem; SLICE: the T' slices congruent to its rank) and the ranks
+combine three tiny per-problem values with torch.distributed (NCCL over NVLink on the B200
+box, gloo in the CPU tests):
+    pass 1    float32 minimum of the FP32 filter key        -> all-reduce MIN
+    pass 2a   exact 256-bit minimum key                     -> all-gather + lexicographic MIN
+    pass 2b   lowest candidate index within the tie band    -> all-reduce MIN
+after which every rank materialises the same plan.  Batches of independent mixes need no
+exchange at all: shard the mixes instead (weak scaling, bench.py).
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+U64_NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
+I64_MAX = np.iinfo(np.int64).max
+
+
+def lexmin_u256(stacked: np.ndarray) -> np.ndarray:
+    """stacked [ranks, n, 4] uint64 little-endian limbs -> [n, 4] lexicographic minimum"""
+    R, n, _ = stacked.shape
+    out = stacked[0].copy()
+    for r in range(1, R):
+        cand = stacked[r]
+        for i in range(n):
+            if tuple(cand[i, ::-1]) < tuple(out[i, ::-1]):
+                out[i] = cand[i]
+    return out
+
+
+class TorchComm:
+    """The three reductions over a torch.distributed process group."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        backend = dist.get_backend(group)
+        self.device = device if device is not None else ("cuda" if backend == "nccl" else "cpu")
+
+    def _t(self, a):
+        return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def min_f32(self, a: np.ndarray) -> np.ndarray:
+        t = self._t(a.astype(np.float32))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return t.cpu().numpy()
+
+    def min_u256(self, a: np.ndarray) -> np.ndarray:
+        t = self._t(a.view(np.int64))
+        world = self.dist.get_world_size(self.group)
+        outs = [self.torch.empty_like(t) for _ in range(world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        stacked = np.stack([o.cpu().numpy().view(np.uint64) for o in outs])
+        return lexmin_u256(stacked)
+
+    def min_u64(self, a: np.ndarray) -> np.ndarray:
+        v = np.where(a == U64_NONE, I64_MAX, a.astype(np.int64))
+        t = self._t(v)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        r = t.cpu().numpy()
+        return np.where(r == I64_MAX, U64_NONE, r.astype(np.uint64))
+
+
+def run_sharded(session, comm, gmax: int = 0):
+    """Drive one rank's session through the protocol; returns the (identical) plan."""
+    m = comm.min_f32(session.pass1())
+    k = comm.min_u256(session.pass2_min(m))
+    f = comm.min_u64(session.pass2_first(k))
+    return session.finish(f, gmax) if not getattr(session, "single", False) else session.finish(f)
+
+
+def plan_distributed(profiles, problem, group=None, **kw):
+    """eclip_plan of one problem sharded over every rank of `group` (torch.distributed)."""
+    import torch.distributed as dist
+    from .eclip import Session
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    s = Session(profiles, problem=problem, shard=rank, n_shards=world, **kw)
+    try:
+        return run_sharded(s, TorchComm(group))
+    finally:
+        s.close()

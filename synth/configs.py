@@ -211,3 +211,24 @@ def random_tiny_problem(seed: int, max_w: int = 3, max_g: int = 3, max_c: int = 
     return Problem(f"tiny{seed}", models, ids, N, R, mode, obj, allowed_mask=mask,
                    qos_ns=qos, slowdown_matrix=M, group_bounds=gb,
                    p_idle_w=float(rng.choice([75.0, 200.0])), p_max_w=float(rng.choice([225.0, 1000.0])))
+
+
+def c5_problem(i: int, models, ids, qos) -> Problem:
+    """Mix i of a C5 batch as a single Problem (for oracle checks of sampled mixes)."""
+    return Problem(f"C5[{i}]", models, [int(x) for x in ids[i]], 148, 14, "exclude_self", "sum",
+                   qos_ns=[float(x) for x in qos[i]], p_idle_w=200.0, p_max_w=1000.0)
+
+
+def problem_hash(p: Problem) -> str:
+    """Hash of a problem's seeded inputs (detects stale golden files)."""
+    import hashlib
+    import json
+    h = hashlib.sha256()
+    for m in p.models:
+        h.update(np.ascontiguousarray(m.exec_ns).tobytes())
+        h.update(str(m.sizes).encode())
+    h.update(json.dumps([list(map(int, p.model_ids)), p.total_sms, p.switch_max, p.mode, p.objective,
+                         p.allowed_mask, p.qos_ns, p.group_bounds, p.p_idle_w, p.p_max_w]).encode())
+    if p.slowdown_matrix is not None:
+        h.update(np.ascontiguousarray(p.slowdown_matrix, dtype=np.float32).tobytes())
+    return h.hexdigest()[:16]

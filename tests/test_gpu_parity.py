@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by element.
+
+Bar: allocation (group sizes, level ranks, candidate index, exact integer
+key) bit-exact; FP64 values within 1e-5 relative (they agree to ~1e-12 by construction).
+Small cases run the oracle live; BASELINE.json's full sizes compare with
+tests/golden/oracle_full.json, written by tools/gen_oracle_golden.py from oracle/ only.
+"""
+import copy
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+import paper_2506_12598_b200 as ec
+from paper_2506_12598_b200 import parallel
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+REL = 1e-5
+
+
+def _gold():
+    return json.load(open(os.path.join(HERE, "golden", "oracle_full.json")))["records"]
+
+
+def _same(g, o, label=""):
+    assert g.status == o.status, label
+    if o.status != "ok":
+        return
+    assert g.winner_levels == o.levels, label
+    assert g.group_sm == o.group_sm, label
+    assert g.winner_index == o.index, label
+    assert g.exact_key == o.key, label
+    assert g.model_switches == o.switches, label
+    assert g.objective == pytest.approx(o.objective, rel=REL), label
+    assert g.makespan_ns == pytest.approx(o.makespan_ns, rel=REL), label
+    assert g.energy_j == pytest.approx(o.energy_j, rel=REL), label
+    assert g.power_w == pytest.approx(o.power_w, rel=REL), label
+    assert g.throughput_rps == pytest.approx(o.throughput_rps, rel=REL), label
+    for a, b in zip(g.model_latency_ns, o.latency_ns):
+        assert a == pytest.approx(b, rel=REL), label
+    for ga, gb in zip(g.group_latency_ns, o.group_latency_ns):
+        for a, b in zip(ga, gb):
+            assert a == pytest.approx(b, rel=REL), label
+
+
+def _gpu(p, engine="auto", **kw):
+    return ec.plan_problem(ec.Profiles.from_models(p.models), p, engine=engine, **kw)
+
+
+# ---------------------------------------------------------------- worked examples
+def test_worked_examples_on_gpu():
+    from test_oracle import _golden_problem
+    gold = json.load(open(os.path.join(HERE, "golden", "appB_examples.json")))
+    for case in gold["cases"]:
+        p = _golden_problem(case, gold)
+        for engine in ("enum", "slice"):
+            g = _gpu(p, engine)
+            assert g.group_sm == case["expect_sizes"], (case["name"], engine)
+            assert g.objective == pytest.approx(case["expect_J"] * 1000, rel=1e-12)
+
+
+# ---------------------------------------------------------------- random tiny instances
+@pytest.mark.parametrize("chunk", range(4))
+def test_random_instances_vs_oracle(chunk):
+    for s in range(chunk * 100, chunk * 100 + 100):
+        p = synth.random_tiny_problem(s, max_w=4, max_g=4, max_c=4)
+        o = oracle.solve(p)
+        _same(_gpu(p, "enum"), o, f"enum seed {s}")
+        if p.mode != "matrix":
+            _same(_gpu(p, "slice"), o, f"slice seed {s}")
+
+
+def test_c1_sweep():
+    """C1: 2 x 3 groups x {15,30,45,60}; R in {0,1,2}; every mode x objective; QoS on/off."""
+    for R in (0, 1, 2):
+        for mode in ("exclude_self", "paper", "excess", "matrix"):
+            for obj in ("sum", "max", "energy"):
+                for qos in (False, True):
+                    p = synth.make_c1(R, mode, obj, qos)
+                    o = oracle.solve(p)
+                    _same(_gpu(p, "enum"), o, f"C1 {R} {mode} {obj} {qos}")
+                    if mode != "matrix":
+                        _same(_gpu(p, "slice"), o, f"C1 slice {R} {mode} {obj} {qos}")
+
+
+def test_c2_all_modes_objectives():
+    for mode in ("exclude_self", "paper", "excess", "matrix"):
+        for obj in ("sum", "max", "energy"):
+            p = synth.make_c2(mode, obj)
+            o = oracle.solve(p)
+            _same(_gpu(p, "enum"), o, f"C2 {mode} {obj}")
+            if mode != "matrix":
+                _same(_gpu(p, "slice"), o, f"C2 slice {mode} {obj}")
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_single_worker_and_tiny_levels():
+    p = synth.make_c1(R=0)
+    p.model_ids = [1]
+    _same(_gpu(p, "enum"), oracle.solve(p), "W=1")
+    _same(_gpu(p, "slice"), oracle.solve(p), "W=1 slice")
+    # fewer inner levels than a thread holds (L < KIN) and a 1-level worker
+    p = synth.make_c1(R=0)
+    p.allowed_mask = [0b0001, 0b0110]
+    _same(_gpu(p, "enum"), oracle.solve(p), "masks")
+
+
+def test_edge_all_infeasible_qos():
+    p = synth.make_c2()
+    p.qos_ns = [1.0, 1.0, 1.0]
+    assert oracle.solve(p).status == "infeasible"
+    for engine in ("enum", "slice"):
+        assert _gpu(p, engine).status == "infeasible"
+
+
+def test_edge_exact_ties_lowest_index():
+    """duplicated models (P:378 Mix 1 = 2x albert) create exact ties; lowest index wins."""
+    p = synth.make_c2()
+    p.model_ids = [0, 0, 1]
+    o = oracle.solve(p)
+    for engine in ("enum", "slice"):
+        _same(_gpu(p, engine), o, engine)
+    for tol in (0.0, 1e-3):
+        o = oracle.solve(p, tol=tol)
+        _same(_gpu(p, "enum", tie_tol=tol), o, f"tol {tol}")
+
+
+def test_edge_groups_and_large_levels():
+    """kernel groups (c3-K) and a worker with many levels (two C4 models, ENUM)"""
+    p = synth.make_c2()
+    p.group_bounds = [[0, 3, 8], None, [0, 1, 2, 4, 8]]
+    _same(_gpu(p, "enum"), oracle.solve(p), "groups")
+    _same(_gpu(p, "slice"), oracle.solve(p), "groups slice")
+    q = synth.make_c4()
+    q.model_ids = [0, 1]
+    q.qos_ns = q.qos_ns[:2]
+    o = oracle.solve(q, "slice")
+    _same(_gpu(q, "enum"), o, "C4x2 enum")
+    _same(_gpu(q, "slice"), o, "C4x2 slice")
+
+
+# ---------------------------------------------------------------- full sizes (golden)
+def _check_gold(g, rec, label):
+    assert rec["status"] == g.status, label
+    assert g.winner_levels == rec["levels"], label
+    assert g.group_sm == rec["group_sm"], label
+    assert g.winner_index == rec["index"], label
+    assert g.exact_key == int(rec["key"]), label
+    assert g.objective == pytest.approx(rec["objective"], rel=REL)
+    assert g.energy_j == pytest.approx(rec["energy_j"], rel=REL)
+    assert g.makespan_ns == pytest.approx(rec["makespan_ns"], rel=REL)
+
+
+def test_c3_full_matrix_vs_golden():
+    rec = _gold()["C3"]
+    p = synth.make_c3("matrix")
+    assert synth.problem_hash(p) == rec["hash"], "golden file is stale: rerun tools/gen_oracle_golden.py"
+    g = _gpu(p, "enum")
+    assert g.candidates == 113 ** 4 and g.units_scored == 113 ** 4
+    _check_gold(g, rec, "C3")
+
+
+def test_c3_excl_enum_equals_slice_equals_golden():
+    rec = _gold()["C3_excl"]
+    p = synth.make_c3("exclude_self")
+    assert synth.problem_hash(p) == rec["hash"]
+    a, b = _gpu(p, "enum"), _gpu(p, "slice")
+    _check_gold(a, rec, "C3 excl enum")
+    _check_gold(b, rec, "C3 excl slice")
+
+
+def test_c4_full_slice_vs_golden():
+    rec = _gold()["C4"]
+    p = synth.make_c4()
+    assert synth.problem_hash(p) == rec["hash"]
+    g = _gpu(p)  # AUTO must pick SLICE (1.2e22 tuples)
+    assert g.engine == "slice"
+    _check_gold(g, rec, "C4")
+
+
+def test_s6_full_vs_golden():
+    rec = _gold()["S6"]
+    p = synth.make_s6()
+    assert synth.problem_hash(p) == rec["hash"]
+    _check_gold(_gpu(p, "slice"), rec, "S6 slice")
+
+
+def test_c5_batch_full_sampled_vs_golden():
+    """the bench configuration: 4096 mixes in one launch sequence; sampled mixes vs oracle"""
+    models, ids, qos = synth.make_c5(4096)
+    pr = ec.Profiles.from_models(models)
+    out = ec.plan_batch(pr, ids, total_sms=148, switch_max=14, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+    gold = _gold()
+    for i in (0, 1, 2047, 4095):
+        rec = gold[f"C5_{i}"]
+        assert synth.problem_hash(synth.c5_problem(i, models, ids, qos)) == rec["hash"]
+        st = int(out["status"][i])
+        assert (st == 0) == (rec["status"] == "ok")
+        if st == 0:
+            assert out["winner_levels"][i].tolist() == rec["levels"]
+            assert int(out["winner_index"][i]) == rec["index"]
+            assert out["objective"][i] == pytest.approx(rec["objective"], rel=REL)
+            gsm = [out["group_sm"][i, w, :16].tolist() for w in range(4)]
+            assert gsm == rec["group_sm"]
+    # every mix: QoS met, budget met, sizes allowed
+    ok = out["status"] == 0
+    assert ok.sum() > 0
+    assert np.all(out["model_switches"][ok] <= 14)
+    assert np.all(out["model_latency_ns"][ok] <= qos[ok] * (1 + 1e-12))
+
+
+def test_c5_small_batch_each_mix_vs_oracle():
+    models, ids, qos = synth.make_c5(24, seed=3)
+    pr = ec.Profiles.from_models(models)
+    out = ec.plan_batch(pr, ids, total_sms=148, switch_max=14, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+    for i in range(24):
+        o = oracle.solve(synth.c5_problem(i, models, ids, qos), "slice")
+        assert (out["status"][i] == 0) == (o.status == "ok")
+        if o.status == "ok":
+            assert out["winner_levels"][i].tolist() == o.levels
+            assert int(out["winner_index"][i]) == o.index
+
+
+def test_batch_device_path_equals_host_path():
+    import torch
+    models, ids, qos = synth.make_c5(64, seed=7)
+    pr = ec.Profiles.from_models(models)
+    host = ec.plan_batch(pr, ids, total_sms=148, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0)
+    d_ids = torch.from_numpy(ids).cuda()
+    d_q = torch.from_numpy(qos).cuda()
+    dev = ec.plan_batch(pr, d_ids, total_sms=148, qos_ns=d_q, p_idle_w=200.0, p_max_w=1000.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev["winner_index"].cpu().numpy().view(np.uint64), host["winner_index"])
+    assert np.array_equal(dev["status"].cpu().numpy(), host["status"])
+    assert np.allclose(dev["objective"].cpu().numpy(), host["objective"], rtol=0, atol=0)
+
+
+# ---------------------------------------------------------------- sharding
+class _NumpyComm:
+    """combines the per-shard values in-process (the reductions of parallel.TorchComm)"""
+
+    def __init__(self, sessions):
+        self.s = sessions
+
+
+def _run_shards(make, n_shards):
+    ss = [make(k) for k in range(n_shards)]
+    m = np.minimum.reduce([s.pass1() for s in ss])
+    k = parallel.lexmin_u256(np.stack([s.pass2_min(m) for s in ss]))
+    f = np.minimum.reduce([s.pass2_first(k) for s in ss])
+    return [s.finish(f) for s in ss]
+
+
+@pytest.mark.parametrize("n_shards", [2, 3, 8])
+def test_sharded_single_problem_equals_unsharded(n_shards):
+    for p, eng in ((synth.make_c2(), "enum"), (synth.make_c2(), "slice"), (synth.make_c3("matrix"), "enum"),
+                   (synth.make_c4(), "slice")):
+        pr = ec.Profiles.from_models(p.models)
+        ref = ec.plan_problem(pr, p, engine=eng)
+        outs = _run_shards(lambda k: ec.Session(pr, problem=p, shard=k, n_shards=n_shards, engine=eng), n_shards)
+        for o in outs:
+            assert o.winner_index == ref.winner_index and o.group_sm == ref.group_sm and o.exact_key == ref.exact_key
+
+
+def test_sharded_batch_equals_unsharded():
+    models, ids, qos = synth.make_c5(16, seed=11)
+    pr = ec.Profiles.from_models(models)
+    ref = ec.plan_batch(pr, ids, total_sms=148, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0)
+    b = dict(model_ids=ids, qos_ns=qos, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
+    outs = _run_shards(lambda k: ec.Session(pr, batch=b, shard=k, n_shards=3), 3)
+    for o in outs:
+        assert np.array_equal(o["winner_index"], ref["winner_index"])
