@@ -120,8 +120,9 @@ typedef struct {
     double power_w;               /* p_idle + (p_max - p_idle) min(1, sum_w CUAverage_w / N) */
     double energy_j;              /* power x makespan */
     double throughput_rps;        /* sum_w 1e9 / L_w (each worker back to back) */
-    uint64_t winner_index;        /* mixed-radix index of the winning level tuple (worker 0 most significant) */
-    uint64_t candidates;          /* level tuples in the search space (prod_w L_w) */
+    uint64_t winner_index;        /* mixed-radix index of the winning level tuple (worker 0 most significant);
+                                     UINT64_MAX when prod_w L_w exceeds 2^64 (winner_levels is always exact) */
+    uint64_t candidates;          /* level tuples in the search space (prod_w L_w; UINT64_MAX if >= 2^64) */
     uint64_t units_scored;        /* ENUM: tuples scored; SLICE: lattice points evaluated */
     uint64_t exact_key[4];        /* the winner's exact integer key, little-endian limbs */
 } eclip_result;
@@ -183,7 +184,9 @@ int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* batch, const
  * opt->n_shards.  Between the steps the caller combines per-problem values across shards:
  *   pass1      -> float m[n]        : combine with MIN
  *   pass2_min  -> uint64 key[4n]    : combine with lexicographic MIN on (key[3],key[2],key[1],key[0])
- *   pass2_first-> uint64 index[n]   : combine with MIN (UINT64_MAX = none in this shard)
+ *   pass2_first-> uint64 tuple[4n]  : the lowest qualifying level tuple, packed as a 256-bit integer
+ *                                     sum_w l_w << 16(15-w) (little-endian limbs); combine with the same
+ *                                     lexicographic MIN as pass2_min (all-ones = none in this shard)
  * then finish() materialises the results (identical on every shard).  All buffers are host
  * memory.  eclip_plan / eclip_plan_batch are exactly session(shard 0 of 1) + these steps. */
 typedef struct eclip_session eclip_session;
@@ -191,8 +194,8 @@ int eclip_session_create(const eclip_profiles* prof, const eclip_batch* batch, c
                          eclip_session** out);
 int eclip_session_pass1(eclip_session* s, float* min_key32);
 int eclip_session_pass2_min(eclip_session* s, const float* global_min_key32, uint64_t* exact_min);
-int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_index);
-int eclip_session_finish(eclip_session* s, const uint64_t* global_first_index, eclip_batch_out* out);
+int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_tuple);
+int eclip_session_finish(eclip_session* s, const uint64_t* global_first_tuple, eclip_batch_out* out);
 void eclip_session_free(eclip_session* s);
 
 /* Single-problem sessions (the per-worker masks / groups of eclip_problem; used to shard
@@ -200,7 +203,7 @@ void eclip_session_free(eclip_session* s);
  * n = 1; finish_problem fills an eclip_result exactly like eclip_plan. */
 int eclip_session_create_problem(const eclip_profiles* prof, const eclip_problem* problem,
                                  const eclip_options* opt, eclip_session** out);
-int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_index, eclip_result* result);
+int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_tuple, eclip_result* result);
 
 #ifdef __cplusplus
 }

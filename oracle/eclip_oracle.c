@@ -641,9 +641,14 @@ int or_slice(const or_problem* p, or_result* r) {
             }
             if (less) { memcpy(best, cur, sizeof(int32_t) * W); haveb = 1; }
         }
-        uint64_t idx = 0;
-        for (int w = 0; w < W; w++) { idx = idx * (uint64_t)p->L[w] + (uint64_t)best[w]; r->levels[w] = best[w]; }
-        r->index = idx;
+        u128 idx = 0;
+        int fits = 1;
+        for (int w = 0; w < W; w++) {
+            idx = idx * (u128)p->L[w] + (u128)best[w];
+            if (idx >> 64) fits = 0;
+            r->levels[w] = best[w];
+        }
+        r->index = fits ? (uint64_t)idx : UINT64_MAX;   /* index needs more than 64 bits */
         u256 k;
         or_key(&c, best, &k);
         memcpy(r->key, k.w, sizeof k.w);

@@ -800,14 +800,14 @@ extern "C" int eclip_session_pass2_min(eclip_session* s, const float* global_min
     return ECLIP_OK;
 }
 
-extern "C" int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_index) {
+extern "C" int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_tuple) {
     if (!s) return fail(ECLIP_E_INVALID_ARG, "null session");
     if (global_exact_min)
         CU(cudaMemcpyAsync(s->wk.hstar, global_exact_min, 32 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
     int rc = step_pass2_first(s);
     if (rc) return rc;
-    if (first_index) {
-        CU(cudaMemcpyAsync(first_index, s->wk.first, 8 * (size_t)s->n, cudaMemcpyDeviceToHost, s->st));
+    if (first_tuple) {
+        CU(cudaMemcpyAsync(first_tuple, s->wk.first, 32 * (size_t)s->n, cudaMemcpyDeviceToHost, s->st));
         CU(cudaStreamSynchronize(s->st));
     }
     return ECLIP_OK;
@@ -871,10 +871,10 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     return ECLIP_OK;
 }
 
-extern "C" int eclip_session_finish(eclip_session* s, const uint64_t* global_first_index, eclip_batch_out* out) {
+extern "C" int eclip_session_finish(eclip_session* s, const uint64_t* global_first_tuple, eclip_batch_out* out) {
     if (!s || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
-    if (global_first_index)
-        CU(cudaMemcpyAsync(s->wk.first, global_first_index, 8 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
+    if (global_first_tuple)
+        CU(cudaMemcpyAsync(s->wk.first, global_first_tuple, 32 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
     return finish_batch(s, out);
 }
 
@@ -917,7 +917,7 @@ static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_ove
     o.status = st.data(); o.winner_levels = lv.data(); o.winner_index = idx.data(); o.objective = obj.data();
     o.makespan_ns = mk.data(); o.power_w = pw.data(); o.energy_j = en.data(); o.throughput_rps = thr.data();
     o.model_latency_ns = lat.data(); o.model_switches = sw.data(); o.group_sm = gsm.data(); o.group_stride = gmax;
-    if (first_override) CU(cudaMemcpyAsync(s->wk.first, first_override, 8, cudaMemcpyHostToDevice, s->st));
+    if (first_override) CU(cudaMemcpyAsync(s->wk.first, first_override, 32, cudaMemcpyHostToDevice, s->st));
     int rc = finish_batch(s, &o, glat.data(), key.data());
     if (rc) return rc;
     r->status = st[0] == 0 ? ECLIP_OK : ECLIP_INFEASIBLE;
@@ -925,8 +925,9 @@ static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_ove
     r->objective = obj[0]; r->makespan_ns = mk[0]; r->power_w = pw[0]; r->energy_j = en[0];
     r->throughput_rps = thr[0]; r->winner_index = idx[0];
     for (int i = 0; i < 4; i++) r->exact_key[i] = key[i];
-    uint64_t total = 1;
-    for (int w = 0; w < W; w++) total *= (uint64_t)std::max(1, s->tabL[s->h_table_of[w]]);
+    long double totl = 1;
+    for (int w = 0; w < W; w++) totl *= (long double)std::max(1, s->tabL[s->h_table_of[w]]);
+    uint64_t total = totl < 1.8e19L ? (uint64_t)totl : ~0ull;   // all-ones: more than 2^64 tuples
     r->candidates = total;
     r->units_scored = s->engine == ECLIP_ENGINE_ENUM ? total : slice_units(s->slice);
     size_t off = 0;

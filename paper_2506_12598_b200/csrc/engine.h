@@ -123,7 +123,7 @@ struct Work {
     float* m32;                 // [n] local (then global) minimum
     float* m32_sure;            // [n]
     U256* hstar;                // [n] exact minimum
-    uint64_t* first;            // [n] lowest index within tolerance
+    U256* first;                // [n] winner: lowest tuple within tolerance, packed (pack_tuple); all-ones = none
     uint64_t* scored;           // [n]
 };
 

@@ -181,12 +181,13 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
     P.lam = (int64_t)lam;
     P.lamN = (int64_t)(lam * (u64)su.N);
     if ((u128)P.lamN * (u128)(W + 1) >= ((u128)1 << 24)) P.status = P.status < 0 ? P.status : -5;
+    // index-space sizes, saturating (only the ENUM engine needs them; the host checks its limits)
     uint64_t Pn = 1, tot = 1;
+    const uint64_t SAT = (uint64_t)1 << 62;
     for (int w = 0; w < W; w++) {
-        u128 t2 = (u128)tot * (u128)(P.L[w] > 0 ? P.L[w] : 1);
-        if (t2 >= ((u128)1 << 62)) P.status = -5;
-        tot = (uint64_t)t2;
-        if (w < W - 1) Pn *= (uint64_t)(P.L[w] > 0 ? P.L[w] : 1);
+        uint64_t Lw = (uint64_t)(P.L[w] > 0 ? P.L[w] : 1);
+        tot = (tot >= SAT / Lw) ? SAT : tot * Lw;
+        if (w < W - 1) Pn = (Pn >= SAT / Lw) ? SAT : Pn * Lw;
     }
     P.P = Pn;
     P.total = tot;
@@ -791,7 +792,7 @@ __device__ float band_bound(const Setup& su, float m, float ms) {
 template <int PASS>
 __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
-                                               const float* m32_sure, U256* hstar, uint64_t* first) {
+                                               const float* m32_sure, U256* hstar, U256* first) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ U256 red[512];
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     if (isinf(m32[prob])) {  // nothing feasible anywhere (global minimum is +inf)
         if (threadIdx.x == 0) {
             if (PASS == 0) hstar[prob] = u256_max();
-            else first[prob] = ~0ull;
+            else first[prob] = u256_max();
         }
         return;
     }
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     uint64_t besti = ~0ull;
     U256 hs = (PASS == 1) ? hstar[prob] : u256_zero();
     if (PASS == 1 && u256_is_max(hs)) {  // no exactly-feasible candidate
-        if (threadIdx.x == 0) first[prob] = ~0ull;
+        if (threadIdx.x == 0) first[prob] = u256_max();
         return;
     }
     for (uint64_t it = slo; it < shi; it++) {
@@ -871,7 +872,18 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
             if (threadIdx.x < s && redi[threadIdx.x + s] < redi[threadIdx.x]) redi[threadIdx.x] = redi[threadIdx.x + s];
             __syncthreads();
         }
-        if (threadIdx.x == 0) first[prob] = redi[0];
+        if (threadIdx.x == 0) {
+            uint64_t idx = redi[0];
+            if (idx == ~0ull) first[prob] = u256_max();
+            else {
+                int lv[MAXW_ENUM];
+                for (int w = W - 1; w >= 0; w--) {
+                    lv[w] = (int)(idx % (uint64_t)P.L[w]);
+                    idx /= (uint64_t)P.L[w];
+                }
+                first[prob] = pack_tuple(lv, W);
+            }
+        }
     }
 }
 
@@ -898,13 +910,13 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
 // materialisation (a9): one thread per problem
 // ------------------------------------------------------------------------------------------
 __global__ void k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs, const U256* hstar,
-                              const uint64_t* first, const int32_t* sizes, int C, MatOut o) {
+                              const U256* first, const int32_t* sizes, int C, MatOut o) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= su.n_problems) return;
     const Prob& P = probs[p];
     const int W = su.W;
     int status = P.status;
-    if (status == 0 && (first[p] == ~0ull || u256_is_max(hstar[p]))) status = 1;  // infeasible
+    if (status == 0 && (u256_is_max(first[p]) || u256_is_max(hstar[p]))) status = 1;  // infeasible
     if (o.status) o.status[p] = status;
     if (status != 0) {
         if (o.index) o.index[p] = 0;
@@ -922,15 +934,19 @@ __global__ void k_materialize(Setup su, Tables tb, const Prob* probs, const Lev*
         }
         return;
     }
-    uint64_t idx = first[p];
-    int lv[MAXW_ENUM];
-    uint64_t q = idx;
-    for (int w = W - 1; w >= 0; w--) {
-        lv[w] = (int)(q % (uint64_t)P.L[w]);
-        q /= (uint64_t)P.L[w];
+    int lv[MAXW];
+    unpack_tuple(first[p], W, lv);
+    // mixed-radix candidate index (worker 0 most significant); all-ones if it needs > 64 bits
+    uint64_t idx = 0;
+    bool fits = true;
+    for (int w = 0; w < W; w++) {
+        u128 t = (u128)idx * (u128)P.L[w] + (u128)lv[w];
+        if (t >> 64) fits = false;
+        idx = (uint64_t)t;
     }
+    if (!fits) idx = ~0ull;
     // FP64 values from exact integers
-    double avg[MAXW_ENUM], Bw[MAXW_ENUM], sum_avg = 0.0;
+    double avg[MAXW], Bw[MAXW], sum_avg = 0.0;
     for (int w = 0; w < W; w++) {
         int t = P.table[w];
         avg[w] = (double)tb.S[t][lv[w]] / (double)tb.K[t];

@@ -62,6 +62,24 @@ EX_HD bool within_tol(const U256& key, const U256& m, uint64_t tol_num, uint64_t
     return u256_cmp(u256_mul64(key, tol_den), u256_mul64(m, tol_den + tol_num)) <= 0;
 }
 
+// Level tuple (l_0..l_{W-1}), W <= 16, packed with worker 0 most significant:
+// value = sum_w l_w << 16 (15 - w).  Numeric order == lexicographic (candidate index) order,
+// and it exists even when prod_w L_w overflows 64 bits (BASELINE config 4: 1.2e22 tuples).
+EX_HD U256 pack_tuple(const int* lv, int W) {
+    U256 r = u256_zero();
+    for (int w = 0; w < W; w++) {
+        int bit = 16 * (15 - w);
+        r.w[bit / 64] |= (uint64_t)(uint16_t)lv[w] << (bit % 64);
+    }
+    return r;
+}
+EX_HD void unpack_tuple(const U256& t, int W, int* lv) {
+    for (int w = 0; w < W; w++) {
+        int bit = 16 * (15 - w);
+        lv[w] = (int)((t.w[bit / 64] >> (bit % 64)) & 0xffffu);
+    }
+}
+
 EX_HD uint64_t gcd_u64(uint64_t a, uint64_t b) { while (b) { uint64_t t = a % b; a = b; b = t; } return a; }
 
 }  // namespace eclip

@@ -267,6 +267,15 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_exact(SliceDev S, const Pr
     }
 }
 
+// lexicographically smallest qualifying tuple over the band slices
+__global__ void k_slice_first(const int32_t* nband, const U256* wtup, U256* first) {
+    if (threadIdx.x != 0) return;
+    U256 m = u256_max();
+    for (int i = 0; i < *nband; i++)
+        if (u256_cmp(wtup[i], m) < 0) m = wtup[i];
+    first[0] = m;
+}
+
 __global__ void k_slice_hstar(const int32_t* band, const int32_t* nband, const U256* Jex, U256* hstar) {
     if (threadIdx.x != 0) return;
     U256 m = u256_max();
@@ -279,13 +288,18 @@ __global__ void k_slice_hstar(const int32_t* band, const int32_t* nband, const U
 __global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Prob* probs, const Lev* levs,
                                                            const int16_t* dense, const int32_t* band,
                                                            const int32_t* nband, uint64_t* scratch, const U256* Jex,
-                                                           const U256* hstar, unsigned long long* first) {
+                                                           const U256* hstar, U256* wtup) {
     const Prob& P = probs[0];
     __shared__ int64_t dlo[MAXW + 1], dhi[MAXW + 1];
     uint64_t* scr = scratch + (size_t)blockIdx.x * (S.gtot + (size_t)(S.W) * S.maxrange);
     const U256 hs = hstar[0];
-    if (u256_is_max(hs)) return;
+    if (u256_is_max(hs)) {
+        for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x)
+            if (threadIdx.x == 0) wtup[bi] = u256_max();
+        return;
+    }
     for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x) {
+        if (threadIdx.x == 0) wtup[bi] = u256_max();
         if (u256_is_max(Jex[band[bi]]) || !within_tol(Jex[band[bi]], hs, S.tol_num, S.tol_den)) continue;
         int64_t T = S.Tlo + band[bi];
         slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
@@ -322,11 +336,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Pro
                 }
                 ok = found;
             }
-            if (ok) {
-                uint64_t idx = 0;
-                for (int w = 0; w < W; w++) idx = idx * (uint64_t)P.L[w] + (uint64_t)lv[w];
-                atomicMin(first, (unsigned long long)idx);
-            }
+            if (ok) wtup[bi] = pack_tuple(lv, W);
         }
         __syncthreads();
     }
@@ -365,6 +375,7 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
         S.n_slices = 0; S.gtot = 1; S.maxrange = 1; S.gS = 1; S.Tlo = 0; S.Thi = -1;
         CK(salloc(s, &s.dense, 1)); CK(salloc(s, &s.J32, 1)); CK(salloc(s, &s.Jex, 1));
         CK(salloc(s, &s.band, 1)); CK(salloc(s, &s.nband, 1)); CK(salloc(s, &s.scratch, 1));
+        CK(salloc(s, &s.wtup, 1));
         CK(salloc(s, &s.d_units, 1));
         CK(cudaMemsetAsync(s.nband, 0, 4, st));
         s.slots = 1;
@@ -409,6 +420,7 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     CK(salloc(s, &s.J32, (size_t)S.n_slices));
     CK(salloc(s, &s.Jex, (size_t)S.n_slices));
     CK(salloc(s, &s.band, (size_t)S.n_slices));
+    CK(salloc(s, &s.wtup, (size_t)S.n_slices));
     CK(salloc(s, &s.nband, 1));
     s.slots = 148 * 2;
     CK(salloc(s, &s.scratch, (size_t)s.slots * (S.gtot + (size_t)W * S.maxrange)));
@@ -440,9 +452,9 @@ cudaError_t slice_pass2_min(SliceState& s, const Setup& su, const Tables& tb, Wo
 cudaError_t slice_pass2_first(SliceState& s, const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
     (void)su; (void)tb;
     const SliceDev& S = s.h;
-    CK(cudaMemsetAsync(wk.first, 0xff, sizeof(uint64_t), st));
     k_slice_walk<<<s.slots, SL_THREADS, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex,
-                                                 wk.hstar, (unsigned long long*)wk.first);
+                                                 wk.hstar, s.wtup);
+    k_slice_first<<<1, 32, 0, st>>>(s.nband, s.wtup, wk.first);
     return cudaGetLastError();
 }
 

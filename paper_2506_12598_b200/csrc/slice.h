@@ -37,6 +37,7 @@ struct SliceState {
     U256* Jex = nullptr;            // [n_slices]
     int32_t* band = nullptr;        // [n_slices] compacted slice list
     int32_t* nband = nullptr;       // [1]
+    U256* wtup = nullptr;           // [n_slices] per band slice: its lexmin qualifying tuple (packed)
     uint64_t* scratch = nullptr;    // exact DP tables, per CTA slot
     int32_t slots = 0;
     unsigned long long* d_units = nullptr;  // lattice points of pass 1 (this shard)

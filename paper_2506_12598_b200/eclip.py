@@ -405,8 +405,10 @@ class Session:
         return k
 
     def pass2_first(self, global_exact_min: np.ndarray) -> np.ndarray:
+        """-> [n, 4] uint64: the lowest qualifying level tuple of this shard, packed
+        (sum_w l_w << 16 (15 - w)); all-ones = none."""
         g = _np(global_exact_min, np.uint64)
-        f = np.zeros(self.n, np.uint64)
+        f = np.zeros((self.n, 4), np.uint64)
         _check(lib().eclip_session_pass2_first(self._h, _ptr(g, C.c_uint64), _ptr(f, C.c_uint64)))
         return f
 

@@ -7,7 +7,7 @@ combine three tiny per-problem values with torch.distributed (NCCL over NVLink o
 box, gloo in the CPU tests):
     pass 1    float32 minimum of the FP32 filter key        -> all-reduce MIN
     pass 2a   exact 256-bit minimum key                     -> all-gather + lexicographic MIN
-    pass 2b   lowest candidate index within the tie band    -> all-reduce MIN
+    pass 2b   lowest qualifying level tuple (packed 256-bit) -> all-gather + lexicographic MIN
 after which every rank materialises the same plan.  Batches of independent mixes need no
 exchange at all: shard the mixes instead (weak scaling, bench.py).
 """
@@ -71,7 +71,7 @@ def run_sharded(session, comm, gmax: int = 0):
     """Drive one rank's session through the protocol; returns the (identical) plan."""
     m = comm.min_f32(session.pass1())
     k = comm.min_u256(session.pass2_min(m))
-    f = comm.min_u64(session.pass2_first(k))
+    f = comm.min_u256(session.pass2_first(k))
     return session.finish(f, gmax) if not getattr(session, "single", False) else session.finish(f)
 
 
@@ -85,3 +85,16 @@ def plan_distributed(profiles, problem, group=None, **kw):
         return run_sharded(s, TorchComm(group))
     finally:
         s.close()
+
+
+def pack_tuple(levels) -> np.ndarray:
+    """level tuple -> [4] uint64 limbs of sum_w l_w << 16 (15 - w) (include/eclip.h)"""
+    v = 0
+    for w, l in enumerate(levels):
+        v |= int(l) << (16 * (15 - w))
+    return np.array([(v >> (64 * i)) & 0xFFFFFFFFFFFFFFFF for i in range(4)], np.uint64)
+
+
+def unpack_tuple(limbs, W: int):
+    v = sum(int(limbs[i]) << (64 * i) for i in range(4))
+    return [(v >> (16 * (15 - w))) & 0xFFFF for w in range(W)]

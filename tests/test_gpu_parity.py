@@ -251,7 +251,7 @@ def _run_shards(make, n_shards):
     ss = [make(k) for k in range(n_shards)]
     m = np.minimum.reduce([s.pass1() for s in ss])
     k = parallel.lexmin_u256(np.stack([s.pass2_min(m) for s in ss]))
-    f = np.minimum.reduce([s.pass2_first(k) for s in ss])
+    f = parallel.lexmin_u256(np.stack([s.pass2_first(k) for s in ss]))
     return [s.finish(f) for s in ss]
 
 
