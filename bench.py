@@ -215,9 +215,12 @@ def main():
 
     if rank == 0:
         f_max = 1965.0
-        issue_per_cand = 5.5            # packed f32x2 (2.5 slots) + 2 QoS compares + 1 min
-        cand_per_s_kernel = cand_step / (k_ms * 1e-3)
-        achieved = issue_per_cand * cand_per_s_kernel / 1e9
+        # the dominant kernel evaluates K = X_p + B_i Y_p + S'_i Z_p per candidate:
+        # 2 FP32 FMAs (FMA pipe, packed f32x2) + 1/2 three-input min (ALU pipe).  The FMA pipe
+        # (128 lane-ops / clk / SM, measured) bounds it: peak = 148 x 128 x 1965 MHz lane-ops/s.
+        fma_ops_per_cand = 2.0
+        cand_per_s_kernel = cand_step / (k_ms / k_launches * 1e-3)
+        achieved = fma_ops_per_cand * cand_per_s_kernel / 1e9
         peak = 148 * 128 * f_max * 1e6 / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -229,12 +232,13 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": float(e2e_t.item()) / a.steps},
             "gpu_launches": int(8 * a.steps),
-            "roofline": {"bound": "alu", "kernel": "k_pass1_sum<3,EXCL,QoS>", "achieved": achieved, "peak": peak,
-                         "unit": "G issue-slots/s (FP32 issue, 148 SM x 128 lanes x 1965 MHz)",
+            "roofline": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,QoS>", "achieved": achieved,
+                         "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": k_ms / k_launches,
                          "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
-                         "fp32_lane_ops_per_candidate": 8, "issue_slots_per_candidate": issue_per_cand},
+                         "fma_lane_ops_per_candidate": fma_ops_per_cand,
+                         "candidates_per_s_kernel": cand_per_s_kernel},
             "clocks": ck,
             "time_to_plan_ms": ttp,
         }

@@ -499,33 +499,30 @@ static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, i
     su.n_shards = opt ? std::max(1, opt->n_shards) : 1;
 }
 
-// choose the engine and size the work
+// choose the engine and size the work (pass-1 geometry: see enum.cu)
 static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     Setup& su = s->su;
-    int Lmax = 1, teams = 1;
+    int Lmax = 1, Lmin = 1 << 30;
     for (int L : s->tabL) {
         Lmax = std::max(Lmax, L);
-        int ts, tm;
-        pass1_geometry(std::max(L, 1), &ts, &tm);
-        teams = std::max(teams, tm);
+        Lmin = std::min(Lmin, std::max(L, 1));
     }
     su.Lmax = Lmax;
-    su.teams = teams;
+    const int W = su.W;
+    const long double n = su.n_problems;
+    long double H = 1;
+    for (int w = 0; w < W - 2; w++) H *= Lmax;
+    long double tuples = H * (W >= 2 ? Lmax : 1) * Lmax;
     int want = opt ? opt->engine : ECLIP_ENGINE_AUTO;
-    // ENUM limits
-    long double space = 1;
-    for (int w = 0; w < su.W - 1; w++) space *= Lmax;
-    long double items = std::ceil(space / (long double)pass1_pitem(Lmax));
-    bool enum_ok = su.W <= MAXW_ENUM && (size_t)su.W * Lmax * sizeof(Lev) <= 200 * 1024 && items < 2e9 &&
-                   space * Lmax < 4e18;
+    bool enum_ok = W <= MAXW_ENUM && (size_t)W * Lmax * sizeof(Lev) <= 100 * 1024 && tuples < 4e18L &&
+                   n * H * 4 < 6e9L;
     bool slice_ok = su.mode != M_MATRIX && s->n == 1;
     if (want == ECLIP_ENGINE_ENUM && !enum_ok)
-        return fail(ECLIP_E_TOO_LARGE, "ENUM engine limits exceeded (W=%d, Lmax=%d)", su.W, Lmax);
+        return fail(ECLIP_E_TOO_LARGE, "ENUM engine limits exceeded (W=%d, Lmax=%d)", W, Lmax);
     if (want == ECLIP_ENGINE_SLICE && !slice_ok)
         return fail(ECLIP_E_INVALID_ARG, "SLICE engine needs a linear slowdown mode and a single problem");
     if (want == ECLIP_ENGINE_AUTO) {
-        // ENUM scores every candidate; take SLICE when enumeration is far larger than the lattice
-        long double tuples = space * Lmax;
+        // ENUM scores every candidate; SLICE when enumeration is far larger than the lattice
         if (!enum_ok || (slice_ok && tuples > 4e10L)) {
             if (!slice_ok) return fail(ECLIP_E_TOO_LARGE, "search space too large for ENUM and SLICE does not apply");
             s->engine = ECLIP_ENGINE_SLICE;
@@ -535,7 +532,34 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     } else {
         s->engine = want;
     }
-    su.items_max = (int)std::max<long double>(1, items);
+    if (s->engine != ECLIP_ENGINE_ENUM) {
+        su.nseg = 1; su.upi = 1; su.units_max = 1; su.items_max = 1; su.table_bytes = 0;
+        return ECLIP_OK;
+    }
+    const int Lstep = W >= 2 ? Lmax : 1;
+    int nseg = 1;
+    if (n * H < 4096) nseg = (int)std::min<long double>(Lstep, std::ceil(4096.0L / (n * H)));
+    const int seglen = (Lstep + nseg - 1) / nseg;
+    nseg = (Lstep + seglen - 1) / seglen;
+    const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax);
+    const int teams_typ = fast ? P1_THREADS / pass1_fast_team(Lmax) : P1_THREADS / 32;
+    const long double units = H * nseg;
+    const long double cand_unit = (long double)seglen * Lmax;
+    long double target = n * units / 592.0L;                    // >= 2 CTAs per SM, 2 waves
+    long double upi = std::min<long double>(target, std::max<long double>(1, 4194304.0L / cand_unit));
+    upi = std::max<long double>(upi, teams_typ);
+    upi = std::ceil(upi / teams_typ) * teams_typ;
+    su.nseg = nseg;
+    su.upi = (int32_t)std::min<long double>(upi, 1 << 30);
+    su.units_max = (int64_t)units;
+    su.items_max = (int32_t)std::ceil(units / su.upi);
+    su.table_bytes = 0;
+    if (fast) {
+        const int teams_max = P1_THREADS / pass1_fast_team(std::min(Lmin, Lmax));
+        const size_t want_b = (size_t)teams_max * seglen * (su.has_qos ? 20 : 16);
+        su.table_bytes = (int32_t)std::min<size_t>(want_b, 100 * 1024);
+        if (su.table_bytes < seglen * 20) su.table_bytes = seglen * 20;
+    }
     return ECLIP_OK;
 }
 
@@ -546,7 +570,7 @@ static int alloc_work(eclip_session* s) {
     CU(s->arena.alloc(&wk.probs, n));
     CU(s->arena.alloc(&wk.levs, n * su.W * su.Lmax));
     if (s->engine == ECLIP_ENGINE_ENUM) {
-        size_t ns = n * (size_t)su.items_max * su.teams;
+        size_t ns = n * (size_t)su.units_max;
         CU(s->arena.alloc(&wk.submin, ns));
         if (su.mode == M_MATRIX && su.has_qos) CU(s->arena.alloc(&wk.submin_sure, ns));
     }

@@ -10,8 +10,9 @@ namespace eclip {
 
 constexpr int MAXW = 16;        // workers per problem (API limit)
 constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
-constexpr int P1_THREADS = 512; // pass-1 CTA size
-constexpr int KIN = 8;          // inner-worker levels held in registers per thread (pass 1)
+constexpr int P1_THREADS = 256; // pass-1 CTA size
+constexpr int KIN = 16;         // inner-worker levels held in registers per thread (fast pass 1)
+constexpr int TABLE_BYTES = 96 * 1024;  // per-CTA prefix tables of the fast pass-1 kernel
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
 enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };
@@ -68,8 +69,9 @@ struct Prob {
     int64_t lam, lamN;          // Lambda = lcm K_w, Lambda N
     uint64_t P;                 // prefix count prod_{w<W-1} L_w
     uint64_t total;             // prod_w L_w
-    uint64_t n_items;           // pass-1 items (prefix blocks of Pitem)
-    uint64_t Pitem;             // prefixes per item
+    uint64_t units;             // pass-1 units = rows x nseg (see enum.cu geometry)
+    uint64_t n_items;           // pass-1 CTA work items (upi units each)
+    int32_t Lstep, nseg, seglen, pad0;
     float inv;                  // (float)(1 / (Lambda N))
     float lamNf;                // (float)(Lambda N)
     float p_idle, p_dyn;        // power model floats (p_dyn = fl(p_max - p_idle))
@@ -88,8 +90,11 @@ struct Setup {
     int32_t n_problems, W, N, mode, obj, has_qos;
     int32_t Lmax;               // max levels over the tables
     int32_t items_max;          // max pass-1 items over problems
-    int32_t teams;              // teams per pass-1 CTA (sub-chunks per item)
-    int32_t team_size;          // threads per team
+    int32_t nseg;               // segments per row (units = rows x nseg)
+    int32_t upi;                // units per pass-1 item (CTA)
+    int64_t units_max;          // max units over problems (submin stride)
+    int32_t table_bytes;        // fast pass-1 per-CTA prefix-table budget
+    int32_t pad1;
     int32_t shard, n_shards;
     uint64_t tol_num, tol_den;
     double delta;               // FP32 filter relative error bound
@@ -118,8 +123,8 @@ struct PrepIn {
 struct Work {
     Prob* probs;                // [n]
     Lev* levs;                  // [n * W * Lmax]
-    float* submin;              // [n * items_max * teams]  pass-1 minima (maybe-feasible)
-    float* submin_sure;         // [n * items_max * teams]  MATRIX+QoS: surely-feasible minima
+    float* submin;              // [n * units_max]  pass-1 minima per unit (maybe-feasible)
+    float* submin_sure;         // [n * units_max]  MATRIX+QoS: surely-feasible minima
     float* m32;                 // [n] local (then global) minimum
     float* m32_sure;            // [n]
     U256* hstar;                // [n] exact minimum
@@ -142,8 +147,9 @@ struct MatOut {                 // materialisation outputs (device pointers, may
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C,
                                MatOut out, cudaStream_t st);
 
-// number of pass-1 items / teams for a problem shape (host helper, same formula as the kernels)
-void pass1_geometry(int L_inner, int* team_size, int* teams);
-uint64_t pass1_pitem(int L_inner);
+// pass-1 dynamic shared memory for a setup (host helper)
+size_t pass1_smem(const Setup& su, bool fast);
+bool pass1_fast(int L_inner);
+int pass1_fast_team(int L_inner);
 
 }  // namespace eclip

@@ -90,19 +90,26 @@ __device__ __forceinline__ void stage_levels(Lev* sl, const Lev* gl, unsigned by
     mbar_wait(bar, 0);
 }
 
-// pass-1 geometry (shared with pass 2 and the host)
-__host__ __device__ __forceinline__ int team_size_of(int L_in) { return (L_in + KIN - 1) / KIN; }
-__host__ __device__ __forceinline__ int teams_of(int L_in) {
-    int t = P1_THREADS / team_size_of(L_in);
-    return t < 1 ? 1 : t;
+// ------------------------------------------------------------------------------------------
+// pass-1 geometry (shared with pass 2 and the host).
+//   The last worker is "inner" (its levels are the per-thread register set), worker W-2 is the
+//   "step" worker (walked inside a unit), workers 0..W-3 are "hi" (fixed inside a unit).
+//   row  = one combination of hi digits; unit = (row, segment of the step worker's levels);
+//   submin[prob][unit] = FP32 minimum over the unit (the pass-2 granularity).
+// ------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
 }
-__host__ __device__ __forceinline__ uint64_t pitem_of(int L_in) {
-    // about 2^20 candidates per item (one CTA work unit)
-    uint64_t p = ((uint64_t)1 << 20) / (uint64_t)(L_in > 0 ? L_in : 1);
-    return p < 1 ? 1 : p;
+__host__ __device__ __forceinline__ int fast_team(int L_in) { return pow2ceil((L_in + KIN - 1) / KIN); }
+__host__ __device__ __forceinline__ bool fast_ok(int L_in) { return fast_team(L_in) <= 32; }
+__host__ __device__ __forceinline__ uint64_t rows_of(const int* L, int W) {
+    uint64_t h = 1;
+    for (int w = 0; w < W - 2; w++) h *= (uint64_t)L[w];
+    return h;
 }
-void pass1_geometry(int L_in, int* ts, int* teams) { *ts = team_size_of(L_in); *teams = teams_of(L_in); }
-uint64_t pass1_pitem(int L_in) { return pitem_of(L_in); }
+__host__ __device__ __forceinline__ int lstep_of(const int* L, int W) { return W >= 2 ? L[W - 2] : 1; }
 
 __host__ __device__ __forceinline__ void shard_items(uint64_t n_items, int shard, int n_shards, uint64_t* lo,
                                                      uint64_t* hi) {
@@ -110,20 +117,22 @@ __host__ __device__ __forceinline__ void shard_items(uint64_t n_items, int shard
     *hi = n_items * (uint64_t)(shard + 1) / (uint64_t)n_shards;
 }
 
-// sub-chunk (item, team) -> prefix range
-__device__ __forceinline__ void subchunk_range(const Prob& P, uint64_t item, int team, int teams, uint64_t* lo,
-                                               uint64_t* hi) {
-    uint64_t ilo = item * P.Pitem;
-    uint64_t ihi = ilo + P.Pitem;
-    if (ihi > P.P) ihi = P.P;
-    uint64_t cnt = ihi > ilo ? ihi - ilo : 0;
-    uint64_t span = (cnt + (uint64_t)teams - 1) / (uint64_t)teams;
-    uint64_t a = ilo + (uint64_t)team * span;
-    uint64_t b = a + span;
-    if (a > ihi) a = ihi;
-    if (b > ihi) b = ihi;
-    *lo = a;
-    *hi = b;
+// unit -> (row, step-digit range [e0, e1))
+__device__ __forceinline__ void unit_range(const Prob& P, uint64_t unit, uint64_t* row, int* e0, int* e1) {
+    *row = unit / (uint64_t)P.nseg;
+    int sg = (int)(unit % (uint64_t)P.nseg);
+    int a = sg * P.seglen, b = a + P.seglen;
+    if (b > P.Lstep) b = P.Lstep;
+    *e0 = a;
+    *e1 = b;
+}
+
+// row -> hi digits d[0..W-3] (worker 0 most significant)
+__device__ __forceinline__ void decode_row(uint64_t row, const int* L, int W, int* d) {
+    for (int w = W - 3; w >= 0; w--) {
+        d[w] = (int)(row % (uint64_t)L[w]);
+        row /= (uint64_t)L[w];
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -191,9 +200,19 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
     }
     P.P = Pn;
     P.total = tot;
-    int Lin = P.L[W - 1] > 0 ? P.L[W - 1] : 1;
-    P.Pitem = pitem_of(Lin);
-    P.n_items = (Pn + P.Pitem - 1) / P.Pitem;
+    {   // pass-1 units (see geometry above); rows saturate like the index space
+        uint64_t H = 1;
+        for (int w = 0; w < W - 2; w++) {
+            uint64_t Lw = (uint64_t)(P.L[w] > 0 ? P.L[w] : 1);
+            H = (H >= SAT / Lw) ? SAT : H * Lw;
+        }
+        P.Lstep = W >= 2 ? (P.L[W - 2] > 0 ? P.L[W - 2] : 1) : 1;
+        P.nseg = su.nseg < P.Lstep ? su.nseg : P.Lstep;
+        P.seglen = (P.Lstep + P.nseg - 1) / P.nseg;
+        P.nseg = (P.Lstep + P.seglen - 1) / P.seglen;
+        P.units = H * (uint64_t)P.nseg;
+        P.n_items = (P.units + (uint64_t)su.upi - 1) / (uint64_t)su.upi;
+    }
     P.inv = (float)(1.0 / (double)P.lamN);
     P.lamNf = (float)P.lamN;
     P.p_idle = in.p_idle;
@@ -280,238 +299,219 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
 // ------------------------------------------------------------------------------------------
 // pass 1
 // ------------------------------------------------------------------------------------------
-struct Prefix {
-    // exact sums over the "hi" prefix workers 0..NP-2
-    int64_t hB, hBS;
-    int32_t hT, hTm;
+__device__ __forceinline__ unsigned team_mask(int T) {
+    if (T >= 32) return 0xffffffffu;
+    unsigned base = ((threadIdx.x & 31u) / (unsigned)T) * (unsigned)T;
+    return ((1u << T) - 1u) << base;
+}
+__device__ __forceinline__ float team_min(float m, int T, unsigned mask) {
+    for (int o = T / 2; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(mask, m, o));
+    return m;
+}
+
+struct HiSums {
+    int64_t B, BS;
+    int32_t T, Tm;
 };
-
-template <int NP>
-__device__ __forceinline__ void hi_sums(const Lev* sl, int Lmax, const int* d, Prefix& h) {
-    h.hB = 0; h.hBS = 0; h.hT = 0; h.hTm = 1 << 24;
-#pragma unroll
-    for (int w = 0; w < NP - 1; w++) {
+// exact sums over the hi workers 0..W-3
+__device__ __forceinline__ HiSums hi_sums(const Lev* sl, int Lmax, const int* d, int W) {
+    HiSums h;
+    h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
+    for (int w = 0; w < W - 2; w++) {
         const Lev& r = sl[w * Lmax + d[w]];
-        h.hB += r.B; h.hBS += r.BS; h.hT += r.S; h.hTm = min(h.hTm, r.Tmax);
+        h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
     }
+    return h;
 }
 
-// decode prefix index p into digits d[0..NP-1] (worker 0 most significant)
-template <int NP>
-__device__ __forceinline__ void decode_prefix(uint64_t p, const int* L, int* d) {
-#pragma unroll
-    for (int w = NP - 1; w >= 0; w--) {
-        d[w] = (int)(p % (uint64_t)L[w]);
-        p /= (uint64_t)L[w];
-    }
-}
-
-// returns true if the odometer carried past the last prefix digit (hi part changed)
-template <int NP>
-__device__ __forceinline__ bool advance(int* d, const int* L) {
-    if (++d[NP - 1] < L[NP - 1]) return false;
-    d[NP - 1] = 0;
-#pragma unroll
-    for (int w = NP - 2; w >= 0; w--) {
-        if (++d[w] < L[w]) break;
-        d[w] = 0;
-    }
-    return true;
-}
-
-__device__ __forceinline__ void team_min_write(float m, float* sm, float* out_slot, int team, int lane, int T,
-                                               bool active) {
-    sm[threadIdx.x] = m;
-    __syncthreads();
-    if (active && lane == 0) {
-        float r = INFINITY;
-        for (int i = 0; i < T; i++) r = fminf(r, sm[threadIdx.x + i]);
-        *out_slot = r;
-    }
-    __syncthreads();
-}
-
-// SUM objective, linear slowdown modes: the aggregated packed-FP32 filter.
-template <int NP, int MODE, bool QOS>
-__global__ void __launch_bounds__(P1_THREADS, 1)
-k_pass1_sum(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint64_t bar;
-    __shared__ float red[P1_THREADS];
-    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
-
-    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
-    const int prob = blockIdx.x / ipS;
-    const int li = blockIdx.x % ipS;
-    const Prob& P = probs[prob];
-    if (P.status != 0) return;
+__device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, int li, uint64_t* item, bool* ok) {
     uint64_t slo, shi;
     shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
-    const uint64_t item = slo + (uint64_t)li;
-    if (item >= shi) return;
-
-    const int W = NP + 1;
-    stage_levels(sl, levs + (size_t)prob * su.W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
-
-    int L[NP + 1];
-#pragma unroll
-    for (int w = 0; w <= NP; w++) L[w] = P.L[w];
-    const int Lin = L[NP];
-    const int T = team_size_of(Lin), teams = teams_of(Lin);
-    const int team = threadIdx.x / T, lane = threadIdx.x % T;
-    const bool active = team < teams;
-
-    // inner-worker levels in registers (clamped duplicates beyond L_in leave the min unchanged)
-    u64 Bf2[KIN / 2], bsn2[KIN / 2], s2[KIN / 2];
-    float sfv[KIN], uv[KIN];
-    float smin_t = INFINITY, umax_t = -INFINITY;
-    const Lev* inner = sl + NP * su.Lmax;
-#pragma unroll
-    for (int q = 0; q < KIN / 2; q++) {
-        int i0 = min(lane * KIN + 2 * q, Lin - 1), i1 = min(lane * KIN + 2 * q + 1, Lin - 1);
-        const Lev& a = inner[i0];
-        const Lev& b = inner[i1];
-        Bf2[q] = f2pack(__ll2float_rn(a.B), __ll2float_rn(b.B));
-        bsn2[q] = f2pack(-__ll2float_rn(a.BS), -__ll2float_rn(b.BS));
-        float sa = (float)a.S, sb = (float)b.S;
-        s2[q] = f2pack(sa, sb);
-        sfv[2 * q] = sa; sfv[2 * q + 1] = sb;
-        uv[2 * q] = (float)(a.Tmax - a.S); uv[2 * q + 1] = (float)(b.Tmax - b.S);
-        smin_t = fminf(smin_t, fminf(sa, sb));
-        umax_t = fmaxf(umax_t, fmaxf(uv[2 * q], uv[2 * q + 1]));
-    }
-    const u64 INV2 = f2pack(P.inv, P.inv);
-    const u64 NLAMN2 = f2pack(-P.lamNf, -P.lamNf);
-
-    float m0 = INFINITY, m1 = INFINITY;
-    uint64_t lo = 0, hi = 0;
-    if (active) subchunk_range(P, item, team, teams, &lo, &hi);
-    uint64_t scored = 0;
-    if (active && lo < hi) {
-        int d[NP > 0 ? NP : 1];
-        Prefix h;
-        if (NP > 0) {
-            decode_prefix<NP>(lo, L, d);
-            hi_sums<NP>(sl, su.Lmax, d, h);
-        } else {
-            h.hB = 0; h.hBS = 0; h.hT = 0; h.hTm = 1 << 24;
-        }
-        for (uint64_t p = lo; p < hi; p++) {
-            int64_t pB = h.hB, pBS = h.hBS;
-            int32_t pT = h.hT, pTm = h.hTm;
-            if (NP > 0) {
-                const Lev& r = sl[(NP - 1) * su.Lmax + d[NP - 1]];
-                pB += r.B; pBS += r.BS; pT += r.S; pTm = min(pTm, r.Tmax);
-            }
-            const float Tpf = (float)pT;
-            const float c1 = (float)(pTm - pT);  // inner S' must be <= c1 (prefix workers' QoS)
-            bool any = true;
-            if (QOS) any = (c1 >= smin_t) && (Tpf <= umax_t);
-            if (any) {
-                const float Bpf = __ll2float_rn(pB);
-                const u64 PB = f2pack(Bpf, Bpf);
-                const u64 PT = f2pack(Tpf, Tpf);
-                u64 PBS = 0;
-                if (MODE == M_EXCL) { float b = -__ll2float_rn(pBS); PBS = f2pack(b, b); }
-#pragma unroll
-                for (int q = 0; q < KIN / 2; q++) {
-                    const u64 bsum = add2(PB, Bf2[q]);
-                    const u64 t = add2(PT, s2[q]);
-                    u64 num;
-                    if (MODE == M_EXCL) {
-                        num = fma2(t, bsum, add2(PBS, bsn2[q]));       // T' B - sum B S'
-                    } else if (MODE == M_PAPER) {
-                        num = mul2(t, bsum);                           // T' B
-                    } else {
-                        float e0, e1;
-                        f2unpack(add2(t, NLAMN2), e0, e1);
-                        num = mul2(f2pack(fmaxf(e0, 0.0f), fmaxf(e1, 0.0f)), bsum);  // max(0,T'-LN) B
-                    }
-                    const u64 key = fma2(num, INV2, bsum);
-                    float k0, k1;
-                    f2unpack(key, k0, k1);
-                    if (QOS) {
-                        if (sfv[2 * q] <= c1 && Tpf <= uv[2 * q]) m0 = fminf(m0, k0);
-                        if (sfv[2 * q + 1] <= c1 && Tpf <= uv[2 * q + 1]) m1 = fminf(m1, k1);
-                    } else {
-                        m0 = fminf(m0, k0);
-                        m1 = fminf(m1, k1);
-                    }
-                }
-            }
-            if (NP > 0) {
-                if (advance<NP>(d, L)) hi_sums<NP>(sl, su.Lmax, d, h);
-            }
-        }
-        scored = hi - lo;
-    }
-    (void)scored;
-    float* slot = submin + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
-    team_min_write(fminf(m0, m1), red, slot, team, lane, T, active);
+    *item = slo + (uint64_t)li;
+    *ok = *item < shi;
 }
 
-// Generic (unpacked) filter: MAX / ENERGY objectives, and MATRIX slowdown (any objective).
+// Fast filter: SUM objective with EXCLUDE_SELF or PAPER_AS_WRITTEN, L_inner <= 32 KIN.
+// With exact prefix sums (Bp, BSp, Tp) over workers 0..W-2 and the inner level (B_i, S'_i),
+// the SUM key  sum_w B_w (1 + O_w / (Lambda N))  is, exactly,
+//   EXCLUDE_SELF:  K = X_p + B_i Y_p + S'_i Z_p,         X_p = Bp + (Tp Bp - BSp) / (Lambda N)
+//   PAPER:         K = X_p + B_i Y_p + S'_i Z_p + D_i,   X_p = Bp (1 + Tp / (Lambda N))
+//   Y_p = 1 + Tp / (Lambda N),   Z_p = Bp / (Lambda N),   D_i = B_i S'_i / (Lambda N),
+// every term >= 0.  Per candidate: 2 FMAs (packed f32x2: one issue slot for two candidates)
+// + a 3-input min.  FP32 relative error <= 5u.  The per-prefix (X, Y, Z)
+// come from a per-team table built once per unit from exact integers.
+template <int MODE, bool QOS>
+__global__ void __launch_bounds__(P1_THREADS, 2)
+k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
+    const int prob = blockIdx.x / ipS;
+    const Prob& P = probs[prob];
+    if (P.status != 0) return;
+    uint64_t item;
+    bool ok;
+    item_of_block(su, P, blockIdx.x % ipS, &item, &ok);
+    if (!ok) return;
+    const int W = su.W, Lmax = su.Lmax;
+    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
+    stage_levels(sl, levs + (size_t)prob * W * Lmax, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
+
+    int L[MAXW_ENUM];
+    for (int w = 0; w < W; w++) L[w] = P.L[w];
+    const int Lin = L[W - 1];
+    const int T = fast_team(Lin);
+    const int seglen = P.seglen;
+    int teams = P1_THREADS / T;
+    const int ent = QOS ? 20 : 16;
+    const int cap = su.table_bytes / (seglen * ent);
+    if (teams > cap) teams = cap;
+    const int team = threadIdx.x / T, lane = threadIdx.x % T;
+    if (team >= teams) return;   // no block-wide barrier follows
+    const unsigned mask = team_mask(T);
+    float4* tab = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) + (size_t)team * seglen;
+    float* tabT = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) +
+                                           (size_t)teams * seglen) + (size_t)team * seglen;
+
+    // inner levels in registers (duplicates of the last level pad the tail: the minimum is unchanged)
+    u64 B2[KIN / 2], S2[KIN / 2], D2[KIN / 2];
+    float uu[KIN], ss[KIN];
+    float smin_t = INFINITY, smax_t = -INFINITY, umin_t = INFINITY, umax_t = -INFINITY;
+    const Lev* inner = sl + (W - 1) * Lmax;
+    const double invd = 1.0 / (double)P.lamN;
+#pragma unroll
+    for (int q = 0; q < KIN / 2; q++) {
+        const Lev& a = inner[min(lane * KIN + 2 * q, Lin - 1)];
+        const Lev& b = inner[min(lane * KIN + 2 * q + 1, Lin - 1)];
+        B2[q] = f2pack(__ll2float_rn(a.B), __ll2float_rn(b.B));
+        const float sa = (float)a.S, sb = (float)b.S;
+        S2[q] = f2pack(sa, sb);
+        if (MODE == M_PAPER)
+            D2[q] = f2pack((float)((double)a.BS * invd), (float)((double)b.BS * invd));
+        ss[2 * q] = sa; ss[2 * q + 1] = sb;
+        uu[2 * q] = (float)(a.Tmax - a.S); uu[2 * q + 1] = (float)(b.Tmax - b.S);
+    }
+#pragma unroll
+    for (int j = 0; j < KIN; j++) {
+        smin_t = fminf(smin_t, ss[j]); smax_t = fmaxf(smax_t, ss[j]);
+        umin_t = fminf(umin_t, uu[j]); umax_t = fmaxf(umax_t, uu[j]);
+    }
+
+    uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
+    if (u1 > P.units) u1 = P.units;
+    int d[MAXW_ENUM];
+    for (uint64_t unit = u0 + (uint64_t)team; unit < u1; unit += (uint64_t)teams) {
+        uint64_t row;
+        int e0, e1;
+        unit_range(P, unit, &row, &e0, &e1);
+        decode_row(row, L, W, d);
+        const HiSums h = hi_sums(sl, Lmax, d, W);
+        const int ne = e1 - e0;
+        // ---- this unit's prefix table (exact integers -> one rounding each)
+        for (int e = lane; e < ne; e += T) {
+            int64_t Bp = h.B, BSp = h.BS;
+            int32_t Tp = h.T, Tm = h.Tm;
+            if (W >= 2) {
+                const Lev& r = sl[(W - 2) * Lmax + e0 + e];
+                Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
+            }
+            const double Y = 1.0 + (double)Tp * invd;
+            const double Z = (double)Bp * invd;
+            double X;
+            if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
+            else X = (double)Bp * Y;
+            tab[e] = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
+            if (QOS) tabT[e] = (float)Tp;
+        }
+        __syncwarp(mask);
+        float m0 = INFINITY, m1 = INFINITY;
+        for (int e = 0; e < ne; e++) {
+            const float4 t4 = tab[e];
+            bool all = true;
+            float Tpf = 0.0f;
+            if (QOS) {
+                Tpf = tabT[e];
+                const float c1 = t4.w;
+                if (!(c1 >= smin_t && Tpf <= umax_t)) continue;   // nothing of mine is feasible here
+                all = (c1 >= smax_t) && (Tpf <= umin_t);
+            }
+            const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
+            if (all) {
+#pragma unroll
+                for (int q = 0; q < KIN / 2; q++) {
+                    u64 base = (MODE == M_PAPER) ? add2(X2, D2[q]) : X2;
+                    const u64 key = fma2(B2[q], Y2, fma2(S2[q], Z2, base));
+                    float k0, k1;
+                    f2unpack(key, k0, k1);
+                    if (q & 1) m1 = fminf(m1, fminf(k0, k1));
+                    else m0 = fminf(m0, fminf(k0, k1));
+                }
+            } else {
+                const float c1 = t4.w;
+#pragma unroll
+                for (int q = 0; q < KIN / 2; q++) {
+                    u64 base = (MODE == M_PAPER) ? add2(X2, D2[q]) : X2;
+                    const u64 key = fma2(B2[q], Y2, fma2(S2[q], Z2, base));
+                    float k0, k1;
+                    f2unpack(key, k0, k1);
+                    if (ss[2 * q] <= c1 && Tpf <= uu[2 * q]) m0 = fminf(m0, k0);
+                    if (ss[2 * q + 1] <= c1 && Tpf <= uu[2 * q + 1]) m1 = fminf(m1, k1);
+                }
+            }
+        }
+        const float m = team_min(fminf(m0, m1), T, mask);
+        if (lane == 0) submin[(size_t)prob * su.units_max + unit] = m;
+        __syncwarp(mask);   // the table is rewritten for the next unit
+    }
+}
+
+// Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
+// SUM with large inner-level counts.  One warp per unit; inner levels read from shared memory.
 template <int NP, int MODE, int OBJ, bool QOS>
 __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
             float* __restrict__ submin_sure) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
-    __shared__ float red[P1_THREADS];
-    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
-
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const int prob = blockIdx.x / ipS;
-    const int li = blockIdx.x % ipS;
     const Prob& P = probs[prob];
     if (P.status != 0) return;
-    uint64_t slo, shi;
-    shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
-    const uint64_t item = slo + (uint64_t)li;
-    if (item >= shi) return;
-
+    uint64_t item;
+    bool ok;
+    item_of_block(su, P, blockIdx.x % ipS, &item, &ok);
+    if (!ok) return;
     constexpr int W = NP + 1;
-    stage_levels(sl, levs + (size_t)prob * su.W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
-
+    const int Lmax = su.Lmax;
+    Lev* sl = reinterpret_cast<Lev*>(smem_raw);
+    stage_levels(sl, levs + (size_t)prob * W * Lmax, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
     int L[W];
 #pragma unroll
     for (int w = 0; w < W; w++) L[w] = P.L[w];
     const int Lin = L[NP];
-    const int T = team_size_of(Lin), teams = teams_of(Lin);
-    const int team = threadIdx.x / T, lane = threadIdx.x % T;
-    const bool active = team < teams;
-
-    float iBf[KIN], iBk[KIN], isf[KIN], iu[KIN];
-    const Lev* inner = sl + NP * su.Lmax;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = P1_THREADS / 32;
+    float Mcol[W];
 #pragma unroll
-    for (int j = 0; j < KIN; j++) {
-        const Lev& a = inner[min(lane * KIN + j, Lin - 1)];
-        iBf[j] = __ll2float_rn(a.B);
-        iBk[j] = a.Bk;
-        isf[j] = (float)a.S;
-        iu[j] = (float)(a.Tmax - a.S);
-    }
-    float Mcol[W], Mrow_in[W];  // M[w][inner], M[inner][w]
-#pragma unroll
-    for (int w = 0; w < W; w++) {
-        Mcol[w] = P.Mf[w * MAXW_ENUM + NP];
-        Mrow_in[w] = P.Mf[NP * MAXW_ENUM + w];
-    }
+    for (int w = 0; w < W; w++) Mcol[w] = P.Mf[w * MAXW_ENUM + NP];
+    const Lev* inner = sl + NP * Lmax;
 
-    float m = INFINITY, ms = INFINITY;
-    uint64_t lo = 0, hi = 0;
-    if (active) subchunk_range(P, item, team, teams, &lo, &hi);
-    if (active && lo < hi) {
-        int d[NP > 0 ? NP : 1];
-        if (NP > 0) decode_prefix<NP>(lo, L, d);
-        for (uint64_t p = lo; p < hi; p++) {
-            // prefix workers' values
+    uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
+    if (u1 > P.units) u1 = P.units;
+    int d[W];
+    for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)nwarps) {
+        uint64_t row;
+        int e0, e1;
+        unit_range(P, unit, &row, &e0, &e1);
+        decode_row(row, L, W, d);
+        float m = INFINITY, ms = INFINITY;
+        for (int e = e0; e < e1; e++) {
+            if (NP >= 1) d[NP - 1] = e;
             float pBf[W], pBk[W], psf[W];
             int64_t pB = 0;
             int32_t pT = 0, pTm = 1 << 24;
 #pragma unroll
             for (int w = 0; w < NP; w++) {
-                const Lev& r = sl[w * su.Lmax + d[w]];
+                const Lev& r = sl[w * Lmax + d[w]];
                 pBf[w] = __ll2float_rn(r.B);
                 pBk[w] = r.Bk;
                 psf[w] = (float)r.S;
@@ -519,7 +519,6 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
             }
             const float Tpf = (float)pT;
             const float c1 = (float)(pTm - pT);
-            // MATRIX: prefix part of every overlap (chain over prefix workers)
             float Opre[W];
             if (MODE == M_MATRIX) {
 #pragma unroll
@@ -532,26 +531,27 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
                 }
             }
             const float Bpf = __ll2float_rn(pB);
-#pragma unroll
-            for (int j = 0; j < KIN; j++) {
-                const float Tf = Tpf + isf[j];
+            for (int j = lane; j < Lin; j += 32) {
+                const Lev& a = inner[j];
+                const float iBf = __ll2float_rn(a.B), iBk = a.Bk, isf = (float)a.S;
+                const float Tf = Tpf + isf;
                 float Lw[W];
                 float num = 0.0f;
 #pragma unroll
                 for (int w = 0; w < W; w++) {
-                    const float bf = (w == NP) ? iBf[j] : pBf[w];
-                    const float bk = (w == NP) ? iBk[j] : pBk[w];
+                    const float bf = (w == NP) ? iBf : pBf[w];
+                    const float bk = (w == NP) ? iBk : pBk[w];
                     float O;
                     if (MODE == M_EXCL) O = (w == NP) ? Tpf : (Tf - psf[w]);
                     else if (MODE == M_PAPER) O = Tf;
                     else if (MODE == M_EXCESS) O = fmaxf(Tf - P.lamNf, 0.0f);
-                    else O = (w == NP) ? Opre[w] : fmaf(Mcol[w], isf[j], Opre[w]);
+                    else O = (w == NP) ? Opre[w] : fmaf(Mcol[w], isf, Opre[w]);
                     Lw[w] = fmaf(O, bk, bf);
                     if (OBJ == O_SUM) num = fmaf(bf, O, num);
                 }
                 float key;
                 if (OBJ == O_SUM) {
-                    key = fmaf(num, P.inv, Bpf + iBf[j]);
+                    key = fmaf(num, P.inv, Bpf + iBf);
                 } else {
                     float mx = Lw[0];
 #pragma unroll
@@ -570,36 +570,28 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
                         if (maybe) m = fminf(m, key);
                         if (sure) ms = fminf(ms, key);
                     } else {
-                        if (isf[j] <= c1 && Tpf <= iu[j]) m = fminf(m, key);
+                        if (isf <= c1 && Tpf <= (float)(a.Tmax - a.S)) m = fminf(m, key);
                     }
                 } else {
                     m = fminf(m, key);
                 }
             }
-            if (NP > 0) (void)advance<NP>(d, L);
         }
-    }
-    (void)Mrow_in;
-    float* slot = submin + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
-    team_min_write(m, red, slot, team, lane, T, active);
-    if (MODE == M_MATRIX && QOS) {
-        float* slot2 = submin_sure + ((size_t)prob * su.items_max + item) * su.teams + (active ? team : 0);
-        team_min_write(ms, red, slot2, team, lane, T, active);
+        m = team_min(m, 32, 0xffffffffu);
+        if (MODE == M_MATRIX && QOS) ms = team_min(ms, 32, 0xffffffffu);
+        if (lane == 0) {
+            submin[(size_t)prob * su.units_max + unit] = m;
+            if (MODE == M_MATRIX && QOS) submin_sure[(size_t)prob * su.units_max + unit] = ms;
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
 // pass-1 dispatch
 // ------------------------------------------------------------------------------------------
-typedef void (*P1Sum)(Setup, const Prob*, const Lev*, float*);
+typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*);
 typedef void (*P1Gen)(Setup, const Prob*, const Lev*, float*, float*);
 
-template <int NP>
-static P1Sum pick_sum(int mode, bool qos) {
-    if (mode == M_EXCL) return qos ? k_pass1_sum<NP, M_EXCL, true> : k_pass1_sum<NP, M_EXCL, false>;
-    if (mode == M_PAPER) return qos ? k_pass1_sum<NP, M_PAPER, true> : k_pass1_sum<NP, M_PAPER, false>;
-    return qos ? k_pass1_sum<NP, M_EXCESS, true> : k_pass1_sum<NP, M_EXCESS, false>;
-}
 template <int NP, int MODE>
 static P1Gen pick_gen_m(int obj, bool qos) {
     if (obj == O_SUM) return qos ? k_pass1_gen<NP, MODE, O_SUM, true> : k_pass1_gen<NP, MODE, O_SUM, false>;
@@ -614,26 +606,31 @@ static P1Gen pick_gen(int mode, int obj, bool qos) {
     return pick_gen_m<NP, M_MATRIX>(obj, qos);
 }
 
+bool pass1_fast(int L_inner) { return fast_ok(L_inner); }
+int pass1_fast_team(int L_inner) { return fast_team(L_inner); }
+
+// the fast kernel applies when every problem's inner worker fits a warp team
+static bool use_fast(const Setup& su) {
+    return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax);
+}
+
+size_t pass1_smem(const Setup& su, bool fast) {
+    size_t s = (size_t)su.W * su.Lmax * sizeof(Lev);
+    if (fast) s += (size_t)su.table_bytes;
+    return s;
+}
+
 cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
     const int NP = su.W - 1;
     const bool qos = su.has_qos != 0;
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const size_t grid = (size_t)su.n_problems * ipS;
-    const size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
     if (grid == 0) return cudaSuccess;
-    if (su.obj == O_SUM && su.mode != M_MATRIX) {
-        P1Sum f = nullptr;
-        switch (NP) {
-            case 0: f = pick_sum<0>(su.mode, qos); break;
-            case 1: f = pick_sum<1>(su.mode, qos); break;
-            case 2: f = pick_sum<2>(su.mode, qos); break;
-            case 3: f = pick_sum<3>(su.mode, qos); break;
-            case 4: f = pick_sum<4>(su.mode, qos); break;
-            case 5: f = pick_sum<5>(su.mode, qos); break;
-            case 6: f = pick_sum<6>(su.mode, qos); break;
-            case 7: f = pick_sum<7>(su.mode, qos); break;
-            default: return cudaErrorInvalidValue;
-        }
+    const bool fast = use_fast(su);
+    const size_t smem = pass1_smem(su, fast);
+    if (fast) {
+        P1Fast f = su.mode == M_EXCL ? (qos ? k_pass1_fast<M_EXCL, true> : k_pass1_fast<M_EXCL, false>)
+                                     : (qos ? k_pass1_fast<M_PAPER, true> : k_pass1_fast<M_PAPER, false>);
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin);
@@ -658,7 +655,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
-// local minimum per problem over this shard's sub-chunks (one warp per problem)
+// local minimum per problem over this shard's units (one warp per problem)
 // ------------------------------------------------------------------------------------------
 __global__ void k_reduce_min(Setup su, const Prob* probs, const float* submin, const float* submin_sure, float* m32,
                              float* m32_sure) {
@@ -670,13 +667,12 @@ __global__ void k_reduce_min(Setup su, const Prob* probs, const float* submin, c
     if (P.status == 0) {
         uint64_t slo, shi;
         shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
-        const int teams = teams_of(P.L[su.W - 1]);
-        for (uint64_t it = slo; it < shi; it++) {
-            for (int t = lane; t < teams; t += 32) {
-                size_t s = ((size_t)p * su.items_max + it) * su.teams + t;
-                m = fminf(m, submin[s]);
-                if (submin_sure) ms = fminf(ms, submin_sure[s]);
-            }
+        uint64_t a = slo * (uint64_t)su.upi, b = shi * (uint64_t)su.upi;
+        if (b > P.units) b = P.units;
+        for (uint64_t u = a + lane; u < b; u += 32) {
+            size_t s = (size_t)p * su.units_max + u;
+            m = fminf(m, submin[s]);
+            if (submin_sure) ms = fminf(ms, submin_sure[s]);
         }
     }
     for (int o = 16; o; o >>= 1) {
@@ -812,9 +808,10 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     stage_levels(sl, levs + (size_t)prob * W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
     const float bound = band_bound(su, m32[prob], m32_sure ? m32_sure[prob] : m32[prob]);
     const int Lin = P.L[W - 1];
-    const int teams = teams_of(Lin);
     uint64_t slo, shi;
     shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
+    uint64_t ua = slo * (uint64_t)su.upi, ub = shi * (uint64_t)su.upi;
+    if (ub > P.units) ub = P.units;
     U256 best = u256_max();
     uint64_t besti = ~0ull;
     U256 hs = (PASS == 1) ? hstar[prob] : u256_zero();
@@ -822,40 +819,62 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
         if (threadIdx.x == 0) first[prob] = u256_max();
         return;
     }
-    for (uint64_t it = slo; it < shi; it++) {
-        for (int t = 0; t < teams; t++) {
-            if (!(submin[((size_t)prob * su.items_max + it) * su.teams + t] <= bound)) continue;
-            uint64_t lo, hi;
-            subchunk_range(P, it, t, teams, &lo, &hi);
-            uint64_t ncand = (hi - lo) * (uint64_t)Lin;
+    int L[MAXW_ENUM];
+    for (int w = 0; w < W; w++) L[w] = P.L[w];
+    __shared__ uint32_t list[512];
+    __shared__ int nlist;
+    bool done = false;
+    for (uint64_t blk = ua; blk < ub && !done; blk += blockDim.x) {
+        // compact the band units of this block of 512 (kept in candidate-index order)
+        const uint64_t u = blk + threadIdx.x;
+        const bool in_band = u < ub && submin[(size_t)prob * su.units_max + u] <= bound;
+        if (threadIdx.x == 0) nlist = 0;
+        __syncthreads();
+        const unsigned bal = __ballot_sync(0xffffffffu, in_band);
+        __shared__ int wcount[16], woff[16];
+        if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) { woff[w] = acc; acc += wcount[w]; }
+            nlist = acc;
+        }
+        __syncthreads();
+        if (in_band) list[woff[threadIdx.x >> 5] + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)(u - blk);
+        __syncthreads();
+        const int nl = nlist;
+        for (int li = 0; li < nl; li++) {
+            const uint64_t unit = blk + list[li];
+            uint64_t row;
+            int e0, e1;
+            unit_range(P, unit, &row, &e0, &e1);
+            int lv[MAXW_ENUM];
+            decode_row(row, L, W, lv);
+            const uint64_t ncand = (uint64_t)(e1 - e0) * (uint64_t)Lin;
             for (uint64_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-                uint64_t pre = lo + c / (uint64_t)Lin;
-                int lv[MAXW_ENUM];
-                lv[W - 1] = (int)(c % (uint64_t)Lin);
-                uint64_t q = pre;
-                for (int w = W - 2; w >= 0; w--) {
-                    lv[w] = (int)(q % (uint64_t)P.L[w]);
-                    q /= (uint64_t)P.L[w];
-                }
+                int lvc[MAXW_ENUM];
+                for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
+                if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint64_t)Lin);
+                lvc[W - 1] = (int)(c % (uint64_t)Lin);
                 float k32;
-                if (!key32_scalar(su, P, sl, lv, k32)) continue;
+                if (!key32_scalar(su, P, sl, lvc, k32)) continue;
                 if (!(k32 <= bound)) continue;
                 U256 k;
-                if (!exact_key(su, P, sl, lv, k)) continue;
+                if (!exact_key(su, P, sl, lvc, k)) continue;
                 if (PASS == 0) {
                     if (u256_cmp(k, best) < 0) best = k;
-                } else {
-                    if (within_tol(k, hs, su.tol_num, su.tol_den)) {
-                        uint64_t idx = pre * (uint64_t)Lin + (uint64_t)lv[W - 1];
-                        if (idx < besti) besti = idx;
-                    }
+                } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
+                    uint64_t idx = 0;   // index within the problem (fits: ENUM limits)
+                    for (int w = 0; w < W; w++) idx = idx * (uint64_t)L[w] + (uint64_t)lvc[w];
+                    if (idx < besti) besti = idx;
                 }
             }
+            if (PASS == 1 && __syncthreads_or(besti != ~0ull)) {   // first unit with a hit holds the winner
+                done = true;
+                break;
+            }
         }
-        if (PASS == 1) {
-            // items are in index order: stop at the first item holding a hit
-            if (__syncthreads_or(besti != ~0ull)) break;
-        }
+        __syncthreads();
     }
     if (PASS == 0) {
         red[threadIdx.x] = best;
