@@ -391,6 +391,13 @@ static int setup_device(eclip_session* s, const eclip_options* opt) {
                     e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
     if (s->device < 0 || s->device >= ndev) return fail(ECLIP_E_INVALID_ARG, "device %d out of range", s->device);
     CU(cudaSetDevice(s->device));
+    {   // keep freed workspace in the device's stream-ordered pool between calls (no re-mapping)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, s->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     if (opt && opt->cuda_stream) {
         s->st = (cudaStream_t)opt->cuda_stream;
     } else {
@@ -514,7 +521,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     for (int w = 0; w < W - 2; w++) H *= Lmax;
     long double tuples = H * (W >= 2 ? Lmax : 1) * Lmax;
     int want = opt ? opt->engine : ECLIP_ENGINE_AUTO;
-    bool enum_ok = W <= MAXW_ENUM && (size_t)W * Lmax * sizeof(Lev) <= 100 * 1024 && tuples < 4e18L &&
+    bool enum_ok = W <= MAXW_ENUM && (size_t)W * Lmax * sizeof(Lev) <= 100 * 1024 && tuples < 4e18L && Lmax <= 4096 &&
                    n * H * 4 < 6e9L;
     bool slice_ok = su.mode != M_MATRIX && s->n == 1;
     if (want == ECLIP_ENGINE_ENUM && !enum_ok)
@@ -542,7 +549,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     const int seglen = (Lstep + nseg - 1) / nseg;
     nseg = (Lstep + seglen - 1) / seglen;
     const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax);
-    const int teams_typ = fast ? P1_THREADS / pass1_fast_team(Lmax) : P1_THREADS / 32;
+    const int teams_typ = P1_THREADS / 32;   // one unit per warp in both pass-1 kernels
     const long double units = H * nseg;
     const long double cand_unit = (long double)seglen * Lmax;
     long double target = n * units / 592.0L;                    // >= 2 CTAs per SM, 2 waves
@@ -554,12 +561,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.units_max = (int64_t)units;
     su.items_max = (int32_t)std::ceil(units / su.upi);
     su.table_bytes = 0;
-    if (fast) {
-        const int teams_max = P1_THREADS / pass1_fast_team(std::min(Lmin, Lmax));
-        const size_t want_b = (size_t)teams_max * seglen * (su.has_qos ? 20 : 16);
-        su.table_bytes = (int32_t)std::min<size_t>(want_b, 100 * 1024);
-        if (su.table_bytes < seglen * 20) su.table_bytes = seglen * 20;
-    }
+    if (fast) su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * seglen * 20);   // per-warp tables
     return ECLIP_OK;
 }
 

@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
+    __shared__ uint16_t perm[4096];   // inner levels sorted by S' (pass 1 is order-free)
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const int prob = blockIdx.x / ipS;
     const Prob& P = probs[prob];
@@ -360,78 +361,103 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     int L[MAXW_ENUM];
     for (int w = 0; w < W; w++) L[w] = P.L[w];
     const int Lin = L[W - 1];
-    const int T = fast_team(Lin);
-    const int seglen = P.seglen;
-    int teams = P1_THREADS / T;
-    const int ent = QOS ? 20 : 16;
-    const int cap = su.table_bytes / (seglen * ent);
-    if (teams > cap) teams = cap;
-    const int team = threadIdx.x / T, lane = threadIdx.x % T;
-    if (team >= teams) return;   // no block-wide barrier follows
-    const unsigned mask = team_mask(T);
-    float4* tab = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) + (size_t)team * seglen;
-    float* tabT = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) +
-                                           (size_t)teams * seglen) + (size_t)team * seglen;
+    const Lev* inner = sl + (W - 1) * Lmax;
+    // rank every inner level by S' (distinct per level) -> perm
+    for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
+        const int si = inner[i].S;
+        int rk = 0;
+        for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
+        perm[rk] = (uint16_t)i;
+    }
+    __syncthreads();
 
-    // inner levels in registers (duplicates of the last level pad the tail: the minimum is unchanged)
+    // a warp works on one unit; its G = 32 / T teams interleave over the unit's steps
+    const int T = fast_team(Lin), G = 32 / T;
+    const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+    const int team = wl / T, lane = wl % T;
+    const unsigned tmask = team_mask(T);
+    const int seglen = P.seglen;
+    float4* tab = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) + (size_t)warp * seglen;
+    float* tabT = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) +
+                                           (size_t)(P1_THREADS / 32) * seglen) + (size_t)warp * seglen;
+
+    // inner levels in registers, S'-sorted blocks of KIN per lane (tail padded with the last one)
     u64 B2[KIN / 2], S2[KIN / 2], D2[KIN / 2];
     float uu[KIN], ss[KIN];
-    float smin_t = INFINITY, smax_t = -INFINITY, umin_t = INFINITY, umax_t = -INFINITY;
-    const Lev* inner = sl + (W - 1) * Lmax;
     const double invd = 1.0 / (double)P.lamN;
 #pragma unroll
     for (int q = 0; q < KIN / 2; q++) {
-        const Lev& a = inner[min(lane * KIN + 2 * q, Lin - 1)];
-        const Lev& b = inner[min(lane * KIN + 2 * q + 1, Lin - 1)];
+        const Lev& a = inner[perm[min(lane * KIN + 2 * q, Lin - 1)]];
+        const Lev& b = inner[perm[min(lane * KIN + 2 * q + 1, Lin - 1)]];
         B2[q] = f2pack(__ll2float_rn(a.B), __ll2float_rn(b.B));
         const float sa = (float)a.S, sb = (float)b.S;
         S2[q] = f2pack(sa, sb);
-        if (MODE == M_PAPER)
-            D2[q] = f2pack((float)((double)a.BS * invd), (float)((double)b.BS * invd));
+        if (MODE == M_PAPER) D2[q] = f2pack((float)((double)a.BS * invd), (float)((double)b.BS * invd));
         ss[2 * q] = sa; ss[2 * q + 1] = sb;
         uu[2 * q] = (float)(a.Tmax - a.S); uu[2 * q + 1] = (float)(b.Tmax - b.S);
     }
+    float smin_t = INFINITY, smax_t = -INFINITY, umin_t = INFINITY, umax_t = -INFINITY;
 #pragma unroll
     for (int j = 0; j < KIN; j++) {
         smin_t = fminf(smin_t, ss[j]); smax_t = fmaxf(smax_t, ss[j]);
         umin_t = fminf(umin_t, uu[j]); umax_t = fmaxf(umax_t, uu[j]);
     }
+    // warp-wide bounds: a step no lane can use is dropped when the table is built
+    float smin_w = smin_t, umax_w = umax_t;
+    for (int o = 16; o; o >>= 1) {
+        smin_w = fminf(smin_w, __shfl_xor_sync(0xffffffffu, smin_w, o));
+        umax_w = fmaxf(umax_w, __shfl_xor_sync(0xffffffffu, umax_w, o));
+    }
 
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
     int d[MAXW_ENUM];
-    for (uint64_t unit = u0 + (uint64_t)team; unit < u1; unit += (uint64_t)teams) {
+    for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)(P1_THREADS / 32)) {
         uint64_t row;
         int e0, e1;
         unit_range(P, unit, &row, &e0, &e1);
         decode_row(row, L, W, d);
         const HiSums h = hi_sums(sl, Lmax, d, W);
-        const int ne = e1 - e0;
-        // ---- this unit's prefix table (exact integers -> one rounding each)
-        for (int e = lane; e < ne; e += T) {
-            int64_t Bp = h.B, BSp = h.BS;
-            int32_t Tp = h.T, Tm = h.Tm;
-            if (W >= 2) {
-                const Lev& r = sl[(W - 2) * Lmax + e0 + e];
-                Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
+        // ---- this unit's prefix table: exact integers -> one rounding each; compacted
+        int nc = 0;
+        for (int eb = e0; eb < e1; eb += 32) {
+            const int e = eb + wl;
+            bool use = false;
+            float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
+            float tp = 0.f;
+            if (e < e1) {
+                int64_t Bp = h.B, BSp = h.BS;
+                int32_t Tp = h.T, Tm = h.Tm;
+                if (W >= 2) {
+                    const Lev& r = sl[(W - 2) * Lmax + e];
+                    Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
+                }
+                const double Y = 1.0 + (double)Tp * invd;
+                const double Z = (double)Bp * invd;
+                double X;
+                if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
+                else X = (double)Bp * Y;
+                ent = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
+                tp = (float)Tp;
+                use = !QOS || (ent.w >= smin_w && tp <= umax_w);
             }
-            const double Y = 1.0 + (double)Tp * invd;
-            const double Z = (double)Bp * invd;
-            double X;
-            if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
-            else X = (double)Bp * Y;
-            tab[e] = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
-            if (QOS) tabT[e] = (float)Tp;
+            const unsigned bal = __ballot_sync(0xffffffffu, use);
+            if (use) {
+                const int pos = nc + __popc(bal & ((1u << wl) - 1u));
+                tab[pos] = ent;
+                if (QOS) tabT[pos] = tp;
+            }
+            nc += __popc(bal);
         }
-        __syncwarp(mask);
+        __syncwarp();
         float m0 = INFINITY, m1 = INFINITY;
-        for (int e = 0; e < ne; e++) {
-            const float4 t4 = tab[e];
+        for (int i = team; i < nc; i += G) {
+            const float4 t4 = tab[i];
             bool all = true;
             float Tpf = 0.0f;
+            const float c1 = t4.w;
             if (QOS) {
-                Tpf = tabT[e];
-                const float c1 = t4.w;
+                Tpf = tabT[i];
                 if (!(c1 >= smin_t && Tpf <= umax_t)) continue;   // nothing of mine is feasible here
                 all = (c1 >= smax_t) && (Tpf <= umin_t);
             }
@@ -447,7 +473,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     else m0 = fminf(m0, fminf(k0, k1));
                 }
             } else {
-                const float c1 = t4.w;
 #pragma unroll
                 for (int q = 0; q < KIN / 2; q++) {
                     u64 base = (MODE == M_PAPER) ? add2(X2, D2[q]) : X2;
@@ -459,10 +484,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 }
             }
         }
-        const float m = team_min(fminf(m0, m1), T, mask);
-        if (lane == 0) submin[(size_t)prob * su.units_max + unit] = m;
-        __syncwarp(mask);   // the table is rewritten for the next unit
+        float m = fminf(m0, m1);
+        for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (wl == 0) submin[(size_t)prob * su.units_max + unit] = m;
+        __syncwarp();   // the table is rewritten for the next unit
     }
+    (void)tmask;
 }
 
 // Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
@@ -616,7 +643,7 @@ static bool use_fast(const Setup& su) {
 
 size_t pass1_smem(const Setup& su, bool fast) {
     size_t s = (size_t)su.W * su.Lmax * sizeof(Lev);
-    if (fast) s += (size_t)su.table_bytes;
+    if (fast) s += (size_t)su.table_bytes;   // per-warp prefix tables
     return s;
 }
 

@@ -1,0 +1,31 @@
+"""Workloads for ncu (one GPU): `python tools/profile_driver.py c5|c4|c3 [--mixes N]`.
+Runs one warm-up and one measured call of the named workload through the public API."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2506_12598_b200 as ec  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("what", choices=["c5", "c4", "c3", "s6"])
+ap.add_argument("--mixes", type=int, default=4096)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+if a.what == "c5":
+    models, ids, qos = synth.make_c5(a.mixes)
+    pr = ec.Profiles.from_models(models)
+    d_ids, d_q = torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda()
+    out = ec.alloc_batch_out(a.mixes, 4, 16, device="cuda")
+    for _ in range(a.reps):
+        ec.plan_batch(pr, d_ids, total_sms=148, qos_ns=d_q, p_idle_w=200.0, p_max_w=1000.0, out=out, gmax=16)
+    torch.cuda.synchronize()
+else:
+    p = {"c4": synth.make_c4, "c3": lambda: synth.make_c3("matrix"), "s6": synth.make_s6}[a.what]()
+    pr = ec.Profiles.from_models(p.models)
+    for _ in range(a.reps):
+        r = ec.plan_problem(pr, p)
+    print(r.engine, r.objective)
