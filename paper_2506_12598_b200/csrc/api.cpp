@@ -319,6 +319,8 @@ static int build_host_table(const eclip_profiles* P, const TableSpec& sp, HostTa
     if (bmax >= ((int64_t)1 << 36))
         return fail(ECLIP_E_TOO_LARGE, "model %d: solo request time %lld ns exceeds 2^36 ns", sp.model, (long long)bmax);
     if (smax > (1 << 22)) return fail(ECLIP_E_TOO_LARGE, "model %d: CU-sum range too large", sp.model);
+    if ((double)G * C * (std::min(sp.R, G - 1) + 1) * (smax + 1) >= 2147483647.0)
+        return fail(ECLIP_E_TOO_LARGE, "model %d: level-DP state space exceeds 2^31", sp.model);
     t->smax = (int)smax;
     t->K = sp.bounds.back();
     t->Lcap = (int)smax + 1;
@@ -436,11 +438,11 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
         hbeta[i] = beta;
         CU(s->arena.alloc(&J.V, t.v_elems));
         size_t ns = (size_t)(t.Reff + 1) * (t.smax + 1);
-        CU(s->arena.alloc(&J.best, 2 * ns + t.smax + 1));
-        CU(s->arena.alloc(&J.barg, ns));
+        CU(s->arena.alloc(&J.best, 4 * ns));
+        CU(s->arena.alloc(&J.barg, 2 * ns));
+        CU(s->arena.alloc(&J.bstar, t.smax + 1));
         CU(s->arena.alloc(&J.sidx, t.smax + 1));
-        CU(s->arena.alloc(&J.wtmp, (size_t)(t.smax + 1) * t.G));
-        CU(s->arena.alloc(&J.rank, t.smax + 1));
+        CU(s->arena.alloc(&J.wtmp, (size_t)(t.smax + 1) * ((t.G + 7) / 8)));
         CU(s->arena.alloc(&J.outS, t.Lcap));
         CU(s->arena.alloc(&J.outB, t.Lcap));
         CU(s->arena.alloc(&J.outW, (size_t)t.Lcap * t.G));
@@ -451,7 +453,8 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
     LevelJob* djobs;
     CU(s->arena.alloc(&djobs, nt));
     CU(cudaMemcpyAsync(djobs, jobs.data(), sizeof(LevelJob) * nt, cudaMemcpyHostToDevice, s->st));
-    CU(launch_levels(djobs, jobs.data(), nt, s->st));
+    for (int c0 = 0; c0 < nt; c0 += 64)   // K1 handles up to 64 tables per cooperative launch
+        CU(launch_levels(djobs + c0, jobs.data() + c0, std::min(64, nt - c0), s->st));
     // device table views
     std::vector<int64_t> hK(nt);
     s->tabG.resize(nt);

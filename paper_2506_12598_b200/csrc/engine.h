@@ -28,12 +28,12 @@ struct LevelJob {
     int32_t Lcap;               // capacity of the outputs
     const int64_t* beta;        // [G*C] group solo times (ns)
     const int32_t* need;        // [G*C] n_g c_j / u
-    int64_t* V;                 // workspace [G*C*(R+1)*(smax+1)]
-    int64_t* best;              // workspace [(R+1)*(smax+1)*2]: (b1 | j1<<?) packed as b1, b2 pairs
-    int32_t* barg;              // workspace [(R+1)*(smax+1)] argmin of b1
+    int64_t* V;                 // workspace [G*C*(R+1)*(smax+1)] (< 2^31 entries)
+    int64_t* best;              // workspace [2][(R+1)*(smax+1)][2]: best / second-best over j (2 layer buffers)
+    int32_t* barg;              // workspace [2][(R+1)*(smax+1)] arg-best
+    int64_t* bstar;             // workspace [smax+1] B*(s)
     int32_t* sidx;              // workspace [smax+1] compacted level -> s
-    uint8_t* wtmp;              // workspace [(smax+1)*G] witnesses in s order
-    int32_t* rank;              // workspace [smax+1]
+    uint64_t* wtmp;             // workspace [(smax+1) * ceil(G/8)] packed witnesses in s order
     // outputs (rank order)
     int64_t* outS;              // [Lcap] level CU-sum in SMs
     int64_t* outB;              // [Lcap] B*(S) ns

@@ -369,6 +369,20 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
         perm[rk] = (uint16_t)i;
     }
+    // the step worker's levels sorted by S' inside each segment (a unit covers one segment;
+    // pass 1 only needs the set), so the QoS-usable steps form a prefix of the sorted order
+    __shared__ uint16_t sperm[4096];
+    const int Lst = P.Lstep, segl = P.seglen;
+    if (W >= 2) {
+        const Lev* stepw = sl + (W - 2) * Lmax;
+        for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
+            const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
+            const int si = stepw[i].S;
+            int rk = 0;
+            for (int j = b0; j < b1; j++) rk += stepw[j].S < si;
+            sperm[b0 + rk] = (uint16_t)i;
+        }
+    }
     __syncthreads();
 
     // a warp works on one unit; its G = 32 / T teams interleave over the unit's steps
@@ -412,24 +426,48 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
     int d[MAXW_ENUM];
+    const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
+    const int smin_wi = (int)smin_w, umax_wi = (int)umax_w;
     for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)(P1_THREADS / 32)) {
         uint64_t row;
         int e0, e1;
         unit_range(P, unit, &row, &e0, &e1);
-        decode_row(row, L, W, d);
+        if (row < 0xffffffffull) {      // 32-bit digit decode
+            uint32_t r32 = (uint32_t)row;
+            for (int w = W - 3; w >= 0; w--) { d[w] = (int)(r32 % (uint32_t)L[w]); r32 /= (uint32_t)L[w]; }
+        } else {
+            decode_row(row, L, W, d);
+        }
         const HiSums h = hi_sums(sl, Lmax, d, W);
+        const int ne = e1 - e0;
+        // QoS: step level e is usable by some lane only if  s_e <= sb  (prefix of the sorted
+        // order) and  Tmax_e - s_e - hT >= smin_w  (checked per entry)
+        int sb = 1 << 30;
+        if (QOS) sb = min(h.Tm - h.T - smin_wi, umax_wi - h.T);
         // ---- this unit's prefix table: exact integers -> one rounding each; compacted
         int nc = 0;
-        for (int eb = e0; eb < e1; eb += 32) {
-            const int e = eb + wl;
+        for (int kb = 0; kb < ne; kb += 32) {
+            const int k = kb + wl;
             bool use = false;
-            float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
-            float tp = 0.f;
-            if (e < e1) {
+            bool past = true;
+            int e = 0;
+            if (k < ne) {
+                e = (W >= 2) ? (int)sperm[e0 + k] : 0;
+                if (W >= 2) {
+                    const Lev& r = stepw[e];
+                    past = QOS && r.S > sb;
+                    use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_wi));
+                } else {
+                    past = false;
+                    use = true;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, use);
+            if (use) {
                 int64_t Bp = h.B, BSp = h.BS;
                 int32_t Tp = h.T, Tm = h.Tm;
                 if (W >= 2) {
-                    const Lev& r = sl[(W - 2) * Lmax + e];
+                    const Lev& r = stepw[e];
                     Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
                 }
                 const double Y = 1.0 + (double)Tp * invd;
@@ -437,17 +475,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 double X;
                 if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
                 else X = (double)Bp * Y;
-                ent = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
-                tp = (float)Tp;
-                use = !QOS || (ent.w >= smin_w && tp <= umax_w);
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, use);
-            if (use) {
                 const int pos = nc + __popc(bal & ((1u << wl) - 1u));
-                tab[pos] = ent;
-                if (QOS) tabT[pos] = tp;
+                tab[pos] = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
+                if (QOS) tabT[pos] = (float)Tp;
             }
             nc += __popc(bal);
+            if (__all_sync(0xffffffffu, past)) break;   // the rest of the sorted segment is unusable
         }
         __syncwarp();
         float m0 = INFINITY, m1 = INFINITY;

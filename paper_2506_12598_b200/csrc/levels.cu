@@ -13,11 +13,12 @@
 //                   inside g..G-1, and suffix level s (units of u = gcd of allowed sizes)
 //   V[G-1][j][r][s] = beta[G-1][j]            if s == need[G-1][j]
 //   V[g][j][r][s]   = beta[g][j] + min( V[g+1][j][r][s-need_gj],
-//                                       min_{j' != j} V[g+1][j'][r-1][s-need_gj] )
-// using the best / second-best over j' (O(1) per state).  All G layers are kept (global
-// memory, L2-resident) for the greedy witness reconstruction.
-//
-// One cooperative launch covers every table; layers are separated by grid-wide barriers.
+//                                       min_{j' != j} V[g+1][j'][r-1][s-need_gj] ).
+// One thread owns a (table, r, s) cell of a layer: it computes all C sizes j and, from
+// them, the best / second-best / arg-best over j that the next layer needs, so each layer
+// costs one grid-wide barrier.  All layers stay in global memory (L2-resident) for the
+// greedy witness reconstruction.  Witnesses are packed 8 groups per 64-bit word (group 0
+// in the top byte) so ranking compares words.  One cooperative launch covers every table.
 #include <cooperative_groups.h>
 
 #include "engine.h"
@@ -27,96 +28,90 @@ namespace cg = cooperative_groups;
 namespace eclip {
 
 static constexpr int64_t INF64 = INT64_MAX;
+static constexpr int MAXJ = 64;      // tables per launch (host splits larger sets)
 
-__device__ __forceinline__ size_t vidx(const LevelJob& J, int g, int j, int r, int s) {
-    return ((((size_t)g * J.C + j) * (J.R + 1) + r) * (size_t)(J.smax + 1)) + s;
+__device__ __forceinline__ int vidx(const LevelJob& J, int g, int j, int r, int s) {
+    return (((g * J.C + j) * (J.R + 1) + r) * (J.smax + 1)) + s;
 }
+__device__ __forceinline__ int nwords(const LevelJob& J) { return (J.G + 7) / 8; }
 
 __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax) {
     cg::grid_group grid = cg::this_grid();
-    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t gstride = (size_t)gridDim.x * blockDim.x;
+    __shared__ LevelJob sj[MAXJ];
+    __shared__ int off[MAXJ + 1];
+    for (int t = threadIdx.x; t < n_jobs; t += blockDim.x) sj[t] = jobs[t];
+    __syncthreads();
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gstride = gridDim.x * blockDim.x;
 
+    // ---- DP layers G-1 .. 0 (one cell = (table, r, s); all C sizes per cell) ----
     for (int step = 0; step < gmax; step++) {
-        // ---- phase A: best / second-best over j' of layer g+1 (for steps >= 1) ----
-        if (step > 0) {
-            for (int t = 0; t < n_jobs; t++) {
-                const LevelJob& J = jobs[t];
-                int g = J.G - 1 - step;
-                if (g < 0) continue;
-                size_t n = (size_t)(J.R + 1) * (J.smax + 1);
-                for (size_t i = gtid; i < n; i += gstride) {
-                    int r = (int)(i / (J.smax + 1)), s = (int)(i % (J.smax + 1));
-                    int64_t b1 = INF64, b2 = INF64;
-                    int a1 = -1;
-                    for (int j = 0; j < J.C; j++) {
-                        if (!((J.mask >> j) & 1u)) continue;
-                        int64_t v = J.V[vidx(J, g + 1, j, r, s)];
-                        if (v < b1) { b2 = b1; b1 = v; a1 = j; }
-                        else if (v < b2) { b2 = v; }
-                    }
-                    J.best[2 * i] = b1;
-                    J.best[2 * i + 1] = b2;
-                    J.barg[i] = a1;
-                }
-            }
-            grid.sync();
+        if (threadIdx.x == 0) {
+            off[0] = 0;
+            for (int t = 0; t < n_jobs; t++)
+                off[t + 1] = off[t] + ((sj[t].G - 1 - step >= 0) ? (sj[t].R + 1) * (sj[t].smax + 1) : 0);
         }
-        // ---- phase B: layer g ----
-        for (int t = 0; t < n_jobs; t++) {
-            const LevelJob& J = jobs[t];
-            int g = J.G - 1 - step;
-            if (g < 0) continue;
-            size_t n = (size_t)J.C * (J.R + 1) * (J.smax + 1);
-            for (size_t i = gtid; i < n; i += gstride) {
-                int s = (int)(i % (J.smax + 1));
-                size_t q = i / (J.smax + 1);
-                int r = (int)(q % (J.R + 1));
-                int j = (int)(q / (J.R + 1));
+        __syncthreads();
+        const int total = off[n_jobs];
+        for (int i = gtid; i < total; i += gstride) {
+            int t = 0;
+            while (off[t + 1] <= i) t++;
+            const LevelJob& J = sj[t];
+            const int k = i - off[t];
+            const int S1 = J.smax + 1, ncell = (J.R + 1) * S1;
+            const int r = k / S1, s = k - r * S1;
+            const int g = J.G - 1 - step;
+            const int cur = g & 1, nxt = cur ^ 1;
+            int64_t b1 = INF64, b2 = INF64;
+            int a1 = -1;
+            for (int j = 0; j < J.C; j++) {
                 int64_t out = INF64;
                 if ((J.mask >> j) & 1u) {
-                    int nd = J.need[g * J.C + j];
-                    int64_t b = J.beta[g * J.C + j];
+                    const int nd = J.need[g * J.C + j];
+                    const int64_t b = J.beta[g * J.C + j];
                     if (g == J.G - 1) {
                         if (s == nd) out = b;
                     } else if (nd <= s) {
-                        int sp = s - nd;
+                        const int sp = s - nd;
                         int64_t v = J.V[vidx(J, g + 1, j, r, sp)];
                         if (r >= 1) {
-                            size_t bi = (size_t)(r - 1) * (J.smax + 1) + sp;
-                            int64_t w = (J.barg[bi] != j) ? J.best[2 * bi] : J.best[2 * bi + 1];
+                            const int bi = nxt * ncell + (r - 1) * S1 + sp;
+                            const int64_t w = (J.barg[bi] != j) ? J.best[2 * bi] : J.best[2 * bi + 1];
                             if (w < v) v = w;
                         }
                         if (v != INF64) out = b + v;
                     }
                 }
                 J.V[vidx(J, g, j, r, s)] = out;
+                if (out < b1) { b2 = b1; b1 = out; a1 = j; }
+                else if (out < b2) { b2 = out; }
             }
+            const int bo = cur * ncell + k;
+            J.best[2 * bo] = b1;
+            J.best[2 * bo + 1] = b2;
+            J.barg[bo] = a1;
         }
         grid.sync();
     }
 
-    // ---- phase C/D: per job (one CTA each): B*(s), compaction of attained levels ----
+    // ---- per table (one CTA each): B*(s) = best over j of layer 0 at r = R; compact ----
     for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) {
-        const LevelJob& J = jobs[t];
+        const LevelJob& J = sj[t];
         __shared__ int s_count;
         __shared__ int s_warp[32];
         if (threadIdx.x == 0) s_count = 0;
         __syncthreads();
+        const int S1 = J.smax + 1;
         for (int base = 0; base <= J.smax; base += blockDim.x) {
-            int s = base + threadIdx.x;
+            const int s = base + threadIdx.x;
             int64_t b = INF64;
             if (s <= J.smax) {
-                for (int j = 0; j < J.C; j++) {
-                    if (!((J.mask >> j) & 1u)) continue;
-                    int64_t v = J.V[vidx(J, 0, j, J.R, s)];
-                    if (v < b) b = v;
-                }
-                J.best[s] = b;  // reuse workspace: B*(s)
+                b = J.best[2 * (J.R * S1 + s)];   // layer 0 lives in buffer 0
+                J.bstar[s] = b;
             }
-            int valid = (s <= J.smax) && (b != INF64);
-            unsigned bal = __ballot_sync(0xffffffffu, valid);
-            int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const int valid = (s <= J.smax) && (b != INF64);
+            const unsigned bal = __ballot_sync(0xffffffffu, valid);
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
             if (lane == 0) s_warp[warp] = __popc(bal);
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -125,10 +120,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
                 s_count = acc;
             }
             __syncthreads();
-            if (valid) {
-                int pos = s_warp[warp] + __popc(bal & ((1u << lane) - 1u));
-                J.sidx[pos] = s;
-            }
+            if (valid) J.sidx[s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = s;
             __syncthreads();
         }
         if (threadIdx.x == 0) *J.outL = s_count;
@@ -136,69 +128,74 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     }
     grid.sync();
 
-    // ---- phase E: greedy reconstruction of the canonical witness of every level ----
-    for (int t = 0; t < n_jobs; t++) {
-        const LevelJob& J = jobs[t];
-        int L = *J.outL;
-        for (size_t l = gtid; l < (size_t)L; l += gstride) {
-            int rem = J.sidx[l];
-            int64_t opt = J.best[rem];
-            int r = J.R, prev = -1;
-            for (int g = 0; g < J.G; g++) {
-                int pick = -1;
-                for (int j = 0; j < J.C && pick < 0; j++) {
-                    if (!((J.mask >> j) & 1u)) continue;
-                    int nd = J.need[g * J.C + j];
-                    if (nd > rem) continue;
-                    int rr = (g == 0 || j == prev) ? r : r - 1;
-                    if (rr < 0) continue;
-                    if (J.V[vidx(J, g, j, rr, rem)] == opt) pick = j;
-                }
-                // pick >= 0 always holds (opt is attained); guard anyway
-                if (pick < 0) pick = 0;
-                if (g > 0 && pick != prev) r--;
-                opt -= J.beta[g * J.C + pick];
-                rem -= J.need[g * J.C + pick];
-                prev = pick;
-                J.wtmp[l * J.G + g] = (uint8_t)pick;
+    // flattened (table, level) work for the remaining phases
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        for (int t = 0; t < n_jobs; t++) off[t + 1] = off[t] + *sj[t].outL;
+    }
+    __syncthreads();
+    const int nlev = off[n_jobs];
+
+    // ---- greedy reconstruction of every level's canonical witness (packed words) ----
+    for (int i = gtid; i < nlev; i += gstride) {
+        int t = 0;
+        while (off[t + 1] <= i) t++;
+        const LevelJob& J = sj[t];
+        const int l = i - off[t];
+        int rem = J.sidx[l];
+        int64_t opt = J.bstar[rem];
+        int r = J.R, prev = -1;
+        const int nw = nwords(J);
+        uint64_t word = 0;
+        for (int g = 0; g < J.G; g++) {
+            int pick = -1;
+            for (int j = 0; j < J.C && pick < 0; j++) {
+                if (!((J.mask >> j) & 1u)) continue;
+                const int nd = J.need[g * J.C + j];
+                if (nd > rem) continue;
+                const int rr = (g == 0 || j == prev) ? r : r - 1;
+                if (rr < 0) continue;
+                if (J.V[vidx(J, g, j, rr, rem)] == opt) pick = j;
+            }
+            if (pick < 0) pick = 0;   // unreachable: opt is attained
+            if (g > 0 && pick != prev) r--;
+            opt -= J.beta[g * J.C + pick];
+            rem -= J.need[g * J.C + pick];
+            prev = pick;
+            word |= (uint64_t)pick << (8 * (7 - (g & 7)));
+            if ((g & 7) == 7 || g == J.G - 1) {
+                J.wtmp[(size_t)l * nw + (g >> 3)] = word;
+                word = 0;
             }
         }
     }
     grid.sync();
 
-    // ---- phase F: rank of every level = number of lexicographically smaller witnesses ----
-    for (int t = 0; t < n_jobs; t++) {
-        const LevelJob& J = jobs[t];
-        int L = *J.outL;
-        for (size_t l = gtid; l < (size_t)L; l += gstride) {
-            const uint8_t* a = J.wtmp + l * J.G;
-            int rk = 0;
-            for (int m = 0; m < L; m++) {
-                const uint8_t* b = J.wtmp + (size_t)m * J.G;
-                for (int g = 0; g < J.G; g++) {
-                    if (b[g] != a[g]) { rk += (b[g] < a[g]); break; }
-                }
+    // ---- rank = number of lexicographically smaller witnesses; scatter to rank order ----
+    for (int i = gtid; i < nlev; i += gstride) {
+        int t = 0;
+        while (off[t + 1] <= i) t++;
+        const LevelJob& J = sj[t];
+        const int l = i - off[t];
+        const int L = off[t + 1] - off[t];
+        const int nw = nwords(J);
+        const uint64_t* a = J.wtmp + (size_t)l * nw;
+        int rk = 0;
+        for (int m = 0; m < L; m++) {
+            const uint64_t* b = J.wtmp + (size_t)m * nw;
+            for (int q = 0; q < nw; q++) {
+                if (b[q] != a[q]) { rk += (b[q] < a[q]); break; }
             }
-            J.rank[l] = rk;
         }
-    }
-    grid.sync();
-
-    // ---- phase G: scatter to rank order ----
-    for (int t = 0; t < n_jobs; t++) {
-        const LevelJob& J = jobs[t];
-        int L = *J.outL;
-        for (size_t l = gtid; l < (size_t)L; l += gstride) {
-            int rk = J.rank[l];
-            int s = J.sidx[l];
-            J.outS[rk] = (int64_t)s * J.u;
-            J.outB[rk] = J.best[s];
-            for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = J.wtmp[l * J.G + g];
-        }
+        const int s = J.sidx[l];
+        J.outS[rk] = (int64_t)s * J.u;
+        J.outB[rk] = J.bstar[s];
+        for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
     }
 }
 
 cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, cudaStream_t st) {
+    if (n_jobs > MAXJ) return cudaErrorInvalidValue;
     int gmax = 0;
     for (int i = 0; i < n_jobs; i++) gmax = h_jobs[i].G > gmax ? h_jobs[i].G : gmax;
     int dev = 0, nsm = 0, per_sm = 0;
@@ -207,7 +204,7 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, 256, 0);
     if (e != cudaSuccess) return e;
-    if (per_sm > 4) per_sm = 4;
+    if (per_sm > 2) per_sm = 2;
     int grid = nsm * (per_sm > 0 ? per_sm : 1);
     void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax};
     return cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, 0, st);
