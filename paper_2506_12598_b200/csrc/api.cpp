@@ -564,7 +564,9 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.units_max = (int64_t)units;
     su.items_max = (int32_t)std::ceil(units / su.upi);
     su.table_bytes = 0;
-    if (fast) su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * seglen * 20);   // per-warp tables
+    if (fast)   // inner pair arrays + sorted S' + prefix minima + per-warp tables {X,Y,Z,Tp}{k_hi,clean}
+        su.table_bytes = (int32_t)((((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 8 + 15) / 16 * 16 +
+                                   (size_t)(P1_THREADS / 32) * seglen * 24);
     return ECLIP_OK;
 }
 

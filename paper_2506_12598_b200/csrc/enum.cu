@@ -331,21 +331,27 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
     *ok = *item < shi;
 }
 
-// Fast filter: SUM objective with EXCLUDE_SELF or PAPER_AS_WRITTEN, L_inner <= 32 KIN.
+// Fast filter: SUM objective with EXCLUDE_SELF or PAPER_AS_WRITTEN.
 // With exact prefix sums (Bp, BSp, Tp) over workers 0..W-2 and the inner level (B_i, S'_i),
 // the SUM key  sum_w B_w (1 + O_w / (Lambda N))  is, exactly,
 //   EXCLUDE_SELF:  K = X_p + B_i Y_p + S'_i Z_p,         X_p = Bp + (Tp Bp - BSp) / (Lambda N)
 //   PAPER:         K = X_p + B_i Y_p + S'_i Z_p + D_i,   X_p = Bp (1 + Tp / (Lambda N))
 //   Y_p = 1 + Tp / (Lambda N),   Z_p = Bp / (Lambda N),   D_i = B_i S'_i / (Lambda N),
-// every term >= 0.  Per candidate: 2 FMAs (packed f32x2: one issue slot for two candidates)
-// + a 3-input min.  FP32 relative error <= 5u.  The per-prefix (X, Y, Z)
-// come from a per-team table built once per unit from exact integers.
+// every term >= 0.  Per candidate: 2 FMAs (packed f32x2: one issue slot per two candidates)
+// + a 3-input min; FP32 relative error <= 5u.
+// Mapping: a warp owns a unit (one hi-digit row x one segment of the step worker).  Its
+// lanes build a compacted table of the usable step levels (exact integers -> X, Y, Z, one
+// rounding each), then each lane takes its own table entries and sweeps the inner worker's
+// levels, S'-sorted and broadcast from shared memory, up to its exact QoS cut
+//   k_hi = #{i : S'_i <= c1},  c1 = min_w Tmax_w - Tp  (prefix workers' QoS);
+// the inner worker's own bound (Tp <= u_i) is masked only when it can bind (prefix minimum).
 template <int MODE, bool QOS>
 __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
-    __shared__ uint16_t perm[4096];   // inner levels sorted by S' (pass 1 is order-free)
+    __shared__ uint16_t perm[4096];    // inner levels sorted by S'
+    __shared__ uint16_t sperm[4096];   // step levels sorted by S' within each segment
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const int prob = blockIdx.x / ipS;
     const Prob& P = probs[prob];
@@ -361,20 +367,30 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     int L[MAXW_ENUM];
     for (int w = 0; w < W; w++) L[w] = P.L[w];
     const int Lin = L[W - 1];
+    const int npair = (Lin + 1) / 2;
     const Lev* inner = sl + (W - 1) * Lmax;
-    // rank every inner level by S' (distinct per level) -> perm
+    const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
+    const int Lst = P.Lstep, segl = P.seglen;
+    // shared layout after the staged records
+    unsigned char* p0 = smem_raw + (size_t)W * Lmax * sizeof(Lev);
+    float4* ip = reinterpret_cast<float4*>(p0);                       // [npair] {B_k, B_k+1, S_k, S_k+1}
+    float2* iu = reinterpret_cast<float2*>(ip + ((Lmax + 1) / 2));      // [npair] {u_k, u_k+1}
+    float2* iD = iu + ((Lmax + 1) / 2);                                 // [npair] PAPER: {D_k, D_k+1}
+    int* ssort = reinterpret_cast<int*>(iD + ((Lmax + 1) / 2));         // [Lin] sorted S'
+    float* uminp = reinterpret_cast<float*>(ssort + Lmax + 1);          // [Lin+1] prefix min of u
+    float4* tab0 = reinterpret_cast<float4*>(p0 + (((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 8 + 15) / 16 * 16);
+    const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+    float4* tab = tab0 + (size_t)warp * segl;                                          // {X, Y, Z, Tp}
+    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)(P1_THREADS / 32) * segl) + (size_t)warp * segl;  // {k_hi, clean}
+
+    const double invd = 1.0 / (double)P.lamN;
     for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
         const int si = inner[i].S;
         int rk = 0;
         for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
         perm[rk] = (uint16_t)i;
     }
-    // the step worker's levels sorted by S' inside each segment (a unit covers one segment;
-    // pass 1 only needs the set), so the QoS-usable steps form a prefix of the sorted order
-    __shared__ uint16_t sperm[4096];
-    const int Lst = P.Lstep, segl = P.seglen;
     if (W >= 2) {
-        const Lev* stepw = sl + (W - 2) * Lmax;
         for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
             const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
             const int si = stepw[i].S;
@@ -384,50 +400,31 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
     }
     __syncthreads();
-
-    // a warp works on one unit; its G = 32 / T teams interleave over the unit's steps
-    const int T = fast_team(Lin), G = 32 / T;
-    const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
-    const int team = wl / T, lane = wl % T;
-    const unsigned tmask = team_mask(T);
-    const int seglen = P.seglen;
-    float4* tab = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) + (size_t)warp * seglen;
-    float* tabT = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev)) +
-                                           (size_t)(P1_THREADS / 32) * seglen) + (size_t)warp * seglen;
-
-    // inner levels in registers, S'-sorted blocks of KIN per lane (tail padded with the last one)
-    u64 B2[KIN / 2], S2[KIN / 2], D2[KIN / 2];
-    float uu[KIN], ss[KIN];
-    const double invd = 1.0 / (double)P.lamN;
-#pragma unroll
-    for (int q = 0; q < KIN / 2; q++) {
-        const Lev& a = inner[perm[min(lane * KIN + 2 * q, Lin - 1)]];
-        const Lev& b = inner[perm[min(lane * KIN + 2 * q + 1, Lin - 1)]];
-        B2[q] = f2pack(__ll2float_rn(a.B), __ll2float_rn(b.B));
-        const float sa = (float)a.S, sb = (float)b.S;
-        S2[q] = f2pack(sa, sb);
-        if (MODE == M_PAPER) D2[q] = f2pack((float)((double)a.BS * invd), (float)((double)b.BS * invd));
-        ss[2 * q] = sa; ss[2 * q + 1] = sb;
-        uu[2 * q] = (float)(a.Tmax - a.S); uu[2 * q + 1] = (float)(b.Tmax - b.S);
+    for (int p = threadIdx.x; p < npair; p += blockDim.x) {
+        const Lev& a = inner[perm[2 * p]];
+        const Lev& b = inner[perm[min(2 * p + 1, Lin - 1)]];
+        ip[p] = make_float4(__ll2float_rn(a.B), __ll2float_rn(b.B), (float)a.S, (float)b.S);
+        iu[p] = make_float2((float)(a.Tmax - a.S), (float)(b.Tmax - b.S));
+        if (MODE == M_PAPER) iD[p] = make_float2((float)((double)a.BS * invd), (float)((double)b.BS * invd));
     }
-    float smin_t = INFINITY, smax_t = -INFINITY, umin_t = INFINITY, umax_t = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < KIN; j++) {
-        smin_t = fminf(smin_t, ss[j]); smax_t = fmaxf(smax_t, ss[j]);
-        umin_t = fminf(umin_t, uu[j]); umax_t = fmaxf(umax_t, uu[j]);
+    for (int k = threadIdx.x; k < Lin; k += blockDim.x) ssort[k] = inner[perm[k]].S;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = INFINITY;
+        uminp[0] = m;
+        for (int k = 0; k < Lin; k++) {
+            m = fminf(m, (float)(inner[perm[k]].Tmax - inner[perm[k]].S));
+            uminp[k + 1] = m;
+        }
     }
-    // warp-wide bounds: a step no lane can use is dropped when the table is built
-    float smin_w = smin_t, umax_w = umax_t;
-    for (int o = 16; o; o >>= 1) {
-        smin_w = fminf(smin_w, __shfl_xor_sync(0xffffffffu, smin_w, o));
-        umax_w = fmaxf(umax_w, __shfl_xor_sync(0xffffffffu, umax_w, o));
-    }
+    __syncthreads();
+    float umax_all = -INFINITY;
+    for (int k = 0; k < Lin; k++) umax_all = fmaxf(umax_all, (float)(inner[k].Tmax - inner[k].S));
+    const int smin_i = ssort[0], umax_i = (int)umax_all;
 
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
     int d[MAXW_ENUM];
-    const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
-    const int smin_wi = (int)smin_w, umax_wi = (int)umax_w;
     for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)(P1_THREADS / 32)) {
         uint64_t row;
         int e0, e1;
@@ -440,29 +437,28 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         const HiSums h = hi_sums(sl, Lmax, d, W);
         const int ne = e1 - e0;
-        // QoS: step level e is usable by some lane only if  s_e <= sb  (prefix of the sorted
-        // order) and  Tmax_e - s_e - hT >= smin_w  (checked per entry)
+        // step level e can be used only if  s_e <= sb  (a prefix of the sorted order) and
+        // Tmax_e - s_e - hT >= min_i S'_i
         int sb = 1 << 30;
-        if (QOS) sb = min(h.Tm - h.T - smin_wi, umax_wi - h.T);
-        // ---- this unit's prefix table: exact integers -> one rounding each; compacted
+        if (QOS) sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
         int nc = 0;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
-            bool use = false;
-            bool past = true;
+            bool use = false, past = true;
             int e = 0;
             if (k < ne) {
-                e = (W >= 2) ? (int)sperm[e0 + k] : 0;
                 if (W >= 2) {
+                    e = (int)sperm[e0 + k];
                     const Lev& r = stepw[e];
                     past = QOS && r.S > sb;
-                    use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_wi));
+                    use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_i));
                 } else {
                     past = false;
                     use = true;
                 }
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, use);
+            float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
+            int khi = Lin, clean = 1;
             if (use) {
                 int64_t Bp = h.B, BSp = h.BS;
                 int32_t Tp = h.T, Tm = h.Tm;
@@ -475,45 +471,73 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 double X;
                 if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
                 else X = (double)Bp * Y;
+                ent = make_float4((float)X, (float)Y, (float)Z, (float)Tp);
+                if (QOS) {
+                    const int c1 = Tm - Tp;   // inner S' must be <= c1
+                    int lo = 0, hi = Lin;     // khi = #{k : ssort[k] <= c1}
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (ssort[mid] <= c1) lo = mid + 1; else hi = mid;
+                    }
+                    khi = lo;
+                    clean = (float)Tp <= uminp[khi];
+                    use = khi > 0;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, use);
+            if (use) {
                 const int pos = nc + __popc(bal & ((1u << wl) - 1u));
-                tab[pos] = make_float4((float)X, (float)Y, (float)Z, (float)(Tm - Tp));
-                if (QOS) tabT[pos] = (float)Tp;
+                tab[pos] = ent;
+                tabk[pos] = make_int2(khi, clean);
             }
             nc += __popc(bal);
             if (__all_sync(0xffffffffu, past)) break;   // the rest of the sorted segment is unusable
         }
         __syncwarp();
         float m0 = INFINITY, m1 = INFINITY;
-        for (int i = team; i < nc; i += G) {
+        for (int i = wl; i < nc; i += 32) {
             const float4 t4 = tab[i];
-            bool all = true;
-            float Tpf = 0.0f;
-            const float c1 = t4.w;
-            if (QOS) {
-                Tpf = tabT[i];
-                if (!(c1 >= smin_t && Tpf <= umax_t)) continue;   // nothing of mine is feasible here
-                all = (c1 >= smax_t) && (Tpf <= umin_t);
-            }
+            const int2 kk = tabk[i];
             const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
-            if (all) {
-#pragma unroll
-                for (int q = 0; q < KIN / 2; q++) {
-                    u64 base = (MODE == M_PAPER) ? add2(X2, D2[q]) : X2;
-                    const u64 key = fma2(B2[q], Y2, fma2(S2[q], Z2, base));
+            const int np = kk.x >> 1;
+            const bool masked = QOS && !kk.y;
+            if (!masked) {
+                int p = 0;
+#pragma unroll 4
+                for (; p < np; p++) {
+                    const float4 r = ip[p];
+                    u64 base = X2;
+                    if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                    const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
                     float k0, k1;
                     f2unpack(key, k0, k1);
-                    if (q & 1) m1 = fminf(m1, fminf(k0, k1));
+                    if (p & 1) m1 = fminf(m1, fminf(k0, k1));
                     else m0 = fminf(m0, fminf(k0, k1));
                 }
+                if (kk.x & 1) {   // odd tail: first element of pair np
+                    const float4 r = ip[np];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += iD[np].x;
+                    m0 = fminf(m0, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
+                }
             } else {
-#pragma unroll
-                for (int q = 0; q < KIN / 2; q++) {
-                    u64 base = (MODE == M_PAPER) ? add2(X2, D2[q]) : X2;
-                    const u64 key = fma2(B2[q], Y2, fma2(S2[q], Z2, base));
+                const float Tpf = t4.w;
+                for (int p = 0; p < np; p++) {
+                    const float4 r = ip[p];
+                    const float2 uu2 = iu[p];
+                    u64 base = X2;
+                    if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                    const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
                     float k0, k1;
                     f2unpack(key, k0, k1);
-                    if (ss[2 * q] <= c1 && Tpf <= uu[2 * q]) m0 = fminf(m0, k0);
-                    if (ss[2 * q + 1] <= c1 && Tpf <= uu[2 * q + 1]) m1 = fminf(m1, k1);
+                    if (Tpf <= uu2.x) m0 = fminf(m0, k0);
+                    if (Tpf <= uu2.y) m1 = fminf(m1, k1);
+                }
+                if (kk.x & 1) {
+                    const float4 r = ip[np];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += iD[np].x;
+                    if (Tpf <= iu[np].x) m0 = fminf(m0, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
                 }
             }
         }
@@ -522,7 +546,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (wl == 0) submin[(size_t)prob * su.units_max + unit] = m;
         __syncwarp();   // the table is rewritten for the next unit
     }
-    (void)tmask;
 }
 
 // Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
