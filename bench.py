@@ -188,7 +188,7 @@ def main():
     value = world * a.steps * cand_step / (t_max_ms * 1e-3)
 
     # ---- pass-1 kernel alone (the dominant kernel): CUDA events on the launching stream
-    k_ms, k_launches = pass1_time(ec, pr, ids, qos, stream, local)
+    k_ms, k_launches, k_eval = pass1_time(ec, pr, ids, qos, stream, local)
 
     # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
     pin_ids = torch.from_numpy(ids).pin_memory()
@@ -215,12 +215,15 @@ def main():
 
     if rank == 0:
         f_max = 1965.0
-        # the dominant kernel evaluates K = X_p + B_i Y_p + S'_i Z_p per candidate:
-        # 2 FP32 FMAs (FMA pipe, packed f32x2) + 1/2 three-input min (ALU pipe).  The FMA pipe
-        # (128 lane-ops / clk / SM, measured) bounds it: peak = 148 x 128 x 1965 MHz lane-ops/s.
+        # the dominant kernel evaluates K = X_p + B_i Y_p + S'_i Z_p for every
+        # QoS-feasible candidate: 2 FP32 FMAs (FMA pipe, packed f32x2) + 1/2 three-input min;
+        # QoS-infeasible candidates are classified by exact range cuts with no FP work.  Roofline
+        # = FMA pipe (128 lane-ops / clk / SM measured): peak 148 x 128 x 1965 MHz lane-ops/s,
+        # achieved = 2 x evaluated candidates / kernel time.
         fma_ops_per_cand = 2.0
-        cand_per_s_kernel = cand_step / (k_ms / k_launches * 1e-3)
-        achieved = fma_ops_per_cand * cand_per_s_kernel / 1e9
+        k_s = k_ms / k_launches * 1e-3
+        cand_per_s_kernel = cand_step / k_s
+        achieved = fma_ops_per_cand * k_eval / k_s / 1e9
         peak = 148 * 128 * f_max * 1e6 / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -237,7 +240,9 @@ def main():
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": k_ms / k_launches,
                          "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
-                         "fma_lane_ops_per_candidate": fma_ops_per_cand,
+                         "fma_lane_ops_per_evaluated_candidate": fma_ops_per_cand,
+                         "evaluated_candidates_per_launch": k_eval,
+                         "evaluated_fraction": k_eval / cand_step,
                          "candidates_per_s_kernel": cand_per_s_kernel},
             "clocks": ck,
             "time_to_plan_ms": ttp,
@@ -259,10 +264,11 @@ def level_counts(pr, ec):
 
 
 def pass1_time(ec, pr, ids, qos, stream, local):
-    """CUDA-event time of the pass-1 kernel(s) alone, via the split API on the same stream"""
+    """CUDA-event time of the pass-1 kernel (+ its tiny reduction) alone, via the split API on
+    the same stream; also returns how many candidates pass 1 evaluated in FP32."""
     import torch
     from paper_2506_12598_b200.eclip import Session
-    tot, launches = 0.0, 0
+    tot, launches, evaluated = 0.0, 0, 0
     for rep in range(3):
         s = Session(pr, batch=dict(model_ids=ids, qos_ns=qos, total_sms=148, p_idle_w=200.0, p_max_w=1000.0),
                     engine="enum", device=local, stream=stream.cuda_stream)
@@ -275,8 +281,9 @@ def pass1_time(ec, pr, ids, qos, stream, local):
         if rep > 0:
             tot += e0.elapsed_time(e1)
             launches += 1
+            evaluated = s.stats()["evaluated_candidates"]
         s.close()
-    return tot, launches
+    return tot, launches, evaluated
 
 
 def time_to_plan(ec, world, rank, dist):

@@ -197,6 +197,10 @@ int eclip_session_pass2_min(eclip_session* s, const float* global_min_key32, uin
 int eclip_session_pass2_first(eclip_session* s, const uint64_t* global_exact_min, uint64_t* first_tuple);
 int eclip_session_finish(eclip_session* s, const uint64_t* global_first_tuple, eclip_batch_out* out);
 void eclip_session_free(eclip_session* s);
+/* Counters of the last pass 1 of this session: candidates whose FP32 key was evaluated
+ * (QoS-feasible; the others are classified infeasible by exact range cuts without
+ * arithmetic) — used by bench.py to report the roofline on the work actually done. */
+int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
 
 /* Single-problem sessions (the per-worker masks / groups of eclip_problem; used to shard
  * one large problem, e.g. BASELINE config 4, across GPUs).  Same steps as above with

@@ -564,9 +564,11 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.units_max = (int64_t)units;
     su.items_max = (int32_t)std::ceil(units / su.upi);
     su.table_bytes = 0;
-    if (fast)   // inner pair arrays + sorted S' + prefix minima + per-warp tables {X,Y,Z,Tp}{k_hi,clean}
-        su.table_bytes = (int32_t)((((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 8 + 15) / 16 * 16 +
-                                   (size_t)(P1_THREADS / 32) * seglen * 24);
+    if (fast) {   // inner pairs + sorted S' / suffix-min / prefix-max + perms + 2 lookup tables + per-warp tables
+        size_t b = ((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 2 * (size_t)P1_TABN * 2;
+        b = (b + 15) / 16 * 16;
+        su.table_bytes = (int32_t)(b + (size_t)(P1_THREADS / 32) * seglen * 24);
+    }
     return ECLIP_OK;
 }
 
@@ -585,6 +587,8 @@ static int alloc_work(eclip_session* s) {
     CU(s->arena.alloc(&wk.m32_sure, n));
     CU(s->arena.alloc(&wk.hstar, n));
     CU(s->arena.alloc(&wk.first, n));
+    CU(s->arena.alloc(&wk.feasible, 1));
+    CU(cudaMemsetAsync(wk.feasible, 0, sizeof(unsigned long long), s->st));
     return ECLIP_OK;
 }
 
@@ -910,6 +914,15 @@ extern "C" int eclip_session_finish(eclip_session* s, const uint64_t* global_fir
 }
 
 extern "C" void eclip_session_free(eclip_session* s) { delete s; }
+
+extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
+    if (!s || !evaluated) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    unsigned long long v = 0;
+    if (s->wk.feasible) CU(cudaMemcpyAsync(&v, s->wk.feasible, sizeof v, cudaMemcpyDeviceToHost, s->st));
+    CU(cudaStreamSynchronize(s->st));
+    *evaluated = v;
+    return ECLIP_OK;
+}
 
 // ------------------------------------------------------------------------------------------
 // one-shot entry points

@@ -12,7 +12,7 @@ constexpr int MAXW = 16;        // workers per problem (API limit)
 constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
 constexpr int P1_THREADS = 256; // pass-1 CTA size
 constexpr int KIN = 16;         // inner-worker levels held in registers per thread (fast pass 1)
-constexpr int TABLE_BYTES = 96 * 1024;  // per-CTA prefix tables of the fast pass-1 kernel
+constexpr int P1_TABN = 8192;   // entries of each QoS range lookup table (fast pass 1)
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
 enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };
@@ -130,6 +130,7 @@ struct Work {
     U256* hstar;                // [n] exact minimum
     U256* first;                // [n] winner: lowest tuple within tolerance, packed (pack_tuple); all-ones = none
     uint64_t* scored;           // [n]
+    unsigned long long* feasible;  // [1] QoS-feasible candidates evaluated by the fast pass 1
 };
 
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,

@@ -338,20 +338,23 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 //   PAPER:         K = X_p + B_i Y_p + S'_i Z_p + D_i,   X_p = Bp (1 + Tp / (Lambda N))
 //   Y_p = 1 + Tp / (Lambda N),   Z_p = Bp / (Lambda N),   D_i = B_i S'_i / (Lambda N),
 // every term >= 0.  Per candidate: 2 FMAs (packed f32x2: one issue slot per two candidates)
-// + a 3-input min; FP32 relative error <= 5u.
+// + a 3-input min; FP32 relative error <= 8u.
 // Mapping: a warp owns a unit (one hi-digit row x one segment of the step worker).  Its
-// lanes build a compacted table of the usable step levels (exact integers -> X, Y, Z, one
-// rounding each), then each lane takes its own table entries and sweeps the inner worker's
-// levels, S'-sorted and broadcast from shared memory, up to its exact QoS cut
-//   k_hi = #{i : S'_i <= c1},  c1 = min_w Tmax_w - Tp  (prefix workers' QoS);
-// the inner worker's own bound (Tp <= u_i) is masked only when it can bind (prefix minimum).
+// lanes build a compacted table of the usable step levels, then each lane takes its own
+// entries and sweeps the inner worker's levels (S'-sorted, broadcast from shared memory)
+// over the exact QoS-feasible range:
+//   prefix workers' QoS:  S'_k <= c1 = min_w Tmax_w - Tp   ->  k < k_hi   (prefix of sorted order)
+//   inner worker's QoS:   Tp <= u_k = Tmax_k - S'_k        ->  k >= k_lo where k_lo is the first
+//       index of the suffix-minimum of u that reaches Tp (exact when u is non-decreasing in S',
+//       i.e. B* non-increasing; otherwise the earlier levels are swept with a mask).
+// Both ends come from lookup tables indexed by value (binary search if a range is too wide).
 template <int MODE, bool QOS>
 __global__ void __launch_bounds__(P1_THREADS, 2)
-k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin) {
+k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
+             unsigned long long* __restrict__ feasible) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
-    __shared__ uint16_t perm[4096];    // inner levels sorted by S'
-    __shared__ uint16_t sperm[4096];   // step levels sorted by S' within each segment
+    __shared__ int sh_range[4];
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const int prob = blockIdx.x / ipS;
     const Prob& P = probs[prob];
@@ -371,19 +374,28 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const Lev* inner = sl + (W - 1) * Lmax;
     const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
     const int Lst = P.Lstep, segl = P.seglen;
-    // shared layout after the staged records
+    // ---- shared layout after the staged records (host: pass1 table_bytes)
+    const int LP = (Lmax + 1) / 2;
     unsigned char* p0 = smem_raw + (size_t)W * Lmax * sizeof(Lev);
-    float4* ip = reinterpret_cast<float4*>(p0);                       // [npair] {B_k, B_k+1, S_k, S_k+1}
-    float2* iu = reinterpret_cast<float2*>(ip + ((Lmax + 1) / 2));      // [npair] {u_k, u_k+1}
-    float2* iD = iu + ((Lmax + 1) / 2);                                 // [npair] PAPER: {D_k, D_k+1}
-    int* ssort = reinterpret_cast<int*>(iD + ((Lmax + 1) / 2));         // [Lin] sorted S'
-    float* uminp = reinterpret_cast<float*>(ssort + Lmax + 1);          // [Lin+1] prefix min of u
-    float4* tab0 = reinterpret_cast<float4*>(p0 + (((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 8 + 15) / 16 * 16);
+    float4* ip = reinterpret_cast<float4*>(p0);                 // [LP] {B_k, B_k+1, S_k, S_k+1}
+    float2* iu = reinterpret_cast<float2*>(ip + LP);             // [LP] {u_k, u_k+1}
+    float2* iD = iu + LP;                                        // [LP] PAPER: {D_k, D_k+1}
+    int* ssort = reinterpret_cast<int*>(iD + LP);                // [Lmax+1] sorted S'
+    int* usuf = ssort + (Lmax + 1);                              // [Lmax+1] suffix min of u (usuf[Lin] = +big)
+    int* umaxp = usuf + (Lmax + 1);                              // [Lmax+1] prefix max of u
+    uint16_t* perm = reinterpret_cast<uint16_t*>(umaxp + (Lmax + 1));   // [Lmax] inner sorted by S'
+    uint16_t* sperm = perm + Lmax;                                       // [Lmax] step sorted by S' per segment
+    uint16_t* khi_tab = sperm + Lmax;                                    // [TABN]
+    uint16_t* klo_tab = khi_tab + P1_TABN;                               // [TABN]
+    float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + (size_t)su.table_bytes -
+                                             (size_t)(P1_THREADS / 32) * segl * 24);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
-    float4* tab = tab0 + (size_t)warp * segl;                                          // {X, Y, Z, Tp}
-    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)(P1_THREADS / 32) * segl) + (size_t)warp * segl;  // {k_hi, clean}
+    float4* tab = tab0 + (size_t)warp * segl;                                                           // {X,Y,Z,Tp}
+    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)(P1_THREADS / 32) * segl) + (size_t)warp * segl;  // {k_lo, k_hi}
 
+    const float invf = P.inv;
     const double invd = 1.0 / (double)P.lamN;
+    // ---- sort inner levels and the step worker's segments by S'
     for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
         const int si = inner[i].S;
         int rk = 0;
@@ -408,23 +420,51 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (MODE == M_PAPER) iD[p] = make_float2((float)((double)a.BS * invd), (float)((double)b.BS * invd));
     }
     for (int k = threadIdx.x; k < Lin; k += blockDim.x) ssort[k] = inner[perm[k]].S;
-    __syncthreads();
     if (threadIdx.x == 0) {
-        float m = INFINITY;
-        uminp[0] = m;
+        int m = 1 << 30;
+        usuf[Lin] = m;
+        for (int k = Lin - 1; k >= 0; k--) {
+            m = min(m, inner[perm[k]].Tmax - inner[perm[k]].S);
+            usuf[k] = m;
+        }
+        int M = -(1 << 30);
+        umaxp[0] = M;
         for (int k = 0; k < Lin; k++) {
-            m = fminf(m, (float)(inner[perm[k]].Tmax - inner[perm[k]].S));
-            uminp[k + 1] = m;
+            M = max(M, inner[perm[k]].Tmax - inner[perm[k]].S);
+            umaxp[k + 1] = M;
+        }
+        sh_range[0] = ssort[0];
+        sh_range[1] = ssort[Lin - 1] - ssort[0] + 1 <= P1_TABN;         // k_hi table usable
+        sh_range[2] = usuf[0];
+        sh_range[3] = usuf[Lin - 1] - usuf[0] + 1 <= P1_TABN;           // k_lo table usable
+    }
+    __syncthreads();
+    const int s0 = sh_range[0], u0v = sh_range[2];
+    const bool khi_ok = sh_range[1] != 0, klo_ok = sh_range[3] != 0;
+    // khi_tab[v - s0] = #{k : S'_k <= v};  klo_tab[v - u0] = min{k : usuf[k] >= v}
+    if (khi_ok) {
+        const int n = ssort[Lin - 1] - s0 + 1;
+        for (int v = threadIdx.x; v < n; v += blockDim.x) {
+            int lo = 0, hi = Lin;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (ssort[mid] <= s0 + v) lo = mid + 1; else hi = mid; }
+            khi_tab[v] = (uint16_t)lo;
+        }
+    }
+    if (klo_ok) {
+        const int n = usuf[Lin - 1] - u0v + 1;
+        for (int v = threadIdx.x; v < n; v += blockDim.x) {
+            int lo = 0, hi = Lin;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (usuf[mid] >= u0v + v) hi = mid; else lo = mid + 1; }
+            klo_tab[v] = (uint16_t)lo;
         }
     }
     __syncthreads();
-    float umax_all = -INFINITY;
-    for (int k = 0; k < Lin; k++) umax_all = fmaxf(umax_all, (float)(inner[k].Tmax - inner[k].S));
-    const int smin_i = ssort[0], umax_i = (int)umax_all;
+    const int smin_i = ssort[0], umax_i = umaxp[Lin];
 
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
     int d[MAXW_ENUM];
+    unsigned long long nfeas = 0;
     for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)(P1_THREADS / 32)) {
         uint64_t row;
         int e0, e1;
@@ -437,8 +477,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         const HiSums h = hi_sums(sl, Lmax, d, W);
         const int ne = e1 - e0;
-        // step level e can be used only if  s_e <= sb  (a prefix of the sorted order) and
-        // Tmax_e - s_e - hT >= min_i S'_i
+        // step level e is usable only if  s_e <= sb  (a prefix of the sorted order) and
+        // Tmax_e - s_e - hT >= min_k S'_k
         int sb = 1 << 30;
         if (QOS) sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
         int nc = 0;
@@ -458,7 +498,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 }
             }
             float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
-            int khi = Lin, clean = 1;
+            int klo = 0, khi = Lin;
             if (use) {
                 int64_t Bp = h.B, BSp = h.BS;
                 int32_t Tp = h.T, Tm = h.Tm;
@@ -466,29 +506,44 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     const Lev& r = stepw[e];
                     Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
                 }
-                const double Y = 1.0 + (double)Tp * invd;
-                const double Z = (double)Bp * invd;
-                double X;
-                if (MODE == M_EXCL) X = (double)Bp + (double)((u128)Tp * (u128)Bp - (u128)BSp) * invd;
-                else X = (double)Bp * Y;
-                ent = make_float4((float)X, (float)Y, (float)Z, (float)Tp);
+                const float Bpf = __ll2float_rn(Bp), Tpf = (float)Tp;
+                float X;
+                if (MODE == M_EXCL) {
+                    const u128 Dn = (u128)Tp * (u128)Bp - (u128)BSp;   // = sum_w B_w (Tp - S'_w) >= 0
+                    const float Df = (Dn >> 64) ? (float)(double)Dn : __ull2float_rn((unsigned long long)Dn);
+                    X = fmaf(Df, invf, Bpf);
+                } else {
+                    X = Bpf * fmaf(Tpf, invf, 1.0f);
+                }
+                ent = make_float4(X, fmaf(Tpf, invf, 1.0f), Bpf * invf, Tpf);
                 if (QOS) {
                     const int c1 = Tm - Tp;   // inner S' must be <= c1
-                    int lo = 0, hi = Lin;     // khi = #{k : ssort[k] <= c1}
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (ssort[mid] <= c1) lo = mid + 1; else hi = mid;
+                    if (c1 < s0) khi = 0;
+                    else if (khi_ok) khi = (c1 - s0 >= P1_TABN) ? Lin : (int)khi_tab[min(c1 - s0, ssort[Lin - 1] - s0)];
+                    else {
+                        int lo = 0, hi = Lin;
+                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (ssort[mid] <= c1) lo = mid + 1; else hi = mid; }
+                        khi = lo;
                     }
-                    khi = lo;
-                    clean = (float)Tp <= uminp[khi];
-                    use = khi > 0;
+                    if (Tp <= u0v) klo = 0;
+                    else if (Tp > usuf[Lin - 1]) klo = Lin;
+                    else if (klo_ok) klo = (int)klo_tab[Tp - u0v];
+                    else {
+                        int lo = 0, hi = Lin;
+                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (usuf[mid] >= Tp) hi = mid; else lo = mid + 1; }
+                        klo = lo;
+                    }
+                    // levels before klo: none qualifies unless u is non-monotone there (rare)
+                    const bool pre = umaxp[min(klo, khi)] >= Tp;
+                    use = khi > klo || pre;
+                    if (pre) klo = -1 - klo;   // flag: sweep [0, |klo|) with a mask first
                 }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, use);
             if (use) {
                 const int pos = nc + __popc(bal & ((1u << wl) - 1u));
                 tab[pos] = ent;
-                tabk[pos] = make_int2(khi, clean);
+                tabk[pos] = make_int2(klo, khi);
             }
             nc += __popc(bal);
             if (__all_sync(0xffffffffu, past)) break;   // the rest of the sorted segment is unusable
@@ -497,48 +552,48 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         float m0 = INFINITY, m1 = INFINITY;
         for (int i = wl; i < nc; i += 32) {
             const float4 t4 = tab[i];
-            const int2 kk = tabk[i];
+            int2 kk = tabk[i];
+            if (QOS && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
+                kk.x = -1 - kk.x;
+                const int kend = min(kk.x, kk.y);
+                for (int k = 0; k < kend; k++) {
+                    const float4 r = ip[k >> 1];
+                    const float2 uu2 = iu[k >> 1];
+                    const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) { const float2 dd = iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
+                    if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
+                }
+            }
+            const int ka = max(kk.x, 0), kb2 = kk.y;
+            if (ka >= kb2) continue;
+            nfeas += (unsigned long long)(kb2 - ka);
             const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
-            const int np = kk.x >> 1;
-            const bool masked = QOS && !kk.y;
-            if (!masked) {
-                int p = 0;
+            int k = ka;
+            if (k & 1) {   // leading odd element
+                const float4 r = ip[k >> 1];
+                float b0 = t4.x;
+                if (MODE == M_PAPER) b0 += iD[k >> 1].y;
+                m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
+                k++;
+            }
+            const int pend = kb2 >> 1;
 #pragma unroll 4
-                for (; p < np; p++) {
-                    const float4 r = ip[p];
-                    u64 base = X2;
-                    if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
-                    const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
-                    float k0, k1;
-                    f2unpack(key, k0, k1);
-                    if (p & 1) m1 = fminf(m1, fminf(k0, k1));
-                    else m0 = fminf(m0, fminf(k0, k1));
-                }
-                if (kk.x & 1) {   // odd tail: first element of pair np
-                    const float4 r = ip[np];
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) b0 += iD[np].x;
-                    m0 = fminf(m0, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
-                }
-            } else {
-                const float Tpf = t4.w;
-                for (int p = 0; p < np; p++) {
-                    const float4 r = ip[p];
-                    const float2 uu2 = iu[p];
-                    u64 base = X2;
-                    if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
-                    const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
-                    float k0, k1;
-                    f2unpack(key, k0, k1);
-                    if (Tpf <= uu2.x) m0 = fminf(m0, k0);
-                    if (Tpf <= uu2.y) m1 = fminf(m1, k1);
-                }
-                if (kk.x & 1) {
-                    const float4 r = ip[np];
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) b0 += iD[np].x;
-                    if (Tpf <= iu[np].x) m0 = fminf(m0, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
-                }
+            for (int p = k >> 1; p < pend; p++) {
+                const float4 r = ip[p];
+                u64 base = X2;
+                if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+                float k0, k1;
+                f2unpack(key, k0, k1);
+                if (p & 1) m1 = fminf(m1, fminf(k0, k1));
+                else m0 = fminf(m0, fminf(k0, k1));
+            }
+            if (kb2 & 1) {  // trailing odd element
+                const float4 r = ip[kb2 >> 1];
+                float b0 = t4.x;
+                if (MODE == M_PAPER) b0 += iD[kb2 >> 1].x;
+                m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
             }
         }
         float m = fminf(m0, m1);
@@ -546,6 +601,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (wl == 0) submin[(size_t)prob * su.units_max + unit] = m;
         __syncwarp();   // the table is rewritten for the next unit
     }
+    for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
+    if (wl == 0 && nfeas) atomicAdd(feasible, nfeas);
 }
 
 // Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
@@ -672,7 +729,7 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
 // ------------------------------------------------------------------------------------------
 // pass-1 dispatch
 // ------------------------------------------------------------------------------------------
-typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*);
+typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*, unsigned long long*);
 typedef void (*P1Gen)(Setup, const Prob*, const Lev*, float*, float*);
 
 template <int NP, int MODE>
@@ -716,7 +773,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
                                      : (qos ? k_pass1_fast<M_PAPER, true> : k_pass1_fast<M_PAPER, false>);
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin);
+        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible);
     } else {
         P1Gen f = nullptr;
         switch (NP) {

@@ -75,7 +75,7 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_profiles_info", "eclip_last_error", "eclip_version", "eclip_default_options", "eclip_plan",
            "eclip_plan_batch", "eclip_session_create", "eclip_session_pass1", "eclip_session_pass2_min",
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
-           "eclip_session_create_problem", "eclip_session_finish_problem"]
+           "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats"]
 
 
 def lib():
@@ -106,6 +106,7 @@ def lib():
         L.eclip_session_pass2_first.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
         L.eclip_session_finish.argtypes = [vp, P(C.c_uint64), P(BatchOut)]
         L.eclip_session_finish_problem.argtypes = [vp, P(C.c_uint64), P(Result)]
+        L.eclip_session_stats.argtypes = [vp, P(C.c_uint64)]
         L.eclip_session_free.argtypes = [vp]
         L.eclip_session_free.restype = None
         _lib = L
@@ -422,6 +423,12 @@ class Session:
         b = _batch_out_struct(out)
         _check(lib().eclip_session_finish(self._h, _ptr(g, C.c_uint64), C.byref(b)))
         return out
+
+    def stats(self) -> dict:
+        """counters of the last pass 1 (evaluated = QoS-feasible candidates scored in FP32)"""
+        v = C.c_uint64()
+        _check(lib().eclip_session_stats(self._h, C.byref(v)))
+        return {"evaluated_candidates": int(v.value)}
 
     def close(self):
         if self._h is not None and self._h.value:
