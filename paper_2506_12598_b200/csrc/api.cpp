@@ -556,7 +556,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     const long double units = H * nseg;
     const long double cand_unit = (long double)seglen * Lmax;
     long double target = n * units / 592.0L;                    // >= 2 CTAs per SM, 2 waves
-    long double upi = std::min<long double>(target, std::max<long double>(1, 4194304.0L / cand_unit));
+    long double upi = std::min<long double>(target, std::max<long double>(1, 16777216.0L / cand_unit));
     upi = std::max<long double>(upi, teams_typ);
     upi = std::ceil(upi / teams_typ) * teams_typ;
     su.nseg = nseg;

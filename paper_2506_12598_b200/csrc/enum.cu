@@ -420,44 +420,26 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (MODE == M_PAPER) iD[p] = make_float2((float)((double)a.BS * invd), (float)((double)b.BS * invd));
     }
     for (int k = threadIdx.x; k < Lin; k += blockDim.x) ssort[k] = inner[perm[k]].S;
-    if (threadIdx.x == 0) {
-        int m = 1 << 30;
-        usuf[Lin] = m;
-        for (int k = Lin - 1; k >= 0; k--) {
-            m = min(m, inner[perm[k]].Tmax - inner[perm[k]].S);
-            usuf[k] = m;
-        }
-        int M = -(1 << 30);
-        umaxp[0] = M;
-        for (int k = 0; k < Lin; k++) {
-            M = max(M, inner[perm[k]].Tmax - inner[perm[k]].S);
-            umaxp[k + 1] = M;
-        }
-        sh_range[0] = ssort[0];
-        sh_range[1] = ssort[Lin - 1] - ssort[0] + 1 <= P1_TABN;         // k_hi table usable
-        sh_range[2] = usuf[0];
-        sh_range[3] = usuf[Lin - 1] - usuf[0] + 1 <= P1_TABN;           // k_lo table usable
+    __syncthreads();
+    // suffix minimum / prefix maximum of u in S' order (O(L^2) / threads, no serial section)
+    for (int k = threadIdx.x; k <= Lin; k += blockDim.x) {
+        int mn = 1 << 30, mx = -(1 << 30);
+        for (int j = k; j < Lin; j++) mn = min(mn, inner[perm[j]].Tmax - ssort[j]);
+        for (int j = 0; j < k; j++) mx = max(mx, inner[perm[j]].Tmax - ssort[j]);
+        usuf[k] = mn;
+        umaxp[k] = mx;
     }
     __syncthreads();
-    const int s0 = sh_range[0], u0v = sh_range[2];
-    const bool khi_ok = sh_range[1] != 0, klo_ok = sh_range[3] != 0;
-    // khi_tab[v - s0] = #{k : S'_k <= v};  klo_tab[v - u0] = min{k : usuf[k] >= v}
-    if (khi_ok) {
-        const int n = ssort[Lin - 1] - s0 + 1;
-        for (int v = threadIdx.x; v < n; v += blockDim.x) {
-            int lo = 0, hi = Lin;
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (ssort[mid] <= s0 + v) lo = mid + 1; else hi = mid; }
-            khi_tab[v] = (uint16_t)lo;
-        }
-    }
-    if (klo_ok) {
-        const int n = usuf[Lin - 1] - u0v + 1;
-        for (int v = threadIdx.x; v < n; v += blockDim.x) {
-            int lo = 0, hi = Lin;
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (usuf[mid] >= u0v + v) hi = mid; else lo = mid + 1; }
-            klo_tab[v] = (uint16_t)lo;
-        }
-    }
+    const int s0 = ssort[0], u0v = usuf[0];
+    const bool khi_ok = ssort[Lin - 1] - s0 + 1 <= P1_TABN, klo_ok = usuf[Lin - 1] - u0v + 1 <= P1_TABN;
+    // khi_tab[v - s0] = #{k : S'_k <= v}: value k on [S'_{k-1}, S'_k)  (interval fill)
+    // klo_tab[v - u0] = min{k : usuf[k] >= v}: value k on (usuf[k-1], usuf[k]]
+    if (khi_ok)
+        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
+            for (int v = ssort[k]; v < (k + 1 < Lin ? ssort[k + 1] : ssort[k] + 1); v++) khi_tab[v - s0] = (uint16_t)(k + 1);
+    if (klo_ok)
+        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
+            for (int v = (k == 0 ? usuf[0] : usuf[k - 1] + 1); v <= usuf[k]; v++) klo_tab[v - u0v] = (uint16_t)k;
     __syncthreads();
     const int smin_i = ssort[0], umax_i = umaxp[Lin];
 
@@ -480,7 +462,14 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         // step level e is usable only if  s_e <= sb  (a prefix of the sorted order) and
         // Tmax_e - s_e - hT >= min_k S'_k
         int sb = 1 << 30;
-        if (QOS) sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
+        if (QOS) {
+            sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
+            // the smallest step level of this unit is already too large: nothing is feasible
+            if (W >= 2 && stepw[sperm[e0]].S > sb) {
+                if (wl == 0) submin[(size_t)prob * su.units_max + unit] = INFINITY;
+                continue;
+            }
+        }
         int nc = 0;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
