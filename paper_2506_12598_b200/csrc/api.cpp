@@ -543,7 +543,8 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
         s->engine = want;
     }
     if (s->engine != ECLIP_ENGINE_ENUM) {
-        su.nseg = 1; su.upi = 1; su.units_max = 1; su.items_max = 1; su.table_bytes = 0;
+        su.nseg = 1; su.upi = 1; su.units_max = 1; su.items_max = 1; su.table_bytes = 0; su.aux_bytes = 0;
+        su.lev_stride = W * Lmax;
         return ECLIP_OK;
     }
     const int Lstep = W >= 2 ? Lmax : 1;
@@ -564,11 +565,12 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.units_max = (int64_t)units;
     su.items_max = (int32_t)std::ceil(units / su.upi);
     su.table_bytes = 0;
-    if (fast) {   // inner pairs + sorted S' / suffix-min / prefix-max + perms + 2 lookup tables + per-warp tables
-        size_t b = ((size_t)(Lmax + 1) / 2) * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 2 * (size_t)P1_TABN * 2;
-        b = (b + 15) / 16 * 16;
-        su.table_bytes = (int32_t)(b + (size_t)(P1_THREADS / 32) * seglen * 24);
+    su.aux_bytes = 0;
+    if (fast) {   // per-problem aux block (staged with the Lev records) + per-warp prefix tables
+        su.aux_bytes = (int32_t)pass1_aux_bytes(Lmax);
+        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * seglen * 24);
     }
+    su.lev_stride = W * Lmax + su.aux_bytes / (int)sizeof(Lev);
     return ECLIP_OK;
 }
 
@@ -577,7 +579,7 @@ static int alloc_work(eclip_session* s) {
     Work& wk = s->wk;
     const size_t n = (size_t)su.n_problems;
     CU(s->arena.alloc(&wk.probs, n));
-    CU(s->arena.alloc(&wk.levs, n * su.W * su.Lmax));
+    CU(s->arena.alloc(&wk.levs, n * (size_t)su.lev_stride));
     if (s->engine == ECLIP_ENGINE_ENUM) {
         size_t ns = n * (size_t)su.units_max;
         CU(s->arena.alloc(&wk.submin, ns));

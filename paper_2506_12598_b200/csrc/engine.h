@@ -93,7 +93,9 @@ struct Setup {
     int32_t nseg;               // segments per row (units = rows x nseg)
     int32_t upi;                // units per pass-1 item (CTA)
     int64_t units_max;          // max units over problems (submin stride)
-    int32_t table_bytes;        // fast pass-1 per-CTA prefix-table budget
+    int32_t table_bytes;        // fast pass-1 per-CTA table budget (per-warp prefix tables)
+    int32_t aux_bytes;          // fast pass-1 per-problem aux block (after the Lev records)
+    int32_t lev_stride;         // Lev records per problem block (W*Lmax + aux_bytes/32)
     int32_t pad1;
     int32_t shard, n_shards;
     uint64_t tol_num, tol_den;
@@ -152,5 +154,6 @@ cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, cons
 size_t pass1_smem(const Setup& su, bool fast);
 bool pass1_fast(int L_inner);
 int pass1_fast_team(int L_inner);
+size_t pass1_aux_bytes(int Lmax);
 
 }  // namespace eclip

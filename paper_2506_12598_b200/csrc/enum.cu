@@ -268,6 +268,7 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
     const Prob& P = probs[p];
     Lev r;
     r.B = 0; r.BS = 0; r.S = 0; r.Tmax = -1; r.Bk = 0.0f; r.pad = 0;
+    Lev* dst = levs + (size_t)p * su.lev_stride + (size_t)w * su.Lmax + l;
     if (P.status >= 0 && l < P.L[w]) {
         int t = P.table[w];
         int64_t B = tb.B[t][l];
@@ -293,7 +294,102 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
         }
         r.Tmax = (int32_t)T;
     }
-    levs[i] = r;
+    *dst = r;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// fast pass-1 aux block (per problem, right after its Lev records; staged with them)
+//   ip    float4[LP]   inner levels sorted by S', in pairs {B_k, B_k+1, S'_k, S'_k+1}
+//   iu    float2[LP]   {u_k, u_k+1},  u = Tmax - S'  (inner worker's own QoS: Tp <= u)
+//   iD    float2[LP]   PAPER: {B_k S'_k/(Lambda N), ...}
+//   ssort int[Lmax+1]  sorted S';  usuf int[Lmax+1] suffix min of u;  umaxp int[Lmax+1] prefix max
+//   perm  u16[Lmax]    inner sorted by S';  sperm u16[Lmax] step worker sorted by S' per segment
+//   khi   u16[TABN]    #{k : S'_k <= s0 + v};   klo u16[TABN]  min{k : usuf[k] >= u0 + v}
+//   hdr   int[4]       s0, u0, khi_ok, klo_ok
+// ------------------------------------------------------------------------------------------
+struct AuxView {
+    float4* ip; float2* iu; float2* iD; int* ssort; int* usuf; int* umaxp; uint16_t* perm; uint16_t* sperm;
+    uint16_t* khi; uint16_t* klo; int* hdr;
+};
+__host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
+    const size_t LP = (size_t)(Lmax + 1) / 2;
+    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 16;
+    return (b + 31) / 32 * 32;
+}
+size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
+__device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
+    AuxView a;
+    const int LP = (Lmax + 1) / 2;
+    a.ip = reinterpret_cast<float4*>(base);
+    a.iu = reinterpret_cast<float2*>(a.ip + LP);
+    a.iD = a.iu + LP;
+    a.ssort = reinterpret_cast<int*>(a.iD + LP);
+    a.usuf = a.ssort + (Lmax + 1);
+    a.umaxp = a.usuf + (Lmax + 1);
+    a.perm = reinterpret_cast<uint16_t*>(a.umaxp + (Lmax + 1));
+    a.sperm = a.perm + Lmax;
+    a.khi = a.sperm + Lmax;
+    a.klo = a.khi + P1_TABN;
+    a.hdr = reinterpret_cast<int*>(a.klo + P1_TABN);
+    return a;
+}
+
+// one CTA per problem: sort, pair up, and tabulate the inner / step workers once
+template <int MODE>
+__global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, Lev* levs) {
+    const int prob = blockIdx.x;
+    const Prob& P = probs[prob];
+    if (P.status != 0) return;
+    const int W = su.W, Lmax = su.Lmax;
+    Lev* base = levs + (size_t)prob * su.lev_stride;
+    const Lev* inner = base + (W - 1) * Lmax;
+    const Lev* stepw = base + (W >= 2 ? (W - 2) : 0) * Lmax;
+    AuxView A = aux_view(reinterpret_cast<unsigned char*>(base + (size_t)W * Lmax), Lmax);
+    const int Lin = P.L[W - 1], Lst = P.Lstep, segl = P.seglen;
+    const double invd = 1.0 / (double)P.lamN;
+    for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
+        const int si = inner[i].S;
+        int rk = 0;
+        for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
+        A.perm[rk] = (uint16_t)i;
+    }
+    if (W >= 2) {
+        for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
+            const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
+            const int si = stepw[i].S;
+            int rk = 0;
+            for (int j = b0; j < b1; j++) rk += stepw[j].S < si;
+            A.sperm[b0 + rk] = (uint16_t)i;
+        }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < (Lin + 1) / 2; p += blockDim.x) {
+        const Lev& a = inner[A.perm[2 * p]];
+        const Lev& b = inner[A.perm[min(2 * p + 1, Lin - 1)]];
+        A.ip[p] = make_float4(__ll2float_rn(a.B), __ll2float_rn(b.B), (float)a.S, (float)b.S);
+        A.iu[p] = make_float2((float)(a.Tmax - a.S), (float)(b.Tmax - b.S));
+        if (MODE == M_PAPER) A.iD[p] = make_float2((float)((double)a.BS * invd), (float)((double)b.BS * invd));
+    }
+    for (int k = threadIdx.x; k < Lin; k += blockDim.x) A.ssort[k] = inner[A.perm[k]].S;
+    __syncthreads();
+    for (int k = threadIdx.x; k <= Lin; k += blockDim.x) {
+        int mn = 1 << 30, mx = -(1 << 30);
+        for (int j = k; j < Lin; j++) mn = min(mn, inner[A.perm[j]].Tmax - A.ssort[j]);
+        for (int j = 0; j < k; j++) mx = max(mx, inner[A.perm[j]].Tmax - A.ssort[j]);
+        A.usuf[k] = mn;
+        A.umaxp[k] = mx;
+    }
+    __syncthreads();
+    const int s0 = A.ssort[0], u0 = A.usuf[0];
+    const bool khi_ok = A.ssort[Lin - 1] - s0 + 1 <= P1_TABN, klo_ok = A.usuf[Lin - 1] - u0 + 1 <= P1_TABN;
+    if (khi_ok)
+        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
+            for (int v = A.ssort[k]; v < (k + 1 < Lin ? A.ssort[k + 1] : A.ssort[k] + 1); v++) A.khi[v - s0] = (uint16_t)(k + 1);
+    if (klo_ok)
+        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
+            for (int v = (k == 0 ? A.usuf[0] : A.usuf[k - 1] + 1); v <= A.usuf[k]; v++) A.klo[v - u0] = (uint16_t)k;
+    if (threadIdx.x == 0) { A.hdr[0] = s0; A.hdr[1] = u0; A.hdr[2] = khi_ok; A.hdr[3] = klo_ok; }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -354,7 +450,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
              unsigned long long* __restrict__ feasible) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
-    __shared__ int sh_range[4];
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
     const int prob = blockIdx.x / ipS;
     const Prob& P = probs[prob];
@@ -365,83 +460,24 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     if (!ok) return;
     const int W = su.W, Lmax = su.Lmax;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
-    stage_levels(sl, levs + (size_t)prob * W * Lmax, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
+    // level records + this problem's aux block in one TMA bulk copy
+    stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
+    const AuxView A = aux_view(smem_raw + (size_t)W * Lmax * sizeof(Lev), Lmax);
 
     int L[MAXW_ENUM];
     for (int w = 0; w < W; w++) L[w] = P.L[w];
     const int Lin = L[W - 1];
-    const int npair = (Lin + 1) / 2;
-    const Lev* inner = sl + (W - 1) * Lmax;
     const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
-    const int Lst = P.Lstep, segl = P.seglen;
-    // ---- shared layout after the staged records (host: pass1 table_bytes)
-    const int LP = (Lmax + 1) / 2;
-    unsigned char* p0 = smem_raw + (size_t)W * Lmax * sizeof(Lev);
-    float4* ip = reinterpret_cast<float4*>(p0);                 // [LP] {B_k, B_k+1, S_k, S_k+1}
-    float2* iu = reinterpret_cast<float2*>(ip + LP);             // [LP] {u_k, u_k+1}
-    float2* iD = iu + LP;                                        // [LP] PAPER: {D_k, D_k+1}
-    int* ssort = reinterpret_cast<int*>(iD + LP);                // [Lmax+1] sorted S'
-    int* usuf = ssort + (Lmax + 1);                              // [Lmax+1] suffix min of u (usuf[Lin] = +big)
-    int* umaxp = usuf + (Lmax + 1);                              // [Lmax+1] prefix max of u
-    uint16_t* perm = reinterpret_cast<uint16_t*>(umaxp + (Lmax + 1));   // [Lmax] inner sorted by S'
-    uint16_t* sperm = perm + Lmax;                                       // [Lmax] step sorted by S' per segment
-    uint16_t* khi_tab = sperm + Lmax;                                    // [TABN]
-    uint16_t* klo_tab = khi_tab + P1_TABN;                               // [TABN]
-    float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + (size_t)su.table_bytes -
-                                             (size_t)(P1_THREADS / 32) * segl * 24);
+    const int segl = P.seglen;
+    float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + su.aux_bytes);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
-    float4* tab = tab0 + (size_t)warp * segl;                                                           // {X,Y,Z,Tp}
+    float4* tab = tab0 + (size_t)warp * segl;                                                             // {X,Y,Z,Tp}
     int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)(P1_THREADS / 32) * segl) + (size_t)warp * segl;  // {k_lo, k_hi}
-
     const float invf = P.inv;
     const double invd = 1.0 / (double)P.lamN;
-    // ---- sort inner levels and the step worker's segments by S'
-    for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
-        const int si = inner[i].S;
-        int rk = 0;
-        for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
-        perm[rk] = (uint16_t)i;
-    }
-    if (W >= 2) {
-        for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
-            const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
-            const int si = stepw[i].S;
-            int rk = 0;
-            for (int j = b0; j < b1; j++) rk += stepw[j].S < si;
-            sperm[b0 + rk] = (uint16_t)i;
-        }
-    }
-    __syncthreads();
-    for (int p = threadIdx.x; p < npair; p += blockDim.x) {
-        const Lev& a = inner[perm[2 * p]];
-        const Lev& b = inner[perm[min(2 * p + 1, Lin - 1)]];
-        ip[p] = make_float4(__ll2float_rn(a.B), __ll2float_rn(b.B), (float)a.S, (float)b.S);
-        iu[p] = make_float2((float)(a.Tmax - a.S), (float)(b.Tmax - b.S));
-        if (MODE == M_PAPER) iD[p] = make_float2((float)((double)a.BS * invd), (float)((double)b.BS * invd));
-    }
-    for (int k = threadIdx.x; k < Lin; k += blockDim.x) ssort[k] = inner[perm[k]].S;
-    __syncthreads();
-    // suffix minimum / prefix maximum of u in S' order (O(L^2) / threads, no serial section)
-    for (int k = threadIdx.x; k <= Lin; k += blockDim.x) {
-        int mn = 1 << 30, mx = -(1 << 30);
-        for (int j = k; j < Lin; j++) mn = min(mn, inner[perm[j]].Tmax - ssort[j]);
-        for (int j = 0; j < k; j++) mx = max(mx, inner[perm[j]].Tmax - ssort[j]);
-        usuf[k] = mn;
-        umaxp[k] = mx;
-    }
-    __syncthreads();
-    const int s0 = ssort[0], u0v = usuf[0];
-    const bool khi_ok = ssort[Lin - 1] - s0 + 1 <= P1_TABN, klo_ok = usuf[Lin - 1] - u0v + 1 <= P1_TABN;
-    // khi_tab[v - s0] = #{k : S'_k <= v}: value k on [S'_{k-1}, S'_k)  (interval fill)
-    // klo_tab[v - u0] = min{k : usuf[k] >= v}: value k on (usuf[k-1], usuf[k]]
-    if (khi_ok)
-        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
-            for (int v = ssort[k]; v < (k + 1 < Lin ? ssort[k + 1] : ssort[k] + 1); v++) khi_tab[v - s0] = (uint16_t)(k + 1);
-    if (klo_ok)
-        for (int k = threadIdx.x; k < Lin; k += blockDim.x)
-            for (int v = (k == 0 ? usuf[0] : usuf[k - 1] + 1); v <= usuf[k]; v++) klo_tab[v - u0v] = (uint16_t)k;
-    __syncthreads();
-    const int smin_i = ssort[0], umax_i = umaxp[Lin];
+    const int s0 = A.hdr[0], u0v = A.hdr[1];
+    const bool khi_ok = A.hdr[2] != 0, klo_ok = A.hdr[3] != 0;
+    const int smin_i = A.ssort[0], umax_i = A.umaxp[Lin], slast = A.ssort[Lin - 1], ulast = A.usuf[Lin - 1];
 
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
@@ -459,28 +495,37 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         const HiSums h = hi_sums(sl, Lmax, d, W);
         const int ne = e1 - e0;
-        // step level e is usable only if  s_e <= sb  (a prefix of the sorted order) and
-        // Tmax_e - s_e - hT >= min_k S'_k
         int sb = 1 << 30;
         if (QOS) {
             sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
-            // the smallest step level of this unit is already too large: nothing is feasible
-            if (W >= 2 && stepw[sperm[e0]].S > sb) {
+            if (W >= 2 && stepw[A.sperm[e0]].S > sb) {   // even the smallest step level is infeasible
                 if (wl == 0) submin[(size_t)prob * su.units_max + unit] = INFINITY;
                 continue;
             }
         }
+        // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
+        //   X_e = Xh + B_e Yh + S'_e Zh (+ D_e for PAPER),  Y_e = Yh + S'_e inv,  Z_e = Zh + B_e inv
+        const double hBd = (double)h.B;
+        const float Yh = (float)(1.0 + (double)h.T * invd), Zh = (float)(hBd * invd);
+        float Xh;
+        if (MODE == M_EXCL) Xh = (float)(hBd + (double)((u128)h.T * (u128)h.B - (u128)h.BS) * invd);
+        else Xh = (float)(hBd * (1.0 + (double)h.T * invd));
         int nc = 0;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
             bool use = false, past = true;
-            int e = 0;
+            int Sp = 0, Tme = 1 << 24;
+            float Be = 0.0f, De = 0.0f;
             if (k < ne) {
                 if (W >= 2) {
-                    e = (int)sperm[e0 + k];
-                    const Lev& r = stepw[e];
+                    const Lev& r = stepw[A.sperm[e0 + k]];
+                    Sp = r.S; Tme = r.Tmax;
                     past = QOS && r.S > sb;
                     use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_i));
+                    if (use) {
+                        Be = __ll2float_rn(r.B);
+                        if (MODE == M_PAPER) De = (float)((double)r.BS * invd);
+                    }
                 } else {
                     past = false;
                     use = true;
@@ -489,41 +534,31 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
             int klo = 0, khi = Lin;
             if (use) {
-                int64_t Bp = h.B, BSp = h.BS;
-                int32_t Tp = h.T, Tm = h.Tm;
-                if (W >= 2) {
-                    const Lev& r = stepw[e];
-                    Bp += r.B; BSp += r.BS; Tp += r.S; Tm = min(Tm, r.Tmax);
-                }
-                const float Bpf = __ll2float_rn(Bp), Tpf = (float)Tp;
-                float X;
-                if (MODE == M_EXCL) {
-                    const u128 Dn = (u128)Tp * (u128)Bp - (u128)BSp;   // = sum_w B_w (Tp - S'_w) >= 0
-                    const float Df = (Dn >> 64) ? (float)(double)Dn : __ull2float_rn((unsigned long long)Dn);
-                    X = fmaf(Df, invf, Bpf);
-                } else {
-                    X = Bpf * fmaf(Tpf, invf, 1.0f);
-                }
-                ent = make_float4(X, fmaf(Tpf, invf, 1.0f), Bpf * invf, Tpf);
+                const int Tp = h.T + Sp, Tm = min(h.Tm, Tme);
+                const float Sf = (float)Sp;
+                float X = fmaf(Be, Yh, fmaf(Sf, Zh, Xh));
+                if (MODE == M_PAPER) X += De;
+                ent = make_float4(X, fmaf(Sf, invf, Yh), fmaf(Be, invf, Zh), (float)Tp);
                 if (QOS) {
                     const int c1 = Tm - Tp;   // inner S' must be <= c1
                     if (c1 < s0) khi = 0;
-                    else if (khi_ok) khi = (c1 - s0 >= P1_TABN) ? Lin : (int)khi_tab[min(c1 - s0, ssort[Lin - 1] - s0)];
+                    else if (c1 >= slast) khi = Lin;
+                    else if (khi_ok) khi = (int)A.khi[c1 - s0];
                     else {
                         int lo = 0, hi = Lin;
-                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (ssort[mid] <= c1) lo = mid + 1; else hi = mid; }
+                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.ssort[mid] <= c1) lo = mid + 1; else hi = mid; }
                         khi = lo;
                     }
                     if (Tp <= u0v) klo = 0;
-                    else if (Tp > usuf[Lin - 1]) klo = Lin;
-                    else if (klo_ok) klo = (int)klo_tab[Tp - u0v];
+                    else if (Tp > ulast) klo = Lin;
+                    else if (klo_ok) klo = (int)A.klo[Tp - u0v];
                     else {
                         int lo = 0, hi = Lin;
-                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (usuf[mid] >= Tp) hi = mid; else lo = mid + 1; }
+                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.usuf[mid] >= Tp) hi = mid; else lo = mid + 1; }
                         klo = lo;
                     }
                     // levels before klo: none qualifies unless u is non-monotone there (rare)
-                    const bool pre = umaxp[min(klo, khi)] >= Tp;
+                    const bool pre = A.umaxp[min(klo, khi)] >= Tp;
                     use = khi > klo || pre;
                     if (pre) klo = -1 - klo;   // flag: sweep [0, |klo|) with a mask first
                 }
@@ -546,11 +581,11 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 kk.x = -1 - kk.x;
                 const int kend = min(kk.x, kk.y);
                 for (int k = 0; k < kend; k++) {
-                    const float4 r = ip[k >> 1];
-                    const float2 uu2 = iu[k >> 1];
+                    const float4 r = A.ip[k >> 1];
+                    const float2 uu2 = A.iu[k >> 1];
                     const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
                     float b0 = t4.x;
-                    if (MODE == M_PAPER) { const float2 dd = iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
+                    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
                     if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
                 }
             }
@@ -560,18 +595,18 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
             int k = ka;
             if (k & 1) {   // leading odd element
-                const float4 r = ip[k >> 1];
+                const float4 r = A.ip[k >> 1];
                 float b0 = t4.x;
-                if (MODE == M_PAPER) b0 += iD[k >> 1].y;
+                if (MODE == M_PAPER) b0 += A.iD[k >> 1].y;
                 m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
                 k++;
             }
             const int pend = kb2 >> 1;
 #pragma unroll 4
             for (int p = k >> 1; p < pend; p++) {
-                const float4 r = ip[p];
+                const float4 r = A.ip[p];
                 u64 base = X2;
-                if (MODE == M_PAPER) { const float2 dd = iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                if (MODE == M_PAPER) { const float2 dd = A.iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
                 const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
                 float k0, k1;
                 f2unpack(key, k0, k1);
@@ -579,9 +614,9 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 else m0 = fminf(m0, fminf(k0, k1));
             }
             if (kb2 & 1) {  // trailing odd element
-                const float4 r = ip[kb2 >> 1];
+                const float4 r = A.ip[kb2 >> 1];
                 float b0 = t4.x;
-                if (MODE == M_PAPER) b0 += iD[kb2 >> 1].x;
+                if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
                 m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
             }
         }
@@ -613,7 +648,7 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
     constexpr int W = NP + 1;
     const int Lmax = su.Lmax;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
-    stage_levels(sl, levs + (size_t)prob * W * Lmax, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
+    stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
     int L[W];
 #pragma unroll
     for (int w = 0; w < W; w++) L[w] = P.L[w];
@@ -745,7 +780,7 @@ static bool use_fast(const Setup& su) {
 
 size_t pass1_smem(const Setup& su, bool fast) {
     size_t s = (size_t)su.W * su.Lmax * sizeof(Lev);
-    if (fast) s += (size_t)su.table_bytes;   // per-warp prefix tables
+    if (fast) s += (size_t)su.aux_bytes + (size_t)su.table_bytes;   // aux block + per-warp prefix tables
     return s;
 }
 
@@ -934,7 +969,7 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
         return;
     }
     const int W = su.W;
-    stage_levels(sl, levs + (size_t)prob * W * su.Lmax, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
+    stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * su.Lmax * sizeof(Lev)), &bar);
     const float bound = band_bound(su, m32[prob], m32_sure ? m32_sure[prob] : m32[prob]);
     const int Lin = P.L[W - 1];
     uint64_t slo, shi;
@@ -1146,7 +1181,7 @@ __global__ void k_materialize(Setup su, Tables tb, const Prob* probs, const Lev*
     if (o.thr) o.thr[p] = thr;
     if (o.key) {
         U256 k;
-        exact_key(su, P, levs + (size_t)p * W * su.Lmax, lv, k);
+        exact_key(su, P, levs + (size_t)p * su.lev_stride, lv, k);
         for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
     }
 }
@@ -1164,6 +1199,10 @@ cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Wor
     k_prep_prob<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, in, wk.probs);
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
+    if (su.aux_bytes > 0) {
+        if (su.mode == M_PAPER) k_prep_aux<M_PAPER><<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.levs);
+        else k_prep_aux<M_EXCL><<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.levs);
+    }
     return cudaGetLastError();
 }
 

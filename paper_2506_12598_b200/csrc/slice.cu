@@ -40,8 +40,14 @@ __device__ __forceinline__ int64_t overlap_exact(int mode, int64_t Tp, int64_t S
 }
 
 // ------------------------------------------------------------------------------------------
-// K3: FP32 filter DP, one CTA per slice (interleaved over shards)
+// K3: FP32 filter DP, one CTA per slice (interleaved over shards).
+// D buffers carry PAD = max level span of +inf on both sides, so the inner (min,+) loop has no
+// bounds checks; each thread owns RB consecutive outputs P and slides a window of RB D values
+// over k (one shared load of g[k] and one of D per k for RB lattice points).
 // ------------------------------------------------------------------------------------------
+constexpr int RB = 8;
+
+template <int OBJ>
 __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob* probs, const Lev* __restrict__ levs,
                                                           const int16_t* __restrict__ dense, float* J32,
                                                           unsigned long long* units) {
@@ -51,9 +57,11 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
     int64_t T = S.Tlo + S.shard + (int64_t)S.n_shards * blockIdx.x;
     if (T > S.Thi) return;
     const int W = S.W;
+    const int PAD = S.pad;
+    const int BUF = S.maxrange + 2 * PAD + RB;
     float* g = sm;                       // [gtot]
-    float* Da = g + S.gtot;              // [maxrange]
-    float* Db = Da + S.maxrange;         // [maxrange]
+    float* Da = g + S.gtot + PAD;        // [-PAD, maxrange + PAD + RB)
+    float* Db = Da + BUF;
     const int64_t Tp = T * S.gS;
     const float Tpf = (float)Tp;
     for (int i = threadIdx.x; i < S.gtot; i += blockDim.x) {
@@ -70,6 +78,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
         }
         g[i] = v;
     }
+    for (int i = threadIdx.x; i < 2 * BUF; i += blockDim.x) Da[i - PAD] = INFINITY;
     __syncthreads();
     float* Dn = Da;   // D_{w+1}
     float* Dc = Db;   // D_w
@@ -84,21 +93,42 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
             drange(S, T, w, &lo, &hi);
             const float* gw2 = g + S.doff[w];
             const int nk = S.smax[w] - S.smin[w] + 1;
-            for (int64_t p = lo + threadIdx.x; p <= hi; p += blockDim.x) {
-                float best = INFINITY;
-                // rest = p - smin_w - k must lie in [nlo, nhi]
-                int64_t k0 = p - S.smin[w] - nhi, k1 = p - S.smin[w] - nlo;
-                int ka = (int)(k0 > 0 ? k0 : 0), kb = (int)(k1 < nk - 1 ? k1 : nk - 1);
-                const float* dn = Dn + (p - S.smin[w] - nlo);
-                if (kb >= ka) cnt += (unsigned long long)(kb - ka + 1);
-                for (int k = ka; k <= kb; k++) {
-                    float v = (S.obj == O_SUM) ? gw2[k] + dn[-k] : fmaxf(gw2[k], dn[-k]);
-                    best = fminf(best, v);
+            const int np = (int)(hi - lo + 1);
+            for (int c = threadIdx.x * RB; c < np; c += blockDim.x * RB) {
+                // outputs p = lo + c + j (j < RB) read Dn[b + j - k], b = lo + c - smin_w - nlo
+                const int b = (int)(lo + c - S.smin[w] - nlo);
+                const int nprev = (int)(nhi - nlo + 1);
+                const int ks = max(0, b - (nprev - 1)), ke = min(nk, b + RB);   // k outside is +inf
+                float best[RB], win[RB];
+#pragma unroll
+                for (int j = 0; j < RB; j++) best[j] = INFINITY;
+                if (ks < ke) {
+#pragma unroll
+                    for (int j = 0; j < RB; j++) win[j] = Dn[b + j - ks];
+                    for (int k = ks; k < ke; k++) {
+                        const float gk = gw2[k];
+#pragma unroll
+                        for (int j = 0; j < RB; j++) {
+                            const float v = (OBJ == O_SUM) ? gk + win[j] : fmaxf(gk, win[j]);
+                            best[j] = fminf(best[j], v);
+                        }
+#pragma unroll
+                        for (int j = RB - 1; j > 0; j--) win[j] = win[j - 1];
+                        win[0] = Dn[b - k - 1];
+                    }
+                    cnt += (unsigned long long)(ke - ks) * RB;
                 }
-                Dc[p - lo] = best;
+#pragma unroll
+                for (int j = 0; j < RB; j++)
+                    if (c + j < np) Dc[c + j] = best[j];
             }
             __syncthreads();
+            // clear the stale tail of the buffer that becomes D_{w+1}'s neighbour next stage
+            for (int i = threadIdx.x; i < BUF; i += blockDim.x)
+                if (i - PAD < 0 || i - PAD >= np) Dc[i - PAD] = INFINITY;
             float* t = Dn; Dn = Dc; Dc = t;
+            for (int i = threadIdx.x; i < BUF; i += blockDim.x) Dc[i - PAD] = INFINITY;
+            __syncthreads();
             nlo = lo; nhi = hi;
         }
     }
@@ -114,11 +144,11 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
         } else {
             if (rest < nlo || rest > nhi) continue;
             float d = Dn[rest - nlo];
-            v = (S.obj == O_SUM) ? g[k] + d : fmaxf(g[k], d);
+            v = (OBJ == O_SUM) ? g[k] + d : fmaxf(g[k], d);
         }
         J = fminf(J, v);
-        cnt++;
     }
+    if (threadIdx.x == 0) cnt += (unsigned long long)nk0;
     if (cnt) atomicAdd(units, cnt);
     __shared__ float red[SL_THREADS];
     red[threadIdx.x] = J;
@@ -129,7 +159,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
     }
     if (threadIdx.x == 0) {
         float j = red[0];
-        if (S.obj == O_ENERGY && j < INFINITY) j = fmaf(P.p_dyn, fminf(1.0f, Tpf * P.inv), P.p_idle) * j;
+        if (OBJ == O_ENERGY && j < INFINITY) j = fmaf(P.p_dyn, fminf(1.0f, Tpf * P.inv), P.p_idle) * j;
         J32[T - S.Tlo] = j;
     }
 }
@@ -414,6 +444,9 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
             mr = std::max<int64_t>(mr, hi - lo + 1);
         }
     S.maxrange = (int32_t)mr;
+    int pad = 1;
+    for (int w = 0; w < W; w++) pad = std::max(pad, S.smax[w] - S.smin[w] + 1);
+    S.pad = pad + RB;
     CK(salloc(s, &s.d_units, 1));
     CK(salloc(s, &s.dense, dense.size()));
     CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
@@ -431,11 +464,18 @@ cudaError_t slice_pass1(SliceState& s, const Setup& su, const Tables& tb, Work& 
     (void)su; (void)tb;
     const SliceDev& S = s.h;
     int64_t mine = S.n_slices > S.shard ? (S.n_slices - S.shard + S.n_shards - 1) / S.n_shards : 0;
-    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * (size_t)S.maxrange);
+    const size_t BUF = (size_t)S.maxrange + 2 * (size_t)S.pad + RB;
+    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * BUF + 2 * (size_t)S.pad);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    CK(cudaFuncSetAttribute((const void*)k_slice_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const void* f = S.obj == O_SUM ? (const void*)k_slice_f32<O_SUM> : (S.obj == O_MAX ? (const void*)k_slice_f32<O_MAX>
+                                                                                       : (const void*)k_slice_f32<O_ENERGY>);
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaMemsetAsync(s.d_units, 0, sizeof(unsigned long long), st));
-    if (mine > 0) k_slice_f32<<<(unsigned)mine, SL_THREADS, smem, st>>>(S, wk.probs, wk.levs, s.dense, s.J32, s.d_units);
+    if (mine > 0) {
+        if (S.obj == O_SUM) k_slice_f32<O_SUM><<<(unsigned)mine, SL_THREADS, smem, st>>>(S, wk.probs, wk.levs, s.dense, s.J32, s.d_units);
+        else if (S.obj == O_MAX) k_slice_f32<O_MAX><<<(unsigned)mine, SL_THREADS, smem, st>>>(S, wk.probs, wk.levs, s.dense, s.J32, s.d_units);
+        else k_slice_f32<O_ENERGY><<<(unsigned)mine, SL_THREADS, smem, st>>>(S, wk.probs, wk.levs, s.dense, s.J32, s.d_units);
+    }
     k_slice_min<<<1, 1024, 0, st>>>(S, s.J32, wk.m32);
     return cudaGetLastError();
 }

@@ -24,6 +24,7 @@ struct SliceDev {
     int64_t slo[MAXW + 1], shi[MAXW + 1];  // suffix sums over workers w..W-1
     int32_t doff[MAXW];         // offset of worker w's dense map
     int32_t maxrange;           // max D range length
+    int32_t pad;                // +inf padding of the FP32 D buffers (max level span + RB)
     int32_t gtot;               // total dense entries
     int32_t shard, n_shards;
     uint64_t tol_num, tol_den;
