@@ -444,10 +444,11 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 //       index of the suffix-minimum of u that reaches Tp (exact when u is non-decreasing in S',
 //       i.e. B* non-increasing; otherwise the earlier levels are swept with a mask).
 // Both ends come from lookup tables indexed by value (binary search if a range is too wide).
-template <int MODE, bool QOS>
+template <int NW, int MODE, bool QOS>
 __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
              unsigned long long* __restrict__ feasible) {
+    constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
@@ -458,58 +459,85 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     bool ok;
     item_of_block(su, P, blockIdx.x % ipS, &item, &ok);
     if (!ok) return;
-    const int W = su.W, Lmax = su.Lmax;
+    const int W = NW, Lmax = su.Lmax;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
     stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
     const AuxView A = aux_view(smem_raw + (size_t)W * Lmax * sizeof(Lev), Lmax);
 
-    int L[MAXW_ENUM];
-    for (int w = 0; w < W; w++) L[w] = P.L[w];
-    const int Lin = L[W - 1];
+    int L[NW];
+#pragma unroll
+    for (int w = 0; w < NW; w++) L[w] = P.L[w];
+    const int Lin = L[NW - 1];
     const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
-    const int segl = P.seglen;
+    const int segl = P.seglen, nseg = P.nseg, Lstep = P.Lstep;
+    const uint64_t units = P.units;
     float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + su.aux_bytes);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
-    float4* tab = tab0 + (size_t)warp * segl;                                                             // {X,Y,Z,Tp}
-    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)(P1_THREADS / 32) * segl) + (size_t)warp * segl;  // {k_lo, k_hi}
+    constexpr int NWARP = P1_THREADS / 32;
+    float4* tab = tab0 + (size_t)warp * segl;                                                    // {X,Y,Z,Tp}
+    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * segl) + (size_t)warp * segl;     // {k_lo, k_hi}
     const float invf = P.inv;
     const double invd = 1.0 / (double)P.lamN;
     const int s0 = A.hdr[0], u0v = A.hdr[1];
     const bool khi_ok = A.hdr[2] != 0, klo_ok = A.hdr[3] != 0;
     const int smin_i = A.ssort[0], umax_i = A.umaxp[Lin], slast = A.ssort[Lin - 1], ulast = A.usuf[Lin - 1];
+    float* subp = submin + (size_t)prob * su.units_max;
 
-    uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
-    if (u1 > P.units) u1 = P.units;
-    int d[MAXW_ENUM];
+    uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
+    if (ub > units) ub = units;
+    // this warp's units: ua + warp, + NWARP, ... ; (row, seg) and the hi digits advance incrementally
+    uint64_t unit = ua + (uint64_t)warp;
+    int seg = (int)(unit % (uint64_t)nseg);
+    uint64_t row = unit / (uint64_t)nseg;
+    int d[NH > 0 ? NH : 1];
+#pragma unroll
+    for (int w = NH - 1; w >= 0; w--) { d[w] = (int)(row % (uint64_t)L[w]); row /= (uint64_t)L[w]; }
+    const int dq = NWARP / nseg, dr = NWARP % nseg;
     unsigned long long nfeas = 0;
-    for (uint64_t unit = u0 + (uint64_t)warp; unit < u1; unit += (uint64_t)(P1_THREADS / 32)) {
-        uint64_t row;
-        int e0, e1;
-        unit_range(P, unit, &row, &e0, &e1);
-        if (row < 0xffffffffull) {      // 32-bit digit decode
-            uint32_t r32 = (uint32_t)row;
-            for (int w = W - 3; w >= 0; w--) { d[w] = (int)(r32 % (uint32_t)L[w]); r32 /= (uint32_t)L[w]; }
-        } else {
-            decode_row(row, L, W, d);
+    for (; unit < ub; unit += NWARP) {
+        const int e0 = seg * segl, e1 = min(Lstep, e0 + segl);
+        HiSums h;
+        h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
+#pragma unroll
+        for (int w = 0; w < NH; w++) {
+            const Lev& r = sl[w * Lmax + d[w]];
+            h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
         }
-        const HiSums h = hi_sums(sl, Lmax, d, W);
+        // advance to this warp's next unit (no divisions)
+        {
+            seg += dr;
+            int carry = dq;
+            if (seg >= nseg) { seg -= nseg; carry++; }
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                int v = d[w] + carry;
+                carry = 0;
+                while (v >= L[w]) { v -= L[w]; carry++; }
+                d[w] = v;
+            }
+        }
         const int ne = e1 - e0;
         int sb = 1 << 30;
         if (QOS) {
             sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
             if (W >= 2 && stepw[A.sperm[e0]].S > sb) {   // even the smallest step level is infeasible
-                if (wl == 0) submin[(size_t)prob * su.units_max + unit] = INFINITY;
+                if (wl == 0) subp[unit] = INFINITY;
                 continue;
             }
         }
-        // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
+    // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
         //   X_e = Xh + B_e Yh + S'_e Zh (+ D_e for PAPER),  Y_e = Yh + S'_e inv,  Z_e = Zh + B_e inv
-        const double hBd = (double)h.B;
-        const float Yh = (float)(1.0 + (double)h.T * invd), Zh = (float)(hBd * invd);
+        const float hBf = __ll2float_rn(h.B), hTf = (float)h.T;
+        const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
         float Xh;
-        if (MODE == M_EXCL) Xh = (float)(hBd + (double)((u128)h.T * (u128)h.B - (u128)h.BS) * invd);
-        else Xh = (float)(hBd * (1.0 + (double)h.T * invd));
+        if (MODE == M_EXCL) {
+            const u128 Dh = (u128)h.T * (u128)h.B - (u128)h.BS;   // = sum_hi B_w (hT - S'_w) >= 0
+            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            Xh = fmaf(Dhf, invf, hBf);
+        } else {
+            Xh = hBf * Yh;
+        }
         int nc = 0;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
@@ -622,7 +650,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         float m = fminf(m0, m1);
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (wl == 0) submin[(size_t)prob * su.units_max + unit] = m;
+        if (wl == 0) subp[unit] = m;
         __syncwarp();   // the table is rewritten for the next unit
     }
     for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
@@ -756,6 +784,12 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
 typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*, unsigned long long*);
 typedef void (*P1Gen)(Setup, const Prob*, const Lev*, float*, float*);
 
+template <int NW>
+static P1Fast pick_fast(int mode, bool qos) {
+    if (mode == M_EXCL) return qos ? k_pass1_fast<NW, M_EXCL, true> : k_pass1_fast<NW, M_EXCL, false>;
+    return qos ? k_pass1_fast<NW, M_PAPER, true> : k_pass1_fast<NW, M_PAPER, false>;
+}
+
 template <int NP, int MODE>
 static P1Gen pick_gen_m(int obj, bool qos) {
     if (obj == O_SUM) return qos ? k_pass1_gen<NP, MODE, O_SUM, true> : k_pass1_gen<NP, MODE, O_SUM, false>;
@@ -793,8 +827,18 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
     const bool fast = use_fast(su);
     const size_t smem = pass1_smem(su, fast);
     if (fast) {
-        P1Fast f = su.mode == M_EXCL ? (qos ? k_pass1_fast<M_EXCL, true> : k_pass1_fast<M_EXCL, false>)
-                                     : (qos ? k_pass1_fast<M_PAPER, true> : k_pass1_fast<M_PAPER, false>);
+        P1Fast f = nullptr;
+        switch (su.W) {
+            case 1: f = pick_fast<1>(su.mode, qos); break;
+            case 2: f = pick_fast<2>(su.mode, qos); break;
+            case 3: f = pick_fast<3>(su.mode, qos); break;
+            case 4: f = pick_fast<4>(su.mode, qos); break;
+            case 5: f = pick_fast<5>(su.mode, qos); break;
+            case 6: f = pick_fast<6>(su.mode, qos); break;
+            case 7: f = pick_fast<7>(su.mode, qos); break;
+            case 8: f = pick_fast<8>(su.mode, qos); break;
+            default: return cudaErrorInvalidValue;
+        }
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible);
@@ -1090,106 +1134,123 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
-// materialisation (a9): one thread per problem
+// materialisation (a9): one CTA per problem (thread 0: per-worker scalars; all threads: groups)
 // ------------------------------------------------------------------------------------------
-__global__ void k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs, const U256* hstar,
-                              const U256* first, const int32_t* sizes, int C, MatOut o) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= su.n_problems) return;
+__global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs,
+                                                     const U256* hstar, const U256* first, const int32_t* sizes,
+                                                     int C, MatOut o) {
+    const int p = blockIdx.x;
     const Prob& P = probs[p];
     const int W = su.W;
-    int status = P.status;
-    if (status == 0 && (u256_is_max(first[p]) || u256_is_max(hstar[p]))) status = 1;  // infeasible
-    if (o.status) o.status[p] = status;
-    if (status != 0) {
-        if (o.index) o.index[p] = 0;
-        if (o.objective) o.objective[p] = 0.0;
-        if (o.makespan) o.makespan[p] = 0.0;
-        if (o.power) o.power[p] = 0.0;
-        if (o.energy) o.energy[p] = 0.0;
-        if (o.thr) o.thr[p] = 0.0;
-        for (int w = 0; w < W; w++) {
-            if (o.levels) o.levels[(size_t)p * W + w] = -1;
-            if (o.latency) o.latency[(size_t)p * W + w] = 0.0;
-            if (o.switches) o.switches[(size_t)p * W + w] = 0;
-            if (o.group_sm)
-                for (int g = 0; g < o.group_stride; g++) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = 0;
+    __shared__ int s_status;
+    __shared__ int lv[MAXW];
+    __shared__ double alpha_w[MAXW];
+    if (threadIdx.x == 0) {
+        int status = P.status;
+        if (status == 0 && (u256_is_max(first[p]) || u256_is_max(hstar[p]))) status = 1;  // infeasible
+        s_status = status;
+        if (o.status) o.status[p] = status;
+    }
+    __syncthreads();
+    if (s_status != 0) {
+        if (threadIdx.x == 0) {
+            if (o.index) o.index[p] = 0;
+            if (o.objective) o.objective[p] = 0.0;
+            if (o.makespan) o.makespan[p] = 0.0;
+            if (o.power) o.power[p] = 0.0;
+            if (o.energy) o.energy[p] = 0.0;
+            if (o.thr) o.thr[p] = 0.0;
         }
-        return;
-    }
-    int lv[MAXW];
-    unpack_tuple(first[p], W, lv);
-    // mixed-radix candidate index (worker 0 most significant); all-ones if it needs > 64 bits
-    uint64_t idx = 0;
-    bool fits = true;
-    for (int w = 0; w < W; w++) {
-        u128 t = (u128)idx * (u128)P.L[w] + (u128)lv[w];
-        if (t >> 64) fits = false;
-        idx = (uint64_t)t;
-    }
-    if (!fits) idx = ~0ull;
-    // FP64 values from exact integers
-    double avg[MAXW], Bw[MAXW], sum_avg = 0.0;
-    for (int w = 0; w < W; w++) {
-        int t = P.table[w];
-        avg[w] = (double)tb.S[t][lv[w]] / (double)tb.K[t];
-        Bw[w] = (double)tb.B[t][lv[w]];
-        sum_avg += avg[w];
-    }
-    const double N = (double)su.N;
-    double mk = 0.0, obj = 0.0, thr = 0.0;
-    for (int w = 0; w < W; w++) {
-        double ov;
-        if (su.mode == M_EXCL) ov = sum_avg - avg[w];
-        else if (su.mode == M_PAPER) ov = sum_avg;
-        else if (su.mode == M_EXCESS) ov = sum_avg - N > 0.0 ? sum_avg - N : 0.0;
-        else {
-            ov = 0.0;
-            for (int v = 0; v < W; v++)
-                if (v != w) ov += (double)P.Mf[w * MAXW_ENUM + v] * avg[v];
-        }
-        double alpha = ov / N;
-        double Lw = Bw[w] * (1.0 + alpha);
-        mk = Lw > mk ? Lw : mk;
-        obj += Lw;
-        thr += 1e9 / Lw;
-        int t = P.table[w];
-        int G = tb.G[t];
-        const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
-        int sw = 0;
-        for (int g = 0; g < G; g++) {
-            if (g > 0 && wit[g] != wit[g - 1]) sw++;
-            if (o.group_sm && g < o.group_stride) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = sizes[wit[g]];
-            if (o.group_lat) o.group_lat[((size_t)p * W + w) * o.group_stride + g] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha);
+        for (int i = threadIdx.x; i < W; i += blockDim.x) {
+            if (o.levels) o.levels[(size_t)p * W + i] = -1;
+            if (o.latency) o.latency[(size_t)p * W + i] = 0.0;
+            if (o.switches) o.switches[(size_t)p * W + i] = 0;
         }
         if (o.group_sm)
-            for (int g = G; g < o.group_stride; g++) o.group_sm[((size_t)p * W + w) * o.group_stride + g] = 0;
-        if (o.latency) o.latency[(size_t)p * W + w] = Lw;
-        if (o.switches) o.switches[(size_t)p * W + w] = sw;
-        if (o.levels) o.levels[(size_t)p * W + w] = lv[w];
+            for (int i = threadIdx.x; i < W * o.group_stride; i += blockDim.x) o.group_sm[(size_t)p * W * o.group_stride + i] = 0;
+        return;
     }
-    double frac = sum_avg / N;
-    if (frac > 1.0) frac = 1.0;
-    double pw = (double)P.p_idle + ((double)P.p_max - (double)P.p_idle) * frac;
-    if (su.obj == O_MAX) obj = mk;
-    else if (su.obj == O_ENERGY) obj = pw * mk;
-    if (o.index) o.index[p] = idx;
-    if (o.objective) o.objective[p] = obj;
-    if (o.makespan) o.makespan[p] = mk;
-    if (o.power) o.power[p] = pw;
-    if (o.energy) o.energy[p] = pw * mk * 1e-9;
-    if (o.thr) o.thr[p] = thr;
-    if (o.key) {
-        U256 k;
-        exact_key(su, P, levs + (size_t)p * su.lev_stride, lv, k);
-        for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
+    if (threadIdx.x == 0) {
+        int l[MAXW];
+        unpack_tuple(first[p], W, l);
+        // mixed-radix candidate index (worker 0 most significant); all-ones if it needs > 64 bits
+        uint64_t idx = 0;
+        bool fits = true;
+        for (int w = 0; w < W; w++) {
+            u128 t = (u128)idx * (u128)P.L[w] + (u128)l[w];
+            if (t >> 64) fits = false;
+            idx = (uint64_t)t;
+            lv[w] = l[w];
+        }
+        // FP64 values from exact integers
+        double avg[MAXW], Bw[MAXW], sum_avg = 0.0;
+        for (int w = 0; w < W; w++) {
+            const int t = P.table[w];
+            avg[w] = (double)tb.S[t][l[w]] / (double)tb.K[t];
+            Bw[w] = (double)tb.B[t][l[w]];
+            sum_avg += avg[w];
+        }
+        const double N = (double)su.N;
+        double mk = 0.0, obj = 0.0, thr = 0.0;
+        for (int w = 0; w < W; w++) {
+            double ov;
+            if (su.mode == M_EXCL) ov = sum_avg - avg[w];
+            else if (su.mode == M_PAPER) ov = sum_avg;
+            else if (su.mode == M_EXCESS) ov = sum_avg - N > 0.0 ? sum_avg - N : 0.0;
+            else {
+                ov = 0.0;
+                for (int v = 0; v < W; v++)
+                    if (v != w) ov += (double)P.Mf[w * MAXW_ENUM + v] * avg[v];
+            }
+            const double alpha = ov / N;
+            const double Lw = Bw[w] * (1.0 + alpha);
+            alpha_w[w] = alpha;
+            mk = Lw > mk ? Lw : mk;
+            obj += Lw;
+            thr += 1e9 / Lw;
+            if (o.latency) o.latency[(size_t)p * W + w] = Lw;
+            if (o.levels) o.levels[(size_t)p * W + w] = l[w];
+        }
+        double frac = sum_avg / N;
+        if (frac > 1.0) frac = 1.0;
+        const double pw = (double)P.p_idle + ((double)P.p_max - (double)P.p_idle) * frac;
+        if (su.obj == O_MAX) obj = mk;
+        else if (su.obj == O_ENERGY) obj = pw * mk;
+        if (o.index) o.index[p] = fits ? idx : ~0ull;
+        if (o.objective) o.objective[p] = obj;
+        if (o.makespan) o.makespan[p] = mk;
+        if (o.power) o.power[p] = pw;
+        if (o.energy) o.energy[p] = pw * mk * 1e-9;
+        if (o.thr) o.thr[p] = thr;
+        if (o.key) {
+            U256 k;
+            exact_key(su, P, levs + (size_t)p * su.lev_stride, l, k);
+            for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
+        }
+    }
+    __syncthreads();
+    // per worker: switch count; per group: pool size and e_g = beta_g (1 + alpha_w)
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const int t = P.table[w], G = tb.G[t];
+        const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
+        int sw = 0;
+        for (int g = 1; g < G; g++) sw += wit[g] != wit[g - 1];
+        if (o.switches) o.switches[(size_t)p * W + w] = sw;
+    }
+    for (int w = 0; w < W; w++) {
+        const int t = P.table[w], G = tb.G[t];
+        const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
+        for (int g = threadIdx.x; g < o.group_stride; g += blockDim.x) {
+            const size_t at = ((size_t)p * W + w) * o.group_stride + g;
+            if (o.group_sm) o.group_sm[at] = g < G ? sizes[wit[g]] : 0;
+            if (o.group_lat && g < G) o.group_lat[at] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha_w[w]);
+        }
     }
 }
 
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C, MatOut out,
                                cudaStream_t st) {
-    k_materialize<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes,
-                                                               C, out);
+    k_materialize<<<su.n_problems, 128, 0, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes, C, out);
     return cudaGetLastError();
 }
 

@@ -314,60 +314,68 @@ __global__ void k_slice_hstar(const int32_t* band, const int32_t* nband, const U
     hstar[0] = m;
 }
 
-// pass 2b: exact DP + lexicographic walk in every slice whose exact J is within tolerance
+// pass 2b: exact DP + lexicographic walk in every slice whose exact J is within tolerance.
+// The walk is block-parallel: for worker w = 0..W-1 every level l (rank order) is tested at
+// once -- "does some completion of (prefix, l) inside this slice reach key <= H*(1+tau)?",
+// exact by the DP tables -- and the smallest qualifying rank is kept.
 __global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Prob* probs, const Lev* levs,
                                                            const int16_t* dense, const int32_t* band,
                                                            const int32_t* nband, uint64_t* scratch, const U256* Jex,
                                                            const U256* hstar, U256* wtup) {
     const Prob& P = probs[0];
     __shared__ int64_t dlo[MAXW + 1], dhi[MAXW + 1];
+    __shared__ int s_pick;
+    __shared__ int64_t s_rem;
+    __shared__ uint64_t s_hp[MAXW];
+    __shared__ int s_lv[MAXW];
     uint64_t* scr = scratch + (size_t)blockIdx.x * (S.gtot + (size_t)(S.W) * S.maxrange);
     const U256 hs = hstar[0];
-    if (u256_is_max(hs)) {
-        for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x)
-            if (threadIdx.x == 0) wtup[bi] = u256_max();
-        return;
-    }
     for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x) {
         if (threadIdx.x == 0) wtup[bi] = u256_max();
-        if (u256_is_max(Jex[band[bi]]) || !within_tol(Jex[band[bi]], hs, S.tol_num, S.tol_den)) continue;
-        int64_t T = S.Tlo + band[bi];
+        if (u256_is_max(hs) || u256_is_max(Jex[band[bi]]) || !within_tol(Jex[band[bi]], hs, S.tol_num, S.tol_den))
+            continue;
+        const int64_t T = S.Tlo + band[bi];
         slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
-        if (threadIdx.x == 0) {
-            const int W = S.W;
-            const int64_t Tp = T * S.gS;
-            int64_t rem = T;
-            uint64_t hp[MAXW];
-            int lv[MAXW];
-            bool ok = true;
-            for (int w = 0; w < W && ok; w++) {
-                bool found = false;
-                int L = P.L[w];
-                for (int l = 0; l < L; l++) {
-                    const Lev& r = levs[w * S.Lmax + l];
-                    int64_t s = r.S / S.gS;
-                    int64_t rest = rem - s;
-                    uint64_t hw = scr[S.doff[w] + (s - S.smin[w])];
-                    if (hw == UINF) continue;
-                    uint64_t v;
-                    if (w == W - 1) {
-                        if (rest != 0) continue;
-                        v = hw;
-                    } else {
-                        if (rest < dlo[w + 1] || rest > dhi[w + 1]) continue;
-                        v = comb_u(S.obj, hw, scr[S.gtot + (size_t)w * S.maxrange + (rest - dlo[w + 1])]);
-                    }
-                    for (int u = 0; u < w; u++) v = comb_u(S.obj, hp[u], v);
-                    if (v == UINF) continue;
-                    if (within_tol(slice_key(S, P, Tp, v), hs, S.tol_num, S.tol_den)) {
-                        lv[w] = l; hp[w] = hw; rem = rest; found = true;
-                        break;
-                    }
+        const int W = S.W;
+        const int64_t Tp = T * S.gS;
+        if (threadIdx.x == 0) s_rem = T;
+        __syncthreads();
+        bool ok = true;
+        for (int w = 0; w < W && ok; w++) {
+            if (threadIdx.x == 0) s_pick = INT_MAX;
+            __syncthreads();
+            const int64_t rem = s_rem;
+            for (int l = threadIdx.x; l < P.L[w]; l += blockDim.x) {
+                const Lev& r = levs[w * S.Lmax + l];
+                const int64_t s = r.S / S.gS;
+                const int64_t rest = rem - s;
+                const uint64_t hw = scr[S.doff[w] + (s - S.smin[w])];
+                if (hw == UINF) continue;
+                uint64_t v;
+                if (w == W - 1) {
+                    if (rest != 0) continue;
+                    v = hw;
+                } else {
+                    if (rest < dlo[w + 1] || rest > dhi[w + 1]) continue;
+                    v = comb_u(S.obj, hw, scr[S.gtot + (size_t)w * S.maxrange + (rest - dlo[w + 1])]);
                 }
-                ok = found;
+                for (int u = 0; u < w; u++) v = comb_u(S.obj, s_hp[u], v);
+                if (v == UINF) continue;
+                if (within_tol(slice_key(S, P, Tp, v), hs, S.tol_num, S.tol_den)) atomicMin(&s_pick, l);
             }
-            if (ok) wtup[bi] = pack_tuple(lv, W);
+            __syncthreads();
+            const int pick = s_pick;
+            ok = pick != INT_MAX;
+            if (ok && threadIdx.x == 0) {
+                const Lev& r = levs[w * S.Lmax + pick];
+                const int64_t s = r.S / S.gS;
+                s_lv[w] = pick;
+                s_hp[w] = scr[S.doff[w] + (s - S.smin[w])];
+                s_rem = rem - s;
+            }
+            __syncthreads();
         }
+        if (ok && threadIdx.x == 0) wtup[bi] = pack_tuple(s_lv, W);
         __syncthreads();
     }
 }
