@@ -311,10 +311,11 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
 struct AuxView {
     float4* ip; float2* iu; float2* iD; int* ssort; int* usuf; int* umaxp; uint16_t* perm; uint16_t* sperm;
     uint16_t* khi; uint16_t* klo; int* hdr;
+    int* stS; int* stU; int* stUmax;   // step worker, sorted per segment: S', suffix-min of u, prefix-max of u
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
-    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 16;
+    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 16 + (size_t)Lmax * 12;
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -332,6 +333,9 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.khi = a.sperm + Lmax;
     a.klo = a.khi + P1_TABN;
     a.hdr = reinterpret_cast<int*>(a.klo + P1_TABN);
+    a.stS = a.hdr + 4;
+    a.stU = a.stS + Lmax;
+    a.stUmax = a.stU + Lmax;
     return a;
 }
 
@@ -390,6 +394,18 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
         for (int k = threadIdx.x; k < Lin; k += blockDim.x)
             for (int v = (k == 0 ? A.usuf[0] : A.usuf[k - 1] + 1); v <= A.usuf[k]; v++) A.klo[v - u0] = (uint16_t)k;
     if (threadIdx.x == 0) { A.hdr[0] = s0; A.hdr[1] = u0; A.hdr[2] = khi_ok; A.hdr[3] = klo_ok; }
+    // step worker, per segment in S' order: S', suffix minimum and (inclusive) prefix maximum of u
+    if (W >= 2) {
+        for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
+            const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
+            A.stS[i] = stepw[A.sperm[i]].S;
+            int mn = 1 << 30, mx = -(1 << 30);
+            for (int j = i; j < b1; j++) mn = min(mn, stepw[A.sperm[j]].Tmax - stepw[A.sperm[j]].S);
+            for (int j = b0; j <= i; j++) mx = max(mx, stepw[A.sperm[j]].Tmax - stepw[A.sperm[j]].S);
+            A.stU[i] = mn;
+            A.stUmax[i] = mx;
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -517,11 +533,22 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 d[w] = v;
             }
         }
-        const int ne = e1 - e0;
+        // the usable step levels form a range [ea, eb) of the segment's S'-sorted order:
+        //   S'_e <= sb  (prefix workers' QoS and the inner worker's loosest bound), and
+        //   u_e = Tmax_e - S'_e >= hT + min_k S'_k  (the step worker's own QoS; a suffix when u is
+        //   monotone, else the whole prefix [e0, eb) is scanned)
+        int ea = e0, eb = e1;
         int sb = 1 << 30;
-        if (QOS) {
+        if (QOS && W >= 2) {
             sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
-            if (W >= 2 && stepw[A.sperm[e0]].S > sb) {   // even the smallest step level is infeasible
+            int lo = e0, hi = e1;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.stS[mid] <= sb) lo = mid + 1; else hi = mid; }
+            eb = lo;
+            const int need = h.T + smin_i;
+            lo = e0; hi = eb;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.stU[mid] >= need) hi = mid; else lo = mid + 1; }
+            ea = (lo > e0 && A.stUmax[lo - 1] >= need) ? e0 : lo;   // max of u over [e0, lo)
+            if (ea >= eb) {
                 if (wl == 0) subp[unit] = INFINITY;
                 continue;
             }
@@ -539,6 +566,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             Xh = hBf * Yh;
         }
         int nc = 0;
+        const int ne = eb - ea;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
             bool use = false, past = true;
@@ -546,7 +574,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             float Be = 0.0f, De = 0.0f;
             if (k < ne) {
                 if (W >= 2) {
-                    const Lev& r = stepw[A.sperm[e0 + k]];
+                    const Lev& r = stepw[A.sperm[ea + k]];
                     Sp = r.S; Tme = r.Tmax;
                     past = QOS && r.S > sb;
                     use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_i));
@@ -638,8 +666,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
                 float k0, k1;
                 f2unpack(key, k0, k1);
-                if (p & 1) m1 = fminf(m1, fminf(k0, k1));
-                else m0 = fminf(m0, fminf(k0, k1));
+                m0 = fminf(m0, fminf(k0, k1));
             }
             if (kb2 & 1) {  // trailing odd element
                 const float4 r = A.ip[kb2 >> 1];
