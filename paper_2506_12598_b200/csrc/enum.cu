@@ -533,27 +533,16 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 d[w] = v;
             }
         }
-        // the usable step levels form a range [ea, eb) of the segment's S'-sorted order:
-        //   S'_e <= sb  (prefix workers' QoS and the inner worker's loosest bound), and
-        //   u_e = Tmax_e - S'_e >= hT + min_k S'_k  (the step worker's own QoS; a suffix when u is
-        //   monotone, else the whole prefix [e0, eb) is scanned)
-        int ea = e0, eb = e1;
+        const int ne = e1 - e0;
         int sb = 1 << 30;
-        if (QOS && W >= 2) {
+        if (QOS) {
             sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
-            int lo = e0, hi = e1;
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.stS[mid] <= sb) lo = mid + 1; else hi = mid; }
-            eb = lo;
-            const int need = h.T + smin_i;
-            lo = e0; hi = eb;
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.stU[mid] >= need) hi = mid; else lo = mid + 1; }
-            ea = (lo > e0 && A.stUmax[lo - 1] >= need) ? e0 : lo;   // max of u over [e0, lo)
-            if (ea >= eb) {
+            if (W >= 2 && stepw[A.sperm[e0]].S > sb) {   // even the smallest step level is infeasible
                 if (wl == 0) subp[unit] = INFINITY;
                 continue;
             }
         }
-    // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
+        // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
         //   X_e = Xh + B_e Yh + S'_e Zh (+ D_e for PAPER),  Y_e = Yh + S'_e inv,  Z_e = Zh + B_e inv
         const float hBf = __ll2float_rn(h.B), hTf = (float)h.T;
         const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
@@ -566,7 +555,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             Xh = hBf * Yh;
         }
         int nc = 0;
-        const int ne = eb - ea;
         for (int kb = 0; kb < ne; kb += 32) {
             const int k = kb + wl;
             bool use = false, past = true;
@@ -574,7 +562,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             float Be = 0.0f, De = 0.0f;
             if (k < ne) {
                 if (W >= 2) {
-                    const Lev& r = stepw[A.sperm[ea + k]];
+                    const Lev& r = stepw[A.sperm[e0 + k]];
                     Sp = r.S; Tme = r.Tmax;
                     past = QOS && r.S > sb;
                     use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_i));

@@ -239,10 +239,12 @@ __device__ void slice_exact_dp(const SliceDev& S, const Prob& P, const Lev* levs
             const int nk = S.smax[w] - S.smin[w] + 1;
             for (int64_t p = dlo[w] + threadIdx.x; p <= dhi[w]; p += blockDim.x) {
                 uint64_t best = UINF;
-                for (int k = 0; k < nk; k++) {
-                    int64_t rest = p - S.smin[w] - k;
-                    if (rest < dlo[w + 1] || rest > dhi[w + 1]) continue;
-                    uint64_t v = comb_u(S.obj, hw2[k], Dn[rest - dlo[w + 1]]);
+                // rest = p - smin_w - k must lie in [dlo[w+1], dhi[w+1]]
+                const int64_t k0 = p - S.smin[w] - dhi[w + 1], k1 = p - S.smin[w] - dlo[w + 1];
+                const int ka = (int)(k0 > 0 ? k0 : 0), kb = (int)(k1 < nk - 1 ? k1 : nk - 1);
+                const uint64_t* dn = Dn + (p - S.smin[w] - dlo[w + 1]);
+                for (int k = ka; k <= kb; k++) {
+                    const uint64_t v = comb_u(S.obj, hw2[k], dn[-k]);
                     if (v < best) best = v;
                 }
                 Dc[p - dlo[w]] = best;
@@ -335,7 +337,14 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Pro
         if (u256_is_max(hs) || u256_is_max(Jex[band[bi]]) || !within_tol(Jex[band[bi]], hs, S.tol_num, S.tol_den))
             continue;
         const int64_t T = S.Tlo + band[bi];
-        slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
+        if (*nband <= (int)gridDim.x) {
+            // pass 2a left this slice's exact tables in this CTA's scratch slot (same grid mapping)
+            if (threadIdx.x == 0)
+                for (int w = 1; w < S.W; w++) drange(S, T, w, &dlo[w], &dhi[w]);
+            __syncthreads();
+        } else {
+            slice_exact_dp(S, P, levs, dense, T, scr, dlo, dhi);
+        }
         const int W = S.W;
         const int64_t Tp = T * S.gS;
         if (threadIdx.x == 0) s_rem = T;
