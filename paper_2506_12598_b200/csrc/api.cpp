@@ -932,6 +932,10 @@ extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
 static int run_all_steps(eclip_session* s) {
     int rc = step_pass1(s);
     if (rc) return rc;
+    if (s->engine == ECLIP_ENGINE_ENUM && s->su.n_shards == 1) {   // unsharded: one band rescan
+        CU(launch_pass2_both(s->su, s->wk, s->st));
+        return ECLIP_OK;
+    }
     rc = step_pass2_min(s);
     if (rc) return rc;
     return step_pass2_first(s);

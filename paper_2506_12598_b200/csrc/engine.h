@@ -141,6 +141,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st);
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st);
 cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st);
 cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st);
+cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st);   // unsharded: one rescan
 
 struct MatOut {                 // materialisation outputs (device pointers, may be null)
     int32_t* status; int32_t* levels; uint64_t* index; double* objective; double* makespan;

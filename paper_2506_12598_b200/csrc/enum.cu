@@ -1007,7 +1007,10 @@ __device__ float band_bound(const Setup& su, float m, float ms) {
     return __double2float_ru(b);
 }
 
-// one CTA per problem.  mode 0: exact minimum over the band.  mode 1: lowest index within tol.
+// One CTA per problem.  PASS 0: exact minimum H* over the band.  PASS 1: lowest index whose exact
+// key is within tol of the (global) H*.  PASS 2 (unsharded runs): both in one rescan -- the band's
+// exactly evaluated candidates are kept in shared memory (a second rescan only on overflow).
+constexpr int P2_CAP = 256;
 template <int PASS>
 __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
@@ -1016,14 +1019,21 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     __shared__ uint64_t bar;
     __shared__ U256 red[512];
     __shared__ uint64_t redi[512];
+    __shared__ uint32_t list[512];
+    __shared__ int nlist;
+    __shared__ int wcount[16], woff[16];
+    __shared__ uint64_t c_idx[P2_CAP];
+    __shared__ U256 c_key[P2_CAP];
+    __shared__ int c_n;
+    __shared__ U256 s_hs;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     const int prob = blockIdx.x;
     Prob& P = probs[prob];
     if (P.status != 0) return;
     if (isinf(m32[prob])) {  // nothing feasible anywhere (global minimum is +inf)
         if (threadIdx.x == 0) {
-            if (PASS == 0) hstar[prob] = u256_max();
-            else first[prob] = u256_max();
+            if (PASS != 1) hstar[prob] = u256_max();
+            if (PASS != 0) first[prob] = u256_max();
         }
         return;
     }
@@ -1035,98 +1045,121 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
     uint64_t ua = slo * (uint64_t)su.upi, ub = shi * (uint64_t)su.upi;
     if (ub > P.units) ub = P.units;
-    U256 best = u256_max();
-    uint64_t besti = ~0ull;
-    U256 hs = (PASS == 1) ? hstar[prob] : u256_zero();
-    if (PASS == 1 && u256_is_max(hs)) {  // no exactly-feasible candidate
+    int L[MAXW_ENUM];
+    for (int w = 0; w < W; w++) L[w] = P.L[w];
+    if (threadIdx.x == 0) {
+        c_n = 0;
+        s_hs = (PASS == 1) ? hstar[prob] : u256_max();
+    }
+    __syncthreads();
+    if (PASS == 1 && u256_is_max(s_hs)) {  // no exactly-feasible candidate
         if (threadIdx.x == 0) first[prob] = u256_max();
         return;
     }
-    int L[MAXW_ENUM];
-    for (int w = 0; w < W; w++) L[w] = P.L[w];
-    __shared__ uint32_t list[512];
-    __shared__ int nlist;
-    bool done = false;
-    for (uint64_t blk = ua; blk < ub && !done; blk += blockDim.x) {
-        // compact the band units of this block of 512 (kept in candidate-index order)
-        const uint64_t u = blk + threadIdx.x;
-        const bool in_band = u < ub && submin[(size_t)prob * su.units_max + u] <= bound;
-        if (threadIdx.x == 0) nlist = 0;
-        __syncthreads();
-        const unsigned bal = __ballot_sync(0xffffffffu, in_band);
-        __shared__ int wcount[16], woff[16];
-        if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); w++) { woff[w] = acc; acc += wcount[w]; }
-            nlist = acc;
-        }
-        __syncthreads();
-        if (in_band) list[woff[threadIdx.x >> 5] + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)(u - blk);
-        __syncthreads();
-        const int nl = nlist;
-        for (int li = 0; li < nl; li++) {
-            const uint64_t unit = blk + list[li];
-            uint64_t row;
-            int e0, e1;
-            unit_range(P, unit, &row, &e0, &e1);
-            int lv[MAXW_ENUM];
-            decode_row(row, L, W, lv);
-            const uint64_t ncand = (uint64_t)(e1 - e0) * (uint64_t)Lin;
-            for (uint64_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-                int lvc[MAXW_ENUM];
-                for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
-                if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint64_t)Lin);
-                lvc[W - 1] = (int)(c % (uint64_t)Lin);
-                float k32;
-                if (!key32_scalar(su, P, sl, lvc, k32)) continue;
-                if (!(k32 <= bound)) continue;
-                U256 k;
-                if (!exact_key(su, P, sl, lvc, k)) continue;
-                if (PASS == 0) {
-                    if (u256_cmp(k, best) < 0) best = k;
-                } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
+
+    // phase 0: exact minimum (+ record the band when PASS 2);  phase 1: lowest index within tol
+    auto scan = [&](int phase, U256& best, uint64_t& besti) {
+        const U256 hs = s_hs;
+        bool done = false;
+        for (uint64_t blk = ua; blk < ub && !done; blk += blockDim.x) {
+            const uint64_t u = blk + threadIdx.x;
+            const bool in_band = u < ub && submin[(size_t)prob * su.units_max + u] <= bound;
+            if (threadIdx.x == 0) nlist = 0;
+            __syncthreads();
+            const unsigned bal = __ballot_sync(0xffffffffu, in_band);
+            if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int acc = 0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); w++) { woff[w] = acc; acc += wcount[w]; }
+                nlist = acc;
+            }
+            __syncthreads();
+            if (in_band) list[woff[threadIdx.x >> 5] + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)(u - blk);
+            __syncthreads();
+            const int nl = nlist;
+            for (int li = 0; li < nl; li++) {   // units in candidate-index order
+                const uint64_t unit = blk + list[li];
+                uint64_t row;
+                int e0, e1;
+                unit_range(P, unit, &row, &e0, &e1);
+                int lv[MAXW_ENUM];
+                decode_row(row, L, W, lv);
+                const uint32_t ncand = (uint32_t)(e1 - e0) * (uint32_t)Lin;
+                for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
+                    int lvc[MAXW_ENUM];
+                    for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
+                    if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint32_t)Lin);
+                    lvc[W - 1] = (int)(c % (uint32_t)Lin);
+                    float k32;
+                    if (!key32_scalar(su, P, sl, lvc, k32)) continue;
+                    if (!(k32 <= bound)) continue;
+                    U256 k;
+                    if (!exact_key(su, P, sl, lvc, k)) continue;
                     uint64_t idx = 0;   // index within the problem (fits: ENUM limits)
                     for (int w = 0; w < W; w++) idx = idx * (uint64_t)L[w] + (uint64_t)lvc[w];
-                    if (idx < besti) besti = idx;
+                    if (phase == 0) {
+                        if (u256_cmp(k, best) < 0) best = k;
+                        if (PASS == 2) {
+                            const int slot = atomicAdd(&c_n, 1);
+                            if (slot < P2_CAP) { c_idx[slot] = idx; c_key[slot] = k; }
+                        }
+                    } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
+                        if (idx < besti) besti = idx;
+                    }
+                }
+                if (phase == 1 && __syncthreads_or(besti != ~0ull)) {   // first unit with a hit holds the winner
+                    done = true;
+                    break;
                 }
             }
-            if (PASS == 1 && __syncthreads_or(besti != ~0ull)) {   // first unit with a hit holds the winner
-                done = true;
-                break;
-            }
-        }
-        __syncthreads();
-    }
-    if (PASS == 0) {
-        red[threadIdx.x] = best;
-        __syncthreads();
-        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-            if (threadIdx.x < s && u256_cmp(red[threadIdx.x + s], red[threadIdx.x]) < 0) red[threadIdx.x] = red[threadIdx.x + s];
             __syncthreads();
         }
-        if (threadIdx.x == 0) hstar[prob] = red[0];
-    } else {
-        redi[threadIdx.x] = besti;
+    };
+    auto write_first = [&](uint64_t idx) {
+        if (idx == ~0ull) first[prob] = u256_max();
+        else {
+            int lv[MAXW_ENUM];
+            for (int w = W - 1; w >= 0; w--) { lv[w] = (int)(idx % (uint64_t)L[w]); idx /= (uint64_t)L[w]; }
+            first[prob] = pack_tuple(lv, W);
+        }
+    };
+
+    U256 best = u256_max();
+    uint64_t besti = ~0ull;
+    if (PASS != 1) {
+        scan(0, best, besti);
+        red[threadIdx.x] = best;
         __syncthreads();
-        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-            if (threadIdx.x < s && redi[threadIdx.x + s] < redi[threadIdx.x]) redi[threadIdx.x] = redi[threadIdx.x + s];
+        for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+            if (threadIdx.x < s2 && u256_cmp(red[threadIdx.x + s2], red[threadIdx.x]) < 0) red[threadIdx.x] = red[threadIdx.x + s2];
             __syncthreads();
         }
         if (threadIdx.x == 0) {
-            uint64_t idx = redi[0];
-            if (idx == ~0ull) first[prob] = u256_max();
-            else {
-                int lv[MAXW_ENUM];
-                for (int w = W - 1; w >= 0; w--) {
-                    lv[w] = (int)(idx % (uint64_t)P.L[w]);
-                    idx /= (uint64_t)P.L[w];
-                }
-                first[prob] = pack_tuple(lv, W);
-            }
+            hstar[prob] = red[0];
+            s_hs = red[0];
+        }
+        __syncthreads();
+        if (PASS == 0) return;
+        if (u256_is_max(s_hs)) {
+            if (threadIdx.x == 0) first[prob] = u256_max();
+            return;
         }
     }
+    if (PASS == 2 && c_n <= P2_CAP) {   // the whole band is in shared memory
+        const U256 hs = s_hs;
+        for (int i = threadIdx.x; i < c_n; i += blockDim.x)
+            if (within_tol(c_key[i], hs, su.tol_num, su.tol_den) && c_idx[i] < besti) besti = c_idx[i];
+    } else {
+        scan(1, best, besti);
+    }
+    redi[threadIdx.x] = besti;
+    __syncthreads();
+    for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2 && redi[threadIdx.x + s2] < redi[threadIdx.x]) redi[threadIdx.x] = redi[threadIdx.x + s2];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) write_first(redi[0]);
 }
 
 cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
@@ -1134,6 +1167,15 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_pass2<0><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 wk.hstar, wk.first);
+    return cudaGetLastError();
+}
+cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
+    size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_pass2<2><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first);
     return cudaGetLastError();

@@ -274,3 +274,56 @@ def test_sharded_batch_equals_unsharded():
     outs = _run_shards(lambda k: ec.Session(pr, batch=b, shard=k, n_shards=3), 3)
     for o in outs:
         assert np.array_equal(o["winner_index"], ref["winner_index"])
+
+
+# ---------------------------------------------------------------- more shapes
+def _many_workers_problem(W, seed, mode="exclude_self", objective="sum", qos=True, R=1):
+    sizes = synth.lattice_sizes(3, 60)
+    models = [synth.synthesize_model(f"m{i}", "uniform", 2, sizes, 900 + 17 * seed + i) for i in range(3)]
+    rng = np.random.default_rng(seed)
+    ids = [int(x) for x in rng.integers(0, 3, size=W)]
+    q = synth.qos_3x(models, ids, factor=float(W) * 0.9) if qos else None
+    M = None
+    if mode == "matrix":
+        M = rng.uniform(0.5, 1.5, size=(W, W)).astype(np.float32)
+        np.fill_diagonal(M, 0.0)
+    return synth.Problem(f"W{W}", models, ids, 60, R, mode, objective, qos_ns=q, slowdown_matrix=M)
+
+
+@pytest.mark.parametrize("W", [5, 6, 7, 8])
+def test_many_workers_fast_and_generic_kernels(W):
+    """the W-templated pass-1 kernels (W = 5..8) on small level tables, every mode / objective"""
+    for seed in range(3):
+        for mode in ("exclude_self", "paper", "excess", "matrix"):
+            for obj in ("sum", "max", "energy"):
+                for qos in (False, True):
+                    p = _many_workers_problem(W, seed, mode, obj, qos)
+                    o = oracle.solve(p)
+                    _same(_gpu(p, "enum"), o, f"W{W} {seed} {mode} {obj} {qos}")
+
+
+def test_matrix_with_qos_full_size_sampled():
+    """MATRIX + QoS (maybe/surely-feasible filter) on C3 shapes, oracle live"""
+    p = synth.make_c3("matrix")
+    p.qos_ns = synth.qos_3x(p.models, p.model_ids, factor=3.5)   # binding (the optimum changes vs no QoS)
+    o = oracle.solve(p)
+    assert o.status == "ok"
+    _same(_gpu(p, "enum"), o, "C3 matrix qos")
+
+
+def test_batch_paper_mode_and_masks():
+    """batched path with PAPER_AS_WRITTEN (fast kernel's D_i term) and per-model masks"""
+    models, ids, qos = synth.make_c5(12, seed=21)
+    pr = ec.Profiles.from_models(models)
+    masks = [0xFF, 0xFE, 0x7F, 0xFF, 0x3C, 0xFF, 0xF0]
+    out = ec.plan_batch(pr, ids, total_sms=148, slowdown="paper", qos_ns=qos * 2.0, allowed_mask=masks,
+                        p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+    for i in range(12):
+        p = synth.c5_problem(i, models, ids, qos * 2.0)
+        p.mode = "paper"
+        p.allowed_mask = [masks[m] for m in ids[i]]
+        o = oracle.solve(p, "slice")
+        assert (int(out["status"][i]) == 0) == (o.status == "ok"), i
+        if o.status == "ok":
+            assert out["winner_levels"][i].tolist() == o.levels, i
+            assert out["objective"][i] == pytest.approx(o.objective, rel=REL)
