@@ -14,11 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("what", choices=["c5", "c4", "c3", "s6"])
 ap.add_argument("--mixes", type=int, default=4096)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--noqos", action="store_true")
 a = ap.parse_args()
 if a.what == "c5":
     models, ids, qos = synth.make_c5(a.mixes)
     pr = ec.Profiles.from_models(models)
-    d_ids, d_q = torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda()
+    d_ids, d_q = torch.from_numpy(ids).cuda(), (None if a.noqos else torch.from_numpy(qos).cuda())
     out = ec.alloc_batch_out(a.mixes, 4, 16, device="cuda")
     for _ in range(a.reps):
         ec.plan_batch(pr, d_ids, total_sms=148, qos_ns=d_q, p_idle_w=200.0, p_max_w=1000.0, out=out, gmax=16)
