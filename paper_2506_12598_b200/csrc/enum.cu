@@ -460,77 +460,6 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 //       index of the suffix-minimum of u that reaches Tp (exact when u is non-decreasing in S',
 //       i.e. B* non-increasing; otherwise the earlier levels are swept with a mask).
 // Both ends come from lookup tables indexed by value (binary search if a range is too wide).
-// ---- sweeps of the inner worker's S'-sorted levels [k0, k1) for one or two prefix entries
-// entry t = {X, Y, Z, Tp}:  key_k = fma(B_k, Y, fma(S'_k, Z, X (+ D_k)))
-template <int MODE>
-__device__ __forceinline__ float key1(const AuxView& A, const float4& t, int k) {
-    const float4 r = A.ip[k >> 1];
-    const bool hi = k & 1;
-    float b0 = t.x;
-    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += hi ? dd.y : dd.x; }
-    return fmaf(hi ? r.y : r.x, t.y, fmaf(hi ? r.w : r.z, t.z, b0));
-}
-template <int MODE>
-__device__ __forceinline__ void sweep1(const AuxView& A, const float4& t, int k0, int k1, float& m) {
-    const u64 X2 = f2pack(t.x, t.x), Y2 = f2pack(t.y, t.y), Z2 = f2pack(t.z, t.z);
-    int k = k0;
-    if (k & 1) { m = fminf(m, key1<MODE>(A, t, k)); k++; }
-    const int pend = k1 >> 1;
-#pragma unroll 4
-    for (int p = k >> 1; p < pend; p++) {
-        const float4 r = A.ip[p];
-        u64 base = X2;
-        if (MODE == M_PAPER) { const float2 dd = A.iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
-        const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
-        float a, b;
-        f2unpack(key, a, b);
-        m = fminf(m, fminf(a, b));
-    }
-    if ((k1 & 1) && k1 - 1 >= k) m = fminf(m, key1<MODE>(A, t, k1 - 1));
-}
-template <int MODE>
-__device__ __forceinline__ void sweep2(const AuxView& A, const float4& ta, const float4& tb, int k0, int k1, float& ma,
-                                       float& mb) {
-    const u64 XA = f2pack(ta.x, ta.x), YA = f2pack(ta.y, ta.y), ZA = f2pack(ta.z, ta.z);
-    const u64 XB = f2pack(tb.x, tb.x), YB = f2pack(tb.y, tb.y), ZB = f2pack(tb.z, tb.z);
-    int k = k0;
-    if (k & 1) { ma = fminf(ma, key1<MODE>(A, ta, k)); mb = fminf(mb, key1<MODE>(A, tb, k)); k++; }
-    const int pend = k1 >> 1;
-#pragma unroll 4
-    for (int p = k >> 1; p < pend; p++) {
-        const float4 r = A.ip[p];
-        const u64 B2 = f2pack(r.x, r.y), S2 = f2pack(r.z, r.w);
-        u64 ba = XA, bb = XB;
-        if (MODE == M_PAPER) {
-            const float2 dd = A.iD[p];
-            const u64 D2 = f2pack(dd.x, dd.y);
-            ba = add2(XA, D2);
-            bb = add2(XB, D2);
-        }
-        const u64 kA = fma2(B2, YA, fma2(S2, ZA, ba));
-        const u64 kB = fma2(B2, YB, fma2(S2, ZB, bb));
-        float a0, a1, b0, b1;
-        f2unpack(kA, a0, a1);
-        f2unpack(kB, b0, b1);
-        ma = fminf(ma, fminf(a0, a1));
-        mb = fminf(mb, fminf(b0, b1));
-    }
-    if ((k1 & 1) && k1 - 1 >= k) {
-        ma = fminf(ma, key1<MODE>(A, ta, k1 - 1));
-        mb = fminf(mb, key1<MODE>(A, tb, k1 - 1));
-    }
-}
-// masked sweep of [0, kend) (inner worker's own bound checked per level; non-monotone u only)
-template <int MODE>
-__device__ __forceinline__ unsigned long long sweep_masked(const AuxView& A, const float4& t, int kend, float& m) {
-    unsigned long long n = 0;
-    for (int k = 0; k < kend; k++) {
-        const float2 uu2 = A.iu[k >> 1];
-        if (t.w <= ((k & 1) ? uu2.y : uu2.x)) { m = fminf(m, key1<MODE>(A, t, k)); n++; }
-    }
-    return n;
-}
-
 template <int NW, int MODE, bool QOS>
 __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
@@ -689,34 +618,50 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         __syncwarp();
         float m0 = INFINITY, m1 = INFINITY;
-        // each lane sweeps two table entries jointly (i, i + 32): one shared load of an inner pair
-        // feeds four candidates on their common range; the remainders are swept singly
-        for (int i = wl; i < nc; i += 64) {
-            const int j = i + 32;
-            float4 ta = tab[i];
-            int2 ka = tabk[i];
-            float4 tb = make_float4(0.f, 0.f, 0.f, 0.f);
-            int2 kb = make_int2(0, 0);
-            const bool two = j < nc;
-            if (two) { tb = tab[j]; kb = tabk[j]; }
-            if (QOS && ka.x < 0) { ka.x = -1 - ka.x; nfeas += sweep_masked<MODE>(A, ta, min(ka.x, ka.y), m0); }
-            if (QOS && two && kb.x < 0) { kb.x = -1 - kb.x; nfeas += sweep_masked<MODE>(A, tb, min(kb.x, kb.y), m1); }
-            if (!two) {
-                if (ka.x < ka.y) { nfeas += ka.y - ka.x; sweep1<MODE>(A, ta, ka.x, ka.y, m0); }
-                continue;
+        for (int i = wl; i < nc; i += 32) {
+            const float4 t4 = tab[i];
+            int2 kk = tabk[i];
+            if (QOS && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
+                kk.x = -1 - kk.x;
+                const int kend = min(kk.x, kk.y);
+                for (int k = 0; k < kend; k++) {
+                    const float4 r = A.ip[k >> 1];
+                    const float2 uu2 = A.iu[k >> 1];
+                    const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
+                    if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
+                }
             }
-            const int c0 = max(ka.x, kb.x), c1 = min(ka.y, kb.y);
-            if (c0 < c1) {
-                sweep2<MODE>(A, ta, tb, c0, c1, m0, m1);
-                if (ka.x < c0) sweep1<MODE>(A, ta, ka.x, c0, m0);
-                if (c1 < ka.y) sweep1<MODE>(A, ta, c1, ka.y, m0);
-                if (kb.x < c0) sweep1<MODE>(A, tb, kb.x, c0, m1);
-                if (c1 < kb.y) sweep1<MODE>(A, tb, c1, kb.y, m1);
-            } else {
-                if (ka.x < ka.y) sweep1<MODE>(A, ta, ka.x, ka.y, m0);
-                if (kb.x < kb.y) sweep1<MODE>(A, tb, kb.x, kb.y, m1);
+            const int ka = max(kk.x, 0), kb2 = kk.y;
+            if (ka >= kb2) continue;
+            nfeas += (unsigned long long)(kb2 - ka);
+            const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
+            int k = ka;
+            if (k & 1) {   // leading odd element
+                const float4 r = A.ip[k >> 1];
+                float b0 = t4.x;
+                if (MODE == M_PAPER) b0 += A.iD[k >> 1].y;
+                m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
+                k++;
             }
-            nfeas += (unsigned long long)(max(ka.y - ka.x, 0) + max(kb.y - kb.x, 0));
+            const int pend = kb2 >> 1;
+#pragma unroll 4
+            for (int p = k >> 1; p < pend; p++) {
+                const float4 r = A.ip[p];
+                u64 base = X2;
+                if (MODE == M_PAPER) { const float2 dd = A.iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+                float k0, k1;
+                f2unpack(key, k0, k1);
+                m0 = fminf(m0, fminf(k0, k1));
+            }
+            if (kb2 & 1) {  // trailing odd element
+                const float4 r = A.ip[kb2 >> 1];
+                float b0 = t4.x;
+                if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
+                m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
+            }
         }
         float m = fminf(m0, m1);
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
