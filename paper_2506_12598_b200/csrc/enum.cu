@@ -310,12 +310,14 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
 // ------------------------------------------------------------------------------------------
 struct AuxView {
     float4* ip; float2* iu; float2* iD; int* ssort; int* usuf; int* umaxp; uint16_t* perm; uint16_t* sperm;
-    uint16_t* khi; uint16_t* klo; int* hdr;
-    int* stS; int* stU; int* stUmax;   // step worker, sorted per segment: S', suffix-min of u, prefix-max of u
+    uint8_t* khi; uint8_t* klo;       // inner worker: #{k : S'_k <= s0 + v};  min{k : usuf[k] >= u0 + v}
+    uint8_t* shi; uint8_t* slo;       // step worker (one segment): same two tables
+    int* hdr;                         // s0, u0, khi_ok, klo_ok, ss0, su0, shi_ok, slo_ok
+    int* stS; int* stU; int* stUmax;  // step worker, sorted per segment: S', suffix-min of u, prefix-max of u
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
-    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 16 + (size_t)Lmax * 12;
+    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 32 + (size_t)Lmax * 12;
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -330,10 +332,12 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.umaxp = a.usuf + (Lmax + 1);
     a.perm = reinterpret_cast<uint16_t*>(a.umaxp + (Lmax + 1));
     a.sperm = a.perm + Lmax;
-    a.khi = a.sperm + Lmax;
+    a.khi = reinterpret_cast<uint8_t*>(a.sperm + Lmax);
     a.klo = a.khi + P1_TABN;
-    a.hdr = reinterpret_cast<int*>(a.klo + P1_TABN);
-    a.stS = a.hdr + 4;
+    a.shi = a.klo + P1_TABN;
+    a.slo = a.shi + P1_TABN;
+    a.hdr = reinterpret_cast<int*>(a.slo + P1_TABN);
+    a.stS = a.hdr + 8;
     a.stU = a.stS + Lmax;
     a.stUmax = a.stU + Lmax;
     return a;
@@ -386,14 +390,14 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     }
     __syncthreads();
     const int s0 = A.ssort[0], u0 = A.usuf[0];
-    const bool khi_ok = A.ssort[Lin - 1] - s0 + 1 <= P1_TABN, klo_ok = A.usuf[Lin - 1] - u0 + 1 <= P1_TABN;
+    const bool khi_ok = Lin <= 255 && A.ssort[Lin - 1] - s0 + 1 <= P1_TABN;
+    const bool klo_ok = Lin <= 255 && A.usuf[Lin - 1] - u0 + 1 <= P1_TABN;
     if (khi_ok)
         for (int k = threadIdx.x; k < Lin; k += blockDim.x)
-            for (int v = A.ssort[k]; v < (k + 1 < Lin ? A.ssort[k + 1] : A.ssort[k] + 1); v++) A.khi[v - s0] = (uint16_t)(k + 1);
+            for (int v = A.ssort[k]; v < (k + 1 < Lin ? A.ssort[k + 1] : A.ssort[k] + 1); v++) A.khi[v - s0] = (uint8_t)(k + 1);
     if (klo_ok)
         for (int k = threadIdx.x; k < Lin; k += blockDim.x)
-            for (int v = (k == 0 ? A.usuf[0] : A.usuf[k - 1] + 1); v <= A.usuf[k]; v++) A.klo[v - u0] = (uint16_t)k;
-    if (threadIdx.x == 0) { A.hdr[0] = s0; A.hdr[1] = u0; A.hdr[2] = khi_ok; A.hdr[3] = klo_ok; }
+            for (int v = (k == 0 ? A.usuf[0] : A.usuf[k - 1] + 1); v <= A.usuf[k]; v++) A.klo[v - u0] = (uint8_t)k;
     // step worker, per segment in S' order: S', suffix minimum and (inclusive) prefix maximum of u
     if (W >= 2) {
         for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
@@ -405,6 +409,25 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
             A.stU[i] = mn;
             A.stUmax[i] = mx;
         }
+    }
+    __syncthreads();
+    // step-worker lookup tables (whole-row units only): #{e : S'_e <= ss0 + v}, min{e : stU[e] >= su0 + v}
+    bool shi_ok = false, slo_ok = false;
+    int ss0 = 0, su0 = 0;
+    if (W >= 2 && P.nseg == 1 && Lst <= 255) {
+        ss0 = A.stS[0]; su0 = A.stU[0];
+        shi_ok = A.stS[Lst - 1] - ss0 + 1 <= P1_TABN;
+        slo_ok = A.stU[Lst - 1] - su0 + 1 <= P1_TABN;
+        if (shi_ok)
+            for (int e = threadIdx.x; e < Lst; e += blockDim.x)
+                for (int v = A.stS[e]; v < (e + 1 < Lst ? A.stS[e + 1] : A.stS[e] + 1); v++) A.shi[v - ss0] = (uint8_t)(e + 1);
+        if (slo_ok)
+            for (int e = threadIdx.x; e < Lst; e += blockDim.x)
+                for (int v = (e == 0 ? A.stU[0] : A.stU[e - 1] + 1); v <= A.stU[e]; v++) A.slo[v - su0] = (uint8_t)e;
+    }
+    if (threadIdx.x == 0) {
+        A.hdr[0] = s0; A.hdr[1] = u0; A.hdr[2] = khi_ok; A.hdr[3] = klo_ok;
+        A.hdr[4] = ss0; A.hdr[5] = su0; A.hdr[6] = shi_ok; A.hdr[7] = slo_ok;
     }
 }
 
@@ -498,6 +521,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const int s0 = A.hdr[0], u0v = A.hdr[1];
     const bool khi_ok = A.hdr[2] != 0, klo_ok = A.hdr[3] != 0;
     const int smin_i = A.ssort[0], umax_i = A.umaxp[Lin], slast = A.ssort[Lin - 1], ulast = A.usuf[Lin - 1];
+    const int ss0 = A.hdr[4], su0 = A.hdr[5];
+    const bool step_tab = W >= 2 && A.hdr[6] != 0 && A.hdr[7] != 0;
+    const int shi_n = step_tab ? A.stS[P.Lstep - 1] - ss0 + 1 : 0;
+    const int sulast = step_tab ? A.stU[P.Lstep - 1] : 0;
     float* subp = submin + (size_t)prob * su.units_max;
 
     uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
@@ -533,13 +560,28 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 d[w] = v;
             }
         }
-        const int ne = e1 - e0;
+        int ne = e1 - e0;
         int sb = 1 << 30;
+        int ea = e0;
         if (QOS) {
             sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
-            if (W >= 2 && stepw[A.sperm[e0]].S > sb) {   // even the smallest step level is infeasible
+            if (W >= 2 && A.stS[e0] > sb) {   // even the smallest step level is infeasible
                 if (wl == 0) subp[unit] = INFINITY;
                 continue;
+            }
+            if (step_tab) {
+                // usable step levels: S'_e <= sb (a prefix) and u_e >= hT + min S'_k (a suffix of the
+                // suffix-minimum; the prefix maximum says whether earlier levels could qualify)
+                const int eb = (sb - ss0 >= shi_n) ? Lstep : (int)A.shi[sb - ss0];
+                const int need = h.T + smin_i;
+                int lo = (need <= su0) ? 0 : ((need > sulast) ? Lstep : (int)A.slo[need - su0]);
+                if (lo > 0 && A.stUmax[lo - 1] >= need) lo = 0;
+                ea = lo;
+                ne = eb - lo;
+                if (ne <= 0) {
+                    if (wl == 0) subp[unit] = INFINITY;
+                    continue;
+                }
             }
         }
         // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
@@ -562,7 +604,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             float Be = 0.0f, De = 0.0f;
             if (k < ne) {
                 if (W >= 2) {
-                    const Lev& r = stepw[A.sperm[e0 + k]];
+                    const Lev& r = stepw[A.sperm[ea + k]];
                     Sp = r.S; Tme = r.Tmax;
                     past = QOS && r.S > sb;
                     use = !past && (!QOS || (r.Tmax - r.S - h.T >= smin_i));
