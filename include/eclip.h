@@ -61,6 +61,12 @@ extern "C" {
 #define ECLIP_ENGINE_AUTO 0
 #define ECLIP_ENGINE_ENUM 1         /* exhaustive level-tuple enumeration (every candidate scored) */
 #define ECLIP_ENGINE_SLICE 2        /* exact T'-sliced DP (linear slowdown modes only) */
+#define ECLIP_ENGINE_BASELINE 3     /* result of eclip_baseline_plan (a fixed comparison plan, no search) */
+
+/* ---- comparison planners (eclip_baseline_plan) ----------------------------------------- */
+#define ECLIP_BASELINE_ALL_MAX 0     /* every group at the worker's largest allowed size ("Baseline") */
+#define ECLIP_BASELINE_MODEL_WISE 1  /* one size per model (Model-Wise right-sizing) */
+#define ECLIP_BASELINE_KERNEL_WISE 2 /* every group at its minimum-CU threshold (KW) */
 
 /* ---- profiles ------------------------------------------------------------------------ */
 typedef struct eclip_profiles eclip_profiles;
@@ -208,6 +214,35 @@ int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
 int eclip_session_create_problem(const eclip_profiles* prof, const eclip_problem* problem,
                                  const eclip_options* opt, eclip_session** out);
 int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_tuple, eclip_result* result);
+
+/* ---- comparison planners and the lookup table -----------------------
+ * eclip_baseline_plan: the paper's comparison plans (§V), evaluated on the GPU with
+ * the same model as eclip_plan (slowdown mode, objective, power, exact QoS check):
+ *   ECLIP_BASELINE_ALL_MAX     param ignored
+ *   ECLIP_BASELINE_MODEL_WISE  param = latency factor f >= 1 (the paper's 3x): the smallest
+ *                              allowed size c with sum_g beta_g(c) <= f sum_g beta_g(c_max)
+ *   ECLIP_BASELINE_KERNEL_WISE param = tolerance t >= 0 (SPEC default 0.05): per group the
+ *                              smallest allowed size c with beta_g(c) <= (1 + t) beta_g(c_max)
+ * f and t are taken as the rationals round(x 1e9) / 1e9 and compared exactly.  The switch budget
+ * is NOT enforced (the baselines do not have one; model_switches reports what the plan uses).
+ * result: status ECLIP_OK, or ECLIP_INFEASIBLE when the plan violates a QoS bound (every other
+ * field still describes the plan); engine_used = ECLIP_ENGINE_BASELINE; winner_levels = -1;
+ * winner_index = UINT64_MAX; candidates = units_scored = 1; exact_key = 0.
+ * Errors: as eclip_plan (ECLIP_E_INVALID_ARG for an unknown kind / out-of-range param). */
+int eclip_baseline_plan(const eclip_profiles* prof, const eclip_problem* problem, int32_t kind, double param,
+                        const eclip_options* opt, eclip_result* result);
+
+/* Serialize a plan as the lookup table ("store the results in a lookup table"; SPEC
+ * S:225-233): every (worker, kernel) -> its pool size, as the JSON text
+ *   {"meta":{"hash":"0x<16 hex>","mode":"exclude_self|paper|excess|matrix","switch_max":R},
+ *    "workers":[{"worker_id":w,"configs":[c_0,...,c_{K_w-1}]},...]}
+ * (no whitespace).  hash = 64-bit FNV-1a over the same text without the "hash" member.
+ * group_sm: [sum_w G_w] sizes per group (eclip_result.group_sm); problem gives the workers,
+ * models and group bounds.  buf may be NULL to query the length; *len receives the text length
+ * (excluding the terminating NUL); buf must hold len + 1 bytes.  Host-only (no GPU work).
+ * Errors: ECLIP_E_INVALID_ARG. */
+int eclip_lookup_table_json(const eclip_profiles* prof, const eclip_problem* problem, const int32_t* group_sm,
+                            char* buf, size_t cap, size_t* len, uint64_t* hash);
 
 #ifdef __cplusplus
 }

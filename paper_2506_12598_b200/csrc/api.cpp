@@ -600,26 +600,16 @@ static int status_error(const eclip_session* s, int st, int p) {
     return fail(ECLIP_E_INVALID_ARG, "problem %d is invalid (model id / QoS / matrix / power values)", p);
 }
 
-// ------------------------------------------------------------------------------------------
-// session construction
-// ------------------------------------------------------------------------------------------
-static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr, const eclip_options* opt,
-                                eclip_session** out) {
-    if (!pr) return fail(ECLIP_E_INVALID_ARG, "null problem");
+// per-worker table specs of a problem (validated: model ids, masks, group bounds, QoS)
+static int worker_specs(const eclip_profiles* P, const eclip_problem* pr, std::vector<TableSpec>* out) {
     const int W = pr->n_models;
-    double tol = opt ? opt->tie_tol : 1e-5;
-    int rc = check_common(P, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, pr->p_idle_w, pr->p_max_w, tol);
-    if (rc) return rc;
-    if (!pr->model_ids) return fail(ECLIP_E_INVALID_ARG, "null model_ids");
     const int C = P->C();
-    std::vector<TableSpec> specs;
-    std::map<TableSpec, int> ids;
-    std::vector<int32_t> table_of(W);
+    out->assign(W, TableSpec{});
     const int32_t* gb = pr->group_bounds;
     for (int w = 0; w < W; w++) {
         int m = pr->model_ids[w];
         if (m < 0 || m >= P->n()) return fail(ECLIP_E_INVALID_ARG, "model id %d of worker %d out of range", m, w);
-        TableSpec sp;
+        TableSpec& sp = (*out)[w];
         sp.model = m;
         sp.R = pr->switch_max;
         sp.mask = pr->allowed_mask ? pr->allowed_mask[w] : ((C == 32) ? 0xffffffffu : ((1u << C) - 1u));
@@ -644,14 +634,6 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
         } else {
             for (int k = 0; k <= K; k++) sp.bounds.push_back(k);
         }
-        auto it = ids.find(sp);
-        if (it == ids.end()) {
-            ids[sp] = (int)specs.size();
-            table_of[w] = (int)specs.size();
-            specs.push_back(sp);
-        } else {
-            table_of[w] = it->second;
-        }
         if (pr->qos_ns && !(pr->qos_ns[w] >= 0.0)) return fail(ECLIP_E_INVALID_ARG, "qos_ns[%d] must be >= 0 or +inf", w);
     }
     if (pr->slowdown == ECLIP_MATRIX) {
@@ -661,6 +643,37 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
             float m = pr->slowdown_matrix[i];
             if (i / W != i % W && !(std::isfinite(m) && m >= 0.0f && m < 1024.0f))
                 return fail(ECLIP_E_INVALID_ARG, "slowdown_matrix entries must be finite, >= 0 and < 1024");
+        }
+    }
+    return ECLIP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// session construction
+// ------------------------------------------------------------------------------------------
+static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr, const eclip_options* opt,
+                                eclip_session** out) {
+    if (!pr) return fail(ECLIP_E_INVALID_ARG, "null problem");
+    const int W = pr->n_models;
+    double tol = opt ? opt->tie_tol : 1e-5;
+    int rc = check_common(P, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, pr->p_idle_w, pr->p_max_w, tol);
+    if (rc) return rc;
+    if (!pr->model_ids) return fail(ECLIP_E_INVALID_ARG, "null model_ids");
+    const int C = P->C();
+    std::vector<TableSpec> wspec, specs;
+    rc = worker_specs(P, pr, &wspec);
+    if (rc) return rc;
+    std::map<TableSpec, int> ids;
+    std::vector<int32_t> table_of(W);
+    for (int w = 0; w < W; w++) {
+        const TableSpec& sp = wspec[w];
+        auto it = ids.find(sp);
+        if (it == ids.end()) {
+            ids[sp] = (int)specs.size();
+            table_of[w] = (int)specs.size();
+            specs.push_back(sp);
+        } else {
+            table_of[w] = it->second;
         }
     }
     auto s = std::make_unique<eclip_session>();
@@ -1024,4 +1037,162 @@ extern "C" int eclip_plan(const eclip_profiles* prof, const eclip_problem* probl
     rc = run_all_steps(s);
     if (rc) return rc;
     return plan_one(s, r, nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// comparison planners and the lookup table
+// ------------------------------------------------------------------------------------------
+extern "C" int eclip_baseline_plan(const eclip_profiles* P, const eclip_problem* pr, int32_t kind, double param,
+                                   const eclip_options* opt, eclip_result* r) {
+    if (!pr || !r) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    const int W = pr->n_models;
+    int rc = check_common(P, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, pr->p_idle_w, pr->p_max_w,
+                          0.0);
+    if (rc) return rc;
+    if (!pr->model_ids) return fail(ECLIP_E_INVALID_ARG, "null model_ids");
+    if (kind < ECLIP_BASELINE_ALL_MAX || kind > ECLIP_BASELINE_KERNEL_WISE)
+        return fail(ECLIP_E_INVALID_ARG, "unknown baseline kind %d", kind);
+    if (kind == ECLIP_BASELINE_KERNEL_WISE && !(param >= 0.0 && param <= 1e6))
+        return fail(ECLIP_E_INVALID_ARG, "kernel-wise tolerance must be in [0, 1e6]");
+    if (kind == ECLIP_BASELINE_MODEL_WISE && !(param >= 1.0 && param <= 1e6))
+        return fail(ECLIP_E_INVALID_ARG, "model-wise latency factor must be in [1, 1e6]");
+    std::vector<TableSpec> ws;
+    rc = worker_specs(P, pr, &ws);
+    if (rc) return rc;
+    const int C = P->C();
+    // same exact-arithmetic ranges as the optimizer (status -5 in k_prep_prob)
+    uint64_t lam = 1;
+    for (int w = 0; w < W; w++) {
+        const uint64_t K = (uint64_t)P->nk[ws[w].model];
+        lam = lam / (uint64_t)gcd64((int64_t)lam, (int64_t)K) * K;
+        if (lam > ((uint64_t)1 << 40)) return fail(ECLIP_E_TOO_LARGE, "lcm of kernel counts too large");
+    }
+    if ((long double)lam * pr->total_sms * (W + 1) >= (long double)(1 << 24))
+        return fail(ECLIP_E_TOO_LARGE, "Lambda N (W+1) >= 2^24");
+    for (int w = 0; w < W; w++) {
+        int64_t bm = 0;
+        for (int k = 0; k < P->nk[ws[w].model]; k++) {
+            int64_t mx = 0;
+            for (int j = 0; j < C; j++) mx = std::max(mx, P->row(ws[w].model, k)[j]);
+            bm += mx;
+        }
+        if (bm >= ((int64_t)1 << 36)) return fail(ECLIP_E_TOO_LARGE, "worker %d: solo time exceeds 2^36 ns", w);
+    }
+    eclip_session s;   // stream + arena only
+    s.prof = P;
+    rc = setup_device(&s, opt);
+    if (rc) return rc;
+    BaseJob J{};
+    J.W = W; J.C = C; J.N = pr->total_sms; J.mode = pr->slowdown; J.obj = pr->objective; J.kind = kind;
+    J.den = 1000000000ull;
+    J.num = (uint64_t)llround(param * 1e9);
+    J.p_idle = pr->p_idle_w; J.p_max = pr->p_max_w;
+    int gmax = 1;
+    for (int w = 0; w < W; w++) gmax = std::max(gmax, (int)ws[w].bounds.size() - 1);
+    int32_t* dsz;
+    CU(s.arena.alloc(&dsz, C));
+    CU(cudaMemcpyAsync(dsz, P->sizes.data(), 4 * C, cudaMemcpyHostToDevice, s.st));
+    J.sizes = dsz;
+    for (int w = 0; w < W; w++) {
+        const int m = ws[w].model, K = P->nk[m];
+        const int G = (int)ws[w].bounds.size() - 1;
+        J.G[w] = G; J.K[w] = K; J.mask[w] = ws[w].mask;
+        J.Q[w] = pr->qos_ns ? pr->qos_ns[w] : (double)INFINITY;
+        int64_t* dex; int32_t* dgb;
+        CU(s.arena.alloc(&dex, (size_t)K * C));
+        CU(s.arena.alloc(&dgb, G + 1));
+        CU(cudaMemcpyAsync(dex, P->row(m, 0), (size_t)K * C * 8, cudaMemcpyHostToDevice, s.st));
+        CU(cudaMemcpyAsync(dgb, ws[w].bounds.data(), (size_t)(G + 1) * 4, cudaMemcpyHostToDevice, s.st));
+        J.exec[w] = dex; J.bounds[w] = dgb;
+    }
+    if (pr->slowdown == ECLIP_MATRIX)
+        for (int a = 0; a < W; a++)
+            for (int b = 0; b < W; b++) J.M[a * MAXW_ENUM + b] = a == b ? 0.0f : pr->slowdown_matrix[a * W + b];
+    // one device block for every output: status, switches, group_sm | scalars, latency, group_lat
+    const size_t ni = 1 + (size_t)W + (size_t)W * gmax, nd = 5 + (size_t)W + (size_t)W * gmax;
+    int32_t* di; double* dd;
+    CU(s.arena.alloc(&di, ni));
+    CU(s.arena.alloc(&dd, nd));
+    BaseOut o{};
+    o.status = di; o.switches = di + 1; o.group_sm = di + 1 + W; o.stride = gmax;
+    o.scalars = dd; o.latency = dd + 5; o.group_lat = dd + 5 + W;
+    CU(launch_baseline(J, o, s.st));
+    std::vector<int32_t> hi(ni);
+    std::vector<double> hd(nd);
+    CU(cudaMemcpyAsync(hi.data(), di, ni * 4, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(hd.data(), dd, nd * 8, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaStreamSynchronize(s.st));
+    r->status = hi[0] == 0 ? ECLIP_OK : ECLIP_INFEASIBLE;
+    r->engine_used = ECLIP_ENGINE_BASELINE;
+    r->objective = hd[0]; r->makespan_ns = hd[1]; r->power_w = hd[2]; r->energy_j = hd[3]; r->throughput_rps = hd[4];
+    r->winner_index = ~0ull;
+    r->candidates = 1;
+    r->units_scored = 1;
+    for (int i = 0; i < 4; i++) r->exact_key[i] = 0;
+    size_t off = 0;
+    for (int w = 0; w < W; w++) {
+        const int G = J.G[w];
+        if (r->model_latency_ns) r->model_latency_ns[w] = hd[5 + w];
+        if (r->model_switches) r->model_switches[w] = hi[1 + w];
+        if (r->winner_levels) r->winner_levels[w] = -1;
+        for (int g = 0; g < G; g++) {
+            if (r->group_sm) r->group_sm[off + g] = hi[1 + W + (size_t)w * gmax + g];
+            if (r->group_latency_ns) r->group_latency_ns[off + g] = hd[5 + W + (size_t)w * gmax + g];
+        }
+        off += G;
+    }
+    return ECLIP_OK;
+}
+
+// 64-bit FNV-1a (offset basis 0xcbf29ce484222325, prime 0x100000001b3)
+static uint64_t fnv1a64(const std::string& s) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+extern "C" int eclip_lookup_table_json(const eclip_profiles* P, const eclip_problem* pr, const int32_t* group_sm,
+                                       char* buf, size_t cap, size_t* len, uint64_t* hash) {
+    if (!P || !pr || !group_sm || !pr->model_ids) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    const int W = pr->n_models;
+    if (W < 1 || W > MAXW) return fail(ECLIP_E_INVALID_ARG, "n_models must be in [1, %d]", MAXW);
+    if (pr->slowdown < 0 || pr->slowdown > 3) return fail(ECLIP_E_INVALID_ARG, "unknown slowdown mode");
+    std::vector<TableSpec> ws;
+    int rc = worker_specs(P, pr, &ws);
+    if (rc) return rc;
+    static const char* names[4] = {"exclude_self", "paper", "excess", "matrix"};
+    std::string body = "\"workers\":[";
+    size_t off = 0;
+    for (int w = 0; w < W; w++) {
+        body += (w ? ",{\"worker_id\":" : "{\"worker_id\":") + std::to_string(w) + ",\"configs\":[";
+        const std::vector<int32_t>& b = ws[w].bounds;
+        bool first = true;
+        for (size_t g = 0; g + 1 < b.size(); g++) {
+            const int32_t c = group_sm[off + g];
+            for (int k = b[g]; k < b[g + 1]; k++) {
+                body += (first ? "" : ",") + std::to_string(c);
+                first = false;
+            }
+        }
+        off += b.size() - 1;
+        body += "]}";
+    }
+    body += "]";
+    const std::string meta_tail = "\"mode\":\"" + std::string(names[pr->slowdown]) + "\",\"switch_max\":" +
+                                  std::to_string(pr->switch_max) + "}";
+    const std::string canon = "{\"meta\":{" + meta_tail + "," + body + "}";
+    const uint64_t h = fnv1a64(canon);
+    char hx[32];
+    snprintf(hx, sizeof hx, "0x%016llx", (unsigned long long)h);
+    const std::string text = "{\"meta\":{\"hash\":\"" + std::string(hx) + "\"," + meta_tail + "," + body + "}";
+    if (hash) *hash = h;
+    if (len) *len = text.size();
+    if (buf) {
+        if (cap < text.size() + 1) return fail(ECLIP_E_INVALID_ARG, "buffer too small: need %zu bytes", text.size() + 1);
+        memcpy(buf, text.c_str(), text.size() + 1);
+    }
+    return ECLIP_OK;
 }

@@ -157,4 +157,32 @@ bool pass1_fast(int L_inner);
 int pass1_fast_team(int L_inner);
 size_t pass1_aux_bytes(int Lmax);
 
+
+// ---- comparison planners (baseline.cu) ----
+struct BaseJob {
+    int32_t W, C, N, mode, obj, kind;
+    uint64_t num, den;                 // tol (KERNEL_WISE) or factor (MODEL_WISE) = num / den
+    float p_idle, p_max;
+    const int32_t* sizes;              // [C]
+    int32_t G[MAXW];
+    int64_t K[MAXW];
+    uint32_t mask[MAXW];
+    const int64_t* exec[MAXW];         // [K_w * C] the worker's per-kernel profile rows (ns)
+    const int32_t* bounds[MAXW];       // [G_w + 1] group kernel offsets
+    double Q[MAXW];
+    float M[MAXW_ENUM * MAXW_ENUM];
+};
+
+struct BaseOut {
+    int32_t* status;                   // [1] 0 = meets every QoS bound, 1 = does not
+    int32_t* group_sm;                 // [W * stride]
+    double* group_lat;                 // [W * stride]
+    int32_t stride;
+    double* latency;                   // [W]
+    int32_t* switches;                 // [W]
+    double* scalars;                   // [5] objective, makespan, power, energy, throughput
+};
+
+cudaError_t launch_baseline(const BaseJob& j, BaseOut o, cudaStream_t st);
+
 }  // namespace eclip

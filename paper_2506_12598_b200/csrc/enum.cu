@@ -138,35 +138,6 @@ __device__ __forceinline__ void decode_row(uint64_t row, const int* L, int W, in
 // ------------------------------------------------------------------------------------------
 // prep
 // ------------------------------------------------------------------------------------------
-__device__ int frac_bits_d(double x, int limit) {
-    for (int k = 0; k <= limit; k++) {
-        double y = ldexp(x, k);
-        if (y == floor(y)) return k;
-    }
-    return -1;
-}
-
-// floor(q * D) for q >= 0 (double, may be inf); saturates to all-ones when >= 2^120
-__device__ u128 floor_qD(double q, u128 D) {
-    if (isinf(q)) return ~(u128)0;
-    if (!(q > 0.0)) return 0;
-    int ex;
-    double f = frexp(q, &ex);
-    u64 mant = (u64)ldexp(f, 53);
-    int e = ex - 53;
-    // mant * D < 2^53 * 2^60
-    U256 prod = u256_mul128((u128)mant, D);
-    if (prod.w[3] || prod.w[2]) return ~(u128)0;
-    u128 x = ((u128)prod.w[1] << 64) | prod.w[0];
-    if (e >= 0) {
-        // every exact h is < 2^112 (host-validated ranges), so any bound >= 2^120 is "none"
-        if (e >= 120 || (x >> (120 - e)) != 0) return ~(u128)0;
-        return x << e;
-    }
-    int s = -e;
-    return s >= 128 ? (u128)0 : (x >> s);
-}
-
 __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= su.n_problems) return;

@@ -82,4 +82,35 @@ EX_HD void unpack_tuple(const U256& t, int W, int* lv) {
 
 EX_HD uint64_t gcd_u64(uint64_t a, uint64_t b) { while (b) { uint64_t t = a % b; a = b; b = t; } return a; }
 
+#ifdef __CUDACC__
+// smallest k >= 0 with x 2^k integral (x >= 0 finite), or -1 if k > limit
+__device__ __forceinline__ int frac_bits_d(double x, int limit) {
+    for (int k = 0; k <= limit; k++) {
+        double y = ldexp(x, k);
+        if (y == floor(y)) return k;
+    }
+    return -1;
+}
+
+// floor(q * D) for q >= 0 (double, may be inf); saturates to all-ones when >= 2^120
+// (every exact h is < 2^112 by the host-validated ranges, so that reads as "no bound")
+__device__ __forceinline__ u128 floor_qD(double q, u128 D) {
+    if (isinf(q)) return ~(u128)0;
+    if (!(q > 0.0)) return 0;
+    int ex;
+    double f = frexp(q, &ex);
+    uint64_t mant = (uint64_t)ldexp(f, 53);
+    int e = ex - 53;
+    U256 prod = u256_mul128((u128)mant, D);
+    if (prod.w[3] || prod.w[2]) return ~(u128)0;
+    u128 x = ((u128)prod.w[1] << 64) | prod.w[0];
+    if (e >= 0) {
+        if (e >= 120 || (x >> (120 - e)) != 0) return ~(u128)0;
+        return x << e;
+    }
+    int s = -e;
+    return s >= 128 ? (u128)0 : (x >> s);
+}
+#endif
+
 }  // namespace eclip

@@ -22,7 +22,7 @@ E_PARSE, E_MISSING_CONFIG, E_NONMONOTONE, E_INVALID_ARG, E_TOO_LARGE, E_CUDA, E_
 MODES = {"exclude_self": 0, "paper": 1, "paper_as_written": 1, "excess": 2, "excess_over_capacity": 2, "matrix": 3}
 OBJECTIVES = {"sum": 0, "max": 1, "energy": 2}
 ENGINES = {"auto": 0, "enum": 1, "slice": 2}
-ENGINE_NAMES = {1: "enum", 2: "slice"}
+ENGINE_NAMES = {1: "enum", 2: "slice", 3: "baseline"}
 
 
 class EclipError(RuntimeError):
@@ -75,7 +75,8 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_profiles_info", "eclip_last_error", "eclip_version", "eclip_default_options", "eclip_plan",
            "eclip_plan_batch", "eclip_session_create", "eclip_session_pass1", "eclip_session_pass2_min",
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
-           "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats"]
+           "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats",
+           "eclip_baseline_plan", "eclip_lookup_table_json"]
 
 
 def lib():
@@ -109,6 +110,9 @@ def lib():
         L.eclip_session_stats.argtypes = [vp, P(C.c_uint64)]
         L.eclip_session_free.argtypes = [vp]
         L.eclip_session_free.restype = None
+        L.eclip_baseline_plan.argtypes = [vp, P(Problem), C.c_int32, C.c_double, P(Options), P(Result)]
+        L.eclip_lookup_table_json.argtypes = [vp, P(Problem), P(C.c_int32), C.c_char_p, C.c_size_t,
+                                              P(C.c_size_t), P(C.c_uint64)]
         _lib = L
     return _lib
 
@@ -302,6 +306,41 @@ def plan_problem(profiles: Profiles, p, **kw) -> Plan:
                 objective=p.objective, allowed_mask=p.allowed_mask, qos_ns=p.qos_ns,
                 slowdown_matrix=p.slowdown_matrix, group_bounds=p.group_bounds, p_idle_w=p.p_idle_w,
                 p_max_w=p.p_max_w, **kw)
+
+
+BASELINES = {"all_max": 0, "model_wise": 1, "kernel_wise": 2}
+
+
+def baseline_plan(profiles: Profiles, model_ids, *, kind: str, param: float = 0.0, total_sms: int,
+                  switch_max: int = 14, slowdown: str = "exclude_self", objective: str = "sum", allowed_mask=None,
+                  qos_ns=None, slowdown_matrix=None, group_bounds=None, p_idle_w: float = 75.0,
+                  p_max_w: float = 225.0, device: int = 0, stream=None) -> Plan:
+    """eclip_baseline_plan: the paper's comparison plans (Baseline / Model-Wise / Kernel-Wise,
+    PAPER.md §V) evaluated on the GPU under the same model as plan()."""
+    a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
+                     slowdown_matrix, group_bounds, p_idle_w, p_max_w)
+    o = _options("auto", device, stream)
+    r, bufs = _result_buffers(a.W, a.G)
+    _check(lib().eclip_baseline_plan(profiles.handle, C.byref(a.c), BASELINES[kind], float(param), C.byref(o),
+                                     C.byref(r)))
+    return _to_plan(r, bufs, a.G)
+
+
+def lookup_table_json(profiles: Profiles, model_ids, group_sm, *, total_sms: int, switch_max: int = 14,
+                      slowdown: str = "exclude_self", group_bounds=None, slowdown_matrix=None):
+    """eclip_lookup_table_json: (JSON text, FNV-1a 64 hash) of a plan's lookup table."""
+    if slowdown == "matrix" and slowdown_matrix is None:
+        slowdown_matrix = np.zeros((len(model_ids), len(model_ids)), np.float32)
+    a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, "sum", None, None, slowdown_matrix,
+                     group_bounds, 75.0, 225.0)
+    g = _np([c for row in group_sm for c in row], np.int32)
+    n, h = C.c_size_t(), C.c_uint64()
+    _check(lib().eclip_lookup_table_json(profiles.handle, C.byref(a.c), _ptr(g, C.c_int32), None, 0, C.byref(n),
+                                         C.byref(h)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().eclip_lookup_table_json(profiles.handle, C.byref(a.c), _ptr(g, C.c_int32), buf, len(buf),
+                                         C.byref(n), C.byref(h)))
+    return buf.value.decode(), int(h.value)
 
 
 # ------------------------------------------------------------------------------------------
