@@ -41,7 +41,7 @@ N_MIXES = 4096
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mixes", type=int, default=N_MIXES)
@@ -59,17 +59,30 @@ def dist_env():
 
 # ----------------------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML
+    (nvidia-ml-py) polled every 5 ms from a thread; nvidia-smi -lms 100 if NVML is missing."""
+    NAMES = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.proc, self.nv, self.run = gpu, [], None, None, False
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.run = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
+        try:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -77,28 +90,44 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nv
+        while self.run:
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((float(mhz), [n for n, b in self.NAMES.items() if rs & b]))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            r = [c.strip() for c in line.split(",")]
+            if r and r[0].replace(".", "").isdigit():
+                self.max_mhz = float(r[1])
+                self.rows.append((float(r[0]), [n for k, n in enumerate(names) if len(r) > 2 + k and
+                                                r[2 + k].lower() == "active"]))
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for k, n in enumerate(names):
-                if len(r) > 3 + k and r[3 + k].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.nv is not None:
+            self.run = False
+            self.t.join(timeout=2)
+            src = "nvml 5 ms"
+        elif self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            src = "nvidia-smi 100 ms"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["no clock source"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[1]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(getattr(self, "max_mhz", 0)) or None,
+                "sm_mhz_min": min(sm) if sm else None, "samples": len(sm), "source": src, "reasons": reasons}
 
 
 # ----------------------------------------------------------------------------------------- oracle
@@ -188,9 +217,11 @@ def main():
     value = world * a.steps * cand_step / (t_max_ms * 1e-3)
 
     # ---- pass-1 kernel alone (the dominant kernel): CUDA events on the launching stream
-    k_ms, k_launches, k_eval = pass1_time(ec, pr, ids, qos, stream, local)
-    # the same kernel on the same mixes without QoS bounds: every candidate needs its FP32 key
-    n_ms, n_launches, n_eval = pass1_time(ec, pr, ids, None, stream, local)
+    k_ms, k_launches, k_eval, k_units = pass1_time(ec, pr, ids, qos, stream, local)
+    # the same pass without row pruning (every row classified) and without QoS bounds, for context
+    x_ms, x_launches, x_eval, _ = pass1_time(ec, pr, ids, qos, stream, local, prune=False)
+    n_ms, n_launches, n_eval, n_units = pass1_time(ec, pr, ids, None, stream, local)
+    units_total = int(sum(Ls[row[0]] * Ls[row[1]] for row in ids))
 
     # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
     pin_ids = torch.from_numpy(ids).pin_memory()
@@ -246,6 +277,11 @@ def main():
                          "evaluated_candidates_per_launch": k_eval,
                          "evaluated_fraction": k_eval / cand_step,
                          "candidates_per_s_kernel": cand_per_s_kernel},
+            "pruning": {"units_total_per_launch": units_total, "units_processed_per_launch": k_units,
+                        "pass1_ms_pruned": k_ms / k_launches, "pass1_ms_exhaustive": x_ms / x_launches,
+                        "evaluated_candidates_exhaustive": x_eval,
+                        "note": "row lower bounds (DESIGN.md §3.9) prove the skipped rows hold no candidate within "
+                                "the tolerance band of the best key found; exhaustive = every row classified"},
             "roofline_noqos": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,noQoS>",
                                "achieved": fma_ops_per_cand * n_eval / (n_ms / n_launches * 1e-3) / 1e9,
                                "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s",
@@ -272,17 +308,18 @@ def level_counts(pr, ec):
     return [ec.plan(pr, [m], total_sms=148, switch_max=14).candidates for m in range(n)]
 
 
-def pass1_time(ec, pr, ids, qos, stream, local):
-    """CUDA-event time of the pass-1 kernel (+ its tiny reduction) alone, via the split API on
-    the same stream; also returns how many candidates pass 1 evaluated in FP32."""
+def pass1_time(ec, pr, ids, qos, stream, local, prune=True):
+    """CUDA-event time of pass 1 alone (row bounds + pruned waves + its tiny reduction), via the
+    split API on the same stream; also returns how many candidates pass 1 evaluated in FP32 and
+    how many units (rows) it processed."""
     import torch
     from paper_2506_12598_b200.eclip import Session
-    tot, launches, evaluated = 0.0, 0, 0
+    tot, launches, evaluated, units = 0.0, 0, 0, 0
     batch = dict(model_ids=ids, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
     if qos is not None:
         batch["qos_ns"] = qos
     for rep in range(3):
-        s = Session(pr, batch=batch, engine="enum", device=local, stream=stream.cuda_stream)
+        s = Session(pr, batch=batch, engine="enum", device=local, stream=stream.cuda_stream, prune=prune)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -292,9 +329,10 @@ def pass1_time(ec, pr, ids, qos, stream, local):
         if rep > 0:
             tot += e0.elapsed_time(e1)
             launches += 1
-            evaluated = s.stats()["evaluated_candidates"]
+            st = s.stats()
+            evaluated, units = st["evaluated_candidates"], st["units_processed"]
         s.close()
-    return tot, launches, evaluated
+    return tot, launches, evaluated, units
 
 
 def time_to_plan(ec, world, rank, dist):

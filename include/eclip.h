@@ -139,6 +139,9 @@ typedef struct {
     void* cuda_stream;            /* cudaStream_t to run on (NULL => the library's own stream) */
     double tie_tol;               /* tau: ties within key <= m (1 + tau) go to the lowest index (default 1e-5) */
     int32_t shard, n_shards;      /* candidate-space shard of this call (default 0 / 1); see eclip_session_* */
+    int32_t no_prune;             /* ENUM, SUM, linear modes, W >= 3: 0 (default) = skip rows of candidates whose
+                                     proven lower bound exceeds the tolerance band of the best key found so far
+                                     (same answer); 1 = score every QoS-feasible candidate */
 } eclip_options;
 
 void eclip_default_options(eclip_options* o);
@@ -207,6 +210,11 @@ void eclip_session_free(eclip_session* s);
  * (QoS-feasible; the others are classified infeasible by exact range cuts without
  * arithmetic) — used by bench.py to report the roofline on the work actually done. */
 int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
+/* All pass-1 counters of this session, out[0..n): [0] candidates whose FP32 key was evaluated,
+ * [1] pass-1 units (rows x segments) processed under row pruning (0 when pruning is off;
+ * the rest were proven outside the tolerance band by their lower bound).
+ * Entries beyond the defined ones are set to 0.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_CUDA. */
+int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n);
 
 /* Single-problem sessions (the per-worker masks / groups of eclip_problem; used to shard
  * one large problem, e.g. BASELINE config 4, across GPUs).  Same steps as above with

@@ -507,6 +507,7 @@ static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, i
     su.delta = (double)(8 * W + 16) * std::ldexp(1.0, -24);
     su.shard = opt ? opt->shard : 0;
     su.n_shards = opt ? std::max(1, opt->n_shards) : 1;
+    su.prune = (opt && opt->no_prune) ? 0 : 1;
 }
 
 // choose the engine and size the work (pass-1 geometry: see enum.cu)
@@ -559,10 +560,16 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     long double target = n * units / 592.0L;                    // >= 2 CTAs per SM, 2 waves
     long double upi = std::min<long double>(target, std::max<long double>(1, 16777216.0L / cand_unit));
     upi = std::max<long double>(upi, teams_typ);
+    if (su.prune && W >= 3 && fast) {
+        // row pruning leaves few units per item: larger items (up to a whole problem) amortise the
+        // staging, as long as there are >= 8 CTAs per SM
+        upi = std::max<long double>(upi, std::min<long double>(units, std::ceil(n * units / 1184.0L)));
+    }
     upi = std::ceil(upi / teams_typ) * teams_typ;
     su.nseg = nseg;
     su.upi = (int32_t)std::min<long double>(upi, 1 << 30);
     su.units_max = (int64_t)units;
+    su.rows_max = (int64_t)H;
     su.items_max = (int32_t)std::ceil(units / su.upi);
     su.table_bytes = 0;
     su.aux_bytes = 0;
@@ -591,6 +598,16 @@ static int alloc_work(eclip_session* s) {
     CU(s->arena.alloc(&wk.first, n));
     CU(s->arena.alloc(&wk.feasible, 1));
     CU(cudaMemsetAsync(wk.feasible, 0, sizeof(unsigned long long), s->st));
+    CU(s->arena.alloc(&wk.rows_done, 1));
+    CU(cudaMemsetAsync(wk.rows_done, 0, sizeof(unsigned long long), s->st));
+    if (s->engine == ECLIP_ENGINE_ENUM && pass1_prunable(su)) {
+        CU(s->arena.alloc(&wk.rowlb, n * (size_t)su.rows_max));
+        CU(s->arena.alloc(&wk.lbmin, n));
+        CU(s->arena.alloc(&wk.inc, n));
+        CU(s->arena.alloc(&wk.hull, n * 4 * (size_t)su.Lmax));
+        CU(s->arena.alloc(&wk.ftab, n * (size_t)FT_CAP));
+        CU(s->arena.alloc(&wk.rowhdr, n));
+    }
     return ECLIP_OK;
 }
 
@@ -936,6 +953,16 @@ extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
     if (s->wk.feasible) CU(cudaMemcpyAsync(&v, s->wk.feasible, sizeof v, cudaMemcpyDeviceToHost, s->st));
     CU(cudaStreamSynchronize(s->st));
     *evaluated = v;
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n) {
+    if (!s || !out || n < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    unsigned long long v[2] = {0, 0};
+    if (s->wk.feasible) CU(cudaMemcpyAsync(&v[0], s->wk.feasible, sizeof v[0], cudaMemcpyDeviceToHost, s->st));
+    if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[1], s->wk.rows_done, sizeof v[1], cudaMemcpyDeviceToHost, s->st));
+    CU(cudaStreamSynchronize(s->st));
+    for (int i = 0; i < n; i++) out[i] = i < 2 ? v[i] : 0;
     return ECLIP_OK;
 }
 

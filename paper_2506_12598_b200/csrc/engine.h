@@ -100,6 +100,9 @@ struct Setup {
     int32_t shard, n_shards;
     uint64_t tol_num, tol_den;
     double delta;               // FP32 filter relative error bound
+    int32_t prune;              // fast pass 1: skip rows whose lower bound exceeds the incumbent's band (§3.9)
+    int32_t pad2;
+    int64_t rows_max;           // max rows (hi-digit combinations) over problems (rowlb stride)
 };
 
 // Device view of all level tables
@@ -133,6 +136,25 @@ struct Work {
     U256* first;                // [n] winner: lowest tuple within tolerance, packed (pack_tuple); all-ones = none
     uint64_t* scored;           // [n]
     unsigned long long* feasible;  // [1] QoS-feasible candidates evaluated by the fast pass 1
+    // row-level bound pruning (fast pass 1, W >= 3)
+    float* rowlb;               // [n * rows_max] lower bound of every exact key in the row (+inf: no feasible candidate)
+    unsigned* lbmin;            // [n] min over rows of rowlb (float bits)
+    unsigned* inc;              // [n] incumbent: smallest FP32 key found so far (float bits)
+    float2* hull;               // [n][2][2][Lmax]: step / inner worker lower-left hull vertices {B, S'}, then its
+                                //   edges {B_i - B_i+1, S'_i+1 - S'_i}
+    int32_t* ftab;              // [n * FT_CAP] exact row feasibility: F(t0 + i) (see k_prep_bound)
+    struct RowHdr* rowhdr;      // [n]
+    unsigned long long* rows_done;  // [1] rows (units) pass 1 actually processed
+};
+
+constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem
+
+struct RowHdr {                 // per-problem constants of the row bound (k_prep_bound)
+    int32_t nh[2];              // hull sizes (step, inner)
+    int32_t smin_in, umax_in;   // inner worker: min S', max (Tmax - S')
+    int32_t smin_st, umax_st;   // step worker:  min S', max (Tmax - S')
+    float Sminf_in, Bminf_in;   // inner worker: (float) min S', (float) min B
+    int32_t t0, tn;             // feasibility table covers hT in [t0, t0 + tn); tn = 0: no table
 };
 
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
@@ -156,6 +178,7 @@ size_t pass1_smem(const Setup& su, bool fast);
 bool pass1_fast(int L_inner);
 int pass1_fast_team(int L_inner);
 size_t pass1_aux_bytes(int Lmax);
+bool pass1_prunable(const Setup& su);
 
 
 // ---- comparison planners (baseline.cu) ----

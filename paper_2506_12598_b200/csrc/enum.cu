@@ -18,6 +18,8 @@
 #include <cfloat>
 #include <cstdio>
 
+#include <algorithm>
+
 #include "engine.h"
 
 namespace eclip {
@@ -403,6 +405,234 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
 }
 
 // ------------------------------------------------------------------------------------------
+// Row lower bound.  For a row (hi digits fixed: exact sums hB, hT, hBS), every
+// EXCLUDE_SELF key of the row is, exactly (step level e, inner level k),
+//   K = Xh + B_e Yh + S'_e Zh + B_k Yh + S'_k Zh + (S'_e B_k + S'_k B_e) / (Lambda N)
+// with Xh = hB + (hT hB - hBS)/(Lambda N), Yh = 1 + hT/(Lambda N), Zh = hB/(Lambda N), every term
+// >= 0 (PAPER keys are larger by sum_w B_w S'_w/(Lambda N) >= 0, so the bound holds there too).
+// Bounding the cross term below by S'_e Bmin_k + Smin_k B_e separates the two workers:
+//   K >= Xh + min_e [B_e (Yh + Smin_k/ΛN) + S'_e (Zh + Bmin_k/ΛN)] + min_k [B_k Yh + S'_k Zh]
+// and each minimum of a positive linear form over a point set is attained on its lower-left
+// convex hull (built exactly here, once per problem).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool hull_pop(const Lev& a, const Lev& b, const Lev& c) {
+    // drop b unless it lies strictly below the segment a-c (points (S', B), S' increasing)
+    const __int128 cr = (__int128)(b.S - a.S) * (__int128)(c.B - a.B) - (__int128)(b.B - a.B) * (__int128)(c.S - a.S);
+    return cr <= 0;
+}
+
+// One CTA per problem (256 threads):
+//  * rank-sort the step and inner workers by (S', B, index); one thread per worker builds the
+//    lower-left hull (Pareto staircase + lower convex chain, exact integer orientation tests)
+//    and its edges {B_i - B_i+1 > 0, S'_i+1 - S'_i > 0}, whose slopes decrease along the chain;
+//  * the exact row-feasibility table.  A candidate (row, e, k) meets every QoS bound iff
+//    T' = hT + S'_e + S'_k <= min(hTm, Tmax_e, Tmax_k), i.e. iff
+//        hT <= min(u_e - S'_k, u_k - S'_e)  (u = Tmax - S')   and   S'_e + S'_k <= hTm - hT.
+//    With F(t) = min { S'_e + S'_k : min(u_e - S'_k, u_k - S'_e) >= t } (non-decreasing in t), a
+//    row has a feasible candidate iff F(hT) <= hTm - hT.  F is tabulated for hT in [t0, t1]
+//    (sums of the hi workers' min / max S'), when that range fits FT_CAP entries.
+__global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs, const Lev* levs, float2* hull,
+                                                    int32_t* ftab, RowHdr* hdr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int* G = reinterpret_cast<int*>(smem_raw);                          // [FT_CAP]
+    Lev* sv = reinterpret_cast<Lev*>(G + FT_CAP);                      // [2][Lmax] step, inner records
+    uint16_t* ord = reinterpret_cast<uint16_t*>(sv + 2 * su.Lmax);     // [2][Lmax]
+    uint16_t* stk = ord + 2 * su.Lmax;                                 // [2][Lmax]
+    __shared__ int s_t0, s_t1, s_part[256];
+    const int prob = blockIdx.x;
+    const Prob& P = probs[prob];
+    if (P.status != 0 || su.W < 3) return;
+    const int W = su.W, Lmax = su.Lmax;
+    const Lev* gbase = levs + (size_t)prob * su.lev_stride;
+    for (int i = threadIdx.x; i < 2 * Lmax; i += blockDim.x) sv[i] = gbase[(size_t)(W - 2) * Lmax + i];
+    if (threadIdx.x == 0) { s_t0 = 0; s_t1 = 0; }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // range of hT over the hi workers (warp 0)
+        for (int w = 0; w < W - 2; w++) {
+            int mn = 1 << 30, mx = 0;
+            for (int l = threadIdx.x; l < P.L[w]; l += 32) {
+                const int v = gbase[(size_t)w * Lmax + l].S;
+                mn = min(mn, v); mx = max(mx, v);
+            }
+            for (int o = 16; o; o >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if (threadIdx.x == 0) { s_t0 += mn; s_t1 += mx; }
+        }
+    }
+    for (int which = 0; which < 2; which++) {
+        const Lev* lv = sv + (size_t)which * Lmax;
+        const int L = P.L[W - 2 + which];
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+            const Lev& a = lv[i];
+            int rk = 0;
+            for (int j = 0; j < L; j++) {
+                const Lev& b = lv[j];
+                rk += (b.S < a.S) || (b.S == a.S && (b.B < a.B || (b.B == a.B && j < i)));
+            }
+            ord[which * Lmax + rk] = (uint16_t)i;
+        }
+    }
+    __syncthreads();
+    const int t0 = s_t0, tn = (s_t1 - s_t0 + 1 <= FT_CAP && su.has_qos) ? s_t1 - s_t0 + 1 : 0;
+    if ((threadIdx.x & 31) == 0 && threadIdx.x < 64) {
+        const int which = threadIdx.x >> 5;
+        const Lev* lv = sv + (size_t)which * Lmax;
+        const int L = P.L[W - 2 + which];
+        uint16_t* o = ord + which * Lmax;
+        uint16_t* sk = stk + which * Lmax;
+        int n = 0, umax = -(1 << 30);
+        int64_t bmin = INT64_MAX;
+        for (int t = 0; t < L; t++) {
+            const Lev& p = lv[o[t]];
+            umax = max(umax, p.Tmax - p.S);
+            bmin = min(bmin, p.B);
+            if (n > 0 && p.B >= lv[sk[n - 1]].B) continue;      // dominated (S' not smaller, B not smaller)
+            while (n >= 2 && hull_pop(lv[sk[n - 2]], lv[sk[n - 1]], p)) n--;
+            sk[n++] = o[t];
+        }
+        float2* h = hull + ((size_t)prob * 2 + which) * 2 * Lmax;
+        for (int i = 0; i < n; i++) {
+            const Lev& v = lv[sk[i]];
+            h[i] = make_float2(__ll2float_rn(v.B), (float)v.S);
+            if (i + 1 < n) {
+                const Lev& x = lv[sk[i + 1]];
+                h[Lmax + i] = make_float2(__ll2float_rn(v.B - x.B), (float)(x.S - v.S));
+            }
+        }
+        RowHdr* H = hdr + prob;
+        H->nh[which] = n;
+        const int smin = lv[o[0]].S;
+        if (which == 0) { H->smin_st = smin; H->umax_st = umax; H->t0 = t0; H->tn = tn; }
+        else { H->smin_in = smin; H->umax_in = umax; H->Sminf_in = (float)smin; H->Bminf_in = __ll2float_rn(bmin); }
+    }
+    if (tn == 0) return;
+    // F(t) for t in [t0, t0 + tn): bucket every (e, k) pair at its last valid t, then a suffix minimum
+    for (int i = threadIdx.x; i < tn; i += blockDim.x) G[i] = INT_MAX;
+    __syncthreads();
+    const Lev* st = sv;
+    const Lev* in = sv + Lmax;
+    const int Le = P.L[W - 2], Lk = P.L[W - 1];
+    for (int pidx = threadIdx.x; pidx < Le * Lk; pidx += blockDim.x) {
+        const Lev& e = st[pidx / Lk];
+        const Lev& k = in[pidx % Lk];
+        const int tm = min(e.Tmax - e.S - k.S, k.Tmax - k.S - e.S);
+        if (tm < t0) continue;
+        atomicMin(&G[min(tm, t0 + tn - 1) - t0], e.S + k.S);
+    }
+    __syncthreads();
+    const int chunk = (tn + blockDim.x - 1) / blockDim.x;
+    const int c0 = threadIdx.x * chunk, c1 = min(tn, c0 + chunk);
+    int m = INT_MAX;
+    for (int i = c1 - 1; i >= c0; i--) { m = min(m, G[i]); G[i] = m; }
+    s_part[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int i = (int)blockDim.x - 2; i >= 0; i--) s_part[i] = min(s_part[i], s_part[i + 1]);
+    __syncthreads();
+    const int after = threadIdx.x + 1 < (int)blockDim.x ? s_part[threadIdx.x + 1] : INT_MAX;
+    for (int i = c0; i < c1; i++) ftab[(size_t)prob * FT_CAP + i] = min(G[i], after);
+}
+
+// min over a lower-left hull of B y + S' z (y, z > 0): the edge slopes (B_i - B_i+1)/(S'_i+1 - S'_i)
+// decrease along the chain, so the minimiser is the first vertex whose outgoing edge has
+// slope <= z / y (binary search); its neighbours are evaluated too.  A vertex picked wrongly
+// because of FP32 rounding of the slope test differs from the minimum by <= ~1e-6 relative
+// (the misjudged edges have slopes within rounding of z/y), far inside the bound's margin.
+__device__ __forceinline__ float hull_min(const float2* v, const float2* ed, int n, float y, float z) {
+    int lo = 0, hi = n - 1;   // first edge index i in [0, n-1) with slope_i <= z/y, else n-1
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float2 e = ed[mid];
+        if (e.x * y > e.y * z) lo = mid + 1; else hi = mid;
+    }
+    float m = fmaf(v[lo].x, y, v[lo].y * z);
+    if (lo > 0) m = fminf(m, fmaf(v[lo - 1].x, y, v[lo - 1].y * z));
+    if (lo + 1 < n) m = fminf(m, fmaf(v[lo + 1].x, y, v[lo + 1].y * z));
+    return m;
+}
+
+// one thread per row: the bound above, times (1 - 2^-16) (covers its FP32 rounding, <= 16u, and
+// the hull search), or +inf when no candidate of the row meets every QoS bound (exact)
+template <int NW, bool QOS>
+__global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, const Lev* levs, const float2* hull,
+                                               const int32_t* ftab, const RowHdr* hdr, float* rowlb,
+                                               unsigned* lbmin) {
+    constexpr int NH = NW - 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* sh = reinterpret_cast<float2*>(smem_raw);   // [2][2][Lmax]
+    __shared__ float red[8];
+    const int prob = blockIdx.y;
+    const Prob& P = probs[prob];
+    if (P.status != 0) return;
+    const RowHdr H = hdr[prob];
+    const int Lmax = su.Lmax;
+    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)prob * 4 * Lmax + i];
+    __syncthreads();
+    const Lev* base = levs + (size_t)prob * su.lev_stride;
+    const uint64_t rows = P.units / (uint64_t)P.nseg;
+    const int32_t* ft = ftab + (size_t)prob * FT_CAP;
+    const float invf = P.inv;
+    uint32_t Lh[NH > 0 ? NH : 1];
+#pragma unroll
+    for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
+    float bm = INFINITY;
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t hB = 0, hBS = 0;
+        int hT = 0, hTm = 1 << 24;
+        if (rows <= 0xffffffffull) {
+            uint32_t x = (uint32_t)r;
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                const uint32_t d = x % Lh[w];
+                x /= Lh[w];
+                const Lev& v = base[(size_t)w * Lmax + d];
+                hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
+            }
+        } else {
+            uint64_t x = r;
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                const int d = (int)(x % (uint64_t)Lh[w]);
+                x /= (uint64_t)Lh[w];
+                const Lev& v = base[(size_t)w * Lmax + d];
+                hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
+            }
+        }
+        bool feas = true;
+        if (QOS) {
+            if (H.tn > 0) feas = ft[hT - H.t0] <= hTm - hT;
+            else feas = !(H.smin_st > min(hTm - hT - H.smin_in, H.umax_in - hT) || H.umax_st < hT + H.smin_in);
+        }
+        float lb = INFINITY;
+        if (feas) {
+            const float hBf = __ll2float_rn(hB), hTf = (float)hT;
+            const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
+            const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
+            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            const float Xh = fmaf(Dhf, invf, hBf);
+            const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
+            lb = (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
+                 0.99998474121f;   // 1 - 2^-16
+        }
+        rowlb[(size_t)prob * su.rows_max + r] = lb;
+        bm = fminf(bm, lb);
+    }
+    for (int o = 16; o; o >>= 1) bm = fminf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = bm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++) bm = fminf(bm, red[i]);
+        if (bm < INFINITY) atomicMin(lbmin + prob, __float_as_uint(bm));
+    }
+}
+
+__global__ void k_fill_u32(unsigned* p, size_t n, unsigned v) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// ------------------------------------------------------------------------------------------
 // pass 1
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned team_mask(int T) {
@@ -413,6 +643,15 @@ __device__ __forceinline__ unsigned team_mask(int T) {
 __device__ __forceinline__ float team_min(float m, int T, unsigned mask) {
     for (int o = T / 2; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(mask, m, o));
     return m;
+}
+
+__device__ float band_bound(const Setup& su, float m, float ms) {
+    // every candidate with exact key <= H*(1+tau) has key32 <= bound; H* <= ms / (1 - delta)
+    double base = (su.mode == M_MATRIX && su.has_qos) ? (double)ms : (double)m;
+    if (isinf(base)) return INFINITY;
+    double tau = (double)su.tol_num / (double)su.tol_den;
+    double b = base * (1.0 + tau) * (1.0 + su.delta) / (1.0 - su.delta) * (1.0 + 1e-12);
+    return __double2float_ru(b);
 }
 
 struct HiSums {
@@ -454,10 +693,25 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 //       index of the suffix-minimum of u that reaches Tp (exact when u is non-decreasing in S',
 //       i.e. B* non-increasing; otherwise the earlier levels are swept with a mask).
 // Both ends come from lookup tables indexed by value (binary search if a range is too wide).
-template <int NW, int MODE, bool QOS>
+// Row pruning (BB): a unit is processed only if its row bound lies in this
+// wave's window (lbmin*lo_f, lbmin*hi_f] and below the band of the problem's incumbent `inc`
+// (the smallest FP32 key found so far, updated here); skipped units keep submin = +inf.
+struct BBArgs {
+    const float* rowlb;
+    const unsigned* lbmin;
+    unsigned* inc;
+    unsigned long long* rows_done;
+};
+// Waves: each CTA processes its units in windows of their bound relative to the
+// problem's smallest bound, so the rows most likely to hold the optimum set the incumbent before
+// the bulk of the rows is tested against it.
+constexpr int BB_NWAVE = 5;
+__constant__ float c_bb_wave[BB_NWAVE] = {1.001f, 1.005f, 1.02f, 1.1f, INFINITY};
+
+template <int NW, int MODE, bool QOS, bool BB>
 __global__ void __launch_bounds__(P1_THREADS, 2)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
-             unsigned long long* __restrict__ feasible) {
+             unsigned long long* __restrict__ feasible, BBArgs bb) {
     constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
@@ -470,6 +724,20 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     item_of_block(su, P, blockIdx.x % ipS, &item, &ok);
     if (!ok) return;
     const int W = NW, Lmax = su.Lmax;
+    const uint64_t units = P.units;
+    uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
+    if (ub > units) ub = units;
+    const int nseg = P.nseg;
+    const float* rlb = BB ? bb.rowlb + (size_t)prob * su.rows_max : nullptr;
+    __shared__ unsigned s_inc;
+    float lbm = 0.0f;
+    if (BB) {   // leave before staging if no unit of this item can hold a feasible candidate
+        lbm = __uint_as_float(bb.lbmin[prob]);
+        bool any = false;
+        for (uint64_t u = ua + threadIdx.x; u < ub && !any; u += blockDim.x) any = rlb[u / (uint64_t)nseg] < INFINITY;
+        if (!__syncthreads_or(any)) return;
+        if (threadIdx.x == 0) s_inc = 0x7f800000u;
+    }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
     stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
@@ -480,8 +748,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     for (int w = 0; w < NW; w++) L[w] = P.L[w];
     const int Lin = L[NW - 1];
     const Lev* stepw = sl + (W >= 2 ? (W - 2) : 0) * Lmax;
-    const int segl = P.seglen, nseg = P.nseg, Lstep = P.Lstep;
-    const uint64_t units = P.units;
+    const int segl = P.seglen, Lstep = P.Lstep;
     float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + su.aux_bytes);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
     constexpr int NWARP = P1_THREADS / 32;
@@ -498,39 +765,58 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const int sulast = step_tab ? A.stU[P.Lstep - 1] : 0;
     float* subp = submin + (size_t)prob * su.units_max;
 
-    uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
-    if (ub > units) ub = units;
-    // this warp's units: ua + warp, + NWARP, ... ; (row, seg) and the hi digits advance incrementally
-    uint64_t unit = ua + (uint64_t)warp;
-    int seg = (int)(unit % (uint64_t)nseg);
-    uint64_t row = unit / (uint64_t)nseg;
-    int d[NH > 0 ? NH : 1];
-#pragma unroll
-    for (int w = NH - 1; w >= 0; w--) { d[w] = (int)(row % (uint64_t)L[w]); row /= (uint64_t)L[w]; }
-    const int dq = NWARP / nseg, dr = NWARP % nseg;
-    unsigned long long nfeas = 0;
-    for (; unit < ub; unit += NWARP) {
-        const int e0 = seg * segl, e1 = min(Lstep, e0 + segl);
-        HiSums h;
-        h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
-#pragma unroll
-        for (int w = 0; w < NH; w++) {
-            const Lev& r = sl[w * Lmax + d[w]];
-            h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
-        }
-        // advance to this warp's next unit (no divisions)
-        {
-            seg += dr;
-            int carry = dq;
-            if (seg >= nseg) { seg -= nseg; carry++; }
-#pragma unroll
-            for (int w = NH - 1; w >= 0; w--) {
-                int v = d[w] + carry;
-                carry = 0;
-                while (v >= L[w]) { v -= L[w]; carry++; }
-                d[w] = v;
+    // this warp's units: 32 consecutive units per round (rounds strided by NWARP * 32); the row
+    // bounds of the 32 are checked lane-parallel, the wanted units are then processed one by one
+    unsigned long long nfeas = 0, ndone = 0;
+    float bnd = INFINITY, incv = INFINITY, tlo = 0.0f, thi = 0.0f;
+  for (int wave = 0; wave < (BB ? BB_NWAVE : 1); wave++) {
+    if (BB) {   // this CTA's incumbent: its own best so far and every other CTA's (global)
+        tlo = wave ? lbm * c_bb_wave[wave - 1] : -INFINITY;
+        thi = lbm * c_bb_wave[wave];
+        __syncthreads();
+        if (threadIdx.x == 0) s_inc = min(s_inc, *(volatile const unsigned*)(bb.inc + prob));
+        __syncthreads();
+    }
+    for (uint64_t base = ua + (uint64_t)warp * 32; base < ub; base += (uint64_t)NWARP * 32) {
+        bool want = base + wl < ub;
+        if (BB) {
+            incv = __uint_as_float(*(volatile unsigned*)&s_inc);
+            bnd = band_bound(su, incv, 0.0f);
+            if (want) {
+                const float lb = rlb[(base + wl) / (uint64_t)nseg];
+                want = lb < INFINITY && lb > tlo && lb <= thi && lb <= bnd;
             }
         }
+        unsigned pend = __ballot_sync(0xffffffffu, want);
+      while (pend) {
+        const uint64_t unit = base + (uint64_t)(__ffs(pend) - 1);
+        pend &= pend - 1;
+        if (BB) ndone++;
+        int seg;
+        HiSums h;
+        h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
+        if (units <= 0xffffffffull) {   // 32-bit decode (the common case)
+            uint32_t row = (uint32_t)unit;
+            if (nseg > 1) { seg = (int)(row % (uint32_t)nseg); row /= (uint32_t)nseg; } else seg = 0;
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                const uint32_t dw = row % (uint32_t)L[w];
+                row /= (uint32_t)L[w];
+                const Lev& r = sl[w * Lmax + dw];
+                h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
+            }
+        } else {
+            seg = (int)(unit % (uint64_t)nseg);
+            uint64_t row = unit / (uint64_t)nseg;
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                const int dw = (int)(row % (uint64_t)L[w]);
+                row /= (uint64_t)L[w];
+                const Lev& r = sl[w * Lmax + dw];
+                h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
+            }
+        }
+        const int e0 = seg * segl, e1 = min(Lstep, e0 + segl);
         int ne = e1 - e0;
         int sb = 1 << 30;
         int ea = e0;
@@ -678,11 +964,21 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         float m = fminf(m0, m1);
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (wl == 0) subp[unit] = m;
+        if (wl == 0) {
+            subp[unit] = m;
+            if (BB && m < incv) {
+                atomicMin(&s_inc, __float_as_uint(m));
+                atomicMin(bb.inc + prob, __float_as_uint(m));
+                incv = m;
+            }
+        }
         __syncwarp();   // the table is rewritten for the next unit
+      }
     }
+  }
     for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
     if (wl == 0 && nfeas) atomicAdd(feasible, nfeas);
+    if (BB && wl == 0 && ndone) atomicAdd(bb.rows_done, ndone);
 }
 
 // Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
@@ -809,14 +1105,17 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
 // ------------------------------------------------------------------------------------------
 // pass-1 dispatch
 // ------------------------------------------------------------------------------------------
-typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*, unsigned long long*);
+typedef void (*P1Fast)(Setup, const Prob*, const Lev*, float*, unsigned long long*, BBArgs);
 typedef void (*P1Gen)(Setup, const Prob*, const Lev*, float*, float*);
+typedef void (*RowLB)(Setup, const Prob*, const Lev*, const float2*, const int32_t*, const RowHdr*, float*, unsigned*);
 
-template <int NW>
+template <int NW, bool BB>
 static P1Fast pick_fast(int mode, bool qos) {
-    if (mode == M_EXCL) return qos ? k_pass1_fast<NW, M_EXCL, true> : k_pass1_fast<NW, M_EXCL, false>;
-    return qos ? k_pass1_fast<NW, M_PAPER, true> : k_pass1_fast<NW, M_PAPER, false>;
+    if (mode == M_EXCL) return qos ? k_pass1_fast<NW, M_EXCL, true, BB> : k_pass1_fast<NW, M_EXCL, false, BB>;
+    return qos ? k_pass1_fast<NW, M_PAPER, true, BB> : k_pass1_fast<NW, M_PAPER, false, BB>;
 }
+template <int NW>
+static RowLB pick_rowlb(bool qos) { return qos ? k_rowlb<NW, true> : k_rowlb<NW, false>; }
 
 template <int NP, int MODE>
 static P1Gen pick_gen_m(int obj, bool qos) {
@@ -840,6 +1139,17 @@ static bool use_fast(const Setup& su) {
     return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax);
 }
 
+bool pass1_prunable(const Setup& su) { return su.prune != 0 && su.W >= 3 && use_fast(su); }
+
+static cudaError_t fill_u32(void* p, size_t n, unsigned v, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    size_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_fill_u32<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<unsigned*>(p), n, v);
+    return cudaGetLastError();
+}
+
+
 size_t pass1_smem(const Setup& su, bool fast) {
     size_t s = (size_t)su.W * su.Lmax * sizeof(Lev);
     if (fast) s += (size_t)su.aux_bytes + (size_t)su.table_bytes;   // aux block + per-warp prefix tables
@@ -854,22 +1164,53 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
     if (grid == 0) return cudaSuccess;
     const bool fast = use_fast(su);
     const size_t smem = pass1_smem(su, fast);
-    if (fast) {
+    if (fast && pass1_prunable(su)) {
+        P1Fast f = nullptr;
+        RowLB r = nullptr;
+        switch (su.W) {
+            case 3: f = pick_fast<3, true>(su.mode, qos); r = pick_rowlb<3>(qos); break;
+            case 4: f = pick_fast<4, true>(su.mode, qos); r = pick_rowlb<4>(qos); break;
+            case 5: f = pick_fast<5, true>(su.mode, qos); r = pick_rowlb<5>(qos); break;
+            case 6: f = pick_fast<6, true>(su.mode, qos); r = pick_rowlb<6>(qos); break;
+            case 7: f = pick_fast<7, true>(su.mode, qos); r = pick_rowlb<7>(qos); break;
+            case 8: f = pick_fast<8, true>(su.mode, qos); r = pick_rowlb<8>(qos); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e;
+        const size_t n = (size_t)su.n_problems;
+        if ((e = fill_u32(wk.submin, n * (size_t)su.units_max, 0x7f800000u, st)) != cudaSuccess) return e;
+        if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
+        if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
+        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 * sizeof(Lev));
+        if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
+            return e;
+        k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr);
+        // enough CTAs to fill the GPU (8 per SM), each looping over many rows of its problem
+        const long long want = std::max<long long>(1, (148LL * 8 + su.n_problems - 1) / su.n_problems);
+        const long long gx = std::min<long long>((su.rows_max + 255) / 256, want);
+        r<<<dim3((unsigned)gx, (unsigned)su.n_problems), 256, (size_t)su.Lmax * 32, st>>>(
+            su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.rowlb, wk.lbmin);
+        if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return e;
+        BBArgs bb{wk.rowlb, wk.lbmin, wk.inc, wk.rows_done};
+        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
+    } else if (fast) {
         P1Fast f = nullptr;
         switch (su.W) {
-            case 1: f = pick_fast<1>(su.mode, qos); break;
-            case 2: f = pick_fast<2>(su.mode, qos); break;
-            case 3: f = pick_fast<3>(su.mode, qos); break;
-            case 4: f = pick_fast<4>(su.mode, qos); break;
-            case 5: f = pick_fast<5>(su.mode, qos); break;
-            case 6: f = pick_fast<6>(su.mode, qos); break;
-            case 7: f = pick_fast<7>(su.mode, qos); break;
-            case 8: f = pick_fast<8>(su.mode, qos); break;
+            case 1: f = pick_fast<1, false>(su.mode, qos); break;
+            case 2: f = pick_fast<2, false>(su.mode, qos); break;
+            case 3: f = pick_fast<3, false>(su.mode, qos); break;
+            case 4: f = pick_fast<4, false>(su.mode, qos); break;
+            case 5: f = pick_fast<5, false>(su.mode, qos); break;
+            case 6: f = pick_fast<6, false>(su.mode, qos); break;
+            case 7: f = pick_fast<7, false>(su.mode, qos); break;
+            case 8: f = pick_fast<8, false>(su.mode, qos); break;
             default: return cudaErrorInvalidValue;
         }
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible);
+        BBArgs bb{};
+        f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
     } else {
         P1Gen f = nullptr;
         switch (NP) {
@@ -1011,14 +1352,6 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
     return feas;
 }
 
-__device__ float band_bound(const Setup& su, float m, float ms) {
-    // every candidate with exact key <= H*(1+tau) has key32 <= bound; H* <= ms / (1 - delta)
-    double base = (su.mode == M_MATRIX && su.has_qos) ? (double)ms : (double)m;
-    if (isinf(base)) return INFINITY;
-    double tau = (double)su.tol_num / (double)su.tol_den;
-    double b = base * (1.0 + tau) * (1.0 + su.delta) / (1.0 - su.delta) * (1.0 + 1e-12);
-    return __double2float_ru(b);
-}
 
 // One CTA per problem.  PASS 0: exact minimum H* over the band.  PASS 1: lowest index whose exact
 // key is within tol of the (global) H*.  PASS 2 (unsharded runs): both in one rescan -- the band's

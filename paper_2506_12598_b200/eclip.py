@@ -52,7 +52,7 @@ class Result(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("engine", C.c_int32), ("device", C.c_int32), ("cuda_stream", C.c_void_p), ("tie_tol", C.c_double),
-                ("shard", C.c_int32), ("n_shards", C.c_int32)]
+                ("shard", C.c_int32), ("n_shards", C.c_int32), ("no_prune", C.c_int32)]
 
 
 class Batch(C.Structure):
@@ -76,6 +76,7 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_plan_batch", "eclip_session_create", "eclip_session_pass1", "eclip_session_pass2_min",
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
            "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats",
+           "eclip_session_counters",
            "eclip_baseline_plan", "eclip_lookup_table_json"]
 
 
@@ -108,6 +109,7 @@ def lib():
         L.eclip_session_finish.argtypes = [vp, P(C.c_uint64), P(BatchOut)]
         L.eclip_session_finish_problem.argtypes = [vp, P(C.c_uint64), P(Result)]
         L.eclip_session_stats.argtypes = [vp, P(C.c_uint64)]
+        L.eclip_session_counters.argtypes = [vp, P(C.c_uint64), C.c_int32]
         L.eclip_session_free.argtypes = [vp]
         L.eclip_session_free.restype = None
         L.eclip_baseline_plan.argtypes = [vp, P(Problem), C.c_int32, C.c_double, P(Options), P(Result)]
@@ -219,7 +221,7 @@ class Plan:
     exact_key: int
 
 
-def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1) -> Options:
+def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True) -> Options:
     o = Options()
     lib().eclip_default_options(C.byref(o))
     o.engine = ENGINES[engine]
@@ -227,6 +229,7 @@ def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shar
     o.cuda_stream = stream if isinstance(stream, int) or stream is None else getattr(stream, "cuda_stream", stream)
     o.tie_tol = tie_tol
     o.shard, o.n_shards = shard, n_shards
+    o.no_prune = 0 if prune else 1
     return o
 
 
@@ -290,11 +293,11 @@ def _to_plan(r: Result, bufs, G) -> Plan:
 def plan(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
          objective: str = "sum", allowed_mask=None, qos_ns=None, slowdown_matrix=None, group_bounds=None,
          p_idle_w: float = 75.0, p_max_w: float = 225.0, engine: str = "auto", tie_tol: float = 1e-5,
-         device: int = 0, stream=None) -> Plan:
+         device: int = 0, stream=None, prune: bool = True) -> Plan:
     """eclip_plan: the exact optimum of one co-location problem (§IV-B)."""
     a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
                      slowdown_matrix, group_bounds, p_idle_w, p_max_w)
-    o = _options(engine, device, stream, tie_tol)
+    o = _options(engine, device, stream, tie_tol, prune=prune)
     r, bufs = _result_buffers(a.W, a.G)
     _check(lib().eclip_plan(profiles.handle, C.byref(a.c), C.byref(o), C.byref(r)))
     return _to_plan(r, bufs, a.G)
@@ -391,7 +394,8 @@ def _batch_out_struct(out) -> BatchOut:
 
 def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
                objective: str = "sum", qos_ns=None, slowdown_matrix=None, allowed_mask=None, p_idle_w: float = 75.0,
-               p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0, stream=None, out=None, gmax: int = 0):
+               p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0, stream=None, out=None, gmax: int = 0,
+               prune: bool = True):
     """eclip_plan_batch: many independent mixes per launch (BASELINE config 5).
 
     With torch CUDA tensors for model_ids / qos_ns / slowdown_matrix (and `out` from
@@ -402,7 +406,7 @@ def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int
     if out is None:
         out = alloc_batch_out(a.n, a.W, gmax, device=(model_ids.device if on_device else None))
     b = _batch_out_struct(out)
-    o = _options("enum", device, stream, tie_tol)
+    o = _options("enum", device, stream, tie_tol, prune=prune)
     _check(lib().eclip_plan_batch(profiles.handle, C.byref(a.c), C.byref(o), C.byref(b)))
     return out
 
@@ -413,10 +417,10 @@ class Session:
     the per-step values across shards (see parallel.py)."""
 
     def __init__(self, profiles: Profiles, *, problem=None, batch=None, shard=0, n_shards=1, engine="auto",
-                 tie_tol=1e-5, device=0, stream=None, **problem_kw):
+                 tie_tol=1e-5, device=0, stream=None, prune=True, **problem_kw):
         self.profiles = profiles
         self._h = C.c_void_p()
-        o = _options(engine, device, stream, tie_tol, shard, n_shards)
+        o = _options(engine, device, stream, tie_tol, shard, n_shards, prune)
         if problem is not None:
             self.args = _ProblemArgs(profiles, problem.model_ids, problem.total_sms, problem.switch_max, problem.mode,
                                      problem.objective, problem.allowed_mask, problem.qos_ns,
@@ -464,10 +468,11 @@ class Session:
         return out
 
     def stats(self) -> dict:
-        """counters of the last pass 1 (evaluated = QoS-feasible candidates scored in FP32)"""
-        v = C.c_uint64()
-        _check(lib().eclip_session_stats(self._h, C.byref(v)))
-        return {"evaluated_candidates": int(v.value)}
+        """counters of the last pass 1: evaluated = QoS-feasible candidates scored in FP32;
+        units_processed = pass-1 units (rows) not pruned by their bound (0 when pruning is off)"""
+        v = (C.c_uint64 * 2)()
+        _check(lib().eclip_session_counters(self._h, v, 2))
+        return {"evaluated_candidates": int(v[0]), "units_processed": int(v[1])}
 
     def close(self):
         if self._h is not None and self._h.value:

@@ -327,3 +327,48 @@ def test_batch_paper_mode_and_masks():
         if o.status == "ok":
             assert out["winner_levels"][i].tolist() == o.levels, i
             assert out["objective"][i] == pytest.approx(o.objective, rel=REL)
+
+
+# ---------------------------------------------------------------- row-bound pruning
+@pytest.mark.parametrize("mode,qf", [("exclude_self", 1.0), ("exclude_self", None), ("paper", 2.0)])
+def test_pruned_equals_exhaustive_batch(mode, qf):
+    """pruning is exact: the same winners, keys and values as classifying every candidate"""
+    models, ids, qos = synth.make_c5(256, seed=31)
+    pr = ec.Profiles.from_models(models)
+    kw = dict(total_sms=148, slowdown=mode, qos_ns=None if qf is None else qos * qf, p_idle_w=200.0,
+              p_max_w=1000.0, gmax=16)
+    a = ec.plan_batch(pr, ids, prune=True, **kw)
+    b = ec.plan_batch(pr, ids, prune=False, **kw)
+    for k in ("status", "winner_index", "winner_levels", "objective", "group_sm", "model_latency_ns"):
+        assert np.array_equal(a[k], b[k]), k
+    # and the pruned pass 1 really skipped rows
+    batch = dict(model_ids=ids, total_sms=148, slowdown=mode, p_idle_w=200.0, p_max_w=1000.0)
+    if qf is not None:
+        batch["qos_ns"] = qos * qf
+    s = ec.Session(pr, batch=batch, engine="enum")
+    s.pass1()
+    rows = sum(int(np.prod([pr_levels(pr, m) for m in row[:2]])) for row in ids)
+    done = s.stats()["units_processed"]
+    s.close()
+    assert 0 < done < rows
+
+
+def pr_levels(pr, m, _cache={}):
+    key = (id(pr), m)
+    if key not in _cache:
+        _cache[key] = ec.plan(pr, [m], total_sms=148, switch_max=14).candidates
+    return _cache[key]
+
+
+def test_pruned_sampled_mixes_vs_oracle_without_qos():
+    """no QoS: pruning is the only thing that skips work; sampled mixes vs the oracle"""
+    models, ids, _ = synth.make_c5(32, seed=41)
+    pr = ec.Profiles.from_models(models)
+    out = ec.plan_batch(pr, ids, total_sms=148, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+    for i in range(0, 32, 4):
+        p = synth.c5_problem(i, models, ids, np.full_like(ids, np.inf, dtype=np.float64))
+        p.qos_ns = None
+        o = oracle.solve(p, "slice")
+        assert o.status == "ok" and int(out["status"][i]) == 0
+        assert out["winner_levels"][i].tolist() == o.levels, i
+        assert int(out["winner_index"][i]) == o.index, i
