@@ -590,6 +590,8 @@ static int alloc_work(eclip_session* s) {
     if (s->engine == ECLIP_ENGINE_ENUM) {
         size_t ns = n * (size_t)su.units_max;
         CU(s->arena.alloc(&wk.submin, ns));
+        CU(s->arena.alloc(&wk.bandn, n));
+        CU(s->arena.alloc(&wk.bandlist, n * (size_t)BAND_CAP));
         if (su.mode == M_MATRIX && su.has_qos) CU(s->arena.alloc(&wk.submin_sure, ns));
     }
     CU(s->arena.alloc(&wk.m32, n));
@@ -606,6 +608,9 @@ static int alloc_work(eclip_session* s) {
         CU(s->arena.alloc(&wk.inc, n));
         CU(s->arena.alloc(&wk.hull, n * 4 * (size_t)su.Lmax));
         CU(s->arena.alloc(&wk.ftab, n * (size_t)FT_CAP));
+        const size_t grid = n * (size_t)((su.items_max + su.n_shards - 1) / su.n_shards);
+        CU(s->arena.alloc(&wk.ulist, grid * (size_t)su.upi));
+        CU(s->arena.alloc(&wk.ulist_n, grid));
         CU(s->arena.alloc(&wk.rowhdr, n));
     }
     return ECLIP_OK;

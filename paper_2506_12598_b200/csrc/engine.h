@@ -143,11 +143,16 @@ struct Work {
     float2* hull;               // [n][2][2][Lmax]: step / inner worker lower-left hull vertices {B, S'}, then its
                                 //   edges {B_i - B_i+1, S'_i+1 - S'_i}
     int32_t* ftab;              // [n * FT_CAP] exact row feasibility: F(t0 + i) (see k_prep_bound)
+    uint2* ulist;               // [pass-1 grid][upi] bucket-ordered candidate units of each item (k_bucket)
+    int32_t* ulist_n;           // [pass-1 grid]
     struct RowHdr* rowhdr;      // [n]
     unsigned long long* rows_done;  // [1] rows (units) pass 1 actually processed
+    int32_t* bandn;             // [n] units in the pass-2 band list (-1: more than BAND_CAP, rescan all)
+    uint64_t* bandlist;         // [n * BAND_CAP] band units in index order (k_reduce_min)
 };
 
 constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem
+constexpr int BAND_CAP = 64;    // pass-2 band list capacity per problem
 
 struct RowHdr {                 // per-problem constants of the row bound (k_prep_bound)
     int32_t nh[2];              // hull sizes (step, inner)

@@ -697,16 +697,67 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 // wave's window (lbmin*lo_f, lbmin*hi_f] and below the band of the problem's incumbent `inc`
 // (the smallest FP32 key found so far, updated here); skipped units keep submin = +inf.
 struct BBArgs {
-    const float* rowlb;
-    const unsigned* lbmin;
-    unsigned* inc;
+    const uint2* ulist;         // [grid][upi] this item's candidate units {unit - ua, bound bits}, bucket-ordered
+    const int32_t* ulist_n;     // [grid]
+    const unsigned* lbmin;      // [n] smallest row bound of the problem (float bits)
+    unsigned* inc;              // [n] global incumbent (float bits)
     unsigned long long* rows_done;
 };
-// Waves: each CTA processes its units in windows of their bound relative to the
-// problem's smallest bound, so the rows most likely to hold the optimum set the incumbent before
-// the bulk of the rows is tested against it.
-constexpr int BB_NWAVE = 5;
-__constant__ float c_bb_wave[BB_NWAVE] = {1.001f, 1.005f, 1.02f, 1.1f, INFINITY};
+// Best-first order: each item's units with a finite row bound are listed by
+// bucket of bound / (smallest bound of the problem) - 1 in steps of 1/BB_SCALE (counting sort,
+// k_bucket), so the rows most likely to hold the optimum set the incumbent first, and the list
+// can be abandoned as soon as a bucket's lower edge leaves the incumbent's band.
+constexpr int BB_NB = 256;
+constexpr float BB_SCALE = 1024.0f;
+__device__ __forceinline__ int bb_bucket(float lb, float lbm) {
+    const float r = __fmul_rn(__fsub_rn(__fdiv_rn(lb, lbm), 1.0f), BB_SCALE);
+    return r <= 0.0f ? 0 : (r >= (float)(BB_NB - 1) ? BB_NB - 1 : (int)r);
+}
+// a value <= every bound in bucket b (one bucket of slack covers the rounding of bb_bucket)
+__device__ __forceinline__ float bb_edge(int b, float lbm) { return b <= 1 ? 0.0f : lbm * (1.0f + (float)(b - 1) / BB_SCALE); }
+
+// one CTA per pass-1 item: counting sort of the item's units with a finite row bound by bucket
+__global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, const float* rowlb, const unsigned* lbmin,
+                                                uint2* ulist, int32_t* ulist_n) {
+    __shared__ int hist[BB_NB], cur[BB_NB];
+    const int ipS = (su.items_max + su.n_shards - 1) / su.n_shards;
+    const int prob = blockIdx.x / ipS;
+    const Prob& P = probs[prob];
+    uint64_t item = 0;
+    bool ok = P.status == 0;
+    if (ok) item_of_block(su, P, blockIdx.x % ipS, &item, &ok);
+    if (!ok) {
+        if (threadIdx.x == 0) ulist_n[blockIdx.x] = 0;
+        return;
+    }
+    uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
+    if (ub > P.units) ub = P.units;
+    const int nseg = P.nseg;
+    const float* rlb = rowlb + (size_t)prob * su.rows_max;
+    const float lbm = __uint_as_float(lbmin[prob]);
+    for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint64_t u = ua + threadIdx.x; u < ub; u += blockDim.x) {
+        const float lb = rlb[nseg == 1 ? u : u / (uint64_t)nseg];
+        if (lb < INFINITY) atomicAdd(&hist[bb_bucket(lb, lbm)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
+        int v[BB_NB / 32], t = 0;
+        for (int i = 0; i < BB_NB / 32; i++) { v[i] = hist[threadIdx.x * (BB_NB / 32) + i]; t += v[i]; }
+        int x = t;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (threadIdx.x >= o) x += y; }
+        int run = x - t;
+        for (int i = 0; i < BB_NB / 32; i++) { cur[threadIdx.x * (BB_NB / 32) + i] = run; run += v[i]; }
+        if (threadIdx.x == 31) ulist_n[blockIdx.x] = x;
+    }
+    __syncthreads();
+    uint2* out = ulist + (size_t)blockIdx.x * su.upi;
+    for (uint64_t u = ua + threadIdx.x; u < ub; u += blockDim.x) {
+        const float lb = rlb[nseg == 1 ? u : u / (uint64_t)nseg];
+        if (lb < INFINITY) out[atomicAdd(&cur[bb_bucket(lb, lbm)], 1)] = make_uint2((unsigned)(u - ua), __float_as_uint(lb));
+    }
+}
 
 template <int NW, int MODE, bool QOS, bool BB>
 __global__ void __launch_bounds__(P1_THREADS, 2)
@@ -728,15 +779,17 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     uint64_t ua = item * (uint64_t)su.upi, ub = ua + (uint64_t)su.upi;
     if (ub > units) ub = units;
     const int nseg = P.nseg;
-    const float* rlb = BB ? bb.rowlb + (size_t)prob * su.rows_max : nullptr;
     __shared__ unsigned s_inc;
+    __shared__ int s_next, s_stop;
     float lbm = 0.0f;
+    int lcnt = 0;
+    const uint2* lst = nullptr;
     if (BB) {   // leave before staging if no unit of this item can hold a feasible candidate
+        lcnt = bb.ulist_n[blockIdx.x];
+        if (lcnt == 0) return;
+        lst = bb.ulist + (size_t)blockIdx.x * su.upi;
         lbm = __uint_as_float(bb.lbmin[prob]);
-        bool any = false;
-        for (uint64_t u = ua + threadIdx.x; u < ub && !any; u += blockDim.x) any = rlb[u / (uint64_t)nseg] < INFINITY;
-        if (!__syncthreads_or(any)) return;
-        if (threadIdx.x == 0) s_inc = 0x7f800000u;
+        if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; s_stop = 0; }
     }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
@@ -765,32 +818,50 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const int sulast = step_tab ? A.stU[P.Lstep - 1] : 0;
     float* subp = submin + (size_t)prob * su.units_max;
 
-    // this warp's units: 32 consecutive units per round (rounds strided by NWARP * 32); the row
-    // bounds of the 32 are checked lane-parallel, the wanted units are then processed one by one
+    // BB: warps take 32 list entries at a time (best-first), process the ones within the band of the
+    // incumbent, and stop when the rest of the list is provably outside it.  Otherwise: 32
+    // consecutive units per round, rounds strided by NWARP * 32.
     unsigned long long nfeas = 0, ndone = 0;
-    float bnd = INFINITY, incv = INFINITY, tlo = 0.0f, thi = 0.0f;
-  for (int wave = 0; wave < (BB ? BB_NWAVE : 1); wave++) {
-    if (BB) {   // this CTA's incumbent: its own best so far and every other CTA's (global)
-        tlo = wave ? lbm * c_bb_wave[wave - 1] : -INFINITY;
-        thi = lbm * c_bb_wave[wave];
-        __syncthreads();
-        if (threadIdx.x == 0) s_inc = min(s_inc, *(volatile const unsigned*)(bb.inc + prob));
-        __syncthreads();
-    }
-    for (uint64_t base = ua + (uint64_t)warp * 32; base < ub; base += (uint64_t)NWARP * 32) {
-        bool want = base + wl < ub;
+    float bnd = INFINITY, incv = INFINITY, bnd_of = -1.0f;
+    constexpr uint64_t RSTEP = (uint64_t)NWARP * 32;
+    uint64_t rbase = ua + (uint64_t)warp * 32;
+    int nfetch = 0;
+    for (;;) {
+        unsigned pend;
+        uint32_t loff = 0;
+        uint64_t base = 0;
         if (BB) {
-            incv = __uint_as_float(*(volatile unsigned*)&s_inc);
-            bnd = band_bound(su, incv, 0.0f);
-            if (want) {
-                const float lb = rlb[(base + wl) / (uint64_t)nseg];
-                want = lb < INFINITY && lb > tlo && lb <= thi && lb <= bnd;
+            int b0 = 0;
+            if (wl == 0) {
+                b0 = *(volatile int*)&s_stop ? lcnt : atomicAdd(&s_next, 32);
+                if ((nfetch++ & 3) == 0) atomicMin(&s_inc, *(volatile const unsigned*)(bb.inc + prob));
             }
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (b0 >= lcnt) break;
+            const int e = b0 + wl;
+            const uint2 en = e < lcnt ? lst[e] : make_uint2(0u, 0x7f800000u);
+            loff = en.x;
+            const float lb = __uint_as_float(en.y);
+            incv = __uint_as_float(*(volatile unsigned*)&s_inc);
+            if (incv != bnd_of) { bnd = band_bound(su, incv, 0.0f); bnd_of = incv; }
+            pend = __ballot_sync(0xffffffffu, lb <= bnd);
+            if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
+                float mn = lb;
+                for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                if (wl == 0 && bb_edge(bb_bucket(mn, lbm), lbm) > bnd) s_stop = 1;
+                continue;
+            }
+        } else {
+            if (rbase >= ub) break;
+            base = rbase;
+            rbase += RSTEP;
+            pend = __ballot_sync(0xffffffffu, base + wl < ub);
         }
-        unsigned pend = __ballot_sync(0xffffffffu, want);
       while (pend) {
-        const uint64_t unit = base + (uint64_t)(__ffs(pend) - 1);
+        const int jl = __ffs(pend) - 1;
         pend &= pend - 1;
+        const uint32_t lo_j = __shfl_sync(0xffffffffu, loff, jl);
+        const uint64_t unit = BB ? ua + (uint64_t)lo_j : base + (uint64_t)jl;
         if (BB) ndone++;
         int seg;
         HiSums h;
@@ -975,7 +1046,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         __syncwarp();   // the table is rewritten for the next unit
       }
     }
-  }
     for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
     if (wl == 0 && nfeas) atomicAdd(feasible, nfeas);
     if (BB && wl == 0 && ndone) atomicAdd(bb.rows_done, ndone);
@@ -1192,7 +1262,8 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
             su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.rowlb, wk.lbmin);
         if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
-        BBArgs bb{wk.rowlb, wk.lbmin, wk.inc, wk.rows_done};
+        k_bucket<<<(unsigned)grid, 256, 0, st>>>(su, wk.probs, wk.rowlb, wk.lbmin, wk.ulist, wk.ulist_n);
+        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done};
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
     } else if (fast) {
         P1Fast f = nullptr;
@@ -1234,40 +1305,74 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // local minimum per problem over this shard's units (one warp per problem)
 // ------------------------------------------------------------------------------------------
-__global__ void k_reduce_min(Setup su, const Prob* probs, const float* submin, const float* submin_sure, float* m32,
-                             float* m32_sure) {
-    int p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    int lane = threadIdx.x & 31;
-    if (p >= su.n_problems) return;
+// one CTA (256 threads) per problem: this shard's minimum over its units' pass-1 minima, then the
+// units pass 2 must rescan (submin within the band of this shard's minimum; the global minimum is
+// never larger, so its band is a subset), sorted into index order; bandn = -1: more than BAND_CAP
+__global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs, const float* submin,
+                                                    const float* submin_sure, float* m32, float* m32_sure,
+                                                    int32_t* bandn, uint64_t* bandlist) {
+    __shared__ float rm[8], rs[8];
+    __shared__ int s_cnt;
+    __shared__ uint64_t s_list[BAND_CAP];
+    const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
     const Prob& P = probs[p];
     float m = INFINITY, ms = INFINITY;
+    uint64_t a = 0, b = 0;
     if (P.status == 0) {
         uint64_t slo, shi;
         shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
-        uint64_t a = slo * (uint64_t)su.upi, b = shi * (uint64_t)su.upi;
+        a = slo * (uint64_t)su.upi;
+        b = shi * (uint64_t)su.upi;
         if (b > P.units) b = P.units;
-        for (uint64_t u = a + lane; u < b; u += 32) {
-            size_t s = (size_t)p * su.units_max + u;
-            m = fminf(m, submin[s]);
-            if (submin_sure) ms = fminf(ms, submin_sure[s]);
+        const float* sp = submin + (size_t)p * su.units_max;
+        for (uint64_t u = a + tid; u < b; u += blockDim.x) {
+            m = fminf(m, sp[u]);
+            if (submin_sure) ms = fminf(ms, submin_sure[(size_t)p * su.units_max + u]);
         }
     }
     for (int o = 16; o; o >>= 1) {
         m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
         ms = fminf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
     }
-    if (lane == 0) {
+    if (lane == 0) { rm[tid >> 5] = m; rs[tid >> 5] = ms; }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    m = rm[0]; ms = rs[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); i++) { m = fminf(m, rm[i]); ms = fminf(ms, rs[i]); }
+    if (tid == 0) {
         m32[p] = m;
         if (m32_sure) m32_sure[p] = submin_sure ? ms : m;
+    }
+    if (!bandn) return;
+    if (P.status == 0 && !isinf(m)) {
+        const float bound = band_bound(su, m, submin_sure ? ms : m);
+        const float* sp = submin + (size_t)p * su.units_max;
+        for (uint64_t u = a + tid; u < b; u += blockDim.x)
+            if (sp[u] <= bound) {
+                const int pos = atomicAdd(&s_cnt, 1);
+                if (pos < BAND_CAP) s_list[pos] = u;
+            }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int n = s_cnt;
+        if (n <= BAND_CAP) {
+            for (int i = 1; i < n; i++) {   // insertion sort: index order
+                const uint64_t v = s_list[i];
+                int j = i - 1;
+                while (j >= 0 && s_list[j] > v) { s_list[j + 1] = s_list[j]; j--; }
+                s_list[j + 1] = v;
+            }
+            for (int i = 0; i < n; i++) bandlist[(size_t)p * BAND_CAP + i] = s_list[i];
+        }
+        bandn[p] = n <= BAND_CAP ? n : -1;
     }
 }
 
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
     const bool two = su.mode == M_MATRIX && su.has_qos;
-    int wpb = 8;
-    k_reduce_min<<<(su.n_problems + wpb - 1) / wpb, 32 * wpb, 0, st>>>(su, wk.probs, wk.submin,
-                                                                       two ? wk.submin_sure : nullptr, wk.m32,
-                                                                       wk.m32_sure);
+    k_reduce_min<<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
+                                                wk.m32_sure, wk.bandn, wk.bandlist);
     return cudaGetLastError();
 }
 
@@ -1360,7 +1465,8 @@ constexpr int P2_CAP = 256;
 template <int PASS>
 __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
-                                               const float* m32_sure, U256* hstar, U256* first) {
+                                               const float* m32_sure, U256* hstar, U256* first,
+                                               const int32_t* bandn, const uint64_t* bandlist) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ U256 red[512];
@@ -1404,8 +1510,49 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
     }
 
     // phase 0: exact minimum (+ record the band when PASS 2);  phase 1: lowest index within tol
+    auto unit_scan = [&](int phase, uint64_t unit, const U256& hs, U256& best, uint64_t& besti) {
+        uint64_t row;
+        int e0, e1;
+        unit_range(P, unit, &row, &e0, &e1);
+        int lv[MAXW_ENUM];
+        decode_row(row, L, W, lv);
+        const uint32_t ncand = (uint32_t)(e1 - e0) * (uint32_t)Lin;
+        for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
+            int lvc[MAXW_ENUM];
+            for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
+            if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint32_t)Lin);
+            lvc[W - 1] = (int)(c % (uint32_t)Lin);
+            float k32;
+            if (!key32_scalar(su, P, sl, lvc, k32)) continue;
+            if (!(k32 <= bound)) continue;
+            U256 k;
+            if (!exact_key(su, P, sl, lvc, k)) continue;
+            uint64_t idx = 0;   // index within the problem (fits: ENUM limits)
+            for (int w = 0; w < W; w++) idx = idx * (uint64_t)L[w] + (uint64_t)lvc[w];
+            if (phase == 0) {
+                if (u256_cmp(k, best) < 0) best = k;
+                if (PASS == 2) {
+                    const int slot = atomicAdd(&c_n, 1);
+                    if (slot < P2_CAP) { c_idx[slot] = idx; c_key[slot] = k; }
+                }
+            } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
+                if (idx < besti) besti = idx;
+            }
+        }
+    };
+    const int nband = bandn ? bandn[prob] : -1;
     auto scan = [&](int phase, U256& best, uint64_t& besti) {
         const U256 hs = s_hs;
+        if (nband >= 0) {   // the band's units, listed in index order by k_reduce_min
+            for (int i = 0; i < nband; i++) {
+                const uint64_t unit = bandlist[(size_t)prob * BAND_CAP + i];
+                if (!(submin[(size_t)prob * su.units_max + unit] <= bound)) continue;
+                unit_scan(phase, unit, hs, best, besti);
+                if (phase == 1 && __syncthreads_or(besti != ~0ull)) break;   // first unit with a hit holds the winner
+            }
+            __syncthreads();
+            return;
+        }
         bool done = false;
         for (uint64_t blk = ua; blk < ub && !done; blk += blockDim.x) {
             const uint64_t u = blk + threadIdx.x;
@@ -1426,34 +1573,7 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
             const int nl = nlist;
             for (int li = 0; li < nl; li++) {   // units in candidate-index order
                 const uint64_t unit = blk + list[li];
-                uint64_t row;
-                int e0, e1;
-                unit_range(P, unit, &row, &e0, &e1);
-                int lv[MAXW_ENUM];
-                decode_row(row, L, W, lv);
-                const uint32_t ncand = (uint32_t)(e1 - e0) * (uint32_t)Lin;
-                for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-                    int lvc[MAXW_ENUM];
-                    for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
-                    if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint32_t)Lin);
-                    lvc[W - 1] = (int)(c % (uint32_t)Lin);
-                    float k32;
-                    if (!key32_scalar(su, P, sl, lvc, k32)) continue;
-                    if (!(k32 <= bound)) continue;
-                    U256 k;
-                    if (!exact_key(su, P, sl, lvc, k)) continue;
-                    uint64_t idx = 0;   // index within the problem (fits: ENUM limits)
-                    for (int w = 0; w < W; w++) idx = idx * (uint64_t)L[w] + (uint64_t)lvc[w];
-                    if (phase == 0) {
-                        if (u256_cmp(k, best) < 0) best = k;
-                        if (PASS == 2) {
-                            const int slot = atomicAdd(&c_n, 1);
-                            if (slot < P2_CAP) { c_idx[slot] = idx; c_key[slot] = k; }
-                        }
-                    } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
-                        if (idx < besti) besti = idx;
-                    }
-                }
+                unit_scan(phase, unit, hs, best, besti);
                 if (phase == 1 && __syncthreads_or(besti != ~0ull)) {   // first unit with a hit holds the winner
                     done = true;
                     break;
@@ -1514,7 +1634,7 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<0><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
@@ -1523,7 +1643,7 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<2><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
@@ -1532,7 +1652,7 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<1><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
 }
 
