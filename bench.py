@@ -217,10 +217,12 @@ def main():
     value = world * a.steps * cand_step / (t_max_ms * 1e-3)
 
     # ---- pass-1 kernel alone (the dominant kernel): CUDA events on the launching stream
-    k_ms, k_launches, k_eval, k_units = pass1_time(ec, pr, ids, qos, stream, local)
+    # chain_ms = the whole pass-1 chain (row bounds, bucket sort, the kernel, its reduction);
+    # k_ms = the dominant kernel alone (events recorded around its launch inside the library)
+    chain_ms, k_launches, k_eval, k_units, k_ms = pass1_time(ec, pr, ids, qos, stream, local)
     # the same pass without row pruning (every row classified) and without QoS bounds, for context
-    x_ms, x_launches, x_eval, _ = pass1_time(ec, pr, ids, qos, stream, local, prune=False)
-    n_ms, n_launches, n_eval, n_units = pass1_time(ec, pr, ids, None, stream, local)
+    x_ms, x_launches, x_eval, _, x_kms = pass1_time(ec, pr, ids, qos, stream, local, prune=False)
+    n_ms, n_launches, n_eval, n_units, n_kms = pass1_time(ec, pr, ids, None, stream, local)
     units_total = int(sum(Ls[row[0]] * Ls[row[1]] for row in ids))
 
     # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
@@ -270,7 +272,7 @@ def main():
             "gpu_launches": int(8 * a.steps),
             "roofline": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,QoS>", "achieved": achieved,
                          "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(a.mixes),
                          "kernel_ms_per_launch": k_ms / k_launches,
                          "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
                          "fma_lane_ops_per_evaluated_candidate": fma_ops_per_cand,
@@ -278,15 +280,16 @@ def main():
                          "evaluated_fraction": k_eval / cand_step,
                          "candidates_per_s_kernel": cand_per_s_kernel},
             "pruning": {"units_total_per_launch": units_total, "units_processed_per_launch": k_units,
-                        "pass1_ms_pruned": k_ms / k_launches, "pass1_ms_exhaustive": x_ms / x_launches,
+                        "pass1_chain_ms_pruned": chain_ms / k_launches, "pass1_chain_ms_exhaustive": x_ms / x_launches,
+                        "pass1_kernel_ms_exhaustive": x_kms / x_launches,
                         "evaluated_candidates_exhaustive": x_eval,
                         "note": "row lower bounds (DESIGN.md §3.9) prove the skipped rows hold no candidate within "
                                 "the tolerance band of the best key found; exhaustive = every row classified"},
             "roofline_noqos": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,noQoS>",
-                               "achieved": fma_ops_per_cand * n_eval / (n_ms / n_launches * 1e-3) / 1e9,
+                               "achieved": fma_ops_per_cand * n_eval / (n_kms / n_launches * 1e-3) / 1e9,
                                "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s",
-                               "frac": fma_ops_per_cand * n_eval / (n_ms / n_launches * 1e-3) / 1e9 / peak,
-                               "kernel_ms_per_launch": n_ms / n_launches, "evaluated_candidates_per_launch": n_eval,
+                               "frac": fma_ops_per_cand * n_eval / (n_kms / n_launches * 1e-3) / 1e9 / peak,
+                               "kernel_ms_per_launch": n_kms / n_launches, "evaluated_candidates_per_launch": n_eval,
                                "note": "same C5 mixes without QoS bounds (every candidate evaluated); context for the "
                                        "headline kernel, whose QoS cuts leave 2-3% of candidates needing FP work"},
             "clocks": ck,
@@ -302,6 +305,17 @@ def main():
         dist.destroy_process_group()
 
 
+def ncu_traffic(mixes):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_pass1_fast launch on this workload,
+    from the committed `ncu --set full` capture (profiles/pass1_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "pass1_traffic.json")) as f:
+            t = json.load(f)
+        return t["bytes_per_launch"] if t.get("mixes") == mixes else None
+    except Exception:
+        return None
+
+
 def level_counts(pr, ec):
     """level count L_m of every library model = the candidate count of a 1-worker plan"""
     n = pr.info()["n_models"]
@@ -314,7 +328,7 @@ def pass1_time(ec, pr, ids, qos, stream, local, prune=True):
     how many units (rows) it processed."""
     import torch
     from paper_2506_12598_b200.eclip import Session
-    tot, launches, evaluated, units = 0.0, 0, 0, 0
+    tot, launches, evaluated, units, kern = 0.0, 0, 0, 0, 0.0
     batch = dict(model_ids=ids, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
     if qos is not None:
         batch["qos_ns"] = qos
@@ -331,8 +345,9 @@ def pass1_time(ec, pr, ids, qos, stream, local, prune=True):
             launches += 1
             st = s.stats()
             evaluated, units = st["evaluated_candidates"], st["units_processed"]
+            kern += st["kernel_ms"]
         s.close()
-    return tot, launches, evaluated, units
+    return tot, launches, evaluated, units, kern
 
 
 def time_to_plan(ec, world, rank, dist):

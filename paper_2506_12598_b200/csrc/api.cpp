@@ -377,6 +377,8 @@ struct eclip_session {
     ~eclip_session() {
         slice.release();
         arena.release();
+        for (cudaEvent_t& e : wk.kev)
+            if (e) cudaEventDestroy(e);
         if (own_stream && st) {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
@@ -407,10 +409,24 @@ static int setup_device(eclip_session* s, const eclip_options* opt) {
         s->own_stream = true;
     }
     s->arena.st = s->st;
+    for (cudaEvent_t& e : s->wk.kev) CU(cudaEventCreate(&e));
     return ECLIP_OK;
 }
 
-// Build tables with K1 on the GPU and fetch their level counts.
+// One device block carved into 256-byte aligned pieces (one cudaMallocAsync instead of dozens).
+struct Bump {
+    size_t off = 0;
+    template <class T>
+    size_t take(size_t n) {
+        const size_t o = off;
+        off = (off + std::max<size_t>(n, 1) * sizeof(T) + 255) & ~(size_t)255;
+        return o;
+    }
+};
+
+// Build tables with K1 on the GPU and fetch their level counts.  Inputs (group times, level
+// steps, job descriptors, table views) are packed host-side into the front of one device block
+// and sent with a single copy; the K1 workspaces and outputs follow in the same block.
 static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
     const eclip_profiles* P = s->prof;
     s->tabs.resize(specs.size());
@@ -419,65 +435,80 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
         if (rc) return rc;
     }
     const int nt = (int)specs.size();
+    struct Off { size_t beta, need, V, best, barg, bstar, sidx, wtmp, outS, outB, outW; };
+    std::vector<Off> off(nt);
+    Bump bp;
+    for (int i = 0; i < nt; i++) {   // inputs first (the copied prefix)
+        off[i].beta = bp.take<int64_t>(s->tabs[i].beta.size());
+        off[i].need = bp.take<int32_t>(s->tabs[i].need.size());
+    }
+    const size_t o_jobs = bp.take<LevelJob>(nt), o_K = bp.take<int64_t>(nt), o_G = bp.take<int32_t>(nt);
+    const size_t o_S = bp.take<int64_t*>(nt), o_B = bp.take<int64_t*>(nt), o_W = bp.take<uint8_t*>(nt);
+    const size_t o_beta = bp.take<int64_t*>(nt);
+    const size_t in_bytes = bp.off;
+    const size_t o_L = bp.take<int32_t>(nt);
+    for (int i = 0; i < nt; i++) {
+        const HostTable& t = s->tabs[i];
+        const size_t ns = (size_t)(t.Reff + 1) * (t.smax + 1);
+        off[i].V = bp.take<int64_t>(t.v_elems);
+        off[i].best = bp.take<int64_t>(4 * ns);
+        off[i].barg = bp.take<int32_t>(2 * ns);
+        off[i].bstar = bp.take<int64_t>(t.smax + 1);
+        off[i].sidx = bp.take<int32_t>(t.smax + 1);
+        off[i].wtmp = bp.take<uint64_t>((size_t)(t.smax + 1) * ((t.G + 7) / 8));
+        off[i].outS = bp.take<int64_t>(t.Lcap);
+        off[i].outB = bp.take<int64_t>(t.Lcap);
+        off[i].outW = bp.take<uint8_t>((size_t)t.Lcap * t.G);
+    }
+    unsigned char* base;
+    CU(s->arena.alloc(&base, bp.off));
+    std::vector<unsigned char> h(in_bytes);
+    auto at = [&](size_t o) { return base + o; };
     std::vector<LevelJob> jobs(nt);
-    std::vector<int64_t*> hS(nt), hB(nt), hbeta(nt);
-    std::vector<uint8_t*> hW(nt);
-    int32_t* dL;
-    CU(s->arena.alloc(&dL, nt));
+    std::vector<int64_t> hK(nt);
+    std::vector<const void*> hS(nt), hB(nt), hW(nt), hbeta(nt);
+    s->tabG.resize(nt);
     s->gmax = 0;
     for (int i = 0; i < nt; i++) {
-        HostTable& t = s->tabs[i];
+        const HostTable& t = s->tabs[i];
+        std::memcpy(h.data() + off[i].beta, t.beta.data(), t.beta.size() * 8);
+        std::memcpy(h.data() + off[i].need, t.need.data(), t.need.size() * 4);
         LevelJob& J = jobs[i];
         J.G = t.G; J.C = t.C; J.R = t.Reff; J.smax = t.smax; J.u = t.u; J.mask = t.mask; J.Lcap = t.Lcap;
-        int64_t* beta; int32_t* need;
-        CU(s->arena.alloc(&beta, t.beta.size()));
-        CU(s->arena.alloc(&need, t.need.size()));
-        CU(cudaMemcpyAsync(beta, t.beta.data(), t.beta.size() * 8, cudaMemcpyHostToDevice, s->st));
-        CU(cudaMemcpyAsync(need, t.need.data(), t.need.size() * 4, cudaMemcpyHostToDevice, s->st));
-        J.beta = beta; J.need = need;
-        hbeta[i] = beta;
-        CU(s->arena.alloc(&J.V, t.v_elems));
-        size_t ns = (size_t)(t.Reff + 1) * (t.smax + 1);
-        CU(s->arena.alloc(&J.best, 4 * ns));
-        CU(s->arena.alloc(&J.barg, 2 * ns));
-        CU(s->arena.alloc(&J.bstar, t.smax + 1));
-        CU(s->arena.alloc(&J.sidx, t.smax + 1));
-        CU(s->arena.alloc(&J.wtmp, (size_t)(t.smax + 1) * ((t.G + 7) / 8)));
-        CU(s->arena.alloc(&J.outS, t.Lcap));
-        CU(s->arena.alloc(&J.outB, t.Lcap));
-        CU(s->arena.alloc(&J.outW, (size_t)t.Lcap * t.G));
-        J.outL = dL + i;
-        hS[i] = J.outS; hB[i] = J.outB; hW[i] = J.outW;
+        J.beta = (const int64_t*)at(off[i].beta);
+        J.need = (const int32_t*)at(off[i].need);
+        J.V = (int64_t*)at(off[i].V);
+        J.best = (int64_t*)at(off[i].best);
+        J.barg = (int32_t*)at(off[i].barg);
+        J.bstar = (int64_t*)at(off[i].bstar);
+        J.sidx = (int32_t*)at(off[i].sidx);
+        J.wtmp = (uint64_t*)at(off[i].wtmp);
+        J.outS = (int64_t*)at(off[i].outS);
+        J.outB = (int64_t*)at(off[i].outB);
+        J.outW = (uint8_t*)at(off[i].outW);
+        J.outL = (int32_t*)at(o_L) + i;
+        hK[i] = t.K; s->tabG[i] = t.G;
+        hS[i] = J.outS; hB[i] = J.outB; hW[i] = J.outW; hbeta[i] = J.beta;
         s->gmax = std::max(s->gmax, t.G);
     }
-    LevelJob* djobs;
-    CU(s->arena.alloc(&djobs, nt));
-    CU(cudaMemcpyAsync(djobs, jobs.data(), sizeof(LevelJob) * nt, cudaMemcpyHostToDevice, s->st));
+    std::memcpy(h.data() + o_jobs, jobs.data(), sizeof(LevelJob) * nt);
+    std::memcpy(h.data() + o_K, hK.data(), 8 * nt);
+    std::memcpy(h.data() + o_G, s->tabG.data(), 4 * nt);
+    std::memcpy(h.data() + o_S, hS.data(), 8 * nt);
+    std::memcpy(h.data() + o_B, hB.data(), 8 * nt);
+    std::memcpy(h.data() + o_W, hW.data(), 8 * nt);
+    std::memcpy(h.data() + o_beta, hbeta.data(), 8 * nt);
+    CU(cudaMemcpyAsync(base, h.data(), in_bytes, cudaMemcpyHostToDevice, s->st));
+    LevelJob* djobs = (LevelJob*)at(o_jobs);
     for (int c0 = 0; c0 < nt; c0 += 64)   // K1 handles up to 64 tables per cooperative launch
         CU(launch_levels(djobs + c0, jobs.data() + c0, std::min(64, nt - c0), s->st));
-    // device table views
-    std::vector<int64_t> hK(nt);
-    s->tabG.resize(nt);
-    for (int i = 0; i < nt; i++) { hK[i] = s->tabs[i].K; s->tabG[i] = s->tabs[i].G; }
-    int64_t* dK; int32_t* dG;
-    int64_t** dS; int64_t** dB; uint8_t** dW; int64_t** dbeta;
-    CU(s->arena.alloc(&dK, nt));
-    CU(s->arena.alloc(&dG, nt));
-    CU(s->arena.alloc(&dS, nt));
-    CU(s->arena.alloc(&dB, nt));
-    CU(s->arena.alloc(&dW, nt));
-    CU(s->arena.alloc(&dbeta, nt));
-    CU(cudaMemcpyAsync(dK, hK.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
-    CU(cudaMemcpyAsync(dG, s->tabG.data(), 4 * nt, cudaMemcpyHostToDevice, s->st));
-    CU(cudaMemcpyAsync(dS, hS.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
-    CU(cudaMemcpyAsync(dB, hB.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
-    CU(cudaMemcpyAsync(dW, hW.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
-    CU(cudaMemcpyAsync(dbeta, hbeta.data(), 8 * nt, cudaMemcpyHostToDevice, s->st));
+    int32_t* dL = (int32_t*)at(o_L);
     s->tabL.resize(nt);
     CU(cudaMemcpyAsync(s->tabL.data(), dL, 4 * nt, cudaMemcpyDeviceToHost, s->st));
     CU(cudaStreamSynchronize(s->st));   // level counts size the enumeration
-    s->tb.n = nt; s->tb.L = dL; s->tb.K = dK; s->tb.G = dG;
-    s->tb.S = dS; s->tb.B = dB; s->tb.wit = dW; s->tb.beta = dbeta;
+    s->tb.n = nt; s->tb.L = dL; s->tb.K = (const int64_t*)at(o_K); s->tb.G = (const int32_t*)at(o_G);
+    s->tb.S = (const int64_t* const*)at(o_S); s->tb.B = (const int64_t* const*)at(o_B);
+    s->tb.wit = (const uint8_t* const*)at(o_W); s->tb.beta = (const int64_t* const*)at(o_beta);
     return ECLIP_OK;
 }
 
@@ -585,33 +616,53 @@ static int alloc_work(eclip_session* s) {
     Setup& su = s->su;
     Work& wk = s->wk;
     const size_t n = (size_t)su.n_problems;
-    CU(s->arena.alloc(&wk.probs, n));
-    CU(s->arena.alloc(&wk.levs, n * (size_t)su.lev_stride));
-    if (s->engine == ECLIP_ENGINE_ENUM) {
-        size_t ns = n * (size_t)su.units_max;
-        CU(s->arena.alloc(&wk.submin, ns));
-        CU(s->arena.alloc(&wk.bandn, n));
-        CU(s->arena.alloc(&wk.bandlist, n * (size_t)BAND_CAP));
-        if (su.mode == M_MATRIX && su.has_qos) CU(s->arena.alloc(&wk.submin_sure, ns));
+    const bool en = s->engine == ECLIP_ENGINE_ENUM, bb = en && pass1_prunable(su);
+    const size_t ns = n * (size_t)su.units_max;
+    const size_t grid = n * (size_t)((su.items_max + su.n_shards - 1) / su.n_shards);
+    Bump bp;   // one block; null pieces stay null
+    const size_t o_cnt = bp.take<unsigned long long>(2);   // feasible, rows_done (zeroed)
+    const size_t o_probs = bp.take<Prob>(n), o_levs = bp.take<Lev>(n * (size_t)su.lev_stride);
+    const size_t o_sub = en ? bp.take<float>(ns) : 0, o_bandn = en ? bp.take<int32_t>(n) : 0;
+    const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
+    const size_t o_sure = (en && su.mode == M_MATRIX && su.has_qos) ? bp.take<float>(ns) : 0;
+    const size_t o_m32 = bp.take<float>(n), o_m32s = bp.take<float>(n), o_hs = bp.take<U256>(n), o_first = bp.take<U256>(n);
+    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0;
+    if (bb) {
+        o_rowlb = bp.take<float>(n * (size_t)su.rows_max);
+        o_lbmin = bp.take<unsigned>(n);
+        o_inc = bp.take<unsigned>(n);
+        o_hull = bp.take<float2>(n * 4 * (size_t)su.Lmax);
+        o_ftab = bp.take<int32_t>(n * (size_t)FT_CAP);
+        o_ulist = bp.take<uint2>(grid * (size_t)su.upi);
+        o_uln = bp.take<int32_t>(grid);
+        o_rh = bp.take<RowHdr>(n);
     }
-    CU(s->arena.alloc(&wk.m32, n));
-    CU(s->arena.alloc(&wk.m32_sure, n));
-    CU(s->arena.alloc(&wk.hstar, n));
-    CU(s->arena.alloc(&wk.first, n));
-    CU(s->arena.alloc(&wk.feasible, 1));
-    CU(cudaMemsetAsync(wk.feasible, 0, sizeof(unsigned long long), s->st));
-    CU(s->arena.alloc(&wk.rows_done, 1));
-    CU(cudaMemsetAsync(wk.rows_done, 0, sizeof(unsigned long long), s->st));
-    if (s->engine == ECLIP_ENGINE_ENUM && pass1_prunable(su)) {
-        CU(s->arena.alloc(&wk.rowlb, n * (size_t)su.rows_max));
-        CU(s->arena.alloc(&wk.lbmin, n));
-        CU(s->arena.alloc(&wk.inc, n));
-        CU(s->arena.alloc(&wk.hull, n * 4 * (size_t)su.Lmax));
-        CU(s->arena.alloc(&wk.ftab, n * (size_t)FT_CAP));
-        const size_t grid = n * (size_t)((su.items_max + su.n_shards - 1) / su.n_shards);
-        CU(s->arena.alloc(&wk.ulist, grid * (size_t)su.upi));
-        CU(s->arena.alloc(&wk.ulist_n, grid));
-        CU(s->arena.alloc(&wk.rowhdr, n));
+    unsigned char* base;
+    CU(s->arena.alloc(&base, bp.off));
+    wk.feasible = (unsigned long long*)(base + o_cnt);
+    wk.rows_done = wk.feasible + 1;
+    CU(cudaMemsetAsync(wk.feasible, 0, 2 * sizeof(unsigned long long), s->st));
+    wk.probs = (Prob*)(base + o_probs);
+    wk.levs = (Lev*)(base + o_levs);
+    if (en) {
+        wk.submin = (float*)(base + o_sub);
+        wk.bandn = (int32_t*)(base + o_bandn);
+        wk.bandlist = (uint64_t*)(base + o_bandl);
+        if (o_sure) wk.submin_sure = (float*)(base + o_sure);
+    }
+    wk.m32 = (float*)(base + o_m32);
+    wk.m32_sure = (float*)(base + o_m32s);
+    wk.hstar = (U256*)(base + o_hs);
+    wk.first = (U256*)(base + o_first);
+    if (bb) {
+        wk.rowlb = (float*)(base + o_rowlb);
+        wk.lbmin = (unsigned*)(base + o_lbmin);
+        wk.inc = (unsigned*)(base + o_inc);
+        wk.hull = (float2*)(base + o_hull);
+        wk.ftab = (int32_t*)(base + o_ftab);
+        wk.ulist = (uint2*)(base + o_ulist);
+        wk.ulist_n = (int32_t*)(base + o_uln);
+        wk.rowhdr = (RowHdr*)(base + o_rh);
     }
     return ECLIP_OK;
 }
@@ -963,11 +1014,15 @@ extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
 
 extern "C" int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n) {
     if (!s || !out || n < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
-    unsigned long long v[2] = {0, 0};
+    unsigned long long v[3] = {0, 0, 0};
     if (s->wk.feasible) CU(cudaMemcpyAsync(&v[0], s->wk.feasible, sizeof v[0], cudaMemcpyDeviceToHost, s->st));
     if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[1], s->wk.rows_done, sizeof v[1], cudaMemcpyDeviceToHost, s->st));
     CU(cudaStreamSynchronize(s->st));
-    for (int i = 0; i < n; i++) out[i] = i < 2 ? v[i] : 0;
+    float ms = 0.0f;   // the events exist from session creation; unrecorded (SLICE) -> error -> 0
+    if (s->engine == ECLIP_ENGINE_ENUM && cudaEventElapsedTime(&ms, s->wk.kev[0], s->wk.kev[1]) == cudaSuccess)
+        v[2] = (unsigned long long)llround((double)ms * 1e6);
+    cudaGetLastError();
+    for (int i = 0; i < n; i++) out[i] = i < 3 ? v[i] : 0;
     return ECLIP_OK;
 }
 

@@ -12,6 +12,7 @@ constexpr int MAXW = 16;        // workers per problem (API limit)
 constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
 constexpr int P1_THREADS = 256; // pass-1 CTA size
 constexpr int KIN = 16;         // inner-worker levels held in registers per thread (fast pass 1)
+constexpr int P1_CS = 4;        // step-level chunk of the pass-1 chunk filter
 constexpr int P1_TABN = 8192;   // entries of each QoS range lookup table (fast pass 1)
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
@@ -149,6 +150,7 @@ struct Work {
     unsigned long long* rows_done;  // [1] rows (units) pass 1 actually processed
     int32_t* bandn;             // [n] units in the pass-2 band list (-1: more than BAND_CAP, rescan all)
     uint64_t* bandlist;         // [n * BAND_CAP] band units in index order (k_reduce_min)
+    cudaEvent_t kev[2];         // recorded on the launching stream around the dominant pass-1 kernel (or null)
 };
 
 constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem

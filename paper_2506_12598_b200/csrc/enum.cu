@@ -16,6 +16,7 @@
 //   materialize (a9): winner -> witnesses -> per-group pool sizes, FP64 latency / power /
 //            energy / throughput.
 #include <cfloat>
+#include <climits>
 #include <cstdio>
 
 #include <algorithm>
@@ -287,10 +288,13 @@ struct AuxView {
     uint8_t* shi; uint8_t* slo;       // step worker (one segment): same two tables
     int* hdr;                         // s0, u0, khi_ok, klo_ok, ss0, su0, shi_ok, slo_ok
     int* stS; int* stU; int* stUmax;  // step worker, sorted per segment: S', suffix-min of u, prefix-max of u
+    float* preminB;                   // inner worker, S'-sorted: preminB[k] = (float) min_{j<k} B_j (+inf at 0)
+    float* chB;                       // step worker, S'-sorted: (float) min B over each aligned chunk of P1_CS
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
-    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 32 + (size_t)Lmax * 12;
+    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 32 + (size_t)Lmax * 12 +
+               (size_t)(Lmax + 1) * 4 + (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -313,6 +317,8 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.stS = a.hdr + 8;
     a.stU = a.stS + Lmax;
     a.stUmax = a.stU + Lmax;
+    a.preminB = reinterpret_cast<float*>(a.stUmax + Lmax);
+    a.chB = a.preminB + (Lmax + 1);
     return a;
 }
 
@@ -324,9 +330,21 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     if (P.status != 0) return;
     const int W = su.W, Lmax = su.Lmax;
     Lev* base = levs + (size_t)prob * su.lev_stride;
-    const Lev* inner = base + (W - 1) * Lmax;
-    const Lev* stepw = base + (W >= 2 ? (W - 2) : 0) * Lmax;
-    AuxView A = aux_view(reinterpret_cast<unsigned char*>(base + (size_t)W * Lmax), Lmax);
+    // the block is built in shared memory from shared copies of the two workers' records, then
+    // written out once (coalesced)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Lev* inner_s = reinterpret_cast<Lev*>(smem_raw);
+    Lev* step_s = inner_s + Lmax;
+    unsigned char* aux_s = reinterpret_cast<unsigned char*>(step_s + Lmax);
+    {
+        const Lev* gi = base + (W - 1) * Lmax;
+        const Lev* gs = base + (W >= 2 ? (W - 2) : 0) * Lmax;
+        for (int i = threadIdx.x; i < Lmax; i += blockDim.x) { inner_s[i] = gi[i]; step_s[i] = gs[i]; }
+    }
+    __syncthreads();
+    const Lev* inner = inner_s;
+    const Lev* stepw = step_s;
+    AuxView A = aux_view(aux_s, Lmax);
     const int Lin = P.L[W - 1], Lst = P.Lstep, segl = P.seglen;
     const double invd = 1.0 / (double)P.lamN;
     for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
@@ -354,13 +372,73 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     }
     for (int k = threadIdx.x; k < Lin; k += blockDim.x) A.ssort[k] = inner[A.perm[k]].S;
     __syncthreads();
-    for (int k = threadIdx.x; k <= Lin; k += blockDim.x) {
-        int mn = 1 << 30, mx = -(1 << 30);
-        for (int j = k; j < Lin; j++) mn = min(mn, inner[A.perm[j]].Tmax - A.ssort[j]);
-        for (int j = 0; j < k; j++) mx = max(mx, inner[A.perm[j]].Tmax - A.ssort[j]);
-        A.usuf[k] = mn;
-        A.umaxp[k] = mx;
+    // warp scans (S'-sorted order): warp 0 preminB (exclusive prefix min of B), warp 1 usuf (suffix min
+    // of u = Tmax - S'), warp 2 umaxp (exclusive prefix max of u), warps 3/4 the step worker's
+    // per-segment suffix min / inclusive prefix max of u
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        float carry = INFINITY;
+        if (lane == 0) A.preminB[0] = INFINITY;
+        for (int b = 0; b < Lin; b += 32) {
+            float v = b + lane < Lin ? __ll2float_rn(inner[A.perm[b + lane]].B) : INFINITY;
+            for (int o = 1; o < 32; o <<= 1) { const float y = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v = fminf(v, y); }
+            v = fminf(v, carry);
+            if (b + lane < Lin) A.preminB[b + lane + 1] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    } else if (warp == 1) {
+        int carry = 1 << 30;
+        if (lane == 0) A.usuf[Lin] = 1 << 30;
+        for (int e = Lin; e > 0; e -= 32) {   // chunk [e-32, e)
+            const int k = e - 32 + lane;
+            int v = k >= 0 ? inner[A.perm[k]].Tmax - A.ssort[k] : (1 << 30);
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(0xffffffffu, v, o); if (lane + o < 32) v = min(v, y); }
+            v = min(v, carry);
+            if (k >= 0) A.usuf[k] = v;
+            carry = __shfl_sync(0xffffffffu, v, 0);
+        }
+    } else if (warp == 2) {
+        int carry = -(1 << 30);
+        if (lane == 0) A.umaxp[0] = -(1 << 30);
+        for (int b = 0; b < Lin; b += 32) {
+            int v = b + lane < Lin ? inner[A.perm[b + lane]].Tmax - A.ssort[b + lane] : -(1 << 30);
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v = max(v, y); }
+            v = max(v, carry);
+            if (b + lane < Lin) A.umaxp[b + lane + 1] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    } else if (W >= 2 && (warp == 3 || warp == 4)) {
+        for (int b0 = 0; b0 < Lst; b0 += segl) {   // segments
+            const int b1 = min(b0 + segl, Lst);
+            if (warp == 3) {
+                int carry = 1 << 30;
+                for (int e = b1; e > b0; e -= 32) {
+                    const int i = e - 32 + lane;
+                    int v = i >= b0 ? stepw[A.sperm[i]].Tmax - stepw[A.sperm[i]].S : (1 << 30);
+                    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(0xffffffffu, v, o); if (lane + o < 32) v = min(v, y); }
+                    v = min(v, carry);
+                    if (i >= b0) { A.stU[i] = v; A.stS[i] = stepw[A.sperm[i]].S; }
+                    carry = __shfl_sync(0xffffffffu, v, 0);
+                }
+            } else {
+                int carry = -(1 << 30);
+                for (int b = b0; b < b1; b += 32) {
+                    const int i = b + lane;
+                    int v = i < b1 ? stepw[A.sperm[i]].Tmax - stepw[A.sperm[i]].S : -(1 << 30);
+                    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v = max(v, y); }
+                    v = max(v, carry);
+                    if (i < b1) A.stUmax[i] = v;
+                    carry = __shfl_sync(0xffffffffu, v, 31);
+                }
+            }
+        }
     }
+    if (W >= 2)
+        for (int c = threadIdx.x; c * P1_CS < Lst; c += blockDim.x) {
+            float m = INFINITY;
+            for (int i = c * P1_CS; i < min(Lst, c * P1_CS + P1_CS); i++) m = fminf(m, __ll2float_rn(stepw[A.sperm[i]].B));
+            A.chB[c] = m;
+        }
     __syncthreads();
     const int s0 = A.ssort[0], u0 = A.usuf[0];
     const bool khi_ok = Lin <= 255 && A.ssort[Lin - 1] - s0 + 1 <= P1_TABN;
@@ -371,19 +449,6 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     if (klo_ok)
         for (int k = threadIdx.x; k < Lin; k += blockDim.x)
             for (int v = (k == 0 ? A.usuf[0] : A.usuf[k - 1] + 1); v <= A.usuf[k]; v++) A.klo[v - u0] = (uint8_t)k;
-    // step worker, per segment in S' order: S', suffix minimum and (inclusive) prefix maximum of u
-    if (W >= 2) {
-        for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
-            const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
-            A.stS[i] = stepw[A.sperm[i]].S;
-            int mn = 1 << 30, mx = -(1 << 30);
-            for (int j = i; j < b1; j++) mn = min(mn, stepw[A.sperm[j]].Tmax - stepw[A.sperm[j]].S);
-            for (int j = b0; j <= i; j++) mx = max(mx, stepw[A.sperm[j]].Tmax - stepw[A.sperm[j]].S);
-            A.stU[i] = mn;
-            A.stUmax[i] = mx;
-        }
-    }
-    __syncthreads();
     // step-worker lookup tables (whole-row units only): #{e : S'_e <= ss0 + v}, min{e : stU[e] >= su0 + v}
     bool shi_ok = false, slo_ok = false;
     int ss0 = 0, su0 = 0;
@@ -402,6 +467,10 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
         A.hdr[0] = s0; A.hdr[1] = u0; A.hdr[2] = khi_ok; A.hdr[3] = klo_ok;
         A.hdr[4] = ss0; A.hdr[5] = su0; A.hdr[6] = shi_ok; A.hdr[7] = slo_ok;
     }
+    __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(aux_s);
+    uint4* dst = reinterpret_cast<uint4*>(base + (size_t)W * Lmax);
+    for (int i = threadIdx.x; i < su.aux_bytes / 16; i += blockDim.x) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------------------------------
@@ -461,39 +530,85 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
             if (threadIdx.x == 0) { s_t0 += mn; s_t1 += mx; }
         }
     }
-    for (int which = 0; which < 2; which++) {
-        const Lev* lv = sv + (size_t)which * Lmax;
-        const int L = P.L[W - 2 + which];
-        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    // rank sort of both workers by (S', B, index), concurrently (threads [0,128): step, [128,256): inner)
+    uint8_t* vflag = reinterpret_cast<uint8_t*>(stk + 2 * Lmax);      // [2][Lmax] hull-vertex flags (S' order)
+    const int which_t = threadIdx.x >> 7, tw = threadIdx.x & 127;
+    {
+        const Lev* lv = sv + (size_t)which_t * Lmax;
+        const int L = P.L[W - 2 + which_t];
+        for (int i = tw; i < L; i += 128) {
             const Lev& a = lv[i];
             int rk = 0;
             for (int j = 0; j < L; j++) {
                 const Lev& b = lv[j];
                 rk += (b.S < a.S) || (b.S == a.S && (b.B < a.B || (b.B == a.B && j < i)));
             }
-            ord[which * Lmax + rk] = (uint16_t)i;
+            ord[which_t * Lmax + rk] = (uint16_t)i;
+        }
+    }
+    __syncthreads();
+    // lower-left hull, one point per thread: point p (position t in that order) is a vertex iff no point
+    // before it has B <= B_p (Pareto) and the weights lambda = z / y for which p minimises B y + S' z form
+    // a non-empty open interval: max over later points with smaller B of (B_p - B_j)/(S'_j - S'_p)  <
+    // min over earlier points of (B_j - B_p)/(S'_p - S'_j)  (exact: numerators < 2^36, denominators
+    // < 2^24, so the cross products fit in int64).  Collinear middle points are dropped, as the
+    // sequential monotone chain does.
+    {
+        const Lev* lv = sv + (size_t)which_t * Lmax;
+        const uint16_t* o = ord + which_t * Lmax;
+        const int L = P.L[W - 2 + which_t];
+        for (int t = tw; t < L; t += 128) {
+            const Lev& p = lv[o[t]];
+            bool vert = true;
+            int64_t lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 0;   // lo = 0, hi = +inf
+            for (int r = 0; r < L && vert; r++) {
+                if (r == t) continue;
+                const Lev& q = lv[o[r]];
+                if (r < t) {
+                    if (q.B <= p.B) vert = false;                 // dominated (S'_q <= S'_p)
+                    else {                                        // S'_q < S'_p here
+                        const int64_t n = q.B - p.B, d = (int64_t)(p.S - q.S);
+                        if (hi_d == 0 || n * hi_d < hi_n * d) { hi_n = n; hi_d = d; }
+                    }
+                } else if (q.S > p.S && q.B < p.B) {
+                    const int64_t n = p.B - q.B, d = (int64_t)(q.S - p.S);
+                    if (n * lo_d > lo_n * d) { lo_n = n; lo_d = d; }
+                }
+            }
+            if (vert && hi_d != 0) vert = lo_n * hi_d < hi_n * lo_d;
+            vflag[which_t * Lmax + t] = vert ? 1 : 0;
         }
     }
     __syncthreads();
     const int t0 = s_t0, tn = (s_t1 - s_t0 + 1 <= FT_CAP && su.has_qos) ? s_t1 - s_t0 + 1 : 0;
-    if ((threadIdx.x & 31) == 0 && threadIdx.x < 64) {
-        const int which = threadIdx.x >> 5;
+    if (threadIdx.x < 64) {   // warp w compacts worker w's vertices in S' order and writes hull + edges
+        const int which = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const Lev* lv = sv + (size_t)which * Lmax;
         const int L = P.L[W - 2 + which];
-        uint16_t* o = ord + which * Lmax;
+        const uint16_t* o = ord + which * Lmax;
         uint16_t* sk = stk + which * Lmax;
         int n = 0, umax = -(1 << 30);
-        int64_t bmin = INT64_MAX;
-        for (int t = 0; t < L; t++) {
-            const Lev& p = lv[o[t]];
-            umax = max(umax, p.Tmax - p.S);
-            bmin = min(bmin, p.B);
-            if (n > 0 && p.B >= lv[sk[n - 1]].B) continue;      // dominated (S' not smaller, B not smaller)
-            while (n >= 2 && hull_pop(lv[sk[n - 2]], lv[sk[n - 1]], p)) n--;
-            sk[n++] = o[t];
+        long long bmin = LLONG_MAX;
+        for (int b0 = 0; b0 < L; b0 += 32) {
+            const int t = b0 + lane;
+            bool f = false;
+            if (t < L) {
+                const Lev& p = lv[o[t]];
+                umax = max(umax, p.Tmax - p.S);
+                bmin = min(bmin, (long long)p.B);
+                f = vflag[which * Lmax + t] != 0;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (f) sk[n + __popc(bal & ((1u << lane) - 1u))] = o[t];
+            n += __popc(bal);
         }
+        for (int off = 16; off; off >>= 1) {
+            umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+            bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, off));
+        }
+        __syncwarp();
         float2* h = hull + ((size_t)prob * 2 + which) * 2 * Lmax;
-        for (int i = 0; i < n; i++) {
+        for (int i = lane; i < n; i += 32) {
             const Lev& v = lv[sk[i]];
             h[i] = make_float2(__ll2float_rn(v.B), (float)v.S);
             if (i + 1 < n) {
@@ -501,11 +616,13 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
                 h[Lmax + i] = make_float2(__ll2float_rn(v.B - x.B), (float)(x.S - v.S));
             }
         }
-        RowHdr* H = hdr + prob;
-        H->nh[which] = n;
-        const int smin = lv[o[0]].S;
-        if (which == 0) { H->smin_st = smin; H->umax_st = umax; H->t0 = t0; H->tn = tn; }
-        else { H->smin_in = smin; H->umax_in = umax; H->Sminf_in = (float)smin; H->Bminf_in = __ll2float_rn(bmin); }
+        if (lane == 0) {
+            RowHdr* H = hdr + prob;
+            H->nh[which] = n;
+            const int smin = lv[o[0]].S;
+            if (which == 0) { H->smin_st = smin; H->umax_st = umax; H->t0 = t0; H->tn = tn; }
+            else { H->smin_in = smin; H->umax_in = umax; H->Sminf_in = (float)smin; H->Bminf_in = __ll2float_rn(bmin); }
+        }
     }
     if (tn == 0) return;
     // F(t) for t in [t0, t0 + tn): bucket every (e, k) pair at its last valid t, then a suffix minimum
@@ -528,11 +645,23 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
     for (int i = c1 - 1; i >= c0; i--) { m = min(m, G[i]); G[i] = m; }
     s_part[threadIdx.x] = m;
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int i = (int)blockDim.x - 2; i >= 0; i--) s_part[i] = min(s_part[i], s_part[i + 1]);
+    if (threadIdx.x < 32) {   // suffix minimum of the 256 chunk minima (8 per lane + a warp scan)
+        int v[8], x = INT_MAX;
+        for (int q = 7; q >= 0; q--) { x = min(x, s_part[threadIdx.x * 8 + q]); v[q] = x; }
+        int y = x;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int z = __shfl_down_sync(0xffffffffu, y, off);
+            if (threadIdx.x + off < 32) y = min(y, z);
+        }
+        const int after = __shfl_down_sync(0xffffffffu, y, 1);
+        const int tail = threadIdx.x < 31 ? after : INT_MAX;
+        for (int q = 0; q < 8; q++) s_part[threadIdx.x * 8 + q] = min(v[q], tail);
+    }
     __syncthreads();
-    const int after = threadIdx.x + 1 < (int)blockDim.x ? s_part[threadIdx.x + 1] : INT_MAX;
-    for (int i = c0; i < c1; i++) ftab[(size_t)prob * FT_CAP + i] = min(G[i], after);
+    for (int i = threadIdx.x; i < tn; i += blockDim.x) {   // coalesced
+        const int c = i / chunk;
+        ftab[(size_t)prob * FT_CAP + i] = min(G[i], c + 1 < (int)blockDim.x ? s_part[c + 1] : INT_MAX);
+    }
 }
 
 // min over a lower-left hull of B y + S' z (y, z > 0): the edge slopes (B_i - B_i+1)/(S'_i+1 - S'_i)
@@ -628,6 +757,116 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
     }
 }
 
+constexpr int BB_NB = 256;
+constexpr float BB_SCALE = 1024.0f;
+__device__ __forceinline__ int bb_bucket(float lb, float lbm) {
+    const float r = __fmul_rn(__fsub_rn(__fdiv_rn(lb, lbm), 1.0f), BB_SCALE);
+    return r <= 0.0f ? 0 : (r >= (float)(BB_NB - 1) ? BB_NB - 1 : (int)r);
+}
+// a value <= every bound in bucket b (one bucket of slack covers the rounding of bb_bucket)
+__device__ __forceinline__ float bb_edge(int b, float lbm) { return b <= 1 ? 0.0f : lbm * (1.0f + (float)(b - 1) / BB_SCALE); }
+
+// Row bound + best-first list in one kernel, for batches where one pass-1 item is a whole
+// problem (nseg = 1, one item per problem, unsharded) and its rows fit in shared memory (C5):
+// one CTA per problem computes every row's bound into shared memory (hi records and hull staged
+// there), the problem's minimum bound, and the bucket-ordered unit list -- the bounds never go
+// to global memory.  Same arithmetic as k_rowlb + k_bucket.
+constexpr int RLF_THREADS = 512;
+constexpr int RLF_ROWS_CAP = 24576;
+template <int NW, bool QOS>
+__global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Prob* probs, const Lev* levs,
+                                                             const float2* hull, const int32_t* ftab,
+                                                             const RowHdr* hdr, unsigned* lbmin, uint2* ulist,
+                                                             int32_t* ulist_n) {
+    constexpr int NH = NW - 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int Lmax = su.Lmax;
+    float2* sh = reinterpret_cast<float2*>(smem_raw);                  // [2][2][Lmax] hulls + edges
+    Lev* hrec = reinterpret_cast<Lev*>(sh + 4 * Lmax);                  // [NH][Lmax] hi records
+    float* lbs = reinterpret_cast<float*>(hrec + NH * Lmax);            // [rows]
+    __shared__ float red[RLF_THREADS / 32];
+    __shared__ int hist[BB_NB], cur[BB_NB];
+    const int prob = blockIdx.x;
+    const Prob& P = probs[prob];
+    if (P.status != 0) {
+        if (threadIdx.x == 0) ulist_n[prob] = 0;
+        return;
+    }
+    const RowHdr H = hdr[prob];
+    const Lev* base = levs + (size_t)prob * su.lev_stride;
+    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)prob * 4 * Lmax + i];
+    for (int i = threadIdx.x; i < NH * Lmax; i += blockDim.x) hrec[i] = base[i];
+    for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t rows = (uint32_t)P.units;
+    const int32_t* ft = ftab + (size_t)prob * FT_CAP;
+    const float invf = P.inv;
+    uint32_t Lh[NH > 0 ? NH : 1];
+#pragma unroll
+    for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
+    float bm = INFINITY;
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        int64_t hB = 0, hBS = 0;
+        int hT = 0, hTm = 1 << 24;
+        uint32_t x = r;
+#pragma unroll
+        for (int w = NH - 1; w >= 0; w--) {
+            const uint32_t d = x % Lh[w];
+            x /= Lh[w];
+            const Lev& v = hrec[w * Lmax + d];
+            hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
+        }
+        bool feas = true;
+        if (QOS) {
+            if (H.tn > 0) feas = ft[hT - H.t0] <= hTm - hT;
+            else feas = !(H.smin_st > min(hTm - hT - H.smin_in, H.umax_in - hT) || H.umax_st < hT + H.smin_in);
+        }
+        float lb = INFINITY;
+        if (feas) {
+            const float hBf = __ll2float_rn(hB), hTf = (float)hT;
+            const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
+            const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
+            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            const float Xh = fmaf(Dhf, invf, hBf);
+            const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
+            lb = (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
+                 0.99998474121f;   // 1 - 2^-16
+        }
+        lbs[r] = lb;
+        bm = fminf(bm, lb);
+    }
+    for (int o = 16; o; o >>= 1) bm = fminf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = bm;
+    __syncthreads();
+    bm = red[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); i++) bm = fminf(bm, red[i]);
+    if (threadIdx.x == 0) lbmin[prob] = __float_as_uint(bm);   // +inf bits when no row is feasible
+    if (!(bm < INFINITY)) {
+        if (threadIdx.x == 0) ulist_n[prob] = 0;
+        return;
+    }
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        const float lb = lbs[r];
+        if (lb < INFINITY) atomicAdd(&hist[bb_bucket(lb, bm)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
+        int v[BB_NB / 32], t = 0;
+        for (int i = 0; i < BB_NB / 32; i++) { v[i] = hist[threadIdx.x * (BB_NB / 32) + i]; t += v[i]; }
+        int xx = t;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xx, o); if (threadIdx.x >= o) xx += y; }
+        int run = xx - t;
+        for (int i = 0; i < BB_NB / 32; i++) { cur[threadIdx.x * (BB_NB / 32) + i] = run; run += v[i]; }
+        if (threadIdx.x == 31) ulist_n[prob] = xx;
+    }
+    __syncthreads();
+    uint2* out = ulist + (size_t)prob * su.upi;
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        const float lb = lbs[r];
+        if (lb < INFINITY) out[atomicAdd(&cur[bb_bucket(lb, bm)], 1)] = make_uint2(r, __float_as_uint(lb));
+    }
+}
+
 __global__ void k_fill_u32(unsigned* p, size_t n, unsigned v) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -652,6 +891,24 @@ __device__ float band_bound(const Setup& su, float m, float ms) {
     double tau = (double)su.tol_num / (double)su.tol_den;
     double b = base * (1.0 + tau) * (1.0 + su.delta) / (1.0 - su.delta) * (1.0 + 1e-12);
     return __double2float_ru(b);
+}
+
+// inner worker (S'-sorted): khi = #{k : S'_k <= c1}; klo = min{k : usuf[k] >= Tp}
+__device__ __forceinline__ int inner_khi(const AuxView& A, int c1, int s0, int slast, bool khi_ok, int Lin) {
+    if (c1 < s0) return 0;
+    if (c1 >= slast) return Lin;
+    if (khi_ok) return (int)A.khi[c1 - s0];
+    int lo = 0, hi = Lin;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.ssort[mid] <= c1) lo = mid + 1; else hi = mid; }
+    return lo;
+}
+__device__ __forceinline__ int inner_klo(const AuxView& A, int Tp, int u0v, int ulast, bool klo_ok, int Lin) {
+    if (Tp <= u0v) return 0;
+    if (Tp > ulast) return Lin;
+    if (klo_ok) return (int)A.klo[Tp - u0v];
+    int lo = 0, hi = Lin;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.usuf[mid] >= Tp) hi = mid; else lo = mid + 1; }
+    return lo;
 }
 
 struct HiSums {
@@ -707,15 +964,6 @@ struct BBArgs {
 // bucket of bound / (smallest bound of the problem) - 1 in steps of 1/BB_SCALE (counting sort,
 // k_bucket), so the rows most likely to hold the optimum set the incumbent first, and the list
 // can be abandoned as soon as a bucket's lower edge leaves the incumbent's band.
-constexpr int BB_NB = 256;
-constexpr float BB_SCALE = 1024.0f;
-__device__ __forceinline__ int bb_bucket(float lb, float lbm) {
-    const float r = __fmul_rn(__fsub_rn(__fdiv_rn(lb, lbm), 1.0f), BB_SCALE);
-    return r <= 0.0f ? 0 : (r >= (float)(BB_NB - 1) ? BB_NB - 1 : (int)r);
-}
-// a value <= every bound in bucket b (one bucket of slack covers the rounding of bb_bucket)
-__device__ __forceinline__ float bb_edge(int b, float lbm) { return b <= 1 ? 0.0f : lbm * (1.0f + (float)(b - 1) / BB_SCALE); }
-
 // one CTA per pass-1 item: counting sort of the item's units with a finite row bound by bucket
 __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, const float* rowlb, const unsigned* lbmin,
                                                 uint2* ulist, int32_t* ulist_n) {
@@ -760,7 +1008,7 @@ __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, con
 }
 
 template <int NW, int MODE, bool QOS, bool BB>
-__global__ void __launch_bounds__(P1_THREADS, 2)
+__global__ void __launch_bounds__(P1_THREADS, 3)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
              unsigned long long* __restrict__ feasible, BBArgs bb) {
     constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)
@@ -925,12 +1173,13 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             Xh = hBf * Yh;
         }
         int nc = 0;
-        for (int kb = 0; kb < ne; kb += 32) {
-            const int k = kb + wl;
+        // one step entry per lane (relative index k in [ea, ea + ne)); appends the usable ones to
+        // the warp's table; returns whether the lane's level lies past the QoS prefix
+        auto entry = [&](int k, bool valid) -> bool {
             bool use = false, past = true;
             int Sp = 0, Tme = 1 << 24;
             float Be = 0.0f, De = 0.0f;
-            if (k < ne) {
+            if (valid) {
                 if (W >= 2) {
                     const Lev& r = stepw[A.sperm[ea + k]];
                     Sp = r.S; Tme = r.Tmax;
@@ -954,26 +1203,17 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 if (MODE == M_PAPER) X += De;
                 ent = make_float4(X, fmaf(Sf, invf, Yh), fmaf(Be, invf, Zh), (float)Tp);
                 if (QOS) {
-                    const int c1 = Tm - Tp;   // inner S' must be <= c1
-                    if (c1 < s0) khi = 0;
-                    else if (c1 >= slast) khi = Lin;
-                    else if (khi_ok) khi = (int)A.khi[c1 - s0];
-                    else {
-                        int lo = 0, hi = Lin;
-                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.ssort[mid] <= c1) lo = mid + 1; else hi = mid; }
-                        khi = lo;
-                    }
-                    if (Tp <= u0v) klo = 0;
-                    else if (Tp > ulast) klo = Lin;
-                    else if (klo_ok) klo = (int)A.klo[Tp - u0v];
-                    else {
-                        int lo = 0, hi = Lin;
-                        while (lo < hi) { const int mid = (lo + hi) >> 1; if (A.usuf[mid] >= Tp) hi = mid; else lo = mid + 1; }
-                        klo = lo;
-                    }
+                    khi = inner_khi(A, Tm - Tp, s0, slast, khi_ok, Lin);
+                    klo = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
                     // levels before klo: none qualifies unless u is non-monotone there (rare)
                     const bool pre = A.umaxp[min(klo, khi)] >= Tp;
                     use = khi > klo || pre;
+                    if (BB && use) {   // entry bound: every swept key >= X + Y minB + Z minS
+                        const int ka = pre ? 0 : klo;
+                        const float lbe = fmaf(ent.y, A.preminB[khi], fmaf(ent.z, (float)A.ssort[ka], ent.x)) *
+                                          0.99998474121f;   // 1 - 2^-16
+                        use = !(lbe > bnd);
+                    }
                     if (pre) klo = -1 - klo;   // flag: sweep [0, |klo|) with a mask first
                 }
             }
@@ -984,8 +1224,49 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 tabk[pos] = make_int2(klo, khi);
             }
             nc += __popc(bal);
-            if (__all_sync(0xffffffffu, past)) break;   // the rest of the sorted segment is unusable
+            return past;
+        };
+        bool chunked = false;
+        if (BB && QOS && step_tab) {
+            // chunk filter: the S'-sorted step levels in aligned chunks of P1_CS; for a
+            // chunk with smallest S' = Sa and smallest B = Bm, every key of its entries is
+            //   >= (Xh + Bm Yh + Sa Zh) + (Yh + Sa/LN) minB_k + (Zh + Bm/LN) minS_k
+            // over the inner range that is QoS-feasible at T' = hT + Sa (a superset of every entry's)
+            const int c_lo = ea / P1_CS, c_hi = (ea + ne + P1_CS - 1) / P1_CS;
+            if (c_hi - c_lo <= 32) {
+                chunked = true;
+                const int c = c_lo + wl;
+                bool keep = false;
+                if (c < c_hi) {
+                    const int Sa = A.stS[c * P1_CS];
+                    const float Bm = A.chB[c];
+                    const int Tp = h.T + Sa;
+                    const int khi2 = inner_khi(A, h.Tm - Tp, s0, slast, khi_ok, Lin);
+                    const int klo2 = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
+                    const int ka = A.umaxp[klo2] >= Tp ? 0 : klo2;
+                    if (khi2 > ka) {
+                        const float Sf = (float)Sa;
+                        const float Xc = fmaf(Bm, Yh, fmaf(Sf, Zh, Xh));
+                        const float lbc = fmaf(fmaf(Sf, invf, Yh), A.preminB[khi2],
+                                               fmaf(fmaf(Bm, invf, Zh), (float)A.ssort[ka], Xc)) *
+                                          0.99998474121f;   // 1 - 2^-16
+                        keep = !(lbc > bnd);
+                    }
+                }
+                unsigned cm = __ballot_sync(0xffffffffu, keep);
+                const int q = wl / P1_CS, j = wl % P1_CS;
+                while (cm) {   // 32 / P1_CS surviving chunks per pass, one entry per lane
+                    unsigned mm = cm;
+                    for (int t = 0; t < q && mm; t++) mm &= mm - 1;
+                    const int k = mm ? (c_lo + __ffs(mm) - 1) * P1_CS + j - ea : -1;
+                    entry(k, k >= 0 && k < ne);
+                    for (int t = 0; t < 32 / P1_CS && cm; t++) cm &= cm - 1;
+                }
+            }
         }
+        if (!chunked)
+            for (int kb = 0; kb < ne; kb += 32)
+                if (__all_sync(0xffffffffu, entry(kb + wl, kb + wl < ne))) break;   // the rest of the sorted segment is unusable
         __syncwarp();
         float m0 = INFINITY, m1 = INFINITY;
         for (int i = wl; i < nc; i += 32) {
@@ -1186,6 +1467,14 @@ static P1Fast pick_fast(int mode, bool qos) {
 }
 template <int NW>
 static RowLB pick_rowlb(bool qos) { return qos ? k_rowlb<NW, true> : k_rowlb<NW, false>; }
+typedef void (*RowLBF)(Setup, const Prob*, const Lev*, const float2*, const int32_t*, const RowHdr*, unsigned*, uint2*,
+                       int32_t*);
+template <int NW>
+static RowLBF pick_rowlbf(bool qos) { return qos ? k_rowlb_fused<NW, true> : k_rowlb_fused<NW, false>; }
+// one pass-1 item per problem (whole rows), unsharded, rows within the shared-memory cap
+static bool rowlb_fused_ok(const Setup& su) {
+    return su.n_shards == 1 && su.nseg == 1 && su.items_max == 1 && su.rows_max <= RLF_ROWS_CAP && su.upi >= su.rows_max;
+}
 
 template <int NP, int MODE>
 static P1Gen pick_gen_m(int obj, bool qos) {
@@ -1251,10 +1540,34 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = fill_u32(wk.submin, n * (size_t)su.units_max, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
-        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 * sizeof(Lev));
+        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 + 2 * sizeof(Lev));
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
         k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr);
+        const size_t fsm = (size_t)su.Lmax * (4 * sizeof(float2) + (size_t)(su.W - 2) * sizeof(Lev)) + (size_t)su.rows_max * 4;
+        if (rowlb_fused_ok(su) && fsm <= 160 * 1024) {
+            RowLBF rf = nullptr;
+            switch (su.W) {
+                case 3: rf = pick_rowlbf<3>(qos); break;
+                case 4: rf = pick_rowlbf<4>(qos); break;
+                case 5: rf = pick_rowlbf<5>(qos); break;
+                case 6: rf = pick_rowlbf<6>(qos); break;
+                case 7: rf = pick_rowlbf<7>(qos); break;
+                case 8: rf = pick_rowlbf<8>(qos); break;
+                default: return cudaErrorInvalidValue;
+            }
+            if ((e = cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm)) != cudaSuccess)
+                return e;
+            rf<<<su.n_problems, RLF_THREADS, fsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.lbmin,
+                                                       wk.ulist, wk.ulist_n);
+            if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+                return e;
+            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done};
+            if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
+            f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
+            if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
+            return cudaGetLastError();
+        }
         // enough CTAs to fill the GPU (8 per SM), each looping over many rows of its problem
         const long long want = std::max<long long>(1, (148LL * 8 + su.n_problems - 1) / su.n_problems);
         const long long gx = std::min<long long>((su.rows_max + 255) / 256, want);
@@ -1264,7 +1577,9 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
             return e;
         k_bucket<<<(unsigned)grid, 256, 0, st>>>(su, wk.probs, wk.rowlb, wk.lbmin, wk.ulist, wk.ulist_n);
         BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done};
+        if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
+        if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
     } else if (fast) {
         P1Fast f = nullptr;
         switch (su.W) {
@@ -1281,7 +1596,9 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         BBArgs bb{};
+        if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
+        if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
     } else {
         P1Gen f = nullptr;
         switch (NP) {
@@ -1297,7 +1614,9 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         }
         cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.submin_sure);
+        if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
     }
     return cudaGetLastError();
 }
@@ -1517,11 +1836,32 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
         int lv[MAXW_ENUM];
         decode_row(row, L, W, lv);
         const uint32_t ncand = (uint32_t)(e1 - e0) * (uint32_t)Lin;
+        // exact integer QoS test first (the same predicate as key32_scalar's in the linear modes):
+        // hi sums once per unit, then T' = hT + S'_e + S'_k <= min(hTm, Tmax_e, Tmax_k)
+        const bool qlin = su.has_qos && su.mode != M_MATRIX;
+        int64_t hT = 0;
+        int hTm = 1 << 30;
+        if (qlin)
+            for (int w = 0; w < W - 2; w++) {
+                const Lev& r = sl[w * su.Lmax + lv[w]];
+                hT += r.S;
+                hTm = min(hTm, r.Tmax);
+            }
+        const Lev* se = sl + (W >= 2 ? (W - 2) : 0) * su.Lmax;
+        const Lev* sk = sl + (W - 1) * su.Lmax;
         for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
+            const int ke = W >= 2 ? e0 + (int)(c / (uint32_t)Lin) : 0, kk = (int)(c % (uint32_t)Lin);
+            if (qlin) {
+                const Lev& rk = sk[kk];
+                int64_t Tp = hT + rk.S;
+                int Tm = min(hTm, rk.Tmax);
+                if (W >= 2) { Tp += se[ke].S; Tm = min(Tm, se[ke].Tmax); }
+                if (Tp > (int64_t)Tm) continue;
+            }
             int lvc[MAXW_ENUM];
             for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
-            if (W >= 2) lvc[W - 2] = e0 + (int)(c / (uint32_t)Lin);
-            lvc[W - 1] = (int)(c % (uint32_t)Lin);
+            if (W >= 2) lvc[W - 2] = ke;
+            lvc[W - 1] = kk;
             float k32;
             if (!key32_scalar(su, P, sl, lvc, k32)) continue;
             if (!(k32 <= bound)) continue;
@@ -1784,8 +2124,11 @@ cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Wor
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
     if (su.aux_bytes > 0) {
-        if (su.mode == M_PAPER) k_prep_aux<M_PAPER><<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.levs);
-        else k_prep_aux<M_EXCL><<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.levs);
+        const size_t sm = (size_t)2 * su.Lmax * sizeof(Lev) + (size_t)su.aux_bytes;
+        auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;
+        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs);
     }
     return cudaGetLastError();
 }
