@@ -1029,6 +1029,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const int nseg = P.nseg;
     __shared__ unsigned s_inc;
     __shared__ int s_next, s_stop;
+    __shared__ uint8_t s_chunk[P1_THREADS / 32][32];
     float lbm = 0.0f;
     int lcnt = 0;
     const uint2* lst = nullptr;
@@ -1253,15 +1254,15 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                         keep = !(lbc > bnd);
                     }
                 }
-                unsigned cm = __ballot_sync(0xffffffffu, keep);
-                const int q = wl / P1_CS, j = wl % P1_CS;
-                while (cm) {   // 32 / P1_CS surviving chunks per pass, one entry per lane
-                    unsigned mm = cm;
-                    for (int t = 0; t < q && mm; t++) mm &= mm - 1;
-                    const int k = mm ? (c_lo + __ffs(mm) - 1) * P1_CS + j - ea : -1;
+                const unsigned cm = __ballot_sync(0xffffffffu, keep);
+                if (keep) s_chunk[warp][__popc(cm & ((1u << wl) - 1u))] = (uint8_t)wl;   // surviving chunks, in order
+                __syncwarp();
+                const int nk = __popc(cm), q = wl / P1_CS, j = wl % P1_CS;
+                for (int p0 = 0; p0 < nk; p0 += 32 / P1_CS) {   // 32 / P1_CS surviving chunks per pass, one entry per lane
+                    const int k = p0 + q < nk ? (c_lo + s_chunk[warp][p0 + q]) * P1_CS + j - ea : -1;
                     entry(k, k >= 0 && k < ne);
-                    for (int t = 0; t < 32 / P1_CS && cm; t++) cm &= cm - 1;
                 }
+                __syncwarp();
             }
         }
         if (!chunked)
@@ -1849,24 +1850,23 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
             }
         const Lev* se = sl + (W >= 2 ? (W - 2) : 0) * su.Lmax;
         const Lev* sk = sl + (W - 1) * su.Lmax;
-        for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-            const int ke = W >= 2 ? e0 + (int)(c / (uint32_t)Lin) : 0, kk = (int)(c % (uint32_t)Lin);
+        auto cand = [&](int ke, int kk) {
             if (qlin) {
                 const Lev& rk = sk[kk];
                 int64_t Tp = hT + rk.S;
                 int Tm = min(hTm, rk.Tmax);
                 if (W >= 2) { Tp += se[ke].S; Tm = min(Tm, se[ke].Tmax); }
-                if (Tp > (int64_t)Tm) continue;
+                if (Tp > (int64_t)Tm) return;
             }
             int lvc[MAXW_ENUM];
             for (int w = 0; w < W - 2; w++) lvc[w] = lv[w];
             if (W >= 2) lvc[W - 2] = ke;
             lvc[W - 1] = kk;
             float k32;
-            if (!key32_scalar(su, P, sl, lvc, k32)) continue;
-            if (!(k32 <= bound)) continue;
+            if (!key32_scalar(su, P, sl, lvc, k32)) return;
+            if (!(k32 <= bound)) return;
             U256 k;
-            if (!exact_key(su, P, sl, lvc, k)) continue;
+            if (!exact_key(su, P, sl, lvc, k)) return;
             uint64_t idx = 0;   // index within the problem (fits: ENUM limits)
             for (int w = 0; w < W; w++) idx = idx * (uint64_t)L[w] + (uint64_t)lvc[w];
             if (phase == 0) {
@@ -1878,6 +1878,17 @@ __global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev*
             } else if (within_tol(k, hs, su.tol_num, su.tol_den)) {
                 if (idx < besti) besti = idx;
             }
+        };
+        // 2-D thread map (inner level fixed per thread, step levels strided) when a padded row of
+        // inner levels fits the block: no division per candidate
+        const int KP = (Lin + 31) & ~31;
+        if (KP <= (int)blockDim.x) {
+            const int EP = (int)blockDim.x / KP, kk = (int)threadIdx.x % KP, eo = (int)threadIdx.x / KP;
+            if (kk < Lin && eo < EP)
+                for (int ke = e0 + eo; ke < e1; ke += EP) cand(ke, kk);
+        } else {
+            for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x)
+                cand(W >= 2 ? e0 + (int)(c / (uint32_t)Lin) : 0, (int)(c % (uint32_t)Lin));
         }
     };
     const int nband = bandn ? bandn[prob] : -1;
