@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["levels.cu", "enum.cu", "slice.cu", "baseline.cu", "api.cpp"]
+SOURCES = ["levels.cu", "enum.cu", "slice.cu", "baseline.cu", "runtime.cu", "api.cpp"]
 HEADERS = ["engine.h", "exact.cuh", "slice.h"]
 
 
@@ -33,7 +33,7 @@ def _newer(src_list, target):
 def _compile(src: str, force: bool) -> str:
     path = os.path.join(CSRC, src)
     obj = os.path.join(OBJ, src + ".o")
-    deps = [path] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "eclip.h")]
+    deps = [path] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", h) for h in ("eclip.h", "eclip_runtime.h")]
     if force or _newer(deps, obj):
         lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
         cmd = [NVCC] + ARCH + FLAGS + lang + ["-c", path, "-o", obj]

@@ -37,6 +37,14 @@ static int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+namespace eclip {
+// the same thread-local message for the other translation units (runtime.cu)
+int set_error(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace eclip
+
 #define CU(x)                                                                                       \
     do {                                                                                            \
         cudaError_t _e = (x);                                                                       \

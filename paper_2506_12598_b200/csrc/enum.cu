@@ -1782,16 +1782,17 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
 // key is within tol of the (global) H*.  PASS 2 (unsharded runs): both in one rescan -- the band's
 // exactly evaluated candidates are kept in shared memory (a second rescan only on overflow).
 constexpr int P2_CAP = 256;
+constexpr int P2_THREADS = 128;   // small CTAs: pass 2 is latency-bound (a few exact evaluations per problem)
 template <int PASS>
-__global__ void __launch_bounds__(512) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
+__global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
                                                const float* m32_sure, U256* hstar, U256* first,
                                                const int32_t* bandn, const uint64_t* bandlist) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
-    __shared__ U256 red[512];
-    __shared__ uint64_t redi[512];
-    __shared__ uint32_t list[512];
+    __shared__ U256 red[P2_THREADS];
+    __shared__ uint64_t redi[P2_THREADS];
+    __shared__ uint32_t list[P2_THREADS];
     __shared__ int nlist;
     __shared__ int wcount[16], woff[16];
     __shared__ uint64_t c_idx[P2_CAP];
@@ -1983,7 +1984,7 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_pass2<0><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+    k_pass2<0><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
@@ -1992,7 +1993,7 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_pass2<2><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+    k_pass2<2><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
@@ -2001,7 +2002,7 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
     size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_pass2<1><<<su.n_problems, 512, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
+    k_pass2<1><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist);
     return cudaGetLastError();
