@@ -254,6 +254,57 @@ int eclip_baseline_plan(const eclip_profiles* prof, const eclip_problem* problem
 int eclip_lookup_table_json(const eclip_profiles* prof, const eclip_problem* problem, const int32_t* group_sm,
                             char* buf, size_t cap, size_t* len, uint64_t* hash);
 
+/* ---- batched co-location simulator (SPEC simulator + metrics S:266-430) ----
+ * Evaluates lookup tables (plans) by simulating co-located execution, many scenarios per launch
+ * (one GPU thread per scenario; the event loop of one scenario is serial and deterministic).
+ * Per scenario: W workers run n_requests requests each, closed loop (R19); kernel k of
+ * worker w runs on pool table[k] (a set of SM groups, mask[w][j]; j = n_sizes-1 is the full device =
+ * the default stream, one FIFO shared by every worker when shared_default); kernel
+ * k waits for kernel k-1 plus, in ECLIP_SIM_PREALLOC mode, barrier_ns when it changes
+ * stream, or in ECLIP_SIM_IOCTL mode a repartition cost ~ triangular(lo, mode, hi) when
+ * it changes pool size (SplitMix64 counter-based draws keyed by (seed, scenario,
+ * worker, request, kernel)); it runs beta x oversub ns of solo work at rate 1/(1 + alpha(t)),
+ * alpha = sum over co-running kernels of shared SMs / N.  Outputs: throughput
+ * (requests / the worker's finish time), nearest-rank p95 and mean request latency, makespan,
+ * energy = integral of p_idle + (p_max - p_idle) busy/N over [0, makespan], requests/J.
+ * All arrays are host memory, row-major, caller-owned. */
+#define ECLIP_SIM_PREALLOC 0
+#define ECLIP_SIM_IOCTL 1
+typedef struct {
+    int32_t n_scenarios;      /* S >= 1 */
+    int32_t n_workers;        /* W in [1, 8] */
+    int32_t max_kernels;      /* K >= 1 (row stride of beta_ns / table) */
+    int32_t n_sizes;          /* C in [1, 32]; pool C-1 is the full device */
+    int32_t n_groups;         /* G in [1, 32] */
+    const int32_t* n_kernels; /* [S*W] kernels per request, in [1, K] */
+    const double* beta_ns;    /* [S*W*K*C] solo time (ns, finite, > 0) of kernel k on pool j */
+    const int32_t* table;     /* [S*W*K] pool index per kernel (the lookup table) */
+    const uint32_t* mask;     /* [W*C] group bitset of worker w's pool j (bits < G) */
+    const int32_t* group_sm;  /* [G] SMs per group (>= 0; include any remainder group in the full mask) */
+    int32_t total_sms;        /* N >= 1 */
+    int32_t n_requests;       /* per worker, in [1, 4096] */
+    int32_t shared_default;   /* 1: pool C-1 is ONE stream shared by every worker (FIFO) */
+    int32_t mode;             /* ECLIP_SIM_PREALLOC | ECLIP_SIM_IOCTL */
+    double barrier_ns;        /* PREALLOC: delay of a kernel that changes stream */
+    double ioctl_lo_ns, ioctl_mode_ns, ioctl_hi_ns;  /* IOCTL: triangular repartition cost */
+    double oversub;           /* >= 1: queue-oversubscription multiplier */
+    double p_idle_w, p_max_w; /* 0 <= p_idle <= p_max */
+    uint64_t seed;
+} eclip_sim_batch;
+typedef struct {
+    double* throughput_rps;   /* [S*W] */
+    double* p95_ns;           /* [S*W] */
+    double* mean_ns;          /* [S*W] */
+    double* makespan_ns;      /* [S] */
+    double* energy_j;         /* [S] */
+    double* req_per_j;        /* [S] */
+    int32_t* barriers;        /* [S] barriers inserted (PREALLOC) */
+    int64_t* events;          /* [S] kernel completions simulated */
+} eclip_sim_out;
+/* opt: device (other fields ignored; NULL = device 0).  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_CUDA,
+ * ECLIP_E_OOM. */
+int eclip_simulate(const eclip_sim_batch* batch, const eclip_options* opt, eclip_sim_out* out);
+
 #ifdef __cplusplus
 }
 #endif

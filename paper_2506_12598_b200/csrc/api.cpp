@@ -1291,3 +1291,83 @@ extern "C" int eclip_lookup_table_json(const eclip_profiles* P, const eclip_prob
     }
     return ECLIP_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// batched co-location simulator (simulate.cu)
+// ------------------------------------------------------------------------------------------
+extern "C" int eclip_simulate(const eclip_sim_batch* b, const eclip_options* opt, eclip_sim_out* out) {
+    if (!b || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    const long long S = b->n_scenarios;
+    const int W = b->n_workers, K = b->max_kernels, C = b->n_sizes, G = b->n_groups;
+    if (S < 1 || W < 1 || W > 8 || K < 1 || C < 1 || C > 32 || G < 1 || G > 32 || b->total_sms < 1 ||
+        b->n_requests < 1 || b->n_requests > 4096 || (b->mode != ECLIP_SIM_PREALLOC && b->mode != ECLIP_SIM_IOCTL))
+        return fail(ECLIP_E_INVALID_ARG, "simulator batch sizes out of range");
+    if (!b->n_kernels || !b->beta_ns || !b->table || !b->mask || !b->group_sm)
+        return fail(ECLIP_E_INVALID_ARG, "null simulator input array");
+    if (!out->throughput_rps || !out->p95_ns || !out->mean_ns || !out->makespan_ns || !out->energy_j ||
+        !out->req_per_j || !out->barriers || !out->events)
+        return fail(ECLIP_E_INVALID_ARG, "null simulator output array");
+    if (!(b->oversub >= 1.0) || !(b->barrier_ns >= 0.0) || !(b->p_idle_w >= 0.0) || !(b->p_max_w >= b->p_idle_w) ||
+        !(b->ioctl_lo_ns >= 0.0 && b->ioctl_mode_ns >= b->ioctl_lo_ns && b->ioctl_hi_ns >= b->ioctl_mode_ns) ||
+        !std::isfinite(b->oversub + b->barrier_ns + b->p_max_w + b->ioctl_hi_ns))
+        return fail(ECLIP_E_INVALID_ARG, "simulator overhead / power model out of range");
+    for (int g = 0; g < G; g++)
+        if (b->group_sm[g] < 0) return fail(ECLIP_E_INVALID_ARG, "group_sm must be >= 0");
+    const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+    for (int i = 0; i < W * C; i++)
+        if (b->mask[i] & ~gbits) return fail(ECLIP_E_INVALID_ARG, "mask %d uses groups beyond n_groups", i);
+    for (long long i = 0; i < S * W; i++) {
+        const int nk = b->n_kernels[i];
+        if (nk < 1 || nk > K) return fail(ECLIP_E_INVALID_ARG, "n_kernels[%lld] must be in [1, max_kernels]", i);
+        for (int k = 0; k < nk; k++) {
+            const int j = b->table[i * K + k];
+            if (j < 0 || j >= C) return fail(ECLIP_E_INVALID_ARG, "table entry out of range (scenario %lld)", i / W);
+            const double v = b->beta_ns[(i * K + k) * C + j];
+            if (!(std::isfinite(v) && v > 0.0)) return fail(ECLIP_E_INVALID_ARG, "beta_ns must be finite and > 0");
+        }
+    }
+    eclip_session s;   // device, stream and arena only
+    int rc = setup_device(&s, opt);
+    if (rc) return rc;
+    Bump bp;
+    const size_t o_nk = bp.take<int32_t>(S * W), o_beta = bp.take<double>((size_t)S * W * K * C);
+    const size_t o_tab = bp.take<int32_t>((size_t)S * W * K), o_mask = bp.take<uint32_t>((size_t)W * C);
+    const size_t o_gsm = bp.take<int32_t>(G);
+    const size_t o_out = bp.take<double>((size_t)S * (3 * W + 3)), o_int = bp.take<int32_t>((size_t)S * 2);
+    const size_t o_ev = bp.take<long long>(S), o_lat = bp.take<double>((size_t)S * W * b->n_requests);
+    unsigned char* base;
+    CU(s.arena.alloc(&base, bp.off));
+    CU(cudaMemcpyAsync(base + o_nk, b->n_kernels, 4 * (size_t)S * W, cudaMemcpyHostToDevice, s.st));
+    CU(cudaMemcpyAsync(base + o_beta, b->beta_ns, 8 * (size_t)S * W * K * C, cudaMemcpyHostToDevice, s.st));
+    CU(cudaMemcpyAsync(base + o_tab, b->table, 4 * (size_t)S * W * K, cudaMemcpyHostToDevice, s.st));
+    CU(cudaMemcpyAsync(base + o_mask, b->mask, 4 * (size_t)W * C, cudaMemcpyHostToDevice, s.st));
+    CU(cudaMemcpyAsync(base + o_gsm, b->group_sm, 4 * (size_t)G, cudaMemcpyHostToDevice, s.st));
+    SimJob J{};
+    J.S = S; J.W = W; J.K = K; J.C = C; J.G = G; J.N = b->total_sms; J.n_requests = b->n_requests;
+    J.shared_default = b->shared_default ? 1 : 0; J.ioctl = b->mode == ECLIP_SIM_IOCTL;
+    J.n_kernels = (const int32_t*)(base + o_nk); J.beta = (const double*)(base + o_beta);
+    J.table = (const int32_t*)(base + o_tab); J.mask = (const uint32_t*)(base + o_mask);
+    J.group_sm = (const int32_t*)(base + o_gsm);
+    J.barrier_ns = b->barrier_ns; J.io_lo = b->ioctl_lo_ns; J.io_mode = b->ioctl_mode_ns; J.io_hi = b->ioctl_hi_ns;
+    J.oversub = b->oversub; J.p_idle = b->p_idle_w; J.p_max = b->p_max_w; J.seed = b->seed;
+    double* od = (double*)(base + o_out);
+    SimOut o{};
+    o.throughput_rps = od; o.p95_ns = od + S * W; o.mean_ns = od + 2 * S * W;
+    o.makespan_ns = od + 3 * S * W; o.energy_j = od + 3 * S * W + S; o.req_per_j = od + 3 * S * W + 2 * S;
+    o.barriers = (int32_t*)(base + o_int); o.status = o.barriers + S; o.events = (long long*)(base + o_ev);
+    CU(launch_simulate(J, o, (double*)(base + o_lat), s.st));
+    std::vector<int32_t> st(S);
+    CU(cudaMemcpyAsync(out->throughput_rps, o.throughput_rps, 8 * (size_t)S * W, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->p95_ns, o.p95_ns, 8 * (size_t)S * W, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->mean_ns, o.mean_ns, 8 * (size_t)S * W, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->makespan_ns, o.makespan_ns, 8 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->energy_j, o.energy_j, 8 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->req_per_j, o.req_per_j, 8 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->barriers, o.barriers, 4 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(out->events, o.events, 8 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(st.data(), o.status, 4 * (size_t)S, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaStreamSynchronize(s.st));
+    for (long long i = 0; i < S; i++)
+        if (st[i] != 0) return fail(ECLIP_E_INVALID_ARG, "scenario %lld cannot progress (simulator deadlock)", i);
+    return ECLIP_OK;
+}

@@ -164,6 +164,27 @@ struct RowHdr {                 // per-problem constants of the row bound (k_pre
     int32_t t0, tn;             // feasibility table covers hT in [t0, t0 + tn); tn = 0: no table
 };
 
+// batched co-location simulator (simulate.cu)
+struct SimJob {
+    long long S;
+    int32_t W, K, C, G, N, n_requests, shared_default, ioctl;
+    const int32_t* n_kernels;   // [S*W]
+    const double* beta;         // [S*W*K*C]
+    const int32_t* table;       // [S*W*K]
+    const uint32_t* mask;       // [W*C]
+    const int32_t* group_sm;    // [G]
+    double barrier_ns, io_lo, io_mode, io_hi, oversub, p_idle, p_max;
+    unsigned long long seed;
+};
+struct SimOut {
+    double *throughput_rps, *p95_ns, *mean_ns;   // [S*W]
+    double *makespan_ns, *energy_j, *req_per_j;  // [S]
+    int32_t* barriers;
+    long long* events;
+    int32_t* status;
+};
+cudaError_t launch_simulate(const SimJob& J, const SimOut& o, double* latbuf, cudaStream_t st);
+
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
                         cudaStream_t st);
 cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st);

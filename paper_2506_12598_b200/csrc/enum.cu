@@ -1782,7 +1782,7 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
 // key is within tol of the (global) H*.  PASS 2 (unsharded runs): both in one rescan -- the band's
 // exactly evaluated candidates are kept in shared memory (a second rescan only on overflow).
 constexpr int P2_CAP = 256;
-constexpr int P2_THREADS = 128;   // small CTAs: pass 2 is latency-bound (a few exact evaluations per problem)
+constexpr int P2_THREADS = 512;
 template <int PASS>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,

@@ -77,7 +77,7 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
            "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats",
            "eclip_session_counters",
-           "eclip_baseline_plan", "eclip_lookup_table_json"]
+           "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate"]
 
 
 def lib():
@@ -485,3 +485,46 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------------------------------
+# batched co-location simulator (include/eclip.h eclip_simulate)
+class _SimBatch(C.Structure):
+    _fields_ = [("n_scenarios", C.c_int32), ("n_workers", C.c_int32), ("max_kernels", C.c_int32),
+                ("n_sizes", C.c_int32), ("n_groups", C.c_int32), ("n_kernels", C.c_void_p), ("beta_ns", C.c_void_p),
+                ("table", C.c_void_p), ("mask", C.c_void_p), ("group_sm", C.c_void_p), ("total_sms", C.c_int32),
+                ("n_requests", C.c_int32), ("shared_default", C.c_int32), ("mode", C.c_int32),
+                ("barrier_ns", C.c_double), ("ioctl_lo_ns", C.c_double), ("ioctl_mode_ns", C.c_double),
+                ("ioctl_hi_ns", C.c_double), ("oversub", C.c_double), ("p_idle_w", C.c_double),
+                ("p_max_w", C.c_double), ("seed", C.c_uint64)]
+
+
+class _SimOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("throughput_rps", "p95_ns", "mean_ns", "makespan_ns", "energy_j",
+                                          "req_per_j", "barriers", "events")]
+
+
+def simulate(n_kernels, beta_ns, table, mask, group_sm, *, total_sms: int, n_requests: int,
+             shared_default: bool = True, ioctl: bool = False, barrier_ns: float = 0.0,
+             ioctl_ns=(10000.0, 30000.0, 55400.0), oversub: float = 1.0, p_idle_w: float = 75.0,
+             p_max_w: float = 225.0, seed: int = 0, device: int = 0) -> dict:
+    """eclip_simulate.  n_kernels [S, W]; beta_ns [S, W, K, C]; table [S, W, K] pool indices;
+    mask [W, C] group bitsets (pool C-1 = full device); group_sm [G].  Returns numpy arrays."""
+    nk = _np(n_kernels, np.int32)
+    be = _np(beta_ns, np.float64)
+    tb = _np(table, np.int32)
+    mk = _np(mask, np.uint32)
+    gs = _np(group_sm, np.int32)
+    S, W, K, Cn = be.shape
+    assert nk.shape == (S, W) and tb.shape == (S, W, K) and mk.shape == (W, Cn)
+    b = _SimBatch(S, W, K, Cn, len(gs), nk.ctypes.data, be.ctypes.data, tb.ctypes.data, mk.ctypes.data,
+                  gs.ctypes.data, total_sms, n_requests, 1 if shared_default else 0, 1 if ioctl else 0,
+                  barrier_ns, ioctl_ns[0], ioctl_ns[1], ioctl_ns[2], oversub, p_idle_w, p_max_w, seed)
+    out = {"throughput_rps": np.zeros((S, W)), "p95_ns": np.zeros((S, W)), "mean_ns": np.zeros((S, W)),
+           "makespan_ns": np.zeros(S), "energy_j": np.zeros(S), "req_per_j": np.zeros(S),
+           "barriers": np.zeros(S, np.int32), "events": np.zeros(S, np.int64)}
+    o = _SimOut(*[out[n].ctypes.data for n, _ in _SimOut._fields_])
+    L = lib()
+    L.eclip_simulate.argtypes = [C.POINTER(_SimBatch), C.POINTER(Options), C.POINTER(_SimOut)]
+    _check(L.eclip_simulate(C.byref(b), C.byref(_options("auto", device)), C.byref(o)))
+    return out
