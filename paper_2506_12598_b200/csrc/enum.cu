@@ -530,20 +530,39 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
             if (threadIdx.x == 0) { s_t0 += mn; s_t1 += mx; }
         }
     }
-    // rank sort of both workers by (S', B, index), concurrently (threads [0,128): step, [128,256): inner)
+    // order of both workers by (S', B, index) (threads [0,128): step, [128,256): inner).  A worker's
+    // levels have distinct S', so with whole-row units it is the aux block's S' order; else rank sort.
     uint8_t* vflag = reinterpret_cast<uint8_t*>(stk + 2 * Lmax);      // [2][Lmax] hull-vertex flags (S' order)
+    int* SS = reinterpret_cast<int*>(vflag + ((2 * Lmax + 15) & ~15));  // [2][Lmax] S' in that order
+    long long* BB = reinterpret_cast<long long*>(SS + 2 * Lmax);       // [2][Lmax] B in that order
     const int which_t = threadIdx.x >> 7, tw = threadIdx.x & 127;
     {
         const Lev* lv = sv + (size_t)which_t * Lmax;
         const int L = P.L[W - 2 + which_t];
-        for (int i = tw; i < L; i += 128) {
-            const Lev& a = lv[i];
-            int rk = 0;
-            for (int j = 0; j < L; j++) {
-                const Lev& b = lv[j];
-                rk += (b.S < a.S) || (b.S == a.S && (b.B < a.B || (b.B == a.B && j < i)));
+        if (su.aux_bytes > 0 && su.nseg == 1) {
+            const AuxView A = aux_view(reinterpret_cast<unsigned char*>(const_cast<Lev*>(gbase) + (size_t)W * Lmax), Lmax);
+            const uint16_t* po = which_t == 0 ? A.sperm : A.perm;
+            for (int i = tw; i < L; i += 128) ord[which_t * Lmax + i] = po[i];
+        } else {
+            for (int i = tw; i < L; i += 128) {
+                const Lev& a = lv[i];
+                int rk = 0;
+                for (int j = 0; j < L; j++) {
+                    const Lev& b = lv[j];
+                    rk += (b.S < a.S) || (b.S == a.S && (b.B < a.B || (b.B == a.B && j < i)));
+                }
+                ord[which_t * Lmax + rk] = (uint16_t)i;
             }
-            ord[which_t * Lmax + rk] = (uint16_t)i;
+        }
+    }
+    __syncthreads();
+    {
+        const Lev* lv = sv + (size_t)which_t * Lmax;
+        const int L = P.L[W - 2 + which_t];
+        for (int t = tw; t < L; t += 128) {
+            const Lev& p = lv[ord[which_t * Lmax + t]];
+            SS[which_t * Lmax + t] = p.S;
+            BB[which_t * Lmax + t] = p.B;
         }
     }
     __syncthreads();
@@ -557,21 +576,24 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
         const Lev* lv = sv + (size_t)which_t * Lmax;
         const uint16_t* o = ord + which_t * Lmax;
         const int L = P.L[W - 2 + which_t];
+        const int* sS = SS + which_t * Lmax;
+        const long long* sB = BB + which_t * Lmax;
         for (int t = tw; t < L; t += 128) {
-            const Lev& p = lv[o[t]];
+            const int pS = sS[t];
+            const long long pB = sB[t];
             bool vert = true;
             int64_t lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 0;   // lo = 0, hi = +inf
-            for (int r = 0; r < L && vert; r++) {
-                if (r == t) continue;
-                const Lev& q = lv[o[r]];
-                if (r < t) {
-                    if (q.B <= p.B) vert = false;                 // dominated (S'_q <= S'_p)
-                    else {                                        // S'_q < S'_p here
-                        const int64_t n = q.B - p.B, d = (int64_t)(p.S - q.S);
-                        if (hi_d == 0 || n * hi_d < hi_n * d) { hi_n = n; hi_d = d; }
-                    }
-                } else if (q.S > p.S && q.B < p.B) {
-                    const int64_t n = p.B - q.B, d = (int64_t)(q.S - p.S);
+            for (int r = 0; r < t; r++) {                      // earlier points (S'_q <= S'_p)
+                const long long qB = sB[r];
+                if (qB <= pB) { vert = false; break; }           // dominated
+                const int64_t n = qB - pB, d = (int64_t)(pS - sS[r]);
+                if (hi_d == 0 || n * hi_d < hi_n * d) { hi_n = n; hi_d = d; }
+            }
+            for (int r = t + 1; r < L && vert; r++) {          // later points
+                const long long qB = sB[r];
+                const int qS = sS[r];
+                if (qS > pS && qB < pB) {
+                    const int64_t n = pB - qB, d = (int64_t)(qS - pS);
                     if (n * lo_d > lo_n * d) { lo_n = n; lo_d = d; }
                 }
             }
@@ -804,36 +826,51 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
     for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
-    float bm = INFINITY;
-    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-        int64_t hB = 0, hBS = 0;
-        int hT = 0, hTm = 1 << 24;
-        uint32_t x = r;
-#pragma unroll
-        for (int w = NH - 1; w >= 0; w--) {
-            const uint32_t d = x % Lh[w];
-            x /= Lh[w];
-            const Lev& v = hrec[w * Lmax + d];
-            hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
-        }
+    auto row_lb = [&](int64_t hB, int64_t hBS, int hT, int hTm) -> float {
         bool feas = true;
         if (QOS) {
             if (H.tn > 0) feas = ft[hT - H.t0] <= hTm - hT;
             else feas = !(H.smin_st > min(hTm - hT - H.smin_in, H.umax_in - hT) || H.umax_st < hT + H.smin_in);
         }
-        float lb = INFINITY;
-        if (feas) {
-            const float hBf = __ll2float_rn(hB), hTf = (float)hT;
-            const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
-            const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
-            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
-            const float Xh = fmaf(Dhf, invf, hBf);
-            const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
-            lb = (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
-                 0.99998474121f;   // 1 - 2^-16
+        if (!feas) return INFINITY;
+        const float hBf = __ll2float_rn(hB), hTf = (float)hT;
+        const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
+        const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
+        const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+        const float Xh = fmaf(Dhf, invf, hBf);
+        const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
+        return (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
+               0.99998474121f;   // 1 - 2^-16
+    };
+    float bm = INFINITY;
+    if (NH == 2 && Lh[NH - 1] <= 128) {
+        // rows = (d0, d1), d1 least significant: thread -> d1 (its record stays in registers), d0 strided
+        const int L0 = (int)Lh[0], L1 = (int)Lh[NH - 1], d1 = threadIdx.x & 127;
+        if (d1 < L1) {
+            const Lev r1 = hrec[(NH - 1) * Lmax + d1];
+            for (int d0 = threadIdx.x >> 7; d0 < L0; d0 += RLF_THREADS / 128) {
+                const Lev& r0 = hrec[d0];
+                const float lb = row_lb(r0.B + r1.B, r0.BS + r1.BS, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
+                lbs[d0 * L1 + d1] = lb;
+                bm = fminf(bm, lb);
+            }
         }
-        lbs[r] = lb;
-        bm = fminf(bm, lb);
+    } else {
+        for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+            int64_t hB = 0, hBS = 0;
+            int hT = 0, hTm = 1 << 24;
+            uint32_t x = r;
+#pragma unroll
+            for (int w = NH - 1; w >= 0; w--) {
+                const uint32_t d = x % Lh[w];
+                x /= Lh[w];
+                const Lev& v = hrec[w * Lmax + d];
+                hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
+            }
+            const float lb = row_lb(hB, hBS, hT, hTm);
+            lbs[r] = lb;
+            bm = fminf(bm, lb);
+        }
     }
     for (int o = 16; o; o >>= 1) bm = fminf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = bm;
@@ -1541,7 +1578,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = fill_u32(wk.submin, n * (size_t)su.units_max, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
-        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 + 2 * sizeof(Lev));
+        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 + 2 * sizeof(Lev) + 24) + 16;
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
         k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr);
@@ -1783,6 +1820,7 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
 // exactly evaluated candidates are kept in shared memory (a second rescan only on overflow).
 constexpr int P2_CAP = 256;
 constexpr int P2_THREADS = 512;
+constexpr int P2_ELIST = 1024;   // step levels per unit the pass-2 entry filter handles
 template <int PASS>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
@@ -1799,6 +1837,8 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
     __shared__ U256 c_key[P2_CAP];
     __shared__ int c_n;
     __shared__ U256 s_hs;
+    __shared__ int16_t s_elist[P2_ELIST];
+    __shared__ int s_ne;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     const int prob = blockIdx.x;
     Prob& P = probs[prob];
@@ -1880,10 +1920,67 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
                 if (idx < besti) besti = idx;
             }
         };
+        // entry filter (SUM, EXCLUDE_SELF / PAPER with QoS, W >= 3): a step level whose QoS-feasible
+        // inner range is empty, or whose every key is provably above the band (the pass-1 entry bound,
+        // DESIGN.md §3.9), is not scanned
+        int ne_list = -1;
+        if (su.aux_bytes > 0 && W >= 3 && su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && su.has_qos &&
+            e1 - e0 <= P2_ELIST) {
+            const AuxView A = aux_view(reinterpret_cast<unsigned char*>(const_cast<Lev*>(levs) +
+                                                                          (size_t)prob * su.lev_stride + (size_t)W * su.Lmax),
+                                       su.Lmax);
+            int64_t rB = 0, rBS = 0;
+            int rT = 0, rTm = 1 << 24;
+            for (int w = 0; w < W - 2; w++) {
+                const Lev& r = sl[w * su.Lmax + lv[w]];
+                rB += r.B; rBS += r.BS; rT += r.S; rTm = min(rTm, r.Tmax);
+            }
+            const float invf = P.inv;
+            const float hBf = __ll2float_rn(rB), hTf = (float)rT;
+            const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
+            float Xh;
+            if (su.mode == M_EXCL) {
+                const u128 Dh = (u128)rT * (u128)rB - (u128)rBS;
+                const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+                Xh = fmaf(Dhf, invf, hBf);
+            } else {
+                Xh = hBf * Yh;
+            }
+            const int s0 = A.hdr[0], u0v = A.hdr[1], slast = A.ssort[Lin - 1], ulast = A.usuf[Lin - 1];
+            const bool khi_ok = A.hdr[2] != 0, klo_ok = A.hdr[3] != 0;
+            const double invd = 1.0 / (double)P.lamN;
+            __syncthreads();   // the previous unit's list is no longer read
+            if (threadIdx.x == 0) s_ne = 0;
+            __syncthreads();
+            for (int e = e0 + (int)threadIdx.x; e < e1; e += blockDim.x) {
+                const Lev& r = se[e];
+                const int Tp = rT + r.S, Tm = min(rTm, r.Tmax);
+                const int khi = inner_khi(A, Tm - Tp, s0, slast, khi_ok, Lin);
+                const int klo = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
+                const bool pre = A.umaxp[min(klo, khi)] >= Tp;
+                bool keep = false;
+                if (khi > klo || pre) {
+                    const int ka = pre ? 0 : klo;
+                    const float Be = __ll2float_rn(r.B), Sf = (float)r.S;
+                    float X = fmaf(Be, Yh, fmaf(Sf, Zh, Xh));
+                    if (su.mode == M_PAPER) X += (float)((double)r.BS * invd);
+                    const float lbe = fmaf(fmaf(Sf, invf, Yh), A.preminB[khi], fmaf(fmaf(Be, invf, Zh), (float)A.ssort[ka], X)) *
+                                      0.99998474121f;   // 1 - 2^-16
+                    keep = !(lbe > bound);
+                }
+                if (keep) s_elist[atomicAdd(&s_ne, 1)] = (int16_t)e;
+            }
+            __syncthreads();
+            ne_list = s_ne;
+        }
         // 2-D thread map (inner level fixed per thread, step levels strided) when a padded row of
         // inner levels fits the block: no division per candidate
         const int KP = (Lin + 31) & ~31;
-        if (KP <= (int)blockDim.x) {
+        if (KP <= (int)blockDim.x && ne_list >= 0) {
+            const int EP = (int)blockDim.x / KP, kk = (int)threadIdx.x % KP, eo = (int)threadIdx.x / KP;
+            if (kk < Lin && eo < EP)
+                for (int i = eo; i < ne_list; i += EP) cand(s_elist[i], kk);
+        } else if (KP <= (int)blockDim.x) {
             const int EP = (int)blockDim.x / KP, kk = (int)threadIdx.x % KP, eo = (int)threadIdx.x / KP;
             if (kk < Lin && eo < EP)
                 for (int ke = e0 + eo; ke < e1; ke += EP) cand(ke, kk);
