@@ -156,6 +156,7 @@ static int parse_profiles(const char* text, size_t len, eclip_profiles** out) {
             }
         }
         if (cfg.empty()) return fail(ECLIP_E_PARSE, "parse failure: model %s: empty configs", name.c_str());
+        if (cfg.size() > 32) return fail(ECLIP_E_PARSE, "parse failure: model %s: more than 32 configs", name.c_str());
         if (P->sizes.empty()) P->sizes = cfg;
         else if (P->sizes != cfg)
             return fail(ECLIP_E_PARSE, "parse failure: model %s: configs differ from the first model's", name.c_str());
@@ -634,7 +635,7 @@ static int alloc_work(eclip_session* s) {
     const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
     const size_t o_sure = (en && su.mode == M_MATRIX && su.has_qos) ? bp.take<float>(ns) : 0;
     const size_t o_m32 = bp.take<float>(n), o_m32s = bp.take<float>(n), o_hs = bp.take<U256>(n), o_first = bp.take<U256>(n);
-    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0;
+    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0, o_pl = 0, o_pln = 0;
     if (bb) {
         o_rowlb = bp.take<float>(n * (size_t)su.rows_max);
         o_lbmin = bp.take<unsigned>(n);
@@ -644,6 +645,8 @@ static int alloc_work(eclip_session* s) {
         o_ulist = bp.take<uint2>(grid * (size_t)su.upi);
         o_uln = bp.take<int32_t>(grid);
         o_rh = bp.take<RowHdr>(n);
+        o_pl = bp.take<uint32_t>(n * (size_t)PL_CAP);
+        o_pln = bp.take<int32_t>(n);
     }
     unsigned char* base;
     CU(s->arena.alloc(&base, bp.off));
@@ -671,6 +674,8 @@ static int alloc_work(eclip_session* s) {
         wk.ulist = (uint2*)(base + o_ulist);
         wk.ulist_n = (int32_t*)(base + o_uln);
         wk.rowhdr = (RowHdr*)(base + o_rh);
+        wk.plist = (uint32_t*)(base + o_pl);
+        wk.plist_n = (int32_t*)(base + o_pln);
     }
     return ECLIP_OK;
 }

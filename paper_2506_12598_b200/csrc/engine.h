@@ -150,11 +150,14 @@ struct Work {
     unsigned long long* rows_done;  // [1] rows (units) pass 1 actually processed
     int32_t* bandn;             // [n] units in the pass-2 band list (-1: more than BAND_CAP, rescan all)
     uint64_t* bandlist;         // [n * BAND_CAP] band units in index order (k_reduce_min)
+    uint32_t* plist;            // [n * PL_CAP] units pass 1 processed with a finite minimum (pruned pass 1)
+    int32_t* plist_n;           // [n] their count (> PL_CAP: overflow, reduce_min scans every unit)
     cudaEvent_t kev[2];         // recorded on the launching stream around the dominant pass-1 kernel (or null)
 };
 
 constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem
-constexpr int BAND_CAP = 64;    // pass-2 band list capacity per problem
+constexpr int BAND_CAP = 64;
+constexpr int PL_CAP = 4096;   // processed-unit list capacity per problem    // pass-2 band list capacity per problem
 
 struct RowHdr {                 // per-problem constants of the row bound (k_prep_bound)
     int32_t nh[2];              // hull sizes (step, inner)

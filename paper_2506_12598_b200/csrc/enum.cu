@@ -468,9 +468,20 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
         A.hdr[4] = ss0; A.hdr[5] = su0; A.hdr[6] = shi_ok; A.hdr[7] = slo_ok;
     }
     __syncthreads();
-    const uint4* src = reinterpret_cast<const uint4*>(aux_s);
-    uint4* dst = reinterpret_cast<uint4*>(base + (size_t)W * Lmax);
-    for (int i = threadIdx.x; i < su.aux_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    // write out the fixed arrays, the used span of each lookup table (the rest is never read) and
+    // the header / step arrays
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(aux_s);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(base + (size_t)W * Lmax);
+    auto cp = [&](size_t off, size_t bytes) {
+        for (size_t i = threadIdx.x; i < (bytes + 3) / 4; i += blockDim.x) dst[off / 4 + i] = src[off / 4 + i];
+    };
+    const size_t o_khi = (size_t)(A.khi - aux_s), o_hdr = (size_t)(reinterpret_cast<unsigned char*>(A.hdr) - aux_s);
+    cp(0, o_khi);
+    if (khi_ok) cp(o_khi, (size_t)(A.ssort[Lin - 1] - s0 + 1));
+    if (klo_ok) cp(o_khi + P1_TABN, (size_t)(A.usuf[Lin - 1] - u0 + 1));
+    if (shi_ok) cp(o_khi + 2 * P1_TABN, (size_t)(A.stS[Lst - 1] - ss0 + 1));
+    if (slo_ok) cp(o_khi + 3 * P1_TABN, (size_t)(A.stU[Lst - 1] - su0 + 1));
+    cp(o_hdr, (size_t)su.aux_bytes - o_hdr);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -996,6 +1007,8 @@ struct BBArgs {
     const unsigned* lbmin;      // [n] smallest row bound of the problem (float bits)
     unsigned* inc;              // [n] global incumbent (float bits)
     unsigned long long* rows_done;
+    uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
+    int32_t* plist_n;
 };
 // Best-first order: each item's units with a finite row bound are listed by
 // bucket of bound / (smallest bound of the problem) - 1 in steps of 1/BB_SCALE (counting sort,
@@ -1356,6 +1369,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (wl == 0) {
             subp[unit] = m;
+            if (BB && m < INFINITY) {
+                const int pos = atomicAdd(bb.plist_n + prob, 1);
+                if (pos < PL_CAP) bb.plist[(size_t)prob * PL_CAP + pos] = (uint32_t)unit;
+            }
             if (BB && m < incv) {
                 atomicMin(&s_inc, __float_as_uint(m));
                 atomicMin(bb.inc + prob, __float_as_uint(m));
@@ -1578,6 +1595,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = fill_u32(wk.submin, n * (size_t)su.units_max, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(wk.plist_n, 0, n * sizeof(int32_t), st)) != cudaSuccess) return e;
         const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 + 2 * sizeof(Lev) + 24) + 16;
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
@@ -1600,7 +1618,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
                                                        wk.ulist, wk.ulist_n);
             if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
                 return e;
-            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done};
+            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n};
             if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
             f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
             if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
@@ -1614,7 +1632,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
         k_bucket<<<(unsigned)grid, 256, 0, st>>>(su, wk.probs, wk.rowlb, wk.lbmin, wk.ulist, wk.ulist_n);
-        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done};
+        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n};
         if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
         if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
@@ -1667,7 +1685,8 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
 // never larger, so its band is a subset), sorted into index order; bandn = -1: more than BAND_CAP
 __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs, const float* submin,
                                                     const float* submin_sure, float* m32, float* m32_sure,
-                                                    int32_t* bandn, uint64_t* bandlist) {
+                                                    int32_t* bandn, uint64_t* bandlist, const uint32_t* plist,
+                                                    const int32_t* plist_n) {
     __shared__ float rm[8], rs[8];
     __shared__ int s_cnt;
     __shared__ uint64_t s_list[BAND_CAP];
@@ -1675,6 +1694,10 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
     const Prob& P = probs[p];
     float m = INFINITY, ms = INFINITY;
     uint64_t a = 0, b = 0;
+    // units listed by the pruned pass 1 (every other unit kept submin = +inf); unsharded, no overflow
+    const int nl = plist_n ? plist_n[p] : -1;
+    const uint32_t* lst = (plist && su.n_shards == 1 && !submin_sure && nl >= 0 && nl <= PL_CAP) ? plist + (size_t)p * PL_CAP
+                                                                                                  : nullptr;
     if (P.status == 0) {
         uint64_t slo, shi;
         shard_items(P.n_items, su.shard, su.n_shards, &slo, &shi);
@@ -1682,9 +1705,13 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
         b = shi * (uint64_t)su.upi;
         if (b > P.units) b = P.units;
         const float* sp = submin + (size_t)p * su.units_max;
-        for (uint64_t u = a + tid; u < b; u += blockDim.x) {
-            m = fminf(m, sp[u]);
-            if (submin_sure) ms = fminf(ms, submin_sure[(size_t)p * su.units_max + u]);
+        if (lst) {   // pruned pass 1: only the listed units can be finite
+            for (int i = tid; i < nl; i += blockDim.x) m = fminf(m, sp[lst[i]]);
+        } else {
+            for (uint64_t u = a + tid; u < b; u += blockDim.x) {
+                m = fminf(m, sp[u]);
+                if (submin_sure) ms = fminf(ms, submin_sure[(size_t)p * su.units_max + u]);
+            }
         }
     }
     for (int o = 16; o; o >>= 1) {
@@ -1704,11 +1731,19 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
     if (P.status == 0 && !isinf(m)) {
         const float bound = band_bound(su, m, submin_sure ? ms : m);
         const float* sp = submin + (size_t)p * su.units_max;
-        for (uint64_t u = a + tid; u < b; u += blockDim.x)
-            if (sp[u] <= bound) {
-                const int pos = atomicAdd(&s_cnt, 1);
-                if (pos < BAND_CAP) s_list[pos] = u;
-            }
+        if (lst) {
+            for (int i = tid; i < nl; i += blockDim.x)
+                if (sp[lst[i]] <= bound) {
+                    const int pos = atomicAdd(&s_cnt, 1);
+                    if (pos < BAND_CAP) s_list[pos] = lst[i];
+                }
+        } else {
+            for (uint64_t u = a + tid; u < b; u += blockDim.x)
+                if (sp[u] <= bound) {
+                    const int pos = atomicAdd(&s_cnt, 1);
+                    if (pos < BAND_CAP) s_list[pos] = u;
+                }
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -1729,7 +1764,7 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
     const bool two = su.mode == M_MATRIX && su.has_qos;
     k_reduce_min<<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
-                                                wk.m32_sure, wk.bandn, wk.bandlist);
+                                                wk.m32_sure, wk.bandn, wk.bandlist, wk.plist, wk.plist_n);
     return cudaGetLastError();
 }
 

@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             const int cur = g & 1, nxt = cur ^ 1;
             int64_t b1 = INF64, b2 = INF64;
             int a1 = -1;
+            // all loads of the cell first (independent across j, so they overlap), then the stores
+            int64_t outv[32];
+#pragma unroll 8
             for (int j = 0; j < J.C; j++) {
                 int64_t out = INF64;
                 if ((J.mask >> j) & 1u) {
@@ -82,6 +85,10 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
                         if (v != INF64) out = b + v;
                     }
                 }
+                outv[j] = out;
+            }
+            for (int j = 0; j < J.C; j++) {
+                const int64_t out = outv[j];
                 J.V[vidx(J, g, j, r, s)] = out;
                 if (out < b1) { b2 = b1; b1 = out; a1 = j; }
                 else if (out < b2) { b2 = out; }
@@ -149,14 +156,20 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         uint64_t word = 0;
         for (int g = 0; g < J.G; g++) {
             int pick = -1;
-            for (int j = 0; j < J.C && pick < 0; j++) {
+            // the candidates' values are loaded together (independent), then the first match is taken
+            int64_t cv[32];
+#pragma unroll 8
+            for (int j = 0; j < J.C; j++) {
+                cv[j] = INF64;
                 if (!((J.mask >> j) & 1u)) continue;
                 const int nd = J.need[g * J.C + j];
                 if (nd > rem) continue;
                 const int rr = (g == 0 || j == prev) ? r : r - 1;
                 if (rr < 0) continue;
-                if (J.V[vidx(J, g, j, rr, rem)] == opt) pick = j;
+                cv[j] = J.V[vidx(J, g, j, rr, rem)];
             }
+            for (int j = 0; j < J.C && pick < 0; j++)
+                if (cv[j] == opt) pick = j;
             if (pick < 0) pick = 0;   // unreachable: opt is attained
             if (g > 0 && pick != prev) r--;
             opt -= J.beta[g * J.C + pick];
