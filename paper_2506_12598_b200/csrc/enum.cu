@@ -1058,7 +1058,10 @@ __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, con
 }
 
 template <int NW, int MODE, bool QOS, bool BB>
-__global__ void __launch_bounds__(P1_THREADS, 3)
+#ifndef P1_MINB
+#define P1_MINB 3
+#endif
+__global__ void __launch_bounds__(P1_THREADS, P1_MINB)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
              unsigned long long* __restrict__ feasible, BBArgs bb) {
     constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)

@@ -35,6 +35,134 @@ __device__ __forceinline__ int vidx(const LevelJob& J, int g, int j, int r, int 
 }
 __device__ __forceinline__ int nwords(const LevelJob& J) { return (J.G + 7) / 8; }
 
+// one (r, s) cell of layer g = G-1-step: V for all sizes j, and best / second best / arg over j
+__device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
+    const int S1 = J.smax + 1, ncell = (J.R + 1) * S1;
+    const int r = k / S1, s = k - r * S1;
+    const int g = J.G - 1 - step;
+    const int cur = g & 1, nxt = cur ^ 1;
+    int64_t b1 = INF64, b2 = INF64;
+    int a1 = -1;
+    // all loads of the cell first (independent across j, so they overlap), then the stores
+    int64_t outv[32];
+#pragma unroll 8
+    for (int j = 0; j < J.C; j++) {
+        int64_t out = INF64;
+        if ((J.mask >> j) & 1u) {
+            const int nd = J.need[g * J.C + j];
+            const int64_t b = J.beta[g * J.C + j];
+            if (g == J.G - 1) {
+                if (s == nd) out = b;
+            } else if (nd <= s) {
+                const int sp = s - nd;
+                int64_t v = J.V[vidx(J, g + 1, j, r, sp)];
+                if (r >= 1) {
+                    const int bi = nxt * ncell + (r - 1) * S1 + sp;
+                    const int64_t w = (J.barg[bi] != j) ? J.best[2 * bi] : J.best[2 * bi + 1];
+                    if (w < v) v = w;
+                }
+                if (v != INF64) out = b + v;
+            }
+        }
+        outv[j] = out;
+    }
+    for (int j = 0; j < J.C; j++) {
+        const int64_t out = outv[j];
+        J.V[vidx(J, g, j, r, s)] = out;
+        if (out < b1) { b2 = b1; b1 = out; a1 = j; }
+        else if (out < b2) { b2 = out; }
+    }
+    const int bo = cur * ncell + k;
+    J.best[2 * bo] = b1;
+    J.best[2 * bo + 1] = b2;
+    J.barg[bo] = a1;
+}
+
+// greedy reconstruction of level l's canonical witness (packed words)
+__device__ __forceinline__ void reconstruct(const LevelJob& J, int l) {
+    int rem = J.sidx[l];
+    int64_t opt = J.bstar[rem];
+    int r = J.R, prev = -1;
+    const int nw = nwords(J);
+    uint64_t word = 0;
+    for (int g = 0; g < J.G; g++) {
+        int pick = -1;
+        // the candidates' values are loaded together (independent), then the first match is taken
+        int64_t cv[32];
+#pragma unroll 8
+        for (int j = 0; j < J.C; j++) {
+            cv[j] = INF64;
+            if (!((J.mask >> j) & 1u)) continue;
+            const int nd = J.need[g * J.C + j];
+            if (nd > rem) continue;
+            const int rr = (g == 0 || j == prev) ? r : r - 1;
+            if (rr < 0) continue;
+            cv[j] = J.V[vidx(J, g, j, rr, rem)];
+        }
+        for (int j = 0; j < J.C && pick < 0; j++)
+            if (cv[j] == opt) pick = j;
+        if (pick < 0) pick = 0;   // unreachable: opt is attained
+        if (g > 0 && pick != prev) r--;
+        opt -= J.beta[g * J.C + pick];
+        rem -= J.need[g * J.C + pick];
+        prev = pick;
+        word |= (uint64_t)pick << (8 * (7 - (g & 7)));
+        if ((g & 7) == 7 || g == J.G - 1) {
+            J.wtmp[(size_t)l * nw + (g >> 3)] = word;
+            word = 0;
+        }
+    }
+}
+
+// rank of level l = number of lexicographically smaller witnesses; scatter to rank order
+__device__ __forceinline__ void rank_level(const LevelJob& J, int l, int L) {
+    const int nw = nwords(J);
+    const uint64_t* a = J.wtmp + (size_t)l * nw;
+    int rk = 0;
+    for (int m = 0; m < L; m++) {
+        const uint64_t* b = J.wtmp + (size_t)m * nw;
+        for (int q = 0; q < nw; q++) {
+            if (b[q] != a[q]) { rk += (b[q] < a[q]); break; }
+        }
+    }
+    const int s = J.sidx[l];
+    J.outS[rk] = (int64_t)s * J.u;
+    J.outB[rk] = J.bstar[s];
+    for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
+}
+
+// B*(s) = best over j of layer 0 at r = R; compact the attained levels (one CTA per table)
+__device__ __forceinline__ void compact_table(const LevelJob& J) {
+    __shared__ int s_count;
+    __shared__ int s_warp[32];
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    const int S1 = J.smax + 1;
+    for (int base = 0; base <= J.smax; base += blockDim.x) {
+        const int s = base + threadIdx.x;
+        int64_t b = INF64;
+        if (s <= J.smax) {
+            b = J.best[2 * (J.R * S1 + s)];   // layer 0 lives in buffer 0
+            J.bstar[s] = b;
+        }
+        const int valid = (s <= J.smax) && (b != INF64);
+        const unsigned bal = __ballot_sync(0xffffffffu, valid);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = s_count;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) { int c = s_warp[w]; s_warp[w] = acc; acc += c; }
+            s_count = acc;
+        }
+        __syncthreads();
+        if (valid) J.sidx[s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = s;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *J.outL = s_count;
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax) {
     cg::grid_group grid = cg::this_grid();
     __shared__ LevelJob sj[MAXJ];
@@ -58,81 +186,13 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             while (off[t + 1] <= i) t++;
             const LevelJob& J = sj[t];
             const int k = i - off[t];
-            const int S1 = J.smax + 1, ncell = (J.R + 1) * S1;
-            const int r = k / S1, s = k - r * S1;
-            const int g = J.G - 1 - step;
-            const int cur = g & 1, nxt = cur ^ 1;
-            int64_t b1 = INF64, b2 = INF64;
-            int a1 = -1;
-            // all loads of the cell first (independent across j, so they overlap), then the stores
-            int64_t outv[32];
-#pragma unroll 8
-            for (int j = 0; j < J.C; j++) {
-                int64_t out = INF64;
-                if ((J.mask >> j) & 1u) {
-                    const int nd = J.need[g * J.C + j];
-                    const int64_t b = J.beta[g * J.C + j];
-                    if (g == J.G - 1) {
-                        if (s == nd) out = b;
-                    } else if (nd <= s) {
-                        const int sp = s - nd;
-                        int64_t v = J.V[vidx(J, g + 1, j, r, sp)];
-                        if (r >= 1) {
-                            const int bi = nxt * ncell + (r - 1) * S1 + sp;
-                            const int64_t w = (J.barg[bi] != j) ? J.best[2 * bi] : J.best[2 * bi + 1];
-                            if (w < v) v = w;
-                        }
-                        if (v != INF64) out = b + v;
-                    }
-                }
-                outv[j] = out;
-            }
-            for (int j = 0; j < J.C; j++) {
-                const int64_t out = outv[j];
-                J.V[vidx(J, g, j, r, s)] = out;
-                if (out < b1) { b2 = b1; b1 = out; a1 = j; }
-                else if (out < b2) { b2 = out; }
-            }
-            const int bo = cur * ncell + k;
-            J.best[2 * bo] = b1;
-            J.best[2 * bo + 1] = b2;
-            J.barg[bo] = a1;
+            dp_cell(J, step, k);
         }
         grid.sync();
     }
 
     // ---- per table (one CTA each): B*(s) = best over j of layer 0 at r = R; compact ----
-    for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) {
-        const LevelJob& J = sj[t];
-        __shared__ int s_count;
-        __shared__ int s_warp[32];
-        if (threadIdx.x == 0) s_count = 0;
-        __syncthreads();
-        const int S1 = J.smax + 1;
-        for (int base = 0; base <= J.smax; base += blockDim.x) {
-            const int s = base + threadIdx.x;
-            int64_t b = INF64;
-            if (s <= J.smax) {
-                b = J.best[2 * (J.R * S1 + s)];   // layer 0 lives in buffer 0
-                J.bstar[s] = b;
-            }
-            const int valid = (s <= J.smax) && (b != INF64);
-            const unsigned bal = __ballot_sync(0xffffffffu, valid);
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-            if (lane == 0) s_warp[warp] = __popc(bal);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int acc = s_count;
-                for (int w = 0; w < (int)(blockDim.x >> 5); w++) { int c = s_warp[w]; s_warp[w] = acc; acc += c; }
-                s_count = acc;
-            }
-            __syncthreads();
-            if (valid) J.sidx[s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = s;
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) *J.outL = s_count;
-        __syncthreads();
-    }
+    for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) compact_table(sj[t]);
     grid.sync();
 
     // flattened (table, level) work for the remaining phases
@@ -149,38 +209,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         while (off[t + 1] <= i) t++;
         const LevelJob& J = sj[t];
         const int l = i - off[t];
-        int rem = J.sidx[l];
-        int64_t opt = J.bstar[rem];
-        int r = J.R, prev = -1;
-        const int nw = nwords(J);
-        uint64_t word = 0;
-        for (int g = 0; g < J.G; g++) {
-            int pick = -1;
-            // the candidates' values are loaded together (independent), then the first match is taken
-            int64_t cv[32];
-#pragma unroll 8
-            for (int j = 0; j < J.C; j++) {
-                cv[j] = INF64;
-                if (!((J.mask >> j) & 1u)) continue;
-                const int nd = J.need[g * J.C + j];
-                if (nd > rem) continue;
-                const int rr = (g == 0 || j == prev) ? r : r - 1;
-                if (rr < 0) continue;
-                cv[j] = J.V[vidx(J, g, j, rr, rem)];
-            }
-            for (int j = 0; j < J.C && pick < 0; j++)
-                if (cv[j] == opt) pick = j;
-            if (pick < 0) pick = 0;   // unreachable: opt is attained
-            if (g > 0 && pick != prev) r--;
-            opt -= J.beta[g * J.C + pick];
-            rem -= J.need[g * J.C + pick];
-            prev = pick;
-            word |= (uint64_t)pick << (8 * (7 - (g & 7)));
-            if ((g & 7) == 7 || g == J.G - 1) {
-                J.wtmp[(size_t)l * nw + (g >> 3)] = word;
-                word = 0;
-            }
-        }
+        reconstruct(J, l);
     }
     grid.sync();
 
@@ -190,20 +219,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         while (off[t + 1] <= i) t++;
         const LevelJob& J = sj[t];
         const int l = i - off[t];
-        const int L = off[t + 1] - off[t];
-        const int nw = nwords(J);
-        const uint64_t* a = J.wtmp + (size_t)l * nw;
-        int rk = 0;
-        for (int m = 0; m < L; m++) {
-            const uint64_t* b = J.wtmp + (size_t)m * nw;
-            for (int q = 0; q < nw; q++) {
-                if (b[q] != a[q]) { rk += (b[q] < a[q]); break; }
-            }
-        }
-        const int s = J.sidx[l];
-        J.outS[rk] = (int64_t)s * J.u;
-        J.outB[rk] = J.bstar[s];
-        for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
+        rank_level(J, l, off[t + 1] - off[t]);
     }
 }
 

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeclip.so")
+LIB_PATH = os.environ.get("ECLIP_LIB") or os.path.join(_HERE, "libeclip.so")   # ECLIP_LIB: A/B builds only
 
 OK, INFEASIBLE = 0, 1
 E_PARSE, E_MISSING_CONFIG, E_NONMONOTONE, E_INVALID_ARG, E_TOO_LARGE, E_CUDA, E_OOM, E_IO = range(-1, -9, -1)
