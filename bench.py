@@ -272,7 +272,8 @@ def main():
             "gpu_launches": int(8 * a.steps),
             "roofline": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,QoS>", "achieved": achieved,
                          "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
-                         "frac": achieved / peak, "traffic": ncu_traffic(a.mixes),
+                         "frac": achieved / peak, "traffic": (ncu_pass1(a.mixes) or {}).get("bytes_per_launch"),
+                         "issue_slots_busy_pct_ncu": (ncu_pass1(a.mixes) or {}).get("issue_active_pct"),
                          "kernel_ms_per_launch": k_ms / k_launches,
                          "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
                          "fma_lane_ops_per_evaluated_candidate": fma_ops_per_cand,
@@ -305,13 +306,14 @@ def main():
         dist.destroy_process_group()
 
 
-def ncu_traffic(mixes):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one k_pass1_fast launch on this workload,
-    from the committed `ncu --set full` capture (profiles/pass1_traffic.json), else None."""
+def ncu_pass1(mixes):
+    """From the committed `ncu --set full` capture of k_pass1_fast on this workload
+    (profiles/pass1_traffic.json): dram__bytes_read.sum + dram__bytes_write.sum per launch, and the
+    issue-slot utilisation (sm__inst_issued.avg.pct_of_peak_sustained_active); None if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "pass1_traffic.json")) as f:
             t = json.load(f)
-        return t["bytes_per_launch"] if t.get("mixes") == mixes else None
+        return t if t.get("mixes") == mixes else None
     except Exception:
         return None
 
