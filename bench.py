@@ -228,7 +228,7 @@ def main():
     # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
     pin_ids = torch.from_numpy(ids).pin_memory()
     pin_q = torch.from_numpy(qos).pin_memory()
-    h_out = ec.alloc_batch_out(a.mixes, 4, 16)
+    h_out = ec.alloc_batch_out(a.mixes, 4, 16, pinned=True)   # page-locked result buffers
     e2e_ms = []
     barrier()
     for _ in range(a.steps):

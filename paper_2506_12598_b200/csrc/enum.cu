@@ -293,7 +293,8 @@ struct AuxView {
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
-    size_t b = LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 4 * (size_t)P1_TABN + 32 + (size_t)Lmax * 12 +
+    size_t b = ((LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 15) & ~(size_t)15) + 4 * (size_t)P1_TABN + 32 +
+               (size_t)Lmax * 12 +
                (size_t)(Lmax + 1) * 4 + (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;
     return (b + 31) / 32 * 32;
 }
@@ -309,7 +310,7 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.umaxp = a.usuf + (Lmax + 1);
     a.perm = reinterpret_cast<uint16_t*>(a.umaxp + (Lmax + 1));
     a.sperm = a.perm + Lmax;
-    a.khi = reinterpret_cast<uint8_t*>(a.sperm + Lmax);
+    a.khi = base + ((reinterpret_cast<unsigned char*>(a.sperm + Lmax) - base + 15) & ~(size_t)15);   // 16-aligned tables
     a.klo = a.khi + P1_TABN;
     a.shi = a.klo + P1_TABN;
     a.slo = a.shi + P1_TABN;
@@ -470,10 +471,11 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     __syncthreads();
     // write out the fixed arrays, the used span of each lookup table (the rest is never read) and
     // the header / step arrays
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(aux_s);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(base + (size_t)W * Lmax);
-    auto cp = [&](size_t off, size_t bytes) {
-        for (size_t i = threadIdx.x; i < (bytes + 3) / 4; i += blockDim.x) dst[off / 4 + i] = src[off / 4 + i];
+    const uint4* src = reinterpret_cast<const uint4*>(aux_s);
+    uint4* dst = reinterpret_cast<uint4*>(base + (size_t)W * Lmax);
+    auto cp = [&](size_t off, size_t bytes) {   // off is 16-aligned (aux layout)
+        const int n = (int)((bytes + 15) / 16), o = (int)(off / 16);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[o + i] = src[o + i];
     };
     const size_t o_khi = (size_t)(A.khi - aux_s), o_hdr = (size_t)(reinterpret_cast<unsigned char*>(A.hdr) - aux_s);
     cp(0, o_khi);

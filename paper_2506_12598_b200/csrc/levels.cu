@@ -163,7 +163,8 @@ __device__ __forceinline__ void compact_table(const LevelJob& J) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax) {
+__global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax,
+                                                size_t wsm_words) {
     cg::grid_group grid = cg::this_grid();
     __shared__ LevelJob sj[MAXJ];
     __shared__ int off[MAXJ + 1];
@@ -213,13 +214,41 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     }
     grid.sync();
 
-    // ---- rank = number of lexicographically smaller witnesses; scatter to rank order ----
-    for (int i = gtid; i < nlev; i += gstride) {
-        int t = 0;
-        while (off[t + 1] <= i) t++;
+    // ---- rank = number of lexicographically smaller witnesses; scatter to rank order.  One CTA
+    // per table with the table's witness words staged in shared memory (the comparisons are
+    // O(L^2); from global memory each thread would walk L dependent L2 loads) ----
+    extern __shared__ uint64_t wsm[];
+    if (wsm_words == 0) {   // large tables: one thread per level over the whole grid, from global memory
+        for (int i = gtid; i < nlev; i += gstride) {
+            int t = 0;
+            while (off[t + 1] <= i) t++;
+            rank_level(sj[t], i - off[t], off[t + 1] - off[t]);
+        }
+        return;
+    }
+    for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) {
         const LevelJob& J = sj[t];
-        const int l = i - off[t];
-        rank_level(J, l, off[t + 1] - off[t]);
+        const int L = off[t + 1] - off[t], nw = nwords(J);
+        if ((size_t)L * nw <= wsm_words) {
+            for (int i = threadIdx.x; i < L * nw; i += blockDim.x) wsm[i] = J.wtmp[i];
+            __syncthreads();
+            for (int l = threadIdx.x; l < L; l += blockDim.x) {
+                const uint64_t* a = wsm + (size_t)l * nw;
+                int rk = 0;
+                for (int m = 0; m < L; m++) {
+                    const uint64_t* b = wsm + (size_t)m * nw;
+                    for (int q = 0; q < nw; q++)
+                        if (b[q] != a[q]) { rk += (b[q] < a[q]); break; }
+                }
+                const int s = J.sidx[l];
+                J.outS[rk] = (int64_t)s * J.u;
+                J.outB[rk] = J.bstar[s];
+                for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
+            }
+            __syncthreads();
+        } else {
+            for (int l = threadIdx.x; l < L; l += blockDim.x) rank_level(J, l, L);
+        }
     }
 }
 
@@ -231,12 +260,22 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, 256, 0);
+    // shared memory for the ranking phase: the largest table's witness words (level count <= Lcap)
+    size_t wsm = 0;
+    for (int i = 0; i < n_jobs; i++) {
+        const size_t w = (size_t)h_jobs[i].Lcap * ((h_jobs[i].G + 7) / 8);
+        if (w > wsm) wsm = w;
+    }
+    if (wsm > 2048) wsm = 0;   // large tables (many levels, e.g. BASELINE C4) rank from global memory (measured faster)
+    size_t wsm_words = wsm;
+    e = cudaFuncSetAttribute((const void*)k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsm * 8));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, 256, wsm * 8);
     if (e != cudaSuccess) return e;
     if (per_sm > 2) per_sm = 2;
     int grid = nsm * (per_sm > 0 ? per_sm : 1);
-    void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax};
-    return cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, 0, st);
+    void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax, (void*)&wsm_words};
+    return cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, wsm * 8, st);
 }
 
 }  // namespace eclip

@@ -364,10 +364,15 @@ class _BatchArgs:
                        switch_max, MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 1 if on_device else 0)
 
 
-def alloc_batch_out(n: int, W: int, gmax: int = 0, device=None):
-    """result buffers for plan_batch: numpy (host) or torch tensors on `device`"""
+def alloc_batch_out(n: int, W: int, gmax: int = 0, device=None, pinned: bool = False):
+    """result buffers for plan_batch: numpy (host; page-locked when pinned) or torch tensors on `device`"""
     if device is None:
-        mk = lambda shape, dt: np.zeros(shape, dt)
+        if pinned:
+            import torch
+            tdt = {np.int32: torch.int32, np.uint64: torch.int64, np.float64: torch.float64}
+            mk = lambda shape, dt: torch.zeros(shape, dtype=tdt[dt]).pin_memory().numpy().view(dt)
+        else:
+            mk = lambda shape, dt: np.zeros(shape, dt)
         i32, u64, f64 = np.int32, np.uint64, np.float64
     else:
         import torch
