@@ -220,6 +220,7 @@ def main():
     # chain_ms = the whole pass-1 chain (row bounds, bucket sort, the kernel, its reduction);
     # k_ms = the dominant kernel alone (events recorded around its launch inside the library)
     chain_ms, k_launches, k_eval, k_units, k_ms = pass1_time(ec, pr, ids, qos, stream, local)
+    p1_extra = dict(pass1_time.extra)
     # the same pass without row pruning (every row classified) and without QoS bounds, for context
     x_ms, x_launches, x_eval, _, x_kms = pass1_time(ec, pr, ids, qos, stream, local, prune=False)
     n_ms, n_launches, n_eval, n_units, n_kms = pass1_time(ec, pr, ids, None, stream, local)
@@ -281,6 +282,8 @@ def main():
                          "evaluated_fraction": k_eval / cand_step,
                          "candidates_per_s_kernel": cand_per_s_kernel},
             "pruning": {"units_total_per_launch": units_total, "units_processed_per_launch": k_units,
+                        "units_with_swept_entries_per_launch": p1_extra["units_with_swept_entries"],
+                        "entries_swept_per_launch": p1_extra["entries_swept"],
                         "pass1_chain_ms_pruned": chain_ms / k_launches, "pass1_chain_ms_exhaustive": x_ms / x_launches,
                         "pass1_kernel_ms_exhaustive": x_kms / x_launches,
                         "evaluated_candidates_exhaustive": x_eval,
@@ -348,7 +351,9 @@ def pass1_time(ec, pr, ids, qos, stream, local, prune=True):
             st = s.stats()
             evaluated, units = st["evaluated_candidates"], st["units_processed"]
             kern += st["kernel_ms"]
+            extra = {"units_with_swept_entries": st["units_with_swept_entries"], "entries_swept": st["entries_swept"]}
         s.close()
+    pass1_time.extra = extra
     return tot, launches, evaluated, units, kern
 
 

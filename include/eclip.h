@@ -214,7 +214,9 @@ int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
  * [1] pass-1 units (rows x segments) processed under row pruning (0 when pruning is off;
  * the rest were proven outside the tolerance band by their lower bound),
  * [2] device time in ns of the last launch of the dominant pass-1 kernel (k_pass1_fast or
- * k_pass1_gen), from CUDA events recorded around it on the launching stream (0 for SLICE).
+ * k_pass1_gen), from CUDA events recorded around it on the launching stream (0 for SLICE),
+ * [3] pruned pass 1: units in which at least one step entry survived the chunk / entry bounds and
+ * was swept, [4] entries swept.
  * Entries beyond the defined ones are set to 0.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_CUDA. */
 int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n);
 

@@ -476,9 +476,10 @@ class Session:
         """counters of the last pass 1: evaluated = QoS-feasible candidates scored in FP32;
         units_processed = pass-1 units (rows) not pruned by their bound (0 when pruning is off);
         kernel_ms = CUDA-event time of the dominant pass-1 kernel's last launch"""
-        v = (C.c_uint64 * 3)()
-        _check(lib().eclip_session_counters(self._h, v, 3))
-        return {"evaluated_candidates": int(v[0]), "units_processed": int(v[1]), "kernel_ms": int(v[2]) * 1e-6}
+        v = (C.c_uint64 * 5)()
+        _check(lib().eclip_session_counters(self._h, v, 5))
+        return {"evaluated_candidates": int(v[0]), "units_processed": int(v[1]), "kernel_ms": int(v[2]) * 1e-6,
+                "units_with_swept_entries": int(v[3]), "entries_swept": int(v[4])}
 
     def close(self):
         if self._h is not None and self._h.value:
