@@ -629,7 +629,7 @@ static int alloc_work(eclip_session* s) {
     const size_t ns = n * (size_t)su.units_max;
     const size_t grid = n * (size_t)((su.items_max + su.n_shards - 1) / su.n_shards);
     Bump bp;   // one block; null pieces stay null
-    const size_t o_cnt = bp.take<unsigned long long>(2);   // feasible, rows_done (zeroed)
+    const size_t o_cnt = bp.take<unsigned long long>(4);   // feasible, rows_done[3] (zeroed)
     const size_t o_probs = bp.take<Prob>(n), o_levs = bp.take<Lev>(n * (size_t)su.lev_stride);
     const size_t o_sub = en ? bp.take<float>(ns) : 0, o_bandn = en ? bp.take<int32_t>(n) : 0;
     const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
@@ -652,7 +652,7 @@ static int alloc_work(eclip_session* s) {
     CU(s->arena.alloc(&base, bp.off));
     wk.feasible = (unsigned long long*)(base + o_cnt);
     wk.rows_done = wk.feasible + 1;
-    CU(cudaMemsetAsync(wk.feasible, 0, 2 * sizeof(unsigned long long), s->st));
+    CU(cudaMemsetAsync(wk.feasible, 0, 4 * sizeof(unsigned long long), s->st));
     wk.probs = (Prob*)(base + o_probs);
     wk.levs = (Lev*)(base + o_levs);
     if (en) {
@@ -1027,15 +1027,16 @@ extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
 
 extern "C" int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n) {
     if (!s || !out || n < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
-    unsigned long long v[3] = {0, 0, 0};
+    unsigned long long v[5] = {0, 0, 0, 0, 0};
     if (s->wk.feasible) CU(cudaMemcpyAsync(&v[0], s->wk.feasible, sizeof v[0], cudaMemcpyDeviceToHost, s->st));
     if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[1], s->wk.rows_done, sizeof v[1], cudaMemcpyDeviceToHost, s->st));
+    if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[3], s->wk.rows_done + 1, 2 * sizeof v[0], cudaMemcpyDeviceToHost, s->st));
     CU(cudaStreamSynchronize(s->st));
     float ms = 0.0f;   // the events exist from session creation; unrecorded (SLICE) -> error -> 0
     if (s->engine == ECLIP_ENGINE_ENUM && cudaEventElapsedTime(&ms, s->wk.kev[0], s->wk.kev[1]) == cudaSuccess)
         v[2] = (unsigned long long)llround((double)ms * 1e6);
     cudaGetLastError();
-    for (int i = 0; i < n; i++) out[i] = i < 3 ? v[i] : 0;
+    for (int i = 0; i < n; i++) out[i] = i < 5 ? v[i] : 0;
     return ECLIP_OK;
 }
 

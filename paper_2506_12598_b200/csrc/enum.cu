@@ -1008,7 +1008,7 @@ struct BBArgs {
     const int32_t* ulist_n;     // [grid]
     const unsigned* lbmin;      // [n] smallest row bound of the problem (float bits)
     unsigned* inc;              // [n] global incumbent (float bits)
-    unsigned long long* rows_done;
+    unsigned long long* rows_done;  // [3]: units processed, units with >= 1 swept entry, entries swept
     uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
     int32_t* plist_n;
 };
@@ -1125,7 +1125,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // BB: warps take 32 list entries at a time (best-first), process the ones within the band of the
     // incumbent, and stop when the rest of the list is provably outside it.  Otherwise: 32
     // consecutive units per round, rounds strided by NWARP * 32.
-    unsigned long long nfeas = 0, ndone = 0;
+    unsigned long long nfeas = 0, ndone = 0, nue = 0, nent = 0;
     float bnd = INFINITY, incv = INFINITY, bnd_of = -1.0f;
     constexpr uint64_t RSTEP = (uint64_t)NWARP * 32;
     uint64_t rbase = ua + (uint64_t)warp * 32;
@@ -1280,6 +1280,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 tabk[pos] = make_int2(klo, khi);
             }
             nc += __popc(bal);
+            if (wl == 0) nent += __popc(bal);
             return past;
         };
         bool chunked = false;
@@ -1324,6 +1325,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             for (int kb = 0; kb < ne; kb += 32)
                 if (__all_sync(0xffffffffu, entry(kb + wl, kb + wl < ne))) break;   // the rest of the sorted segment is unusable
         __syncwarp();
+        if (BB && wl == 0 && nc > 0) nue++;
         float m0 = INFINITY, m1 = INFINITY;
         for (int i = wl; i < nc; i += 32) {
             const float4 t4 = tab[i];
@@ -1389,7 +1391,11 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     }
     for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
     if (wl == 0 && nfeas) atomicAdd(feasible, nfeas);
-    if (BB && wl == 0 && ndone) atomicAdd(bb.rows_done, ndone);
+    if (BB && wl == 0 && ndone) {
+        atomicAdd(bb.rows_done, ndone);
+        atomicAdd(bb.rows_done + 1, nue);
+        atomicAdd(bb.rows_done + 2, nent);
+    }
 }
 
 // Generic (unpacked) filter: MAX / ENERGY objectives, EXCESS, MATRIX (any objective), and
