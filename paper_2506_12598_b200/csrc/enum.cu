@@ -717,6 +717,40 @@ __device__ __forceinline__ float hull_min(const float2* v, const float2* ed, int
     return m;
 }
 
+// min over the points of a lower-left hull's point set with S' in [slo, shi] of B y + S' z (y, z >= 0),
+// bounded below: the objective along the hull is convex in S', so the constrained minimum is at the
+// unconstrained minimiser when it lies in the range, else at the nearer end, where the hull's B is
+// interpolated (beyond the last vertex -- the minimum-B point -- every point has B >= its B).  An
+// argmin misjudged by FP32 rounding moves the value by ~1e-7 relative (adjacent vertices then have
+// equal objectives up to rounding), far inside the callers' 1 - 2^-16 margin.
+__device__ __forceinline__ float hull_min_in(const float2* v, const float2* ed, int n, float y, float z, float slo,
+                                            float shi) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float2 e = ed[mid];
+        if (e.x * y > e.y * z) lo = mid + 1; else hi = mid;
+    }
+    const float s = v[lo].y;
+    if (s >= slo && s <= shi) {
+        float m = fmaf(v[lo].x, y, s * z);
+        if (lo > 0) m = fminf(m, fmaf(v[lo - 1].x, y, v[lo - 1].y * z));
+        if (lo + 1 < n) m = fminf(m, fmaf(v[lo + 1].x, y, v[lo + 1].y * z));
+        return m;
+    }
+    const float c = s < slo ? slo : shi;
+    if (c >= v[n - 1].y) return fmaf(v[n - 1].x, y, c * z);
+    if (c <= v[0].y) return fmaf(v[0].x, y, c * z);
+    int a = 0, b = n - 1;   // last vertex with S' <= c
+    while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (v[mid].y <= c) a = mid; else b = mid - 1;
+    }
+    const float2 p = v[a], q = v[a + 1];
+    const float B = fmaf(q.x - p.x, (c - p.y) / (q.y - p.y), p.x);
+    return fmaf(B, y, c * z);
+}
+
 // one thread per row: the bound above, times (1 - 2^-16) (covers its FP32 rounding, <= 16u, and
 // the hull search), or +inf when no candidate of the row meets every QoS bound (exact)
 template <int NW, bool QOS>
@@ -1011,6 +1045,8 @@ struct BBArgs {
     unsigned long long* rows_done;  // [3]: units processed, units with >= 1 swept entry, entries swept
     uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
     int32_t* plist_n;
+    const float2* hull;         // [n][2][2][Lmax] (k_prep_bound): the inner worker's hull at [2][0], edges [2][1]
+    const RowHdr* rowhdr;       // [n] hull sizes
 };
 // Best-first order: each item's units with a finite row bound are listed by
 // bucket of bound / (smallest bound of the problem) - 1 in steps of 1/BB_SCALE (counting sort,
@@ -1095,6 +1131,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         lbm = __uint_as_float(bb.lbmin[prob]);
         if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; s_stop = 0; }
     }
+    const float2* hv = nullptr;   // inner worker's lower-left hull (vertices {B, S'}, then edges), BB only
+    int nhv = 0;
+    if (BB) {
+        hv = bb.hull + ((size_t)prob * 2 + 1) * 2 * su.Lmax;
+        nhv = bb.rowhdr[prob].nh[1];
+    }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
     stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
@@ -1133,6 +1175,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     for (;;) {
         unsigned pend;
         uint32_t loff = 0;
+        float lbv = INFINITY;
         uint64_t base = 0;
         if (BB) {
             int b0 = 0;
@@ -1146,7 +1189,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             const uint2 en = e < lcnt ? lst[e] : make_uint2(0u, 0x7f800000u);
             loff = en.x;
             const float lb = __uint_as_float(en.y);
-            incv = __uint_as_float(*(volatile unsigned*)&s_inc);
+            lbv = lb;
+            unsigned ci = 0;   // one read, broadcast (warp-uniform bound)
+            if (wl == 0) ci = *(volatile unsigned*)&s_inc;
+            incv = __uint_as_float(__shfl_sync(0xffffffffu, ci, 0));
             if (incv != bnd_of) { bnd = band_bound(su, incv, 0.0f); bnd_of = incv; }
             pend = __ballot_sync(0xffffffffu, lb <= bnd);
             if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
@@ -1166,7 +1212,19 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         pend &= pend - 1;
         const uint32_t lo_j = __shfl_sync(0xffffffffu, loff, jl);
         const uint64_t unit = BB ? ua + (uint64_t)lo_j : base + (uint64_t)jl;
-        if (BB) ndone++;
+        if (BB) {   // re-check the unit against the incumbent found since the batch was fetched
+            const float lbj = __shfl_sync(0xffffffffu, lbv, jl);
+            unsigned ci = 0;   // one read, broadcast: every lane must take the same decision
+            if (wl == 0) ci = *(volatile unsigned*)&s_inc;
+            const float cur = __uint_as_float(__shfl_sync(0xffffffffu, ci, 0));
+            if (cur < incv) {
+                incv = cur;
+                bnd = band_bound(su, incv, 0.0f);
+                bnd_of = incv;
+            }
+            if (lbj > bnd) continue;
+            ndone++;
+        }
         int seg;
         HiSums h;
         h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
@@ -1264,11 +1322,14 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     // levels before klo: none qualifies unless u is non-monotone there (rare)
                     const bool pre = A.umaxp[min(klo, khi)] >= Tp;
                     use = khi > klo || pre;
-                    if (BB && use) {   // entry bound: every swept key >= X + Y minB + Z minS
+                    if (BB && use) {   // entry bound: every swept key >= X + Y minB + Z minS,
+                        // and >= X + min over the inner hull restricted to the entry's S' range
                         const int ka = pre ? 0 : klo;
-                        const float lbe = fmaf(ent.y, A.preminB[khi], fmaf(ent.z, (float)A.ssort[ka], ent.x)) *
-                                          0.99998474121f;   // 1 - 2^-16
-                        use = !(lbe > bnd);
+                        float lbe = fmaf(ent.y, A.preminB[khi], fmaf(ent.z, (float)A.ssort[ka], ent.x));
+                        if (!(lbe * 0.99998474121f > bnd))
+                            lbe = fmaxf(lbe, ent.x + hull_min_in(hv, hv + su.Lmax, nhv, ent.y, ent.z, (float)A.ssort[ka],
+                                                                 (float)A.ssort[khi - 1]));
+                        use = !(lbe * 0.99998474121f > bnd);   // 1 - 2^-16
                     }
                     if (pre) klo = -1 - klo;   // flag: sweep [0, |klo|) with a mask first
                 }
@@ -1304,10 +1365,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     if (khi2 > ka) {
                         const float Sf = (float)Sa;
                         const float Xc = fmaf(Bm, Yh, fmaf(Sf, Zh, Xh));
-                        const float lbc = fmaf(fmaf(Sf, invf, Yh), A.preminB[khi2],
-                                               fmaf(fmaf(Bm, invf, Zh), (float)A.ssort[ka], Xc)) *
-                                          0.99998474121f;   // 1 - 2^-16
-                        keep = !(lbc > bnd);
+                        const float Yc = fmaf(Sf, invf, Yh), Zc = fmaf(Bm, invf, Zh);
+                        float lbc = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
+                        if (!(lbc * 0.99998474121f > bnd))
+                            lbc = fmaxf(lbc, Xc + hull_min_in(hv, hv + su.Lmax, nhv, Yc, Zc, (float)A.ssort[ka],
+                                                              (float)A.ssort[khi2 - 1]));
+                        keep = !(lbc * 0.99998474121f > bnd);   // 1 - 2^-16
                     }
                 }
                 const unsigned cm = __ballot_sync(0xffffffffu, keep);
@@ -1383,8 +1446,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (BB && m < incv) {
                 atomicMin(&s_inc, __float_as_uint(m));
                 atomicMin(bb.inc + prob, __float_as_uint(m));
-                incv = m;
             }
+        }
+        if (BB && m < incv) {   // every lane (m and incv are warp-uniform): a tighter band at once
+            incv = m;
+            bnd = band_bound(su, incv, 0.0f);
+            bnd_of = incv;
         }
         __syncwarp();   // the table is rewritten for the next unit
       }
@@ -1629,7 +1696,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
                                                        wk.ulist, wk.ulist_n);
             if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
                 return e;
-            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n};
+            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.hull, wk.rowhdr};
             if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
             f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
             if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
@@ -1643,7 +1710,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
         k_bucket<<<(unsigned)grid, 256, 0, st>>>(su, wk.probs, wk.rowlb, wk.lbmin, wk.ulist, wk.ulist_n);
-        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n};
+        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.hull, wk.rowhdr};
         if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
         if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
