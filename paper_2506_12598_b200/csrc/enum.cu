@@ -1938,7 +1938,8 @@ template <int PASS>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
                                                const float* m32_sure, U256* hstar, U256* first,
-                                               const int32_t* bandn, const uint64_t* bandlist) {
+                                               const int32_t* bandn, const uint64_t* bandlist,
+                                               const float2* hull, const RowHdr* rowhdr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ U256 red[P2_THREADS];
@@ -2077,9 +2078,14 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
                     const float Be = __ll2float_rn(r.B), Sf = (float)r.S;
                     float X = fmaf(Be, Yh, fmaf(Sf, Zh, Xh));
                     if (su.mode == M_PAPER) X += (float)((double)r.BS * invd);
-                    const float lbe = fmaf(fmaf(Sf, invf, Yh), A.preminB[khi], fmaf(fmaf(Be, invf, Zh), (float)A.ssort[ka], X)) *
-                                      0.99998474121f;   // 1 - 2^-16
-                    keep = !(lbe > bound);
+                    const float Ye = fmaf(Sf, invf, Yh), Ze = fmaf(Be, invf, Zh);
+                    float lbe = fmaf(Ye, A.preminB[khi], fmaf(Ze, (float)A.ssort[ka], X));
+                    if (hull && !(lbe * 0.99998474121f > bound)) {   // the inner hull restricted to the S' range
+                        const float2* hv = hull + ((size_t)prob * 2 + 1) * 2 * su.Lmax;
+                        lbe = fmaxf(lbe, X + hull_min_in(hv, hv + su.Lmax, rowhdr[prob].nh[1], Ye, Ze, (float)A.ssort[ka],
+                                                         (float)A.ssort[khi - 1]));
+                    }
+                    keep = !(lbe * 0.99998474121f > bound);   // 1 - 2^-16
                 }
                 if (keep) s_elist[atomicAdd(&s_ne, 1)] = (int16_t)e;
             }
@@ -2196,7 +2202,7 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<0><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2205,7 +2211,7 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<2><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2214,7 +2220,7 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<1><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
     return cudaGetLastError();
 }
 
