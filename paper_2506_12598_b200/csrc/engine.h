@@ -152,6 +152,10 @@ struct Work {
     uint64_t* bandlist;         // [n * BAND_CAP] band units in index order (k_reduce_min)
     uint32_t* plist;            // [n * PL_CAP] units pass 1 processed with a finite minimum (pruned pass 1)
     int32_t* plist_n;           // [n] their count (> PL_CAP: overflow, reduce_min scans every unit)
+    uint16_t* thull;            // [tables * Lmax] hull vertex levels of every level table (k_table_hull)
+    int32_t* thull_n;           // [tables]
+    const int32_t* table_of;    // [n * W] table of each (problem, worker) (PrepIn.table_of)
+    Tables tb;                  // the level tables
     cudaEvent_t kev[2];         // recorded on the launching stream around the dominant pass-1 kernel (or null)
 };
 

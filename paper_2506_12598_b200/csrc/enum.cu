@@ -513,13 +513,72 @@ __device__ __forceinline__ bool hull_pop(const Lev& a, const Lev& b, const Lev& 
 //    With F(t) = min { S'_e + S'_k : min(u_e - S'_k, u_k - S'_e) >= t } (non-decreasing in t), a
 //    row has a feasible candidate iff F(hT) <= hTm - hT.  F is tabulated for hT in [t0, t1]
 //    (sums of the hi workers' min / max S'), when that range fits FT_CAP entries.
+// Lower-left hull of every level table in (S, B*) (one CTA per table).  A problem's step / inner worker
+// uses its table's levels with S' = S Lambda / K: a positive scaling of S keeps every orientation test,
+// so the vertex set (level indices, in S order) is the table's and is computed once per table instead
+// of once per problem.  Exact O(L^2) interval test, one point per thread: point p is a vertex iff no
+// point before it (smaller S) has B <= B_p and max over later points with smaller B of
+// (B_p - B_j)/(S_j - S_p)  <  min over earlier points of (B_j - B_p)/(S_p - S_j) (cross products of
+// B < 2^36 and S < 2^24 differences fit in int64); collinear middle points are dropped.
+__global__ void __launch_bounds__(256) k_table_hull(Tables tb, int Lmax, uint16_t* thull, int32_t* thull_n) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    long long* sB = reinterpret_cast<long long*>(smem_raw);    // [Lmax] B in S order
+    int* sS = reinterpret_cast<int*>(sB + Lmax);               // [Lmax] S in S order
+    uint16_t* ord = reinterpret_cast<uint16_t*>(sS + Lmax);    // [Lmax] level index in S order
+    uint8_t* vf = reinterpret_cast<uint8_t*>(ord + Lmax);      // [Lmax] vertex flags
+    const int t = blockIdx.x, L = tb.L[t];
+    const int64_t* S = tb.S[t];
+    const int64_t* B = tb.B[t];
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {   // levels have distinct S: rank = #{smaller S}
+        const int64_t sl = S[l];
+        int rk = 0;
+        for (int j = 0; j < L; j++) rk += S[j] < sl;
+        ord[rk] = (uint16_t)l;
+        sS[rk] = (int)sl;
+        sB[rk] = (long long)B[l];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < L; p += blockDim.x) {
+        const int pS = sS[p];
+        const long long pB = sB[p];
+        bool vert = true;
+        int64_t lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 0;   // lo = 0, hi = +inf
+        for (int r = 0; r < p; r++) {
+            const long long qB = sB[r];
+            if (qB <= pB) { vert = false; break; }
+            const int64_t n = qB - pB, d = (int64_t)(pS - sS[r]);
+            if (hi_d == 0 || n * hi_d < hi_n * d) { hi_n = n; hi_d = d; }
+        }
+        for (int r = p + 1; r < L && vert; r++) {
+            const long long qB = sB[r];
+            if (qB < pB) {
+                const int64_t n = pB - qB, d = (int64_t)(sS[r] - pS);
+                if (n * lo_d > lo_n * d) { lo_n = n; lo_d = d; }
+            }
+        }
+        if (vert && hi_d != 0) vert = lo_n * hi_d < hi_n * lo_d;
+        vf[p] = vert ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int n = 0;
+        for (int b0 = 0; b0 < L; b0 += 32) {
+            const int p = b0 + (int)threadIdx.x;
+            const bool f = p < L && vf[p];
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (f) thull[(size_t)t * Lmax + n + __popc(bal & ((1u << threadIdx.x) - 1u))] = ord[p];
+            n += __popc(bal);
+        }
+        if (threadIdx.x == 0) thull_n[t] = n;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs, const Lev* levs, float2* hull,
-                                                    int32_t* ftab, RowHdr* hdr) {
+                                                    int32_t* ftab, RowHdr* hdr, const int32_t* table_of,
+                                                    const uint16_t* thull, const int32_t* thull_n) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int* G = reinterpret_cast<int*>(smem_raw);                          // [FT_CAP]
     Lev* sv = reinterpret_cast<Lev*>(G + FT_CAP);                      // [2][Lmax] step, inner records
-    uint16_t* ord = reinterpret_cast<uint16_t*>(sv + 2 * su.Lmax);     // [2][Lmax]
-    uint16_t* stk = ord + 2 * su.Lmax;                                 // [2][Lmax]
     __shared__ int s_t0, s_t1, s_part[256];
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
@@ -543,118 +602,39 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
             if (threadIdx.x == 0) { s_t0 += mn; s_t1 += mx; }
         }
     }
-    // order of both workers by (S', B, index) (threads [0,128): step, [128,256): inner).  A worker's
-    // levels have distinct S', so with whole-row units it is the aux block's S' order; else rank sort.
-    uint8_t* vflag = reinterpret_cast<uint8_t*>(stk + 2 * Lmax);      // [2][Lmax] hull-vertex flags (S' order)
-    int* SS = reinterpret_cast<int*>(vflag + ((2 * Lmax + 15) & ~15));  // [2][Lmax] S' in that order
-    long long* BB = reinterpret_cast<long long*>(SS + 2 * Lmax);       // [2][Lmax] B in that order
-    const int which_t = threadIdx.x >> 7, tw = threadIdx.x & 127;
-    {
-        const Lev* lv = sv + (size_t)which_t * Lmax;
-        const int L = P.L[W - 2 + which_t];
-        if (su.aux_bytes > 0 && su.nseg == 1) {
-            const AuxView A = aux_view(reinterpret_cast<unsigned char*>(const_cast<Lev*>(gbase) + (size_t)W * Lmax), Lmax);
-            const uint16_t* po = which_t == 0 ? A.sperm : A.perm;
-            for (int i = tw; i < L; i += 128) ord[which_t * Lmax + i] = po[i];
-        } else {
-            for (int i = tw; i < L; i += 128) {
-                const Lev& a = lv[i];
-                int rk = 0;
-                for (int j = 0; j < L; j++) {
-                    const Lev& b = lv[j];
-                    rk += (b.S < a.S) || (b.S == a.S && (b.B < a.B || (b.B == a.B && j < i)));
-                }
-                ord[which_t * Lmax + rk] = (uint16_t)i;
-            }
-        }
-    }
-    __syncthreads();
-    {
-        const Lev* lv = sv + (size_t)which_t * Lmax;
-        const int L = P.L[W - 2 + which_t];
-        for (int t = tw; t < L; t += 128) {
-            const Lev& p = lv[ord[which_t * Lmax + t]];
-            SS[which_t * Lmax + t] = p.S;
-            BB[which_t * Lmax + t] = p.B;
-        }
-    }
-    __syncthreads();
-    // lower-left hull, one point per thread: point p (position t in that order) is a vertex iff no point
-    // before it has B <= B_p (Pareto) and the weights lambda = z / y for which p minimises B y + S' z form
-    // a non-empty open interval: max over later points with smaller B of (B_p - B_j)/(S'_j - S'_p)  <
-    // min over earlier points of (B_j - B_p)/(S'_p - S'_j)  (exact: numerators < 2^36, denominators
-    // < 2^24, so the cross products fit in int64).  Collinear middle points are dropped, as the
-    // sequential monotone chain does.
-    {
-        const Lev* lv = sv + (size_t)which_t * Lmax;
-        const uint16_t* o = ord + which_t * Lmax;
-        const int L = P.L[W - 2 + which_t];
-        const int* sS = SS + which_t * Lmax;
-        const long long* sB = BB + which_t * Lmax;
-        for (int t = tw; t < L; t += 128) {
-            const int pS = sS[t];
-            const long long pB = sB[t];
-            bool vert = true;
-            int64_t lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 0;   // lo = 0, hi = +inf
-            for (int r = 0; r < t; r++) {                      // earlier points (S'_q <= S'_p)
-                const long long qB = sB[r];
-                if (qB <= pB) { vert = false; break; }           // dominated
-                const int64_t n = qB - pB, d = (int64_t)(pS - sS[r]);
-                if (hi_d == 0 || n * hi_d < hi_n * d) { hi_n = n; hi_d = d; }
-            }
-            for (int r = t + 1; r < L && vert; r++) {          // later points
-                const long long qB = sB[r];
-                const int qS = sS[r];
-                if (qS > pS && qB < pB) {
-                    const int64_t n = pB - qB, d = (int64_t)(qS - pS);
-                    if (n * lo_d > lo_n * d) { lo_n = n; lo_d = d; }
-                }
-            }
-            if (vert && hi_d != 0) vert = lo_n * hi_d < hi_n * lo_d;
-            vflag[which_t * Lmax + t] = vert ? 1 : 0;
-        }
-    }
     __syncthreads();
     const int t0 = s_t0, tn = (s_t1 - s_t0 + 1 <= FT_CAP && su.has_qos) ? s_t1 - s_t0 + 1 : 0;
-    if (threadIdx.x < 64) {   // warp w compacts worker w's vertices in S' order and writes hull + edges
+    if (threadIdx.x < 64) {   // warp w: worker w's hull (the vertices of its level table, k_table_hull) + edges
         const int which = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const Lev* lv = sv + (size_t)which * Lmax;
         const int L = P.L[W - 2 + which];
-        const uint16_t* o = ord + which * Lmax;
-        uint16_t* sk = stk + which * Lmax;
-        int n = 0, umax = -(1 << 30);
+        const int tab = table_of[(size_t)prob * W + W - 2 + which];
+        const uint16_t* hx = thull + (size_t)tab * Lmax;
+        const int n = thull_n[tab];
+        int umax = -(1 << 30), smin = INT_MAX;
         long long bmin = LLONG_MAX;
-        for (int b0 = 0; b0 < L; b0 += 32) {
-            const int t = b0 + lane;
-            bool f = false;
-            if (t < L) {
-                const Lev& p = lv[o[t]];
-                umax = max(umax, p.Tmax - p.S);
-                bmin = min(bmin, (long long)p.B);
-                f = vflag[which * Lmax + t] != 0;
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (f) sk[n + __popc(bal & ((1u << lane) - 1u))] = o[t];
-            n += __popc(bal);
+        for (int l = lane; l < L; l += 32) {
+            umax = max(umax, lv[l].Tmax - lv[l].S);
+            bmin = min(bmin, (long long)lv[l].B);
+            smin = min(smin, lv[l].S);
         }
         for (int off = 16; off; off >>= 1) {
             umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, off));
             bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, off));
+            smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, off));
         }
-        __syncwarp();
         float2* h = hull + ((size_t)prob * 2 + which) * 2 * Lmax;
         for (int i = lane; i < n; i += 32) {
-            const Lev& v = lv[sk[i]];
+            const Lev& v = lv[hx[i]];
             h[i] = make_float2(__ll2float_rn(v.B), (float)v.S);
             if (i + 1 < n) {
-                const Lev& x = lv[sk[i + 1]];
+                const Lev& x = lv[hx[i + 1]];
                 h[Lmax + i] = make_float2(__ll2float_rn(v.B - x.B), (float)(x.S - v.S));
             }
         }
         if (lane == 0) {
             RowHdr* H = hdr + prob;
             H->nh[which] = n;
-            const int smin = lv[o[0]].S;
             if (which == 0) { H->smin_st = smin; H->umax_st = umax; H->t0 = t0; H->tn = tn; }
             else { H->smin_in = smin; H->umax_in = umax; H->Sminf_in = (float)smin; H->Bminf_in = __ll2float_rn(bmin); }
         }
@@ -1674,10 +1654,15 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(wk.plist_n, 0, n * sizeof(int32_t), st)) != cudaSuccess) return e;
-        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * (8 + 2 + 2 * sizeof(Lev) + 24) + 16;
+        const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * 2 * sizeof(Lev);
+        const size_t hsm = (size_t)su.Lmax * (8 + 4 + 2 + 1) + 16;
+        if ((e = cudaFuncSetAttribute((const void*)k_table_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm)) != cudaSuccess)
+            return e;
+        k_table_hull<<<wk.tb.n, 256, hsm, st>>>(wk.tb, su.Lmax, wk.thull, wk.thull_n);
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
-        k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr);
+        k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.table_of,
+                                                       wk.thull, wk.thull_n);
         const size_t fsm = (size_t)su.Lmax * (4 * sizeof(float2) + (size_t)(su.W - 2) * sizeof(Lev)) + (size_t)su.rows_max * 4;
         if (rowlb_fused_ok(su) && fsm <= 160 * 1024) {
             RowLBF rf = nullptr;
