@@ -280,7 +280,13 @@ def main():
                          "fma_lane_ops_per_evaluated_candidate": fma_ops_per_cand,
                          "evaluated_candidates_per_launch": k_eval,
                          "evaluated_fraction": k_eval / cand_step,
-                         "candidates_per_s_kernel": cand_per_s_kernel},
+                         "candidates_per_s_kernel": cand_per_s_kernel,
+                         "exhaustive_equivalent_frac": fma_ops_per_cand * cand_step / k_s / 1e9 / peak,
+                         "note": "achieved counts only the candidates the kernel evaluated in FP32; the others are "
+                                 "classified by exact range cuts and lower bounds (DESIGN.md 3.9), so the kernel is "
+                                 "issue-bound on classification (issue_slots_busy_pct_ncu); exhaustive_equivalent_frac "
+                                 "= 2 FMA x every candidate of the step / kernel time / peak (> 1: faster than an "
+                                 "exhaustive scorer at the FMA-pipe roofline)"},
             "pruning": {"units_total_per_launch": units_total, "units_processed_per_launch": k_units,
                         "units_with_swept_entries_per_launch": p1_extra["units_with_swept_entries"],
                         "entries_swept_per_launch": p1_extra["entries_swept"],
