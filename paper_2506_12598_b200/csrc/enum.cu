@@ -853,7 +853,8 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
     for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
-    auto row_lb = [&](int64_t hB, int64_t hBS, int hT, int hTm) -> float {
+    // Dhf: (float) sum over the hi workers of B_w (hT - S'_w) >= 0 (computed by the caller)
+    auto row_lb = [&](int64_t hB, float Dhf, int hT, int hTm) -> float {
         bool feas = true;
         if (QOS) {
             if (H.tn > 0) feas = ft[hT - H.t0] <= hTm - hT;
@@ -862,8 +863,6 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         if (!feas) return INFINITY;
         const float hBf = __ll2float_rn(hB), hTf = (float)hT;
         const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
-        const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
-        const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
         const float Xh = fmaf(Dhf, invf, hBf);
         const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
         return (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
@@ -877,7 +876,10 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
             const Lev r1 = hrec[(NH - 1) * Lmax + d1];
             for (int d0 = threadIdx.x >> 7; d0 < L0; d0 += RLF_THREADS / 128) {
                 const Lev& r0 = hrec[d0];
-                const float lb = row_lb(r0.B + r1.B, r0.BS + r1.BS, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
+                // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding <= 3u,
+                // inside the bound's 1 - 2^-16 margin)
+                const float Dhf = fmaf(__ll2float_rn(r0.B), (float)r1.S, __ll2float_rn(r1.B) * (float)r0.S);
+                const float lb = row_lb(r0.B + r1.B, Dhf, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
                 lbs[d0 * L1 + d1] = lb;
                 bm = fminf(bm, lb);
             }
@@ -894,7 +896,9 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
                 const Lev& v = hrec[w * Lmax + d];
                 hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
             }
-            const float lb = row_lb(hB, hBS, hT, hTm);
+            const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
+            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            const float lb = row_lb(hB, Dhf, hT, hTm);
             lbs[r] = lb;
             bm = fminf(bm, lb);
         }
