@@ -1153,6 +1153,9 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // consecutive units per round, rounds strided by NWARP * 32.
     unsigned long long nfeas = 0, ndone = 0, nue = 0, nent = 0;
     float bnd = INFINITY, incv = INFINITY, bnd_of = -1.0f;
+    // band factor of the linear modes, rounded up once: bnd = m x bandf (rounded up) >= band_bound(m)
+    const float bandf = __double2float_ru((1.0 + (double)su.tol_num / (double)su.tol_den) * (1.0 + su.delta) /
+                                          (1.0 - su.delta) * (1.0 + 1e-12));
     constexpr uint64_t RSTEP = (uint64_t)NWARP * 32;
     uint64_t rbase = ua + (uint64_t)warp * 32;
     int nfetch = 0;
@@ -1177,7 +1180,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             unsigned ci = 0;   // one read, broadcast (warp-uniform bound)
             if (wl == 0) ci = *(volatile unsigned*)&s_inc;
             incv = __uint_as_float(__shfl_sync(0xffffffffu, ci, 0));
-            if (incv != bnd_of) { bnd = band_bound(su, incv, 0.0f); bnd_of = incv; }
+            if (incv != bnd_of) { bnd = __fmul_ru(incv, bandf); bnd_of = incv; }
             pend = __ballot_sync(0xffffffffu, lb <= bnd);
             if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
                 float mn = lb;
@@ -1203,7 +1206,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             const float cur = __uint_as_float(__shfl_sync(0xffffffffu, ci, 0));
             if (cur < incv) {
                 incv = cur;
-                bnd = band_bound(su, incv, 0.0f);
+                bnd = __fmul_ru(incv, bandf);
                 bnd_of = incv;
             }
             if (lbj > bnd) continue;
@@ -1420,6 +1423,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             }
         }
         float m = fminf(m0, m1);
+        if (BB && !__any_sync(0xffffffffu, m < INFINITY)) {   // nothing feasible swept: submin stays +inf
+            __syncwarp();
+            continue;
+        }
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (wl == 0) {
             subp[unit] = m;
@@ -1434,7 +1441,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         if (BB && m < incv) {   // every lane (m and incv are warp-uniform): a tighter band at once
             incv = m;
-            bnd = band_bound(su, incv, 0.0f);
+            bnd = __fmul_ru(incv, bandf);
             bnd_of = incv;
         }
         __syncwarp();   // the table is rewritten for the next unit
