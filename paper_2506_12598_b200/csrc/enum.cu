@@ -1928,7 +1928,10 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
 // key is within tol of the (global) H*.  PASS 2 (unsharded runs): both in one rescan -- the band's
 // exactly evaluated candidates are kept in shared memory (a second rescan only on overflow).
 constexpr int P2_CAP = 256;
-constexpr int P2_THREADS = 512;
+#ifndef P2_THREADS_N
+#define P2_THREADS_N 128
+#endif
+constexpr int P2_THREADS = P2_THREADS_N;
 constexpr int P2_ELIST = 1024;   // step levels per unit the pass-2 entry filter handles
 template <int PASS>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,

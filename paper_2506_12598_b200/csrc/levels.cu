@@ -21,6 +21,8 @@
 // in the top byte) so ranking compares words.  One cooperative launch covers every table.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+
 #include "engine.h"
 
 namespace cg = cooperative_groups;
@@ -163,6 +165,17 @@ __device__ __forceinline__ void compact_table(const LevelJob& J) {
     __syncthreads();
 }
 
+#ifdef K1_DEBUG
+__device__ unsigned long long k1_dbg[80];
+#define K1_STAMP(i)                                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                                      \
+        unsigned long long t_;                                                                      \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+        k1_dbg[i] = t_;                                                                             \
+    }
+#else
+#define K1_STAMP(i)
+#endif
 __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax,
                                                 size_t wsm_words) {
     cg::grid_group grid = cg::this_grid();
@@ -173,8 +186,10 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
 
+    K1_STAMP(0)
     // ---- DP layers G-1 .. 0 (one cell = (table, r, s); all C sizes per cell) ----
     for (int step = 0; step < gmax; step++) {
+        K1_STAMP(1 + step)
         if (threadIdx.x == 0) {
             off[0] = 0;
             for (int t = 0; t < n_jobs; t++)
@@ -192,9 +207,11 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         grid.sync();
     }
 
+    K1_STAMP(70)
     // ---- per table (one CTA each): B*(s) = best over j of layer 0 at r = R; compact ----
     for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) compact_table(sj[t]);
     grid.sync();
+    K1_STAMP(71)
 
     // flattened (table, level) work for the remaining phases
     if (threadIdx.x == 0) {
@@ -213,6 +230,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         reconstruct(J, l);
     }
     grid.sync();
+    K1_STAMP(72)
 
     // ---- rank = number of lexicographically smaller witnesses; scatter to rank order.  One CTA
     // per table with the table's witness words staged in shared memory (the comparisons are
@@ -250,6 +268,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             for (int l = threadIdx.x; l < L; l += blockDim.x) rank_level(J, l, L);
         }
     }
+    K1_STAMP(73)
 }
 
 cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, cudaStream_t st) {
@@ -275,7 +294,19 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
     if (per_sm > 2) per_sm = 2;
     int grid = nsm * (per_sm > 0 ? per_sm : 1);
     void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax, (void*)&wsm_words};
+#ifdef K1_DEBUG
+    e = cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, wsm * 8, st);
+    unsigned long long h[80];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, k1_dbg, sizeof h);
+    fprintf(stderr, "K1 grid %d gmax %d: layers", grid, gmax);
+    for (int i = 1; i <= gmax; i++) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " | last layer->compact %.1f compact %.1f reconstruct %.1f rank %.1f us\n", (h[70] - h[gmax]) * 1e-3,
+            (h[71] - h[70]) * 1e-3, (h[72] - h[71]) * 1e-3, (h[73] - h[72]) * 1e-3);
+    return e;
+#else
     return cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, wsm * 8, st);
+#endif
 }
 
 }  // namespace eclip
