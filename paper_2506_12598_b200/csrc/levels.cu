@@ -38,6 +38,7 @@ __device__ __forceinline__ int vidx(const LevelJob& J, int g, int j, int r, int 
 __device__ __forceinline__ int nwords(const LevelJob& J) { return (J.G + 7) / 8; }
 
 // one (r, s) cell of layer g = G-1-step: V for all sizes j, and best / second best / arg over j
+template <int CM>   // CM >= J.C: the loops over sizes are unrolled, so their loads are issued together
 __device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
     const int S1 = J.smax + 1, ncell = (J.R + 1) * S1;
     const int r = k / S1, s = k - r * S1;
@@ -46,21 +47,23 @@ __device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
     int64_t b1 = INF64, b2 = INF64;
     int a1 = -1;
     // all loads of the cell first (independent across j, so they overlap), then the stores
-    int64_t outv[32];
-#pragma unroll 8
-    for (int j = 0; j < J.C; j++) {
+    int64_t outv[CM];
+#pragma unroll
+    for (int j = 0; j < CM; j++) {
         int64_t out = INF64;
-        if ((J.mask >> j) & 1u) {
+        if (j < J.C && ((J.mask >> j) & 1u)) {
             const int nd = J.need[g * J.C + j];
             const int64_t b = J.beta[g * J.C + j];
             if (g == J.G - 1) {
                 if (s == nd) out = b;
             } else if (nd <= s) {
                 const int sp = s - nd;
-                int64_t v = J.V[vidx(J, g + 1, j, r, sp)];
-                if (r >= 1) {
+                int64_t v = __ldcg(J.V + vidx(J, g + 1, j, r, sp));   // written by other CTAs last layer: L2
+                if (r >= 1) {   // arg, best and second best loaded together (no dependent load)
                     const int bi = nxt * ncell + (r - 1) * S1 + sp;
-                    const int64_t w = (J.barg[bi] != j) ? J.best[2 * bi] : J.best[2 * bi + 1];
+                    const int ab = __ldcg(J.barg + bi);
+                    const longlong2 bb2 = __ldcg(reinterpret_cast<const longlong2*>(J.best) + bi);
+                    const int64_t w = ab != j ? bb2.x : bb2.y;
                     if (w < v) v = w;
                 }
                 if (v != INF64) out = b + v;
@@ -68,7 +71,9 @@ __device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
         }
         outv[j] = out;
     }
-    for (int j = 0; j < J.C; j++) {
+#pragma unroll
+    for (int j = 0; j < CM; j++) {
+        if (j >= J.C) break;
         const int64_t out = outv[j];
         J.V[vidx(J, g, j, r, s)] = out;
         if (out < b1) { b2 = b1; b1 = out; a1 = j; }
@@ -81,6 +86,7 @@ __device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
 }
 
 // greedy reconstruction of level l's canonical witness (packed words)
+template <int CM>
 __device__ __forceinline__ void reconstruct(const LevelJob& J, int l) {
     int rem = J.sidx[l];
     int64_t opt = J.bstar[rem];
@@ -90,19 +96,20 @@ __device__ __forceinline__ void reconstruct(const LevelJob& J, int l) {
     for (int g = 0; g < J.G; g++) {
         int pick = -1;
         // the candidates' values are loaded together (independent), then the first match is taken
-        int64_t cv[32];
-#pragma unroll 8
-        for (int j = 0; j < J.C; j++) {
+        int64_t cv[CM];
+#pragma unroll
+        for (int j = 0; j < CM; j++) {
             cv[j] = INF64;
-            if (!((J.mask >> j) & 1u)) continue;
+            if (j >= J.C || !((J.mask >> j) & 1u)) continue;
             const int nd = J.need[g * J.C + j];
             if (nd > rem) continue;
             const int rr = (g == 0 || j == prev) ? r : r - 1;
             if (rr < 0) continue;
             cv[j] = J.V[vidx(J, g, j, rr, rem)];
         }
-        for (int j = 0; j < J.C && pick < 0; j++)
-            if (cv[j] == opt) pick = j;
+#pragma unroll
+        for (int j = CM - 1; j >= 0; j--)   // the smallest matching j
+            if (j < J.C && cv[j] == opt) pick = j;
         if (pick < 0) pick = 0;   // unreachable: opt is attained
         if (g > 0 && pick != prev) r--;
         opt -= J.beta[g * J.C + pick];
@@ -176,6 +183,7 @@ __device__ unsigned long long k1_dbg[80];
 #else
 #define K1_STAMP(i)
 #endif
+template <int CM>
 __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax,
                                                 size_t wsm_words) {
     cg::grid_group grid = cg::this_grid();
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             while (off[t + 1] <= i) t++;
             const LevelJob& J = sj[t];
             const int k = i - off[t];
-            dp_cell(J, step, k);
+            dp_cell<CM>(J, step, k);
         }
         grid.sync();
     }
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         while (off[t + 1] <= i) t++;
         const LevelJob& J = sj[t];
         const int l = i - off[t];
-        reconstruct(J, l);
+        reconstruct<CM>(J, l);
     }
     grid.sync();
     K1_STAMP(72)
@@ -287,15 +295,18 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
     }
     if (wsm > 2048) wsm = 0;   // large tables (many levels, e.g. BASELINE C4) rank from global memory (measured faster)
     size_t wsm_words = wsm;
-    e = cudaFuncSetAttribute((const void*)k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsm * 8));
+    int cmax = 0;
+    for (int i = 0; i < n_jobs; i++) cmax = h_jobs[i].C > cmax ? h_jobs[i].C : cmax;
+    const void* kf = cmax <= 8 ? (const void*)k_levels<8> : cmax <= 16 ? (const void*)k_levels<16> : (const void*)k_levels<32>;
+    e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsm * 8));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, 256, wsm * 8);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, wsm * 8);
     if (e != cudaSuccess) return e;
     if (per_sm > 2) per_sm = 2;
     int grid = nsm * (per_sm > 0 ? per_sm : 1);
     void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax, (void*)&wsm_words};
 #ifdef K1_DEBUG
-    e = cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, wsm * 8, st);
+    e = cudaLaunchCooperativeKernel(kf, dim3(grid), dim3(256), args, wsm * 8, st);
     unsigned long long h[80];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(h, k1_dbg, sizeof h);
@@ -305,7 +316,7 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
             (h[71] - h[70]) * 1e-3, (h[72] - h[71]) * 1e-3, (h[73] - h[72]) * 1e-3);
     return e;
 #else
-    return cudaLaunchCooperativeKernel((void*)k_levels, dim3(grid), dim3(256), args, wsm * 8, st);
+    return cudaLaunchCooperativeKernel(kf, dim3(grid), dim3(256), args, wsm * 8, st);
 #endif
 }
 
