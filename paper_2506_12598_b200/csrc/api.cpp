@@ -635,7 +635,13 @@ static int alloc_work(eclip_session* s) {
     const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
     const size_t o_sure = (en && su.mode == M_MATRIX && su.has_qos) ? bp.take<float>(ns) : 0;
     const size_t o_m32 = bp.take<float>(n), o_m32s = bp.take<float>(n), o_hs = bp.take<U256>(n), o_first = bp.take<U256>(n);
-    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0, o_pl = 0, o_pln = 0, o_th = 0, o_thn = 0;
+    size_t o_th = 0, o_thn = 0, o_tord = 0;
+    if (en && su.aux_bytes > 0) {   // per-table S order and hulls (k_table_hull)
+        o_th = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
+        o_thn = bp.take<int32_t>((size_t)s->tb.n);
+        o_tord = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
+    }
+    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0, o_pl = 0, o_pln = 0;
     if (bb) {
         o_rowlb = bp.take<float>(n * (size_t)su.rows_max);
         o_lbmin = bp.take<unsigned>(n);
@@ -645,8 +651,7 @@ static int alloc_work(eclip_session* s) {
         o_ulist = bp.take<uint2>(grid * (size_t)su.upi);
         o_uln = bp.take<int32_t>(grid);
         o_rh = bp.take<RowHdr>(n);
-        o_th = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
-        o_thn = bp.take<int32_t>((size_t)s->tb.n);
+
         o_pl = bp.take<uint32_t>(n * (size_t)PL_CAP);
         o_pln = bp.take<int32_t>(n);
     }
@@ -656,6 +661,11 @@ static int alloc_work(eclip_session* s) {
     wk.rows_done = wk.feasible + 1;
     CU(cudaMemsetAsync(wk.feasible, 0, 4 * sizeof(unsigned long long), s->st));
     wk.probs = (Prob*)(base + o_probs);
+    if (o_th) {
+        wk.thull = (uint16_t*)(base + o_th);
+        wk.thull_n = (int32_t*)(base + o_thn);
+        wk.tord = (uint16_t*)(base + o_tord);
+    }
     wk.levs = (Lev*)(base + o_levs);
     if (en) {
         wk.submin = (float*)(base + o_sub);
@@ -676,8 +686,7 @@ static int alloc_work(eclip_session* s) {
         wk.ulist = (uint2*)(base + o_ulist);
         wk.ulist_n = (int32_t*)(base + o_uln);
         wk.rowhdr = (RowHdr*)(base + o_rh);
-        wk.thull = (uint16_t*)(base + o_th);
-        wk.thull_n = (int32_t*)(base + o_thn);
+
         wk.plist = (uint32_t*)(base + o_pl);
         wk.plist_n = (int32_t*)(base + o_pln);
     }

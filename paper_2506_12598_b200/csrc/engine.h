@@ -154,6 +154,7 @@ struct Work {
     int32_t* plist_n;           // [n] their count (> PL_CAP: overflow, reduce_min scans every unit)
     uint16_t* thull;            // [tables * Lmax] hull vertex levels of every level table (k_table_hull)
     int32_t* thull_n;           // [tables]
+    uint16_t* tord;             // [tables * Lmax] level indices of every level table in S order (k_table_hull)
     const int32_t* table_of;    // [n * W] table of each (problem, worker) (PrepIn.table_of)
     Tables tb;                  // the level tables
     cudaEvent_t kev[2];         // recorded on the launching stream around the dominant pass-1 kernel (or null)

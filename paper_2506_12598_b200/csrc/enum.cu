@@ -325,7 +325,8 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
 
 // one CTA per problem: sort, pair up, and tabulate the inner / step workers once
 template <int MODE>
-__global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, Lev* levs) {
+__global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, Lev* levs, const int32_t* table_of,
+                                                  const uint16_t* tord) {
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
     if (P.status != 0) return;
@@ -348,13 +349,25 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
     AuxView A = aux_view(aux_s, Lmax);
     const int Lin = P.L[W - 1], Lst = P.Lstep, segl = P.seglen;
     const double invd = 1.0 / (double)P.lamN;
+    // S' order of the inner and step workers: the level tables' S order (k_table_hull; a positive scaling)
+    // with whole-row units, else rank sorts (per segment for the step worker)
+    const bool tab_order = su.nseg == 1;
+    if (tab_order) {
+        const uint16_t* oi = tord + (size_t)table_of[(size_t)prob * W + W - 1] * Lmax;
+        for (int i = threadIdx.x; i < Lin; i += blockDim.x) A.perm[i] = oi[i];
+        if (W >= 2) {
+            const uint16_t* os = tord + (size_t)table_of[(size_t)prob * W + W - 2] * Lmax;
+            for (int i = threadIdx.x; i < Lst; i += blockDim.x) A.sperm[i] = os[i];
+        }
+    } else {
     for (int i = threadIdx.x; i < Lin; i += blockDim.x) {
         const int si = inner[i].S;
         int rk = 0;
         for (int j = 0; j < Lin; j++) rk += inner[j].S < si;
         A.perm[rk] = (uint16_t)i;
     }
-    if (W >= 2) {
+    }
+    if (W >= 2 && !tab_order) {
         for (int i = threadIdx.x; i < Lst; i += blockDim.x) {
             const int b0 = (i / segl) * segl, b1 = min(b0 + segl, Lst);
             const int si = stepw[i].S;
@@ -520,7 +533,8 @@ __device__ __forceinline__ bool hull_pop(const Lev& a, const Lev& b, const Lev& 
 // point before it (smaller S) has B <= B_p and max over later points with smaller B of
 // (B_p - B_j)/(S_j - S_p)  <  min over earlier points of (B_j - B_p)/(S_p - S_j) (cross products of
 // B < 2^36 and S < 2^24 differences fit in int64); collinear middle points are dropped.
-__global__ void __launch_bounds__(256) k_table_hull(Tables tb, int Lmax, uint16_t* thull, int32_t* thull_n) {
+__global__ void __launch_bounds__(256) k_table_hull(Tables tb, int Lmax, uint16_t* thull, int32_t* thull_n,
+                                                    uint16_t* tord) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     long long* sB = reinterpret_cast<long long*>(smem_raw);    // [Lmax] B in S order
     int* sS = reinterpret_cast<int*>(sB + Lmax);               // [Lmax] S in S order
@@ -534,6 +548,7 @@ __global__ void __launch_bounds__(256) k_table_hull(Tables tb, int Lmax, uint16_
         int rk = 0;
         for (int j = 0; j < L; j++) rk += S[j] < sl;
         ord[rk] = (uint16_t)l;
+        tord[(size_t)t * Lmax + rk] = (uint16_t)l;   // the table's S order (= every problem's S' order)
         sS[rk] = (int)sl;
         sB[rk] = (long long)B[l];
     }
@@ -1666,10 +1681,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(wk.plist_n, 0, n * sizeof(int32_t), st)) != cudaSuccess) return e;
         const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * 2 * sizeof(Lev);
-        const size_t hsm = (size_t)su.Lmax * (8 + 4 + 2 + 1) + 16;
-        if ((e = cudaFuncSetAttribute((const void*)k_table_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm)) != cudaSuccess)
-            return e;
-        k_table_hull<<<wk.tb.n, 256, hsm, st>>>(wk.tb, su.Lmax, wk.thull, wk.thull_n);
+
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
         k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.table_of,
@@ -2351,11 +2363,16 @@ cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Wor
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
     if (su.aux_bytes > 0) {
+        // per level table: S order and lower-left hull vertices (shared by every problem using the table)
+        const size_t hsm = (size_t)su.Lmax * (8 + 4 + 2 + 1) + 16;
+        cudaError_t e = cudaFuncSetAttribute((const void*)k_table_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+        if (e != cudaSuccess) return e;
+        k_table_hull<<<tb.n, 256, hsm, st>>>(tb, su.Lmax, wk.thull, wk.thull_n, wk.tord);
         const size_t sm = (size_t)2 * su.Lmax * sizeof(Lev) + (size_t)su.aux_bytes;
         auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;
-        cudaError_t e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
-        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs);
+        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs, in.table_of, wk.tord);
     }
     return cudaGetLastError();
 }
