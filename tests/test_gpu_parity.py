@@ -353,6 +353,19 @@ def test_pruned_equals_exhaustive_batch(mode, qf):
     assert 0 < done < rows
 
 
+@pytest.mark.parametrize("W,qf,seed", [(3, 0.8, 51), (4, 0.7, 52), (4, 1.3, 53), (5, 1.0, 54), (4, 2.5, 55)])
+def test_pruned_equals_exhaustive_stress(W, qf, seed):
+    """the row / chunk / entry bounds (hull-restricted) and the incumbent re-check are exact across
+    worker counts and QoS tightness (partially feasible rows, non-monotone QoS ranges, empty ranges)"""
+    models, ids, qos = synth.make_c5(192, seed=seed, W=W)
+    pr = ec.Profiles.from_models(models)
+    kw = dict(total_sms=148, qos_ns=qos * qf, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+    a = ec.plan_batch(pr, ids, prune=True, **kw)
+    b = ec.plan_batch(pr, ids, prune=False, **kw)
+    for k in ("status", "winner_index", "winner_levels", "objective", "group_sm", "model_latency_ns"):
+        assert np.array_equal(a[k], b[k]), k
+
+
 def pr_levels(pr, m, _cache={}):
     key = (id(pr), m)
     if key not in _cache:
