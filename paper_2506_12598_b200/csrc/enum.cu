@@ -1230,15 +1230,23 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         int seg;
         HiSums h;
         h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
+        int64_t hb[2] = {0, 0};
+        int hs[2] = {0, 0};
+        bool two = false;   // two hi workers decoded by the 32-bit path: the cross term in FP32 below
         if (units <= 0xffffffffull) {   // 32-bit decode (the common case)
+            two = NH == 2;
             uint32_t row = (uint32_t)unit;
             if (nseg > 1) { seg = (int)(row % (uint32_t)nseg); row /= (uint32_t)nseg; } else seg = 0;
 #pragma unroll
             for (int w = NH - 1; w >= 0; w--) {
-                const uint32_t dw = row % (uint32_t)L[w];
-                row /= (uint32_t)L[w];
+                uint32_t dw = row;   // worker 0 is the most significant digit: row < L[0] there
+                if (w > 0) {
+                    dw = row % (uint32_t)L[w];
+                    row /= (uint32_t)L[w];
+                }
                 const Lev& r = sl[w * Lmax + dw];
                 h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
+                if (NH == 2) { hb[w] = r.B; hs[w] = r.S; }
             }
         } else {
             seg = (int)(unit % (uint64_t)nseg);
@@ -1282,8 +1290,13 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
         float Xh;
         if (MODE == M_EXCL) {
-            const u128 Dh = (u128)h.T * (u128)h.B - (u128)h.BS;   // = sum_hi B_w (hT - S'_w) >= 0
-            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            float Dhf;   // = sum_hi B_w (hT - S'_w) >= 0
+            if (NH == 2 && two) {   // B_0 S'_1 + B_1 S'_0: non-negative terms, <= 4u (inside delta)
+                Dhf = fmaf(__ll2float_rn(hb[0]), (float)hs[1], __ll2float_rn(hb[1]) * (float)hs[0]);
+            } else {
+                const u128 Dh = (u128)h.T * (u128)h.B - (u128)h.BS;
+                Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+            }
             Xh = fmaf(Dhf, invf, hBf);
         } else {
             Xh = hBf * Yh;
