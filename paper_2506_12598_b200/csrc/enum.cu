@@ -1171,6 +1171,82 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // band factor of the linear modes, rounded up once: bnd = m x bandf (rounded up) >= band_bound(m)
     const float bandf = __double2float_ru((1.0 + (double)su.tol_num / (double)su.tol_den) * (1.0 + su.delta) /
                                           (1.0 - su.delta) * (1.0 + 1e-12));
+    // unit constants (row decode, exact QoS range cut on the step worker, row constants X_h, Y_h, Z_h),
+    // computed by one lane per unit right after a fetch and broadcast to the warp when the unit is
+    // processed; false: no step level of the unit is usable (its minimum stays +inf)
+    auto unit_consts = [&](uint64_t unit, int& oT, int& oTm, int& oSb, int& oEa, int& oNe, float& oX, float& oY,
+                           float& oZ) -> bool {
+            int seg;
+            HiSums h;
+            h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
+            int64_t hb[2] = {0, 0};
+            int hs[2] = {0, 0};
+            bool two = false;   // two hi workers decoded by the 32-bit path: the cross term in FP32 below
+            if (units <= 0xffffffffull) {   // 32-bit decode (the common case)
+                two = NH == 2;
+                uint32_t row = (uint32_t)unit;
+                if (nseg > 1) { seg = (int)(row % (uint32_t)nseg); row /= (uint32_t)nseg; } else seg = 0;
+    #pragma unroll
+                for (int w = NH - 1; w >= 0; w--) {
+                    uint32_t dw = row;   // worker 0 is the most significant digit: row < L[0] there
+                    if (w > 0) {
+                        dw = row % (uint32_t)L[w];
+                        row /= (uint32_t)L[w];
+                    }
+                    const Lev& r = sl[w * Lmax + dw];
+                    h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
+                    if (NH == 2) { hb[w] = r.B; hs[w] = r.S; }
+                }
+            } else {
+                seg = (int)(unit % (uint64_t)nseg);
+                uint64_t row = unit / (uint64_t)nseg;
+    #pragma unroll
+                for (int w = NH - 1; w >= 0; w--) {
+                    const int dw = (int)(row % (uint64_t)L[w]);
+                    row /= (uint64_t)L[w];
+                    const Lev& r = sl[w * Lmax + dw];
+                    h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
+                }
+            }
+            const int e0 = seg * segl, e1 = min(Lstep, e0 + segl);
+            int ne = e1 - e0;
+            int sb = 1 << 30;
+            int ea = e0;
+            if (QOS) {
+                sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
+                if (W >= 2 && A.stS[e0] > sb) return false;   // even the smallest step level is infeasible
+                if (step_tab) {
+                    // usable step levels: S'_e <= sb (a prefix) and u_e >= hT + min S'_k (a suffix of the
+                    // suffix-minimum; the prefix maximum says whether earlier levels could qualify)
+                    const int eb = (sb - ss0 >= shi_n) ? Lstep : (int)A.shi[sb - ss0];
+                    const int need = h.T + smin_i;
+                    int lo = (need <= su0) ? 0 : ((need > sulast) ? Lstep : (int)A.slo[need - su0]);
+                    if (lo > 0 && A.stUmax[lo - 1] >= need) lo = 0;
+                    ea = lo;
+                    ne = eb - lo;
+                    if (ne <= 0) return false;
+                }
+            }
+            // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
+            //   X_e = Xh + B_e Yh + S'_e Zh (+ D_e for PAPER),  Y_e = Yh + S'_e inv,  Z_e = Zh + B_e inv
+            const float hBf = __ll2float_rn(h.B), hTf = (float)h.T;
+            const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
+            float Xh;
+            if (MODE == M_EXCL) {
+                float Dhf;   // = sum_hi B_w (hT - S'_w) >= 0
+                if (NH == 2 && two) {   // B_0 S'_1 + B_1 S'_0: non-negative terms, <= 4u (inside delta)
+                    Dhf = fmaf(__ll2float_rn(hb[0]), (float)hs[1], __ll2float_rn(hb[1]) * (float)hs[0]);
+                } else {
+                    const u128 Dh = (u128)h.T * (u128)h.B - (u128)h.BS;
+                    Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+                }
+                Xh = fmaf(Dhf, invf, hBf);
+            } else {
+                Xh = hBf * Yh;
+            }
+        oT = h.T; oTm = h.Tm; oSb = sb; oEa = ea; oNe = ne; oX = Xh; oY = Yh; oZ = Zh;
+        return true;
+    };
     constexpr uint64_t RSTEP = (uint64_t)NWARP * 32;
     uint64_t rbase = ua + (uint64_t)warp * 32;
     int nfetch = 0;
@@ -1209,6 +1285,13 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             rbase += RSTEP;
             pend = __ballot_sync(0xffffffffu, base + wl < ub);
         }
+        int uT = 0, uTm = 0, uSb = 0, uEa = 0, uNe = 0;
+        float uX = 0.0f, uY = 0.0f, uZ = 0.0f;
+        bool uok = false;
+        if ((pend >> wl) & 1u) {   // this lane's own unit
+            const uint64_t myunit = BB ? ua + (uint64_t)loff : base + (uint64_t)wl;
+            uok = unit_consts(myunit, uT, uTm, uSb, uEa, uNe, uX, uY, uZ);
+        }
       while (pend) {
         const int jl = __ffs(pend) - 1;
         pend &= pend - 1;
@@ -1227,80 +1310,16 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (lbj > bnd) continue;
             ndone++;
         }
-        int seg;
-        HiSums h;
-        h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
-        int64_t hb[2] = {0, 0};
-        int hs[2] = {0, 0};
-        bool two = false;   // two hi workers decoded by the 32-bit path: the cross term in FP32 below
-        if (units <= 0xffffffffull) {   // 32-bit decode (the common case)
-            two = NH == 2;
-            uint32_t row = (uint32_t)unit;
-            if (nseg > 1) { seg = (int)(row % (uint32_t)nseg); row /= (uint32_t)nseg; } else seg = 0;
-#pragma unroll
-            for (int w = NH - 1; w >= 0; w--) {
-                uint32_t dw = row;   // worker 0 is the most significant digit: row < L[0] there
-                if (w > 0) {
-                    dw = row % (uint32_t)L[w];
-                    row /= (uint32_t)L[w];
-                }
-                const Lev& r = sl[w * Lmax + dw];
-                h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
-                if (NH == 2) { hb[w] = r.B; hs[w] = r.S; }
-            }
-        } else {
-            seg = (int)(unit % (uint64_t)nseg);
-            uint64_t row = unit / (uint64_t)nseg;
-#pragma unroll
-            for (int w = NH - 1; w >= 0; w--) {
-                const int dw = (int)(row % (uint64_t)L[w]);
-                row /= (uint64_t)L[w];
-                const Lev& r = sl[w * Lmax + dw];
-                h.B += r.B; h.BS += r.BS; h.T += r.S; h.Tm = min(h.Tm, r.Tmax);
-            }
+        const int cT = __shfl_sync(0xffffffffu, uT, jl), cTm = __shfl_sync(0xffffffffu, uTm, jl);
+        const int sb = __shfl_sync(0xffffffffu, uSb, jl), ea = __shfl_sync(0xffffffffu, uEa, jl);
+        const int ne = __shfl_sync(0xffffffffu, uNe, jl);
+        const float Xh = __shfl_sync(0xffffffffu, uX, jl), Yh = __shfl_sync(0xffffffffu, uY, jl);
+        const float Zh = __shfl_sync(0xffffffffu, uZ, jl);
+        if (!__shfl_sync(0xffffffffu, (int)uok, jl)) {   // no usable step level
+            if (!BB && wl == 0) subp[unit] = INFINITY;
+            continue;
         }
-        const int e0 = seg * segl, e1 = min(Lstep, e0 + segl);
-        int ne = e1 - e0;
-        int sb = 1 << 30;
-        int ea = e0;
-        if (QOS) {
-            sb = min(h.Tm - h.T - smin_i, umax_i - h.T);
-            if (W >= 2 && A.stS[e0] > sb) {   // even the smallest step level is infeasible
-                if (wl == 0) subp[unit] = INFINITY;
-                continue;
-            }
-            if (step_tab) {
-                // usable step levels: S'_e <= sb (a prefix) and u_e >= hT + min S'_k (a suffix of the
-                // suffix-minimum; the prefix maximum says whether earlier levels could qualify)
-                const int eb = (sb - ss0 >= shi_n) ? Lstep : (int)A.shi[sb - ss0];
-                const int need = h.T + smin_i;
-                int lo = (need <= su0) ? 0 : ((need > sulast) ? Lstep : (int)A.slo[need - su0]);
-                if (lo > 0 && A.stUmax[lo - 1] >= need) lo = 0;
-                ea = lo;
-                ne = eb - lo;
-                if (ne <= 0) {
-                    if (wl == 0) subp[unit] = INFINITY;
-                    continue;
-                }
-            }
-        }
-        // row constants: the prefix terms are bilinear in the step level (BS_e = B_e S'_e):
-        //   X_e = Xh + B_e Yh + S'_e Zh (+ D_e for PAPER),  Y_e = Yh + S'_e inv,  Z_e = Zh + B_e inv
-        const float hBf = __ll2float_rn(h.B), hTf = (float)h.T;
-        const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
-        float Xh;
-        if (MODE == M_EXCL) {
-            float Dhf;   // = sum_hi B_w (hT - S'_w) >= 0
-            if (NH == 2 && two) {   // B_0 S'_1 + B_1 S'_0: non-negative terms, <= 4u (inside delta)
-                Dhf = fmaf(__ll2float_rn(hb[0]), (float)hs[1], __ll2float_rn(hb[1]) * (float)hs[0]);
-            } else {
-                const u128 Dh = (u128)h.T * (u128)h.B - (u128)h.BS;
-                Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
-            }
-            Xh = fmaf(Dhf, invf, hBf);
-        } else {
-            Xh = hBf * Yh;
-        }
+        const struct { int T, Tm; } h = {cT, cTm};
         int nc = 0;
         // one step entry per lane (relative index k in [ea, ea + ne)); appends the usable ones to
         // the warp's table; returns whether the lane's level lies past the QoS prefix
