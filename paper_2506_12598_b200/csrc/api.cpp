@@ -615,7 +615,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.aux_bytes = 0;
     if (fast) {   // per-problem aux block (staged with the Lev records) + per-warp prefix tables
         su.aux_bytes = (int32_t)pass1_aux_bytes(Lmax);
-        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * seglen * 24);
+        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * 32 * 24);   // 32 entries per warp
     }
     su.lev_stride = W * Lmax + su.aux_bytes / (int)sizeof(Lev);
     return ECLIP_OK;

@@ -290,12 +290,18 @@ struct AuxView {
     int* stS; int* stU; int* stUmax;  // step worker, sorted per segment: S', suffix-min of u, prefix-max of u
     float* preminB;                   // inner worker, S'-sorted: preminB[k] = (float) min_{j<k} B_j (+inf at 0)
     float* chB;                       // step worker, S'-sorted: (float) min B over each aligned chunk of P1_CS
+    float2* ih;                       // inner worker's lower-left hull: vertices {B, S'} in S' order
+    float2* ie;                       //   edges {B_i - B_i+1, S'_i+1 - S'_i}
+    int* ihn;                         //   [1] vertex count
+    uint16_t* hpos;                   // inner, S'-sorted position k -> last hull vertex with S' <= S'_k
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
     size_t b = ((LP * 32 + (size_t)(Lmax + 1) * 12 + (size_t)Lmax * 4 + 15) & ~(size_t)15) + 4 * (size_t)P1_TABN + 32 +
                (size_t)Lmax * 12 +
                (size_t)(Lmax + 1) * 4 + (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;
+    b = (b + 7) & ~(size_t)7;
+    b += (size_t)Lmax * 16 + 4 + (size_t)Lmax * 2;   // ih, ie, ihn, hpos
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -320,13 +326,19 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.stUmax = a.stU + Lmax;
     a.preminB = reinterpret_cast<float*>(a.stUmax + Lmax);
     a.chB = a.preminB + (Lmax + 1);
+    unsigned char* q = reinterpret_cast<unsigned char*>(a.chB + (Lmax + P1_CS - 1) / P1_CS);
+    q = base + ((q - base + 7) & ~(size_t)7);
+    a.ih = reinterpret_cast<float2*>(q);
+    a.ie = a.ih + Lmax;
+    a.ihn = reinterpret_cast<int*>(a.ie + Lmax);
+    a.hpos = reinterpret_cast<uint16_t*>(a.ihn + 1);
     return a;
 }
 
 // one CTA per problem: sort, pair up, and tabulate the inner / step workers once
 template <int MODE>
 __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, Lev* levs, const int32_t* table_of,
-                                                  const uint16_t* tord) {
+                                                  const uint16_t* tord, const uint16_t* thull, const int32_t* thull_n) {
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
     if (P.status != 0) return;
@@ -445,6 +457,29 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
                     carry = __shfl_sync(0xffffffffu, v, 31);
                 }
             }
+        }
+    }
+    {   // the inner worker's hull (its table's vertex set, k_table_hull) and the clamp positions
+        const int ti = table_of[(size_t)prob * W + W - 1];
+        const uint16_t* hx = thull + (size_t)ti * Lmax;
+        const int nh = thull_n[ti];
+        for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+            const Lev& v = inner[hx[i]];
+            A.ih[i] = make_float2(__ll2float_rn(v.B), (float)v.S);
+            if (i + 1 < nh) {
+                const Lev& x = inner[hx[i + 1]];
+                A.ie[i] = make_float2(__ll2float_rn(v.B - x.B), (float)(x.S - v.S));
+            }
+        }
+        if (threadIdx.x == 0) *A.ihn = nh;
+        for (int k = threadIdx.x; k < Lin; k += blockDim.x) {   // last vertex with S' <= S'_k (exact ints)
+            const int sk = inner[A.perm[k]].S;
+            int lo = 0, hi = nh - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (inner[hx[mid]].S <= sk) lo = mid; else hi = mid - 1;
+            }
+            A.hpos[k] = (uint16_t)lo;
         }
     }
     if (W >= 2)
@@ -744,6 +779,33 @@ __device__ __forceinline__ float hull_min_in(const float2* v, const float2* ed, 
     const float2 p = v[a], q = v[a + 1];
     const float B = fmaf(q.x - p.x, (c - p.y) / (q.y - p.y), p.x);
     return fmaf(B, y, c * z);
+}
+
+// hull_min_in with the range ends given as inner S'-sorted positions ka <= kb: their S' (ssort) and
+// the last hull vertex at or below each (hpos) are tabulated, so the clamp needs no search
+__device__ __forceinline__ float hull_min_pos(const AuxView& A, int n, float y, float z, int ka, int kb) {
+    const float2* v = A.ih;
+    const float2* ed = A.ie;
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float2 e = ed[mid];
+        if (e.x * y > e.y * z) lo = mid + 1; else hi = mid;
+    }
+    const float s = v[lo].y, slo = (float)A.ssort[ka], shi = (float)A.ssort[kb];
+    if (s >= slo && s <= shi) {
+        float m = fmaf(v[lo].x, y, s * z);
+        if (lo > 0) m = fminf(m, fmaf(v[lo - 1].x, y, v[lo - 1].y * z));
+        if (lo + 1 < n) m = fminf(m, fmaf(v[lo + 1].x, y, v[lo + 1].y * z));
+        return m;
+    }
+    const bool below = s < slo;
+    const float c = below ? slo : shi;
+    const int a = A.hpos[below ? ka : kb];
+    if (a >= n - 1) return fmaf(v[n - 1].x, y, c * z);
+    const float2 p = v[a], q = v[a + 1];
+    const float B = fmaf(q.x - p.x, (c - p.y) / (q.y - p.y), p.x);
+    return fmaf(fmaxf(B, q.x), y, c * z);
 }
 
 // one thread per row: the bound above, times (1 - 2^-16) (covers its FP32 rounding, <= 16u, and
@@ -1130,16 +1192,11 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         lbm = __uint_as_float(bb.lbmin[prob]);
         if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; s_stop = 0; }
     }
-    const float2* hv = nullptr;   // inner worker's lower-left hull (vertices {B, S'}, then edges), BB only
-    int nhv = 0;
-    if (BB) {
-        hv = bb.hull + ((size_t)prob * 2 + 1) * 2 * su.Lmax;
-        nhv = bb.rowhdr[prob].nh[1];
-    }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
     stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
     const AuxView A = aux_view(smem_raw + (size_t)W * Lmax * sizeof(Lev), Lmax);
+    const int nhv = *A.ihn;   // inner hull vertex count (staged with the aux block)
 
     int L[NW];
 #pragma unroll
@@ -1150,8 +1207,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + su.aux_bytes);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
     constexpr int NWARP = P1_THREADS / 32;
-    float4* tab = tab0 + (size_t)warp * segl;                                                    // {X,Y,Z,Tp}
-    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * segl) + (size_t)warp * segl;     // {k_lo, k_hi}
+    float4* tab = tab0 + (size_t)warp * 32;                                                      // {X,Y,Z,Tp}
+    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * 32) + (size_t)warp * 32;         // {k_lo, k_hi}
     const float invf = P.inv;
     const double invd = 1.0 / (double)P.lamN;
     const int s0 = A.hdr[0], u0v = A.hdr[1];
@@ -1321,6 +1378,57 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         const struct { int T, Tm; } h = {cT, cTm};
         int nc = 0;
+        bool had = false;
+        float m0 = INFINITY, m1 = INFINITY;
+        // sweep the warp's table (<= 32 entries, one per lane): packed FMAs over each entry's exact
+        // QoS-feasible inner range; called after every entry pass (surviving entries are rare)
+        auto sweep = [&]() {
+            for (int i = wl; i < nc; i += 32) {
+                const float4 t4 = tab[i];
+                int2 kk = tabk[i];
+                if (QOS && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
+                    kk.x = -1 - kk.x;
+                    const int kend = min(kk.x, kk.y);
+                    for (int k = 0; k < kend; k++) {
+                        const float4 r = A.ip[k >> 1];
+                        const float2 uu2 = A.iu[k >> 1];
+                        const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
+                        float b0 = t4.x;
+                        if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
+                        if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
+                    }
+                }
+                const int ka = max(kk.x, 0), kb2 = kk.y;
+                if (ka >= kb2) continue;
+                nfeas += (unsigned long long)(kb2 - ka);
+                const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
+                int k = ka;
+                if (k & 1) {   // leading odd element
+                    const float4 r = A.ip[k >> 1];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += A.iD[k >> 1].y;
+                    m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
+                    k++;
+                }
+                const int pend = kb2 >> 1;
+    #pragma unroll 4
+                for (int p = k >> 1; p < pend; p++) {
+                    const float4 r = A.ip[p];
+                    u64 base = X2;
+                    if (MODE == M_PAPER) { const float2 dd = A.iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                    const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+                    float k0, k1;
+                    f2unpack(key, k0, k1);
+                    m0 = fminf(m0, fminf(k0, k1));
+                }
+                if (kb2 & 1) {  // trailing odd element
+                    const float4 r = A.ip[kb2 >> 1];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
+                    m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
+                }
+            }
+        };
         // one step entry per lane (relative index k in [ea, ea + ne)); appends the usable ones to
         // the warp's table; returns whether the lane's level lies past the QoS prefix
         auto entry = [&](int k, bool valid) -> bool {
@@ -1361,8 +1469,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                         const int ka = pre ? 0 : klo;
                         float lbe = fmaf(ent.y, A.preminB[khi], fmaf(ent.z, (float)A.ssort[ka], ent.x));
                         if (!(lbe * 0.99998474121f > bnd))
-                            lbe = fmaxf(lbe, ent.x + hull_min_in(hv, hv + su.Lmax, nhv, ent.y, ent.z, (float)A.ssort[ka],
-                                                                 (float)A.ssort[khi - 1]));
+                            lbe = fmaxf(lbe, ent.x + hull_min_pos(A, nhv, ent.y, ent.z, ka, khi - 1));
                         use = !(lbe * 0.99998474121f > bnd);   // 1 - 2^-16
                     }
                     if (pre) klo = -1 - klo;   // flag: sweep [0, |klo|) with a mask first
@@ -1376,6 +1483,13 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             }
             nc += __popc(bal);
             if (wl == 0) nent += __popc(bal);
+            if (nc) {
+                had = true;
+                __syncwarp();
+                sweep();
+                __syncwarp();   // the table is rewritten by the next pass
+                nc = 0;
+            }
             return past;
         };
         bool chunked = false;
@@ -1402,8 +1516,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                         const float Yc = fmaf(Sf, invf, Yh), Zc = fmaf(Bm, invf, Zh);
                         float lbc = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
                         if (!(lbc * 0.99998474121f > bnd))
-                            lbc = fmaxf(lbc, Xc + hull_min_in(hv, hv + su.Lmax, nhv, Yc, Zc, (float)A.ssort[ka],
-                                                              (float)A.ssort[khi2 - 1]));
+                            lbc = fmaxf(lbc, Xc + hull_min_pos(A, nhv, Yc, Zc, ka, khi2 - 1));
                         keep = !(lbc * 0.99998474121f > bnd);   // 1 - 2^-16
                     }
                 }
@@ -1422,53 +1535,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             for (int kb = 0; kb < ne; kb += 32)
                 if (__all_sync(0xffffffffu, entry(kb + wl, kb + wl < ne))) break;   // the rest of the sorted segment is unusable
         __syncwarp();
-        if (BB && wl == 0 && nc > 0) nue++;
-        float m0 = INFINITY, m1 = INFINITY;
-        for (int i = wl; i < nc; i += 32) {
-            const float4 t4 = tab[i];
-            int2 kk = tabk[i];
-            if (QOS && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
-                kk.x = -1 - kk.x;
-                const int kend = min(kk.x, kk.y);
-                for (int k = 0; k < kend; k++) {
-                    const float4 r = A.ip[k >> 1];
-                    const float2 uu2 = A.iu[k >> 1];
-                    const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
-                    if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
-                }
-            }
-            const int ka = max(kk.x, 0), kb2 = kk.y;
-            if (ka >= kb2) continue;
-            nfeas += (unsigned long long)(kb2 - ka);
-            const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
-            int k = ka;
-            if (k & 1) {   // leading odd element
-                const float4 r = A.ip[k >> 1];
-                float b0 = t4.x;
-                if (MODE == M_PAPER) b0 += A.iD[k >> 1].y;
-                m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
-                k++;
-            }
-            const int pend = kb2 >> 1;
-#pragma unroll 4
-            for (int p = k >> 1; p < pend; p++) {
-                const float4 r = A.ip[p];
-                u64 base = X2;
-                if (MODE == M_PAPER) { const float2 dd = A.iD[p]; base = add2(X2, f2pack(dd.x, dd.y)); }
-                const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
-                float k0, k1;
-                f2unpack(key, k0, k1);
-                m0 = fminf(m0, fminf(k0, k1));
-            }
-            if (kb2 & 1) {  // trailing odd element
-                const float4 r = A.ip[kb2 >> 1];
-                float b0 = t4.x;
-                if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
-                m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
-            }
-        }
+        if (BB && wl == 0 && had) nue++;
         float m = fminf(m0, m1);
         if (BB && !__any_sync(0xffffffffu, m < INFINITY)) {   // nothing feasible swept: submin stays +inf
             __syncwarp();
@@ -2404,7 +2471,7 @@ cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Wor
         auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;
         e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
-        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs, in.table_of, wk.tord);
+        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs, in.table_of, wk.tord, wk.thull, wk.thull_n);
     }
     return cudaGetLastError();
 }
