@@ -13,7 +13,10 @@ constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
 constexpr int P1_THREADS = 256; // pass-1 CTA size
 constexpr int KIN = 16;         // inner-worker levels held in registers per thread (fast pass 1)
 constexpr int P1_CS = 4;        // step-level chunk of the pass-1 chunk filter
-constexpr int P1_TABN = 8192;   // entries of each QoS range lookup table (fast pass 1)
+#ifndef P1_TABN_N
+#define P1_TABN_N 6144
+#endif
+constexpr int P1_TABN = P1_TABN_N;   // entries of each QoS range lookup table (fast pass 1)
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
 enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };

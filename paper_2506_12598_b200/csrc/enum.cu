@@ -1158,7 +1158,7 @@ __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, con
 
 template <int NW, int MODE, bool QOS, bool BB>
 #ifndef P1_MINB
-#define P1_MINB 3
+#define P1_MINB 4
 #endif
 __global__ void __launch_bounds__(P1_THREADS, P1_MINB)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
