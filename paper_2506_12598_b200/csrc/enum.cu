@@ -294,6 +294,7 @@ struct AuxView {
     float2* ie;                       //   edges {B_i - B_i+1, S'_i+1 - S'_i}
     int* ihn;                         //   [1] vertex count
     uint16_t* hpos;                   // inner, S'-sorted position k -> last hull vertex with S' <= S'_k
+    float* chBs;                      // step worker: suffix minimum of chB over the chunks
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
@@ -302,6 +303,8 @@ __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
                (size_t)(Lmax + 1) * 4 + (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;
     b = (b + 7) & ~(size_t)7;
     b += (size_t)Lmax * 16 + 4 + (size_t)Lmax * 2;   // ih, ie, ihn, hpos
+    b = (b + 3) & ~(size_t)3;
+    b += (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;   // chBs
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -332,6 +335,8 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.ie = a.ih + Lmax;
     a.ihn = reinterpret_cast<int*>(a.ie + Lmax);
     a.hpos = reinterpret_cast<uint16_t*>(a.ihn + 1);
+    q = reinterpret_cast<unsigned char*>(a.hpos + Lmax);
+    a.chBs = reinterpret_cast<float*>(base + ((q - base + 3) & ~(size_t)3));
     return a;
 }
 
@@ -489,6 +494,10 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
             A.chB[c] = m;
         }
     __syncthreads();
+    if (W >= 2 && threadIdx.x == 0) {   // suffix minimum of the chunk minima
+        float m = INFINITY;
+        for (int c = (Lst + P1_CS - 1) / P1_CS - 1; c >= 0; c--) { m = fminf(m, A.chB[c]); A.chBs[c] = m; }
+    }
     const int s0 = A.ssort[0], u0 = A.usuf[0];
     const bool khi_ok = Lin <= 255 && A.ssort[Lin - 1] - s0 + 1 <= P1_TABN;
     const bool klo_ok = Lin <= 255 && A.usuf[Lin - 1] - u0 + 1 <= P1_TABN;
@@ -1302,6 +1311,24 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 Xh = hBf * Yh;
             }
         oT = h.T; oTm = h.Tm; oSb = sb; oEa = ea; oNe = ne; oX = Xh; oY = Yh; oZ = Zh;
+        if (BB && QOS && step_tab && W >= 2) {
+            // unit bound: the chunk bound with every usable step level as one chunk (smallest S' = S'_ea,
+            // smallest B >= the suffix minimum from ea's chunk); decided against the band at fetch time
+            // (the band only tightens afterwards)
+            const int Sa = A.stS[ea];
+            const float Bm = A.chBs[ea / P1_CS];
+            const int Tp = h.T + Sa;
+            const int khi2 = inner_khi(A, h.Tm - Tp, s0, slast, khi_ok, Lin);
+            const int klo2 = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
+            const int ka = A.umaxp[klo2] >= Tp ? 0 : klo2;
+            if (khi2 <= ka) return false;
+            const float Sf = (float)Sa;
+            const float Xc = fmaf(Bm, Yh, fmaf(Sf, Zh, Xh));
+            const float Yc = fmaf(Sf, invf, Yh), Zc = fmaf(Bm, invf, Zh);
+            float lbu = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
+            if (!(lbu * 0.99998474121f > bnd)) lbu = fmaxf(lbu, Xc + hull_min_pos(A, nhv, Yc, Zc, ka, khi2 - 1));
+            if (lbu * 0.99998474121f > bnd) return false;
+        }
         return true;
     };
     constexpr uint64_t RSTEP = (uint64_t)NWARP * 32;
