@@ -270,9 +270,9 @@ def main():
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": float(e2e_t.item()) / a.steps},
-            # per step: k_levels, k_prep_prob, k_prep_lev, k_table_hull, k_prep_aux, 3 x k_fill_u32, k_prep_bound,
+            # per step: k_levels, k_prep_prob, k_prep_lev, k_table_hull, k_prep_aux, 2 x k_fill_u32, k_prep_bound,
             # k_rowlb_fused, k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/r01_timeline_c5.txt)
-            "gpu_launches": int(14 * a.steps),
+            "gpu_launches": int(13 * a.steps),
             "roofline": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,QoS>", "achieved": achieved,
                          "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
                          "frac": achieved / peak, "traffic": (ncu_pass1(a.mixes) or {}).get("bytes_per_launch"),

@@ -44,18 +44,22 @@ def _compile(src: str, force: bool) -> str:
 
 
 def build_variant(name: str, defines) -> str:
-    """A/B experiments only: libeclip_<name>.so with extra -D flags (load with ECLIP_LIB=...)."""
+    """A/B experiments and test builds only: libeclip_<name>.so with extra -D flags (load with
+    ECLIP_LIB=...)."""
     odir = os.path.join(OBJ, name)
     os.makedirs(odir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+
+    def one(src):
         lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
         obj = os.path.join(odir, src + ".o")
         cmd = [NVCC] + ARCH + FLAGS + [f"-D{d}" for d in defines] + lang + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        objs.append(obj)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(one, SOURCES))
     lib = os.path.join(HERE, f"libeclip_{name}.so")
     r = subprocess.run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs, capture_output=True, text=True)
     if r.returncode != 0:

@@ -641,7 +641,7 @@ static int alloc_work(eclip_session* s) {
         o_thn = bp.take<int32_t>((size_t)s->tb.n);
         o_tord = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
     }
-    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0, o_pl = 0, o_pln = 0;
+    size_t o_rowlb = 0, o_lbmin = 0, o_inc = 0, o_hull = 0, o_ftab = 0, o_ulist = 0, o_uln = 0, o_rh = 0, o_pl = 0, o_pln = 0, o_wb = 0;
     if (bb) {
         o_rowlb = bp.take<float>(n * (size_t)su.rows_max);
         o_lbmin = bp.take<unsigned>(n);
@@ -654,6 +654,7 @@ static int alloc_work(eclip_session* s) {
 
         o_pl = bp.take<uint32_t>(n * (size_t)PL_CAP);
         o_pln = bp.take<int32_t>(n);
+        o_wb = bp.take<uint32_t>(n * (size_t)((su.units_max + 31) >> 5));
     }
     unsigned char* base;
     CU(s->arena.alloc(&base, bp.off));
@@ -689,6 +690,7 @@ static int alloc_work(eclip_session* s) {
 
         wk.plist = (uint32_t*)(base + o_pl);
         wk.plist_n = (int32_t*)(base + o_pln);
+        wk.wbits = (uint32_t*)(base + o_wb);
     }
     return ECLIP_OK;
 }

@@ -155,6 +155,8 @@ struct Work {
     uint64_t* bandlist;         // [n * BAND_CAP] band units in index order (k_reduce_min)
     uint32_t* plist;            // [n * PL_CAP] units pass 1 processed with a finite minimum (pruned pass 1)
     int32_t* plist_n;           // [n] their count (> PL_CAP: overflow, reduce_min scans every unit)
+    uint32_t* wbits;            // [n * ceil(units_max / 32)] pruned pass 1: units whose submin was written
+                                //   (every other unit reads as +inf; replaces a +inf fill of submin)
     uint16_t* thull;            // [tables * Lmax] hull vertex levels of every level table (k_table_hull)
     int32_t* thull_n;           // [tables]
     uint16_t* tord;             // [tables * Lmax] level indices of every level table in S order (k_table_hull)
@@ -164,8 +166,15 @@ struct Work {
 };
 
 constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem
-constexpr int BAND_CAP = 64;
-constexpr int PL_CAP = 4096;   // processed-unit list capacity per problem    // pass-2 band list capacity per problem
+#ifndef BAND_CAP_N
+#define BAND_CAP_N 64
+#endif
+#ifndef PL_CAP_N
+#define PL_CAP_N 4096
+#endif
+constexpr int BAND_CAP = BAND_CAP_N;   // pass-2 band list capacity per problem
+constexpr int PL_CAP = PL_CAP_N;       // processed-unit list capacity per problem (tiny values in test builds
+                                       // exercise the overflow paths)
 
 struct RowHdr {                 // per-problem constants of the row bound (k_prep_bound)
     int32_t nh[2];              // hull sizes (step, inner)

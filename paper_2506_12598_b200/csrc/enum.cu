@@ -1107,6 +1107,12 @@ __device__ __forceinline__ void item_of_block(const Setup& su, const Prob& P, in
 // Row pruning (BB): a unit is processed only if its row bound lies in this
 // wave's window (lbmin*lo_f, lbmin*hi_f] and below the band of the problem's incumbent `inc`
 // (the smallest FP32 key found so far, updated here); skipped units keep submin = +inf.
+// pruned pass 1: submin[prob][u] holds a value only if bit u of the problem's written-unit bitmap is set
+__device__ __forceinline__ size_t wbits_words(const Setup& su) { return (size_t)((su.units_max + 31) >> 5); }
+__device__ __forceinline__ float sub_at(const Setup& su, const float* sp, const uint32_t* wb, int p, uint64_t u) {
+    if (wb && !((wb[(size_t)p * wbits_words(su) + (u >> 5)] >> (u & 31)) & 1u)) return INFINITY;
+    return sp[u];
+}
 struct BBArgs {
     const uint2* ulist;         // [grid][upi] this item's candidate units {unit - ua, bound bits}, bucket-ordered
     const int32_t* ulist_n;     // [grid]
@@ -1115,6 +1121,7 @@ struct BBArgs {
     unsigned long long* rows_done;  // [3]: units processed, units with >= 1 swept entry, entries swept
     uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
     int32_t* plist_n;
+    uint32_t* wbits;            // [n][ceil(units_max / 32)] units whose submin this launch wrote
     const float2* hull;         // [n][2][2][Lmax] (k_prep_bound): the inner worker's hull at [2][0], edges [2][1]
     const RowHdr* rowhdr;       // [n] hull sizes
 };
@@ -1571,6 +1578,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (wl == 0) {
             subp[unit] = m;
+            if (BB) atomicOr(bb.wbits + (size_t)prob * wbits_words(su) + (unit >> 5), 1u << (unit & 31));
             if (BB && m < INFINITY) {
                 const int pos = atomicAdd(bb.plist_n + prob, 1);
                 if (pos < PL_CAP) bb.plist[(size_t)prob * PL_CAP + pos] = (uint32_t)unit;
@@ -1802,7 +1810,9 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         }
         cudaError_t e;
         const size_t n = (size_t)su.n_problems;
-        if ((e = fill_u32(wk.submin, n * (size_t)su.units_max, 0x7f800000u, st)) != cudaSuccess) return e;
+        // unwritten units read as +inf through the bitmap (sub_at), so submin itself is not filled
+        if ((e = cudaMemsetAsync(wk.wbits, 0, n * (size_t)((su.units_max + 31) >> 5) * sizeof(uint32_t), st)) != cudaSuccess)
+            return e;
         if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(wk.plist_n, 0, n * sizeof(int32_t), st)) != cudaSuccess) return e;
@@ -1830,7 +1840,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
                                                        wk.ulist, wk.ulist_n);
             if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
                 return e;
-            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.hull, wk.rowhdr};
+            BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.wbits, wk.hull, wk.rowhdr};
             if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
             f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
             if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
@@ -1844,7 +1854,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
         k_bucket<<<(unsigned)grid, 256, 0, st>>>(su, wk.probs, wk.rowlb, wk.lbmin, wk.ulist, wk.ulist_n);
-        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.hull, wk.rowhdr};
+        BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.wbits, wk.hull, wk.rowhdr};
         if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
         f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
         if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
@@ -1898,7 +1908,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
 __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs, const float* submin,
                                                     const float* submin_sure, float* m32, float* m32_sure,
                                                     int32_t* bandn, uint64_t* bandlist, const uint32_t* plist,
-                                                    const int32_t* plist_n) {
+                                                    const int32_t* plist_n, const uint32_t* wbits) {
     __shared__ float rm[8], rs[8];
     __shared__ int s_cnt;
     __shared__ uint64_t s_list[BAND_CAP];
@@ -1921,7 +1931,7 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
             for (int i = tid; i < nl; i += blockDim.x) m = fminf(m, sp[lst[i]]);
         } else {
             for (uint64_t u = a + tid; u < b; u += blockDim.x) {
-                m = fminf(m, sp[u]);
+                m = fminf(m, sub_at(su, sp, wbits, p, u));
                 if (submin_sure) ms = fminf(ms, submin_sure[(size_t)p * su.units_max + u]);
             }
         }
@@ -1951,7 +1961,7 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
                 }
         } else {
             for (uint64_t u = a + tid; u < b; u += blockDim.x)
-                if (sp[u] <= bound) {
+                if (sub_at(su, sp, wbits, p, u) <= bound) {
                     const int pos = atomicAdd(&s_cnt, 1);
                     if (pos < BAND_CAP) s_list[pos] = u;
                 }
@@ -1976,7 +1986,8 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
     const bool two = su.mode == M_MATRIX && su.has_qos;
     k_reduce_min<<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
-                                                wk.m32_sure, wk.bandn, wk.bandlist, wk.plist, wk.plist_n);
+                                                wk.m32_sure, wk.bandn, wk.bandlist, wk.plist, wk.plist_n,
+                                                pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
 }
 
@@ -2076,7 +2087,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
                                                const float* __restrict__ submin, const float* m32,
                                                const float* m32_sure, U256* hstar, U256* first,
                                                const int32_t* bandn, const uint64_t* bandlist,
-                                               const float2* hull, const RowHdr* rowhdr) {
+                                               const float2* hull, const RowHdr* rowhdr, const uint32_t* wbits) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ U256 red[P2_THREADS];
@@ -2251,7 +2262,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
         if (nband >= 0) {   // the band's units, listed in index order by k_reduce_min
             for (int i = 0; i < nband; i++) {
                 const uint64_t unit = bandlist[(size_t)prob * BAND_CAP + i];
-                if (!(submin[(size_t)prob * su.units_max + unit] <= bound)) continue;
+                if (!(sub_at(su, submin + (size_t)prob * su.units_max, wbits, prob, unit) <= bound)) continue;
                 unit_scan(phase, unit, hs, best, besti);
                 if (phase == 1 && __syncthreads_or(besti != ~0ull)) break;   // first unit with a hit holds the winner
             }
@@ -2261,7 +2272,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
         bool done = false;
         for (uint64_t blk = ua; blk < ub && !done; blk += blockDim.x) {
             const uint64_t u = blk + threadIdx.x;
-            const bool in_band = u < ub && submin[(size_t)prob * su.units_max + u] <= bound;
+            const bool in_band = u < ub && sub_at(su, submin + (size_t)prob * su.units_max, wbits, prob, u) <= bound;
             if (threadIdx.x == 0) nlist = 0;
             __syncthreads();
             const unsigned bal = __ballot_sync(0xffffffffu, in_band);
@@ -2339,7 +2350,8 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<0><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
+                                                 pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2348,7 +2360,8 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<2><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
+                                                 pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2357,7 +2370,8 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_pass2<1><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
                                                  (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr);
+                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
+                                                 pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
 }
 

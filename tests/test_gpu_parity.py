@@ -385,3 +385,25 @@ def test_pruned_sampled_mixes_vs_oracle_without_qos():
         assert o.status == "ok" and int(out["status"][i]) == 0
         assert out["winner_levels"][i].tolist() == o.levels, i
         assert int(out["winner_index"][i]) == o.index, i
+
+
+@pytest.mark.gpu
+def test_overflow_fallbacks_with_tiny_list_capacities():
+    """The fallbacks behind the pruned pass 1's fixed-capacity lists: with a processed-unit list and a
+    pass-2 band list of capacity 1 (a test build, -DPL_CAP_N=1 -DBAND_CAP_N=1), k_reduce_min and pass 2
+    scan every unit and see only the units pass 1 wrote (written-unit bitmap, the rest read +inf).
+    Selected parity tests rerun against that build in a subprocess (the library is loaded once per
+    process)."""
+    import os
+    import subprocess
+    import sys
+    from paper_2506_12598_b200 import build as bld
+    lib = os.path.join(os.path.dirname(bld.__file__), "libeclip_tinycap.so")
+    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(bld.LIB):
+        bld.build_variant("tinycap", ["PL_CAP_N=1", "BAND_CAP_N=1"])
+    env = dict(os.environ, ECLIP_LIB=lib)
+    sel = "pruned_equals_exhaustive or exact_ties or c5_small_batch or c5_batch_full or sharded"
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k", sel, "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
