@@ -59,7 +59,8 @@ extern "C" {
 
 /* ---- engines ------------------------------------------------------------------------ */
 #define ECLIP_ENGINE_AUTO 0
-#define ECLIP_ENGINE_ENUM 1         /* exhaustive level-tuple enumeration (every candidate scored) */
+#define ECLIP_ENGINE_ENUM 1         /* level-tuple enumeration: every candidate is classified exactly (QoS range
+                                       cuts, branch-and-bound lower bounds) and the rest scored */
 #define ECLIP_ENGINE_SLICE 2        /* exact T'-sliced DP (linear slowdown modes only) */
 #define ECLIP_ENGINE_BASELINE 3     /* result of eclip_baseline_plan (a fixed comparison plan, no search) */
 
@@ -129,7 +130,10 @@ typedef struct {
     uint64_t winner_index;        /* mixed-radix index of the winning level tuple (worker 0 most significant);
                                      UINT64_MAX when prod_w L_w exceeds 2^64 (winner_levels is always exact) */
     uint64_t candidates;          /* level tuples in the search space (prod_w L_w; UINT64_MAX if >= 2^64) */
-    uint64_t units_scored;        /* ENUM: tuples scored; SLICE: lattice points evaluated */
+    uint64_t units_scored;        /* ENUM: level tuples covered (= candidates: each one classified exactly or scored);
+                                     SLICE: lattice points evaluated */
+    uint64_t candidates_evaluated;/* ENUM: tuples whose FP32 key pass 1 actually computed (the rest were classified
+                                     without arithmetic: QoS range cuts, lower bounds); SLICE: 0 */
     uint64_t exact_key[4];        /* the winner's exact integer key, little-endian limbs */
 } eclip_result;
 
@@ -146,8 +150,9 @@ typedef struct {
 
 void eclip_default_options(eclip_options* o);
 
-/* Plan one problem.  Every level tuple is scored on the GPU (or the exact SLICE DP covers
- * them); the winner is the lowest-index tuple whose exact key is within (1+tau) of the exact
+/* Plan one problem.  Every level tuple is covered on the GPU: ENUM classifies each one exactly
+ * (infeasible by exact QoS range cuts, provably outside the tolerance band by exact lower bounds,
+ * DESIGN.md §3.9) and scores the rest; SLICE covers them with the exact T'-slice DP.  The winner is the lowest-index tuple whose exact key is within (1+tau) of the exact
  * minimum.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_TOO_LARGE, ECLIP_E_CUDA, ECLIP_E_OOM. */
 int eclip_plan(const eclip_profiles* prof, const eclip_problem* problem, const eclip_options* opt,
                eclip_result* result);
@@ -227,6 +232,22 @@ int eclip_session_create_problem(const eclip_profiles* prof, const eclip_problem
                                  const eclip_options* opt, eclip_session** out);
 int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_tuple, eclip_result* result);
 
+/* ---- level-1 tables (introspection) --------------------------------
+ * eclip_level_table: the level table K1 builds on the GPU for ONE worker — model `model` of the
+ * profiles with kernel groups `group_bounds` (NULL => one group per kernel; else G+1 ascending
+ * kernel offsets 0 = b_0 < ... < b_G = K), allowed size columns `allowed_mask` (0 => all) and
+ * switch budget R >= 0.  For every attained CU-sum S (SMs): B*(S) = the minimum solo
+ * time sum_g beta_g (ns) over plans with <= R switches and the canonical witness (lexicographically
+ * smallest size-column sequence among the minimisers), levels in witness (rank) order — the
+ * candidate order of eclip_plan.  Outputs (caller-allocated host arrays, `cap`
+ * levels): S[cap] int64, B[cap] int64, witness[cap * G] uint8 size columns (level-major);
+ * *n_levels receives L (if L > cap nothing is copied and ECLIP_E_INVALID_ARG is returned with
+ * *n_levels = L, so a call with cap = 0 queries L).  *n_groups (optional) receives G.
+ * Errors: ECLIP_E_INVALID_ARG, ECLIP_E_TOO_LARGE, ECLIP_E_CUDA, ECLIP_E_OOM. */
+int eclip_level_table(const eclip_profiles* prof, int32_t model, const int32_t* group_bounds, uint32_t allowed_mask,
+                      int32_t switch_max, const eclip_options* opt, int32_t cap, int64_t* S, int64_t* B,
+                      uint8_t* witness, int32_t* n_levels, int32_t* n_groups);
+
 /* ---- comparison planners and the lookup table -----------------------
  * eclip_baseline_plan: the paper's comparison plans (§V), evaluated on the GPU with
  * the same model as eclip_plan (slowdown mode, objective, power, exact QoS check):
@@ -239,7 +260,7 @@ int eclip_session_finish_problem(eclip_session* s, const uint64_t* global_first_
  * is NOT enforced (the baselines do not have one; model_switches reports what the plan uses).
  * result: status ECLIP_OK, or ECLIP_INFEASIBLE when the plan violates a QoS bound (every other
  * field still describes the plan); engine_used = ECLIP_ENGINE_BASELINE; winner_levels = -1;
- * winner_index = UINT64_MAX; candidates = units_scored = 1; exact_key = 0.
+ * winner_index = UINT64_MAX; candidates = units_scored = 1; candidates_evaluated = 0; exact_key = 0.
  * Errors: as eclip_plan (ECLIP_E_INVALID_ARG for an unknown kind / out-of-range param). */
 int eclip_baseline_plan(const eclip_profiles* prof, const eclip_problem* problem, int32_t kind, double param,
                         const eclip_options* opt, eclip_result* result);

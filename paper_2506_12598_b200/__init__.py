@@ -5,7 +5,7 @@ this package is its thin Python binding (eclip.py) plus the multi-GPU protocol
 (parallel.py).  Build with `python -m paper_2506_12598_b200.build`.
 """
 from .eclip import (EclipError, Profiles, Plan, Session, plan, plan_batch, plan_problem, alloc_batch_out, lib,
-                    baseline_plan, lookup_table_json, simulate, BASELINES, MODES, OBJECTIVES, EXPORTS)
+                    baseline_plan, lookup_table_json, simulate, level_table, BASELINES, MODES, OBJECTIVES, EXPORTS)
 
 __all__ = ["EclipError", "Profiles", "Plan", "Session", "plan", "plan_batch", "plan_problem", "alloc_batch_out",
-           "baseline_plan", "lookup_table_json", "simulate", "BASELINES", "lib", "MODES", "OBJECTIVES", "EXPORTS"]
+           "baseline_plan", "lookup_table_json", "simulate", "level_table", "BASELINES", "lib", "MODES", "OBJECTIVES", "EXPORTS"]

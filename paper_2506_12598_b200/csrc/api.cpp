@@ -1113,6 +1113,12 @@ static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_ove
     uint64_t total = totl < 1.8e19L ? (uint64_t)totl : ~0ull;   // all-ones: more than 2^64 tuples
     r->candidates = total;
     r->units_scored = s->engine == ECLIP_ENGINE_ENUM ? total : slice_units(s->slice);
+    r->candidates_evaluated = 0;
+    if (s->engine == ECLIP_ENGINE_ENUM && s->wk.feasible) {
+        unsigned long long v = 0;
+        CU(cudaMemcpy(&v, s->wk.feasible, sizeof v, cudaMemcpyDeviceToHost));
+        r->candidates_evaluated = v;
+    }
     size_t off = 0;
     for (int w = 0; w < W; w++) {
         int G = s->tabs[s->h_table_of[w]].G;
@@ -1157,6 +1163,55 @@ extern "C" int eclip_plan(const eclip_profiles* prof, const eclip_problem* probl
     rc = run_all_steps(s);
     if (rc) return rc;
     return plan_one(s, r, nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// level-table introspection (K1 output of one worker)
+// ------------------------------------------------------------------------------------------
+extern "C" int eclip_level_table(const eclip_profiles* P, int32_t model, const int32_t* gb, uint32_t mask, int32_t R,
+                                 const eclip_options* opt, int32_t cap, int64_t* S, int64_t* B, uint8_t* wit,
+                                 int32_t* n_levels, int32_t* n_groups) {
+    if (!P || !n_levels || cap < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    if (model < 0 || model >= P->n()) return fail(ECLIP_E_INVALID_ARG, "model %d out of range", model);
+    if (R < 0) return fail(ECLIP_E_INVALID_ARG, "switch_max must be >= 0");
+    if (cap > 0 && (!S || !B || !wit)) return fail(ECLIP_E_INVALID_ARG, "null output array");
+    const int C = P->C(), K = P->nk[model];
+    TableSpec sp;
+    sp.model = model;
+    sp.R = R;
+    sp.mask = mask ? mask : ((C == 32) ? 0xffffffffu : ((1u << C) - 1u));
+    if (C < 32) sp.mask &= (1u << C) - 1u;
+    if (sp.mask == 0) return fail(ECLIP_E_INVALID_ARG, "no allowed size column");
+    if (gb) {
+        if (gb[0] != 0) return fail(ECLIP_E_INVALID_ARG, "group_bounds must start at 0");
+        sp.bounds.push_back(0);
+        for (int i = 1; sp.bounds.back() != K; i++) {
+            if (gb[i] <= sp.bounds.back() || gb[i] > K) return fail(ECLIP_E_INVALID_ARG, "group_bounds must ascend to %d", K);
+            sp.bounds.push_back(gb[i]);
+        }
+    } else {
+        for (int k = 0; k <= K; k++) sp.bounds.push_back(k);
+    }
+    eclip_session s;   // device, stream, arena
+    s.prof = P;
+    int rc = setup_device(&s, opt);
+    if (rc) return rc;
+    rc = build_tables(&s, std::vector<TableSpec>{sp});
+    if (rc) return rc;
+    const int L = s.tabL[0], G = (int)sp.bounds.size() - 1;
+    *n_levels = L;
+    if (n_groups) *n_groups = G;
+    if (L > cap) return cap == 0 ? ECLIP_OK : fail(ECLIP_E_INVALID_ARG, "cap %d < %d levels", cap, L);
+    std::vector<const void*> ptr(3);
+    CU(cudaMemcpyAsync(ptr.data(), s.tb.S, sizeof(void*), cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(ptr.data() + 1, s.tb.B, sizeof(void*), cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(ptr.data() + 2, s.tb.wit, sizeof(void*), cudaMemcpyDeviceToHost, s.st));
+    CU(cudaStreamSynchronize(s.st));
+    CU(cudaMemcpyAsync(S, ptr[0], 8 * (size_t)L, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(B, ptr[1], 8 * (size_t)L, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaMemcpyAsync(wit, ptr[2], (size_t)L * G, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaStreamSynchronize(s.st));
+    return ECLIP_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1248,6 +1303,7 @@ extern "C" int eclip_baseline_plan(const eclip_profiles* P, const eclip_problem*
     r->winner_index = ~0ull;
     r->candidates = 1;
     r->units_scored = 1;
+    r->candidates_evaluated = 0;
     for (int i = 0; i < 4; i++) r->exact_key[i] = 0;
     size_t off = 0;
     for (int w = 0; w < W; w++) {

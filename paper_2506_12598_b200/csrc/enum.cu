@@ -1363,7 +1363,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (wl == 0) ci = *(volatile unsigned*)&s_inc;
             incv = __uint_as_float(__shfl_sync(0xffffffffu, ci, 0));
             if (incv != bnd_of) { bnd = __fmul_ru(incv, bandf); bnd_of = incv; }
-            pend = __ballot_sync(0xffffffffu, lb <= bnd);
+            // spare lanes of the list's last batch (e >= lcnt) are masked out explicitly: with no
+            // incumbent yet bnd is +inf and their +inf filler bound would pass the comparison
+            pend = __ballot_sync(0xffffffffu, e < lcnt && lb <= bnd);
+            if (!pend && b0 + 32 >= lcnt) break;   // last batch and nothing of it is in the band
             if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
                 float mn = lb;
                 for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));

@@ -47,7 +47,7 @@ class Result(C.Structure):
                 ("model_switches", P(C.c_int32)), ("winner_levels", P(C.c_int32)), ("objective", C.c_double),
                 ("makespan_ns", C.c_double), ("power_w", C.c_double), ("energy_j", C.c_double),
                 ("throughput_rps", C.c_double), ("winner_index", C.c_uint64), ("candidates", C.c_uint64),
-                ("units_scored", C.c_uint64), ("exact_key", C.c_uint64 * 4)]
+                ("units_scored", C.c_uint64), ("candidates_evaluated", C.c_uint64), ("exact_key", C.c_uint64 * 4)]
 
 
 class Options(C.Structure):
@@ -77,7 +77,7 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
            "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats",
            "eclip_session_counters",
-           "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate"]
+           "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate", "eclip_level_table"]
 
 
 def lib():
@@ -115,6 +115,8 @@ def lib():
         L.eclip_baseline_plan.argtypes = [vp, P(Problem), C.c_int32, C.c_double, P(Options), P(Result)]
         L.eclip_lookup_table_json.argtypes = [vp, P(Problem), P(C.c_int32), C.c_char_p, C.c_size_t,
                                               P(C.c_size_t), P(C.c_uint64)]
+        L.eclip_level_table.argtypes = [vp, C.c_int32, P(C.c_int32), C.c_uint32, C.c_int32, P(Options), C.c_int32,
+                                        P(C.c_int64), P(C.c_int64), P(C.c_uint8), P(C.c_int32), P(C.c_int32)]
         _lib = L
     return _lib
 
@@ -219,6 +221,7 @@ class Plan:
     candidates: int
     units_scored: int
     exact_key: int
+    candidates_evaluated: int = 0
 
 
 def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True) -> Options:
@@ -287,7 +290,8 @@ def _to_plan(r: Result, bufs, G) -> Plan:
     key = sum(int(r.exact_key[i]) << (64 * i) for i in range(4))
     return Plan("ok" if r.status == OK else "infeasible", ENGINE_NAMES.get(r.engine_used, "?"), gsm, glat,
                 bufs["lat"].tolist(), bufs["sw"].tolist(), bufs["lv"].tolist(), r.objective, r.makespan_ns, r.power_w,
-                r.energy_j, r.throughput_rps, int(r.winner_index), int(r.candidates), int(r.units_scored), key)
+                r.energy_j, r.throughput_rps, int(r.winner_index), int(r.candidates), int(r.units_scored), key,
+                int(r.candidates_evaluated))
 
 
 def plan(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
@@ -309,6 +313,24 @@ def plan_problem(profiles: Profiles, p, **kw) -> Plan:
                 objective=p.objective, allowed_mask=p.allowed_mask, qos_ns=p.qos_ns,
                 slowdown_matrix=p.slowdown_matrix, group_bounds=p.group_bounds, p_idle_w=p.p_idle_w,
                 p_max_w=p.p_max_w, **kw)
+
+
+def level_table(profiles: Profiles, model: int, *, switch_max: int = 14, group_bounds=None, allowed_mask: int = 0,
+                device: int = 0):
+    """eclip_level_table: the K1 level table of one worker, built on the GPU -> (S [L] int64 SMs,
+    B [L] int64 ns, witness [L, G] uint8 size columns), levels in canonical rank order."""
+    gb = _np(group_bounds, np.int32) if group_bounds is not None else None
+    o = _options("auto", device)
+    L, G = C.c_int32(), C.c_int32()
+    _check(lib().eclip_level_table(profiles.handle, model, _ptr(gb, C.c_int32), allowed_mask, switch_max, C.byref(o),
+                                   0, None, None, None, C.byref(L), C.byref(G)))
+    S = np.zeros(L.value, np.int64)
+    B = np.zeros(L.value, np.int64)
+    wit = np.zeros((L.value, G.value), np.uint8)
+    _check(lib().eclip_level_table(profiles.handle, model, _ptr(gb, C.c_int32), allowed_mask, switch_max, C.byref(o),
+                                   L.value, _ptr(S, C.c_int64), _ptr(B, C.c_int64), _ptr(wit, C.c_uint8), C.byref(L),
+                                   C.byref(G)))
+    return S, B, wit
 
 
 BASELINES = {"all_max": 0, "model_wise": 1, "kernel_wise": 2}

@@ -61,6 +61,53 @@ def test_worked_examples_on_gpu():
             g = _gpu(p, engine)
             assert g.group_sm == case["expect_sizes"], (case["name"], engine)
             assert g.objective == pytest.approx(case["expect_J"] * 1000, rel=1e-12)
+            assert g.makespan_ns == pytest.approx(case["expect_makespan_us"] * 1000, rel=1e-12)
+            assert g.power_w == pytest.approx(case["expect_power_w"], rel=1e-12)
+            assert g.energy_j == pytest.approx(case["expect_energy_j"], rel=1e-12)
+            assert g.throughput_rps == pytest.approx(case["expect_throughput_rps"], rel=1e-12)
+
+
+# ---------------------------------------------------------------- K1 level tables, whole tables
+def _k1_vs_oracle(pr, models, m, R, gb=None, mask=0, label=""):
+    sizes = models[m].sizes
+    S, B, wit = ec.level_table(pr, m, switch_max=R, group_bounds=gb, allowed_mask=mask)
+    beta, n = oracle.group_tables(models[m].exec_ns, gb)
+    So, Bo, Wo = oracle.levels(beta, n, sizes, mask or (1 << len(sizes)) - 1, R)
+    assert np.array_equal(S, So), f"{label}: S"
+    assert np.array_equal(B, Bo), f"{label}: B*"
+    assert np.array_equal(wit, Wo), f"{label}: witnesses / rank order"
+    return len(S)
+
+
+def test_k1_level_tables_vs_oracle():
+    """K1 (the GPU's level-1 DP, suffix recurrence) == O-B's memoised forward recursion, table by
+    table: every attained CU-sum S, B*(S), the canonical witness and the rank order (SURVEY §8(c)
+    c6b).  Random shapes (groups of several kernels, masks, irregular sizes, R sweeps),
+    the C5 library at R = 14 and two C4 models (577 levels, 64 groups)."""
+    rng = np.random.default_rng(17)
+    for t in range(60):
+        G = int(rng.integers(1, 10))
+        Cn = int(rng.integers(1, 9))
+        sizes = synth.lattice_sizes(Cn, 148) if t % 3 else sorted(int(x) for x in rng.choice(np.arange(1, 60), Cn, replace=False))
+        K = G + int(rng.integers(0, 4))
+        mdl = synth.synthesize_model("k", ["uniform", "vgg", "bert", "shufflenet"][t % 4], K, sizes, 4000 + t)
+        pr = ec.Profiles.from_models([mdl])
+        gb = None
+        if K > G:
+            cut = sorted(int(x) for x in rng.choice(np.arange(1, K), size=G - 1, replace=False)) if G > 1 else []
+            gb = [0] + cut + [K]
+        mask = int(rng.integers(1, 1 << Cn)) if t % 2 else 0
+        R = int(rng.integers(0, 6))
+        _k1_vs_oracle(pr, [mdl], 0, R, gb, mask, f"random {t}")
+    models, _, _ = synth.make_c5(1)
+    pr = ec.Profiles.from_models(models)
+    for m in range(len(models)):
+        for R in (0, 3, 14):
+            _k1_vs_oracle(pr, models, m, R, label=f"C5 library {m} R={R}")
+    c4 = synth.make_c4()
+    pr4 = ec.Profiles.from_models(c4.models)
+    for m in (0, 1):
+        assert _k1_vs_oracle(pr4, c4.models, m, 14, label=f"C4 model {m}") == 577
 
 
 # ---------------------------------------------------------------- random tiny instances
@@ -189,28 +236,28 @@ def test_s6_full_vs_golden():
     _check_gold(_gpu(p, "slice"), rec, "S6 slice")
 
 
-def test_c5_batch_full_sampled_vs_golden():
-    """the bench configuration: 4096 mixes in one launch sequence; sampled mixes vs oracle"""
-    models, ids, qos = synth.make_c5(4096)
+@pytest.mark.parametrize("seed", [0, 1, 7])
+def test_c5_batch_every_mix_vs_oracle_golden(seed):
+    """the bench configuration: 4096 mixes in one launch sequence, EVERY mix against the oracle's
+    stored answer (tests/golden/c5_mixes.json: all 7^4 distinct mixes); seeds 0..7 are the
+    batches bench.py plans on ranks 0..7"""
+    import golden_c5
+    models, ids, qos = synth.make_c5(4096, seed=seed)
     pr = ec.Profiles.from_models(models)
     out = ec.plan_batch(pr, ids, total_sms=148, switch_max=14, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
-    gold = _gold()
-    for i in (0, 1, 2047, 4095):
-        rec = gold[f"C5_{i}"]
-        assert synth.problem_hash(synth.c5_problem(i, models, ids, qos)) == rec["hash"]
-        st = int(out["status"][i])
-        assert (st == 0) == (rec["status"] == "ok")
-        if st == 0:
-            assert out["winner_levels"][i].tolist() == rec["levels"]
-            assert int(out["winner_index"][i]) == rec["index"]
-            assert out["objective"][i] == pytest.approx(rec["objective"], rel=REL)
-            gsm = [out["group_sm"][i, w, :16].tolist() for w in range(4)]
-            assert gsm == rec["group_sm"]
-    # every mix: QoS met, budget met, sizes allowed
+    assert golden_c5.check_batch(ids, out, sizes=models[0].sizes) == 4096
+    # every mix: QoS met, budget met
     ok = out["status"] == 0
     assert ok.sum() > 0
     assert np.all(out["model_switches"][ok] <= 14)
     assert np.all(out["model_latency_ns"][ok] <= qos[ok] * (1 + 1e-12))
+    if seed == 0:   # the older per-record golden (oracle_full.json) agrees too
+        gold = _gold()
+        for i in (0, 1, 2047, 4095):
+            rec = gold[f"C5_{i}"]
+            assert synth.problem_hash(synth.c5_problem(i, models, ids, qos)) == rec["hash"]
+            if rec["status"] == "ok":
+                assert int(out["winner_index"][i]) == rec["index"]
 
 
 def test_c5_small_batch_each_mix_vs_oracle():
@@ -256,24 +303,30 @@ def _run_shards(make, n_shards):
 
 
 @pytest.mark.parametrize("n_shards", [2, 3, 8])
-def test_sharded_single_problem_equals_unsharded(n_shards):
-    for p, eng in ((synth.make_c2(), "enum"), (synth.make_c2(), "slice"), (synth.make_c3("matrix"), "enum"),
-                   (synth.make_c4(), "slice")):
+def test_sharded_single_problem_vs_oracle(n_shards):
+    """every shard materialises the oracle's plan (live oracle for C2, stored answers at full size)"""
+    gold = _gold()
+    cases = [(synth.make_c2(), "enum", oracle.solve(synth.make_c2())),
+             (synth.make_c2("paper", "energy"), "slice", oracle.solve(synth.make_c2("paper", "energy"))),
+             (synth.make_c3("matrix"), "enum", gold["C3"]), (synth.make_c4(), "slice", gold["C4"])]
+    for p, eng, o in cases:
         pr = ec.Profiles.from_models(p.models)
-        ref = ec.plan_problem(pr, p, engine=eng)
         outs = _run_shards(lambda k: ec.Session(pr, problem=p, shard=k, n_shards=n_shards, engine=eng), n_shards)
-        for o in outs:
-            assert o.winner_index == ref.winner_index and o.group_sm == ref.group_sm and o.exact_key == ref.exact_key
+        for g in outs:
+            if isinstance(o, dict):
+                _check_gold(g, o, f"{p.name} {eng} x{n_shards}")
+            else:
+                _same(g, o, f"{p.name} {eng} x{n_shards}")
 
 
-def test_sharded_batch_equals_unsharded():
-    models, ids, qos = synth.make_c5(16, seed=11)
+def test_sharded_batch_vs_oracle():
+    import golden_c5
+    models, ids, qos = synth.make_c5(64, seed=11)
     pr = ec.Profiles.from_models(models)
-    ref = ec.plan_batch(pr, ids, total_sms=148, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0)
     b = dict(model_ids=ids, qos_ns=qos, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
     outs = _run_shards(lambda k: ec.Session(pr, batch=b, shard=k, n_shards=3), 3)
     for o in outs:
-        assert np.array_equal(o["winner_index"], ref["winner_index"])
+        assert golden_c5.check_batch(ids, o) == 64
 
 
 # ---------------------------------------------------------------- more shapes
@@ -402,7 +455,7 @@ def test_overflow_fallbacks_with_tiny_list_capacities():
     if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(bld.LIB):
         bld.build_variant("tinycap", ["PL_CAP_N=1", "BAND_CAP_N=1"])
     env = dict(os.environ, ECLIP_LIB=lib)
-    sel = "pruned_equals_exhaustive or exact_ties or c5_small_batch or c5_batch_full or sharded"
+    sel = "pruned_equals_exhaustive or exact_ties or c5_small_batch or c5_batch_every or sharded"
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k", sel, "-p", "no:cacheprovider"],
                        env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

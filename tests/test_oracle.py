@@ -79,10 +79,18 @@ def test_worked_examples(idx):
     assert a is not None
     assert float(a["key"]) == pytest.approx(case["expect_J"] * 1000, rel=1e-12)    # us -> ns
     assert [[gold["sizes"][j] for j in s] for s in a["sigmas"]] == case["expect_sizes"]
+    # O-A's own values of the plan: makespan and power (hand values in the golden)
+    assert float(max(a["L"])) == pytest.approx(case["expect_makespan_us"] * 1000, rel=1e-12)
+    assert float(a["power"]) == pytest.approx(case["expect_power_w"], rel=1e-12)
     for engine in ("enum",) + (("slice",) if p.mode != "matrix" else ()):
         b = oracle.solve(p, engine)
         assert b.group_sm == case["expect_sizes"], engine
         assert b.objective == pytest.approx(case["expect_J"] * 1000, rel=1e-12)
+        # or_eval_f64's reported values against the hand values (units: ns, W, J, requests/s)
+        assert b.makespan_ns == pytest.approx(case["expect_makespan_us"] * 1000, rel=1e-12)
+        assert b.power_w == pytest.approx(case["expect_power_w"], rel=1e-12)
+        assert b.energy_j == pytest.approx(case["expect_energy_j"], rel=1e-12)
+        assert b.throughput_rps == pytest.approx(case["expect_throughput_rps"], rel=1e-12)
 
 
 def test_doubling_anecdote_two_and_three_workers():
@@ -215,6 +223,41 @@ def test_level_efficient_restriction_is_exact_for_sum_tau0():
     assert n > 100
 
 
+@pytest.mark.parametrize("mode", ["exclude_self", "paper", "excess", "matrix"])
+@pytest.mark.parametrize("objective", ["sum", "max", "energy"])
+def test_level_efficient_restriction_keeps_the_exact_minimum(mode, objective):
+    """App. A.1 for every slowdown mode, objective and QoS setting: the exact minimum over ALL
+    raw joint plans (O-A without the level reduction) equals the minimum over level-efficient
+    plans, and feasibility agrees.  (In MAX/ENERGY a raw minimiser need not be level-efficient —
+    a non-bottleneck worker may take a slower plan at the same CU-sum — so only the minimum and
+    the key of the reduced winner are compared; in SUM with tau = 0 the winners coincide.)"""
+    n = n_qos = 0
+    for s in range(60):
+        p = synth.random_tiny_problem(3000 + s, max_w=2, max_g=3, max_c=3)
+        p.mode, p.objective = mode, objective
+        if mode == "matrix" and p.slowdown_matrix is None:
+            rng = np.random.default_rng(s)
+            p.slowdown_matrix = rng.uniform(0.5, 1.5, size=(p.W, p.W)).astype(np.float32)
+            np.fill_diagonal(p.slowdown_matrix, 0.0)
+        if mode != "matrix":
+            p.slowdown_matrix = None
+        try:
+            raw = brute.brute_force(p, tol=0.0, level_efficient=False)
+        except ValueError:
+            continue
+        red = brute.brute_force(p, tol=0.0, level_efficient=True)
+        assert (raw is None) == (red is None), s
+        if raw is None:
+            continue
+        assert raw["min_key"] == red["min_key"], s
+        assert red["key"] == red["min_key"]
+        if objective == "sum":
+            assert raw["sigmas"] == red["sigmas"], s
+        n += 1
+        n_qos += p.qos_ns is not None
+    assert n >= 40 and n_qos >= 10
+
+
 def test_slice_equals_enum_random():
     """T'-slicing (App. A.2) == flat enumeration, exactly, on every linear-mode instance."""
     n = 0
@@ -331,3 +374,29 @@ def test_profile_errors():
         oracle.parse_profiles("not json\n")
     with pytest.raises(oracle.ProfileError, match="non-positive"):
         oracle.parse_profiles(good.replace("0, 4, 3, 2, 1", "0, 4, 3, 2, 0"))
+
+
+# ---------------------------------------------------------------- the stored C5 answers
+def test_c5_golden_table_is_the_live_oracle():
+    """tests/golden/c5_mixes.json (every distinct C5 mix, tools/gen_c5_golden.py) is current: the
+    library it was computed on hashes the same and sampled entries equal the live oracle."""
+    import golden_c5
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import gen_c5_golden
+    doc = golden_c5.load()
+    models, _, _ = synth.make_c5(1)
+    assert doc["library_hash"] == gen_c5_golden.library_hash(models), "stale golden: rerun tools/gen_c5_golden.py"
+    assert doc["n_mixes"] == 7 ** 4 == len(doc["answers"])
+    rng = np.random.default_rng(5)
+    solo = np.array([synth.qos_3x(models, [m])[0] for m in range(len(models))])
+    for _ in range(8):
+        ids = rng.integers(0, 7, size=(1, 4)).astype(np.int32)
+        r = oracle.solve(synth.c5_problem(0, models, ids, solo[ids]), "slice")
+        a = doc["answers"][",".join(map(str, ids[0]))]
+        assert a[0] == r.status
+        if r.status == "ok":
+            assert a[1] == r.levels and a[2] == r.index and int(a[3], 16) == r.key
+            assert float(a[4]) == r.objective
+            assert a[5] == "".join("%x" % c for row in r.group_cols for c in row)
+
