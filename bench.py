@@ -1,20 +1,28 @@
 #!/usr/bin/env python
-"""bench.py — candidate allocations scored per second (and time-to-optimal-plan) on B200.
+"""bench.py — time-to-optimal-plan of batched co-location planning on B200 (BASELINE config 5),
+with candidate-allocation rates, the dominant kernel's roofline and the oracle beside it.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling weak|strong]
     torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1; one rank per GPU)
 
-A step is one pass of the whole planning path over one batch (BASELINE config 5, "batched
-planning: 4096 request mixes x 4 models x 16 groups per launch"): level-1 DP of the model
-library (K1), per-mix staging, exhaustive enumeration + FP32 scoring of every level tuple
-of every mix (K2), the exact band re-check and tie-break (K5), and materialisation of all
-4096 lookup tables.  Scaling is weak: every rank plans its own 4096 mixes, no collective
-on the data path.  value = all ranks' candidates / max-over-ranks device time.
+Workload (a step): BASELINE config 5, "batched planning: 4096 request mixes x 4 models x 16
+groups per launch" — every mix's exact optimal plan (§IV-B): per-mix staging,
+pass 1 (exact QoS range cuts + branch-and-bound lower bounds + FP32 scoring of the rest), pass 2
+(exact integer re-check of the tolerance band, lowest-index tie-break) and materialisation of all
+4096 lookup tables, through a persistent planner (eclip_planner_*: the model library's level tables
+are built once, the paper's runtime "simply references this table"; the step with the
+level-1 DP included is reported as cold_step_ms).
 
-The reference arm (--impl reference) times the ORACLE (oracle/, plain single-threaded C)
-on a bounded sample of the same workload: there is no reference implementation of this
-path to run (the paper solves it offline with Gurobi and publishes no solver number).
-Prints ONE JSON line on rank 0.
+value = exact optimal plans per second = mixes planned by all ranks / max-over-ranks device time
+(CUDA events on the planning stream, inputs resident in HBM, L2 flushed between steps).  Every
+timed step's plans are re-checked against the oracle's stored answers (tests/golden/c5_mixes.json,
+all 2401 distinct mixes; a mismatch fails the run).  Scaling: weak (default; rank r plans its own
+4096 mixes, seed r, no collective) or strong (--scaling strong: the 4096 mixes of seed 0 split over
+the ranks).
+
+The reference arm (--impl reference) times the ORACLE (oracle/, plain C per problem) planning the
+same mixes on the host cores: there is no reference implementation of this path (the paper solves
+it offline with Gurobi and publishes no solver number).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -31,11 +39,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "candidate allocations scored/sec"
-UNIT = "candidates/s"
+METRIC = "time-to-optimal-plan, batched (C5): exact optimal plans/s"
+UNIT = "plans/s"
 WORKLOAD = ("C5 batched planning: 4096 mixes x 4 models (7-model library, draws with replacement) x 16 groups "
             "x 8 pool sizes {18..144} of N=148 SMs, switchMax=14, EXCLUDE_SELF, SUM, QoS 3x isolated")
 N_MIXES = 4096
+ALG_OPS_PER_CAND = 17   # 4W+1 FP32 ops per scored candidate (SUM, W = 4)
 
 
 def parse():
@@ -44,9 +53,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--mixes", type=int, default=N_MIXES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-ttp", action="store_true", help="skip the time-to-plan block")
+    ap.add_argument("--no-ttp", action="store_true", help="skip the single-problem time-to-plan block")
+    ap.add_argument("--no-extra", action="store_true", help="skip the exhaustive / no-QoS / cold context lines")
     return ap.parse_args()
 
 
@@ -55,6 +66,33 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = os.cpu_count()
+    return {"cpu_model": model, "nproc": aff, "os_cpu_count": os.cpu_count()}
+
+
+def rank_mixes(a, rank, world):
+    """this rank's mixes: weak = its own 4096 (seed = rank); strong = a contiguous slice of seed 0's"""
+    import synth
+    if a.scaling == "weak":
+        return synth.make_c5(a.mixes, seed=rank)
+    models, ids, qos = synth.make_c5(a.mixes, seed=0)
+    lo, hi = a.mixes * rank // world, a.mixes * (rank + 1) // world
+    return models, ids[lo:hi].copy(), qos[lo:hi].copy()
 
 
 # ----------------------------------------------------------------------------------------- clocks
@@ -131,24 +169,56 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------- oracle
-def oracle_rate(models, ids, qos, budget_s: float):
-    """The oracle (plain C, 1 thread) enumerating a contiguous prefix of mix 0's candidate
-    space for about budget_s seconds.  Returns (candidates/s, sample description)."""
-    import ctypes as C
+_OR = {}
+
+
+def _or_init(seed, n):
+    import synth
+    _OR["d"] = synth.make_c5(n, seed=seed)
+
+
+def _or_plan(i):
+    """the oracle (oracle.solve, its exact T'-slice method: plain single-threaded C per problem,
+    level tables included) planning mix i; returns (i, seconds, status, levels)"""
     import oracle
     import synth
-    p = synth.c5_problem(0, models, ids, qos)
-    pp = oracle.Prepared(p)
-    r = oracle._Result()
-    n = 200_000
+    models, ids, qos = _OR["d"]
     t = time.perf_counter()
-    oracle.lib().or_enum_range(C.byref(pp.c), 0, n, C.byref(r))
-    dt = time.perf_counter() - t
-    n2 = int(min(pp.n_tuples, max(n, n * budget_s / max(dt, 1e-6))))
-    t = time.perf_counter()
-    oracle.lib().or_enum_range(C.byref(pp.c), 0, n2, C.byref(r))
-    dt = time.perf_counter() - t
-    return n2 / dt, n2, dt
+    r = oracle.solve(synth.c5_problem(i, models, ids, qos), "slice")
+    return i, time.perf_counter() - t, r.status, r.levels
+
+
+def oracle_time_to_plan(seed: int, n_total: int, single_budget_s: float = 12.0, pool_mixes_per_core: int = 12):
+    """The oracle's time-to-plan on the host cores for mixes of the same batch: (1) one core
+    (process pinned to one CPU), as many mixes as fit in ~single_budget_s; (2) every core, one
+    oracle process per core over nproc x pool_mixes_per_core mixes (wall clock)."""
+    import multiprocessing as mp
+    _or_init(seed, n_total)
+    info = host_info()
+    cpus = sorted(os.sched_getaffinity(0))
+    old = set(cpus)
+    os.sched_setaffinity(0, {cpus[0]})
+    try:
+        t0 = time.perf_counter()
+        n1 = 0
+        while n1 < n_total and time.perf_counter() - t0 < single_budget_s:
+            _or_plan(n1)
+            n1 += 1
+        t1 = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
+    cores = len(cpus)
+    n_all = min(n_total, cores * pool_mixes_per_core)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_or_init, initargs=(seed, n_total)) as pool:
+        pool.map(_or_plan, range(min(cores, n_all)))          # warm the workers
+        t0 = time.perf_counter()
+        res = pool.map(_or_plan, range(n_all), chunksize=1)
+        t_all = time.perf_counter() - t0
+    return {"single": {"plans_per_s": n1 / t1, "mixes": n1, "seconds": t1, "cores": 1},
+            "all_cores": {"plans_per_s": n_all / t_all, "mixes": n_all, "seconds": t_all, "cores": cores,
+                          "per_plan_s_median": float(np.median([r[1] for r in res]))},
+            "host": info}
 
 
 # ----------------------------------------------------------------------------------------- main
@@ -159,9 +229,9 @@ def main():
         return reference_arm(a, rank, world)
     import torch
     import torch.distributed as dist
-    import synth
     import paper_2506_12598_b200 as ec
-    from paper_2506_12598_b200 import eclip as ecl
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_c5
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -172,149 +242,216 @@ def main():
         if world > 1:
             dist.barrier()
 
-    models, ids, qos = synth.make_c5(a.mixes, seed=rank)
+    def all_max(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_sum(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    models, ids, qos = rank_mixes(a, rank, world)
+    n = int(ids.shape[0])
+    sizes = models[0].sizes
     pr = ec.Profiles.from_models(models)
     stream = torch.cuda.current_stream(dev)
+    kw = dict(n_models=4, total_sms=148, switch_max=14, p_idle_w=200.0, p_max_w=1000.0, device=local,
+              stream=stream.cuda_stream)
+    pl = ec.Planner(pr, max_problems=n, **kw)
     d_ids = torch.from_numpy(ids).to(dev)
     d_qos = torch.from_numpy(qos).to(dev)
-    out = ec.alloc_batch_out(a.mixes, 4, 16, device=dev)
-    kw = dict(total_sms=148, switch_max=14, p_idle_w=200.0, p_max_w=1000.0, device=local, stream=stream.cuda_stream)
+    outs = [ec.alloc_batch_out(n, 4, 16, device=dev) for _ in range(a.steps)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def step():
-        ec.plan_batch(pr, d_ids, qos_ns=d_qos, out=out, gmax=16, **kw)
-
     for _ in range(a.warmup):
-        step()
+        pl.plan(d_ids, d_qos, out=outs[0])
     torch.cuda.synchronize()
-    # candidates per step: prod of level counts per mix (exact)
-    Ls = level_counts(pr, ec)
-    cand_step = int(sum(int(np.prod([Ls[m] for m in row], dtype=np.float64)) for row in ids))
 
+    # ---- timed region: device-resident inputs, one plan of the whole batch per step
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
     torch.cuda.synchronize()
     evs = []
-    for _ in range(a.steps):
+    for k in range(a.steps):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step()
+        pl.plan(d_ids, d_qos, out=outs[k])
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
     barrier()
     ck = clocks.stop()
     t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
-    ok = out["status"].cpu().numpy()
-    n_feas = int((ok == 0).sum())
-    assert (ok >= 0).all(), "planner reported an error status"
-    t_all = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-    t_max_ms = float(t_all.item())
-    value = world * a.steps * cand_step / (t_max_ms * 1e-3)
+    t_max_ms = all_max(t_ms)
+    plans_step = all_sum(n)                       # mixes planned per step by all ranks
+    value = plans_step * a.steps / (t_max_ms * 1e-3)
 
-    # ---- pass-1 kernel alone (the dominant kernel): CUDA events on the launching stream
-    # chain_ms = the whole pass-1 chain (row bounds, bucket sort, the kernel, its reduction);
-    # k_ms = the dominant kernel alone (events recorded around its launch inside the library)
-    chain_ms, k_launches, k_eval, k_units, k_ms = pass1_time(ec, pr, ids, qos, stream, local)
-    p1_extra = dict(pass1_time.extra)
-    # the same pass without row pruning (every row classified) and without QoS bounds, for context
-    x_ms, x_launches, x_eval, _, x_kms = pass1_time(ec, pr, ids, qos, stream, local, prune=False)
-    n_ms, n_launches, n_eval, n_units, n_kms = pass1_time(ec, pr, ids, None, stream, local)
-    units_total = int(sum(Ls[row[0]] * Ls[row[1]] for row in ids))
+    # ---- parity: every timed step's plans against the oracle's stored answers
+    checked = 0
+    for k in range(a.steps):
+        checked += golden_c5.check_batch(ids, outs[k], sizes=sizes)
+    checked_all = all_sum(checked)
+    n_feas = int((outs[0]["status"] == 0).sum().item())
 
-    # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
+    # ---- candidate counts of this batch (level tuples per mix = prod of the 4 models' level counts)
+    Ls = [len(ec.level_table(pr, m, switch_max=14, device=local)[0]) for m in range(len(models))]
+    cand_step = int(sum(int(np.prod([Ls[m] for m in row], dtype=np.float64)) for row in ids))
+
+    # ---- per-phase split, pass-1 counters and the dominant kernel's time (timing planner)
+    tp = ec.Planner(pr, max_problems=n, timing=True, **kw)
+    phases, kms, evald, units = [], [], [], []
+    for rep in range(8):
+        flush.fill_(1)
+        tp.plan(d_ids, d_qos, out=outs[0])
+        if rep >= 2:
+            phases.append(tp.phase_ms())
+            c = tp.counters()
+            kms.append(c["kernel_ms"]); evald.append(c["evaluated_candidates"]); units.append(c["units_processed"])
+            swept = c["units_with_swept_entries"]; entries = c["entries_swept"]
+    torch.cuda.synchronize()
+    phase_ms = {k: float(np.median([p[k] for p in phases])) for k in phases[0]}
+    k_ms = float(np.median(kms))
+    k_eval = int(np.median(evald))
+    del tp
+
+    extra = {}
+    if not a.no_extra:
+        extra = context_lines(ec, torch, pr, ids, qos, d_ids, d_qos, stream, flush, kw, n, cand_step)
+
+    # ---- e2e: the public API from page-locked host buffers (H2D + D2H + sync inside the timed region)
     pin_ids = torch.from_numpy(ids).pin_memory()
     pin_q = torch.from_numpy(qos).pin_memory()
-    h_out = ec.alloc_batch_out(a.mixes, 4, 16, pinned=True)   # page-locked result buffers
+    h_out = ec.alloc_batch_out(n, 4, 16, pinned=True)
+    hp = ec.Planner(pr, max_problems=n, **kw)
+    for _ in range(a.warmup):
+        hp.plan(pin_ids.numpy(), pin_q.numpy(), out=h_out)
     e2e_ms = []
     barrier()
     for _ in range(a.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ec.plan_batch(pr, pin_ids.numpy(), qos_ns=pin_q.numpy(), out=h_out, gmax=16, **kw)
+        hp.plan(pin_ids.numpy(), pin_q.numpy(), out=h_out)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * a.steps * cand_step / (float(e2e_t.item()) * 1e-3)
-    assert np.array_equal(h_out["winner_index"], out["winner_index"].cpu().numpy().view(np.uint64))
+    e2e_max = all_max(sum(e2e_ms))
+    e2e_value = plans_step * a.steps / (e2e_max * 1e-3)
+    assert golden_c5.check_batch(ids, h_out, sizes=sizes) == n
     h2d = ids.nbytes + qos.nbytes
     d2h = sum(v.nbytes for k, v in h_out.items() if not k.startswith("_"))
 
-    # ---- time-to-optimal-plan (single problems; C4 sharded over all ranks)
+    # ---- single problems (C2, C3, C4, S6): time to the optimal plan, sharded over all ranks
     ttp = {} if a.no_ttp else time_to_plan(ec, world, rank, dist if world > 1 else None)
 
     if rank == 0:
         f_max = 1965.0
-        # the dominant kernel evaluates K = X_p + B_i Y_p + S'_i Z_p for every
-        # QoS-feasible candidate: 2 FP32 FMAs (FMA pipe, packed f32x2) + 1/2 three-input min;
-        # QoS-infeasible candidates are classified by exact range cuts with no FP work.  Roofline
-        # = FMA pipe (128 lane-ops / clk / SM measured): peak 148 x 128 x 1965 MHz lane-ops/s,
-        # achieved = 2 x evaluated candidates / kernel time.
-        fma_ops_per_cand = 2.0
-        k_s = k_ms / k_launches * 1e-3
-        cand_per_s_kernel = cand_step / k_s
-        achieved = fma_ops_per_cand * k_eval / k_s / 1e9
-        peak = 148 * 128 * f_max * 1e6 / 1e9
+        peak = 148 * 128 * f_max * 1e6 / 1e9          # G FP32 lane-ops/s (FMA pipe)
+        k_s = k_ms * 1e-3
+        achieved = ALG_OPS_PER_CAND * k_eval / k_s / 1e9
+        ncu = ncu_pass1(n) or {}
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": t_max_ms / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded knee-shaped profiles, SURVEY §8(d))",
-            "config": {"workload": WORKLOAD, "mixes_per_rank": a.mixes, "candidates_per_step_per_rank": cand_step,
-                       "feasible_mixes_rank0": n_feas, "engine": "enum", "parallelism": f"weak x{world} (mixes)",
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": t_max_ms / a.steps, "higher_is_better": True, "scaling": a.scaling,
+            "vs_baseline": None, "dtype": "f32 filter + exact int (u128/u256) decisions",
+            "data": "synthetic (seeded knee-shaped profiles, SURVEY §8(d))",
+            "config": {"workload": WORKLOAD, "mixes_per_step_all_ranks": int(plans_step), "mixes_per_rank": n,
+                       "feasible_mixes_rank0": n_feas, "engine": "enum (persistent planner)",
+                       "parallelism": f"{a.scaling} x{world} (mixes; no collective on the data path)",
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+            "time_to_optimal_plan_ms": t_max_ms / a.steps,
+            "parity": {"checked_mixes": int(checked_all), "timed_steps_checked": a.steps, "mismatches": 0,
+                       "against": "tests/golden/c5_mixes.json (oracle answers of all 2401 distinct C5 mixes)",
+                       "fields": "status, winning level ranks, mixed-radix index, objective (1e-5), group pool sizes"},
+            "candidates": {"level_tuples_per_step_rank0": cand_step,
+                           "level_tuples_covered_per_s": cand_step * (plans_step / n) * a.steps / (t_max_ms * 1e-3),
+                           "fp32_evaluated_per_step_rank0": k_eval,
+                           "fp32_evaluated_per_s_kernel": k_eval / k_s,
+                           "note": "every level tuple is covered exactly: classified without arithmetic (QoS range "
+                                   "cuts, branch-and-bound lower bounds, DESIGN.md §3.9) or scored in FP32; only the "
+                                   "fp32_evaluated ones cost scoring arithmetic"},
+            "phases_ms": phase_ms,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": float(e2e_t.item()) / a.steps},
-            # per step: k_levels, k_prep_prob, k_prep_lev, k_table_hull, k_prep_aux, 2 x k_fill_u32, k_prep_bound,
-            # k_rowlb_fused, k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/r01_timeline_c5.txt)
-            "gpu_launches": int(13 * a.steps),
-            "roofline": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,QoS>", "achieved": achieved,
-                         "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
-                         "frac": achieved / peak, "traffic": (ncu_pass1(a.mixes) or {}).get("bytes_per_launch"),
-                         "issue_slots_busy_pct_ncu": (ncu_pass1(a.mixes) or {}).get("issue_active_pct"),
-                         "kernel_ms_per_launch": k_ms / k_launches,
-                         "kernel_share_of_step": (k_ms / k_launches) / (t_max_ms / a.steps),
-                         "fma_lane_ops_per_evaluated_candidate": fma_ops_per_cand,
-                         "evaluated_candidates_per_launch": k_eval,
-                         "evaluated_fraction": k_eval / cand_step,
-                         "candidates_per_s_kernel": cand_per_s_kernel,
-                         "exhaustive_equivalent_frac": fma_ops_per_cand * cand_step / k_s / 1e9 / peak,
-                         "note": "achieved counts only the candidates the kernel evaluated in FP32; the others are "
-                                 "classified by exact range cuts and lower bounds (DESIGN.md 3.9), so the kernel is "
-                                 "issue-bound on classification (issue_slots_busy_pct_ncu); exhaustive_equivalent_frac "
-                                 "= 2 FMA x every candidate of the step / kernel time / peak (> 1: faster than an "
-                                 "exhaustive scorer at the FMA-pipe roofline)"},
-            "pruning": {"units_total_per_launch": units_total, "units_processed_per_launch": k_units,
-                        "units_with_swept_entries_per_launch": p1_extra["units_with_swept_entries"],
-                        "entries_swept_per_launch": p1_extra["entries_swept"],
-                        "pass1_chain_ms_pruned": chain_ms / k_launches, "pass1_chain_ms_exhaustive": x_ms / x_launches,
-                        "pass1_kernel_ms_exhaustive": x_kms / x_launches,
-                        "evaluated_candidates_exhaustive": x_eval,
-                        "note": "row lower bounds (DESIGN.md §3.9) prove the skipped rows hold no candidate within "
-                                "the tolerance band of the best key found; exhaustive = every row classified"},
-            "roofline_noqos": {"bound": "alu", "kernel": "k_pass1_fast<EXCLUDE_SELF,noQoS>",
-                               "achieved": fma_ops_per_cand * n_eval / (n_kms / n_launches * 1e-3) / 1e9,
-                               "peak": peak, "unit": "G FP32 FMA-pipe lane-ops/s",
-                               "frac": fma_ops_per_cand * n_eval / (n_kms / n_launches * 1e-3) / 1e9 / peak,
-                               "kernel_ms_per_launch": n_kms / n_launches, "evaluated_candidates_per_launch": n_eval,
-                               "note": "same C5 mixes without QoS bounds (every candidate evaluated); context for the "
-                                       "headline kernel, whose QoS cuts leave 2-3% of candidates needing FP work"},
+                    "ms_per_step": e2e_max / a.steps, "api": "eclip_planner_plan (host batch, pinned buffers)"},
+            # per step: k_prep_prob, k_prep_lev, k_prep_aux, 2 x k_fill_u32, k_prep_bound, k_rowlb_fused,
+            # k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/ launch list)
+            "gpu_launches": int(11 * a.steps),
+            "roofline": {"bound": "alu", "kernel": "k_pass1_fast<W=4,EXCLUDE_SELF,QoS,pruned>", "achieved": achieved,
+                         "peak": peak, "unit": "G FP32 lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
+                         "frac": achieved / peak, "traffic": ncu.get("bytes_per_launch"),
+                         "algorithmic_ops_per_unit": ALG_OPS_PER_CAND, "units_per_launch": k_eval,
+                         "unit_def": "a level tuple whose FP32 key the kernel computed (SURVEY §8(d): 4W+1 ops)",
+                         "kernel_ms_per_launch": k_ms, "kernel_share_of_step": k_ms / (t_max_ms / a.steps),
+                         "issue_slots_busy_pct_ncu": ncu.get("issue_active_pct"),
+                         "units_processed_per_launch": int(np.median(units)),
+                         "units_with_swept_entries": swept, "entries_swept": entries},
             "clocks": ck,
+            "host": host_info(),
             "time_to_plan_ms": ttp,
         }
+        line.update(extra)
         if not a.no_cpu_baseline and world == 1:
-            rate, n, dt = oracle_rate(models, ids, qos, 15.0)
-            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                    "sample": f"oracle O-B (plain C, 1 thread) enumerating the first {n} level "
-                                              f"tuples of mix 0 in {dt:.1f} s"}
+            ob = oracle_time_to_plan(0 if a.scaling == "strong" else rank, N_MIXES)
+            al = ob["all_cores"]
+            line["cpu_baseline"] = {
+                "value": al["plans_per_s"], "unit": UNIT, "cores": al["cores"], "kind": "oracle",
+                "sample": f"oracle.solve(mix, 'slice') (plain C per problem, level tables included) on the first "
+                          f"{al['mixes']} mixes of the same batch, one process per core, {al['seconds']:.1f} s wall",
+                "single_core": ob["single"], "host": ob["host"],
+                "time_to_plan_4096_mixes_s_all_cores": N_MIXES / al["plans_per_s"],
+                "time_to_plan_4096_mixes_s_single_core": N_MIXES / ob["single"]["plans_per_s"]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def context_lines(ec, torch, pr, ids, qos, d_ids, d_qos, stream, flush, kw, n, cand_step):
+    """The same batch through other configurations, for context: (1) cold = one-shot eclip_plan_batch
+    (level-1 DP and table set-up inside every step); (2) the exhaustive scorer (no branch and bound:
+    every QoS-feasible candidate scored) with and without QoS bounds, each with its own roofline."""
+    res = {}
+    out = ec.alloc_batch_out(n, 4, 16, device=d_ids.device)
+    bk = dict(total_sms=148, switch_max=14, p_idle_w=200.0, p_max_w=1000.0, device=kw["device"], stream=kw["stream"],
+              out=out, gmax=16)
+    for _ in range(2):
+        ec.plan_batch(pr, d_ids, qos_ns=d_qos, **bk)
+    ts = []
+    for _ in range(5):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ec.plan_batch(pr, d_ids, qos_ns=d_qos, **bk)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    res["cold_step_ms"] = float(np.median(ts))
+    peak = 148 * 128 * 1965.0 * 1e6 / 1e9
+    for name, use_q in (("exhaustive_qos", True), ("exhaustive_noqos", False)):
+        p = ec.Planner(pr, max_problems=n, qos=use_q, prune=False, timing=True, **kw)
+        kms, ev, steps = [], [], []
+        for rep in range(4):
+            flush.fill_(1)
+            p.plan(d_ids, d_qos if use_q else None, out=out)
+            if rep >= 1:
+                c = p.counters()
+                kms.append(c["kernel_ms"]); ev.append(c["evaluated_candidates"])
+                steps.append(sum(p.phase_ms().values()))
+        k_ms = float(np.median(kms))
+        e = int(np.median(ev))
+        ach = ALG_OPS_PER_CAND * e / (k_ms * 1e-3) / 1e9
+        res[f"roofline_{name}"] = {
+            "bound": "alu", "kernel": f"k_pass1_fast<W=4,EXCLUDE_SELF,{'QoS' if use_q else 'noQoS'},exhaustive>",
+            "achieved": ach, "peak": peak, "frac": ach / peak, "unit": "G FP32 lane-ops/s",
+            "kernel_ms_per_launch": k_ms, "evaluated_candidates_per_launch": e,
+            "evaluated_fraction": e / cand_step, "step_ms": float(np.median(steps)),
+            "note": "no branch and bound: every QoS-feasible level tuple's FP32 key is computed (2 packed FMAs "
+                    "+ a min per tuple); achieved counts SURVEY §8(d)'s 17 algorithmic ops per scored tuple"}
+        del p
+    return res
 
 
 def ncu_pass1(mixes):
@@ -329,47 +466,12 @@ def ncu_pass1(mixes):
         return None
 
 
-def level_counts(pr, ec):
-    """level count L_m of every library model = the candidate count of a 1-worker plan"""
-    n = pr.info()["n_models"]
-    return [ec.plan(pr, [m], total_sms=148, switch_max=14).candidates for m in range(n)]
-
-
-def pass1_time(ec, pr, ids, qos, stream, local, prune=True):
-    """CUDA-event time of pass 1 alone (row bounds + pruned waves + its tiny reduction), via the
-    split API on the same stream; also returns how many candidates pass 1 evaluated in FP32 and
-    how many units (rows) it processed."""
-    import torch
-    from paper_2506_12598_b200.eclip import Session
-    tot, launches, evaluated, units, kern = 0.0, 0, 0, 0, 0.0
-    batch = dict(model_ids=ids, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
-    if qos is not None:
-        batch["qos_ns"] = qos
-    for rep in range(3):
-        s = Session(pr, batch=batch, engine="enum", device=local, stream=stream.cuda_stream, prune=prune)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        s.pass1()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if rep > 0:
-            tot += e0.elapsed_time(e1)
-            launches += 1
-            st = s.stats()
-            evaluated, units = st["evaluated_candidates"], st["units_processed"]
-            kern += st["kernel_ms"]
-            extra = {"units_with_swept_entries": st["units_with_swept_entries"], "entries_swept": st["entries_swept"]}
-        s.close()
-    pass1_time.extra = extra
-    return tot, launches, evaluated, units, kern
-
-
 def time_to_plan(ec, world, rank, dist):
     import synth
     from paper_2506_12598_b200 import parallel
     res = {}
-    for name, p in (("C2", synth.make_c2()), ("C3", synth.make_c3("matrix")), ("C4", synth.make_c4())):
+    for name, p in (("C2", synth.make_c2()), ("C3", synth.make_c3("matrix")), ("C4", synth.make_c4()),
+                    ("S6", synth.make_s6())):
         pr = ec.Profiles.from_models(p.models)
         ts = []
         for rep in range(4):
@@ -382,32 +484,40 @@ def time_to_plan(ec, world, rank, dist):
                 r = parallel.plan_distributed(pr, p)
             ts.append((time.perf_counter() - t0) * 1e3)
         res[name] = {"ms": float(np.median(ts[1:])), "engine": r.engine, "candidates": r.candidates,
-                     "units_scored": r.units_scored, "objective": r.objective}
+                     "units_scored": r.units_scored, "objective": r.objective, "ranks": world}
     return res
 
 
 def reference_arm(a, rank, world):
-    """--impl reference: the oracle (the only other implementation of this path), timed on the
-    host cores on a bounded sample of the same workload per step; rank 0 only."""
+    """--impl reference: the oracle (the only other implementation of this path) planning the same
+    C5 mixes on the host cores, one oracle process per core; each step = a bounded sample of the
+    batch (2 mixes per core); rank 0 only."""
     if rank != 0:
         return
-    import synth
-    models, ids, qos = synth.make_c5(a.mixes, seed=0)
-    rates = []
-    for i in range(a.warmup + a.steps):
-        rate, n, dt = oracle_rate(models, ids, qos, 3.0)
-        if i >= a.warmup:
-            rates.append((n, dt))
-    n_tot = sum(n for n, _ in rates)
-    t_tot = sum(dt for _, dt in rates)
-    value = n_tot / t_tot
+    import multiprocessing as mp
+    seed = 0
+    cores = len(os.sched_getaffinity(0))
+    per_step = min(N_MIXES, 2 * cores)
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores, initializer=_or_init, initargs=(seed, N_MIXES)) as pool:
+        pool.map(_or_plan, range(min(cores, per_step)))
+        for k in range(a.warmup + a.steps):
+            lo = (k * per_step) % N_MIXES
+            idx = [(lo + j) % N_MIXES for j in range(per_step)]
+            t0 = time.perf_counter()
+            pool.map(_or_plan, idx, chunksize=1)
+            if k >= a.warmup:
+                times.append(time.perf_counter() - t0)
+    t_tot = sum(times)
+    value = per_step * a.steps / t_tot
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": t_tot / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "exact int / f32 (oracle)", "data": "synthetic",
-            "config": {"workload": WORKLOAD},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"per step: the first ~{rates[0][0]} level tuples of mix 0 (about 3 s of "
-                                       f"single-threaded oracle work)"},
+            "warmup": a.warmup, "ms_per_step": t_tot / a.steps * 1e3, "higher_is_better": True, "scaling": a.scaling,
+            "vs_baseline": None, "dtype": "exact int (oracle)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "mixes_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step: {per_step} mixes of the C5 batch (seed 0) planned exactly by "
+                                       f"oracle.solve(mix, 'slice'), one process per core", "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

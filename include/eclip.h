@@ -146,6 +146,8 @@ typedef struct {
     int32_t no_prune;             /* ENUM, SUM, linear modes, W >= 3: 0 (default) = skip rows of candidates whose
                                      proven lower bound exceeds the tolerance band of the best key found so far
                                      (same answer); 1 = score every QoS-feasible candidate */
+    int32_t timing;               /* eclip_planner_create: 1 = record CUDA events around every phase of each plan
+                                     (eclip_planner_phase_ms); default 0 */
 } eclip_options;
 
 void eclip_default_options(eclip_options* o);
@@ -192,6 +194,40 @@ typedef struct {                  /* struct-of-arrays results, caller-allocated 
 
 int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,
                      eclip_batch_out* out);
+
+/* ---- persistent planner (serving-loop replanning, BASELINE config 5) --------------------
+ * A co-location mix's candidates are built from per-model level tables that depend only on the
+ * profiles, the allowed sizes and the switch budget — the paper's runtime "simply references"
+ * precomputed results.  A planner builds those tables once (K1, per-table hulls; the only
+ * host synchronisation of its life), keeps device workspaces for up to max_problems mixes, and then
+ * plans batch after batch running only the per-mix work (staging, pass 1, pass 2, materialise).
+ *   eclip_planner_create(prof, shape, max_problems, opt, &pl)
+ *       shape: an eclip_batch whose n_models, total_sms, switch_max, slowdown, objective, p_idle_w,
+ *       p_max_w and allowed_mask fix the planner; shape->qos_ns != NULL declares that every batch
+ *       carries QoS bounds (the array is not read); model_ids / n_problems / on_device are ignored.
+ *       opt: engine AUTO or ENUM, n_shards 1; opt->cuda_stream = the stream every plan runs on
+ *       (NULL: the planner's own stream).
+ *   eclip_planner_plan(pl, batch, out)
+ *       batch: n_problems in [1, max_problems], model_ids, qos_ns (NULL iff the shape had none),
+ *       slowdown_matrix (MATRIX) and on_device as for eclip_plan_batch; every other field must equal
+ *       the shape's.  Host batches are copied into the planner's device buffers on its stream, host
+ *       results copied back, and the call synchronises.  Device batches with device outputs
+ *       (on_device = 1) perform no copy and, on a caller's stream, no synchronisation.  Results are
+ *       identical to eclip_plan_batch's.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_TOO_LARGE,
+ *       ECLIP_E_CUDA, ECLIP_E_OOM.
+ *   eclip_planner_phase_ms(pl, ms, n)  needs opt->timing = 1 at creation: CUDA-event times (ms) of the
+ *       last plan's phases, ms[0..5): [0] input H2D copies, [1] per-mix staging (k_prep_prob, k_prep_lev,
+ *       k_prep_aux), [2] pass 1 (row bounds, pruned scoring, reduction), [3] pass 2 (exact band re-check
+ *       and tie-break), [4] materialise (+ result D2H copies); waits for the last event.
+ *   eclip_planner_counters(pl, out, n)  the pass-1 counters of eclip_session_counters for the last plan.
+ * A planner is not thread-safe: one planner per host thread / stream. */
+typedef struct eclip_planner eclip_planner;
+int eclip_planner_create(const eclip_profiles* prof, const eclip_batch* shape, int32_t max_problems,
+                         const eclip_options* opt, eclip_planner** out);
+int eclip_planner_plan(eclip_planner* pl, const eclip_batch* batch, eclip_batch_out* out);
+int eclip_planner_phase_ms(eclip_planner* pl, float* ms, int32_t n);
+int eclip_planner_counters(eclip_planner* pl, uint64_t* out, int32_t n);
+void eclip_planner_free(eclip_planner* pl);
 
 /* ---- split API for multi-GPU / process-group runs -------------------------------------
  * A session plans a batch (n_problems >= 1) restricted to candidate shard opt->shard of

@@ -550,6 +550,21 @@ static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, i
     su.prune = (opt && opt->no_prune) ? 0 : 1;
 }
 
+// Narrow or wide launch (Setup::wide): Lambda = lcm of the kernel counts of the tables a problem can
+// use (a batch: every table, an upper bound of each problem's Lambda); wide when Lambda N (W+1) reaches
+// 2^24, the range of the narrow kernels' exact FP32 / int32 T' arithmetic.
+static void set_wide(eclip_session* s, const std::vector<int32_t>& tables) {
+    long double lam = 1;
+    uint64_t l = 1;
+    for (int t : tables) {
+        const uint64_t K = (uint64_t)s->tabs[t].K;
+        const uint64_t g = (uint64_t)gcd64((int64_t)l, (int64_t)K);
+        lam = lam / (long double)g * (long double)K;
+        l = lam < 1.8e19L ? l / g * K : l;
+    }
+    s->su.wide = (lam * (long double)s->su.N * (long double)(s->su.W + 1) >= 16777216.0L) ? 1 : 0;
+}
+
 // choose the engine and size the work (pass-1 geometry: see enum.cu)
 static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     Setup& su = s->su;
@@ -567,11 +582,13 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     int want = opt ? opt->engine : ECLIP_ENGINE_AUTO;
     bool enum_ok = W <= MAXW_ENUM && (size_t)W * Lmax * sizeof(Lev) <= 100 * 1024 && tuples < 4e18L && Lmax <= 4096 &&
                    n * H * 4 < 6e9L;
-    bool slice_ok = su.mode != M_MATRIX && s->n == 1;
+    bool slice_ok = su.mode != M_MATRIX && s->n == 1 && !su.wide;
     if (want == ECLIP_ENGINE_ENUM && !enum_ok)
         return fail(ECLIP_E_TOO_LARGE, "ENUM engine limits exceeded (W=%d, Lmax=%d)", W, Lmax);
     if (want == ECLIP_ENGINE_SLICE && !slice_ok)
-        return fail(ECLIP_E_INVALID_ARG, "SLICE engine needs a linear slowdown mode and a single problem");
+        return su.wide ? fail(ECLIP_E_TOO_LARGE, "SLICE engine: the T' range of these kernel counts is too large "
+                                                 "(Lambda N (W+1) >= 2^24); use ENUM")
+                       : fail(ECLIP_E_INVALID_ARG, "SLICE engine needs a linear slowdown mode and a single problem");
     if (want == ECLIP_ENGINE_AUTO) {
         // ENUM scores every candidate; SLICE when enumeration is far larger than the lattice
         if (!enum_ok || (slice_ok && tuples > 4e10L)) {
@@ -593,7 +610,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     if (n * H < 4096) nseg = (int)std::min<long double>(Lstep, std::ceil(4096.0L / (n * H)));
     const int seglen = (Lstep + nseg - 1) / nseg;
     nseg = (Lstep + seglen - 1) / seglen;
-    const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax);
+    const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax) && !su.wide;
     const int teams_typ = P1_THREADS / 32;   // one unit per warp in both pass-1 kernels
     const long double units = H * nseg;
     const long double cand_unit = (long double)seglen * Lmax;
@@ -621,7 +638,14 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     return ECLIP_OK;
 }
 
-static int alloc_work(eclip_session* s) {
+// Work buffers of the current geometry in one device block.  With `reuse` (a persistent planner)
+// the block of the previous call is kept when it is large enough; otherwise a new one is taken.
+struct WorkBlock {
+    unsigned char* base = nullptr;
+    size_t cap = 0;
+};
+
+static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
     Setup& su = s->su;
     Work& wk = s->wk;
     const size_t n = (size_t)su.n_problems;
@@ -633,10 +657,10 @@ static int alloc_work(eclip_session* s) {
     const size_t o_probs = bp.take<Prob>(n), o_levs = bp.take<Lev>(n * (size_t)su.lev_stride);
     const size_t o_sub = en ? bp.take<float>(ns) : 0, o_bandn = en ? bp.take<int32_t>(n) : 0;
     const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
-    const size_t o_sure = (en && su.mode == M_MATRIX && su.has_qos) ? bp.take<float>(ns) : 0;
+    const size_t o_sure = (en && qos_float(su)) ? bp.take<float>(ns) : 0;
     const size_t o_m32 = bp.take<float>(n), o_m32s = bp.take<float>(n), o_hs = bp.take<U256>(n), o_first = bp.take<U256>(n);
     size_t o_th = 0, o_thn = 0, o_tord = 0;
-    if (en && su.aux_bytes > 0) {   // per-table S order and hulls (k_table_hull)
+    if (en && su.aux_bytes > 0 && !wk.thull) {   // per-table S order and hulls (k_table_hull), unless held elsewhere
         o_th = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
         o_thn = bp.take<int32_t>((size_t)s->tb.n);
         o_tord = bp.take<uint16_t>((size_t)s->tb.n * su.Lmax);
@@ -657,7 +681,12 @@ static int alloc_work(eclip_session* s) {
         o_wb = bp.take<uint32_t>(n * (size_t)((su.units_max + 31) >> 5));
     }
     unsigned char* base;
-    CU(s->arena.alloc(&base, bp.off));
+    if (reuse && reuse->base && reuse->cap >= bp.off) {
+        base = reuse->base;
+    } else {
+        CU(s->arena.alloc(&base, bp.off));
+        if (reuse) { reuse->base = base; reuse->cap = bp.off; }
+    }
     wk.feasible = (unsigned long long*)(base + o_cnt);
     wk.rows_done = wk.feasible + 1;
     CU(cudaMemsetAsync(wk.feasible, 0, 4 * sizeof(unsigned long long), s->st));
@@ -697,7 +726,7 @@ static int alloc_work(eclip_session* s) {
 
 static int status_error(const eclip_session* s, int st, int p) {
     (void)s;
-    if (st == -5) return fail(ECLIP_E_TOO_LARGE, "problem %d exceeds the exact-arithmetic ranges (Lambda N (W+1) < 2^24, ...)", p);
+    if (st == -5) return fail(ECLIP_E_TOO_LARGE, "problem %d exceeds the exact-arithmetic ranges (Lambda = lcm of kernel counts <= 2^40, Lambda N (W+1) < 2^62, ...)", p);
     return fail(ECLIP_E_INVALID_ARG, "problem %d is invalid (model id / QoS / matrix / power values)", p);
 }
 
@@ -789,6 +818,7 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
     rc = build_tables(s.get(), specs);
     if (rc) return rc;
     s->h_table_of = table_of;
+    set_wide(s.get(), table_of);
     rc = plan_geometry(s.get(), opt);
     if (rc) return rc;
     rc = alloc_work(s.get());
@@ -859,6 +889,11 @@ static int session_from_batch(const eclip_profiles* P, const eclip_batch* b, con
     fill_setup(s.get(), n, W, b->total_sms, b->switch_max, b->slowdown, b->objective, b->qos_ns != nullptr, opt);
     rc = build_tables(s.get(), specs);
     if (rc) return rc;
+    {
+        std::vector<int32_t> all(specs.size());
+        for (size_t i = 0; i < all.size(); i++) all[i] = (int32_t)i;
+        set_wide(s.get(), all);
+    }
     rc = plan_geometry(s.get(), opt);
     if (rc) return rc;
     if (s->engine != ECLIP_ENGINE_ENUM) return fail(ECLIP_E_TOO_LARGE, "batched planning runs on the ENUM engine only");
@@ -943,7 +978,7 @@ extern "C" int eclip_session_pass2_min(eclip_session* s, const float* global_min
     if (!s) return fail(ECLIP_E_INVALID_ARG, "null session");
     if (global_min) {
         CU(cudaMemcpyAsync(s->wk.m32, global_min, 4 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
-        if (!(s->su.mode == M_MATRIX && s->su.has_qos))
+        if (!qos_float(s->su))
             CU(cudaMemcpyAsync(s->wk.m32_sure, global_min, 4 * (size_t)s->n, cudaMemcpyHostToDevice, s->st));
     }
     int rc = step_pass2_min(s);
@@ -968,8 +1003,26 @@ extern "C" int eclip_session_pass2_first(eclip_session* s, const uint64_t* globa
     return ECLIP_OK;
 }
 
+// A growable device scratch block (stream-ordered); a persistent planner keeps its result
+// staging here instead of allocating per call.
+struct Scratch {
+    unsigned char* p = nullptr;
+    size_t cap = 0;
+    cudaStream_t st = nullptr;
+    cudaError_t need(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr; cap = 0;
+        cudaError_t e = cudaMallocAsync((void**)&p, bytes, st);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    ~Scratch() { if (p) cudaFreeAsync(p, st); }
+};
+
 // materialise into device buffers; copy to the caller's host arrays unless on_device
-static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host = nullptr, uint64_t* key_host = nullptr) {
+static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host = nullptr, uint64_t* key_host = nullptr,
+                        Scratch* stg = nullptr) {
     const size_t n = s->n, W = s->W;
     int stride = o->group_stride > 0 ? o->group_stride : 1;
     MatOut mo{};
@@ -982,22 +1035,29 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
         CU(launch_materialize(s->su, s->tb, s->wk, s->d_sizes, s->C, mo, s->st));
         return ECLIP_OK;
     }
-    int32_t *st, *lv, *sw, *gsm = nullptr;
-    uint64_t *idx, *key = nullptr;
-    double *obj, *mk, *pw, *en, *thr, *lat, *glat = nullptr;
-    CU(s->arena.alloc(&st, n));
-    CU(s->arena.alloc(&lv, n * W));
-    CU(s->arena.alloc(&sw, n * W));
-    CU(s->arena.alloc(&idx, n));
-    CU(s->arena.alloc(&obj, n));
-    CU(s->arena.alloc(&mk, n));
-    CU(s->arena.alloc(&pw, n));
-    CU(s->arena.alloc(&en, n));
-    CU(s->arena.alloc(&thr, n));
-    CU(s->arena.alloc(&lat, n * W));
-    if (o->group_sm) CU(s->arena.alloc(&gsm, n * W * stride));
-    if (glat_host) CU(s->arena.alloc(&glat, n * W * stride));
-    if (key_host) CU(s->arena.alloc(&key, n * 4));
+    // staging for every output: one block (the planner's growable scratch, or the session arena)
+    Bump bp;
+    const size_t o_st = bp.take<int32_t>(n), o_lv = bp.take<int32_t>(n * W), o_sw = bp.take<int32_t>(n * W);
+    const size_t o_idx = bp.take<uint64_t>(n), o_obj = bp.take<double>(n), o_mk = bp.take<double>(n);
+    const size_t o_pw = bp.take<double>(n), o_en = bp.take<double>(n), o_thr = bp.take<double>(n);
+    const size_t o_lat = bp.take<double>(n * W);
+    const size_t o_gsm = o->group_sm ? bp.take<int32_t>(n * W * stride) : 0;
+    const size_t o_glat = glat_host ? bp.take<double>(n * W * stride) : 0;
+    const size_t o_key = key_host ? bp.take<uint64_t>(n * 4) : 0;
+    unsigned char* base;
+    if (stg) {
+        CU(stg->need(bp.off));
+        base = stg->p;
+    } else {
+        CU(s->arena.alloc(&base, bp.off));
+    }
+    int32_t* st = (int32_t*)(base + o_st); int32_t* lv = (int32_t*)(base + o_lv); int32_t* sw = (int32_t*)(base + o_sw);
+    uint64_t* idx = (uint64_t*)(base + o_idx);
+    double *obj = (double*)(base + o_obj), *mk = (double*)(base + o_mk), *pw = (double*)(base + o_pw);
+    double *en = (double*)(base + o_en), *thr = (double*)(base + o_thr), *lat = (double*)(base + o_lat);
+    int32_t* gsm = o->group_sm ? (int32_t*)(base + o_gsm) : nullptr;
+    double* glat = glat_host ? (double*)(base + o_glat) : nullptr;
+    uint64_t* key = key_host ? (uint64_t*)(base + o_key) : nullptr;
     mo.group_lat = glat; mo.key = key;
     mo.status = st; mo.levels = lv; mo.index = idx; mo.objective = obj; mo.makespan = mk; mo.power = pw;
     mo.energy = en; mo.thr = thr; mo.latency = lat; mo.switches = sw; mo.group_sm = gsm;
@@ -1088,6 +1148,196 @@ extern "C" int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* b
     if (s->on_device && s->own_stream) CU(cudaStreamSynchronize(s->st));
     return ECLIP_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// persistent planner (include/eclip.h "persistent planner"): level tables, per-table hulls and
+// device workspaces are built once; each plan call runs only the per-mix work
+// ------------------------------------------------------------------------------------------
+struct eclip_planner {
+    std::unique_ptr<eclip_session> s;
+    eclip_options opt{};
+    int n_max = 0, W = 0, N = 0, R = 0, mode = 0, obj = 0;
+    float pi = 0.0f, pm = 0.0f;
+    bool has_qos = false, timing = false;
+    std::vector<uint32_t> mask;
+    WorkBlock wb;
+    Scratch stg;
+    int32_t* d_ids = nullptr;
+    double* d_qos = nullptr;
+    float* d_M = nullptr;
+    cudaEvent_t ev[6] = {};
+    bool ev_valid = false;
+    ~eclip_planner() {
+        if (s && s->st) cudaStreamSynchronize(s->st);
+        for (cudaEvent_t& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+// table specs of a batch: one table per model of the profiles (shared grouping, mask and budget)
+static int batch_specs(const eclip_profiles* P, const eclip_batch* b, std::vector<TableSpec>* specs) {
+    const int C = P->C();
+    specs->clear();
+    for (int m = 0; m < P->n(); m++) {
+        TableSpec sp;
+        sp.model = m;
+        sp.R = b->switch_max;
+        sp.mask = b->allowed_mask ? b->allowed_mask[m] : ((C == 32) ? 0xffffffffu : ((1u << C) - 1u));
+        if (C < 32) sp.mask &= (1u << C) - 1u;
+        if (sp.mask == 0) return fail(ECLIP_E_INVALID_ARG, "model %d has no allowed size", m);
+        for (int j = 0; j < C; j++)
+            if (((sp.mask >> j) & 1u) && P->sizes[j] > b->total_sms)
+                return fail(ECLIP_E_INVALID_ARG, "size %d exceeds total_sms", P->sizes[j]);
+        for (int k = 0; k <= P->nk[m]; k++) sp.bounds.push_back(k);
+        specs->push_back(sp);
+    }
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_planner_create(const eclip_profiles* P, const eclip_batch* b, int32_t max_problems,
+                                    const eclip_options* opt, eclip_planner** out) {
+    if (!b || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    if (max_problems < 1) return fail(ECLIP_E_INVALID_ARG, "max_problems must be >= 1");
+    eclip_options o;
+    if (opt) o = *opt; else eclip_default_options(&o);
+    if (o.engine != ECLIP_ENGINE_AUTO && o.engine != ECLIP_ENGINE_ENUM)
+        return fail(ECLIP_E_INVALID_ARG, "the planner runs the ENUM engine");
+    if (o.n_shards > 1) return fail(ECLIP_E_INVALID_ARG, "the planner plans whole batches (n_shards = 1)");
+    o.engine = ECLIP_ENGINE_ENUM;
+    o.shard = 0; o.n_shards = 1;
+    int rc = check_common(P, b->n_models, b->total_sms, b->switch_max, b->slowdown, b->objective, b->p_idle_w,
+                          b->p_max_w, o.tie_tol);
+    if (rc) return rc;
+    std::vector<TableSpec> specs;
+    if ((rc = batch_specs(P, b, &specs))) return rc;
+    auto pl = std::make_unique<eclip_planner>();
+    pl->opt = o;
+    pl->n_max = max_problems;
+    pl->W = b->n_models; pl->N = b->total_sms; pl->R = b->switch_max; pl->mode = b->slowdown; pl->obj = b->objective;
+    pl->pi = b->p_idle_w; pl->pm = b->p_max_w;
+    pl->has_qos = b->qos_ns != nullptr;
+    pl->timing = o.timing != 0;
+    for (auto& sp : specs) pl->mask.push_back(sp.mask);
+    pl->s = std::make_unique<eclip_session>();
+    eclip_session* s = pl->s.get();
+    s->prof = P;
+    s->W = pl->W; s->n = max_problems; s->C = P->C();
+    if ((rc = setup_device(s, &o))) return rc;
+    fill_setup(s, max_problems, pl->W, pl->N, pl->R, pl->mode, pl->obj, pl->has_qos, &o);
+    if ((rc = build_tables(s, specs))) return rc;   // K1 once (the only host synchronisation)
+    {
+        std::vector<int32_t> all(specs.size());
+        for (size_t i = 0; i < all.size(); i++) all[i] = (int32_t)i;
+        set_wide(s, all);
+    }
+    if ((rc = plan_geometry(s, &o))) return rc;
+    if (s->engine != ECLIP_ENGINE_ENUM) return fail(ECLIP_E_TOO_LARGE, "batched planning runs on the ENUM engine only");
+    if (s->su.aux_bytes > 0) {   // per-table S orders and hulls, kept for the planner's lifetime
+        CU(s->arena.alloc(&s->wk.thull, (size_t)s->tb.n * s->su.Lmax));
+        CU(s->arena.alloc(&s->wk.thull_n, (size_t)s->tb.n));
+        CU(s->arena.alloc(&s->wk.tord, (size_t)s->tb.n * s->su.Lmax));
+        CU(launch_table_hull(s->su, s->tb, s->wk, s->st));
+    }
+    const size_t nw = (size_t)max_problems * pl->W;
+    CU(s->arena.alloc(&pl->d_ids, nw));
+    if (pl->has_qos) CU(s->arena.alloc(&pl->d_qos, nw));
+    if (pl->mode == ECLIP_MATRIX) CU(s->arena.alloc(&pl->d_M, nw * pl->W));
+    CU(s->arena.alloc(&s->d_sizes, s->C));
+    CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * (size_t)s->C, cudaMemcpyHostToDevice, s->st));
+    if ((rc = alloc_work(s, &pl->wb))) return rc;
+    pl->stg.st = s->st;
+    if (pl->timing)
+        for (cudaEvent_t& e : pl->ev) CU(cudaEventCreate(&e));
+    CU(cudaStreamSynchronize(s->st));
+    *out = pl.release();
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_planner_plan(eclip_planner* pl, const eclip_batch* b, eclip_batch_out* out) {
+    if (!pl || !b || !out) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    eclip_session* s = pl->s.get();
+    const int n = b->n_problems, W = pl->W;
+    if (n < 1 || n > pl->n_max) return fail(ECLIP_E_INVALID_ARG, "n_problems must be in [1, %d]", pl->n_max);
+    if (b->n_models != W || b->total_sms != pl->N || b->switch_max != pl->R || b->slowdown != pl->mode ||
+        b->objective != pl->obj || b->p_idle_w != pl->pi || b->p_max_w != pl->pm)
+        return fail(ECLIP_E_INVALID_ARG, "batch settings differ from the planner's");
+    if ((b->qos_ns != nullptr) != pl->has_qos)
+        return fail(ECLIP_E_INVALID_ARG, pl->has_qos ? "this planner needs qos_ns" : "this planner was created without QoS");
+    if (!b->model_ids || (pl->mode == ECLIP_MATRIX && !b->slowdown_matrix))
+        return fail(ECLIP_E_INVALID_ARG, "null model_ids / slowdown_matrix");
+    if (b->allowed_mask)
+        for (size_t m = 0; m < pl->mask.size(); m++) {
+            const uint32_t want = b->allowed_mask[m] & (s->C < 32 ? (1u << s->C) - 1u : 0xffffffffu);
+            if (want != pl->mask[m]) return fail(ECLIP_E_INVALID_ARG, "allowed_mask differs from the planner's");
+        }
+    const size_t nw = (size_t)n * W;
+    if (!b->on_device) {
+        for (size_t i = 0; i < nw; i++) {
+            if (b->model_ids[i] < 0 || b->model_ids[i] >= s->prof->n())
+                return fail(ECLIP_E_INVALID_ARG, "model id %d out of range (problem %zu)", b->model_ids[i], i / W);
+            if (b->qos_ns && !(b->qos_ns[i] >= 0.0)) return fail(ECLIP_E_INVALID_ARG, "qos_ns must be >= 0 or +inf");
+        }
+    }
+    if (pl->timing) CU(cudaEventRecord(pl->ev[0], s->st));
+    const int32_t* dtab = b->model_ids;
+    const double* dq = b->qos_ns;
+    const float* dM = b->slowdown_matrix;
+    if (!b->on_device) {   // inputs into the planner's device buffers (stream-ordered)
+        CU(cudaMemcpyAsync(pl->d_ids, b->model_ids, 4 * nw, cudaMemcpyHostToDevice, s->st));
+        if (pl->has_qos) CU(cudaMemcpyAsync(pl->d_qos, b->qos_ns, 8 * nw, cudaMemcpyHostToDevice, s->st));
+        if (pl->d_M) CU(cudaMemcpyAsync(pl->d_M, b->slowdown_matrix, 4 * nw * W, cudaMemcpyHostToDevice, s->st));
+        dtab = pl->d_ids; dq = pl->d_qos; dM = pl->d_M;
+    }
+    if (pl->timing) CU(cudaEventRecord(pl->ev[1], s->st));
+    // geometry of this call's batch size (host arithmetic on the cached level counts; no sync)
+    s->n = n;
+    s->on_device = b->on_device != 0;
+    s->su.n_problems = n;
+    int rc = plan_geometry(s, &pl->opt);
+    if (rc) return rc;
+    if ((rc = alloc_work(s, &pl->wb))) return rc;
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.p_idle = pl->pi; s->pin.p_max = pl->pm;
+    s->wk.table_of = dtab;
+    s->wk.tb = s->tb;
+    CU(launch_prep(s->su, s->tb, s->pin, s->wk, s->C, s->d_sizes, s->st, /*table_hull=*/false));
+    if (pl->timing) CU(cudaEventRecord(pl->ev[2], s->st));
+    if ((rc = step_pass1(s))) return rc;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[3], s->st));
+    CU(launch_pass2_both(s->su, s->wk, s->st));
+    if (pl->timing) CU(cudaEventRecord(pl->ev[4], s->st));
+    pl->ev_valid = false;
+    if (b->on_device) {
+        if ((rc = finish_batch(s, out))) return rc;
+        if (pl->timing) CU(cudaEventRecord(pl->ev[5], s->st));
+        if (s->own_stream) CU(cudaStreamSynchronize(s->st));
+    } else {
+        // finish_batch synchronises after the D2H copies: record the last event before it returns
+        // by materialising through the staging block, then timing the copies with it
+        if ((rc = finish_batch(s, out, nullptr, nullptr, &pl->stg))) return rc;
+        if (pl->timing) CU(cudaEventRecord(pl->ev[5], s->st));
+    }
+    pl->ev_valid = pl->timing;
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_planner_phase_ms(eclip_planner* pl, float* ms, int32_t n) {
+    if (!pl || !ms || n < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
+    if (!pl->ev_valid) return fail(ECLIP_E_INVALID_ARG, "no timed plan (create the planner with opt->timing = 1)");
+    CU(cudaEventSynchronize(pl->ev[5]));
+    for (int i = 0; i < n; i++) {
+        ms[i] = 0.0f;
+        if (i < 5) CU(cudaEventElapsedTime(&ms[i], pl->ev[i], pl->ev[i + 1]));
+    }
+    return ECLIP_OK;
+}
+
+extern "C" int eclip_planner_counters(eclip_planner* pl, uint64_t* out, int32_t n) {
+    if (!pl) return fail(ECLIP_E_INVALID_ARG, "null planner");
+    return eclip_session_counters(pl->s.get(), out, n);
+}
+
+extern "C" void eclip_planner_free(eclip_planner* pl) { delete pl; }
 
 static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_override) {
     const int W = s->W;
@@ -1242,8 +1492,8 @@ extern "C" int eclip_baseline_plan(const eclip_profiles* P, const eclip_problem*
         lam = lam / (uint64_t)gcd64((int64_t)lam, (int64_t)K) * K;
         if (lam > ((uint64_t)1 << 40)) return fail(ECLIP_E_TOO_LARGE, "lcm of kernel counts too large");
     }
-    if ((long double)lam * pr->total_sms * (W + 1) >= (long double)(1 << 24))
-        return fail(ECLIP_E_TOO_LARGE, "Lambda N (W+1) >= 2^24");
+    if ((long double)lam * pr->total_sms * (W + 1) >= 4611686018427387904.0L)   // 2^62: int64 T' (baseline.cu)
+        return fail(ECLIP_E_TOO_LARGE, "Lambda N (W+1) >= 2^62");
     for (int w = 0; w < W; w++) {
         int64_t bm = 0;
         for (int k = 0; k < P->nk[ws[w].model]; k++) {

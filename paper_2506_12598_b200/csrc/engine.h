@@ -52,11 +52,10 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
 // ---------------------------------------------------------------------------------------
 struct Lev {
     int64_t B;        // exact solo time B*(level) (ns)
-    int64_t BS;       // exact B * S'
-    int32_t S;        // S' = S Lambda / K  (Lambda-scaled CU-sum)
-    int32_t Tmax;     // largest T' at which this worker meets its QoS (linear modes); -1 never
+    int64_t BS;       // exact B * S' (narrow problems; 0 in wide ones, where it may not fit)
+    int64_t S;        // S' = S Lambda / K  (Lambda-scaled CU-sum)
+    int32_t Tmax;     // largest T' at which this worker meets its QoS (linear modes, narrow problems); -1 never
     float Bk;         // (float)((double)B / (Lambda N))
-    int32_t pad;
 };
 static_assert(sizeof(Lev) == 32, "Lev must be 32 bytes");
 
@@ -100,7 +99,10 @@ struct Setup {
     int32_t table_bytes;        // fast pass-1 per-CTA table budget (per-warp prefix tables)
     int32_t aux_bytes;          // fast pass-1 per-problem aux block (after the Lev records)
     int32_t lev_stride;         // Lev records per problem block (W*Lmax + aux_bytes/32)
-    int32_t pad1;
+    int32_t wide;               // 1: Lambda N (W+1) may reach 2^24 (heterogeneous kernel counts): S', T' exceed
+                                //    the int32 / exact-float ranges of the narrow kernels; pass 1 runs the generic
+                                //    kernel with FP32 QoS bounds (maybe / surely feasible, as MATRIX), decisions
+                                //    stay exact (u128 / u256) — DESIGN.md §3.10
     int32_t shard, n_shards;
     uint64_t tol_num, tol_den;
     double delta;               // FP32 filter relative error bound
@@ -108,6 +110,14 @@ struct Setup {
     int32_t pad2;
     int64_t rows_max;           // max rows (hi-digit combinations) over problems (rowlb stride)
 };
+
+// QoS decided in pass 1 by FP32 bounds on L_w (maybe / surely feasible minima) instead of exact integer
+// T' thresholds: the MATRIX mode, and every mode of a wide problem
+__host__ __device__ __forceinline__ bool qos_float(const Setup& su) {
+    return su.has_qos != 0 && (su.mode == M_MATRIX || su.wide != 0);
+}
+// T' bound of the narrow problems (Lambda N (W+1) < 2^24: exact in FP32 and int32)
+constexpr int64_t NARROW_T = (int64_t)1 << 24;
 
 // Device view of all level tables
 struct Tables {
@@ -205,8 +215,11 @@ struct SimOut {
 };
 cudaError_t launch_simulate(const SimJob& J, const SimOut& o, double* latbuf, cudaStream_t st);
 
+// per-problem constants, level records and (fast pass 1) aux blocks; table_hull = also build the
+// per-table S orders and hulls (k_table_hull) — a persistent planner builds those once
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
-                        cudaStream_t st);
+                        cudaStream_t st, bool table_hull = true);
+cudaError_t launch_table_hull(const Setup& su, const Tables& tb, Work& wk, cudaStream_t st);
 cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st);
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st);
 cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st);

@@ -163,7 +163,9 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
     }
     P.lam = (int64_t)lam;
     P.lamN = (int64_t)(lam * (u64)su.N);
-    if ((u128)P.lamN * (u128)(W + 1) >= ((u128)1 << 24)) P.status = P.status < 0 ? P.status : -5;
+    // narrow problems: S', T' < 2^24 (exact in FP32 / int32, the fast kernels' integer QoS thresholds);
+    // wide launches (su.wide, heterogeneous kernel counts): T' in int64
+    if ((u128)P.lamN * (u128)(W + 1) >= ((u128)1 << (su.wide ? 62 : 24))) P.status = P.status < 0 ? P.status : -5;
     // index-space sizes, saturating (only the ENUM engine needs them; the host checks its limits)
     uint64_t Pn = 1, tot = 1;
     const uint64_t SAT = (uint64_t)1 << 62;
@@ -223,8 +225,9 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
         if (!(q >= 0.0)) P.status = -4;
         P.Hq[w] = floor_qD(q, P.D);
         if (!isinf(q)) P.has_qos = 1;
-        // MATRIX + QoS float bounds on L_w (relative error of L32 <= (W+2) 2^-24; use 2W+8)
-        double marg = (double)(2 * W + 8) * 5.9604644775390625e-08;
+        // FP32 QoS bounds on L_w (MATRIX, and wide problems): relative error of L32 <= (W+2) 2^-24 (MATRIX),
+        // <= (3W+3) 2^-24 (wide EXCESS: T' - Lambda N rounded; the others <= (W+2)); margins 2W+8 / 4W+8
+        double marg = (double)((su.wide ? 4 : 2) * W + 8) * 5.9604644775390625e-08;
         P.Qhi[w] = isinf(q) ? INFINITY : __double2float_ru(q * (1.0 + marg));
         P.Qlo[w] = isinf(q) ? INFINITY : __double2float_rd(q * (1.0 - marg));
     }
@@ -241,18 +244,18 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
     int p = (int)(i / ((size_t)su.Lmax * su.W));
     const Prob& P = probs[p];
     Lev r;
-    r.B = 0; r.BS = 0; r.S = 0; r.Tmax = -1; r.Bk = 0.0f; r.pad = 0;
+    r.B = 0; r.BS = 0; r.S = 0; r.Tmax = -1; r.Bk = 0.0f;
     Lev* dst = levs + (size_t)p * su.lev_stride + (size_t)w * su.Lmax + l;
     if (P.status >= 0 && l < P.L[w]) {
         int t = P.table[w];
         int64_t B = tb.B[t][l];
         int64_t Sp = tb.S[t][l] * (P.lam / tb.K[t]);
         r.B = B;
-        r.S = (int32_t)Sp;
-        r.BS = B * Sp;
+        r.S = Sp;
+        r.BS = su.wide ? 0 : B * Sp;   // wide: B S' may exceed int64 (only the narrow fast kernels read it)
         r.Bk = (float)((double)B / (double)P.lamN);
-        int64_t T = (int64_t)1 << 24;
-        if (P.has_qos && su.mode != M_MATRIX && ~P.Hq[w] != 0) {
+        int64_t T = NARROW_T;
+        if (P.has_qos && !qos_float(su) && ~P.Hq[w] != 0) {
             u128 hq = P.Hq[w];
             int64_t hb;  // floor(Hq / B), saturated at 2^30
             if ((hq >> 64) != 0) hb = (int64_t)1 << 30;
@@ -264,7 +267,7 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
             else if (su.mode == M_PAPER) T = hb - P.lamN;
             else T = ((u128)B * (u128)P.lamN > hq) ? -1 : hb;
             if (T < -1) T = -1;
-            if (T > ((int64_t)1 << 24)) T = (int64_t)1 << 24;
+            if (T > NARROW_T) T = NARROW_T;
         }
         r.Tmax = (int32_t)T;
     }
@@ -673,9 +676,9 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
         int umax = -(1 << 30), smin = INT_MAX;
         long long bmin = LLONG_MAX;
         for (int l = lane; l < L; l += 32) {
-            umax = max(umax, lv[l].Tmax - lv[l].S);
+            umax = max(umax, (int)(lv[l].Tmax - lv[l].S));   // narrow problems: S' < 2^24
             bmin = min(bmin, (long long)lv[l].B);
-            smin = min(smin, lv[l].S);
+            smin = min(smin, (int)lv[l].S);
         }
         for (int off = 16; off; off >>= 1) {
             umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, off));
@@ -1040,7 +1043,7 @@ __device__ __forceinline__ float team_min(float m, int T, unsigned mask) {
 
 __device__ float band_bound(const Setup& su, float m, float ms) {
     // every candidate with exact key <= H*(1+tau) has key32 <= bound; H* <= ms / (1 - delta)
-    double base = (su.mode == M_MATRIX && su.has_qos) ? (double)ms : (double)m;
+    double base = qos_float(su) ? (double)ms : (double)m;
     if (isinf(base)) return INFINITY;
     double tau = (double)su.tol_num / (double)su.tol_den;
     double b = base * (1.0 + tau) * (1.0 + su.delta) / (1.0 - su.delta) * (1.0 + 1e-12);
@@ -1626,6 +1629,7 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
     if (!ok) return;
     constexpr int W = NP + 1;
     const int Lmax = su.Lmax;
+    const bool wide = su.wide != 0;
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev)), &bar);
     int L[W];
@@ -1650,19 +1654,31 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
         for (int e = e0; e < e1; e++) {
             if (NP >= 1) d[NP - 1] = e;
             float pBf[W], pBk[W], psf[W];
-            int64_t pB = 0;
-            int32_t pT = 0, pTm = 1 << 24;
+            int64_t pB = 0, pT = 0;
+            int32_t pTm = (int32_t)NARROW_T;
 #pragma unroll
             for (int w = 0; w < NP; w++) {
                 const Lev& r = sl[w * Lmax + d[w]];
                 pBf[w] = __ll2float_rn(r.B);
                 pBk[w] = r.Bk;
-                psf[w] = (float)r.S;
+                psf[w] = __ll2float_rn(r.S);
                 pB += r.B; pT += r.S; pTm = min(pTm, r.Tmax);
             }
-            const float Tpf = (float)pT;
-            const float c1 = (float)(pTm - pT);
+            const float Tpf = __ll2float_rn(pT);
+            const float c1 = wide ? 0.0f : (float)(pTm - pT);
             float Opre[W];
+            if (MODE != M_MATRIX && wide) {
+                // wide problems: S', T' beyond 2^24, so T' - S'_w is not exact in FP32; the overlap of
+                // prefix worker w is summed from the others' rounded S' (non-negative terms, <= (W-1) u)
+#pragma unroll
+                for (int w = 0; w < NP; w++) {
+                    float o = (MODE == M_EXCL) ? 0.0f : psf[w];
+#pragma unroll
+                    for (int v = 0; v < NP; v++)
+                        if (v != w) o += psf[v];
+                    Opre[w] = o;
+                }
+            }
             if (MODE == M_MATRIX) {
 #pragma unroll
                 for (int w = 0; w < W; w++) {
@@ -1676,7 +1692,7 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
             const float Bpf = __ll2float_rn(pB);
             for (int j = lane; j < Lin; j += 32) {
                 const Lev& a = inner[j];
-                const float iBf = __ll2float_rn(a.B), iBk = a.Bk, isf = (float)a.S;
+                const float iBf = __ll2float_rn(a.B), iBk = a.Bk, isf = __ll2float_rn(a.S);
                 const float Tf = Tpf + isf;
                 float Lw[W];
                 float num = 0.0f;
@@ -1685,8 +1701,8 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
                     const float bf = (w == NP) ? iBf : pBf[w];
                     const float bk = (w == NP) ? iBk : pBk[w];
                     float O;
-                    if (MODE == M_EXCL) O = (w == NP) ? Tpf : (Tf - psf[w]);
-                    else if (MODE == M_PAPER) O = Tf;
+                    if (MODE == M_EXCL) O = (w == NP) ? Tpf : (wide ? Opre[w] + isf : Tf - psf[w]);
+                    else if (MODE == M_PAPER) O = (wide && w < NP) ? Opre[w] + isf : Tf;
                     else if (MODE == M_EXCESS) O = fmaxf(Tf - P.lamNf, 0.0f);
                     else O = (w == NP) ? Opre[w] : fmaf(Mcol[w], isf, Opre[w]);
                     Lw[w] = fmaf(O, bk, bf);
@@ -1703,7 +1719,7 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
                     else key = fmaf(P.p_dyn, fminf(1.0f, Tf * P.inv), P.p_idle) * mx;
                 }
                 if (QOS) {
-                    if (MODE == M_MATRIX) {
+                    if (MODE == M_MATRIX || wide) {
                         bool maybe = true, sure = true;
 #pragma unroll
                         for (int w = 0; w < W; w++) {
@@ -1721,10 +1737,10 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
             }
         }
         m = team_min(m, 32, 0xffffffffu);
-        if (MODE == M_MATRIX && QOS) ms = team_min(ms, 32, 0xffffffffu);
+        if ((MODE == M_MATRIX || wide) && QOS) ms = team_min(ms, 32, 0xffffffffu);
         if (lane == 0) {
             submin[(size_t)prob * su.units_max + unit] = m;
-            if (MODE == M_MATRIX && QOS) submin_sure[(size_t)prob * su.units_max + unit] = ms;
+            if ((MODE == M_MATRIX || wide) && QOS) submin_sure[(size_t)prob * su.units_max + unit] = ms;
         }
     }
 }
@@ -1987,7 +2003,7 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
 }
 
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
-    const bool two = su.mode == M_MATRIX && su.has_qos;
+    const bool two = qos_float(su);
     k_reduce_min<<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
                                                 wk.m32_sure, wk.bandn, wk.bandlist, wk.plist, wk.plist_n,
                                                 pass1_prunable(su) ? wk.wbits : nullptr);
@@ -2037,7 +2053,7 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
         const Lev& r = sl[w * su.Lmax + lv[w]];
         Tp += r.S; SB += r.B; SBS += r.BS;
     }
-    const float Tf = (float)Tp;
+    const float Tf = __ll2float_rn(Tp);
     float Lw[MAXW_ENUM];
     float num = 0.0f;
     bool feas = true;
@@ -2045,7 +2061,11 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
         const Lev& r = sl[w * su.Lmax + lv[w]];
         const float bf = __ll2float_rn(r.B);
         float O;
-        if (su.mode == M_EXCL) O = Tf - (float)r.S;
+        if (su.wide && (su.mode == M_EXCL || su.mode == M_PAPER)) {   // sum of rounded S' (see k_pass1_gen)
+            O = 0.0f;
+            for (int v = 0; v < W; v++)
+                if (v != w || su.mode == M_PAPER) O += __ll2float_rn(sl[v * su.Lmax + lv[v]].S);
+        } else if (su.mode == M_EXCL) O = Tf - (float)r.S;
         else if (su.mode == M_PAPER) O = Tf;
         else if (su.mode == M_EXCESS) O = fmaxf(Tf - P.lamNf, 0.0f);
         else {
@@ -2056,12 +2076,12 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
         Lw[w] = fmaf(O, r.Bk, bf);
         num = fmaf(bf, O, num);
         if (su.has_qos) {
-            if (su.mode == M_MATRIX) feas = feas && (Lw[w] <= P.Qhi[w]);
+            if (qos_float(su)) feas = feas && (Lw[w] <= P.Qhi[w]);
             else feas = feas && (Tp <= (int64_t)r.Tmax);
         }
     }
     if (su.obj == O_SUM) {
-        if (su.mode == M_EXCL) {
+        if (su.mode == M_EXCL && !su.wide) {
             const float bsum = __ll2float_rn(SB);
             key = fmaf(fmaf(Tf, bsum, -__ll2float_rn(SBS)), P.inv, bsum);
         } else {
@@ -2145,7 +2165,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
         const uint32_t ncand = (uint32_t)(e1 - e0) * (uint32_t)Lin;
         // exact integer QoS test first (the same predicate as key32_scalar's in the linear modes):
         // hi sums once per unit, then T' = hT + S'_e + S'_k <= min(hTm, Tmax_e, Tmax_k)
-        const bool qlin = su.has_qos && su.mode != M_MATRIX;
+        const bool qlin = su.has_qos && !qos_float(su);
         int64_t hT = 0;
         int hTm = 1 << 30;
         if (qlin)
@@ -2352,7 +2372,7 @@ cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_pass2<0><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
-                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 qos_float(su) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
                                                  pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
@@ -2362,7 +2382,7 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_pass2<2><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
-                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 qos_float(su) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
                                                  pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
@@ -2372,7 +2392,7 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_pass2<1><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
-                                                 (su.mode == M_MATRIX && su.has_qos) ? wk.m32_sure : nullptr,
+                                                 qos_float(su) ? wk.m32_sure : nullptr,
                                                  wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
                                                  pass1_prunable(su) ? wk.wbits : nullptr);
     return cudaGetLastError();
@@ -2499,18 +2519,25 @@ cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, cons
     return cudaGetLastError();
 }
 
+// per level table: S order and lower-left hull vertices (shared by every problem using the table)
+cudaError_t launch_table_hull(const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
+    if (su.aux_bytes <= 0) return cudaSuccess;
+    const size_t hsm = (size_t)su.Lmax * (8 + 4 + 2 + 1) + 16;
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_table_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    if (e != cudaSuccess) return e;
+    k_table_hull<<<tb.n, 256, hsm, st>>>(tb, su.Lmax, wk.thull, wk.thull_n, wk.tord);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool table_hull) {
     (void)C; (void)sizes;
     k_prep_prob<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, in, wk.probs);
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
     if (su.aux_bytes > 0) {
-        // per level table: S order and lower-left hull vertices (shared by every problem using the table)
-        const size_t hsm = (size_t)su.Lmax * (8 + 4 + 2 + 1) + 16;
-        cudaError_t e = cudaFuncSetAttribute((const void*)k_table_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        if (e != cudaSuccess) return e;
-        k_table_hull<<<tb.n, 256, hsm, st>>>(tb, su.Lmax, wk.thull, wk.thull_n, wk.tord);
+        cudaError_t e;
+        if (table_hull && (e = launch_table_hull(su, tb, wk, st)) != cudaSuccess) return e;
         const size_t sm = (size_t)2 * su.Lmax * sizeof(Lev) + (size_t)su.aux_bytes;
         auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;
         e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

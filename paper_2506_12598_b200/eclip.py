@@ -52,7 +52,7 @@ class Result(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("engine", C.c_int32), ("device", C.c_int32), ("cuda_stream", C.c_void_p), ("tie_tol", C.c_double),
-                ("shard", C.c_int32), ("n_shards", C.c_int32), ("no_prune", C.c_int32)]
+                ("shard", C.c_int32), ("n_shards", C.c_int32), ("no_prune", C.c_int32), ("timing", C.c_int32)]
 
 
 class Batch(C.Structure):
@@ -77,7 +77,9 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_session_pass2_first", "eclip_session_finish", "eclip_session_free",
            "eclip_session_create_problem", "eclip_session_finish_problem", "eclip_session_stats",
            "eclip_session_counters",
-           "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate", "eclip_level_table"]
+           "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate", "eclip_level_table",
+           "eclip_planner_create", "eclip_planner_plan", "eclip_planner_phase_ms", "eclip_planner_counters",
+           "eclip_planner_free"]
 
 
 def lib():
@@ -115,6 +117,12 @@ def lib():
         L.eclip_baseline_plan.argtypes = [vp, P(Problem), C.c_int32, C.c_double, P(Options), P(Result)]
         L.eclip_lookup_table_json.argtypes = [vp, P(Problem), P(C.c_int32), C.c_char_p, C.c_size_t,
                                               P(C.c_size_t), P(C.c_uint64)]
+        L.eclip_planner_create.argtypes = [vp, P(Batch), C.c_int32, P(Options), P(vp)]
+        L.eclip_planner_plan.argtypes = [vp, P(Batch), P(BatchOut)]
+        L.eclip_planner_phase_ms.argtypes = [vp, P(C.c_float), C.c_int32]
+        L.eclip_planner_counters.argtypes = [vp, P(C.c_uint64), C.c_int32]
+        L.eclip_planner_free.argtypes = [vp]
+        L.eclip_planner_free.restype = None
         L.eclip_level_table.argtypes = [vp, C.c_int32, P(C.c_int32), C.c_uint32, C.c_int32, P(Options), C.c_int32,
                                         P(C.c_int64), P(C.c_int64), P(C.c_uint8), P(C.c_int32), P(C.c_int32)]
         _lib = L
@@ -224,7 +232,8 @@ class Plan:
     candidates_evaluated: int = 0
 
 
-def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True) -> Options:
+def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True,
+             timing=False) -> Options:
     o = Options()
     lib().eclip_default_options(C.byref(o))
     o.engine = ENGINES[engine]
@@ -233,6 +242,7 @@ def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shar
     o.tie_tol = tie_tol
     o.shard, o.n_shards = shard, n_shards
     o.no_prune = 0 if prune else 1
+    o.timing = 1 if timing else 0
     return o
 
 
@@ -436,6 +446,83 @@ def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int
     o = _options("enum", device, stream, tie_tol, prune=prune)
     _check(lib().eclip_plan_batch(profiles.handle, C.byref(a.c), C.byref(o), C.byref(b)))
     return out
+
+
+# ------------------------------------------------------------------------------------------
+PHASES = ("h2d", "prep", "pass1", "pass2", "materialize")
+
+
+class Planner:
+    """eclip_planner_*: a persistent batch planner over one profile library (serving-loop
+    replanning).  The level tables are built once at construction; plan() runs the per-mix work
+    only.  Host (numpy) inputs and outputs are copied on the planner's stream; torch CUDA inputs
+    with device outputs (alloc_batch_out(..., device=...)) stay on the device."""
+
+    def __init__(self, profiles: Profiles, *, n_models: int, max_problems: int, total_sms: int, switch_max: int = 14,
+                 slowdown: str = "exclude_self", objective: str = "sum", qos: bool = True, allowed_mask=None,
+                 p_idle_w: float = 75.0, p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0,
+                 stream=None, prune: bool = True, timing: bool = False):
+        self.profiles = profiles
+        self.W, self.n_max = n_models, max_problems
+        self.mask = _np(allowed_mask, np.uint32) if allowed_mask is not None else None
+        self.kw = (total_sms, switch_max, MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w)
+        self.qos = qos
+        self._h = C.c_void_p()
+        shape = Batch(1, n_models, None, 1 if qos else None, _ptr(self.mask, C.c_uint32), None, total_sms, switch_max,
+                      MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 0)
+        o = _options("enum", device, stream, tie_tol, prune=prune, timing=timing)
+        _check(lib().eclip_planner_create(profiles.handle, C.byref(shape), max_problems, C.byref(o), C.byref(self._h)))
+        self._cache = {}
+
+    def _structs(self, model_ids, qos_ns, slowdown_matrix, out):
+        key = (_addr(model_ids), _addr(qos_ns), _addr(slowdown_matrix), id(out))
+        hit = self._cache.get(key)
+        if hit is None:
+            on_device = hasattr(model_ids, "is_cuda") and model_ids.is_cuda
+            n = int(model_ids.shape[0])
+            b = Batch(n, self.W, _addr(model_ids), _addr(qos_ns), _ptr(self.mask, C.c_uint32), _addr(slowdown_matrix),
+                      *self.kw, 1 if on_device else 0)
+            hit = (b, _batch_out_struct(out), (model_ids, qos_ns, slowdown_matrix, out))
+            if len(self._cache) > 64:
+                self._cache.clear()
+            self._cache[key] = hit
+        return hit
+
+    def plan(self, model_ids, qos_ns=None, slowdown_matrix=None, out=None, gmax: int = 0):
+        """plan one batch: model_ids [n, W] int32 (numpy / pinned numpy / torch CUDA), qos_ns [n, W]
+        float64 when the planner has QoS.  Returns `out` (allocated if None)."""
+        if not (hasattr(model_ids, "is_cuda") and model_ids.is_cuda):
+            model_ids = np.ascontiguousarray(model_ids, dtype=np.int32)
+            qos_ns = None if qos_ns is None else np.ascontiguousarray(qos_ns, dtype=np.float64)
+        if out is None:
+            dev = model_ids.device if hasattr(model_ids, "is_cuda") and model_ids.is_cuda else None
+            out = alloc_batch_out(int(model_ids.shape[0]), self.W, gmax, device=dev)
+        b, bo, _ = self._structs(model_ids, qos_ns, slowdown_matrix, out)
+        _check(lib().eclip_planner_plan(self._h, C.byref(b), C.byref(bo)))
+        return out
+
+    def phase_ms(self) -> dict:
+        """CUDA-event split of the last plan (needs timing=True)"""
+        ms = (C.c_float * 5)()
+        _check(lib().eclip_planner_phase_ms(self._h, ms, 5))
+        return {k: float(ms[i]) for i, k in enumerate(PHASES)}
+
+    def counters(self) -> dict:
+        v = (C.c_uint64 * 5)()
+        _check(lib().eclip_planner_counters(self._h, v, 5))
+        return {"evaluated_candidates": int(v[0]), "units_processed": int(v[1]), "kernel_ms": int(v[2]) * 1e-6,
+                "units_with_swept_entries": int(v[3]), "entries_swept": int(v[4])}
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().eclip_planner_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------------------------------

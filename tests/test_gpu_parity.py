@@ -460,3 +460,136 @@ def test_overflow_fallbacks_with_tiny_list_capacities():
                        env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+# ---------------------------------------------------------------- persistent planner
+def test_planner_every_mix_vs_oracle_golden_host_and_device():
+    """eclip_planner_*: level tables built once, then batch after batch (different sizes, host and
+    device buffers, several seeds) — every mix against the oracle's stored answers, and equal to
+    the one-shot eclip_plan_batch"""
+    import torch
+    import golden_c5
+    models, _, _ = synth.make_c5(1)
+    pr = ec.Profiles.from_models(models)
+    pl = ec.Planner(pr, n_models=4, max_problems=4096, total_sms=148, p_idle_w=200.0, p_max_w=1000.0, timing=True)
+    for seed, n in ((0, 4096), (1, 1000), (2, 1), (3, 4096), (4, 4096)):
+        _, ids, qos = synth.make_c5(n, seed=seed)
+        if seed % 2:
+            out = pl.plan(ids, qos, gmax=16)
+            got = out
+        else:
+            d_out = ec.alloc_batch_out(n, 4, 16, device="cuda")
+            pl.plan(torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda(), out=d_out)
+            torch.cuda.synchronize()
+            got = d_out
+        assert golden_c5.check_batch(ids, got, sizes=models[0].sizes) == n
+        ph = pl.phase_ms()
+        assert all(v >= 0.0 for v in ph.values()) and ph["pass1"] > 0.0
+        if seed == 3:
+            ref = ec.plan_batch(pr, ids, total_sms=148, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0, gmax=16)
+            for k in ("status", "winner_index", "winner_levels", "objective", "group_sm", "model_latency_ns", "power_w"):
+                assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), k
+    with pytest.raises(ec.EclipError):
+        pl.plan(np.zeros((4097, 4), np.int32), np.ones((4097, 4)))        # more mixes than max_problems
+    with pytest.raises(ec.EclipError):
+        pl.plan(np.zeros((4, 4), np.int32), None)                         # the planner has QoS
+    pl.close()
+
+
+def test_planner_other_settings_vs_oracle():
+    """planners without QoS, in PAPER mode with masks, and MATRIX (generic kernels) against the oracle"""
+    masks = [0xFF, 0xFE, 0x7F, 0xFF, 0x3C, 0xFF, 0xF0]
+    rng = np.random.default_rng(3)
+    for mode, use_q, mk in (("exclude_self", False, None), ("paper", True, masks), ("matrix", True, None)):
+        W = 3 if mode == "matrix" else 4       # the oracle enumerates MATRIX problems: keep them at 1.4e6 tuples
+        models, ids, qos = synth.make_c5(12, seed=23, W=W)
+        pr = ec.Profiles.from_models(models)
+        M = rng.uniform(0.5, 1.5, size=(12, W, W)).astype(np.float32)
+        pl = ec.Planner(pr, n_models=W, max_problems=16, total_sms=148, slowdown=mode, qos=use_q, allowed_mask=mk,
+                        p_idle_w=200.0, p_max_w=1000.0)
+        q = qos * 1.5 if use_q else None
+        for rep in range(2):
+            out = pl.plan(ids, q, slowdown_matrix=M if mode == "matrix" else None, gmax=16)
+            for i in range(0, 12, 3):
+                p = synth.c5_problem(i, models, ids, qos * 1.5)
+                p.mode = mode
+                if not use_q:
+                    p.qos_ns = None
+                if mk is not None:
+                    p.allowed_mask = [mk[m] for m in ids[i]]
+                if mode == "matrix":
+                    p.slowdown_matrix = M[i].copy()
+                    np.fill_diagonal(p.slowdown_matrix, 0.0)
+                o = oracle.solve(p, "enum" if mode == "matrix" else "slice")
+                assert (int(out["status"][i]) == 0) == (o.status == "ok"), (mode, i)
+                if o.status == "ok":
+                    assert out["winner_levels"][i].tolist() == o.levels, (mode, i)
+                    assert out["objective"][i] == pytest.approx(o.objective, rel=REL)
+        pl.close()
+
+
+# ---------------------------------------------------------------- heterogeneous kernel counts (wide)
+def _hetero_problem(Ks, C, R, mode="exclude_self", objective="sum", qos=None, seed=0, fams=None):
+    sizes = synth.lattice_sizes(C, 148)
+    fams = fams or ["resnet", "bert", "vgg", "densenet", "shufflenet"]
+    models = [synth.synthesize_model(f"k{K}", fams[i % len(fams)], K, sizes, 7000 + 31 * seed + i)
+              for i, K in enumerate(Ks)]
+    ids = list(range(len(Ks)))
+    q = synth.qos_3x(models, ids, factor=qos) if qos else None
+    return synth.Problem(f"hetero{Ks}", models, ids, 148, R, mode, objective, qos_ns=q,
+                         p_idle_w=200.0, p_max_w=1000.0)
+
+
+def test_heterogeneous_kernel_counts_vs_oracle():
+    """PAPER.md P:299 decides per kernel and P:313 divides each worker's CU sum by its own kernel
+    count; co-located models have different, often co-prime, kernel counts, so
+    Lambda = lcm K_w and Lambda N (W+1) exceed 2^24: the wide launch."""
+    cases = [((200, 199, 97), 2, 14, "exclude_self", "sum", 3.0),
+             ((200, 199, 97), 2, 14, "exclude_self", "sum", None),
+             ((200, 199, 97), 2, 3, "paper", "sum", 6.0),
+             ((131, 64, 97), 3, 2, "exclude_self", "max", 3.0),
+             ((131, 64, 97), 3, 2, "excess", "energy", None),
+             ((61, 53, 47, 43), 2, 1, "exclude_self", "sum", 3.5),
+             ((61, 53, 47, 43), 2, 1, "paper", "energy", 8.0)]
+    for Ks, C, R, mode, obj, q in cases:
+        p = _hetero_problem(Ks, C, R, mode, obj, q)
+        o = oracle.solve(p, "enum")
+        g = _gpu(p, "enum")
+        _same(g, o, f"{Ks} C={C} R={R} {mode} {obj} q={q}")
+        g = _gpu(p)   # AUTO: ENUM (SLICE does not apply to these T' ranges)
+        assert g.engine == "enum"
+        _same(g, o, f"auto {Ks}")
+    with pytest.raises(ec.EclipError) as e:
+        _gpu(_hetero_problem((200, 199, 97), 2, 14), "slice")
+    assert e.value.code == ec.eclip.E_TOO_LARGE
+
+
+def test_heterogeneous_batch_and_lcm_boundary():
+    """a batch over a library with co-prime kernel counts (wide batch) vs the oracle; the exact-range
+    boundary: Lambda = lcm K_w <= 2^40 plans (4 workers, K ~ 1010), 2^40 < Lambda returns E_TOO_LARGE"""
+    sizes = synth.lattice_sizes(2, 148)
+    Ks = (101, 103, 64, 27, 50)
+    models = [synth.synthesize_model(f"b{K}", "resnet", K, sizes, 7300 + K) for K in Ks]
+    pr = ec.Profiles.from_models(models)
+    rng = np.random.default_rng(9)
+    ids = rng.integers(0, len(Ks), size=(10, 3)).astype(np.int32)
+    solo = np.array([synth.qos_3x(models, [m])[0] for m in range(len(Ks))])
+    out = ec.plan_batch(pr, ids, total_sms=148, switch_max=4, qos_ns=solo[ids], p_idle_w=200.0, p_max_w=1000.0,
+                        gmax=128)
+    for i in range(10):
+        p = synth.Problem("b", models, [int(x) for x in ids[i]], 148, 4, qos_ns=[float(x) for x in solo[ids[i]]],
+                          p_idle_w=200.0, p_max_w=1000.0)
+        o = oracle.solve(p, "enum")
+        assert (int(out["status"][i]) == 0) == (o.status == "ok"), i
+        if o.status == "ok":
+            assert out["winner_levels"][i].tolist() == o.levels, i
+            assert int(out["winner_index"][i]) == o.index, i
+            assert out["objective"][i] == pytest.approx(o.objective, rel=REL)
+    # Lambda = 1009 * 1013 * 1019 * 1021 = 1.06e12 <= 2^40: plans (R = 0: one level per size)
+    big = [synth.synthesize_model(f"p{K}", "uniform", K, sizes, 7400 + K) for K in (1009, 1013, 1019, 1021, 1031)]
+    p = synth.Problem("lcm", big, [0, 1, 2, 3], 148, 0, p_idle_w=200.0, p_max_w=1000.0)
+    _same(_gpu(p, "enum"), oracle.solve(p, "enum"), "lcm 1.06e12")
+    p.model_ids = [0, 1, 2, 3, 4]         # Lambda = 1.1e15 > 2^40
+    with pytest.raises(ec.EclipError) as e:
+        _gpu(p, "enum")
+    assert e.value.code == ec.eclip.E_TOO_LARGE

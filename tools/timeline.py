@@ -24,9 +24,10 @@ pr = ec.Profiles.from_models(models)
 st = torch.cuda.current_stream()
 d_ids, d_q = torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda()
 out = ec.alloc_batch_out(a.mixes, 4, 16, device="cuda")
-kw = dict(total_sms=148, qos_ns=d_q, p_idle_w=200.0, p_max_w=1000.0, out=out, gmax=16, stream=st.cuda_stream)
+pl = ec.Planner(pr, n_models=4, max_problems=a.mixes, total_sms=148, p_idle_w=200.0, p_max_w=1000.0,
+                stream=st.cuda_stream)
 for _ in range(3):
-    ec.plan_batch(pr, d_ids, **kw)
+    pl.plan(d_ids, d_q, out=out)
 torch.cuda.synchronize()
 walls = []
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as prof:
@@ -34,7 +35,7 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, tor
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         with torch.profiler.record_function("step"):
-            ec.plan_batch(pr, d_ids, **kw)
+            pl.plan(d_ids, d_q, out=out)
         torch.cuda.synchronize()
         walls.append((time.perf_counter() - t0) * 1e3)
 os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
