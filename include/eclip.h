@@ -148,6 +148,9 @@ typedef struct {
                                      (same answer); 1 = score every QoS-feasible candidate */
     int32_t timing;               /* eclip_planner_create: 1 = record CUDA events around every phase of each plan
                                      (eclip_planner_phase_ms); default 0 */
+    void* comm;                   /* eclip_comm* (below) or NULL: shard eclip_plan / eclip_plan_batch over the
+                                     communicator's ranks (shard = rank, n_shards = size, device = its device) with
+                                     the exchanges inside the library; every rank returns the same result */
 } eclip_options;
 
 void eclip_default_options(eclip_options* o);
@@ -228,6 +231,30 @@ int eclip_planner_plan(eclip_planner* pl, const eclip_batch* batch, eclip_batch_
 int eclip_planner_phase_ms(eclip_planner* pl, float* ms, int32_t n);
 int eclip_planner_counters(eclip_planner* pl, uint64_t* out, int32_t n);
 void eclip_planner_free(eclip_planner* pl);
+
+/* ---- multi-GPU inside the library (SURVEY §8(b) nccl_comm, §8(e)) ------------------------
+ * One process per GPU.  A sharded plan (rank r scores shard r of every problem's candidate space:
+ * ENUM a contiguous range of pass-1 items, SLICE the T' slices = r mod size) needs three per-problem
+ * exchanges ("minimize" over all workers' joint plans = one global arg-min): the FP32 filter
+ * minima (MIN), the exact 256-bit minimum key and the lowest qualifying level tuple (lexicographic
+ * MIN; the tuple's packed order is the candidate-index order).  With options.comm the library runs
+ * them itself: an NCCL all-gather of the per-rank values on the planning stream plus an on-device
+ * reduction kernel on every rank — no host round trip.
+ *   eclip_comm_unique_id(id[128])   rank 0: a new NCCL unique id; the caller broadcasts the 128 bytes
+ *                                   to the other ranks (e.g. torch.distributed.broadcast_object_list).
+ *   eclip_comm_create(id, n_ranks, rank, device, &c)   collective over the n_ranks processes.
+ *   eclip_comm_create_local(n_ranks, device, comms[n_ranks])   n linked communicators in ONE process on
+ *                                   one device (testing the sharded protocol on one GPU: drive rank r's
+ *                                   plan call from its own host thread; the exchange is device copies).
+ *   eclip_comm_info / eclip_comm_free.
+ * NCCL is loaded at run time (dlopen libnccl.so.2, reusing the one already in the process).
+ * Errors: ECLIP_E_INVALID_ARG, ECLIP_E_CUDA (no device / NCCL failure), ECLIP_E_OOM. */
+typedef struct eclip_comm eclip_comm;
+int eclip_comm_unique_id(uint8_t* id);
+int eclip_comm_create(const uint8_t* id, int32_t n_ranks, int32_t rank, int32_t device, eclip_comm** out);
+int eclip_comm_create_local(int32_t n_ranks, int32_t device, eclip_comm** comms);
+int eclip_comm_info(const eclip_comm* c, int32_t* rank, int32_t* size, int32_t* device);
+void eclip_comm_free(eclip_comm* c);
 
 /* ---- split API for multi-GPU / process-group runs -------------------------------------
  * A session plans a batch (n_problems >= 1) restricted to candidate shard opt->shard of

@@ -4,8 +4,8 @@ The hot path lives in libeclip.so (CUDA for sm_100a behind the C-ABI of include/
 this package is its thin Python binding (eclip.py) plus the multi-GPU protocol
 (parallel.py).  Build with `python -m paper_2506_12598_b200.build`.
 """
-from .eclip import (EclipError, Profiles, Plan, Session, Planner, plan, plan_batch, plan_problem, alloc_batch_out, lib,
+from .eclip import (EclipError, Profiles, Plan, Session, Planner, Comm, plan, plan_batch, plan_problem, alloc_batch_out, lib,
                     baseline_plan, lookup_table_json, simulate, level_table, BASELINES, MODES, OBJECTIVES, EXPORTS)
 
-__all__ = ["EclipError", "Profiles", "Plan", "Session", "Planner", "plan", "plan_batch", "plan_problem", "alloc_batch_out",
+__all__ = ["EclipError", "Profiles", "Plan", "Session", "Planner", "Comm", "plan", "plan_batch", "plan_problem", "alloc_batch_out",
            "baseline_plan", "lookup_table_json", "simulate", "level_table", "BASELINES", "lib", "MODES", "OBJECTIVES", "EXPORTS"]

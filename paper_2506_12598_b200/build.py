@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["levels.cu", "enum.cu", "slice.cu", "baseline.cu", "runtime.cu", "simulate.cu", "api.cpp"]
+SOURCES = ["levels.cu", "enum.cu", "slice.cu", "baseline.cu", "runtime.cu", "simulate.cu", "comm.cu", "api.cpp"]
 HEADERS = ["engine.h", "exact.cuh", "slice.h"]
 
 

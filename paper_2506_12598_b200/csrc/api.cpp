@@ -382,6 +382,7 @@ struct eclip_session {
     int engine = ECLIP_ENGINE_ENUM;
     int gmax = 0;
     uint64_t scored_local = 0;
+    eclip_comm* comm = nullptr;          // in-library exchange of a sharded plan (opt->comm)
     SliceState slice;
     ~eclip_session() {
         slice.release();
@@ -397,6 +398,10 @@ struct eclip_session {
 
 static int setup_device(eclip_session* s, const eclip_options* opt) {
     s->device = opt ? opt->device : 0;
+    if (opt && opt->comm) {   // the communicator fixes the device and the shard
+        s->comm = (eclip_comm*)opt->comm;
+        s->device = comm_device(s->comm);
+    }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -547,6 +552,10 @@ static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, i
     su.delta = (double)(8 * W + 16) * std::ldexp(1.0, -24);
     su.shard = opt ? opt->shard : 0;
     su.n_shards = opt ? std::max(1, opt->n_shards) : 1;
+    if (s->comm) {
+        su.shard = comm_rank(s->comm);
+        su.n_shards = comm_size(s->comm);
+    }
     su.prune = (opt && opt->no_prune) ? 0 : 1;
 }
 
@@ -1125,6 +1134,18 @@ extern "C" int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n
 static int run_all_steps(eclip_session* s) {
     int rc = step_pass1(s);
     if (rc) return rc;
+    if (s->comm) {   // sharded over the communicator: the three exchanges on device buffers
+        if ((rc = comm_min_f32(s->comm, s->wk.m32, s->n, s->st))) return rc;
+        if (qos_float(s->su)) {
+            if ((rc = comm_min_f32(s->comm, s->wk.m32_sure, s->n, s->st))) return rc;
+        } else {
+            CU(cudaMemcpyAsync(s->wk.m32_sure, s->wk.m32, 4 * (size_t)s->n, cudaMemcpyDeviceToDevice, s->st));
+        }
+        if ((rc = step_pass2_min(s))) return rc;
+        if ((rc = comm_lexmin_u256(s->comm, s->wk.hstar, s->n, s->st))) return rc;
+        if ((rc = step_pass2_first(s))) return rc;
+        return comm_lexmin_u256(s->comm, s->wk.first, s->n, s->st);
+    }
     if (s->engine == ECLIP_ENGINE_ENUM && s->su.n_shards == 1) {   // unsharded: one band rescan
         CU(launch_pass2_both(s->su, s->wk, s->st));
         return ECLIP_OK;
@@ -1202,7 +1223,7 @@ extern "C" int eclip_planner_create(const eclip_profiles* P, const eclip_batch* 
     if (opt) o = *opt; else eclip_default_options(&o);
     if (o.engine != ECLIP_ENGINE_AUTO && o.engine != ECLIP_ENGINE_ENUM)
         return fail(ECLIP_E_INVALID_ARG, "the planner runs the ENUM engine");
-    if (o.n_shards > 1) return fail(ECLIP_E_INVALID_ARG, "the planner plans whole batches (n_shards = 1)");
+    if (o.n_shards > 1 || o.comm) return fail(ECLIP_E_INVALID_ARG, "the planner plans whole batches (n_shards = 1, no comm)");
     o.engine = ECLIP_ENGINE_ENUM;
     o.shard = 0; o.n_shards = 1;
     int rc = check_common(P, b->n_models, b->total_sms, b->switch_max, b->slowdown, b->objective, b->p_idle_w,

@@ -270,3 +270,14 @@ struct BaseOut {
 cudaError_t launch_baseline(const BaseJob& j, BaseOut o, cudaStream_t st);
 
 }  // namespace eclip
+
+// ---- multi-GPU exchange (comm.cu; the C-ABI's eclip_comm) ----
+struct eclip_comm;
+namespace eclip {
+int comm_min_f32(eclip_comm* c, float* buf, int n, cudaStream_t st);        // in place: global MIN (ECLIP_* code)
+int comm_lexmin_u256(eclip_comm* c, U256* buf, int n, cudaStream_t st);     // in place: global lexicographic MIN
+int comm_rank(const eclip_comm* c);
+int comm_size(const eclip_comm* c);
+int comm_device(const eclip_comm* c);
+
+}  // namespace eclip

@@ -648,21 +648,22 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
     const int W = su.W, Lmax = su.Lmax;
     const Lev* gbase = levs + (size_t)prob * su.lev_stride;
     for (int i = threadIdx.x; i < 2 * Lmax; i += blockDim.x) sv[i] = gbase[(size_t)(W - 2) * Lmax + i];
-    if (threadIdx.x == 0) { s_t0 = 0; s_t1 = 0; }
     __syncthreads();
-    if (threadIdx.x < 32) {   // range of hT over the hi workers (warp 0)
+    if (threadIdx.x < 32) {   // range of hT over the hi workers (warp 0; sums in registers, one write)
+        int t0 = 0, t1 = 0;
         for (int w = 0; w < W - 2; w++) {
             int mn = 1 << 30, mx = 0;
             for (int l = threadIdx.x; l < P.L[w]; l += 32) {
-                const int v = gbase[(size_t)w * Lmax + l].S;
+                const int v = (int)gbase[(size_t)w * Lmax + l].S;
                 mn = min(mn, v); mx = max(mx, v);
             }
             for (int o = 16; o; o >>= 1) {
                 mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
                 mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             }
-            if (threadIdx.x == 0) { s_t0 += mn; s_t1 += mx; }
+            t0 += mn; t1 += mx;
         }
+        if (threadIdx.x == 0) { s_t0 = t0; s_t1 = t1; }
     }
     __syncthreads();
     const int t0 = s_t0, tn = (s_t1 - s_t0 + 1 <= FT_CAP && su.has_qos) ? s_t1 - s_t0 + 1 : 0;
@@ -1199,7 +1200,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     if (ub > units) ub = units;
     const int nseg = P.nseg;
     __shared__ unsigned s_inc;
-    __shared__ int s_next, s_stop;
+    __shared__ int s_next;   // next list entry to fetch; raised to the list length to stop every warp
     __shared__ uint8_t s_chunk[P1_THREADS / 32][32];
     float lbm = 0.0f;
     int lcnt = 0;
@@ -1209,7 +1210,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (lcnt == 0) return;
         lst = bb.ulist + (size_t)blockIdx.x * su.upi;
         lbm = __uint_as_float(bb.lbmin[prob]);
-        if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; s_stop = 0; }
+        if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; }
     }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
     // level records + this problem's aux block in one TMA bulk copy
@@ -1352,7 +1353,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (BB) {
             int b0 = 0;
             if (wl == 0) {
-                b0 = *(volatile int*)&s_stop ? lcnt : atomicAdd(&s_next, 32);
+                b0 = atomicAdd(&s_next, 32);
                 if ((nfetch++ & 3) == 0) atomicMin(&s_inc, *(volatile const unsigned*)(bb.inc + prob));
             }
             b0 = __shfl_sync(0xffffffffu, b0, 0);
@@ -1373,7 +1374,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
                 float mn = lb;
                 for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                if (wl == 0 && bb_edge(bb_bucket(mn, lbm), lbm) > bnd) s_stop = 1;
+                if (wl == 0 && bb_edge(bb_bucket(mn, lbm), lbm) > bnd) atomicMax(&s_next, lcnt);   // stop the CTA
                 continue;
             }
         } else {
@@ -1786,8 +1787,8 @@ bool pass1_fast(int L_inner) { return fast_ok(L_inner); }
 int pass1_fast_team(int L_inner) { return fast_team(L_inner); }
 
 // the fast kernel applies when every problem's inner worker fits a warp team
-static bool use_fast(const Setup& su) {
-    return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax);
+static bool use_fast(const Setup& su) {   // (the host's plan_geometry takes the same decision)
+    return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax) && !su.wide;
 }
 
 bool pass1_prunable(const Setup& su) { return su.prune != 0 && su.W >= 3 && use_fast(su); }

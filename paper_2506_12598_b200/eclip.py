@@ -52,7 +52,8 @@ class Result(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("engine", C.c_int32), ("device", C.c_int32), ("cuda_stream", C.c_void_p), ("tie_tol", C.c_double),
-                ("shard", C.c_int32), ("n_shards", C.c_int32), ("no_prune", C.c_int32), ("timing", C.c_int32)]
+                ("shard", C.c_int32), ("n_shards", C.c_int32), ("no_prune", C.c_int32), ("timing", C.c_int32),
+                ("comm", C.c_void_p)]
 
 
 class Batch(C.Structure):
@@ -79,7 +80,8 @@ EXPORTS = ["eclip_load_profiles", "eclip_load_profiles_mem", "eclip_profiles_fro
            "eclip_session_counters",
            "eclip_baseline_plan", "eclip_lookup_table_json", "eclip_simulate", "eclip_level_table",
            "eclip_planner_create", "eclip_planner_plan", "eclip_planner_phase_ms", "eclip_planner_counters",
-           "eclip_planner_free"]
+           "eclip_planner_free", "eclip_comm_unique_id", "eclip_comm_create", "eclip_comm_create_local",
+           "eclip_comm_info", "eclip_comm_free"]
 
 
 def lib():
@@ -123,6 +125,12 @@ def lib():
         L.eclip_planner_counters.argtypes = [vp, P(C.c_uint64), C.c_int32]
         L.eclip_planner_free.argtypes = [vp]
         L.eclip_planner_free.restype = None
+        L.eclip_comm_unique_id.argtypes = [C.c_char_p]
+        L.eclip_comm_create.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, P(vp)]
+        L.eclip_comm_create_local.argtypes = [C.c_int32, C.c_int32, P(vp)]
+        L.eclip_comm_info.argtypes = [vp, P(C.c_int32), P(C.c_int32), P(C.c_int32)]
+        L.eclip_comm_free.argtypes = [vp]
+        L.eclip_comm_free.restype = None
         L.eclip_level_table.argtypes = [vp, C.c_int32, P(C.c_int32), C.c_uint32, C.c_int32, P(Options), C.c_int32,
                                         P(C.c_int64), P(C.c_int64), P(C.c_uint8), P(C.c_int32), P(C.c_int32)]
         _lib = L
@@ -233,7 +241,7 @@ class Plan:
 
 
 def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True,
-             timing=False) -> Options:
+             timing=False, comm=None) -> Options:
     o = Options()
     lib().eclip_default_options(C.byref(o))
     o.engine = ENGINES[engine]
@@ -243,7 +251,54 @@ def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shar
     o.shard, o.n_shards = shard, n_shards
     o.no_prune = 0 if prune else 1
     o.timing = 1 if timing else 0
+    o.comm = comm.handle.value if comm is not None else None
     return o
+
+
+class Comm:
+    """eclip_comm: the in-library exchange of a sharded plan (NCCL, one process per GPU), or one of
+    a local group of communicators in one process (tests).  Pass as comm= to plan / plan_batch."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        b = C.create_string_buffer(128)
+        _check(lib().eclip_comm_unique_id(b))
+        return b.raw
+
+    @classmethod
+    def create(cls, uid: bytes, n_ranks: int, rank: int, device: int) -> "Comm":
+        h = C.c_void_p()
+        _check(lib().eclip_comm_create(uid, n_ranks, rank, device, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def local_group(cls, n_ranks: int, device: int = 0):
+        hs = (C.c_void_p * n_ranks)()
+        _check(lib().eclip_comm_create_local(n_ranks, device, hs))
+        return [cls(h) for h in hs]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        r, n, d = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().eclip_comm_info(self._h, C.byref(r), C.byref(n), C.byref(d)))
+        return dict(rank=r.value, size=n.value, device=d.value)
+
+    def close(self):
+        if self._h is not None and self._h.value and _lib is not None:
+            _lib.eclip_comm_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class _ProblemArgs:
@@ -307,11 +362,12 @@ def _to_plan(r: Result, bufs, G) -> Plan:
 def plan(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
          objective: str = "sum", allowed_mask=None, qos_ns=None, slowdown_matrix=None, group_bounds=None,
          p_idle_w: float = 75.0, p_max_w: float = 225.0, engine: str = "auto", tie_tol: float = 1e-5,
-         device: int = 0, stream=None, prune: bool = True) -> Plan:
-    """eclip_plan: the exact optimum of one co-location problem (§IV-B)."""
+         device: int = 0, stream=None, prune: bool = True, comm: "Comm" = None) -> Plan:
+    """eclip_plan: the exact optimum of one co-location problem (§IV-B); with comm, sharded
+    over the communicator's ranks (every rank returns the same plan)."""
     a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
                      slowdown_matrix, group_bounds, p_idle_w, p_max_w)
-    o = _options(engine, device, stream, tie_tol, prune=prune)
+    o = _options(engine, device, stream, tie_tol, prune=prune, comm=comm)
     r, bufs = _result_buffers(a.W, a.G)
     _check(lib().eclip_plan(profiles.handle, C.byref(a.c), C.byref(o), C.byref(r)))
     return _to_plan(r, bufs, a.G)
@@ -432,7 +488,7 @@ def _batch_out_struct(out) -> BatchOut:
 def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
                objective: str = "sum", qos_ns=None, slowdown_matrix=None, allowed_mask=None, p_idle_w: float = 75.0,
                p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0, stream=None, out=None, gmax: int = 0,
-               prune: bool = True):
+               prune: bool = True, comm: "Comm" = None):
     """eclip_plan_batch: many independent mixes per launch (BASELINE config 5).
 
     With torch CUDA tensors for model_ids / qos_ns / slowdown_matrix (and `out` from
@@ -443,7 +499,7 @@ def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int
     if out is None:
         out = alloc_batch_out(a.n, a.W, gmax, device=(model_ids.device if on_device else None))
     b = _batch_out_struct(out)
-    o = _options("enum", device, stream, tie_tol, prune=prune)
+    o = _options("enum", device, stream, tie_tol, prune=prune, comm=comm)
     _check(lib().eclip_plan_batch(profiles.handle, C.byref(a.c), C.byref(o), C.byref(b)))
     return out
 

@@ -8,8 +8,10 @@ box, gloo in the CPU tests):
     pass 1    float32 minimum of the FP32 filter key        -> all-reduce MIN
     pass 2a   exact 256-bit minimum key                     -> all-gather + lexicographic MIN
     pass 2b   lowest qualifying level tuple (packed 256-bit) -> all-gather + lexicographic MIN
-after which every rank materialises the same plan.  Batches of independent mixes need no
-exchange at all: shard the mixes instead (weak scaling, bench.py).
+after which every rank materialises the same plan.  Two drivers: run_sharded (the split API of
+include/eclip.h, values through torch.distributed — gloo in the CPU tests) and nccl_comm /
+plan_nccl (the library's own NCCL communicator: the exchanges stay on the device, no host round
+trip).  Batches of independent mixes need no exchange at all: shard the mixes instead (bench.py).
 """
 from __future__ import annotations
 
@@ -22,14 +24,17 @@ I64_MAX = np.iinfo(np.int64).max
 
 
 def lexmin_u256(stacked: np.ndarray) -> np.ndarray:
-    """stacked [ranks, n, 4] uint64 little-endian limbs -> [n, 4] lexicographic minimum"""
-    R, n, _ = stacked.shape
+    """stacked [ranks, n, 4] uint64 little-endian limbs -> [n, 4] lexicographic minimum (most
+    significant limb first), vectorised over the n problems"""
     out = stacked[0].copy()
-    for r in range(1, R):
-        cand = stacked[r]
-        for i in range(n):
-            if tuple(cand[i, ::-1]) < tuple(out[i, ::-1]):
-                out[i] = cand[i]
+    for r in range(1, stacked.shape[0]):
+        c = stacked[r]
+        less = np.zeros(out.shape[0], bool)
+        eq = np.ones(out.shape[0], bool)
+        for limb in (3, 2, 1, 0):
+            less |= eq & (c[:, limb] < out[:, limb])
+            eq &= c[:, limb] == out[:, limb]
+        out[less] = c[less]
     return out
 
 
@@ -85,6 +90,27 @@ def plan_distributed(profiles, problem, group=None, **kw):
         return run_sharded(s, TorchComm(group))
     finally:
         s.close()
+
+
+def nccl_comm(group=None, device=None):
+    """The library's own communicator (eclip_comm, NCCL over NVLink / NVSwitch) for the ranks of a
+    torch.distributed group: rank 0 draws the NCCL unique id, the group broadcasts it, every rank
+    creates its communicator on its device.  Pass it as comm= to plan / plan_problem / plan_batch:
+    the library then shards the candidate space and runs the exchanges on device buffers."""
+    import torch
+    import torch.distributed as dist
+    from .eclip import Comm
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    dev = torch.cuda.current_device() if device is None else device
+    return Comm.create(obj[0], world, rank, dev)
+
+
+def plan_nccl(profiles, problem, comm, **kw):
+    """eclip_plan of one problem sharded over `comm` (every rank gets the same plan)."""
+    from .eclip import plan_problem
+    return plan_problem(profiles, problem, comm=comm, **kw)
 
 
 def pack_tuple(levels) -> np.ndarray:

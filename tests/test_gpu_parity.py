@@ -87,7 +87,7 @@ def test_k1_level_tables_vs_oracle():
     rng = np.random.default_rng(17)
     for t in range(60):
         G = int(rng.integers(1, 10))
-        Cn = int(rng.integers(1, 9))
+        Cn = int(rng.integers(2, 9))
         sizes = synth.lattice_sizes(Cn, 148) if t % 3 else sorted(int(x) for x in rng.choice(np.arange(1, 60), Cn, replace=False))
         K = G + int(rng.integers(0, 4))
         mdl = synth.synthesize_model("k", ["uniform", "vgg", "bert", "shufflenet"][t % 4], K, sizes, 4000 + t)
@@ -593,3 +593,78 @@ def test_heterogeneous_batch_and_lcm_boundary():
     with pytest.raises(ec.EclipError) as e:
         _gpu(p, "enum")
     assert e.value.code == ec.eclip.E_TOO_LARGE
+
+
+# ---------------------------------------------------------------- in-library multi-GPU exchange
+def _threads(fn, n):
+    import threading
+    res, errs = [None] * n, []
+
+    def run(r):
+        try:
+            res[r] = fn(r)
+        except Exception as e:   # noqa: BLE001
+            errs.append(e)
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    return res
+
+
+def test_comm_nccl_world_one_vs_oracle():
+    """eclip_comm over NCCL at world size 1 (one B200): the in-library sharded path (device-side
+    exchanges) gives the oracle's plans for ENUM and SLICE problems and a batch"""
+    import golden_c5
+    c = ec.Comm.create(ec.Comm.unique_id(), 1, 0, 0)
+    assert c.info() == dict(rank=0, size=1, device=0)
+    gold = _gold()
+    p = synth.make_c2()
+    pr = ec.Profiles.from_models(p.models)
+    _same(ec.plan_problem(pr, p, engine="enum", comm=c), oracle.solve(p), "C2 nccl enum")
+    _same(ec.plan_problem(pr, p, engine="slice", comm=c), oracle.solve(p), "C2 nccl slice")
+    p4 = synth.make_c4()
+    _check_gold(ec.plan_problem(ec.Profiles.from_models(p4.models), p4, comm=c), gold["C4"], "C4 nccl")
+    models, ids, qos = synth.make_c5(256, seed=2)
+    out = ec.plan_batch(ec.Profiles.from_models(models), ids, total_sms=148, qos_ns=qos, p_idle_w=200.0,
+                        p_max_w=1000.0, comm=c, gmax=16)
+    assert golden_c5.check_batch(ids, out, sizes=models[0].sizes) == 256
+    c.close()
+
+
+@pytest.mark.parametrize("n_ranks", [2, 3])
+def test_comm_local_group_sharded_vs_oracle(n_ranks):
+    """the sharded protocol with the exchanges inside the library: n ranks on one GPU (a local group
+    of communicators, one host thread per rank), each planning its shard; every rank returns the
+    oracle's plan (ENUM, SLICE, MATRIX+QoS with its surely-feasible minimum, a wide problem, a batch)"""
+    import golden_c5
+    gold = _gold()
+    pc3 = synth.make_c3("matrix")
+    pc3.qos_ns = synth.qos_3x(pc3.models, pc3.model_ids, factor=3.5)
+    cases = [(synth.make_c2(), "enum", oracle.solve(synth.make_c2())),
+             (synth.make_c2("excess", "max"), "slice", oracle.solve(synth.make_c2("excess", "max"))),
+             (pc3, "enum", oracle.solve(pc3)),
+             (synth.make_c4(), "slice", gold["C4"]),
+             (_hetero_problem((200, 199, 97), 2, 14, qos=3.0), "enum", None)]
+    for p, eng, o in cases:
+        if o is None:
+            o = oracle.solve(p, "enum")
+        pr = ec.Profiles.from_models(p.models)
+        comms = ec.Comm.local_group(n_ranks, 0)
+        outs = _threads(lambda r: ec.plan_problem(pr, p, engine=eng, comm=comms[r]), n_ranks)
+        for g in outs:
+            if isinstance(o, dict):
+                _check_gold(g, o, f"{p.name} local x{n_ranks}")
+            else:
+                _same(g, o, f"{p.name} {eng} local x{n_ranks}")
+        for c in comms:
+            c.close()
+    models, ids, qos = synth.make_c5(128, seed=5)
+    pr = ec.Profiles.from_models(models)
+    comms = ec.Comm.local_group(n_ranks, 0)
+    outs = _threads(lambda r: ec.plan_batch(pr, ids, total_sms=148, qos_ns=qos, p_idle_w=200.0, p_max_w=1000.0,
+                                            comm=comms[r], gmax=16), n_ranks)
+    for out in outs:
+        assert golden_c5.check_batch(ids, out, sizes=models[0].sizes) == 128
