@@ -22,7 +22,7 @@ import json
 import os
 import subprocess
 from dataclasses import dataclass, field
-from decimal import Decimal, ROUND_HALF_EVEN, InvalidOperation
+from decimal import Decimal, ROUND_HALF_EVEN, ROUND_HALF_UP, InvalidOperation
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -48,7 +48,8 @@ class _Problem(C.Structure):
     _fields_ = [("W", C.c_int32), ("N", C.c_int32), ("mode", C.c_int32), ("objective", C.c_int32),
                 ("L", C.POINTER(C.c_int32)), ("S", C.POINTER(C.c_int64)), ("B", C.POINTER(C.c_int64)),
                 ("K", C.POINTER(C.c_int64)), ("Q", C.POINTER(C.c_double)), ("M", C.POINTER(C.c_float)),
-                ("p_idle", C.c_float), ("p_max", C.c_float), ("tol_num", C.c_int64), ("tol_den", C.c_int64)]
+                ("p_idle", C.c_float), ("p_max", C.c_float), ("tol_num", C.c_int64), ("tol_den", C.c_int64),
+                ("wt", C.POINTER(C.c_int64)), ("wval", C.POINTER(C.c_double))]
 
 
 class _Result(C.Structure):
@@ -177,6 +178,33 @@ def levels(beta: np.ndarray, n: np.ndarray, sizes: Sequence[int], mask: int, R: 
     return S[:L].copy(), B[:L].copy(), wit[:L * G].reshape(L, G).copy()
 
 
+def weight_ints(weights, W: int):
+    """Per-worker objective weights ("weights: per-worker scalar (default all 1)",
+    invariant "weights all strictly positive"; reading R20).  Each weight is taken as
+    the integer n_w = round-half-up(omega_w x 1e6), omega_w x 1e6 computed in binary64, so the
+    objective uses omega_w = n_w / 1e6 exactly; the exact keys use n_w / gcd_w(n_w) (a common
+    positive factor changes neither the arg-min nor the relative tolerance).  Valid: finite,
+    0 < omega_w <= 1000 and n_w >= 1.  Returns (ints, values) or raises ValueError."""
+    import math
+    if weights is None:
+        return [1] * W, [1.0] * W
+    if len(weights) != W:
+        raise ValueError("weights must have one entry per worker")
+    n = []
+    for x in weights:
+        x = float(x)
+        if not (math.isfinite(x) and 0.0 < x <= 1000.0):
+            raise ValueError(f"weight {x} outside (0, 1000]")
+        v = int(Decimal(x * 1e6).quantize(Decimal(1), rounding=ROUND_HALF_UP))
+        if v < 1:
+            raise ValueError(f"weight {x} rounds to 0 at 1e-6 resolution")
+        n.append(v)
+    g = 0
+    for v in n:
+        g = math.gcd(g, v)
+    return [v // g for v in n], [v / 1e6 for v in n]
+
+
 def tol_rational(tol: float):
     """tau as the rational round(tol * 1e9) / 1e9."""
     return int(round(tol * 1e9)), 1_000_000_000
@@ -203,6 +231,7 @@ class OracleResult:
     power_w: float = float("nan")
     energy_j: float = float("nan")
     throughput_rps: float = float("nan")
+    energy_busy_j: float = float("nan")
     group_latency_ns: List[List[float]] = field(default_factory=list)
     tables: list = field(default_factory=list)
 
@@ -235,11 +264,16 @@ class Prepared:
         M = p.slowdown_matrix if p.slowdown_matrix is not None else np.zeros((W, W), np.float32)
         self.M = np.ascontiguousarray(M, dtype=np.float32).reshape(-1)
         tn, td = tol_rational(tol)
+        wi, wv = weight_ints(getattr(p, "weights", None), W)
+        self.weighted = getattr(p, "weights", None) is not None
+        self.wt = np.array(wi, dtype=np.int64)
+        self.wval = np.array(wv, dtype=np.float64)
         self.c = _Problem(W, p.total_sms, MODES[p.mode], OBJECTIVES[p.objective],
                           self.L.ctypes.data_as(C.POINTER(C.c_int32)), self.S.ctypes.data_as(C.POINTER(C.c_int64)),
                           self.B.ctypes.data_as(C.POINTER(C.c_int64)), self.K.ctypes.data_as(C.POINTER(C.c_int64)),
                           self.Q.ctypes.data_as(C.POINTER(C.c_double)), self.M.ctypes.data_as(C.POINTER(C.c_float)),
-                          p.p_idle_w, p.p_max_w, tn, td)
+                          p.p_idle_w, p.p_max_w, tn, td, self.wt.ctypes.data_as(C.POINTER(C.c_int64)),
+                          self.wval.ctypes.data_as(C.POINTER(C.c_double)))
 
     @property
     def n_tuples(self) -> int:
@@ -269,7 +303,35 @@ class Prepared:
             out.group_sm.append([sizes[j] for j in cols])
             out.switches.append(sum(1 for g in range(1, len(cols)) if cols[g] != cols[g - 1]))
             out.group_latency_ns.append([float(beta[g, cols[g]]) * (1.0 + out.alpha[w]) for g in range(len(cols))])
+        p = self.problem
+        out.energy_busy_j = busy_energy_sweep(out.group_sm, out.group_latency_ns, p.total_sms,
+                                              float(np.float32(p.p_idle_w)), float(np.float32(p.p_max_w))) * 1e-9
         return out
+
+
+def busy_energy_sweep(group_sm, group_lat, total: int, p_idle: float, p_max: float) -> float:
+    """Busy-SM energy of a plan's predicted run (SPEC integrate_energy S:416-419 with power_at
+    S:406-409; reading R21), in W x ns: all workers start at 0 and run their groups back
+    to back (group g of worker w on group_sm[w][g] SMs for group_lat[w][g] ns); between consecutive
+    group boundaries the power is p_idle + (p_max - p_idle) min(N, sum of running groups' SMs) / N.
+    An event loop: repeatedly advance to the earliest current-group end over the workers."""
+    W = len(group_sm)
+    g = [0] * W                                   # current group of each worker
+    end = [group_lat[w][0] if group_lat[w] else 0.0 for w in range(W)]
+    t, E = 0.0, 0.0
+    while True:
+        live = [w for w in range(W) if g[w] < len(group_lat[w])]
+        if not live:
+            return E
+        nxt = min(end[w] for w in live)
+        busy = sum(group_sm[w][g[w]] for w in live)
+        E += (p_idle + (p_max - p_idle) * min(busy, total) / total) * (nxt - t)
+        t = nxt
+        for w in live:
+            if end[w] == nxt:                     # this worker's group ends now: start its next one
+                g[w] += 1
+                if g[w] < len(group_lat[w]):
+                    end[w] = end[w] + group_lat[w][g[w]]
 
 
 def solve(problem, engine: str = "enum", tol: float = 1e-5) -> OracleResult:

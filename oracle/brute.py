@@ -8,7 +8,8 @@ Follows PAPER.md §IV-B term by term, for tiny instances:
   CUAverage_w = sum_k c_k / #kernels_w
   CUOverlap_w = per slowdown mode (P:314 and readings c3-O / c3-M)
   alpha_w = CUOverlap_w / total#CUs ;  e_k = beta_k (1 + alpha_w)
-  objective: SUM_w sum_{k in w} e_k (equal weights), or MAX, or ENERGY =
+  objective: SUM_w omega_w sum_{k in w} e_k (equal weights omega = 1; SPEC S:130 per-worker
+  weights, reading R20), or MAX_w omega_w sum_k e_k, or ENERGY =
   power x makespan, power = p_idle + (p_max - p_idle) min(1, sum_w CUAverage_w / N)
   (SPEC power_at S:406-409 applied to the paper's CUAverage abstraction).
   QoS (optional): sum_{k in w} e_k <= Q_w.
@@ -64,6 +65,45 @@ def alpha(overlap, total):
     return Fraction(overlap) / total
 
 
+def weight_values(weights, W):
+    """omega_w as exact rationals round-half-up(omega_w x 1e6 in binary64) / 1e6 (reading R20;
+    SPEC S:130: strictly positive, default all 1)."""
+    from decimal import Decimal, ROUND_HALF_UP
+    if weights is None:
+        return [Fraction(1)] * W
+    return [Fraction(int(Decimal(float(x) * 1e6).quantize(Decimal(1), rounding=ROUND_HALF_UP)), 10**6)
+            for x in weights]
+
+
+def busy_energy(group_sm, group_lat, total, p_idle, p_max):
+    """Busy-SM energy integral of a plan's predicted co-located run (SPEC integrate_energy S:416-419,
+    power_at S:406-409; reading R21): every worker starts at t = 0 and runs its groups back to back,
+    group g of worker w occupying group_sm[w][g] SMs for group_lat[w][g]; busy(t) = min(N, sum of the
+    running groups' SMs); E = integral over [0, makespan] of p_idle + (p_max - p_idle) busy(t) / N.
+    Exact when the inputs are Fractions.  Returns joules per ns-unit (the caller scales)."""
+    W = len(group_sm)
+    ends = []                           # per worker: group end times
+    for w in range(W):
+        t, e = 0, []
+        for d in group_lat[w]:
+            t = t + d
+            e.append(t)
+        ends.append(e)
+    cuts = sorted({0} | {x for e in ends for x in e})
+    E = 0
+    for a, b in zip(cuts, cuts[1:]):
+        busy = 0
+        for w in range(W):
+            start = 0
+            for g, end in enumerate(ends[w]):
+                if start <= a and b <= end and end > start:
+                    busy += group_sm[w][g]
+                    break
+                start = end
+        E += (p_idle + (p_max - p_idle) * Fraction(min(busy, total), total)) * (b - a)
+    return E
+
+
 def power_at(busy, total, p_idle, p_max):
     """p_idle + (p_max - p_idle) * min(1, busy / total) (capped per c3-E)."""
     frac = min(Fraction(1), Fraction(busy) / total)
@@ -115,10 +155,11 @@ def evaluate(problem, choice):
         if p.qos_ns is not None and p.qos_ns[w] != float("inf") and Lw > Fraction(p.qos_ns[w]):
             feas = False
     pw = power_at(sum(avg), p.total_sms, Fraction(float(np.float32(p.p_idle_w))), Fraction(float(np.float32(p.p_max_w))))
+    om = weight_values(getattr(p, "weights", None), W)
     if p.objective == "sum":
-        key = sum(L)
+        key = sum(o * x for o, x in zip(om, L))
     elif p.objective == "max":
-        key = max(L)
+        key = max(o * x for o, x in zip(om, L))
     else:
         key = pw * max(L)
     return feas, key, L, pw, al

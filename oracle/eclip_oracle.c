@@ -28,7 +28,8 @@
  *   O^_w = CUOverlap_w * Lambda * 2^E:  EXCLUDE_SELF (T'-S'_w) | PAPER T' | EXCESS
  *          max(0, T' - Lambda N) | MATRIX sum_{v!=w} M_wv 2^E S'_v,
  *   h_w  = B_w (D + O^_w)            so  L_w = sum_k e_k = B_w (1 + alpha_w) = h_w / D,
- *   SUM: sum_w h_w;  MAX: max_w h_w;
+ *   SUM: sum_w omega_w h_w;  MAX: max_w omega_w h_w  (omega_w = per-worker weight integers, SPEC S:130;
+ *        all 1 = the paper's "identically weighted" objective);
  *   ENERGY: (p_idle Lambda N + (p_max - p_idle) min(Lambda N, T')) 2^k * max_w h_w
  *   QoS: L_w <= Q_w  <=>  h_w <= Q_w D (exact dyadic compare).
  * All keys share one positive denominator per problem, so comparing these integers is
@@ -256,6 +257,10 @@ typedef struct {
     const float* M;         /* [W*W] slowdown matrix (MATRIX only), entries >= 0 */
     float p_idle, p_max;
     int64_t tol_num, tol_den;   /* tau = tol_num / tol_den */
+    const int64_t* wt;      /* [W] per-worker objective weights as positive integers ("weights: per-worker
+                               scalar (default all 1)"; reading R20: round(omega 1e6) divided by the gcd
+                               over workers); NULL = all 1 (the paper's equal weights) */
+    const double* wval;     /* [W] the weights' values round(omega 1e6) / 1e6 (FP64 objective), NULL = all 1 */
 } or_problem;
 
 typedef struct {
@@ -280,6 +285,7 @@ typedef struct {
     const double* Q;
     u128 pi_idle, pi_dyn;   /* p * 2^k  (exact integers) */
     int64_t tol_num, tol_den;
+    int64_t wt[OR_MAXW];    /* objective weights (integers, 1 = unweighted) */
 } or_ctx;
 
 static int64_t gcd64(int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; }
@@ -326,6 +332,12 @@ static int or_ctx_init(const or_problem* p, or_ctx* c) {
     c->pi_idle = (u128)ldexp(pi, k);
     c->pi_dyn = (u128)ldexp(pm, k) - c->pi_idle;
     c->tol_num = p->tol_num; c->tol_den = p->tol_den;
+    /* weights: SUM and MAX only (energy is a physical quantity: no per-worker weights) */
+    for (int w = 0; w < p->W; w++) {
+        c->wt[w] = p->wt ? p->wt[w] : 1;
+        if (c->wt[w] < 1 || c->wt[w] > ((int64_t)1 << 30)) return -1;
+        if (p->objective == OR_ENERGY && c->wt[w] != c->wt[0]) return -1;
+    }
     return 0;
 }
 static void or_ctx_free(or_ctx* c) { free(c->off); free(c->Sp); }
@@ -349,15 +361,18 @@ static u128 or_overlap(const or_ctx* c, const int32_t* lv, int w, int64_t Tp) {
 static int or_key(const or_ctx* c, const int32_t* lv, u256* key) {
     int64_t Tp = 0;
     for (int w = 0; w < c->W; w++) Tp += c->Sp[c->off[w] + lv[w]];
-    u128 sum = 0, mx = 0;
+    u256 sum = u256_zero(), wmx = u256_zero();
+    u128 mx = 0;
     for (int w = 0; w < c->W; w++) {
         u128 h = (u128)c->B[c->off[w] + lv[w]] * (c->D + or_overlap(c, lv, w, Tp));   /* h_w = B_w (D + O^_w) */
         if (!le_dyadic(h, c->Q[w], c->D)) return 1;                                   /* L_w <= Q_w */
-        sum += h;
+        u256 wh = u256_mul128((u128)c->wt[w], h);                                     /* omega_w h_w */
+        sum = u256_add(sum, wh);
+        if (u256_cmp(wh, wmx) > 0) wmx = wh;
         if (h > mx) mx = h;
     }
-    if (c->obj == OR_SUM) *key = u256_from128(sum);
-    else if (c->obj == OR_MAX) *key = u256_from128(mx);
+    if (c->obj == OR_SUM) *key = sum;
+    else if (c->obj == OR_MAX) *key = wmx;
     else {
         int64_t occ = Tp < c->lamN ? Tp : c->lamN;                                    /* min(Lambda N, T') */
         u128 pn = c->pi_idle * (u128)c->lamN + c->pi_dyn * (u128)occ;
@@ -505,7 +520,8 @@ static u128 or_slice_dp(or_slice_ctx* s, int64_t T) {
         for (int l = 0; l < p->L[w]; l++) {
             lv[w] = l;
             u128 h = (u128)c->B[c->off[w] + l] * (c->D + or_overlap(c, lv, w, Tp));
-            s->h[c->off[w] + l] = le_dyadic(h, c->Q[w], c->D) ? h : OR_U128_INF;
+            /* the weighted term omega_w h_w (or_slice checked that it fits with room for W of them) */
+            s->h[c->off[w] + l] = le_dyadic(h, c->Q[w], c->D) ? h * (u128)c->wt[w] : OR_U128_INF;
         }
         lv[w] = 0;
     }
@@ -553,6 +569,7 @@ static u128 or_slice_dp(or_slice_ctx* s, int64_t T) {
 
 static u256 or_slice_key(const or_ctx* c, int obj, int64_t Tp, u128 v) {
     if (obj != OR_ENERGY) return u256_from128(v);
+    v /= (u128)c->wt[0];   /* ENERGY: uniform weights (or_ctx_init), the DP carried wt[0] max h */
     int64_t occ = Tp < c->lamN ? Tp : c->lamN;
     u128 pn = c->pi_idle * (u128)c->lamN + c->pi_dyn * (u128)occ;
     return u256_mul128(pn, v);
@@ -588,6 +605,21 @@ int or_slice(const or_problem* p, or_result* r) {
     s.dlo = (int64_t*)calloc((size_t)W + 1, sizeof(int64_t)); s.dhi = (int64_t*)calloc((size_t)W + 1, sizeof(int64_t));
     for (int w = 1; w < W; w++) s.D[w] = (u128*)malloc(sizeof(u128) * (size_t)(s.shi[w] - s.slo[w] + 1));
     s.h = (u128*)malloc(sizeof(u128) * (size_t)tot);
+    {   /* every weighted term must fit u128 with room for the sum over W workers */
+        u128 lim = (~(u128)0) / (u128)(W + 1);
+        for (int w = 0; w < W; w++)
+            for (int l = 0; l < p->L[w]; l++) {
+                u128 hmax = (u128)p->B[c.off[w] + l] * (c.D + (u128)(s.shi[0] * gS) + (u128)c.lamN);
+                if (hmax > lim / (u128)c.wt[w]) {
+                    r->status = -1;
+                    free(s.h);
+                    for (int v = 1; v < W; v++) free(s.D[v]);
+                    free(s.D); free(s.dlo); free(s.dhi); free(s.smin); free(s.smax); free(s.slo); free(s.shi);
+                    or_ctx_free(&c);
+                    return -1;
+                }
+            }
+    }
 
     int64_t Tlo = s.slo[0], Thi = s.shi[0];
     u256* J = (u256*)malloc(sizeof(u256) * (size_t)(Thi - Tlo + 1));
@@ -667,7 +699,8 @@ done:
 /*   CUAverage_w = S_w / K_w; CUOverlap_w per mode (c3-O/c3-M);             */
 /*   alpha_w = CUOverlap_w / N; L_w = B_w (1 + alpha_w) = sum_k e_k;        */
 /*   power = p_idle + (p_max - p_idle) min(1, sum_w CUAverage_w / N) (c3-E);    */
-/*   makespan = max_w L_w; energy = power x makespan; throughput = sum_w 1e9 / L_w.        */
+/*   makespan = max_w L_w; energy = power x makespan; throughput = sum_w 1e9 / L_w;        */
+/*   objective SUM = sum_w omega_w L_w, MAX = max_w omega_w L_w (omega = wval, default 1). */
 /* out: [0..W-1] L_w (ns); [W] objective; [W+1] makespan (ns); [W+2] power (W);             */
 /*      [W+3] energy (J); [W+4] throughput (1/s); [W+5+w] alpha_w.                          */
 /* ------------------------------------------------------------------------------------ */
@@ -684,7 +717,7 @@ int or_eval_f64(const or_problem* p, const int32_t* lv, double* out) {
         sum_avg += avg[w];
         off += p->L[w];
     }
-    double mk = 0.0, obj = 0.0, thr = 0.0;
+    double mk = 0.0, wmk = 0.0, obj = 0.0, thr = 0.0;
     for (int w = 0; w < W; w++) {
         double ov;
         if (p->mode == OR_EXCLUDE_SELF) ov = sum_avg - avg[w];
@@ -699,13 +732,15 @@ int or_eval_f64(const or_problem* p, const int32_t* lv, double* out) {
         out[w] = Lw;
         out[W + 5 + w] = alpha;
         if (Lw > mk) mk = Lw;
-        obj += Lw;
+        double om = p->wval ? p->wval[w] : 1.0;     /* objective weight (SUM / MAX) */
+        obj += om * Lw;
+        if (om * Lw > wmk) wmk = om * Lw;
         thr += 1e9 / Lw;
     }
     double frac = sum_avg / (double)p->N;
     if (frac > 1.0) frac = 1.0;
     double pw = (double)p->p_idle + ((double)p->p_max - (double)p->p_idle) * frac;
-    if (p->objective == OR_MAX) obj = mk;
+    if (p->objective == OR_MAX) obj = wmk;
     else if (p->objective == OR_ENERGY) obj = pw * mk;
     out[W] = obj;
     out[W + 1] = mk;

@@ -44,6 +44,7 @@ class Problem:
     group_bounds: Optional[List[Optional[List[int]]]] = None
     p_idle_w: float = 75.0
     p_max_w: float = 225.0
+    weights: Optional[List[float]] = None   # per-worker objective weights; None = all 1
 
     @property
     def W(self) -> int:
@@ -231,4 +232,6 @@ def problem_hash(p: Problem) -> str:
                          p.allowed_mask, p.qos_ns, p.group_bounds, p.p_idle_w, p.p_max_w]).encode())
     if p.slowdown_matrix is not None:
         h.update(np.ascontiguousarray(p.slowdown_matrix, dtype=np.float32).tobytes())
+    if p.weights is not None:
+        h.update(json.dumps([float(x) for x in p.weights]).encode())
     return h.hexdigest()[:16]

@@ -400,3 +400,136 @@ def test_c5_golden_table_is_the_live_oracle():
             assert float(a[4]) == r.objective
             assert a[5] == "".join("%x" % c for row in r.group_cols for c in row)
 
+
+
+# ---------------------------------------------------------------- per-worker weights (reading R20)
+def _ex1_weighted(objective, weights):
+    gold = json.load(open(GOLD))
+    case = dict(gold["cases"][0])        # Ex1: two 'heavy' workers, one group each, ExcludeSelf
+    case["objective"] = objective
+    p = _golden_problem(case, gold)
+    p.weights = weights
+    return p
+
+
+@pytest.mark.parametrize("objective,expect_sizes,expect_J_us", [
+    # weights (3, 1), hand-enumerated over the 16 plans (SURVEY App. B profile 'heavy' = 80/40/27/20 us):
+    # SUM  3 L0 + L1: (60,45) = 3*20*1.75 + 27*2 = 105 + 54 = 159 < (60,60) = 160 < (60,30) = 170
+    ("sum", [[60], [45]], 159.0),
+    # MAX  max(3 L0, L1): (60,30) = max(3*20*1.5, 40*2) = max(90, 80) = 90 < (60,45) = 105
+    ("max", [[60], [30]], 90.0)])
+def test_weighted_worked_example(objective, expect_sizes, expect_J_us):
+    """Hand-worked weighted Ex1: weights change the decision (unweighted optimum is (60,60))."""
+    p = _ex1_weighted(objective, [3.0, 1.0])
+    a = brute.brute_force(p)
+    assert [[15, 30, 45, 60][j] for s in a["sigmas"] for j in s] == [x for s in expect_sizes for x in s]
+    assert float(a["key"]) == pytest.approx(expect_J_us * 1000, rel=1e-12)
+    for engine in ("enum", "slice"):
+        b = oracle.solve(p, engine)
+        assert b.group_sm == expect_sizes, engine
+        assert b.objective == pytest.approx(expect_J_us * 1000, rel=1e-12), engine
+
+
+def test_weight_rounding_and_validation():
+    """R20: omega -> round-half-up(omega 1e6) / 1e6; exact keys use the gcd-reduced integers."""
+    assert oracle.weight_ints([2.0, 1.0, 0.5], 3) == ([4, 2, 1], [2.0, 1.0, 0.5])
+    assert oracle.weight_ints([0.1, 0.2, 0.7], 3)[0] == [1, 2, 7]
+    assert oracle.weight_ints(None, 2) == ([1, 1], [1.0, 1.0])
+    assert oracle.weight_ints([1.0000004, 1.0], 2)[0] == [1, 1]          # below the 1e-6 resolution
+    assert oracle.weight_ints([2.5e-6, 1.0], 2)[0][0] == 3                # ... 2.5 rounds half up
+    for bad in ([0.0, 1.0], [-1.0, 1.0], [float("nan"), 1.0], [1001.0, 1.0], [1e-7, 1.0]):
+        with pytest.raises(ValueError):
+            oracle.weight_ints(bad, 2)
+
+
+def test_weighted_equals_brute_force_random():
+    """O-B (level reduction, exact integer keys, enum and slice) == O-A (literal brute force in
+    Fractions) with random per-worker weights, every mode and SUM / MAX; uniform weights give the
+    unweighted answer with the identical exact key (the gcd reduction makes them all 1)."""
+    rng = np.random.default_rng(20)
+    n = 0
+    for s in range(240):
+        p = synth.random_tiny_problem(5000 + s)
+        p.objective = ("sum", "max")[s % 2]
+        if p.mode == "matrix" and p.slowdown_matrix is None:
+            p.mode = "exclude_self"
+        p.weights = [float(x) for x in rng.choice([0.25, 0.5, 1.0, 1.5, 2.0, 3.0, 0.1, 7.3], size=p.W)]
+        try:
+            a = brute.brute_force(p)
+        except ValueError:
+            continue
+        b = oracle.solve(p)
+        if a is None:
+            assert b.status == "infeasible", s
+            continue
+        assert b.group_cols == a["sigmas"], s
+        assert b.objective == pytest.approx(float(a["key"]), rel=1e-12), s
+        if p.mode != "matrix":
+            c = oracle.solve(p, "slice")
+            assert (c.group_cols, c.key) == (b.group_cols, b.key), s
+        u = synth.Problem(**{**p.__dict__, "weights": [2.5] * p.W})
+        u0 = synth.Problem(**{**p.__dict__, "weights": None})
+        ru, r0 = oracle.solve(u), oracle.solve(u0)
+        assert (ru.status, ru.group_cols, ru.key) == (r0.status, r0.group_cols, r0.key), s
+        assert ru.objective == pytest.approx(2.5 * r0.objective, rel=1e-12)
+        n += 1
+    assert n >= 150
+
+
+def test_weighted_energy_rejected_unless_uniform():
+    p = _ex1_weighted("energy", [2.0, 1.0])
+    with pytest.raises(ValueError):
+        oracle.solve(p)
+    p.weights = [2.0, 2.0]
+    p0 = _ex1_weighted("energy", None)
+    assert oracle.solve(p).key == oracle.solve(p0).key
+
+
+# ---------------------------------------------------------------- busy-SM energy integral (S:416-419, reading R21)
+def test_busy_energy_hand_values():
+    """Hand integral, N = 60, p_idle 75 W, p_max 225 W: worker 0 runs 30 SMs for 100 ns then 60 SMs
+    for 50 ns; worker 1 runs 15 SMs for 120 ns.  [0,100): busy 45 -> 187.5 W x 100 = 18750;
+    [100,120): 75 -> capped at 60 -> 225 x 20 = 4500; [120,150): 60 -> 225 x 30 = 6750; total 30000 W ns."""
+    sm, lat = [[30, 60], [15]], [[100, 50], [120]]
+    assert oracle.busy_energy_sweep(sm, lat, 60, 75.0, 225.0) == pytest.approx(30000.0, rel=1e-15)
+    exact = brute.busy_energy(sm, [[Fraction(x) for x in r] for r in lat], 60, Fraction(75), Fraction(225))
+    assert exact == 30000
+    # S:417 "empty timeline of duration T -> p_idle T"; one kernel of 60 CUs, 10 us in a 1 ms window
+    assert oracle.busy_energy_sweep([[60], [0]], [[10_000], [1_000_000]], 60, 75.0, 225.0) == pytest.approx(
+        75.0 * 1e6 + 150.0 * 1e4, rel=1e-15)
+    # S:418 additivity: splitting a group's interval leaves the integral unchanged
+    assert oracle.busy_energy_sweep([[30, 30, 60], [15]], [[40, 60, 50], [120]], 60, 75.0, 225.0) == pytest.approx(
+        30000.0, rel=1e-15)
+
+
+def test_busy_energy_single_worker_closed_form_and_paper_example():
+    """One worker with every size <= N: E = p_idle L + (p_max - p_idle) sum_g c_g e_g / N.  And App. B
+    Ex2 (R=1, ExcludeSelf, SUM): A(60,15), B(15,60), every e = beta x 1.625, busy >= 75 > 60 throughout,
+    so E = 225 W x 48.75 us = 10968.75 W us = power x makespan."""
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        G = int(rng.integers(1, 6))
+        c = [int(x) for x in rng.choice([15, 30, 45, 60], size=G)]
+        e = [float(x) for x in rng.uniform(1, 1000, size=G)]
+        ref = 75.0 * sum(e) + 150.0 * sum(ci * ei for ci, ei in zip(c, e)) / 60
+        assert oracle.busy_energy_sweep([c], [e], 60, 75.0, 225.0) == pytest.approx(ref, rel=1e-13)
+    gold = json.load(open(GOLD))
+    case = [c for c in gold["cases"] if c["name"].startswith("Ex2") and c["R"] == 1 and c["mode"] == "exclude_self"
+            and c["objective"] == "sum"][0]
+    b = oracle.solve(_golden_problem(case, gold))
+    assert b.energy_busy_j == pytest.approx(10968.75e-6 * 1e-3 * 1000, rel=1e-12)   # W us -> J
+
+
+def test_busy_energy_sweep_equals_exact_integral_random():
+    """O-B's event loop (floats) == O-A's interval integral in Fractions on random plans, and
+    E_busy <= power_max x makespan, >= p_idle x makespan."""
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        W = int(rng.integers(1, 5))
+        sm = [[int(x) for x in rng.choice([14, 28, 70, 140, 148], size=int(rng.integers(1, 6)))] for _ in range(W)]
+        lat = [[int(x) for x in rng.integers(1, 10_000, size=len(r))] for r in sm]
+        f = oracle.busy_energy_sweep(sm, [[float(x) for x in r] for r in lat], 148, 200.0, 1000.0)
+        ex = brute.busy_energy(sm, [[Fraction(x) for x in r] for r in lat], 148, Fraction(200), Fraction(1000))
+        assert f == pytest.approx(float(ex), rel=1e-12)
+        mk = max(sum(r) for r in lat)
+        assert 200.0 * mk * (1 - 1e-12) <= f <= 1000.0 * mk * (1 + 1e-12)
