@@ -45,6 +45,7 @@ WORKLOAD = ("C5 batched planning: 4096 mixes x 4 models (7-model library, draws 
             "x 8 pool sizes {18..144} of N=148 SMs, switchMax=14, EXCLUDE_SELF, SUM, QoS 3x isolated")
 N_MIXES = 4096
 ALG_OPS_PER_CAND = 17   # 4W+1 FP32 ops per scored candidate (SUM, W = 4)
+KERNEL_FMA_PER_CAND = 2  # the kernel's own FMA-pipe work per scored candidate (bilinear form)
 
 
 def parse():
@@ -442,14 +443,17 @@ def context_lines(ec, torch, pr, ids, qos, d_ids, d_qos, stream, flush, kw, n, c
                 steps.append(sum(p.phase_ms().values()))
         k_ms = float(np.median(kms))
         e = int(np.median(ev))
-        ach = ALG_OPS_PER_CAND * e / (k_ms * 1e-3) / 1e9
+        ach = KERNEL_FMA_PER_CAND * e / (k_ms * 1e-3) / 1e9
         res[f"roofline_{name}"] = {
-            "bound": "alu", "kernel": f"k_pass1_fast<W=4,EXCLUDE_SELF,{'QoS' if use_q else 'noQoS'},exhaustive>",
-            "achieved": ach, "peak": peak, "frac": ach / peak, "unit": "G FP32 lane-ops/s",
-            "kernel_ms_per_launch": k_ms, "evaluated_candidates_per_launch": e,
+            "bound": "fma_pipe", "kernel": f"k_pass1_fast<W=4,EXCLUDE_SELF,{'QoS' if use_q else 'noQoS'},exhaustive>",
+            "achieved": ach, "peak": peak, "frac": ach / peak, "unit": "G FP32 FMA-pipe lane-ops/s",
+            "ops_per_unit": KERNEL_FMA_PER_CAND, "kernel_ms_per_launch": k_ms, "evaluated_candidates_per_launch": e,
             "evaluated_fraction": e / cand_step, "step_ms": float(np.median(steps)),
-            "note": "no branch and bound: every QoS-feasible level tuple's FP32 key is computed (2 packed FMAs "
-                    "+ a min per tuple); achieved counts SURVEY §8(d)'s 17 algorithmic ops per scored tuple"}
+            "evaluated_candidates_per_s": e / (k_ms * 1e-3),
+            "note": "no branch and bound: every QoS-feasible level tuple's FP32 key is computed; the bilinear form "
+                    "(DESIGN.md §3.5) needs 2 FMAs per tuple (packed f32x2) + half a 3-input min, so achieved counts "
+                    "those 2 FMA-pipe lane-ops against the FMA pipe's 148 x 128 x 1965 MHz (SURVEY §8(d)'s 17 ops "
+                    "per tuple describe the unreduced per-worker formula)"}
         del p
     return res
 

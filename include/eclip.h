@@ -110,6 +110,12 @@ typedef struct {
     const float* slowdown_matrix; /* [W*W] row-major, entries >= 0 (MATRIX only; diagonal ignored) */
     int32_t objective;            /* ECLIP_SUM | ECLIP_MAX | ECLIP_ENERGY */
     float p_idle_w, p_max_w;      /* power model, 0 <= p_idle <= p_max (75 / 225 W) */
+    const double* weights;        /* [W] per-worker objective weights omega_w in (0, 1000] ("weights:
+                                     per-worker scalar (default all 1)"), or NULL = all 1, the paper's "identically
+                                     weighted objective function per worker".  SUM minimises
+                                     sum_w omega_w L_w, MAX minimises max_w omega_w L_w; each weight is taken at 1e-6
+                                     resolution, round(omega 1e6) / 1e6 (R20).  ENERGY: weights must be
+                                     equal (energy is physical).  Errors: ECLIP_E_INVALID_ARG. */
 } eclip_problem;
 
 /* Result of one problem.  Arrays are caller-allocated and may be NULL when not wanted:
@@ -135,6 +141,11 @@ typedef struct {
     uint64_t candidates_evaluated;/* ENUM: tuples whose FP32 key pass 1 actually computed (the rest were classified
                                      without arithmetic: QoS range cuts, lower bounds); SLICE: 0 */
     uint64_t exact_key[4];        /* the winner's exact integer key, little-endian limbs */
+    double energy_busy_j;         /* busy-SM energy integral of the plan's predicted run (SPEC integrate_energy
+                                     S:416-419 with power_at S:406-409; R21): workers start together and
+                                     run their groups back to back (group g for e_g on its pool size), power
+                                     p_idle + (p_max - p_idle) min(N, sum of running pool sizes) / N, integrated over
+                                     [0, makespan] (J) */
 } eclip_result;
 
 typedef struct {
@@ -178,6 +189,8 @@ typedef struct {
                                      1: model_ids, qos_ns, slowdown_matrix and every eclip_batch_out array are
                                      CUDA device pointers; the call then performs no host<->device copy of
                                      per-problem data and does not synchronise the stream before returning. */
+    const double* weights;        /* [n_problems * W] per-worker objective weights (as eclip_problem.weights), or
+                                     NULL = all 1 (host or device memory per on_device) */
 } eclip_batch;
 
 typedef struct {                  /* struct-of-arrays results, caller-allocated (host or device per on_device) */
@@ -193,6 +206,8 @@ typedef struct {                  /* struct-of-arrays results, caller-allocated 
     int32_t* model_switches;      /* [n * W] */
     int32_t* group_sm;            /* [n * W * Gmax] (row of worker w at (i*W + w)*Gmax; unused tail = 0), or NULL */
     int32_t group_stride;         /* Gmax used for group_sm */
+    double* energy_busy_j;        /* [n] busy-SM energy integral of the predicted run (eclip_result.energy_busy_j),
+                                     or NULL */
 } eclip_batch_out;
 
 int eclip_plan_batch(const eclip_profiles* prof, const eclip_batch* batch, const eclip_options* opt,

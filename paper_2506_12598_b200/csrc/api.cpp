@@ -541,6 +541,21 @@ static int check_common(const eclip_profiles* P, int W, int N, int R, int mode, 
     return ECLIP_OK;
 }
 
+// per-worker objective weights (R20): finite, in (0, 1000], >= 5e-7 (so that
+// round(omega 1e6) >= 1); ENERGY needs equal weights.  Returns whether they differ (the weighted kernels).
+static int check_weights(const double* wt, size_t n, int W, int obj, bool* unequal) {
+    *unequal = false;
+    if (!wt) return ECLIP_OK;
+    for (size_t i = 0; i < n * (size_t)W; i++) {
+        if (!(wt[i] > 0.0 && wt[i] <= 1000.0) || llround(wt[i] * 1e6) < 1)
+            return fail(ECLIP_E_INVALID_ARG, "weights must lie in (0, 1000] (1e-6 resolution)");
+        if (llround(wt[i] * 1e6) != llround(wt[i - i % W] * 1e6)) *unequal = true;
+    }
+    if (*unequal && obj == ECLIP_ENERGY)
+        return fail(ECLIP_E_INVALID_ARG, "the ENERGY objective takes no per-worker weights (they must be equal)");
+    return ECLIP_OK;
+}
+
 static void fill_setup(eclip_session* s, int n, int W, int N, int R, int mode, int obj, bool has_qos,
                        const eclip_options* opt) {
     (void)R;
@@ -619,7 +634,8 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     if (n * H < 4096) nseg = (int)std::min<long double>(Lstep, std::ceil(4096.0L / (n * H)));
     const int seglen = (Lstep + nseg - 1) / nseg;
     nseg = (Lstep + seglen - 1) / seglen;
-    const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax) && !su.wide;
+    const bool fast = su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && pass1_fast(Lmax) && !su.wide &&
+                      !su.weighted;
     const int teams_typ = P1_THREADS / 32;   // one unit per warp in both pass-1 kernels
     const long double units = H * nseg;
     const long double cand_unit = (long double)seglen * Lmax;
@@ -823,7 +839,10 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
     bool has_qos = false;
     if (pr->qos_ns)
         for (int w = 0; w < W; w++) has_qos |= !std::isinf(pr->qos_ns[w]);
+    bool unequal = false;
+    if ((rc = check_weights(pr->weights, 1, W, pr->objective, &unequal))) return rc;
     fill_setup(s.get(), 1, W, pr->total_sms, pr->switch_max, pr->slowdown, pr->objective, has_qos, opt);
+    s->su.weighted = unequal ? 1 : 0;
     rc = build_tables(s.get(), specs);
     if (rc) return rc;
     s->h_table_of = table_of;
@@ -844,9 +863,14 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
         CU(s->arena.alloc(&dM, (size_t)W * W));
         CU(cudaMemcpyAsync(dM, pr->slowdown_matrix, 4 * W * W, cudaMemcpyHostToDevice, s->st));
     }
+    double* dw = nullptr;
+    if (pr->weights) {
+        CU(s->arena.alloc(&dw, W));
+        CU(cudaMemcpyAsync(dw, pr->weights, 8 * W, cudaMemcpyHostToDevice, s->st));
+    }
     CU(s->arena.alloc(&s->d_sizes, C));
     CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * C, cudaMemcpyHostToDevice, s->st));
-    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM; s->pin.weights = dw;
     s->wk.table_of = dtab;
     s->wk.tb = s->tb;
     s->pin.p_idle = pr->p_idle_w; s->pin.p_max = pr->p_max_w;
@@ -895,7 +919,10 @@ static int session_from_batch(const eclip_profiles* P, const eclip_batch* b, con
     s->on_device = b->on_device != 0;
     rc = setup_device(s.get(), opt);
     if (rc) return rc;
+    bool unequal = b->weights != nullptr && b->on_device;   // device weights: not inspected on the host
+    if (b->weights && !b->on_device && (rc = check_weights(b->weights, (size_t)n, W, b->objective, &unequal))) return rc;
     fill_setup(s.get(), n, W, b->total_sms, b->switch_max, b->slowdown, b->objective, b->qos_ns != nullptr, opt);
+    s->su.weighted = unequal ? 1 : 0;
     rc = build_tables(s.get(), specs);
     if (rc) return rc;
     {
@@ -911,8 +938,15 @@ static int session_from_batch(const eclip_profiles* P, const eclip_batch* b, con
     const int32_t* dtab = b->model_ids;
     const double* dq = b->qos_ns;
     const float* dM = b->slowdown_matrix;
+    const double* dW = b->weights;
     if (!b->on_device) {
         int32_t* t; double* q = nullptr; float* M = nullptr;
+        if (b->weights) {
+            double* wd;
+            CU(s->arena.alloc(&wd, (size_t)n * W));
+            CU(cudaMemcpyAsync(wd, b->weights, 8 * (size_t)n * W, cudaMemcpyHostToDevice, s->st));
+            dW = wd;
+        }
         CU(s->arena.alloc(&t, (size_t)n * W));
         CU(cudaMemcpyAsync(t, b->model_ids, 4 * (size_t)n * W, cudaMemcpyHostToDevice, s->st));
         if (b->qos_ns) {
@@ -927,7 +961,7 @@ static int session_from_batch(const eclip_profiles* P, const eclip_batch* b, con
     }
     CU(s->arena.alloc(&s->d_sizes, C));
     CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * C, cudaMemcpyHostToDevice, s->st));
-    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM; s->pin.weights = dW;
     s->wk.table_of = dtab;
     s->wk.tb = s->tb;
     s->pin.p_idle = b->p_idle_w; s->pin.p_max = b->p_max_w;
@@ -1040,6 +1074,7 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
         mo.status = o->status; mo.levels = o->winner_levels; mo.index = o->winner_index; mo.objective = o->objective;
         mo.makespan = o->makespan_ns; mo.power = o->power_w; mo.energy = o->energy_j; mo.thr = o->throughput_rps;
         mo.latency = o->model_latency_ns; mo.switches = o->model_switches; mo.group_sm = o->group_sm;
+        mo.energy_busy = o->energy_busy_j;
         if (s->engine == ECLIP_ENGINE_SLICE) CU(slice_decode_winner(s->slice, s->su, s->wk, s->st));
         CU(launch_materialize(s->su, s->tb, s->wk, s->d_sizes, s->C, mo, s->st));
         return ECLIP_OK;
@@ -1050,6 +1085,7 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     const size_t o_idx = bp.take<uint64_t>(n), o_obj = bp.take<double>(n), o_mk = bp.take<double>(n);
     const size_t o_pw = bp.take<double>(n), o_en = bp.take<double>(n), o_thr = bp.take<double>(n);
     const size_t o_lat = bp.take<double>(n * W);
+    const size_t o_eb = o->energy_busy_j ? bp.take<double>(n) : 0;
     const size_t o_gsm = o->group_sm ? bp.take<int32_t>(n * W * stride) : 0;
     const size_t o_glat = glat_host ? bp.take<double>(n * W * stride) : 0;
     const size_t o_key = key_host ? bp.take<uint64_t>(n * 4) : 0;
@@ -1068,6 +1104,7 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     double* glat = glat_host ? (double*)(base + o_glat) : nullptr;
     uint64_t* key = key_host ? (uint64_t*)(base + o_key) : nullptr;
     mo.group_lat = glat; mo.key = key;
+    mo.energy_busy = o->energy_busy_j ? (double*)(base + o_eb) : nullptr;
     mo.status = st; mo.levels = lv; mo.index = idx; mo.objective = obj; mo.makespan = mk; mo.power = pw;
     mo.energy = en; mo.thr = thr; mo.latency = lat; mo.switches = sw; mo.group_sm = gsm;
     if (s->engine == ECLIP_ENGINE_SLICE) CU(slice_decode_winner(s->slice, s->su, s->wk, s->st));
@@ -1085,6 +1122,7 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     CU(cp(o->throughput_rps, thr, 8 * n));
     CU(cp(o->model_latency_ns, lat, 8 * n * W));
     CU(cp(o->model_switches, sw, 4 * n * W));
+    if (mo.energy_busy) CU(cp(o->energy_busy_j, mo.energy_busy, 8 * n));
     if (gsm) CU(cp(o->group_sm, gsm, 4 * n * W * stride));
     if (glat) CU(cp(glat_host, glat, 8 * n * W * stride));
     if (key) CU(cp(key_host, key, 32 * n));
@@ -1179,13 +1217,14 @@ struct eclip_planner {
     eclip_options opt{};
     int n_max = 0, W = 0, N = 0, R = 0, mode = 0, obj = 0;
     float pi = 0.0f, pm = 0.0f;
-    bool has_qos = false, timing = false;
+    bool has_qos = false, has_w = false, timing = false;
     std::vector<uint32_t> mask;
     WorkBlock wb;
     Scratch stg;
     int32_t* d_ids = nullptr;
     double* d_qos = nullptr;
     float* d_M = nullptr;
+    double* d_w = nullptr;
     cudaEvent_t ev[6] = {};
     bool ev_valid = false;
     ~eclip_planner() {
@@ -1237,6 +1276,7 @@ extern "C" int eclip_planner_create(const eclip_profiles* P, const eclip_batch* 
     pl->W = b->n_models; pl->N = b->total_sms; pl->R = b->switch_max; pl->mode = b->slowdown; pl->obj = b->objective;
     pl->pi = b->p_idle_w; pl->pm = b->p_max_w;
     pl->has_qos = b->qos_ns != nullptr;
+    pl->has_w = b->weights != nullptr;
     pl->timing = o.timing != 0;
     for (auto& sp : specs) pl->mask.push_back(sp.mask);
     pl->s = std::make_unique<eclip_session>();
@@ -1245,6 +1285,9 @@ extern "C" int eclip_planner_create(const eclip_profiles* P, const eclip_batch* 
     s->W = pl->W; s->n = max_problems; s->C = P->C();
     if ((rc = setup_device(s, &o))) return rc;
     fill_setup(s, max_problems, pl->W, pl->N, pl->R, pl->mode, pl->obj, pl->has_qos, &o);
+    s->su.weighted = pl->has_w ? 1 : 0;   // weights may differ from call to call: the weighted kernels
+    if (pl->has_w && pl->obj == ECLIP_ENERGY)
+        return fail(ECLIP_E_INVALID_ARG, "the ENERGY objective takes no per-worker weights");
     if ((rc = build_tables(s, specs))) return rc;   // K1 once (the only host synchronisation)
     {
         std::vector<int32_t> all(specs.size());
@@ -1263,6 +1306,7 @@ extern "C" int eclip_planner_create(const eclip_profiles* P, const eclip_batch* 
     CU(s->arena.alloc(&pl->d_ids, nw));
     if (pl->has_qos) CU(s->arena.alloc(&pl->d_qos, nw));
     if (pl->mode == ECLIP_MATRIX) CU(s->arena.alloc(&pl->d_M, nw * pl->W));
+    if (pl->has_w) CU(s->arena.alloc(&pl->d_w, nw));
     CU(s->arena.alloc(&s->d_sizes, s->C));
     CU(cudaMemcpyAsync(s->d_sizes, P->sizes.data(), 4 * (size_t)s->C, cudaMemcpyHostToDevice, s->st));
     if ((rc = alloc_work(s, &pl->wb))) return rc;
@@ -1284,6 +1328,8 @@ extern "C" int eclip_planner_plan(eclip_planner* pl, const eclip_batch* b, eclip
         return fail(ECLIP_E_INVALID_ARG, "batch settings differ from the planner's");
     if ((b->qos_ns != nullptr) != pl->has_qos)
         return fail(ECLIP_E_INVALID_ARG, pl->has_qos ? "this planner needs qos_ns" : "this planner was created without QoS");
+    if ((b->weights != nullptr) != pl->has_w)
+        return fail(ECLIP_E_INVALID_ARG, pl->has_w ? "this planner needs weights" : "this planner was created without weights");
     if (!b->model_ids || (pl->mode == ECLIP_MATRIX && !b->slowdown_matrix))
         return fail(ECLIP_E_INVALID_ARG, "null model_ids / slowdown_matrix");
     if (b->allowed_mask)
@@ -1298,16 +1344,21 @@ extern "C" int eclip_planner_plan(eclip_planner* pl, const eclip_batch* b, eclip
                 return fail(ECLIP_E_INVALID_ARG, "model id %d out of range (problem %zu)", b->model_ids[i], i / W);
             if (b->qos_ns && !(b->qos_ns[i] >= 0.0)) return fail(ECLIP_E_INVALID_ARG, "qos_ns must be >= 0 or +inf");
         }
+        bool unequal;
+        int rcw = check_weights(b->weights, (size_t)n, W, pl->obj, &unequal);
+        if (rcw) return rcw;
     }
     if (pl->timing) CU(cudaEventRecord(pl->ev[0], s->st));
     const int32_t* dtab = b->model_ids;
     const double* dq = b->qos_ns;
     const float* dM = b->slowdown_matrix;
+    const double* dW = b->weights;
     if (!b->on_device) {   // inputs into the planner's device buffers (stream-ordered)
         CU(cudaMemcpyAsync(pl->d_ids, b->model_ids, 4 * nw, cudaMemcpyHostToDevice, s->st));
         if (pl->has_qos) CU(cudaMemcpyAsync(pl->d_qos, b->qos_ns, 8 * nw, cudaMemcpyHostToDevice, s->st));
         if (pl->d_M) CU(cudaMemcpyAsync(pl->d_M, b->slowdown_matrix, 4 * nw * W, cudaMemcpyHostToDevice, s->st));
-        dtab = pl->d_ids; dq = pl->d_qos; dM = pl->d_M;
+        if (pl->d_w) CU(cudaMemcpyAsync(pl->d_w, b->weights, 8 * nw, cudaMemcpyHostToDevice, s->st));
+        dtab = pl->d_ids; dq = pl->d_qos; dM = pl->d_M; dW = pl->d_w;
     }
     if (pl->timing) CU(cudaEventRecord(pl->ev[1], s->st));
     // geometry of this call's batch size (host arithmetic on the cached level counts; no sync)
@@ -1317,7 +1368,7 @@ extern "C" int eclip_planner_plan(eclip_planner* pl, const eclip_batch* b, eclip
     int rc = plan_geometry(s, &pl->opt);
     if (rc) return rc;
     if ((rc = alloc_work(s, &pl->wb))) return rc;
-    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM;
+    s->pin.table_of = dtab; s->pin.qos = dq; s->pin.M = dM; s->pin.weights = dW;
     s->pin.p_idle = pl->pi; s->pin.p_max = pl->pm;
     s->wk.table_of = dtab;
     s->wk.tb = s->tb;
@@ -1366,8 +1417,9 @@ static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_ove
     for (int w = 0; w < W; w++) gmax = std::max(gmax, s->tabs[s->h_table_of[w]].G);
     std::vector<int32_t> st(1), lv(W), sw(W), gsm((size_t)W * gmax);
     std::vector<uint64_t> idx(1), key(4);
-    std::vector<double> obj(1), mk(1), pw(1), en(1), thr(1), lat(W), glat((size_t)W * gmax);
+    std::vector<double> obj(1), mk(1), pw(1), en(1), thr(1), eb(1), lat(W), glat((size_t)W * gmax);
     eclip_batch_out o{};
+    o.energy_busy_j = eb.data();
     o.status = st.data(); o.winner_levels = lv.data(); o.winner_index = idx.data(); o.objective = obj.data();
     o.makespan_ns = mk.data(); o.power_w = pw.data(); o.energy_j = en.data(); o.throughput_rps = thr.data();
     o.model_latency_ns = lat.data(); o.model_switches = sw.data(); o.group_sm = gsm.data(); o.group_stride = gmax;
@@ -1377,7 +1429,7 @@ static int plan_one(eclip_session* s, eclip_result* r, const uint64_t* first_ove
     r->status = st[0] == 0 ? ECLIP_OK : ECLIP_INFEASIBLE;
     r->engine_used = s->engine;
     r->objective = obj[0]; r->makespan_ns = mk[0]; r->power_w = pw[0]; r->energy_j = en[0];
-    r->throughput_rps = thr[0]; r->winner_index = idx[0];
+    r->throughput_rps = thr[0]; r->winner_index = idx[0]; r->energy_busy_j = eb[0];
     for (int i = 0; i < 4; i++) r->exact_key[i] = key[i];
     long double totl = 1;
     for (int w = 0; w < W; w++) totl *= (long double)std::max(1, s->tabL[s->h_table_of[w]]);
@@ -1413,6 +1465,10 @@ extern "C" int eclip_session_create_problem(const eclip_profiles* prof, const ec
     if (rc) { delete s; return rc; }
     if (s->engine == ECLIP_ENGINE_SLICE) {
         cudaError_t e = slice_setup(s->slice, s->su, s->tb, s->wk, s->tabL.data(), s->h_table_of.data(), s->st);
+        if (e == cudaErrorNotSupported) {
+            delete s;
+            return fail(ECLIP_E_TOO_LARGE, "SLICE engine: weighted terms exceed its 64-bit exact DP; use ENUM");
+        }
         if (e != cudaSuccess) { delete s; return fail(ECLIP_E_CUDA, "SLICE setup: %s", cudaGetErrorString(e)); }
     }
     *out = s;
@@ -1533,6 +1589,11 @@ extern "C" int eclip_baseline_plan(const eclip_profiles* P, const eclip_problem*
     J.den = 1000000000ull;
     J.num = (uint64_t)llround(param * 1e9);
     J.p_idle = pr->p_idle_w; J.p_max = pr->p_max_w;
+    {
+        bool unequal;
+        if ((rc = check_weights(pr->weights, 1, W, pr->objective, &unequal))) return rc;
+        for (int w = 0; w < W; w++) J.wv[w] = pr->weights ? (double)llround(pr->weights[w] * 1e6) / 1e6 : 1.0;
+    }
     int gmax = 1;
     for (int w = 0; w < W; w++) gmax = std::max(gmax, (int)ws[w].bounds.size() - 1);
     int32_t* dsz;

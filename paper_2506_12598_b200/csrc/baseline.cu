@@ -67,7 +67,7 @@ __global__ void k_baseline(BaseJob J, BaseOut o) {
         const double N = (double)J.N;
         double avg[MAXW], sum_avg = 0.0;
         for (int v = 0; v < W; v++) { avg[v] = (double)sS[v] / (double)J.K[v]; sum_avg += avg[v]; }
-        double mk = 0.0, obj = 0.0, thr = 0.0;
+        double mk = 0.0, wmk = 0.0, obj = 0.0, thr = 0.0;
         // exact QoS check: h_w = B_w (D + O^_w) <= floor(Q_w D)
         uint64_t lam = 1;
         for (int v = 0; v < W; v++) { const uint64_t g = gcd_u64(lam, (uint64_t)J.K[v]); lam = lam / g * (uint64_t)J.K[v]; }
@@ -104,14 +104,15 @@ __global__ void k_baseline(BaseJob J, BaseOut o) {
             alpha_w[v] = alpha;
             const double Lw = (double)sB[v] * (1.0 + alpha);
             mk = Lw > mk ? Lw : mk;
-            obj += Lw;
+            obj += J.wv[w] * Lw;                       // per-worker weights (R20), 1 by default
+            wmk = J.wv[w] * Lw > wmk ? J.wv[w] * Lw : wmk;
             thr += 1e9 / Lw;
             if (o.latency) o.latency[v] = Lw;
         }
         double frac = sum_avg / N;
         if (frac > 1.0) frac = 1.0;
         const double pw = (double)J.p_idle + ((double)J.p_max - (double)J.p_idle) * frac;
-        if (J.obj == O_MAX) obj = mk;
+        if (J.obj == O_MAX) obj = wmk;
         else if (J.obj == O_ENERGY) obj = pw * mk;
         o.scalars[0] = obj;
         o.scalars[1] = mk;

@@ -86,6 +86,11 @@ struct Prob {
     u128 pi_idle, pi_dyn;       // power model p 2^k (exact)
     int32_t has_qos;
     float p_max;                // power model float (for FP64 reporting)
+    // per-worker objective weights (R20): wt = round(omega 1e6) / gcd (exact keys),
+    // wf = (float)wt (FP32 filters), wv = round(omega 1e6) / 1e6 (FP64 objective); all 1 when unweighted
+    uint64_t wt[MAXW];
+    float wf[MAXW];
+    double wv[MAXW];
 };
 
 // Settings shared by all problems of one launch sequence
@@ -107,7 +112,8 @@ struct Setup {
     uint64_t tol_num, tol_den;
     double delta;               // FP32 filter relative error bound
     int32_t prune;              // fast pass 1: skip rows whose lower bound exceeds the incumbent's band (§3.9)
-    int32_t pad2;
+    int32_t weighted;           // per-worker objective weights given (SUM / MAX): the generic pass 1 and the
+                                //   weighted FP32 / exact keys (the fast bilinear kernels assume equal weights)
     int64_t rows_max;           // max rows (hi-digit combinations) over problems (rowlb stride)
 };
 
@@ -136,6 +142,7 @@ struct PrepIn {
     const double* qos;          // [n*W] or null
     const float* M;             // [n*W*W] or null
     float p_idle, p_max;
+    const double* weights;      // [n*W] per-worker objective weights or null (all 1)
 };
 
 // Device-side outputs / scratch of one launch sequence
@@ -230,6 +237,7 @@ struct MatOut {                 // materialisation outputs (device pointers, may
     int32_t* status; int32_t* levels; uint64_t* index; double* objective; double* makespan;
     double* power; double* energy; double* thr; double* latency; int32_t* switches; int32_t* group_sm;
     double* group_lat; int32_t group_stride; uint64_t* key;
+    double* energy_busy;        // [n] busy-SM energy integral of the predicted run (J; R21)
 };
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C,
                                MatOut out, cudaStream_t st);
@@ -255,6 +263,7 @@ struct BaseJob {
     const int32_t* bounds[MAXW];       // [G_w + 1] group kernel offsets
     double Q[MAXW];
     float M[MAXW_ENUM * MAXW_ENUM];
+    double wv[MAXW];                   // objective weights round(omega 1e6) / 1e6 (1 = unweighted)
 };
 
 struct BaseOut {

@@ -219,6 +219,30 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
             for (int b = 0; b < W; b++) P.Mi[a * MAXW_ENUM + b] = (int64_t)ldexp((double)P.Mf[a * MAXW_ENUM + b], P.E);
     }
     P.D = (u128)P.lamN << P.E;
+    // per-worker objective weights ("weights: per-worker scalar (default all 1)", "strictly
+    // positive"; R20): n_w = round-half-up(omega_w 1e6), exact keys use n_w / gcd_w n_w
+    {
+        u64 g = 0, n[MAXW];
+        for (int w = 0; w < W; w++) {
+            n[w] = 1000000ull;
+            if (in.weights) {
+                const double x = in.weights[(size_t)p * W + w];
+                if (!(x > 0.0 && x <= 1000.0)) { P.status = -4; break; }
+                const double y = x * 1e6;
+                const long long r = llround(y);   // half away from zero == half up (y > 0)
+                if (r < 1) { P.status = -4; break; }
+                n[w] = (u64)r;
+            }
+            g = gcd_u64(g, n[w]);
+        }
+        for (int w = 0; w < W; w++) {
+            const u64 v = (P.status == -4 || g == 0) ? 1 : n[w] / g;
+            P.wt[w] = v;
+            P.wf[w] = (float)v;
+            P.wv[w] = P.status == -4 ? 1.0 : (double)n[w] / 1e6;
+            if (su.obj == O_ENERGY && v != 1) P.status = -4;   // energy is physical: no per-worker weights
+        }
+    }
     P.has_qos = 0;
     for (int w = 0; w < W; w++) {
         double q = in.qos ? in.qos[(size_t)p * W + w] : (double)INFINITY;
@@ -1642,6 +1666,10 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
 #pragma unroll
     for (int w = 0; w < W; w++) Mcol[w] = P.Mf[w * MAXW_ENUM + NP];
     const Lev* inner = sl + NP * Lmax;
+    const bool weighted = su.weighted != 0;
+    float wf[W];
+#pragma unroll
+    for (int w = 0; w < W; w++) wf[w] = P.wf[w];
 
     uint64_t u0 = item * (uint64_t)su.upi, u1 = u0 + (uint64_t)su.upi;
     if (u1 > P.units) u1 = P.units;
@@ -1710,7 +1738,11 @@ k_pass1_gen(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ le
                     if (OBJ == O_SUM) num = fmaf(bf, O, num);
                 }
                 float key;
-                if (OBJ == O_SUM) {
+                if (weighted && OBJ != O_ENERGY) {   // weights (R20): sum / max of omega_w L_w
+                    key = OBJ == O_SUM ? 0.0f : Lw[0] * wf[0];
+#pragma unroll
+                    for (int w = 0; w < W; w++) key = OBJ == O_SUM ? fmaf(wf[w], Lw[w], key) : fmaxf(key, Lw[w] * wf[w]);
+                } else if (OBJ == O_SUM) {
                     key = fmaf(num, P.inv, Bpf + iBf);
                 } else {
                     float mx = Lw[0];
@@ -1788,7 +1820,8 @@ int pass1_fast_team(int L_inner) { return fast_team(L_inner); }
 
 // the fast kernel applies when every problem's inner worker fits a warp team
 static bool use_fast(const Setup& su) {   // (the host's plan_geometry takes the same decision)
-    return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax) && !su.wide;
+    return su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && fast_ok(su.Lmax) && !su.wide &&
+           !su.weighted;
 }
 
 bool pass1_prunable(const Setup& su) { return su.prune != 0 && su.W >= 3 && use_fast(su); }
@@ -2020,6 +2053,7 @@ __device__ bool exact_key(const Setup& su, const Prob& P, const Lev* sl, const i
     int64_t Tp = 0;
     for (int w = 0; w < W; w++) Tp += sl[w * su.Lmax + lv[w]].S;
     u128 sum = 0, mx = 0;
+    U256 wsum = u256_zero(), wmx = u256_zero();
     for (int w = 0; w < W; w++) {
         const Lev& r = sl[w * su.Lmax + lv[w]];
         u128 O;
@@ -2033,10 +2067,16 @@ __device__ bool exact_key(const Setup& su, const Prob& P, const Lev* sl, const i
         }
         u128 h = (u128)r.B * (P.D + O);
         if (h > P.Hq[w]) return false;
+        if (su.weighted) {   // omega_w h_w may exceed 128 bits (R20)
+            const U256 wh = u256_mul128((u128)P.wt[w], h);
+            wsum = u256_add(wsum, wh);
+            if (u256_cmp(wh, wmx) > 0) wmx = wh;
+        }
         sum += h;
         if (h > mx) mx = h;
     }
-    if (su.obj == O_SUM) key = u256_of(sum);
+    if (su.weighted && su.obj != O_ENERGY) key = su.obj == O_SUM ? wsum : wmx;
+    else if (su.obj == O_SUM) key = u256_of(sum);
     else if (su.obj == O_MAX) key = u256_of(mx);
     else {
         int64_t occ = Tp < P.lamN ? Tp : P.lamN;
@@ -2081,7 +2121,11 @@ __device__ bool key32_scalar(const Setup& su, const Prob& P, const Lev* sl, cons
             else feas = feas && (Tp <= (int64_t)r.Tmax);
         }
     }
-    if (su.obj == O_SUM) {
+    if (su.weighted && su.obj != O_ENERGY) {   // sum / max of omega_w L_w: <= (2W + 4) u
+        key = su.obj == O_SUM ? 0.0f : Lw[0] * P.wf[0];
+        for (int w = 0; w < W; w++)
+            key = su.obj == O_SUM ? fmaf(P.wf[w], Lw[w], key) : fmaxf(key, Lw[w] * P.wf[w]);
+    } else if (su.obj == O_SUM) {
         if (su.mode == M_EXCL && !su.wide) {
             const float bsum = __ll2float_rn(SB);
             key = fmaf(fmaf(Tf, bsum, -__ll2float_rn(SBS)), P.inv, bsum);
@@ -2421,6 +2465,7 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
     if (s_status != 0) {
         if (threadIdx.x == 0) {
             if (o.index) o.index[p] = 0;
+            if (o.energy_busy) o.energy_busy[p] = 0.0;
             if (o.objective) o.objective[p] = 0.0;
             if (o.makespan) o.makespan[p] = 0.0;
             if (o.power) o.power[p] = 0.0;
@@ -2457,7 +2502,7 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             sum_avg += avg[w];
         }
         const double N = (double)su.N;
-        double mk = 0.0, obj = 0.0, thr = 0.0;
+        double mk = 0.0, wmk = 0.0, obj = 0.0, thr = 0.0;
         for (int w = 0; w < W; w++) {
             double ov;
             if (su.mode == M_EXCL) ov = sum_avg - avg[w];
@@ -2472,7 +2517,8 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             const double Lw = Bw[w] * (1.0 + alpha);
             alpha_w[w] = alpha;
             mk = Lw > mk ? Lw : mk;
-            obj += Lw;
+            obj += P.wv[w] * Lw;
+            wmk = P.wv[w] * Lw > wmk ? P.wv[w] * Lw : wmk;
             thr += 1e9 / Lw;
             if (o.latency) o.latency[(size_t)p * W + w] = Lw;
             if (o.levels) o.levels[(size_t)p * W + w] = l[w];
@@ -2480,7 +2526,7 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
         double frac = sum_avg / N;
         if (frac > 1.0) frac = 1.0;
         const double pw = (double)P.p_idle + ((double)P.p_max - (double)P.p_idle) * frac;
-        if (su.obj == O_MAX) obj = mk;
+        if (su.obj == O_MAX) obj = wmk;
         else if (su.obj == O_ENERGY) obj = pw * mk;
         if (o.index) o.index[p] = fits ? idx : ~0ull;
         if (o.objective) o.objective[p] = obj;
@@ -2511,6 +2557,40 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             if (o.group_sm) o.group_sm[at] = g < G ? sizes[wit[g]] : 0;
             if (o.group_lat && g < G) o.group_lat[at] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha_w[w]);
         }
+    }
+    // busy-SM energy integral of the predicted run (SPEC integrate_energy S:416-419, power_at S:406-409;
+    // DESIGN.md R21): every worker starts at 0 and runs its groups back to back; between consecutive group
+    // boundaries the power is p_idle + (p_max - p_idle) min(N, sum of the running groups' SMs) / N
+    if (o.energy_busy && threadIdx.x == 0) {
+        int g[MAXW];
+        double end[MAXW];
+        const uint8_t* wit[MAXW];
+        for (int w = 0; w < W; w++) {
+            const int t = P.table[w];
+            wit[w] = tb.wit[t] + (size_t)lv[w] * tb.G[t];
+            g[w] = 0;
+            end[w] = (double)tb.beta[t][wit[w][0] * C] * (1.0 + alpha_w[w]);
+        }
+        const double N = (double)su.N, pi = (double)P.p_idle, pd = (double)P.p_max - (double)P.p_idle;
+        double t = 0.0, E = 0.0;
+        for (;;) {
+            double nxt = INFINITY;
+            int busy = 0;
+            for (int w = 0; w < W; w++)
+                if (g[w] < tb.G[P.table[w]]) {
+                    nxt = fmin(nxt, end[w]);
+                    busy += sizes[wit[w][g[w]]];
+                }
+            if (isinf(nxt)) break;
+            E += (pi + pd * (double)min(busy, su.N) / N) * (nxt - t);
+            t = nxt;
+            for (int w = 0; w < W; w++) {
+                const int tw = P.table[w];
+                if (g[w] < tb.G[tw] && end[w] == nxt && ++g[w] < tb.G[tw])
+                    end[w] += (double)tb.beta[tw][g[w] * C + wit[w][g[w]]] * (1.0 + alpha_w[w]);
+            }
+        }
+        o.energy_busy[p] = E * 1e-9;
     }
 }
 

@@ -42,10 +42,16 @@ __device__ __forceinline__ int64_t overlap_exact(int mode, int64_t Tp, int64_t S
 // ------------------------------------------------------------------------------------------
 // K3: FP32 filter DP, one CTA per slice (interleaved over shards).
 // D buffers carry PAD = max level span of +inf on both sides, so the inner (min,+) loop has no
-// bounds checks; each thread owns RB consecutive outputs P and slides a window of RB D values
-// over k (one shared load of g[k] and one of D per k for RB lattice points).
+// bounds checks.  Each thread owns RB consecutive outputs P; the k loop is unrolled by KU: per
+// block of KU levels it loads a window of RB + KU - 1 D values and the KU g values into registers
+// and does RB x KU adds with the mins folded in pairs (FMNMX3).  RB is odd: a warp's windows start
+// RB floats apart, so its window loads fall on 32 distinct banks (an even RB = 8 put 8 lanes on a bank).
 // ------------------------------------------------------------------------------------------
-constexpr int RB = 8;
+constexpr int RB = 9;
+constexpr int KU = 8;
+
+template <int OBJ>
+__device__ __forceinline__ float comb_f(float g, float d) { return OBJ == O_SUM ? g + d : fmaxf(g, d); }
 
 template <int OBJ>
 __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob* probs, const Lev* __restrict__ levs,
@@ -58,10 +64,11 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
     if (T > S.Thi) return;
     const int W = S.W;
     const int PAD = S.pad;
-    const int BUF = S.maxrange + 2 * PAD + RB;
-    float* g = sm;                       // [gtot]
-    float* Da = g + S.gtot + PAD;        // [-PAD, maxrange + PAD + RB)
-    float* Db = Da + BUF;
+    const int BUF = S.maxrange + 2 * PAD + RB;          // entries [-PAD, maxrange + PAD + RB)
+    const int BUFS = BUF;
+    float* g = sm;                                      // [gtot]
+    float* Da = g + S.gtot;
+    float* Db = Da + BUFS;
     const int64_t Tp = T * S.gS;
     const float Tpf = (float)Tp;
     for (int i = threadIdx.x; i < S.gtot; i += blockDim.x) {
@@ -73,20 +80,21 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
             const Lev& r = levs[w * S.Lmax + l];
             if (Tp <= (int64_t)r.Tmax) {
                 float O = (float)overlap_exact(S.mode, Tp, r.S, P.lamN);
-                v = fmaf(O, r.Bk, __ll2float_rn(r.B));
+                v = fmaf(O, r.Bk, __ll2float_rn(r.B)) * P.wf[w];   // omega_w L_w (weights: DESIGN.md R20)
             }
         }
         g[i] = v;
     }
-    for (int i = threadIdx.x; i < 2 * BUF; i += blockDim.x) Da[i - PAD] = INFINITY;
+    for (int i = threadIdx.x; i < 2 * BUFS; i += blockDim.x) Da[i] = INFINITY;
     __syncthreads();
     float* Dn = Da;   // D_{w+1}
     float* Dc = Db;   // D_w
+    auto at = [&](float* D, int i) -> float& { return D[i + PAD]; };   // index i >= -PAD
     int64_t nlo = 0, nhi = -1;
     if (W >= 2) {
         drange(S, T, W - 1, &nlo, &nhi);
         const float* gw = g + S.doff[W - 1];
-        for (int64_t p = nlo + threadIdx.x; p <= nhi; p += blockDim.x) Dn[p - nlo] = gw[p - S.smin[W - 1]];
+        for (int64_t p = nlo + threadIdx.x; p <= nhi; p += blockDim.x) at(Dn, (int)(p - nlo)) = gw[p - S.smin[W - 1]];
         __syncthreads();
         for (int w = W - 2; w >= 1; w--) {
             int64_t lo, hi;
@@ -94,40 +102,44 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
             const float* gw2 = g + S.doff[w];
             const int nk = S.smax[w] - S.smin[w] + 1;
             const int np = (int)(hi - lo + 1);
+            const int nprev = (int)(nhi - nlo + 1);
             for (int c = threadIdx.x * RB; c < np; c += blockDim.x * RB) {
                 // outputs p = lo + c + j (j < RB) read Dn[b + j - k], b = lo + c - smin_w - nlo
                 const int b = (int)(lo + c - S.smin[w] - nlo);
-                const int nprev = (int)(nhi - nlo + 1);
                 const int ks = max(0, b - (nprev - 1)), ke = min(nk, b + RB);   // k outside is +inf
-                float best[RB], win[RB];
+                float best[RB];
 #pragma unroll
                 for (int j = 0; j < RB; j++) best[j] = INFINITY;
-                if (ks < ke) {
+                int k = ks;
+                for (; k + KU <= ke; k += KU) {
+                    float win[RB + KU - 1], gg[KU];   // win[i] = Dn[b - k - KU + 1 + i]
 #pragma unroll
-                    for (int j = 0; j < RB; j++) win[j] = Dn[b + j - ks];
-                    for (int k = ks; k < ke; k++) {
-                        const float gk = gw2[k];
+                    for (int i = 0; i < RB + KU - 1; i++) win[i] = at(Dn, b - k - KU + 1 + i);
 #pragma unroll
-                        for (int j = 0; j < RB; j++) {
-                            const float v = (OBJ == O_SUM) ? gk + win[j] : fmaxf(gk, win[j]);
-                            best[j] = fminf(best[j], v);
-                        }
+                    for (int u = 0; u < KU; u++) gg[u] = gw2[k + u];
 #pragma unroll
-                        for (int j = RB - 1; j > 0; j--) win[j] = win[j - 1];
-                        win[0] = Dn[b - k - 1];
-                    }
-                    cnt += (unsigned long long)(ke - ks) * RB;
+                    for (int u = 0; u < KU; u += 2)
+#pragma unroll
+                        for (int j = 0; j < RB; j++)   // Dn[b + j - (k + u)] = win[j + KU - 1 - u]
+                            best[j] = fminf(best[j], fminf(comb_f<OBJ>(gg[u], win[j + KU - 1 - u]),
+                                                           comb_f<OBJ>(gg[u + 1], win[j + KU - 2 - u])));
                 }
+                for (; k < ke; k++) {
+                    const float gk = gw2[k];
+#pragma unroll
+                    for (int j = 0; j < RB; j++) best[j] = fminf(best[j], comb_f<OBJ>(gk, at(Dn, b + j - k)));
+                }
+                if (ks < ke) cnt += (unsigned long long)(ke - ks) * RB;
 #pragma unroll
                 for (int j = 0; j < RB; j++)
-                    if (c + j < np) Dc[c + j] = best[j];
+                    if (c + j < np) at(Dc, c + j) = best[j];
             }
             __syncthreads();
             // clear the stale tail of the buffer that becomes D_{w+1}'s neighbour next stage
             for (int i = threadIdx.x; i < BUF; i += blockDim.x)
-                if (i - PAD < 0 || i - PAD >= np) Dc[i - PAD] = INFINITY;
+                if (i - PAD < 0 || i - PAD >= np) at(Dc, i - PAD) = INFINITY;
             float* t = Dn; Dn = Dc; Dc = t;
-            for (int i = threadIdx.x; i < BUF; i += blockDim.x) Dc[i - PAD] = INFINITY;
+            for (int i = threadIdx.x; i < BUFS; i += blockDim.x) Dc[i] = INFINITY;
             __syncthreads();
             nlo = lo; nhi = hi;
         }
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
             v = g[k];
         } else {
             if (rest < nlo || rest > nhi) continue;
-            float d = Dn[rest - nlo];
+            float d = at(Dn, (int)(rest - nlo));
             v = (OBJ == O_SUM) ? g[k] + d : fmaxf(g[k], d);
         }
         J = fminf(J, v);
@@ -220,7 +232,8 @@ __device__ void slice_exact_dp(const SliceDev& S, const Prob& P, const Lev* levs
         uint64_t v = UINF;
         if (l >= 0) {
             const Lev& r = levs[w * S.Lmax + l];
-            if (Tp <= (int64_t)r.Tmax) v = (uint64_t)r.B * (uint64_t)(P.lamN + overlap_exact(S.mode, Tp, r.S, P.lamN));
+            if (Tp <= (int64_t)r.Tmax)   // omega_w h_w (slice_setup checked the u64 range)
+                v = (uint64_t)r.B * (uint64_t)(P.lamN + overlap_exact(S.mode, Tp, r.S, P.lamN)) * P.wt[w];
         }
         h[i] = v;
     }
@@ -454,6 +467,15 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     for (int w = W - 1; w >= 0; w--) { S.slo[w] = S.slo[w + 1] + S.smin[w]; S.shi[w] = S.shi[w + 1] + S.smax[w]; }
     S.Tlo = S.slo[0]; S.Thi = S.shi[0];
     S.n_slices = S.Thi - S.Tlo + 1;
+    {   // the exact DP sums W weighted terms omega_w B (Lambda N + O) in u64 (O <= T'max in every linear mode)
+        const unsigned __int128 lim = (~(unsigned __int128)0 >> 64) / (unsigned __int128)(W + 1);
+        for (int w = 0; w < W; w++)
+            for (int l = 0; l < P.L[w]; l++) {
+                const unsigned __int128 h = (unsigned __int128)lev[(size_t)w * su.Lmax + l].B *
+                                            (unsigned __int128)(P.lamN + S.Thi * g) * (unsigned __int128)P.wt[w];
+                if (h > lim) return cudaErrorNotSupported;   // -> ECLIP_E_TOO_LARGE (use ENUM)
+            }
+    }
     int64_t mr = 1;
     for (int64_t T = S.Tlo; T <= S.Thi; T++)
         for (int w = 1; w < W; w++) {
@@ -463,7 +485,7 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     S.maxrange = (int32_t)mr;
     int pad = 1;
     for (int w = 0; w < W; w++) pad = std::max(pad, S.smax[w] - S.smin[w] + 1);
-    S.pad = pad + RB;
+    S.pad = pad + RB + KU;
     CK(salloc(s, &s.d_units, 1));
     CK(salloc(s, &s.dense, dense.size()));
     CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
@@ -482,7 +504,7 @@ cudaError_t slice_pass1(SliceState& s, const Setup& su, const Tables& tb, Work& 
     const SliceDev& S = s.h;
     int64_t mine = S.n_slices > S.shard ? (S.n_slices - S.shard + S.n_shards - 1) / S.n_shards : 0;
     const size_t BUF = (size_t)S.maxrange + 2 * (size_t)S.pad + RB;
-    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * BUF + 2 * (size_t)S.pad);
+    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * BUF);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     const void* f = S.obj == O_SUM ? (const void*)k_slice_f32<O_SUM> : (S.obj == O_MAX ? (const void*)k_slice_f32<O_MAX>
                                                                                        : (const void*)k_slice_f32<O_ENERGY>);

@@ -38,7 +38,8 @@ class Problem(C.Structure):
     _fields_ = [("n_models", C.c_int32), ("model_ids", P(C.c_int32)), ("group_bounds", P(C.c_int32)),
                 ("total_sms", C.c_int32), ("allowed_mask", P(C.c_uint32)), ("qos_ns", P(C.c_double)),
                 ("switch_max", C.c_int32), ("slowdown", C.c_int32), ("slowdown_matrix", P(C.c_float)),
-                ("objective", C.c_int32), ("p_idle_w", C.c_float), ("p_max_w", C.c_float)]
+                ("objective", C.c_int32), ("p_idle_w", C.c_float), ("p_max_w", C.c_float),
+                ("weights", P(C.c_double))]
 
 
 class Result(C.Structure):
@@ -47,7 +48,8 @@ class Result(C.Structure):
                 ("model_switches", P(C.c_int32)), ("winner_levels", P(C.c_int32)), ("objective", C.c_double),
                 ("makespan_ns", C.c_double), ("power_w", C.c_double), ("energy_j", C.c_double),
                 ("throughput_rps", C.c_double), ("winner_index", C.c_uint64), ("candidates", C.c_uint64),
-                ("units_scored", C.c_uint64), ("candidates_evaluated", C.c_uint64), ("exact_key", C.c_uint64 * 4)]
+                ("units_scored", C.c_uint64), ("candidates_evaluated", C.c_uint64), ("exact_key", C.c_uint64 * 4),
+                ("energy_busy_j", C.c_double)]
 
 
 class Options(C.Structure):
@@ -60,14 +62,16 @@ class Batch(C.Structure):
     _fields_ = [("n_problems", C.c_int32), ("n_models", C.c_int32), ("model_ids", C.c_void_p),
                 ("qos_ns", C.c_void_p), ("allowed_mask", P(C.c_uint32)), ("slowdown_matrix", C.c_void_p),
                 ("total_sms", C.c_int32), ("switch_max", C.c_int32), ("slowdown", C.c_int32),
-                ("objective", C.c_int32), ("p_idle_w", C.c_float), ("p_max_w", C.c_float), ("on_device", C.c_int32)]
+                ("objective", C.c_int32), ("p_idle_w", C.c_float), ("p_max_w", C.c_float), ("on_device", C.c_int32),
+                ("weights", C.c_void_p)]
 
 
 class BatchOut(C.Structure):
     _fields_ = [("status", C.c_void_p), ("winner_levels", C.c_void_p), ("winner_index", C.c_void_p),
                 ("objective", C.c_void_p), ("makespan_ns", C.c_void_p), ("power_w", C.c_void_p),
                 ("energy_j", C.c_void_p), ("throughput_rps", C.c_void_p), ("model_latency_ns", C.c_void_p),
-                ("model_switches", C.c_void_p), ("group_sm", C.c_void_p), ("group_stride", C.c_int32)]
+                ("model_switches", C.c_void_p), ("group_sm", C.c_void_p), ("group_stride", C.c_int32),
+                ("energy_busy_j", C.c_void_p)]
 
 
 _lib = None
@@ -238,6 +242,7 @@ class Plan:
     units_scored: int
     exact_key: int
     candidates_evaluated: int = 0
+    energy_busy_j: float = 0.0
 
 
 def _options(engine="auto", device=0, stream=None, tie_tol=1e-5, shard=0, n_shards=1, prune=True,
@@ -309,7 +314,7 @@ class _ProblemArgs:
         return nk[m] if 0 <= m < len(nk) else 0  # invalid ids are rejected by the library
 
     def __init__(self, profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
-                 slowdown_matrix, group_bounds, p_idle_w, p_max_w):
+                 slowdown_matrix, group_bounds, p_idle_w, p_max_w, weights=None):
         self.ids = _np(model_ids, np.int32)
         W = len(self.ids)
         self.W = W
@@ -328,9 +333,10 @@ class _ProblemArgs:
         self.mask = _np(allowed_mask, np.uint32) if allowed_mask is not None else None
         self.qos = _np(qos_ns, np.float64) if qos_ns is not None else None
         self.M = _np(slowdown_matrix, np.float32).reshape(-1) if slowdown_matrix is not None else None
+        self.wt = _np(weights, np.float64) if weights is not None else None
         self.c = Problem(W, _ptr(self.ids, C.c_int32), _ptr(self.gb, C.c_int32), total_sms, _ptr(self.mask, C.c_uint32),
                          _ptr(self.qos, C.c_double), switch_max, MODES[slowdown], _ptr(self.M, C.c_float),
-                         OBJECTIVES[objective], p_idle_w, p_max_w)
+                         OBJECTIVES[objective], p_idle_w, p_max_w, _ptr(self.wt, C.c_double))
 
 
 def _result_buffers(W, G):
@@ -356,17 +362,18 @@ def _to_plan(r: Result, bufs, G) -> Plan:
     return Plan("ok" if r.status == OK else "infeasible", ENGINE_NAMES.get(r.engine_used, "?"), gsm, glat,
                 bufs["lat"].tolist(), bufs["sw"].tolist(), bufs["lv"].tolist(), r.objective, r.makespan_ns, r.power_w,
                 r.energy_j, r.throughput_rps, int(r.winner_index), int(r.candidates), int(r.units_scored), key,
-                int(r.candidates_evaluated))
+                int(r.candidates_evaluated), float(r.energy_busy_j))
 
 
 def plan(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
          objective: str = "sum", allowed_mask=None, qos_ns=None, slowdown_matrix=None, group_bounds=None,
          p_idle_w: float = 75.0, p_max_w: float = 225.0, engine: str = "auto", tie_tol: float = 1e-5,
-         device: int = 0, stream=None, prune: bool = True, comm: "Comm" = None) -> Plan:
+         device: int = 0, stream=None, prune: bool = True, comm: "Comm" = None, weights=None) -> Plan:
     """eclip_plan: the exact optimum of one co-location problem (§IV-B); with comm, sharded
-    over the communicator's ranks (every rank returns the same plan)."""
+    over the communicator's ranks (every rank returns the same plan).  weights: per-worker objective
+    weights, None = all 1."""
     a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
-                     slowdown_matrix, group_bounds, p_idle_w, p_max_w)
+                     slowdown_matrix, group_bounds, p_idle_w, p_max_w, weights)
     o = _options(engine, device, stream, tie_tol, prune=prune, comm=comm)
     r, bufs = _result_buffers(a.W, a.G)
     _check(lib().eclip_plan(profiles.handle, C.byref(a.c), C.byref(o), C.byref(r)))
@@ -378,7 +385,7 @@ def plan_problem(profiles: Profiles, p, **kw) -> Plan:
     return plan(profiles, p.model_ids, total_sms=p.total_sms, switch_max=p.switch_max, slowdown=p.mode,
                 objective=p.objective, allowed_mask=p.allowed_mask, qos_ns=p.qos_ns,
                 slowdown_matrix=p.slowdown_matrix, group_bounds=p.group_bounds, p_idle_w=p.p_idle_w,
-                p_max_w=p.p_max_w, **kw)
+                p_max_w=p.p_max_w, weights=getattr(p, "weights", None), **kw)
 
 
 def level_table(profiles: Profiles, model: int, *, switch_max: int = 14, group_bounds=None, allowed_mask: int = 0,
@@ -405,11 +412,11 @@ BASELINES = {"all_max": 0, "model_wise": 1, "kernel_wise": 2}
 def baseline_plan(profiles: Profiles, model_ids, *, kind: str, param: float = 0.0, total_sms: int,
                   switch_max: int = 14, slowdown: str = "exclude_self", objective: str = "sum", allowed_mask=None,
                   qos_ns=None, slowdown_matrix=None, group_bounds=None, p_idle_w: float = 75.0,
-                  p_max_w: float = 225.0, device: int = 0, stream=None) -> Plan:
+                  p_max_w: float = 225.0, device: int = 0, stream=None, weights=None) -> Plan:
     """eclip_baseline_plan: the paper's comparison plans (Baseline / Model-Wise / Kernel-Wise,
     PAPER.md §V) evaluated on the GPU under the same model as plan()."""
     a = _ProblemArgs(profiles, model_ids, total_sms, switch_max, slowdown, objective, allowed_mask, qos_ns,
-                     slowdown_matrix, group_bounds, p_idle_w, p_max_w)
+                     slowdown_matrix, group_bounds, p_idle_w, p_max_w, weights)
     o = _options("auto", device, stream)
     r, bufs = _result_buffers(a.W, a.G)
     _check(lib().eclip_baseline_plan(profiles.handle, C.byref(a.c), BASELINES[kind], float(param), C.byref(o),
@@ -437,19 +444,21 @@ def lookup_table_json(profiles: Profiles, model_ids, group_sm, *, total_sms: int
 # ------------------------------------------------------------------------------------------
 class _BatchArgs:
     def __init__(self, model_ids, qos_ns, slowdown_matrix, allowed_mask, total_sms, switch_max, slowdown, objective,
-                 p_idle_w, p_max_w, on_device):
+                 p_idle_w, p_max_w, on_device, weights=None):
         if on_device:
-            self.ids, self.qos, self.M = model_ids, qos_ns, slowdown_matrix
+            self.ids, self.qos, self.M, self.wt = model_ids, qos_ns, slowdown_matrix, weights
             n, W = int(model_ids.shape[0]), int(model_ids.shape[1])
         else:
             self.ids = _np(model_ids, np.int32)
             n, W = self.ids.shape
             self.qos = _np(qos_ns, np.float64) if qos_ns is not None else None
             self.M = _np(slowdown_matrix, np.float32) if slowdown_matrix is not None else None
+            self.wt = _np(weights, np.float64) if weights is not None else None
         self.mask = _np(allowed_mask, np.uint32) if allowed_mask is not None else None
         self.n, self.W = n, W
         self.c = Batch(n, W, _addr(self.ids), _addr(self.qos), _ptr(self.mask, C.c_uint32), _addr(self.M), total_sms,
-                       switch_max, MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 1 if on_device else 0)
+                       switch_max, MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 1 if on_device else 0,
+                       _addr(self.wt))
 
 
 def alloc_batch_out(n: int, W: int, gmax: int = 0, device=None, pinned: bool = False):
@@ -468,7 +477,8 @@ def alloc_batch_out(n: int, W: int, gmax: int = 0, device=None, pinned: bool = F
         i32, u64, f64 = torch.int32, torch.int64, torch.float64
     out = dict(status=mk((n,), i32), winner_levels=mk((n, W), i32), winner_index=mk((n,), u64),
                objective=mk((n,), f64), makespan_ns=mk((n,), f64), power_w=mk((n,), f64), energy_j=mk((n,), f64),
-               throughput_rps=mk((n,), f64), model_latency_ns=mk((n, W), f64), model_switches=mk((n, W), i32))
+               throughput_rps=mk((n,), f64), model_latency_ns=mk((n, W), f64), model_switches=mk((n, W), i32),
+               energy_busy_j=mk((n,), f64))
     if gmax:
         out["group_sm"] = mk((n, W, gmax), i32)
     out["_gmax"] = gmax
@@ -482,20 +492,21 @@ def _batch_out_struct(out) -> BatchOut:
         setattr(b, k, _addr(out[k]))
     b.group_sm = _addr(out.get("group_sm"))
     b.group_stride = int(out.get("_gmax", 0))
+    b.energy_busy_j = _addr(out.get("energy_busy_j"))
     return b
 
 
 def plan_batch(profiles: Profiles, model_ids, *, total_sms: int, switch_max: int = 14, slowdown: str = "exclude_self",
                objective: str = "sum", qos_ns=None, slowdown_matrix=None, allowed_mask=None, p_idle_w: float = 75.0,
                p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0, stream=None, out=None, gmax: int = 0,
-               prune: bool = True, comm: "Comm" = None):
+               prune: bool = True, comm: "Comm" = None, weights=None):
     """eclip_plan_batch: many independent mixes per launch (BASELINE config 5).
 
     With torch CUDA tensors for model_ids / qos_ns / slowdown_matrix (and `out` from
     alloc_batch_out(..., device=...)), everything stays in device memory (on_device=1)."""
     on_device = hasattr(model_ids, "is_cuda") and model_ids.is_cuda
     a = _BatchArgs(model_ids, qos_ns, slowdown_matrix, allowed_mask, total_sms, switch_max, slowdown, objective,
-                   p_idle_w, p_max_w, on_device)
+                   p_idle_w, p_max_w, on_device, weights)
     if out is None:
         out = alloc_batch_out(a.n, a.W, gmax, device=(model_ids.device if on_device else None))
     b = _batch_out_struct(out)
@@ -517,7 +528,7 @@ class Planner:
     def __init__(self, profiles: Profiles, *, n_models: int, max_problems: int, total_sms: int, switch_max: int = 14,
                  slowdown: str = "exclude_self", objective: str = "sum", qos: bool = True, allowed_mask=None,
                  p_idle_w: float = 75.0, p_max_w: float = 225.0, tie_tol: float = 1e-5, device: int = 0,
-                 stream=None, prune: bool = True, timing: bool = False):
+                 stream=None, prune: bool = True, timing: bool = False, weights: bool = False):
         self.profiles = profiles
         self.W, self.n_max = n_models, max_problems
         self.mask = _np(allowed_mask, np.uint32) if allowed_mask is not None else None
@@ -525,35 +536,36 @@ class Planner:
         self.qos = qos
         self._h = C.c_void_p()
         shape = Batch(1, n_models, None, 1 if qos else None, _ptr(self.mask, C.c_uint32), None, total_sms, switch_max,
-                      MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 0)
+                      MODES[slowdown], OBJECTIVES[objective], p_idle_w, p_max_w, 0, 1 if weights else None)
         o = _options("enum", device, stream, tie_tol, prune=prune, timing=timing)
         _check(lib().eclip_planner_create(profiles.handle, C.byref(shape), max_problems, C.byref(o), C.byref(self._h)))
         self._cache = {}
 
-    def _structs(self, model_ids, qos_ns, slowdown_matrix, out):
-        key = (_addr(model_ids), _addr(qos_ns), _addr(slowdown_matrix), id(out))
+    def _structs(self, model_ids, qos_ns, slowdown_matrix, out, weights=None):
+        key = (_addr(model_ids), _addr(qos_ns), _addr(slowdown_matrix), id(out), _addr(weights))
         hit = self._cache.get(key)
         if hit is None:
             on_device = hasattr(model_ids, "is_cuda") and model_ids.is_cuda
             n = int(model_ids.shape[0])
             b = Batch(n, self.W, _addr(model_ids), _addr(qos_ns), _ptr(self.mask, C.c_uint32), _addr(slowdown_matrix),
-                      *self.kw, 1 if on_device else 0)
-            hit = (b, _batch_out_struct(out), (model_ids, qos_ns, slowdown_matrix, out))
+                      *self.kw, 1 if on_device else 0, _addr(weights))
+            hit = (b, _batch_out_struct(out), (model_ids, qos_ns, slowdown_matrix, out, weights))
             if len(self._cache) > 64:
                 self._cache.clear()
             self._cache[key] = hit
         return hit
 
-    def plan(self, model_ids, qos_ns=None, slowdown_matrix=None, out=None, gmax: int = 0):
+    def plan(self, model_ids, qos_ns=None, slowdown_matrix=None, out=None, gmax: int = 0, weights=None):
         """plan one batch: model_ids [n, W] int32 (numpy / pinned numpy / torch CUDA), qos_ns [n, W]
         float64 when the planner has QoS.  Returns `out` (allocated if None)."""
         if not (hasattr(model_ids, "is_cuda") and model_ids.is_cuda):
             model_ids = np.ascontiguousarray(model_ids, dtype=np.int32)
             qos_ns = None if qos_ns is None else np.ascontiguousarray(qos_ns, dtype=np.float64)
+            weights = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
         if out is None:
             dev = model_ids.device if hasattr(model_ids, "is_cuda") and model_ids.is_cuda else None
             out = alloc_batch_out(int(model_ids.shape[0]), self.W, gmax, device=dev)
-        b, bo, _ = self._structs(model_ids, qos_ns, slowdown_matrix, out)
+        b, bo, _ = self._structs(model_ids, qos_ns, slowdown_matrix, out, weights)
         _check(lib().eclip_planner_plan(self._h, C.byref(b), C.byref(bo)))
         return out
 
@@ -595,7 +607,7 @@ class Session:
             self.args = _ProblemArgs(profiles, problem.model_ids, problem.total_sms, problem.switch_max, problem.mode,
                                      problem.objective, problem.allowed_mask, problem.qos_ns,
                                      problem.slowdown_matrix, problem.group_bounds, problem.p_idle_w,
-                                     problem.p_max_w)
+                                     problem.p_max_w, getattr(problem, "weights", None))
             self.n, self.W, self.single = 1, self.args.W, True
             _check(lib().eclip_session_create_problem(profiles.handle, C.byref(self.args.c), C.byref(o),
                                                       C.byref(self._h)))

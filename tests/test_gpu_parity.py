@@ -40,6 +40,9 @@ def _same(g, o, label=""):
     assert g.energy_j == pytest.approx(o.energy_j, rel=REL), label
     assert g.power_w == pytest.approx(o.power_w, rel=REL), label
     assert g.throughput_rps == pytest.approx(o.throughput_rps, rel=REL), label
+    eb = getattr(o, "energy_busy_j", float("nan"))
+    if eb == eb:   # the busy-SM energy integral of the predicted run (R21)
+        assert g.energy_busy_j == pytest.approx(eb, rel=REL), label
     for a, b in zip(g.model_latency_ns, o.latency_ns):
         assert a == pytest.approx(b, rel=REL), label
     for ga, gb in zip(g.group_latency_ns, o.group_latency_ns):
@@ -668,3 +671,102 @@ def test_comm_local_group_sharded_vs_oracle(n_ranks):
                                             comm=comms[r], gmax=16), n_ranks)
     for out in outs:
         assert golden_c5.check_batch(ids, out, sizes=models[0].sizes) == 128
+
+
+# ---------------------------------------------------------------- per-worker weights (R20)
+def _weighted(p, rng):
+    p.weights = [float(x) for x in rng.choice([0.25, 0.5, 1.0, 1.5, 2.0, 3.0, 0.1, 7.3], size=p.W)]
+    return p
+
+
+def test_weighted_worked_example_on_gpu():
+    from test_oracle import _ex1_weighted
+    for obj, sizes in (("sum", [[60], [45]]), ("max", [[60], [30]])):
+        p = _ex1_weighted(obj, [3.0, 1.0])
+        o = oracle.solve(p)
+        assert o.group_sm == sizes
+        for engine in ("enum", "slice"):
+            _same(_gpu(p, engine), o, f"{obj} {engine}")
+
+
+def test_weighted_random_instances_vs_oracle():
+    rng = np.random.default_rng(77)
+    n = 0
+    for s in range(300):
+        p = _weighted(synth.random_tiny_problem(9000 + s, max_w=4, max_g=4, max_c=4), rng)
+        if p.objective == "energy":
+            p.objective = ("sum", "max")[s % 2]
+        o = oracle.solve(p)
+        _same(_gpu(p, "enum"), o, f"enum seed {s}")
+        if p.mode != "matrix":
+            _same(_gpu(p, "slice"), o, f"slice seed {s}")
+        n += o.status == "ok"
+    assert n > 150
+
+
+def test_weighted_c2_c3_and_qos():
+    rng = np.random.default_rng(5)
+    for mode in ("exclude_self", "paper", "excess", "matrix"):
+        for obj in ("sum", "max"):
+            p = _weighted(synth.make_c2(mode, obj), rng)
+            o = oracle.solve(p)
+            _same(_gpu(p, "enum"), o, f"C2 {mode} {obj}")
+            if mode != "matrix":
+                _same(_gpu(p, "slice"), o, f"C2 slice {mode} {obj}")
+    for qf in (None, 3.0):   # C1 with QoS bounds, weighted
+        for mode in ("exclude_self", "paper", "excess"):
+            p = _weighted(synth.make_c1(2, mode, "sum", qos=qf is not None), rng)
+            o = oracle.solve(p)
+            _same(_gpu(p, "enum"), o, f"C1 {mode}")
+            _same(_gpu(p, "slice"), o, f"C1 slice {mode}")
+    # a full-size weighted problem (C3 profiles, EXCLUDE_SELF, 1.6e8 candidates): ENUM == SLICE == oracle SLICE
+    p = synth.make_c3("exclude_self")
+    p.weights = [1.0, 2.0, 0.5, 1.5]
+    o = oracle.solve(p, "slice")
+    _same(_gpu(p, "enum"), o, "C3 weighted enum")
+    _same(_gpu(p, "slice"), o, "C3 weighted slice")
+
+
+def test_weighted_batch_and_planner_vs_oracle():
+    """C5-shaped batch with per-mix weights: host batch, device batch and the persistent planner."""
+    import torch
+    models, ids, qos = synth.make_c5(48, seed=3)
+    rng = np.random.default_rng(8)
+    wts = rng.choice([0.5, 1.0, 2.0, 3.0], size=ids.shape).astype(np.float64)
+    wts[::5] = 1.0   # some mixes with equal weights
+    pr = ec.Profiles.from_models(models)
+    kw = dict(total_sms=148, switch_max=14, p_idle_w=200.0, p_max_w=1000.0)
+    host = ec.plan_batch(pr, ids, qos_ns=qos, weights=wts, gmax=16, **kw)
+    dev = ec.plan_batch(pr, torch.from_numpy(ids).cuda(), qos_ns=torch.from_numpy(qos).cuda(),
+                        weights=torch.from_numpy(wts).cuda(), gmax=16, **kw)
+    pl = ec.Planner(pr, n_models=4, max_problems=48, weights=True, **kw)
+    plo = pl.plan(ids, qos, weights=wts, gmax=16)
+    torch.cuda.synchronize()
+    for i in range(48):
+        p = synth.c5_problem(i, models, ids, qos)
+        p.weights = [float(x) for x in wts[i]]
+        o = oracle.solve(p, "slice")
+        for name, out in (("host", host), ("device", dev), ("planner", plo)):
+            st = int(out["status"][i])
+            assert (st == 0) == (o.status == "ok"), (name, i)
+            if o.status != "ok":
+                continue
+            assert [int(x) for x in out["winner_levels"][i].tolist()] == o.levels, (name, i)
+            assert float(out["objective"][i]) == pytest.approx(o.objective, rel=REL), (name, i)
+            assert float(out["energy_busy_j"][i]) == pytest.approx(o.energy_busy_j, rel=REL), (name, i)
+
+
+def test_weights_invalid_and_energy():
+    p = synth.make_c1(1)
+    for bad in ([0.0, 1.0], [-1.0, 1.0], [float("nan"), 1.0], [2000.0, 1.0]):
+        p.weights = bad
+        with pytest.raises(ec.EclipError) as e:
+            _gpu(p)
+        assert e.value.code == ec.eclip.E_INVALID_ARG
+    p = synth.make_c1(1, objective="energy")
+    p.weights = [2.0, 1.0]
+    with pytest.raises(ec.EclipError):
+        _gpu(p)
+    p.weights = [2.0, 2.0]   # equal weights: the unweighted energy plan
+    q = synth.make_c1(1, objective="energy")
+    _same(_gpu(p), oracle.solve(q))
