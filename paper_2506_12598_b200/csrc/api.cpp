@@ -461,12 +461,28 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
     const size_t o_beta = bp.take<int64_t*>(nt);
     const size_t in_bytes = bp.off;
     const size_t o_L = bp.take<int32_t>(nt);
+    // K1 stores its layers as int32 when every table's largest plan time fits (sum over groups of the
+    // slowest size < 2^31 - 1), else int64
+    bool v32 = true;
+    for (int i = 0; i < nt; i++) {
+        const HostTable& t = s->tabs[i];
+        int64_t mx = 0;
+        for (int g = 0; g < t.G; g++) {
+            int64_t m = 0;
+            for (int j = 0; j < t.C; j++) m = std::max(m, t.beta[(size_t)g * t.C + j]);
+            mx += m;
+        }
+        if (mx >= INT32_MAX) v32 = false;
+    }
+    const size_t vb = v32 ? 4 : 8;
+    std::vector<int32_t> ncp(nt);
     for (int i = 0; i < nt; i++) {
         const HostTable& t = s->tabs[i];
         const size_t ns = (size_t)(t.Reff + 1) * (t.smax + 1);
-        off[i].V = bp.take<int64_t>(t.v_elems);
-        off[i].best = bp.take<int64_t>(4 * ns);
-        off[i].barg = bp.take<int32_t>(2 * ns);
+        ncp[i] = (int32_t)((ns + 31) & ~(size_t)31);   // 128-byte aligned layer slabs (levels.cu)
+        off[i].V = bp.take<unsigned char>((size_t)t.G * t.C * ncp[i] * vb);
+        off[i].best = bp.take<unsigned char>((size_t)t.G * ncp[i] * 2 * vb);
+        off[i].barg = bp.take<uint8_t>((size_t)t.G * ncp[i]);
         off[i].bstar = bp.take<int64_t>(t.smax + 1);
         off[i].sidx = bp.take<int32_t>(t.smax + 1);
         off[i].wtmp = bp.take<uint64_t>((size_t)(t.smax + 1) * ((t.G + 7) / 8));
@@ -491,9 +507,10 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
         J.G = t.G; J.C = t.C; J.R = t.Reff; J.smax = t.smax; J.u = t.u; J.mask = t.mask; J.Lcap = t.Lcap;
         J.beta = (const int64_t*)at(off[i].beta);
         J.need = (const int32_t*)at(off[i].need);
-        J.V = (int64_t*)at(off[i].V);
-        J.best = (int64_t*)at(off[i].best);
-        J.barg = (int32_t*)at(off[i].barg);
+        J.ncp = ncp[i];
+        J.V = at(off[i].V);
+        J.best = at(off[i].best);
+        J.barg = (uint8_t*)at(off[i].barg);
         J.bstar = (int64_t*)at(off[i].bstar);
         J.sidx = (int32_t*)at(off[i].sidx);
         J.wtmp = (uint64_t*)at(off[i].wtmp);
@@ -515,7 +532,7 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
     CU(cudaMemcpyAsync(base, h.data(), in_bytes, cudaMemcpyHostToDevice, s->st));
     LevelJob* djobs = (LevelJob*)at(o_jobs);
     for (int c0 = 0; c0 < nt; c0 += 64)   // K1 handles up to 64 tables per cooperative launch
-        CU(launch_levels(djobs + c0, jobs.data() + c0, std::min(64, nt - c0), s->st));
+        CU(launch_levels(djobs + c0, jobs.data() + c0, std::min(64, nt - c0), v32, s->st));
     int32_t* dL = (int32_t*)at(o_L);
     s->tabL.resize(nt);
     CU(cudaMemcpyAsync(s->tabL.data(), dL, 4 * nt, cudaMemcpyDeviceToHost, s->st));
@@ -705,6 +722,14 @@ static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
         o_pln = bp.take<int32_t>(n);
         o_wb = bp.take<uint32_t>(n * (size_t)((su.units_max + 31) >> 5));
     }
+    // representatives of the step / inner precomputation (fast pass 1, batches)
+    size_t aslots = 0, o_akey = 0, o_aslot = 0;
+    if (en && su.aux_bytes > 0 && n > 1) {
+        aslots = 1024;
+        while (aslots < 2 * n) aslots <<= 1;
+        o_akey = bp.take<AKey>(n);
+        o_aslot = bp.take<unsigned long long>(2 * aslots);
+    }
     unsigned char* base;
     if (reuse && reuse->base && reuse->cap >= bp.off) {
         base = reuse->base;
@@ -728,6 +753,9 @@ static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
         wk.bandlist = (uint64_t*)(base + o_bandl);
         if (o_sure) wk.submin_sure = (float*)(base + o_sure);
     }
+    wk.aslots = (int32_t)aslots;
+    wk.akey = aslots ? (AKey*)(base + o_akey) : nullptr;
+    wk.aslot = aslots ? (unsigned long long*)(base + o_aslot) : nullptr;
     wk.m32 = (float*)(base + o_m32);
     wk.m32_sure = (float*)(base + o_m32s);
     wk.hstar = (U256*)(base + o_hs);
@@ -1070,6 +1098,7 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     int stride = o->group_stride > 0 ? o->group_stride : 1;
     MatOut mo{};
     mo.group_stride = stride;
+    mo.gsum = s->W * std::max(1, s->gmax);
     if (s->on_device) {
         mo.status = o->status; mo.levels = o->winner_levels; mo.index = o->winner_index; mo.objective = o->objective;
         mo.makespan = o->makespan_ns; mo.power = o->power_w; mo.energy = o->energy_j; mo.thr = o->throughput_rps;

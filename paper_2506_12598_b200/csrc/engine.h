@@ -32,9 +32,11 @@ struct LevelJob {
     int32_t Lcap;               // capacity of the outputs
     const int64_t* beta;        // [G*C] group solo times (ns)
     const int32_t* need;        // [G*C] n_g c_j / u
-    int64_t* V;                 // workspace [G*C*(R+1)*(smax+1)] (< 2^31 entries)
-    int64_t* best;              // workspace [2][(R+1)*(smax+1)][2]: best / second-best over j (2 layer buffers)
-    int32_t* barg;              // workspace [2][(R+1)*(smax+1)] arg-best
+    int32_t ncp;                // cells (r, s) of a layer, (R+1)(smax+1), padded to a multiple of 32 (each
+                                //   layer's slabs 128-byte aligned: layer data is read through L1, see levels.cu)
+    void* V;                    // workspace [G][C][ncp] suffix optima (int32 when v32, else int64)
+    void* best;                 // workspace [G][ncp][2]: best / second best over j, per layer
+    uint8_t* barg;              // workspace [G][ncp] arg-best (255: none)
     int64_t* bstar;             // workspace [smax+1] B*(s)
     int32_t* sidx;              // workspace [smax+1] compacted level -> s
     uint64_t* wtmp;             // workspace [(smax+1) * ceil(G/8)] packed witnesses in s order
@@ -45,7 +47,8 @@ struct LevelJob {
     int32_t* outL;              // [1]
 };
 
-cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, cudaStream_t st);
+// v32: every table's suffix sums fit int32 (V / best stored as int32, half the traffic of the layers)
+cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, bool v32, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
 // Staged per-level record of one worker inside one problem (written by the prep kernel).
@@ -91,6 +94,12 @@ struct Prob {
     uint64_t wt[MAXW];
     float wf[MAXW];
     double wv[MAXW];
+    // representative problem of this one's step / inner-worker precomputation (fast pass 1): the aux block,
+    // hulls, row-feasibility table and row-bound header depend only on (step table, inner table, their QoS
+    // thresholds, Lambda, the hi workers' S' range), so problems of a batch with equal keys share the first
+    // one's (k_akey / k_arep); rep == own index otherwise
+    int32_t rep;
+    int32_t pad_rep;
 };
 
 // Settings shared by all problems of one launch sequence
@@ -178,11 +187,20 @@ struct Work {
     int32_t* thull_n;           // [tables]
     uint16_t* tord;             // [tables * Lmax] level indices of every level table in S order (k_table_hull)
     const int32_t* table_of;    // [n * W] table of each (problem, worker) (PrepIn.table_of)
+    struct AKey* akey;          // [n] the precomputation key of every problem (k_akey)
+    unsigned long long* aslot;  // [2 * aslots] hash table {hash, min problem index} of the keys
+    int32_t aslots;             // slot count (power of two, >= 2 n); 0: no deduplication
     Tables tb;                  // the level tables
     cudaEvent_t kev[2];         // recorded on the launching stream around the dominant pass-1 kernel (or null)
 };
 
 constexpr int FT_CAP = 8192;    // entries of the exact row-feasibility table per problem
+
+struct AKey {                   // what a problem's step / inner-worker precomputation depends on (Prob::rep)
+    int32_t tab_step, tab_inner, t0, t1;   // level tables; range of the hi workers' S' sums
+    int64_t lam;
+    u128 hq_step, hq_inner;                // exact QoS thresholds floor(Q D)
+};
 #ifndef BAND_CAP_N
 #define BAND_CAP_N 64
 #endif
@@ -238,6 +256,7 @@ struct MatOut {                 // materialisation outputs (device pointers, may
     double* power; double* energy; double* thr; double* latency; int32_t* switches; int32_t* group_sm;
     double* group_lat; int32_t group_stride; uint64_t* key;
     double* energy_busy;        // [n] busy-SM energy integral of the predicted run (J; R21)
+    int32_t gsum;               // >= sum over workers of the group counts (busy-energy staging)
 };
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C,
                                MatOut out, cudaStream_t st);

@@ -78,6 +78,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         " @!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
 }
 
+// two pieces (level records, then an aux block from elsewhere) into consecutive shared memory, one barrier
+__device__ __forceinline__ void stage_levels2(Lev* sl, const Lev* g1, unsigned b1, const Lev* g2, unsigned b2,
+                                              uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, b1 + b2);
+        const unsigned CH = 32768;
+        for (unsigned off = 0; off < b1; off += CH)
+            bulk_g2s((char*)sl + off, (const char*)g1 + off, b1 - off < CH ? b1 - off : CH, bar);
+        for (unsigned off = 0; off < b2; off += CH)
+            bulk_g2s((char*)sl + b1 + off, (const char*)g2 + off, b2 - off < CH ? b2 - off : CH, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+}
+
 // stage the problem's level records (W x Lmax x 32 B, contiguous) into shared memory
 __device__ __forceinline__ void stage_levels(Lev* sl, const Lev* gl, unsigned bytes, uint64_t* bar) {
     if (threadIdx.x == 0) {
@@ -148,6 +164,7 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
     memset(&P, 0, sizeof(P));
     P.W = su.W;
     P.status = 0;
+    P.rep = p;
     const int W = su.W;
     u64 lam = 1;
     for (int w = 0; w < W; w++) {
@@ -300,6 +317,94 @@ __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
 
 
 // ------------------------------------------------------------------------------------------
+// Sharing of the step / inner-worker precomputation inside a batch.  A problem's aux block (k_prep_aux),
+// hulls, row-feasibility table and row-bound header (k_prep_bound) are functions of its AKey only; the
+// problems of a batch with equal keys (mixes drawn from one model library share worker pairs) use the
+// first one's.  k_akey: one warp per problem computes the key (the hi workers' S' sum range from their
+// level records) and inserts its hash into an open-addressing table with the minimum problem index;
+// k_arep: each problem looks its hash up and takes that index as its representative when the two keys
+// are equal (any hash collision falls back to itself).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long akey_hash(const AKey& k) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull;
+    auto mix = [&](unsigned long long v) {
+        h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xff51afd7ed558ccdull;
+        h ^= h >> 33;
+    };
+    mix(((unsigned long long)(uint32_t)k.tab_step << 32) | (uint32_t)k.tab_inner);
+    mix(((unsigned long long)(uint32_t)k.t0 << 32) | (uint32_t)k.t1);
+    mix((unsigned long long)k.lam);
+    mix((unsigned long long)k.hq_step); mix((unsigned long long)(k.hq_step >> 64));
+    mix((unsigned long long)k.hq_inner); mix((unsigned long long)(k.hq_inner >> 64));
+    return h | 1ull;   // 0 marks an empty slot
+}
+__device__ __forceinline__ bool akey_eq(const AKey& a, const AKey& b) {
+    return a.tab_step == b.tab_step && a.tab_inner == b.tab_inner && a.t0 == b.t0 && a.t1 == b.t1 && a.lam == b.lam &&
+           a.hq_step == b.hq_step && a.hq_inner == b.hq_inner;
+}
+
+__global__ void __launch_bounds__(256) k_akey(Setup su, const Prob* probs, const Lev* levs, AKey* keys,
+                                              unsigned long long* slot, int nslots) {
+    const int p = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (p >= su.n_problems) return;
+    const Prob& P = probs[p];
+    const int W = su.W, Lmax = su.Lmax;
+    AKey k;
+    k.t0 = -1;   // no sharing (invalid problem)
+    if (P.status == 0) {
+        const Lev* base = levs + (size_t)p * su.lev_stride;
+        int t0 = 0, t1 = 0;
+        for (int w = 0; w < W - 2; w++) {
+            int mn = 1 << 30, mx = 0;
+            for (int l = lane; l < P.L[w]; l += 32) {
+                const int v = (int)base[(size_t)w * Lmax + l].S;
+                mn = min(mn, v); mx = max(mx, v);
+            }
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            t0 += mn; t1 += mx;
+        }
+        k.tab_step = P.table[W >= 2 ? W - 2 : 0]; k.tab_inner = P.table[W - 1];
+        k.t0 = t0; k.t1 = t1; k.lam = P.lam;
+        k.hq_step = P.Hq[W >= 2 ? W - 2 : 0]; k.hq_inner = P.Hq[W - 1];
+    }
+    if (lane != 0) return;
+    keys[p] = k;
+    if (k.t0 < 0) return;
+    const unsigned long long h = akey_hash(k);
+    unsigned long long* hs = slot;
+    unsigned long long* ix = slot + nslots;
+    for (int i = (int)(h & (unsigned long long)(nslots - 1)), n = 0; n < nslots; i = (i + 1) & (nslots - 1), n++) {
+        const unsigned long long prev = atomicCAS(hs + i, 0ull, h);
+        if (prev == 0ull || prev == h) {
+            atomicMin(ix + i, (unsigned long long)p);
+            return;
+        }
+    }
+}
+
+__global__ void k_arep(Setup su, Prob* probs, const AKey* keys, const unsigned long long* slot, int nslots) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= su.n_problems) return;
+    const AKey k = keys[p];
+    int rep = p;
+    if (k.t0 >= 0) {
+        const unsigned long long h = akey_hash(k);
+        for (int i = (int)(h & (unsigned long long)(nslots - 1)), n = 0; n < nslots; i = (i + 1) & (nslots - 1), n++) {
+            const unsigned long long hv = slot[i];
+            if (hv == 0ull) break;
+            if (hv == h) {
+                const int q = (int)slot[nslots + i];
+                if (q < p && akey_eq(keys[q], k)) rep = q;
+                break;
+            }
+        }
+    }
+    probs[p].rep = rep;
+}
+
+// ------------------------------------------------------------------------------------------
 // fast pass-1 aux block (per problem, right after its Lev records; staged with them)
 //   ip    float4[LP]   inner levels sorted by S', in pairs {B_k, B_k+1, S'_k, S'_k+1}
 //   iu    float2[LP]   {u_k, u_k+1},  u = Tmax - S'  (inner worker's own QoS: Tp <= u)
@@ -373,7 +478,7 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
                                                   const uint16_t* tord, const uint16_t* thull, const int32_t* thull_n) {
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
-    if (P.status != 0) return;
+    if (P.status != 0 || P.rep != prob) return;   // a representative's block serves this problem
     const int W = su.W, Lmax = su.Lmax;
     Lev* base = levs + (size_t)prob * su.lev_stride;
     // the block is built in shared memory from shared copies of the two workers' records, then
@@ -668,7 +773,7 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
     __shared__ int s_t0, s_t1, s_part[256];
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
-    if (P.status != 0 || su.W < 3) return;
+    if (P.status != 0 || su.W < 3 || P.rep != prob) return;   // a representative's tables serve this problem
     const int W = su.W, Lmax = su.Lmax;
     const Lev* gbase = levs + (size_t)prob * su.lev_stride;
     for (int i = threadIdx.x; i < 2 * Lmax; i += blockDim.x) sv[i] = gbase[(size_t)(W - 2) * Lmax + i];
@@ -858,13 +963,14 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
     const int prob = blockIdx.y;
     const Prob& P = probs[prob];
     if (P.status != 0) return;
-    const RowHdr H = hdr[prob];
+    const int rp = P.rep;   // hulls, feasibility table and header of the representative (k_arep)
+    const RowHdr H = hdr[rp];
     const int Lmax = su.Lmax;
-    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)prob * 4 * Lmax + i];
+    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)rp * 4 * Lmax + i];
     __syncthreads();
     const Lev* base = levs + (size_t)prob * su.lev_stride;
     const uint64_t rows = P.units / (uint64_t)P.nseg;
-    const int32_t* ft = ftab + (size_t)prob * FT_CAP;
+    const int32_t* ft = ftab + (size_t)rp * FT_CAP;
     const float invf = P.inv;
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
@@ -955,14 +1061,15 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         if (threadIdx.x == 0) ulist_n[prob] = 0;
         return;
     }
-    const RowHdr H = hdr[prob];
+    const int rp = P.rep;   // hulls, feasibility table and header of the representative (k_arep)
+    const RowHdr H = hdr[rp];
     const Lev* base = levs + (size_t)prob * su.lev_stride;
-    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)prob * 4 * Lmax + i];
+    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)rp * 4 * Lmax + i];
     for (int i = threadIdx.x; i < NH * Lmax; i += blockDim.x) hrec[i] = base[i];
     for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint32_t rows = (uint32_t)P.units;
-    const int32_t* ft = ftab + (size_t)prob * FT_CAP;
+    const int32_t* ft = ftab + (size_t)rp * FT_CAP;
     const float invf = P.inv;
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
@@ -1237,8 +1344,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (threadIdx.x == 0) { s_inc = 0x7f800000u; s_next = 0; }
     }
     Lev* sl = reinterpret_cast<Lev*>(smem_raw);
-    // level records + this problem's aux block in one TMA bulk copy
-    stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
+    // level records + the aux block (this problem's, or its representative's) by TMA bulk copies
+    if (P.rep == prob)
+        stage_levels(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev) + su.aux_bytes), &bar);
+    else
+        stage_levels2(sl, levs + (size_t)prob * su.lev_stride, (unsigned)(W * Lmax * sizeof(Lev)),
+                      levs + (size_t)P.rep * su.lev_stride + (size_t)W * Lmax, (unsigned)su.aux_bytes, &bar);
     const AuxView A = aux_view(smem_raw + (size_t)W * Lmax * sizeof(Lev), Lmax);
     const int nhv = *A.ihn;   // inner hull vertex count (staged with the aux block)
 
@@ -1447,7 +1558,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         float m0 = INFINITY, m1 = INFINITY;
         // sweep the warp's table (<= 32 entries, one per lane): packed FMAs over each entry's exact
         // QoS-feasible inner range; called after every entry pass (surviving entries are rare)
-        auto sweep = [&]() {
+        // The warp's table holds <= 32 entries, one per lane; each lane sweeps its entry's inner range with packed
+        // FMAs.  Without QoS bounds every range is [0, L_inner): the lanes run in lockstep (broadcast reads of
+        // the inner pairs; lanes without an entry score +inf).
+        auto sweep_qos = [&]() {   // per-lane ranges (QoS): each lane its own entry's exact feasible range
             for (int i = wl; i < nc; i += 32) {
                 const float4 t4 = tab[i];
                 int2 kk = tabk[i];
@@ -1493,6 +1607,76 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
                 }
             }
+        };
+        auto sweep = [&]() {
+            if (QOS) { sweep_qos(); return; }
+            const bool has = wl < nc;
+            float4 t4 = make_float4(INFINITY, 0.0f, 0.0f, 0.0f);
+            int2 kk = make_int2(0, 0);
+            if (has) { t4 = tab[wl]; kk = tabk[wl]; }
+            if (QOS && has && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
+                kk.x = -1 - kk.x;
+                const int kend = min(kk.x, kk.y);
+                for (int k = 0; k < kend; k++) {
+                    const float4 r = A.ip[k >> 1];
+                    const float2 uu2 = A.iu[k >> 1];
+                    const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
+                    if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
+                }
+            }
+            const int ka = max(kk.x, 0), kb2 = kk.y;
+            const bool any = has && ka < kb2;
+            if (any) {
+                nfeas += (unsigned long long)(kb2 - ka);
+                if (ka & 1) {   // leading odd element
+                    const float4 r = A.ip[ka >> 1];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += A.iD[ka >> 1].y;
+                    m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
+                }
+                if (kb2 & 1) {  // trailing odd element
+                    const float4 r = A.ip[kb2 >> 1];
+                    float b0 = t4.x;
+                    if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
+                    m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
+                }
+            }
+            // this lane's pairs [pa, pb); the warp sweeps [pmin, pmax)
+            const int pa = any ? (ka + 1) >> 1 : 0, pb = any ? kb2 >> 1 : 0;
+            const unsigned plen = pb > pa ? (unsigned)(pb - pa) : 0u;
+            const int pmin = __reduce_min_sync(0xffffffffu, plen ? pa : INT_MAX);
+            const int pmax = __reduce_max_sync(0xffffffffu, plen ? pb : 0);
+            if (pmin >= pmax) return;
+            const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
+            // four independent minima: the 3-input min of one pair does not wait on the previous one
+            float ma = INFINITY, mb = INFINITY, mc = INFINITY, md = INFINITY;
+            auto pair = [&](int q) -> float {
+                const float4 r = A.ip[q];
+                u64 base = X2;
+                if (MODE == M_PAPER) { const float2 dd = A.iD[q]; base = add2(X2, f2pack(dd.x, dd.y)); }
+                const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+                float k0, k1;
+                f2unpack(key, k0, k1);
+                return fminf(k0, k1);
+            };
+            int p = pmin;
+            if (!QOS) {   // identical ranges: no per-lane test (lanes without an entry score +inf)
+                for (; p + 4 <= pmax; p += 4) {
+                    const float a0 = pair(p), a1 = pair(p + 1), a2 = pair(p + 2), a3 = pair(p + 3);
+                    ma = fminf(ma, a0); mb = fminf(mb, a1); mc = fminf(mc, a2); md = fminf(md, a3);
+                }
+                for (; p < pmax; p++) ma = fminf(ma, pair(p));
+            } else {   // ranges differ by lane (measured: a lockstep sweep over their union with a per-lane
+                       // range test is slower, the union being much wider than a typical range)
+                for (p = pa; p + 4 <= pb; p += 4) {
+                    const float a0 = pair(p), a1 = pair(p + 1), a2 = pair(p + 2), a3 = pair(p + 3);
+                    ma = fminf(ma, a0); mb = fminf(mb, a1); mc = fminf(mc, a2); md = fminf(md, a3);
+                }
+                for (; p < pb; p++) ma = fminf(ma, pair(p));
+            }
+            m0 = fminf(m0, fminf(fminf(ma, mb), fminf(mc, md)));
         };
         // one step entry per lane (relative index k in [ea, ea + ne)); appends the usable ones to
         // the warp's table; returns whether the lane's level lies past the QoS prefix
@@ -2257,7 +2441,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
         if (su.aux_bytes > 0 && W >= 3 && su.obj == O_SUM && (su.mode == M_EXCL || su.mode == M_PAPER) && su.has_qos &&
             e1 - e0 <= P2_ELIST) {
             const AuxView A = aux_view(reinterpret_cast<unsigned char*>(const_cast<Lev*>(levs) +
-                                                                          (size_t)prob * su.lev_stride + (size_t)W * su.Lmax),
+                                                                          (size_t)P.rep * su.lev_stride + (size_t)W * su.Lmax),
                                        su.Lmax);
             int64_t rB = 0, rBS = 0;
             int rT = 0, rTm = 1 << 24;
@@ -2297,8 +2481,8 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
                     const float Ye = fmaf(Sf, invf, Yh), Ze = fmaf(Be, invf, Zh);
                     float lbe = fmaf(Ye, A.preminB[khi], fmaf(Ze, (float)A.ssort[ka], X));
                     if (hull && !(lbe * 0.99998474121f > bound)) {   // the inner hull restricted to the S' range
-                        const float2* hv = hull + ((size_t)prob * 2 + 1) * 2 * su.Lmax;
-                        lbe = fmaxf(lbe, X + hull_min_in(hv, hv + su.Lmax, rowhdr[prob].nh[1], Ye, Ze, (float)A.ssort[ka],
+                        const float2* hv = hull + ((size_t)P.rep * 2 + 1) * 2 * su.Lmax;
+                        lbe = fmaxf(lbe, X + hull_min_in(hv, hv + su.Lmax, rowhdr[P.rep].nh[1], Ye, Ze, (float)A.ssort[ka],
                                                          (float)A.ssort[khi - 1]));
                     }
                     keep = !(lbe * 0.99998474121f > bound);   // 1 - 2^-16
@@ -2377,17 +2561,23 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
 
     U256 best = u256_max();
     uint64_t besti = ~0ull;
+    const int nwp = (int)(blockDim.x >> 5), wlane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (PASS != 1) {
         scan(0, best, besti);
-        red[threadIdx.x] = best;
-        __syncthreads();
-        for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
-            if (threadIdx.x < s2 && u256_cmp(red[threadIdx.x + s2], red[threadIdx.x]) < 0) red[threadIdx.x] = red[threadIdx.x + s2];
-            __syncthreads();
+        // block minimum: warp shuffles, then the warps' minima
+        for (int o = 16; o; o >>= 1) {
+            U256 y;
+            for (int i = 0; i < 4; i++) y.w[i] = __shfl_xor_sync(0xffffffffu, best.w[i], o);
+            if (u256_cmp(y, best) < 0) best = y;
         }
+        if (wlane == 0) red[wid] = best;
+        __syncthreads();
         if (threadIdx.x == 0) {
-            hstar[prob] = red[0];
-            s_hs = red[0];
+            U256 m = red[0];
+            for (int i = 1; i < nwp; i++)
+                if (u256_cmp(red[i], m) < 0) m = red[i];
+            hstar[prob] = m;
+            s_hs = m;
         }
         __syncthreads();
         if (PASS == 0) return;
@@ -2403,13 +2593,17 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, con
     } else {
         scan(1, best, besti);
     }
-    redi[threadIdx.x] = besti;
-    __syncthreads();
-    for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
-        if (threadIdx.x < s2 && redi[threadIdx.x + s2] < redi[threadIdx.x]) redi[threadIdx.x] = redi[threadIdx.x + s2];
-        __syncthreads();
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, besti, o);
+        besti = y < besti ? y : besti;
     }
-    if (threadIdx.x == 0) write_first(redi[0]);
+    if (wlane == 0) redi[wid] = besti;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t m = redi[0];
+        for (int i = 1; i < nwp; i++) m = redi[i] < m ? redi[i] : m;
+        write_first(m);
+    }
 }
 
 cudaError_t launch_pass2_min(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2561,42 +2755,76 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
     // busy-SM energy integral of the predicted run (SPEC integrate_energy S:416-419, power_at S:406-409;
     // DESIGN.md R21): every worker starts at 0 and runs its groups back to back; between consecutive group
     // boundaries the power is p_idle + (p_max - p_idle) min(N, sum of the running groups' SMs) / N
-    if (o.energy_busy && threadIdx.x == 0) {
-        int g[MAXW];
-        double end[MAXW];
-        const uint8_t* wit[MAXW];
-        for (int w = 0; w < W; w++) {
-            const int t = P.table[w];
-            wit[w] = tb.wit[t] + (size_t)lv[w] * tb.G[t];
-            g[w] = 0;
-            end[w] = (double)tb.beta[t][wit[w][0] * C] * (1.0 + alpha_w[w]);
+    if (o.energy_busy) {
+        // all threads: the workers' group end times (sequential sums, as the run) and pool sizes in shared
+        // memory, the ends ranked into time order, then one elementary interval per rank: its busy SMs from a
+        // binary search of each worker's ends, its energy, and a block sum
+        extern __shared__ __align__(8) unsigned char msm[];
+        const int gs = o.gsum;
+        double* ends = reinterpret_cast<double*>(msm);     // [gs] per worker, groups in order
+        double* srt = ends + gs;                           // [gs] all ends in time order
+        int* csz = reinterpret_cast<int*>(srt + gs);       // [gs] pool size of each group
+        __shared__ int goff[MAXW + 1];
+        __shared__ double red_e[4];
+        if (threadIdx.x == 0) {
+            goff[0] = 0;
+            for (int w = 0; w < W; w++) goff[w + 1] = goff[w] + tb.G[P.table[w]];
         }
-        const double N = (double)su.N, pi = (double)P.p_idle, pd = (double)P.p_max - (double)P.p_idle;
-        double t = 0.0, E = 0.0;
-        for (;;) {
-            double nxt = INFINITY;
-            int busy = 0;
-            for (int w = 0; w < W; w++)
-                if (g[w] < tb.G[P.table[w]]) {
-                    nxt = fmin(nxt, end[w]);
-                    busy += sizes[wit[w][g[w]]];
-                }
-            if (isinf(nxt)) break;
-            E += (pi + pd * (double)min(busy, su.N) / N) * (nxt - t);
-            t = nxt;
-            for (int w = 0; w < W; w++) {
-                const int tw = P.table[w];
-                if (g[w] < tb.G[tw] && end[w] == nxt && ++g[w] < tb.G[tw])
-                    end[w] += (double)tb.beta[tw][g[w] * C + wit[w][g[w]]] * (1.0 + alpha_w[w]);
+        __syncthreads();
+        const int n = goff[W];
+        for (int w = threadIdx.x; w < W; w += blockDim.x) {   // one thread per worker: its run, in order
+            const int t = P.table[w], G = tb.G[t];
+            const uint8_t* wt = tb.wit[t] + (size_t)lv[w] * G;
+            double e = 0.0;
+            for (int g = 0; g < G; g++) {
+                e += (double)tb.beta[t][g * C + wt[g]] * (1.0 + alpha_w[w]);
+                ends[goff[w] + g] = e;
+                csz[goff[w] + g] = sizes[wt[g]];
             }
         }
-        o.energy_busy[p] = E * 1e-9;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {   // rank of end i (ties by position)
+            const double v = ends[i];
+            int rk = 0;
+            for (int j = 0; j < n; j++) rk += ends[j] < v || (ends[j] == v && j < i);
+            srt[rk] = v;
+        }
+        __syncthreads();
+        const double Nd = (double)su.N, pi = (double)P.p_idle, pd = (double)P.p_max - (double)P.p_idle;
+        double E = 0.0;
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {   // interval [srt[k-1], srt[k])
+            const double t0 = k ? srt[k - 1] : 0.0, t1 = srt[k];
+            if (!(t1 > t0)) continue;
+            int busy = 0;
+            for (int w = 0; w < W; w++) {   // the worker's group running at t0: first end > t0
+                int lo = goff[w], hi = goff[w + 1];
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ends[mid] <= t0) lo = mid + 1; else hi = mid;
+                }
+                if (lo < goff[w + 1]) busy += csz[lo];
+            }
+            E += (pi + pd * (double)min(busy, su.N) / Nd) * (t1 - t0);
+        }
+        for (int off = 16; off; off >>= 1) E += __shfl_xor_sync(0xffffffffu, E, off);
+        if ((threadIdx.x & 31) == 0) red_e[threadIdx.x >> 5] = E;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += red_e[i];
+            o.energy_busy[p] = tot * 1e-9;
+        }
     }
 }
 
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C, MatOut out,
                                cudaStream_t st) {
-    k_materialize<<<su.n_problems, 128, 0, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes, C, out);
+    const size_t sm = out.energy_busy ? (size_t)out.gsum * 20 : 0;   // busy-energy staging (k_materialize)
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute((const void*)k_materialize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    k_materialize<<<su.n_problems, 128, sm, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes, C, out);
     return cudaGetLastError();
 }
 
@@ -2618,6 +2846,13 @@ cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Wor
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
     if (su.aux_bytes > 0) {
         cudaError_t e;
+        if (su.n_problems > 1 && wk.aslots > 0) {   // representatives of the step / inner precomputation
+            const size_t ns = (size_t)wk.aslots;
+            if ((e = cudaMemsetAsync(wk.aslot, 0, ns * 8, st)) != cudaSuccess) return e;
+            if ((e = cudaMemsetAsync(wk.aslot + ns, 0xff, ns * 8, st)) != cudaSuccess) return e;
+            k_akey<<<(su.n_problems + 7) / 8, 256, 0, st>>>(su, wk.probs, wk.levs, wk.akey, wk.aslot, wk.aslots);
+            k_arep<<<(su.n_problems + 255) / 256, 256, 0, st>>>(su, wk.probs, wk.akey, wk.aslot, wk.aslots);
+        }
         if (table_hull && (e = launch_table_hull(su, tb, wk, st)) != cudaSuccess) return e;
         const size_t sm = (size_t)2 * su.Lmax * sizeof(Lev) + (size_t)su.aux_bytes;
         auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;

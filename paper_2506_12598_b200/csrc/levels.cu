@@ -29,65 +29,86 @@ namespace cg = cooperative_groups;
 
 namespace eclip {
 
-static constexpr int64_t INF64 = INT64_MAX;
 static constexpr int MAXJ = 64;      // tables per launch (host splits larger sets)
 
-__device__ __forceinline__ int vidx(const LevelJob& J, int g, int j, int r, int s) {
-    return (((g * J.C + j) * (J.R + 1) + r) * (J.smax + 1)) + s;
+template <class VT> struct VPair;
+template <> struct VPair<int32_t> { typedef int2 T; };
+template <> struct VPair<int64_t> { typedef longlong2 T; };
+template <class VT> __device__ __forceinline__ VT vinf() { return VT(~(unsigned long long)0 >> (65 - 8 * sizeof(VT))); }
+
+__device__ __forceinline__ size_t vidx(const LevelJob& J, int g, int j, int k) {
+    return ((size_t)g * J.C + j) * J.ncp + k;
 }
 __device__ __forceinline__ int nwords(const LevelJob& J) { return (J.G + 7) / 8; }
 
-// one (r, s) cell of layer g = G-1-step: V for all sizes j, and best / second best / arg over j
-template <int CM>   // CM >= J.C: the loops over sizes are unrolled, so their loads are issued together
+// one (r, s) cell k of layer g = G-1-step: V for all sizes j, and best / second best / arg over j.
+// Layer g+1's V, best and arg are read through L1 (plain loads): every layer has its own 128-byte
+// aligned region, written completely in its step and read only after the grid barrier that ends it,
+// so no SM can hold a line of it from before it was written; neighbouring cells read overlapping
+// best / arg entries (s - need_j for the C sizes j), which L1 then serves.
+template <int CM, class VT>   // CM >= J.C: the loops over sizes are unrolled, so their loads are issued together
 __device__ __forceinline__ void dp_cell(const LevelJob& J, int step, int k) {
-    const int S1 = J.smax + 1, ncell = (J.R + 1) * S1;
+    typedef typename VPair<VT>::T P2;
+    const VT INF = vinf<VT>();
+    const int S1 = J.smax + 1;
     const int r = k / S1, s = k - r * S1;
     const int g = J.G - 1 - step;
-    const int cur = g & 1, nxt = cur ^ 1;
-    int64_t b1 = INF64, b2 = INF64;
-    int a1 = -1;
-    // all loads of the cell first (independent across j, so they overlap), then the stores
-    int64_t outv[CM];
+    VT* V = reinterpret_cast<VT*>(J.V);
+    const P2* bestp = reinterpret_cast<const P2*>(J.best);
+    VT b1 = INF, b2 = INF;
+    int a1 = 255;
+    // Branch-free: every load of the cell is issued unconditionally at a clamped (valid) address and the
+    // unused values are discarded by selects, so the C sizes' loads are all in flight together (with a
+    // branch per size the compiler keeps them inside the branches: one L2 round trip per size).
+    const int gn = g + 1 < J.G ? g + 1 : g;   // (layer G-1 reads nothing)
+    const bool last = g == J.G - 1;
+    const int rm = r >= 1 ? r - 1 : 0;
+    VT lv[CM], lb1[CM], lb2[CM];
+    int la[CM], lnd[CM];
 #pragma unroll
-    for (int j = 0; j < CM; j++) {
-        int64_t out = INF64;
-        if (j < J.C && ((J.mask >> j) & 1u)) {
-            const int nd = J.need[g * J.C + j];
-            const int64_t b = J.beta[g * J.C + j];
-            if (g == J.G - 1) {
-                if (s == nd) out = b;
-            } else if (nd <= s) {
-                const int sp = s - nd;
-                int64_t v = __ldcg(J.V + vidx(J, g + 1, j, r, sp));   // written by other CTAs last layer: L2
-                if (r >= 1) {   // arg, best and second best loaded together (no dependent load)
-                    const int bi = nxt * ncell + (r - 1) * S1 + sp;
-                    const int ab = __ldcg(J.barg + bi);
-                    const longlong2 bb2 = __ldcg(reinterpret_cast<const longlong2*>(J.best) + bi);
-                    const int64_t w = ab != j ? bb2.x : bb2.y;
-                    if (w < v) v = w;
-                }
-                if (v != INF64) out = b + v;
-            }
-        }
-        outv[j] = out;
+    for (int j = 0; j < CM; j++) {   // loads only
+        const int jc = j < J.C ? j : J.C - 1;
+        const int nd = J.need[g * J.C + jc];
+        const int sp = nd <= s ? s - nd : 0;
+        lnd[j] = nd;
+        lv[j] = V[vidx(J, gn, jc, r * S1 + sp)];
+        const size_t bi = (size_t)gn * J.ncp + rm * S1 + sp;
+        la[j] = J.barg[bi];
+        const P2 bb2 = bestp[bi];
+        lb1[j] = bb2.x; lb2[j] = bb2.y;
+    }
+    VT outv[CM];
+#pragma unroll
+    for (int j = 0; j < CM; j++) {   // then the arithmetic, as selects
+        const int jc = j < J.C ? j : J.C - 1;
+        const bool act = j < J.C && ((J.mask >> j) & 1u);
+        const VT b = (VT)J.beta[g * J.C + jc];
+        const VT w = la[j] != j ? lb1[j] : lb2[j];
+        const VT v = (r >= 1 && w < lv[j]) ? w : lv[j];
+        const VT o_last = (act && s == lnd[j]) ? b : INF;
+        const VT o_in = (act && lnd[j] <= s && v != INF) ? b + v : INF;
+        outv[j] = last ? o_last : o_in;
     }
 #pragma unroll
     for (int j = 0; j < CM; j++) {
         if (j >= J.C) break;
-        const int64_t out = outv[j];
-        J.V[vidx(J, g, j, r, s)] = out;
+        const VT out = outv[j];
+        V[vidx(J, g, j, k)] = out;
         if (out < b1) { b2 = b1; b1 = out; a1 = j; }
         else if (out < b2) { b2 = out; }
     }
-    const int bo = cur * ncell + k;
-    J.best[2 * bo] = b1;
-    J.best[2 * bo + 1] = b2;
-    J.barg[bo] = a1;
+    const size_t bo = (size_t)g * J.ncp + k;
+    P2 o;
+    o.x = b1; o.y = b2;
+    reinterpret_cast<P2*>(J.best)[bo] = o;
+    J.barg[bo] = (uint8_t)a1;
 }
 
 // greedy reconstruction of level l's canonical witness (packed words)
-template <int CM>
+template <int CM, class VT>
 __device__ __forceinline__ void reconstruct(const LevelJob& J, int l) {
+    const VT* V = reinterpret_cast<const VT*>(J.V);
+    const int S1 = J.smax + 1;
     int rem = J.sidx[l];
     int64_t opt = J.bstar[rem];
     int r = J.R, prev = -1;
@@ -96,20 +117,19 @@ __device__ __forceinline__ void reconstruct(const LevelJob& J, int l) {
     for (int g = 0; g < J.G; g++) {
         int pick = -1;
         // the candidates' values are loaded together (independent), then the first match is taken
-        int64_t cv[CM];
+        VT cv[CM];
 #pragma unroll
-        for (int j = 0; j < CM; j++) {
-            cv[j] = INF64;
-            if (j >= J.C || !((J.mask >> j) & 1u)) continue;
-            const int nd = J.need[g * J.C + j];
-            if (nd > rem) continue;
+        for (int j = 0; j < CM; j++) {   // branch-free: every load issued (clamped address), then selected
+            const int jc = j < J.C ? j : J.C - 1;
+            const int nd = J.need[g * J.C + jc];
             const int rr = (g == 0 || j == prev) ? r : r - 1;
-            if (rr < 0) continue;
-            cv[j] = J.V[vidx(J, g, j, rr, rem)];
+            const bool ok = j < J.C && ((J.mask >> j) & 1u) && nd <= rem && rr >= 0;
+            const VT v = V[vidx(J, g, jc, (rr >= 0 ? rr : 0) * S1 + rem)];
+            cv[j] = ok ? v : vinf<VT>();
         }
 #pragma unroll
         for (int j = CM - 1; j >= 0; j--)   // the smallest matching j
-            if (j < J.C && cv[j] == opt) pick = j;
+            if (j < J.C && (int64_t)cv[j] == opt) pick = j;
         if (pick < 0) pick = 0;   // unreachable: opt is attained
         if (g > 0 && pick != prev) r--;
         opt -= J.beta[g * J.C + pick];
@@ -141,6 +161,7 @@ __device__ __forceinline__ void rank_level(const LevelJob& J, int l, int L) {
 }
 
 // B*(s) = best over j of layer 0 at r = R; compact the attained levels (one CTA per table)
+template <class VT>
 __device__ __forceinline__ void compact_table(const LevelJob& J) {
     __shared__ int s_count;
     __shared__ int s_warp[32];
@@ -149,12 +170,13 @@ __device__ __forceinline__ void compact_table(const LevelJob& J) {
     const int S1 = J.smax + 1;
     for (int base = 0; base <= J.smax; base += blockDim.x) {
         const int s = base + threadIdx.x;
-        int64_t b = INF64;
+        int64_t b = INT64_MAX;
         if (s <= J.smax) {
-            b = J.best[2 * (J.R * S1 + s)];   // layer 0 lives in buffer 0
+            const VT v = reinterpret_cast<const VT*>(J.best)[2 * ((size_t)J.R * S1 + s)];   // layer 0, r = R
+            b = v == vinf<VT>() ? INT64_MAX : (int64_t)v;
             J.bstar[s] = b;
         }
-        const int valid = (s <= J.smax) && (b != INF64);
+        const int valid = (s <= J.smax) && (b != INT64_MAX);
         const unsigned bal = __ballot_sync(0xffffffffu, valid);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         if (lane == 0) s_warp[warp] = __popc(bal);
@@ -183,7 +205,7 @@ __device__ unsigned long long k1_dbg[80];
 #else
 #define K1_STAMP(i)
 #endif
-template <int CM>
+template <int CM, class VT>
 __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ jobs, int n_jobs, int gmax,
                                                 size_t wsm_words) {
     cg::grid_group grid = cg::this_grid();
@@ -210,14 +232,14 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             while (off[t + 1] <= i) t++;
             const LevelJob& J = sj[t];
             const int k = i - off[t];
-            dp_cell<CM>(J, step, k);
+            dp_cell<CM, VT>(J, step, k);
         }
         grid.sync();
     }
 
     K1_STAMP(70)
     // ---- per table (one CTA each): B*(s) = best over j of layer 0 at r = R; compact ----
-    for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) compact_table(sj[t]);
+    for (int t = blockIdx.x; t < n_jobs; t += gridDim.x) compact_table<VT>(sj[t]);
     grid.sync();
     K1_STAMP(71)
 
@@ -235,7 +257,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         while (off[t + 1] <= i) t++;
         const LevelJob& J = sj[t];
         const int l = i - off[t];
-        reconstruct<CM>(J, l);
+        reconstruct<CM, VT>(J, l);
     }
     grid.sync();
     K1_STAMP(72)
@@ -279,7 +301,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     K1_STAMP(73)
 }
 
-cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, cudaStream_t st) {
+cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, bool v32, cudaStream_t st) {
     if (n_jobs > MAXJ) return cudaErrorInvalidValue;
     int gmax = 0;
     for (int i = 0; i < n_jobs; i++) gmax = h_jobs[i].G > gmax ? h_jobs[i].G : gmax;
@@ -297,12 +319,19 @@ cudaError_t launch_levels(LevelJob* d_jobs, const LevelJob* h_jobs, int n_jobs, 
     size_t wsm_words = wsm;
     int cmax = 0;
     for (int i = 0; i < n_jobs; i++) cmax = h_jobs[i].C > cmax ? h_jobs[i].C : cmax;
-    const void* kf = cmax <= 8 ? (const void*)k_levels<8> : cmax <= 16 ? (const void*)k_levels<16> : (const void*)k_levels<32>;
+    const void* kf = v32 ? (cmax <= 8    ? (const void*)k_levels<8, int32_t>
+                            : cmax <= 12 ? (const void*)k_levels<12, int32_t>
+                            : cmax <= 16 ? (const void*)k_levels<16, int32_t>
+                                         : (const void*)k_levels<32, int32_t>)
+                         : (cmax <= 8    ? (const void*)k_levels<8, int64_t>
+                            : cmax <= 12 ? (const void*)k_levels<12, int64_t>
+                            : cmax <= 16 ? (const void*)k_levels<16, int64_t>
+                                         : (const void*)k_levels<32, int64_t>);
     e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsm * 8));
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, wsm * 8);
     if (e != cudaSuccess) return e;
-    if (per_sm > 2) per_sm = 2;
+    if (per_sm > 4) per_sm = 4;   // more resident threads: fewer cells per thread on a layer's critical path
     int grid = nsm * (per_sm > 0 ? per_sm : 1);
     void* args[] = {(void*)&d_jobs, (void*)&n_jobs, (void*)&gmax, (void*)&wsm_words};
 #ifdef K1_DEBUG

@@ -49,6 +49,20 @@ __device__ __forceinline__ int64_t overlap_exact(int mode, int64_t Tp, int64_t S
 // ------------------------------------------------------------------------------------------
 constexpr int RB = 9;
 constexpr int KU = 8;
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 f2pack(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(u64 v, float& lo, float& hi) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 
 template <int OBJ>
 __device__ __forceinline__ float comb_f(float g, float d) { return OBJ == O_SUM ? g + d : fmaxf(g, d); }
@@ -117,12 +131,38 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
                     for (int i = 0; i < RB + KU - 1; i++) win[i] = at(Dn, b - k - KU + 1 + i);
 #pragma unroll
                     for (int u = 0; u < KU; u++) gg[u] = gw2[k + u];
+                    if (OBJ == O_SUM) {
+                        // packed adds: output j at level k+u reads win[j + KU-1-u]; the window is consumed as the
+                        // aligned pairs (win[2q], win[2q+1]) for both parities of u (j even / odd), so each level
+                        // is 4 add.f32x2 (g broadcast) + 1 scalar add for the 9 outputs
 #pragma unroll
-                    for (int u = 0; u < KU; u += 2)
+                        for (int u = 0; u < KU; u += 2) {
+                            float s0[RB], s1[RB];
+                            auto sums = [&](int uu, float* sv) {
+                                const int off = KU - 1 - uu;   // win index of output j = j + off
+                                const u64 g2 = f2pack(gg[uu], gg[uu]);
 #pragma unroll
-                        for (int j = 0; j < RB; j++)   // Dn[b + j - (k + u)] = win[j + KU - 1 - u]
-                            best[j] = fminf(best[j], fminf(comb_f<OBJ>(gg[u], win[j + KU - 1 - u]),
-                                                           comb_f<OBJ>(gg[u + 1], win[j + KU - 2 - u])));
+                                for (int j = (off & 1); j + 1 < RB; j += 2) {
+                                    float lo, hi;
+                                    f2unpack(add2(f2pack(win[j + off], win[j + off + 1]), g2), lo, hi);
+                                    sv[j] = lo; sv[j + 1] = hi;
+                                }
+                                if (off & 1) sv[0] = gg[uu] + win[off];                  // j = 0 alone
+                                else sv[RB - 1] = gg[uu] + win[RB - 1 + off];            // j = RB-1 alone
+                            };
+                            sums(u, s0);
+                            sums(u + 1, s1);
+#pragma unroll
+                            for (int j = 0; j < RB; j++) best[j] = fminf(best[j], fminf(s0[j], s1[j]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < KU; u += 2)
+#pragma unroll
+                            for (int j = 0; j < RB; j++)   // Dn[b + j - (k + u)] = win[j + KU - 1 - u]
+                                best[j] = fminf(best[j], fminf(comb_f<OBJ>(gg[u], win[j + KU - 1 - u]),
+                                                               comb_f<OBJ>(gg[u + 1], win[j + KU - 2 - u])));
+                    }
                 }
                 for (; k < ke; k++) {
                     const float gk = gw2[k];
