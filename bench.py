@@ -315,6 +315,7 @@ def main():
             c = tp.counters()
             kms.append(c["kernel_ms"]); evald.append(c["evaluated_candidates"]); units.append(c["units_processed"])
             swept = c["units_with_swept_entries"]; entries = c["entries_swept"]
+            funnel = {k: c[k] for k in ("units_past_unit_bound", "units_with_kept_chunks", "chunks_kept")}
     torch.cuda.synchronize()
     phase_ms = {k: float(np.median([p[k] for p in phases])) for k in phases[0]}
     k_ms = float(np.median(kms))
@@ -378,9 +379,9 @@ def main():
             "phases_ms": phase_ms,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_max / a.steps, "api": "eclip_planner_plan (host batch, pinned buffers)"},
-            # per step: k_prep_prob, k_prep_lev, k_prep_aux, 2 x k_fill_u32, k_prep_bound, k_rowlb_fused,
-            # k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/ launch list)
-            "gpu_launches": int(11 * a.steps),
+            # per step: k_prep_prob, k_prep_lev, k_akey, k_arep, k_prep_aux, 2 x k_fill_u32, k_prep_bound,
+            # k_rowlb_fused, k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/ launch list)
+            "gpu_launches": int(13 * a.steps),
             "roofline": {"bound": "alu", "kernel": "k_pass1_fast<W=4,EXCLUDE_SELF,QoS,pruned>", "achieved": achieved,
                          "peak": peak, "unit": "G FP32 lane-ops/s (148 SM x 128 lanes x 1965 MHz)",
                          "frac": achieved / peak, "traffic": ncu.get("bytes_per_launch"),
@@ -389,7 +390,7 @@ def main():
                          "kernel_ms_per_launch": k_ms, "kernel_share_of_step": k_ms / (t_max_ms / a.steps),
                          "issue_slots_busy_pct_ncu": ncu.get("issue_active_pct"),
                          "units_processed_per_launch": int(np.median(units)),
-                         "units_with_swept_entries": swept, "entries_swept": entries},
+                         "units_with_swept_entries": swept, "entries_swept": entries, **funnel},
             "clocks": ck,
             "host": host_info(),
             "time_to_plan_ms": ttp,

@@ -299,7 +299,8 @@ int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
  * [2] device time in ns of the last launch of the dominant pass-1 kernel (k_pass1_fast or
  * k_pass1_gen), from CUDA events recorded around it on the launching stream (0 for SLICE),
  * [3] pruned pass 1: units in which at least one step entry survived the chunk / entry bounds and
- * was swept, [4] entries swept.
+ * was swept, [4] entries swept, [5] units that passed the exact QoS range cut and the unit bound,
+ * [6] units with at least one step chunk kept by the chunk bound, [7] chunks kept.
  * Entries beyond the defined ones are set to 0.  Errors: ECLIP_E_INVALID_ARG, ECLIP_E_CUDA. */
 int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n);
 

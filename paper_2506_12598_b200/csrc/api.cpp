@@ -674,7 +674,9 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     su.aux_bytes = 0;
     if (fast) {   // per-problem aux block (staged with the Lev records) + per-warp prefix tables
         su.aux_bytes = (int32_t)pass1_aux_bytes(Lmax);
-        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * 32 * 24);   // 32 entries per warp
+        // 32 entries per warp; 64 in the exhaustive pass without QoS (two per lane, k_pass1_fast TWO)
+        const bool two = !su.has_qos && !pass1_prunable(su);
+        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * (two ? 64 : 32) * 24);
     }
     su.lev_stride = W * Lmax + su.aux_bytes / (int)sizeof(Lev);
     return ECLIP_OK;
@@ -695,7 +697,7 @@ static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
     const size_t ns = n * (size_t)su.units_max;
     const size_t grid = n * (size_t)((su.items_max + su.n_shards - 1) / su.n_shards);
     Bump bp;   // one block; null pieces stay null
-    const size_t o_cnt = bp.take<unsigned long long>(4);   // feasible, rows_done[3] (zeroed)
+    const size_t o_cnt = bp.take<unsigned long long>(8);   // feasible, rows_done[6] (zeroed)
     const size_t o_probs = bp.take<Prob>(n), o_levs = bp.take<Lev>(n * (size_t)su.lev_stride);
     const size_t o_sub = en ? bp.take<float>(ns) : 0, o_bandn = en ? bp.take<int32_t>(n) : 0;
     const size_t o_bandl = en ? bp.take<uint64_t>(n * (size_t)BAND_CAP) : 0;
@@ -739,7 +741,7 @@ static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
     }
     wk.feasible = (unsigned long long*)(base + o_cnt);
     wk.rows_done = wk.feasible + 1;
-    CU(cudaMemsetAsync(wk.feasible, 0, 4 * sizeof(unsigned long long), s->st));
+    CU(cudaMemsetAsync(wk.feasible, 0, 8 * sizeof(unsigned long long), s->st));
     wk.probs = (Prob*)(base + o_probs);
     if (o_th) {
         wk.thull = (uint16_t*)(base + o_th);
@@ -1182,16 +1184,16 @@ extern "C" int eclip_session_stats(eclip_session* s, uint64_t* evaluated) {
 
 extern "C" int eclip_session_counters(eclip_session* s, uint64_t* out, int32_t n) {
     if (!s || !out || n < 0) return fail(ECLIP_E_INVALID_ARG, "null argument");
-    unsigned long long v[5] = {0, 0, 0, 0, 0};
+    unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (s->wk.feasible) CU(cudaMemcpyAsync(&v[0], s->wk.feasible, sizeof v[0], cudaMemcpyDeviceToHost, s->st));
     if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[1], s->wk.rows_done, sizeof v[1], cudaMemcpyDeviceToHost, s->st));
-    if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[3], s->wk.rows_done + 1, 2 * sizeof v[0], cudaMemcpyDeviceToHost, s->st));
+    if (s->wk.rows_done) CU(cudaMemcpyAsync(&v[3], s->wk.rows_done + 1, 5 * sizeof v[0], cudaMemcpyDeviceToHost, s->st));
     CU(cudaStreamSynchronize(s->st));
     float ms = 0.0f;   // the events exist from session creation; unrecorded (SLICE) -> error -> 0
     if (s->engine == ECLIP_ENGINE_ENUM && cudaEventElapsedTime(&ms, s->wk.kev[0], s->wk.kev[1]) == cudaSuccess)
         v[2] = (unsigned long long)llround((double)ms * 1e6);
     cudaGetLastError();
-    for (int i = 0; i < n; i++) out[i] = i < 5 ? v[i] : 0;
+    for (int i = 0; i < n; i++) out[i] = i < 8 ? v[i] : 0;
     return ECLIP_OK;
 }
 

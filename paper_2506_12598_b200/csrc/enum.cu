@@ -1253,7 +1253,8 @@ struct BBArgs {
     const int32_t* ulist_n;     // [grid]
     const unsigned* lbmin;      // [n] smallest row bound of the problem (float bits)
     unsigned* inc;              // [n] global incumbent (float bits)
-    unsigned long long* rows_done;  // [3]: units processed, units with >= 1 swept entry, entries swept
+    unsigned long long* rows_done;  // [6]: units processed, units with >= 1 swept entry, entries swept, units past
+                                    //   the unit bound, units with >= 1 chunk kept, chunks kept
     uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
     int32_t* plist_n;
     uint32_t* wbits;            // [n][ceil(units_max / 32)] units whose submin this launch wrote
@@ -1362,8 +1363,11 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     float4* tab0 = reinterpret_cast<float4*>(smem_raw + (size_t)W * Lmax * sizeof(Lev) + su.aux_bytes);
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
     constexpr int NWARP = P1_THREADS / 32;
-    float4* tab = tab0 + (size_t)warp * 32;                                                      // {X,Y,Z,Tp}
-    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * 32) + (size_t)warp * 32;         // {k_lo, k_hi}
+    // exhaustive without QoS: two table entries per lane (one read of an inner pair serves both)
+    constexpr bool TWO = !QOS && !BB;
+    constexpr int TABN = TWO ? 64 : 32;
+    float4* tab = tab0 + (size_t)warp * TABN;                                                    // {X,Y,Z,Tp}
+    int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * TABN) + (size_t)warp * TABN;     // {k_lo, k_hi}
     const float invf = P.inv;
     const double invd = 1.0 / (double)P.lamN;
     const int s0 = A.hdr[0], u0v = A.hdr[1];
@@ -1378,7 +1382,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // BB: warps take 32 list entries at a time (best-first), process the ones within the band of the
     // incumbent, and stop when the rest of the list is provably outside it.  Otherwise: 32
     // consecutive units per round, rounds strided by NWARP * 32.
-    unsigned long long nfeas = 0, ndone = 0, nue = 0, nent = 0;
+    unsigned long long nfeas = 0, ndone = 0, nue = 0, nent = 0, nuok = 0, nuch = 0, nch = 0;
     float bnd = INFINITY, incv = INFINITY, bnd_of = -1.0f;
     // band factor of the linear modes, rounded up once: bnd = m x bandf (rounded up) >= band_bound(m)
     const float bandf = __double2float_ru((1.0 + (double)su.tol_num / (double)su.tol_den) * (1.0 + su.delta) /
@@ -1552,6 +1556,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (!BB && wl == 0) subp[unit] = INFINITY;
             continue;
         }
+        nuok++;
         const struct { int T, Tm; } h = {cT, cTm};
         int nc = 0;
         bool had = false;
@@ -1608,73 +1613,51 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 }
             }
         };
+        // Without QoS bounds every entry's range is [0, L_inner): the lanes sweep in lockstep (broadcast reads of
+        // the inner pairs); lane l takes entries l and (exhaustive pass) l + 32, so one read of an inner pair feeds
+        // four candidates; entries past the table score +inf.
         auto sweep = [&]() {
             if (QOS) { sweep_qos(); return; }
-            const bool has = wl < nc;
-            float4 t4 = make_float4(INFINITY, 0.0f, 0.0f, 0.0f);
-            int2 kk = make_int2(0, 0);
-            if (has) { t4 = tab[wl]; kk = tabk[wl]; }
-            if (QOS && has && kk.x < 0) {   // masked sweep of [0, min(k_lo, k_hi)) (non-monotone u)
-                kk.x = -1 - kk.x;
-                const int kend = min(kk.x, kk.y);
-                for (int k = 0; k < kend; k++) {
-                    const float4 r = A.ip[k >> 1];
-                    const float2 uu2 = A.iu[k >> 1];
-                    const float bk = (k & 1) ? r.y : r.x, sk = (k & 1) ? r.w : r.z, uk = (k & 1) ? uu2.y : uu2.x;
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) { const float2 dd = A.iD[k >> 1]; b0 += (k & 1) ? dd.y : dd.x; }
-                    if (t4.w <= uk) { m0 = fminf(m0, fmaf(bk, t4.y, fmaf(sk, t4.z, b0))); nfeas++; }
-                }
+            const float4 ninf = make_float4(INFINITY, 0.0f, 0.0f, 0.0f);
+            const float4 ta = wl < nc ? tab[wl] : ninf;
+            const float4 tb = (TWO && wl + 32 < nc) ? tab[wl + 32] : ninf;
+            nfeas += (unsigned long long)((wl < nc) + (TWO && wl + 32 < nc)) * (unsigned long long)Lin;
+            if (Lin & 1) {  // trailing odd element
+                const float4 r = A.ip[Lin >> 1];
+                const float d = MODE == M_PAPER ? A.iD[Lin >> 1].x : 0.0f;
+                m1 = fminf(m1, fmaf(r.x, ta.y, fmaf(r.z, ta.z, ta.x + d)));
+                if (TWO) m1 = fminf(m1, fmaf(r.x, tb.y, fmaf(r.z, tb.z, tb.x + d)));
             }
-            const int ka = max(kk.x, 0), kb2 = kk.y;
-            const bool any = has && ka < kb2;
-            if (any) {
-                nfeas += (unsigned long long)(kb2 - ka);
-                if (ka & 1) {   // leading odd element
-                    const float4 r = A.ip[ka >> 1];
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) b0 += A.iD[ka >> 1].y;
-                    m0 = fminf(m0, fmaf(r.y, t4.y, fmaf(r.w, t4.z, b0)));
-                }
-                if (kb2 & 1) {  // trailing odd element
-                    const float4 r = A.ip[kb2 >> 1];
-                    float b0 = t4.x;
-                    if (MODE == M_PAPER) b0 += A.iD[kb2 >> 1].x;
-                    m1 = fminf(m1, fmaf(r.x, t4.y, fmaf(r.z, t4.z, b0)));
-                }
-            }
-            // this lane's pairs [pa, pb); the warp sweeps [pmin, pmax)
-            const int pa = any ? (ka + 1) >> 1 : 0, pb = any ? kb2 >> 1 : 0;
-            const unsigned plen = pb > pa ? (unsigned)(pb - pa) : 0u;
-            const int pmin = __reduce_min_sync(0xffffffffu, plen ? pa : INT_MAX);
-            const int pmax = __reduce_max_sync(0xffffffffu, plen ? pb : 0);
-            if (pmin >= pmax) return;
-            const u64 X2 = f2pack(t4.x, t4.x), Y2 = f2pack(t4.y, t4.y), Z2 = f2pack(t4.z, t4.z);
-            // four independent minima: the 3-input min of one pair does not wait on the previous one
+            const int np2 = Lin >> 1;
+            const u64 Xa = f2pack(ta.x, ta.x), Ya = f2pack(ta.y, ta.y), Za = f2pack(ta.z, ta.z);
+            const u64 Xb = f2pack(tb.x, tb.x), Yb = f2pack(tb.y, tb.y), Zb = f2pack(tb.z, tb.z);
+            // independent minima: the 3-input min of one pair does not wait on the previous one
             float ma = INFINITY, mb = INFINITY, mc = INFINITY, md = INFINITY;
-            auto pair = [&](int q) -> float {
-                const float4 r = A.ip[q];
+            auto key = [&](const float4& r, const float2& dd, u64 X2, u64 Y2, u64 Z2) -> float {
                 u64 base = X2;
-                if (MODE == M_PAPER) { const float2 dd = A.iD[q]; base = add2(X2, f2pack(dd.x, dd.y)); }
-                const u64 key = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+                if (MODE == M_PAPER) base = add2(X2, f2pack(dd.x, dd.y));
+                const u64 k2 = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
                 float k0, k1;
-                f2unpack(key, k0, k1);
+                f2unpack(k2, k0, k1);
                 return fminf(k0, k1);
             };
-            int p = pmin;
-            if (!QOS) {   // identical ranges: no per-lane test (lanes without an entry score +inf)
-                for (; p + 4 <= pmax; p += 4) {
-                    const float a0 = pair(p), a1 = pair(p + 1), a2 = pair(p + 2), a3 = pair(p + 3);
-                    ma = fminf(ma, a0); mb = fminf(mb, a1); mc = fminf(mc, a2); md = fminf(md, a3);
+            const float2 dz = make_float2(0.0f, 0.0f);
+            int p = 0;
+            for (; p + 2 <= np2; p += 2) {
+                const float4 r0 = A.ip[p], r1 = A.ip[p + 1];
+                const float2 d0 = MODE == M_PAPER ? A.iD[p] : dz, d1 = MODE == M_PAPER ? A.iD[p + 1] : dz;
+                ma = fminf(ma, key(r0, d0, Xa, Ya, Za));
+                mb = fminf(mb, key(r1, d1, Xa, Ya, Za));
+                if (TWO) {
+                    mc = fminf(mc, key(r0, d0, Xb, Yb, Zb));
+                    md = fminf(md, key(r1, d1, Xb, Yb, Zb));
                 }
-                for (; p < pmax; p++) ma = fminf(ma, pair(p));
-            } else {   // ranges differ by lane (measured: a lockstep sweep over their union with a per-lane
-                       // range test is slower, the union being much wider than a typical range)
-                for (p = pa; p + 4 <= pb; p += 4) {
-                    const float a0 = pair(p), a1 = pair(p + 1), a2 = pair(p + 2), a3 = pair(p + 3);
-                    ma = fminf(ma, a0); mb = fminf(mb, a1); mc = fminf(mc, a2); md = fminf(md, a3);
-                }
-                for (; p < pb; p++) ma = fminf(ma, pair(p));
+            }
+            for (; p < np2; p++) {
+                const float4 r0 = A.ip[p];
+                const float2 d0 = MODE == M_PAPER ? A.iD[p] : dz;
+                ma = fminf(ma, key(r0, d0, Xa, Ya, Za));
+                if (TWO) mc = fminf(mc, key(r0, d0, Xb, Yb, Zb));
             }
             m0 = fminf(m0, fminf(fminf(ma, mb), fminf(mc, md)));
         };
@@ -1732,7 +1715,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             }
             nc += __popc(bal);
             if (wl == 0) nent += __popc(bal);
-            if (nc) {
+            if (nc && (!TWO || nc > 32)) {   // (TWO: sweep once two passes filled the table)
                 had = true;
                 __syncwarp();
                 sweep();
@@ -1770,6 +1753,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     }
                 }
                 const unsigned cm = __ballot_sync(0xffffffffu, keep);
+                nch += __popc(cm);
+                nuch += cm != 0u;
                 if (keep) s_chunk[warp][__popc(cm & ((1u << wl) - 1u))] = (uint8_t)wl;   // surviving chunks, in order
                 __syncwarp();
                 const int nk = __popc(cm), q = wl / P1_CS, j = wl % P1_CS;
@@ -1783,6 +1768,13 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (!chunked)
             for (int kb = 0; kb < ne; kb += 32)
                 if (__all_sync(0xffffffffu, entry(kb + wl, kb + wl < ne))) break;   // the rest of the sorted segment is unusable
+        if (TWO && nc) {   // the last, partly filled table
+            had = true;
+            __syncwarp();
+            sweep();
+            __syncwarp();
+            nc = 0;
+        }
         __syncwarp();
         if (BB && wl == 0 && had) nue++;
         float m = fminf(m0, m1);
@@ -1817,6 +1809,9 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         atomicAdd(bb.rows_done, ndone);
         atomicAdd(bb.rows_done + 1, nue);
         atomicAdd(bb.rows_done + 2, nent);
+        atomicAdd(bb.rows_done + 3, nuok);
+        atomicAdd(bb.rows_done + 4, nuch);
+        atomicAdd(bb.rows_done + 5, nch);
     }
 }
 
@@ -2772,15 +2767,18 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
         }
         __syncthreads();
         const int n = goff[W];
-        for (int w = threadIdx.x; w < W; w += blockDim.x) {   // one thread per worker: its run, in order
+        for (int w = 0; w < W; w++) {   // every group's duration and pool size, in parallel
             const int t = P.table[w], G = tb.G[t];
             const uint8_t* wt = tb.wit[t] + (size_t)lv[w] * G;
-            double e = 0.0;
-            for (int g = 0; g < G; g++) {
-                e += (double)tb.beta[t][g * C + wt[g]] * (1.0 + alpha_w[w]);
-                ends[goff[w] + g] = e;
+            for (int g = threadIdx.x; g < G; g += blockDim.x) {
+                ends[goff[w] + g] = (double)tb.beta[t][g * C + wt[g]] * (1.0 + alpha_w[w]);
                 csz[goff[w] + g] = sizes[wt[g]];
             }
+        }
+        __syncthreads();
+        for (int w = threadIdx.x; w < W; w += blockDim.x) {   // one thread per worker: its run, in order
+            double e = 0.0;
+            for (int i = goff[w]; i < goff[w + 1]; i++) { e += ends[i]; ends[i] = e; }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += blockDim.x) {   // rank of end i (ties by position)

@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     __syncthreads();
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
+    // work item order that spreads a small set of items over every SM (consecutive items on different CTAs):
+    // the DP cells and the level reconstructions are latency-bound chains, so fewer per SM is faster
+    const int sid = threadIdx.x * gridDim.x + blockIdx.x;
 
     K1_STAMP(0)
     // ---- DP layers G-1 .. 0 (one cell = (table, r, s); all C sizes per cell) ----
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         }
         __syncthreads();
         const int total = off[n_jobs];
-        for (int i = gtid; i < total; i += gstride) {
+        for (int i = sid; i < total; i += gstride) {
             int t = 0;
             while (off[t + 1] <= i) t++;
             const LevelJob& J = sj[t];
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     const int nlev = off[n_jobs];
 
     // ---- greedy reconstruction of every level's canonical witness (packed words) ----
-    for (int i = gtid; i < nlev; i += gstride) {
+    for (int i = sid; i < nlev; i += gstride) {
         int t = 0;
         while (off[t + 1] <= i) t++;
         const LevelJob& J = sj[t];

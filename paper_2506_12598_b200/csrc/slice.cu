@@ -13,6 +13,7 @@ namespace eclip {
 
 static constexpr uint64_t UINF = ~0ull;
 static constexpr int SL_THREADS = 256;
+static constexpr int SLX = 1024;   // exact DP / walk: one CTA per band slice, a wide block (few band slices, each latency-bound)
 
 SliceState::~SliceState() { release(); }
 void SliceState::release() {
@@ -315,12 +316,12 @@ __device__ U256 slice_key(const SliceDev& S, const Prob& P, int64_t Tp, uint64_t
 }
 
 // pass 2a: exact J for every band slice
-__global__ void __launch_bounds__(SL_THREADS) k_slice_exact(SliceDev S, const Prob* probs, const Lev* levs,
+__global__ void __launch_bounds__(SLX) k_slice_exact(SliceDev S, const Prob* probs, const Lev* levs,
                                                             const int16_t* dense, const int32_t* band,
                                                             const int32_t* nband, uint64_t* scratch, U256* Jex) {
     const Prob& P = probs[0];
     __shared__ int64_t dlo[MAXW + 1], dhi[MAXW + 1];
-    __shared__ uint64_t red[SL_THREADS];
+    __shared__ uint64_t red[SLX];
     uint64_t* scr = scratch + (size_t)blockIdx.x * (S.gtot + (size_t)(S.W) * S.maxrange);
     for (int bi = blockIdx.x; bi < *nband; bi += gridDim.x) {
         int64_t T = S.Tlo + band[bi];
@@ -373,7 +374,7 @@ __global__ void k_slice_hstar(const int32_t* band, const int32_t* nband, const U
 // The walk is block-parallel: for worker w = 0..W-1 every level l (rank order) is tested at
 // once -- "does some completion of (prefix, l) inside this slice reach key <= H*(1+tau)?",
 // exact by the DP tables -- and the smallest qualifying rank is kept.
-__global__ void __launch_bounds__(SL_THREADS) k_slice_walk(SliceDev S, const Prob* probs, const Lev* levs,
+__global__ void __launch_bounds__(SLX) k_slice_walk(SliceDev S, const Prob* probs, const Lev* levs,
                                                            const int16_t* dense, const int32_t* band,
                                                            const int32_t* nband, uint64_t* scratch, const U256* Jex,
                                                            const U256* hstar, U256* wtup) {
@@ -563,7 +564,7 @@ cudaError_t slice_pass2_min(SliceState& s, const Setup& su, const Tables& tb, Wo
     (void)su; (void)tb;
     const SliceDev& S = s.h;
     k_slice_band<<<1, 1024, 0, st>>>(S, s.J32, wk.m32, s.band, s.nband);
-    k_slice_exact<<<s.slots, SL_THREADS, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex);
+    k_slice_exact<<<s.slots, SLX, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex);
     k_slice_hstar<<<1, 32, 0, st>>>(s.band, s.nband, s.Jex, wk.hstar);
     return cudaGetLastError();
 }
@@ -571,7 +572,7 @@ cudaError_t slice_pass2_min(SliceState& s, const Setup& su, const Tables& tb, Wo
 cudaError_t slice_pass2_first(SliceState& s, const Setup& su, const Tables& tb, Work& wk, cudaStream_t st) {
     (void)su; (void)tb;
     const SliceDev& S = s.h;
-    k_slice_walk<<<s.slots, SL_THREADS, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex,
+    k_slice_walk<<<s.slots, SLX, 0, st>>>(S, wk.probs, wk.levs, s.dense, s.band, s.nband, s.scratch, s.Jex,
                                                  wk.hstar, s.wtup);
     k_slice_first<<<1, 32, 0, st>>>(s.nband, s.wtup, wk.first);
     return cudaGetLastError();

@@ -576,10 +576,11 @@ class Planner:
         return {k: float(ms[i]) for i, k in enumerate(PHASES)}
 
     def counters(self) -> dict:
-        v = (C.c_uint64 * 5)()
-        _check(lib().eclip_planner_counters(self._h, v, 5))
+        v = (C.c_uint64 * 8)()
+        _check(lib().eclip_planner_counters(self._h, v, 8))
         return {"evaluated_candidates": int(v[0]), "units_processed": int(v[1]), "kernel_ms": int(v[2]) * 1e-6,
-                "units_with_swept_entries": int(v[3]), "entries_swept": int(v[4])}
+                "units_with_swept_entries": int(v[3]), "entries_swept": int(v[4]), "units_past_unit_bound": int(v[5]),
+                "units_with_kept_chunks": int(v[6]), "chunks_kept": int(v[7])}
 
     def close(self):
         if self._h is not None and self._h.value:

@@ -37,7 +37,7 @@ for name, q, prune in (("pruned", True, True), ("exh_qos", True, False), ("exh_n
             ks.append(c["kernel_ms"]); ev.append(c["evaluated_candidates"]); st.append(sum(pl.phase_ms().values()))
     k = float(np.median(ks)); e = int(np.median(ev))
     res[name] = {"kernel_ms": k, "step_ms": float(np.median(st)), "evaluated": e,
-                 "fma_frac": 2 * e / (k * 1e-3) / peak}
+                 "fma_frac": 2 * e / (k * 1e-3) / peak, "counters": c, "phases": pl.phase_ms()}
     del pl
 for name, p in (("C2", synth.make_c2()), ("C3", synth.make_c3("matrix")), ("C4", synth.make_c4()), ("S6", synth.make_s6())):
     prp = ec.Profiles.from_models(p.models)
