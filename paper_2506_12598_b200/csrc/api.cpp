@@ -675,8 +675,7 @@ static int plan_geometry(eclip_session* s, const eclip_options* opt) {
     if (fast) {   // per-problem aux block (staged with the Lev records) + per-warp prefix tables
         su.aux_bytes = (int32_t)pass1_aux_bytes(Lmax);
         // 32 entries per warp; 64 in the exhaustive pass without QoS (two per lane, k_pass1_fast TWO)
-        const bool two = !su.has_qos && !pass1_prunable(su);
-        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * (two ? 64 : 32) * 24);
+        su.table_bytes = (int32_t)((size_t)(P1_THREADS / 32) * 32 * 24);   // 32 entries per warp
     }
     su.lev_stride = W * Lmax + su.aux_bytes / (int)sizeof(Lev);
     return ECLIP_OK;

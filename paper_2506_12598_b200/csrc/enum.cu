@@ -1312,7 +1312,13 @@ template <int NW, int MODE, bool QOS, bool BB>
 #ifndef P1_MINB
 #define P1_MINB 4
 #endif
-__global__ void __launch_bounds__(P1_THREADS, P1_MINB)
+#ifndef P1_NE
+#define P1_NE 4   // entries per lane in the exhaustive pass without QoS
+#endif
+#ifndef P1_MINB_EXH
+#define P1_MINB_EXH 3   // that pass: registers for independent temporaries of its 4 entries (ILP) over a 4th CTA
+#endif
+__global__ void __launch_bounds__(P1_THREADS, (!QOS && !BB && NW >= 2) ? P1_MINB_EXH : P1_MINB)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
              unsigned long long* __restrict__ feasible, BBArgs bb) {
     constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)
@@ -1364,8 +1370,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
     constexpr int NWARP = P1_THREADS / 32;
     // exhaustive without QoS: two table entries per lane (one read of an inner pair serves both)
-    constexpr bool TWO = !QOS && !BB;
-    constexpr int TABN = TWO ? 64 : 32;
+    constexpr bool TWO = !QOS && !BB && NW >= 2;   // (W = 1: no step worker; the table path)
+    constexpr int TABN = 32;   // (TWO keeps its entries in registers)
     float4* tab = tab0 + (size_t)warp * TABN;                                                    // {X,Y,Z,Tp}
     int2* tabk = reinterpret_cast<int2*>(tab0 + (size_t)NWARP * TABN) + (size_t)warp * TABN;     // {k_lo, k_hi}
     const float invf = P.inv;
@@ -1382,7 +1388,8 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // BB: warps take 32 list entries at a time (best-first), process the ones within the band of the
     // incumbent, and stop when the rest of the list is provably outside it.  Otherwise: 32
     // consecutive units per round, rounds strided by NWARP * 32.
-    unsigned long long nfeas = 0, ndone = 0, nue = 0, nent = 0, nuok = 0, nuch = 0, nch = 0;
+    unsigned long long nfeas = 0;
+    unsigned ndone = 0, nue = 0, nent = 0, nuok = 0, nuch = 0, nch = 0;   // per-lane counts (32-bit: registers)
     float bnd = INFINITY, incv = INFINITY, bnd_of = -1.0f;
     // band factor of the linear modes, rounded up once: bnd = m x bandf (rounded up) >= band_bound(m)
     const float bandf = __double2float_ru((1.0 + (double)su.tol_num / (double)su.tol_den) * (1.0 + su.delta) /
@@ -1390,8 +1397,27 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     // unit constants (row decode, exact QoS range cut on the step worker, row constants X_h, Y_h, Z_h),
     // computed by one lane per unit right after a fetch and broadcast to the warp when the unit is
     // processed; false: no step level of the unit is usable (its minimum stays +inf)
+    // chunk bound of aligned chunk c of the S'-sorted step levels: for a chunk with smallest
+    // S' = Sa and smallest B = Bm, every key of its entries is
+    //   >= (Xh + Bm Yh + Sa Zh) + (Yh + Sa/LN) minB_k + (Zh + Bm/LN) minS_k
+    // over the inner range that is QoS-feasible at T' = hT + Sa (a superset of every entry's); true: keep
+    auto chunk_keep = [&](int c, int hT, int hTm, float Xh, float Yh, float Zh) -> bool {
+        const int Sa = A.stS[c * P1_CS];
+        const float Bm = A.chB[c];
+        const int Tp = hT + Sa;
+        const int khi2 = inner_khi(A, hTm - Tp, s0, slast, khi_ok, Lin);
+        const int klo2 = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
+        const int ka = A.umaxp[klo2] >= Tp ? 0 : klo2;
+        if (khi2 <= ka) return false;
+        const float Sf = (float)Sa;
+        const float Xc = fmaf(Bm, Yh, fmaf(Sf, Zh, Xh));
+        const float Yc = fmaf(Sf, invf, Yh), Zc = fmaf(Bm, invf, Zh);
+        float lbc = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
+        if (!(lbc * 0.99998474121f > bnd)) lbc = fmaxf(lbc, Xc + hull_min_pos(A, nhv, Yc, Zc, ka, khi2 - 1));
+        return !(lbc * 0.99998474121f > bnd);   // 1 - 2^-16
+    };
     auto unit_consts = [&](uint64_t unit, int& oT, int& oTm, int& oSb, int& oEa, int& oNe, float& oX, float& oY,
-                           float& oZ) -> bool {
+                           float& oZ, uint32_t& oCm, bool& oCh) -> bool {
             int seg;
             HiSums h;
             h.B = 0; h.BS = 0; h.T = 0; h.Tm = 1 << 24;
@@ -1478,6 +1504,17 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             float lbu = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
             if (!(lbu * 0.99998474121f > bnd)) lbu = fmaxf(lbu, Xc + hull_min_pos(A, nhv, Yc, Zc, ka, khi2 - 1));
             if (lbu * 0.99998474121f > bnd) return false;
+            // the chunk filter, by this lane for its own unit (at fetch time: units whose every chunk is out of the
+            // band never reach the warp-wide processing below)
+            const int c_lo = ea / P1_CS, c_hi = (ea + ne + P1_CS - 1) / P1_CS;
+            if (c_hi - c_lo <= 32) {
+                uint32_t m = 0;
+                for (int c = c_lo; c < c_hi; c++)
+                    if (chunk_keep(c, h.T, h.Tm, Xh, Yh, Zh)) m |= 1u << (c - c_lo);
+                if (!m) return false;
+                oCm = m;
+                oCh = true;
+            }
         }
         return true;
     };
@@ -1524,10 +1561,11 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         }
         int uT = 0, uTm = 0, uSb = 0, uEa = 0, uNe = 0;
         float uX = 0.0f, uY = 0.0f, uZ = 0.0f;
-        bool uok = false;
+        uint32_t uCm = 0;
+        bool uok = false, uCh = false;
         if ((pend >> wl) & 1u) {   // this lane's own unit
             const uint64_t myunit = BB ? ua + (uint64_t)loff : base + (uint64_t)wl;
-            uok = unit_consts(myunit, uT, uTm, uSb, uEa, uNe, uX, uY, uZ);
+            uok = unit_consts(myunit, uT, uTm, uSb, uEa, uNe, uX, uY, uZ, uCm, uCh);
         }
       while (pend) {
         const int jl = __ffs(pend) - 1;
@@ -1557,6 +1595,62 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             continue;
         }
         nuok++;
+        if (TWO) {
+            // exhaustive pass without QoS: every step level of the unit is an entry and every inner level is in
+            // range, so lane wl builds its entries ea + kb + wl + 32 i (i < P1_NE) in registers and sweeps all inner
+            // pairs with them: one broadcast read of a pair feeds 2 P1_NE candidates (no table round trip)
+            float acc[2 * P1_NE];
+#pragma unroll
+            for (int i = 0; i < 2 * P1_NE; i++) acc[i] = INFINITY;
+            const int np2 = Lin >> 1;
+            for (int kb = 0; kb < ne; kb += 32 * P1_NE) {
+                u64 X2[P1_NE], Y2[P1_NE], Z2[P1_NE];
+                float Xs[P1_NE], Ys[P1_NE], Zs[P1_NE];
+                int nv = 0;
+#pragma unroll
+                for (int i = 0; i < P1_NE; i++) {
+                    const int k = kb + wl + 32 * i;
+                    float X = INFINITY, Y = 0.0f, Z = 0.0f;
+                    if (k < ne) {
+                        const Lev& r = stepw[A.sperm[ea + k]];
+                        const float Be = __ll2float_rn(r.B), Sf = (float)r.S;
+                        X = fmaf(Be, Yh, fmaf(Sf, Zh, Xh));
+                        if (MODE == M_PAPER) X += (float)((double)r.BS * invd);
+                        Y = fmaf(Sf, invf, Yh);
+                        Z = fmaf(Be, invf, Zh);
+                        nv++;
+                    }
+                    Xs[i] = X; Ys[i] = Y; Zs[i] = Z;
+                    X2[i] = f2pack(X, X); Y2[i] = f2pack(Y, Y); Z2[i] = f2pack(Z, Z);
+                }
+                nfeas += (unsigned long long)nv * (unsigned long long)Lin;
+                for (int p = 0; p < np2; p++) {
+                    const float4 r = A.ip[p];
+                    const u64 Bp = f2pack(r.x, r.y), Sp = f2pack(r.z, r.w);
+                    u64 dd = 0;
+                    if (MODE == M_PAPER) { const float2 d = A.iD[p]; dd = f2pack(d.x, d.y); }
+#pragma unroll
+                    for (int i = 0; i < P1_NE; i++) {
+                        const u64 base = MODE == M_PAPER ? add2(X2[i], dd) : X2[i];
+                        float k0, k1;
+                        f2unpack(fma2(Bp, Y2[i], fma2(Sp, Z2[i], base)), k0, k1);
+                        acc[2 * i + (p & 1)] = fminf(acc[2 * i + (p & 1)], fminf(k0, k1));
+                    }
+                }
+                if (Lin & 1) {  // trailing odd element
+                    const float4 r = A.ip[Lin >> 1];
+                    const float d = MODE == M_PAPER ? A.iD[Lin >> 1].x : 0.0f;
+#pragma unroll
+                    for (int i = 0; i < P1_NE; i++) acc[2 * i] = fminf(acc[2 * i], fmaf(r.x, Ys[i], fmaf(r.z, Zs[i], Xs[i] + d)));
+                }
+            }
+            float m = acc[0];
+#pragma unroll
+            for (int i = 1; i < 2 * P1_NE; i++) m = fminf(m, acc[i]);
+            for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (wl == 0) subp[unit] = m;
+            continue;
+        }
         const struct { int T, Tm; } h = {cT, cTm};
         int nc = 0;
         bool had = false;
@@ -1614,52 +1708,36 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             }
         };
         // Without QoS bounds every entry's range is [0, L_inner): the lanes sweep in lockstep (broadcast reads of
-        // the inner pairs); lane l takes entries l and (exhaustive pass) l + 32, so one read of an inner pair feeds
-        // four candidates; entries past the table score +inf.
+        // the inner pairs; lanes without an entry score +inf).  (The exhaustive pass keeps its entries in
+        // registers instead, TWO above.)
         auto sweep = [&]() {
             if (QOS) { sweep_qos(); return; }
-            const float4 ninf = make_float4(INFINITY, 0.0f, 0.0f, 0.0f);
-            const float4 ta = wl < nc ? tab[wl] : ninf;
-            const float4 tb = (TWO && wl + 32 < nc) ? tab[wl + 32] : ninf;
-            nfeas += (unsigned long long)((wl < nc) + (TWO && wl + 32 < nc)) * (unsigned long long)Lin;
+            const float4 ta = wl < nc ? tab[wl] : make_float4(INFINITY, 0.0f, 0.0f, 0.0f);
+            nfeas += (unsigned long long)(wl < nc) * (unsigned long long)Lin;
             if (Lin & 1) {  // trailing odd element
                 const float4 r = A.ip[Lin >> 1];
                 const float d = MODE == M_PAPER ? A.iD[Lin >> 1].x : 0.0f;
                 m1 = fminf(m1, fmaf(r.x, ta.y, fmaf(r.z, ta.z, ta.x + d)));
-                if (TWO) m1 = fminf(m1, fmaf(r.x, tb.y, fmaf(r.z, tb.z, tb.x + d)));
             }
             const int np2 = Lin >> 1;
             const u64 Xa = f2pack(ta.x, ta.x), Ya = f2pack(ta.y, ta.y), Za = f2pack(ta.z, ta.z);
-            const u64 Xb = f2pack(tb.x, tb.x), Yb = f2pack(tb.y, tb.y), Zb = f2pack(tb.z, tb.z);
-            // independent minima: the 3-input min of one pair does not wait on the previous one
-            float ma = INFINITY, mb = INFINITY, mc = INFINITY, md = INFINITY;
-            auto key = [&](const float4& r, const float2& dd, u64 X2, u64 Y2, u64 Z2) -> float {
-                u64 base = X2;
-                if (MODE == M_PAPER) base = add2(X2, f2pack(dd.x, dd.y));
-                const u64 k2 = fma2(f2pack(r.x, r.y), Y2, fma2(f2pack(r.z, r.w), Z2, base));
+            float ma = INFINITY, mb = INFINITY;   // two independent minima
+            auto key = [&](int q) -> float {
+                const float4 r = A.ip[q];
+                u64 base = Xa;
+                if (MODE == M_PAPER) { const float2 dd = A.iD[q]; base = add2(Xa, f2pack(dd.x, dd.y)); }
+                const u64 k2 = fma2(f2pack(r.x, r.y), Ya, fma2(f2pack(r.z, r.w), Za, base));
                 float k0, k1;
                 f2unpack(k2, k0, k1);
                 return fminf(k0, k1);
             };
-            const float2 dz = make_float2(0.0f, 0.0f);
             int p = 0;
             for (; p + 2 <= np2; p += 2) {
-                const float4 r0 = A.ip[p], r1 = A.ip[p + 1];
-                const float2 d0 = MODE == M_PAPER ? A.iD[p] : dz, d1 = MODE == M_PAPER ? A.iD[p + 1] : dz;
-                ma = fminf(ma, key(r0, d0, Xa, Ya, Za));
-                mb = fminf(mb, key(r1, d1, Xa, Ya, Za));
-                if (TWO) {
-                    mc = fminf(mc, key(r0, d0, Xb, Yb, Zb));
-                    md = fminf(md, key(r1, d1, Xb, Yb, Zb));
-                }
+                ma = fminf(ma, key(p));
+                mb = fminf(mb, key(p + 1));
             }
-            for (; p < np2; p++) {
-                const float4 r0 = A.ip[p];
-                const float2 d0 = MODE == M_PAPER ? A.iD[p] : dz;
-                ma = fminf(ma, key(r0, d0, Xa, Ya, Za));
-                if (TWO) mc = fminf(mc, key(r0, d0, Xb, Yb, Zb));
-            }
-            m0 = fminf(m0, fminf(fminf(ma, mb), fminf(mc, md)));
+            if (p < np2) ma = fminf(ma, key(p));
+            m0 = fminf(m0, fminf(ma, mb));
         };
         // one step entry per lane (relative index k in [ea, ea + ne)); appends the usable ones to
         // the warp's table; returns whether the lane's level lies past the QoS prefix
@@ -1715,7 +1793,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             }
             nc += __popc(bal);
             if (wl == 0) nent += __popc(bal);
-            if (nc && (!TWO || nc > 32)) {   // (TWO: sweep once two passes filled the table)
+            if (nc) {
                 had = true;
                 __syncwarp();
                 sweep();
@@ -1725,33 +1803,15 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             return past;
         };
         bool chunked = false;
-        if (BB && QOS && step_tab) {
-            // chunk filter: the S'-sorted step levels in aligned chunks of P1_CS; for a
-            // chunk with smallest S' = Sa and smallest B = Bm, every key of its entries is
-            //   >= (Xh + Bm Yh + Sa Zh) + (Yh + Sa/LN) minB_k + (Zh + Bm/LN) minS_k
-            // over the inner range that is QoS-feasible at T' = hT + Sa (a superset of every entry's)
-            const int c_lo = ea / P1_CS, c_hi = (ea + ne + P1_CS - 1) / P1_CS;
-            if (c_hi - c_lo <= 32) {
+        if (BB && QOS && step_tab && __shfl_sync(0xffffffffu, (int)uCh, jl)) {
+            // the chunk filter: the unit's lane evaluated every chunk at fetch time (chunk_keep; a unit with no chunk
+            // in the band never gets here); lane wl re-checks chunk c_lo + wl if it was kept
+            {
+                const int c_lo = ea / P1_CS;
                 chunked = true;
-                const int c = c_lo + wl;
-                bool keep = false;
-                if (c < c_hi) {
-                    const int Sa = A.stS[c * P1_CS];
-                    const float Bm = A.chB[c];
-                    const int Tp = h.T + Sa;
-                    const int khi2 = inner_khi(A, h.Tm - Tp, s0, slast, khi_ok, Lin);
-                    const int klo2 = inner_klo(A, Tp, u0v, ulast, klo_ok, Lin);
-                    const int ka = A.umaxp[klo2] >= Tp ? 0 : klo2;
-                    if (khi2 > ka) {
-                        const float Sf = (float)Sa;
-                        const float Xc = fmaf(Bm, Yh, fmaf(Sf, Zh, Xh));
-                        const float Yc = fmaf(Sf, invf, Yh), Zc = fmaf(Bm, invf, Zh);
-                        float lbc = fmaf(Yc, A.preminB[khi2], fmaf(Zc, (float)A.ssort[ka], Xc));
-                        if (!(lbc * 0.99998474121f > bnd))
-                            lbc = fmaxf(lbc, Xc + hull_min_pos(A, nhv, Yc, Zc, ka, khi2 - 1));
-                        keep = !(lbc * 0.99998474121f > bnd);   // 1 - 2^-16
-                    }
-                }
+                const unsigned cm0 = __shfl_sync(0xffffffffu, uCm, jl);
+                // re-checked against the band as it is now (tighter than at fetch time)
+                const bool keep = ((cm0 >> wl) & 1u) && chunk_keep(c_lo + wl, h.T, h.Tm, Xh, Yh, Zh);
                 const unsigned cm = __ballot_sync(0xffffffffu, keep);
                 nch += __popc(cm);
                 nuch += cm != 0u;
@@ -1768,13 +1828,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if (!chunked)
             for (int kb = 0; kb < ne; kb += 32)
                 if (__all_sync(0xffffffffu, entry(kb + wl, kb + wl < ne))) break;   // the rest of the sorted segment is unusable
-        if (TWO && nc) {   // the last, partly filled table
-            had = true;
-            __syncwarp();
-            sweep();
-            __syncwarp();
-            nc = 0;
-        }
         __syncwarp();
         if (BB && wl == 0 && had) nue++;
         float m = fminf(m0, m1);
@@ -1806,12 +1859,12 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
     for (int o = 16; o; o >>= 1) nfeas += __shfl_xor_sync(0xffffffffu, nfeas, o);
     if (wl == 0 && nfeas) atomicAdd(feasible, nfeas);
     if (BB && wl == 0 && ndone) {
-        atomicAdd(bb.rows_done, ndone);
-        atomicAdd(bb.rows_done + 1, nue);
-        atomicAdd(bb.rows_done + 2, nent);
-        atomicAdd(bb.rows_done + 3, nuok);
-        atomicAdd(bb.rows_done + 4, nuch);
-        atomicAdd(bb.rows_done + 5, nch);
+        atomicAdd(bb.rows_done, (unsigned long long)ndone);
+        atomicAdd(bb.rows_done + 1, (unsigned long long)nue);
+        atomicAdd(bb.rows_done + 2, (unsigned long long)nent);
+        atomicAdd(bb.rows_done + 3, (unsigned long long)nuok);
+        atomicAdd(bb.rows_done + 4, (unsigned long long)nuch);
+        atomicAdd(bb.rows_done + 5, (unsigned long long)nch);
     }
 }
 

@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     __syncthreads();
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
-    // work item order that spreads a small set of items over every SM (consecutive items on different CTAs):
-    // the DP cells and the level reconstructions are latency-bound chains, so fewer per SM is faster
+    // level reconstructions: an order that spreads them over every SM (consecutive levels on different CTAs);
+    // each is a latency-bound chain of dependent loads, so fewer per SM is faster
     const int sid = threadIdx.x * gridDim.x + blockIdx.x;
 
     K1_STAMP(0)
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
         }
         __syncthreads();
         const int total = off[n_jobs];
-        for (int i = sid; i < total; i += gstride) {
+        for (int i = gtid; i < total; i += gstride) {   // consecutive cells on consecutive threads (coalesced)
             int t = 0;
             while (off[t + 1] <= i) t++;
             const LevelJob& J = sj[t];
