@@ -2382,8 +2382,11 @@ constexpr int P2_CAP = 256;
 #endif
 constexpr int P2_THREADS = P2_THREADS_N;
 constexpr int P2_ELIST = 1024;   // step levels per unit the pass-2 entry filter handles
+#ifndef P2_MINB
+#define P2_MINB 6   // 80 registers: 6 CTAs per SM (the band scans are latency-bound; measured 125 -> 109 us on C5)
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(P2_THREADS) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
+__global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* probs, const Lev* __restrict__ levs,
                                                const float* __restrict__ submin, const float* m32,
                                                const float* m32_sure, U256* hstar, U256* first,
                                                const int32_t* bandn, const uint64_t* bandlist,
@@ -2892,7 +2895,7 @@ cudaError_t launch_table_hull(const Setup& su, const Tables& tb, Work& wk, cudaS
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
                         cudaStream_t st, bool table_hull) {
     (void)C; (void)sizes;
-    k_prep_prob<<<(su.n_problems + 127) / 128, 128, 0, st>>>(su, tb, in, wk.probs);
+    k_prep_prob<<<(su.n_problems + 31) / 32, 32, 0, st>>>(su, tb, in, wk.probs);   // one warp per block: all SMs
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
     if (su.aux_bytes > 0) {
