@@ -237,6 +237,17 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
             const int k = i - off[t];
             dp_cell<CM, VT>(J, step, k);
         }
+        // the next layer's profile rows (need, beta) into this SM's L1 while the grid barrier completes:
+        // the first loads of every cell of the next layer then hit L1
+        if (threadIdx.x < n_jobs) {
+            const LevelJob& J = sj[threadIdx.x];
+            const int gn = J.G - 2 - step;
+            if (gn >= 0) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(J.need + gn * J.C));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(J.beta + gn * J.C));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(J.beta + gn * J.C + 8));
+            }
+        }
         grid.sync();
     }
 

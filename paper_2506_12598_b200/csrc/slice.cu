@@ -81,26 +81,32 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
     const int PAD = S.pad;
     const int BUF = S.maxrange + 2 * PAD + RB;          // entries [-PAD, maxrange + PAD + RB)
     const int BUFS = BUF;
-    float* g = sm;                                      // [gtot]
-    float* Da = g + S.gtot;
+    int gspan = 1;
+    for (int w = 0; w < W; w++) gspan = max(gspan, S.smax[w] - S.smin[w] + 1);
+    // g_w(level; T') of one worker at a time (the stage that uses it): a small buffer keeps the block's shared
+    // memory low enough for more CTAs per SM, whose warps fill the issue slots while a stage's barrier waits
+    float* g = sm;                                      // [gspan]
+    float* Da = g + gspan;
     float* Db = Da + BUFS;
     const int64_t Tp = T * S.gS;
     const float Tpf = (float)Tp;
-    for (int i = threadIdx.x; i < S.gtot; i += blockDim.x) {
-        int w = 0;
-        while (w + 1 < W && S.doff[w + 1] <= i) w++;
-        int l = dense[i];
-        float v = INFINITY;
-        if (l >= 0) {
-            const Lev& r = levs[w * S.Lmax + l];
-            if (Tp <= (int64_t)r.Tmax) {
-                float O = (float)overlap_exact(S.mode, Tp, r.S, P.lamN);
-                v = fmaf(O, r.Bk, __ll2float_rn(r.B)) * P.wf[w];   // omega_w L_w (weights: DESIGN.md R20)
+    auto fill_g = [&](int w) {
+        const int span = S.smax[w] - S.smin[w] + 1;
+        for (int i = threadIdx.x; i < span; i += blockDim.x) {
+            const int l = dense[S.doff[w] + i];
+            float v = INFINITY;
+            if (l >= 0) {
+                const Lev& r = levs[w * S.Lmax + l];
+                if (Tp <= (int64_t)r.Tmax) {
+                    float O = (float)overlap_exact(S.mode, Tp, r.S, P.lamN);
+                    v = fmaf(O, r.Bk, __ll2float_rn(r.B)) * P.wf[w];   // omega_w L_w (weights: DESIGN.md R20)
+                }
             }
+            g[i] = v;
         }
-        g[i] = v;
-    }
+    };
     for (int i = threadIdx.x; i < 2 * BUFS; i += blockDim.x) Da[i] = INFINITY;
+    fill_g(W - 1);
     __syncthreads();
     float* Dn = Da;   // D_{w+1}
     float* Dc = Db;   // D_w
@@ -108,13 +114,15 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
     int64_t nlo = 0, nhi = -1;
     if (W >= 2) {
         drange(S, T, W - 1, &nlo, &nhi);
-        const float* gw = g + S.doff[W - 1];
+        const float* gw = g;
         for (int64_t p = nlo + threadIdx.x; p <= nhi; p += blockDim.x) at(Dn, (int)(p - nlo)) = gw[p - S.smin[W - 1]];
         __syncthreads();
         for (int w = W - 2; w >= 1; w--) {
             int64_t lo, hi;
             drange(S, T, w, &lo, &hi);
-            const float* gw2 = g + S.doff[w];
+            fill_g(w);
+            __syncthreads();
+            const float* gw2 = g;
             const int nk = S.smax[w] - S.smin[w] + 1;
             const int np = (int)(hi - lo + 1);
             const int nprev = (int)(nhi - nlo + 1);
@@ -186,6 +194,10 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
         }
     }
     // J = min_k g_0[k] (+) D_1[T - smin_0 - k]
+    if (W >= 2) {   // (W = 1: g holds worker 0 already)
+        fill_g(0);
+        __syncthreads();
+    }
     float J = INFINITY;
     const int nk0 = S.smax[0] - S.smin[0] + 1;
     for (int k = threadIdx.x; k < nk0; k += blockDim.x) {
@@ -545,7 +557,9 @@ cudaError_t slice_pass1(SliceState& s, const Setup& su, const Tables& tb, Work& 
     const SliceDev& S = s.h;
     int64_t mine = S.n_slices > S.shard ? (S.n_slices - S.shard + S.n_shards - 1) / S.n_shards : 0;
     const size_t BUF = (size_t)S.maxrange + 2 * (size_t)S.pad + RB;
-    size_t smem = sizeof(float) * ((size_t)S.gtot + 2 * BUF);
+    size_t gspan = 1;
+    for (int w = 0; w < S.W; w++) gspan = std::max<size_t>(gspan, (size_t)(S.smax[w] - S.smin[w] + 1));
+    size_t smem = sizeof(float) * (gspan + 2 * BUF);   // one worker's g at a time (k_slice_f32)
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     const void* f = S.obj == O_SUM ? (const void*)k_slice_f32<O_SUM> : (S.obj == O_MAX ? (const void*)k_slice_f32<O_MAX>
                                                                                        : (const void*)k_slice_f32<O_ENERGY>);
