@@ -11,6 +11,8 @@
 #include <fstream>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <atomic>
 #include <sstream>
 #include <string>
 #include <tuple>
@@ -402,19 +404,25 @@ static int setup_device(eclip_session* s, const eclip_options* opt) {
         s->comm = (eclip_comm*)opt->comm;
         s->device = comm_device(s->comm);
     }
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0)
+    // device count and the pool setting are queried once per process (per device)
+    static int ndev = -1;
+    static cudaError_t ndev_err = cudaSuccess;
+    static std::once_flag once;
+    std::call_once(once, [] { ndev_err = cudaGetDeviceCount(&ndev); });
+    if (ndev_err != cudaSuccess || ndev <= 0)
         return fail(ECLIP_E_CUDA, "no CUDA device available (%s); the planner has no CPU fallback",
-                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+                    ndev_err == cudaSuccess ? "0 devices" : cudaGetErrorString(ndev_err));
     if (s->device < 0 || s->device >= ndev) return fail(ECLIP_E_INVALID_ARG, "device %d out of range", s->device);
     CU(cudaSetDevice(s->device));
-    {   // keep freed workspace in the device's stream-ordered pool between calls (no re-mapping)
+    static std::atomic<uint64_t> pool_set{0};   // bit d: device d's pool configured
+    if (s->device < 64 && !((pool_set.load() >> s->device) & 1ull)) {
+        // keep freed workspace in the device's stream-ordered pool between calls (no re-mapping)
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, s->device) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
+        pool_set.fetch_or(1ull << s->device);
     }
     if (opt && opt->cuda_stream) {
         s->st = (cudaStream_t)opt->cuda_stream;
@@ -1139,6 +1147,33 @@ static int finish_batch(eclip_session* s, eclip_batch_out* o, double* glat_host 
     mo.energy = en; mo.thr = thr; mo.latency = lat; mo.switches = sw; mo.group_sm = gsm;
     if (s->engine == ECLIP_ENGINE_SLICE) CU(slice_decode_winner(s->slice, s->su, s->wk, s->st));
     CU(launch_materialize(s->su, s->tb, s->wk, s->d_sizes, s->C, mo, s->st));
+    if (!stg && bp.off <= ((size_t)256 << 10)) {
+        // small results (one-shot plans): the staging block in one copy, then host copies into the caller's arrays
+        std::vector<unsigned char> hb(bp.off);
+        CU(cudaMemcpyAsync(hb.data(), base, bp.off, cudaMemcpyDeviceToHost, s->st));
+        CU(cudaStreamSynchronize(s->st));
+        auto hc = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) std::memcpy(dst, hb.data() + ((const unsigned char*)src - base), bytes);
+        };
+        hc(o->status, st, 4 * n);
+        hc(o->winner_levels, lv, 4 * n * W);
+        hc(o->winner_index, idx, 8 * n);
+        hc(o->objective, obj, 8 * n);
+        hc(o->makespan_ns, mk, 8 * n);
+        hc(o->power_w, pw, 8 * n);
+        hc(o->energy_j, en, 8 * n);
+        hc(o->throughput_rps, thr, 8 * n);
+        hc(o->model_latency_ns, lat, 8 * n * W);
+        hc(o->model_switches, sw, 4 * n * W);
+        if (mo.energy_busy) hc(o->energy_busy_j, mo.energy_busy, 8 * n);
+        if (gsm) hc(o->group_sm, gsm, 4 * n * W * stride);
+        if (glat) hc(glat_host, glat, 8 * n * W * stride);
+        if (key) hc(key_host, key, 32 * n);
+        if (o->status)
+            for (size_t i = 0; i < n; i++)
+                if (o->status[i] < 0) return status_error(s, o->status[i], (int)i);
+        return ECLIP_OK;
+    }
     auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
         return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s->st) : cudaSuccess;
     };

@@ -2837,10 +2837,20 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             for (int i = goff[w]; i < goff[w + 1]; i++) { e += ends[i]; ends[i] = e; }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {   // rank of end i (ties by position)
-            const double v = ends[i];
-            int rk = 0;
-            for (int j = 0; j < n; j++) rk += ends[j] < v || (ends[j] == v && j < i);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {   // rank of end i (ties by position): each worker's
+            const double v = ends[i];                           // ends ascend, so count by binary search
+            int wi = 0;
+            while (goff[wi + 1] <= i) wi++;
+            int rk = i - goff[wi];
+            for (int w = 0; w < W; w++) {
+                if (w == wi) continue;
+                int lo = goff[w], hi = goff[w + 1];   // count of ends < v, or <= v for earlier workers
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ends[mid] < v || (w < wi && ends[mid] == v)) lo = mid + 1; else hi = mid;
+                }
+                rk += lo - goff[w];
+            }
             srt[rk] = v;
         }
         __syncthreads();

@@ -117,12 +117,14 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
         const float* gw = g;
         for (int64_t p = nlo + threadIdx.x; p <= nhi; p += blockDim.x) at(Dn, (int)(p - nlo)) = gw[p - S.smin[W - 1]];
         __syncthreads();
+        if (W >= 3) {   // g of the first stage
+            fill_g(W - 2);
+            __syncthreads();
+        }
         for (int w = W - 2; w >= 1; w--) {
             int64_t lo, hi;
             drange(S, T, w, &lo, &hi);
-            fill_g(w);
-            __syncthreads();
-            const float* gw2 = g;
+            const float* gw2 = g;   // g_w (filled before the barrier that ended the previous stage)
             const int nk = S.smax[w] - S.smin[w] + 1;
             const int np = (int)(hi - lo + 1);
             const int nprev = (int)(nhi - nlo + 1);
@@ -184,17 +186,19 @@ __global__ void __launch_bounds__(SL_THREADS) k_slice_f32(SliceDev S, const Prob
                     if (c + j < np) at(Dc, c + j) = best[j];
             }
             __syncthreads();
-            // clear the stale tail of the buffer that becomes D_{w+1}'s neighbour next stage
+            // clear the stale part of the buffer that becomes D_{w+1} next stage (outside [0, np): left over from
+            // two stages ago); the next stage writes every entry of [0, np') of the other buffer, so that one needs
+            // no clearing.  And the next stage's g_{w-1}, under the same barrier.
             for (int i = threadIdx.x; i < BUF; i += blockDim.x)
                 if (i - PAD < 0 || i - PAD >= np) at(Dc, i - PAD) = INFINITY;
+            fill_g(w - 1);
             float* t = Dn; Dn = Dc; Dc = t;
-            for (int i = threadIdx.x; i < BUFS; i += blockDim.x) Dc[i] = INFINITY;
             __syncthreads();
             nlo = lo; nhi = hi;
         }
     }
     // J = min_k g_0[k] (+) D_1[T - smin_0 - k]
-    if (W >= 2) {   // (W = 1: g holds worker 0 already)
+    if (W == 2) {   // (W >= 3: the last stage filled g_0; W = 1: g holds worker 0 already)
         fill_g(0);
         __syncthreads();
     }
@@ -539,16 +543,25 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     int pad = 1;
     for (int w = 0; w < W; w++) pad = std::max(pad, S.smax[w] - S.smin[w] + 1);
     S.pad = pad + RB + KU;
-    CK(salloc(s, &s.d_units, 1));
-    CK(salloc(s, &s.dense, dense.size()));
-    CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
-    CK(salloc(s, &s.J32, (size_t)S.n_slices));
-    CK(salloc(s, &s.Jex, (size_t)S.n_slices));
-    CK(salloc(s, &s.band, (size_t)S.n_slices));
-    CK(salloc(s, &s.wtup, (size_t)S.n_slices));
-    CK(salloc(s, &s.nband, 1));
+    // every buffer in one allocation (256-byte aligned pieces)
     s.slots = 148 * 2;
-    CK(salloc(s, &s.scratch, (size_t)s.slots * (S.gtot + (size_t)W * S.maxrange)));
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off = (off + std::max<size_t>(bytes, 1) + 255) & ~(size_t)255; return o; };
+    const size_t o_units = take(8), o_dense = take(dense.size() * 2), o_J32 = take(4 * (size_t)S.n_slices);
+    const size_t o_Jex = take(sizeof(U256) * (size_t)S.n_slices), o_band = take(4 * (size_t)S.n_slices);
+    const size_t o_wtup = take(sizeof(U256) * (size_t)S.n_slices), o_nband = take(4);
+    const size_t o_scr = take(8 * (size_t)s.slots * (S.gtot + (size_t)W * S.maxrange));
+    unsigned char* blk = nullptr;
+    CK(salloc(s, &blk, off));
+    s.d_units = (unsigned long long*)(blk + o_units);
+    s.dense = (int16_t*)(blk + o_dense);
+    s.J32 = (float*)(blk + o_J32);
+    s.Jex = (U256*)(blk + o_Jex);
+    s.band = (int32_t*)(blk + o_band);
+    s.wtup = (U256*)(blk + o_wtup);
+    s.nband = (int32_t*)(blk + o_nband);
+    s.scratch = (uint64_t*)(blk + o_scr);
+    CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
     return cudaSuccess;
 }
 

@@ -170,6 +170,17 @@ class Profiles:
 
     def __init__(self, handle):
         self._h = C.c_void_p(handle)
+        self._nk = None
+
+    def n_kernels(self) -> List[int]:
+        """kernels per model (cached: profiles are immutable after loading)"""
+        if self._nk is None:
+            n, c = C.c_int32(), C.c_int32()
+            _check(lib().eclip_profiles_info(self._h, C.byref(n), C.byref(c), None, None, None, None, 0))
+            nk = np.zeros(n.value, np.int32)
+            _check(lib().eclip_profiles_info(self._h, None, None, None, _ptr(nk, C.c_int32), None, None, 0))
+            self._nk = nk.tolist()
+        return self._nk
 
     @classmethod
     def from_text(cls, text: str) -> "Profiles":
@@ -320,7 +331,7 @@ class _ProblemArgs:
         self.W = W
         self.gb = None
         self.G = []
-        nk = profiles.info()["n_kernels"]
+        nk = profiles.n_kernels()
         if group_bounds is not None:
             flat = []
             for w in range(W):

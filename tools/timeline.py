@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--mixes", type=int, default=4096)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--out", default="gpurun_out/timeline.json")
+ap.add_argument("--problem", default="", help="c2|c3|c4|s6: one eclip_plan call per step instead of the C5 batch")
 a = ap.parse_args()
 models, ids, qos = synth.make_c5(a.mixes)
 pr = ec.Profiles.from_models(models)
@@ -26,6 +27,14 @@ d_ids, d_q = torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda()
 out = ec.alloc_batch_out(a.mixes, 4, 16, device="cuda")
 pl = ec.Planner(pr, n_models=4, max_problems=a.mixes, total_sms=148, p_idle_w=200.0, p_max_w=1000.0,
                 stream=st.cuda_stream)
+if a.problem:   # single problems: the one-shot eclip_plan (session set-up, K1, search, materialisation)
+    prob = {"c2": synth.make_c2, "c3": lambda: synth.make_c3("matrix"), "c4": synth.make_c4, "s6": synth.make_s6}[a.problem]()
+    prp = ec.Profiles.from_models(prob.models)
+
+    class _One:
+        def plan(self, *args, **kw):
+            ec.plan_problem(prp, prob, stream=st.cuda_stream)
+    pl = _One()
 for _ in range(3):
     pl.plan(d_ids, d_q, out=out)
 torch.cuda.synchronize()
