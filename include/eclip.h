@@ -294,8 +294,8 @@ void eclip_session_free(eclip_session* s);
  * arithmetic) — used by bench.py to report the roofline on the work actually done. */
 int eclip_session_stats(eclip_session* s, uint64_t* evaluated_candidates);
 /* All pass-1 counters of this session, out[0..n): [0] candidates whose FP32 key was evaluated,
- * [1] pass-1 units (rows x segments) processed under row pruning (0 when pruning is off;
- * the rest were proven outside the tolerance band by their lower bound),
+ * [1] pass-1 units (rows x segments) fetched within the band of their row bound under row pruning (0 when
+ * pruning is off; the rest were proven outside the tolerance band by their lower bound),
  * [2] device time in ns of the last launch of the dominant pass-1 kernel (k_pass1_fast or
  * k_pass1_gen), from CUDA events recorded around it on the launching stream (0 for SLICE),
  * [3] pruned pass 1: units in which at least one step entry survived the chunk / entry bounds and

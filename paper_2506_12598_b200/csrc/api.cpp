@@ -721,7 +721,7 @@ static int alloc_work(eclip_session* s, WorkBlock* reuse = nullptr) {
         o_rowlb = bp.take<float>(n * (size_t)su.rows_max);
         o_lbmin = bp.take<unsigned>(n);
         o_inc = bp.take<unsigned>(n);
-        o_hull = bp.take<float2>(n * 4 * (size_t)su.Lmax);
+        o_hull = bp.take<float2>(n * hull_stride(su.Lmax));
         o_ftab = bp.take<int32_t>(n * (size_t)FT_CAP);
         o_ulist = bp.take<uint2>(grid * (size_t)su.upi);
         o_uln = bp.take<int32_t>(grid);

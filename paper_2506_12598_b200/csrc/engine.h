@@ -17,6 +17,11 @@ constexpr int P1_CS = 4;        // step-level chunk of the pass-1 chunk filter
 #define P1_TABN_N 6144
 #endif
 constexpr int P1_TABN = P1_TABN_N;   // entries of each QoS range lookup table (fast pass 1)
+// hull slope tables (enum.cu hull_arg): bins of the query ratio z / y by its float bits, 8 per octave
+constexpr int HT_NB = 256;
+constexpr int HT_F2 = 2 * HT_NB / 8;   // the two tables (step, inner) of a problem, in float2 slots
+// per-problem stride of the row-bound hull buffer (float2): [2][2][Lmax] vertices + edges, then the tables
+__host__ __device__ __forceinline__ size_t hull_stride(int Lmax) { return (size_t)4 * Lmax + HT_F2; }
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
 enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };
@@ -217,6 +222,7 @@ struct RowHdr {                 // per-problem constants of the row bound (k_pre
     int32_t smin_st, umax_st;   // step worker:  min S', max (Tmax - S')
     float Sminf_in, Bminf_in;   // inner worker: (float) min S', (float) min B
     int32_t t0, tn;             // feasibility table covers hT in [t0, t0 + tn); tn = 0: no table
+    int32_t htb[2];             // slope-table bases (step, inner; hull_arg)
 };
 
 // batched co-location simulator (simulate.cu)

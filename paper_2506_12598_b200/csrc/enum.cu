@@ -404,6 +404,44 @@ __global__ void k_arep(Setup su, Prob* probs, const AKey* keys, const unsigned l
     probs[p].rep = rep;
 }
 
+// Slope table of a lower-left hull (n vertices, edges ed[0..n-2] = {B_i - B_i+1, S'_i+1 - S'_i}):
+// the minimiser of B y + S' z is the count of leading edges with ed.x y > ed.y z, which does not
+// increase with q = z / y.  Bin b holds the queries whose float bits satisfy (bits >> 20) = base + b
+// (8 bins per octave); T[b] = that count at the upper end of bin b + 1, so T[b] <= the count of every
+// query of bin b even when q is computed with a few ulps of error (one bin of slack = 9 %); the last
+// bin starts at 0, queries outside the table are clamped to its ends.  The query scans forward from T[b] with the exact predicate (hull_arg): one or two
+// steps instead of a binary search.  Built by threads t < nt of the caller (edge counts by binary search).
+__device__ __forceinline__ void build_slope_table(const float2* ed, int n, uint8_t* T, int* base, int lane, int nt = 32) {
+    int b0 = 0;
+    if (n >= 2) {   // the table spans HT_NB / 8 octaves below the first (largest) slope; smaller queries start
+                    // from bin 0's count (still a valid start)
+        const float smax = ed[0].x / ed[0].y;
+        b0 = (__float_as_int(smax) >> 20) - (HT_NB - 3);
+    }
+    for (int b = lane; b < HT_NB; b += nt) {
+        const int qb = b0 + b + 2;   // bits >> 20 of the upper end of bin b + 1
+        const float q = qb <= 0 ? 0.0f : (qb >= (0x7f800000 >> 20) ? INFINITY : __int_as_float(qb << 20));
+        int lo = 0, hi = max(n - 1, 0);   // the slopes decrease: count = first edge with ed.x <= ed.y q
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ed[mid].x > ed[mid].y * q) lo = mid + 1; else hi = mid;
+        }
+        T[b] = (uint8_t)(b == HT_NB - 1 ? 0 : min(lo, 255));
+    }
+    if (lane == 0) *base = b0;
+}
+__device__ __forceinline__ int hull_arg(const float2* ed, int n, const uint8_t* T, int base, float y, float z) {
+    int b = (__float_as_int(__fdividef(z, y)) >> 20) - base;
+    b = min(max(b, 0), HT_NB - 1);
+    int lo = T[b];
+    while (lo < n - 1) {
+        const float2 e = ed[lo];
+        if (!(e.x * y > e.y * z)) break;
+        lo++;
+    }
+    return lo;
+}
+
 // ------------------------------------------------------------------------------------------
 // fast pass-1 aux block (per problem, right after its Lev records; staged with them)
 //   ip    float4[LP]   inner levels sorted by S', in pairs {B_k, B_k+1, S'_k, S'_k+1}
@@ -427,6 +465,8 @@ struct AuxView {
     int* ihn;                         //   [1] vertex count
     uint16_t* hpos;                   // inner, S'-sorted position k -> last hull vertex with S' <= S'_k
     float* chBs;                      // step worker: suffix minimum of chB over the chunks
+    uint8_t* ht;                      // inner hull's slope table [HT_NB] (build_slope_table)
+    int* htb;                         //   [1] its base
 };
 __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     const size_t LP = (size_t)(Lmax + 1) / 2;
@@ -437,6 +477,7 @@ __host__ __device__ __forceinline__ size_t aux_bytes_of(int Lmax) {
     b += (size_t)Lmax * 16 + 4 + (size_t)Lmax * 2;   // ih, ie, ihn, hpos
     b = (b + 3) & ~(size_t)3;
     b += (size_t)((Lmax + P1_CS - 1) / P1_CS) * 4;   // chBs
+    b += 4 + HT_NB;                                   // htb, ht
     return (b + 31) / 32 * 32;
 }
 size_t pass1_aux_bytes(int Lmax) { return aux_bytes_of(Lmax); }
@@ -469,6 +510,8 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
     a.hpos = reinterpret_cast<uint16_t*>(a.ihn + 1);
     q = reinterpret_cast<unsigned char*>(a.hpos + Lmax);
     a.chBs = reinterpret_cast<float*>(base + ((q - base + 3) & ~(size_t)3));
+    a.htb = reinterpret_cast<int*>(a.chBs + (Lmax + P1_CS - 1) / P1_CS);
+    a.ht = reinterpret_cast<uint8_t*>(a.htb + 1);
     return a;
 }
 
@@ -609,6 +652,8 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
             }
         }
         if (threadIdx.x == 0) *A.ihn = nh;
+        __syncthreads();
+        build_slope_table(A.ie, nh, A.ht, A.htb, threadIdx.x, blockDim.x);
         for (int k = threadIdx.x; k < Lin; k += blockDim.x) {   // last vertex with S' <= S'_k (exact ints)
             const int sk = inner[A.perm[k]].S;
             int lo = 0, hi = nh - 1;
@@ -815,7 +860,7 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
             bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, off));
             smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, off));
         }
-        float2* h = hull + ((size_t)prob * 2 + which) * 2 * Lmax;
+        float2* h = hull + (size_t)prob * hull_stride(Lmax) + (size_t)which * 2 * Lmax;
         for (int i = lane; i < n; i += 32) {
             const Lev& v = lv[hx[i]];
             h[i] = make_float2(__ll2float_rn(v.B), (float)v.S);
@@ -824,9 +869,14 @@ __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs,
                 h[Lmax + i] = make_float2(__ll2float_rn(v.B - x.B), (float)(x.S - v.S));
             }
         }
+        __syncwarp();
+        int htb = 0;
+        build_slope_table(h + Lmax, n, reinterpret_cast<uint8_t*>(hull + (size_t)prob * hull_stride(Lmax) + 4 * (size_t)Lmax) +
+                                           which * HT_NB, &htb, lane);
         if (lane == 0) {
             RowHdr* H = hdr + prob;
             H->nh[which] = n;
+            H->htb[which] = htb;
             if (which == 0) { H->smin_st = smin; H->umax_st = umax; H->t0 = t0; H->tn = tn; }
             else { H->smin_in = smin; H->umax_in = umax; H->Sminf_in = (float)smin; H->Bminf_in = __ll2float_rn(bmin); }
         }
@@ -888,6 +938,15 @@ __device__ __forceinline__ float hull_min(const float2* v, const float2* ed, int
     if (lo + 1 < n) m = fminf(m, fmaf(v[lo + 1].x, y, v[lo + 1].y * z));
     return m;
 }
+// the same with the minimiser found through the hull's slope table
+__device__ __forceinline__ float hull_min_t(const float2* v, const float2* ed, int n, const uint8_t* T, int base, float y,
+                                           float z) {
+    const int lo = hull_arg(ed, n, T, base, y, z);
+    float m = fmaf(v[lo].x, y, v[lo].y * z);
+    if (lo > 0) m = fminf(m, fmaf(v[lo - 1].x, y, v[lo - 1].y * z));
+    if (lo + 1 < n) m = fminf(m, fmaf(v[lo + 1].x, y, v[lo + 1].y * z));
+    return m;
+}
 
 // min over the points of a lower-left hull's point set with S' in [slo, shi] of B y + S' z (y, z >= 0),
 // bounded below: the objective along the hull is convex in S', so the constrained minimum is at the
@@ -927,13 +986,7 @@ __device__ __forceinline__ float hull_min_in(const float2* v, const float2* ed, 
 // the last hull vertex at or below each (hpos) are tabulated, so the clamp needs no search
 __device__ __forceinline__ float hull_min_pos(const AuxView& A, int n, float y, float z, int ka, int kb) {
     const float2* v = A.ih;
-    const float2* ed = A.ie;
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const float2 e = ed[mid];
-        if (e.x * y > e.y * z) lo = mid + 1; else hi = mid;
-    }
+    const int lo = hull_arg(A.ie, n, A.ht, *A.htb, y, z);
     const float s = v[lo].y, slo = (float)A.ssort[ka], shi = (float)A.ssort[kb];
     if (s >= slo && s <= shi) {
         float m = fmaf(v[lo].x, y, s * z);
@@ -958,7 +1011,7 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
                                                unsigned* lbmin) {
     constexpr int NH = NW - 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* sh = reinterpret_cast<float2*>(smem_raw);   // [2][2][Lmax]
+    float2* sh = reinterpret_cast<float2*>(smem_raw);   // [2][2][Lmax] + slope tables (hull_stride)
     __shared__ float red[8];
     const int prob = blockIdx.y;
     const Prob& P = probs[prob];
@@ -966,7 +1019,8 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
     const int rp = P.rep;   // hulls, feasibility table and header of the representative (k_arep)
     const RowHdr H = hdr[rp];
     const int Lmax = su.Lmax;
-    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)rp * 4 * Lmax + i];
+    for (int i = threadIdx.x; i < (int)hull_stride(Lmax); i += blockDim.x) sh[i] = hull[(size_t)rp * hull_stride(Lmax) + i];
+    const uint8_t* sht = reinterpret_cast<const uint8_t*>(sh + 4 * Lmax);
     __syncthreads();
     const Lev* base = levs + (size_t)prob * su.lev_stride;
     const uint64_t rows = P.units / (uint64_t)P.nseg;
@@ -1011,7 +1065,8 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
             const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
             const float Xh = fmaf(Dhf, invf, hBf);
             const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
-            lb = (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
+            lb = (Xh + hull_min_t(sh, sh + Lmax, H.nh[0], sht, H.htb[0], Y2, Z2) +
+                  hull_min_t(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], sht + HT_NB, H.htb[1], Yh, Zh)) *
                  0.99998474121f;   // 1 - 2^-16
         }
         rowlb[(size_t)prob * su.rows_max + r] = lb;
@@ -1050,8 +1105,8 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     constexpr int NH = NW - 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Lmax = su.Lmax;
-    float2* sh = reinterpret_cast<float2*>(smem_raw);                  // [2][2][Lmax] hulls + edges
-    Lev* hrec = reinterpret_cast<Lev*>(sh + 4 * Lmax);                  // [NH][Lmax] hi records
+    float2* sh = reinterpret_cast<float2*>(smem_raw);                  // [2][2][Lmax] hulls + edges, slope tables
+    Lev* hrec = reinterpret_cast<Lev*>(sh + hull_stride(Lmax));         // [NH][Lmax] hi records
     float* lbs = reinterpret_cast<float*>(hrec + NH * Lmax);            // [rows]
     __shared__ float red[RLF_THREADS / 32];
     __shared__ int hist[BB_NB], cur[BB_NB];
@@ -1064,7 +1119,8 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     const int rp = P.rep;   // hulls, feasibility table and header of the representative (k_arep)
     const RowHdr H = hdr[rp];
     const Lev* base = levs + (size_t)prob * su.lev_stride;
-    for (int i = threadIdx.x; i < 4 * Lmax; i += blockDim.x) sh[i] = hull[(size_t)rp * 4 * Lmax + i];
+    for (int i = threadIdx.x; i < (int)hull_stride(Lmax); i += blockDim.x) sh[i] = hull[(size_t)rp * hull_stride(Lmax) + i];
+    const uint8_t* sht = reinterpret_cast<const uint8_t*>(sh + 4 * Lmax);
     for (int i = threadIdx.x; i < NH * Lmax; i += blockDim.x) hrec[i] = base[i];
     for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
     __syncthreads();
@@ -1086,24 +1142,29 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
         const float Xh = fmaf(Dhf, invf, hBf);
         const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
-        return (Xh + hull_min(sh, sh + Lmax, H.nh[0], Y2, Z2) + hull_min(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], Yh, Zh)) *
+        return (Xh + hull_min_t(sh, sh + Lmax, H.nh[0], sht, H.htb[0], Y2, Z2) +
+                hull_min_t(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], sht + HT_NB, H.htb[1], Yh, Zh)) *
                0.99998474121f;   // 1 - 2^-16
     };
     float bm = INFINITY;
-    if (NH == 2 && Lh[NH - 1] <= 128) {
-        // rows = (d0, d1), d1 least significant: thread -> d1 (its record stays in registers), d0 strided
-        const int L0 = (int)Lh[0], L1 = (int)Lh[NH - 1], d1 = threadIdx.x & 127;
-        if (d1 < L1) {
-            const Lev r1 = hrec[(NH - 1) * Lmax + d1];
-            for (int d0 = threadIdx.x >> 7; d0 < L0; d0 += RLF_THREADS / 128) {
-                const Lev& r0 = hrec[d0];
-                // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding <= 3u,
-                // inside the bound's 1 - 2^-16 margin)
-                const float Dhf = fmaf(__ll2float_rn(r0.B), (float)r1.S, __ll2float_rn(r1.B) * (float)r0.S);
-                const float lb = row_lb(r0.B + r1.B, Dhf, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
-                lbs[d0 * L1 + d1] = lb;
-                bm = fminf(bm, lb);
-            }
+    if (NH == 2) {
+        // rows = (d0, d1), d1 least significant, strided over every thread (no idle lanes when L1 is not a
+        // multiple of the block); d0 = r / L1 from a float quotient corrected by one step (r < 2^24)
+        const int L1 = (int)Lh[NH - 1];
+        const float rL1 = 1.0f / (float)L1;
+        for (int r = threadIdx.x; r < (int)rows; r += RLF_THREADS) {
+            int d0 = __float2int_rz((float)r * rL1);
+            if (d0 * L1 > r) d0--;
+            else if ((d0 + 1) * L1 <= r) d0++;
+            const int d1 = r - d0 * L1;
+            const Lev& r0 = hrec[d0];
+            const Lev& r1 = hrec[(NH - 1) * Lmax + d1];
+            // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding <= 3u,
+            // inside the bound's 1 - 2^-16 margin)
+            const float Dhf = fmaf(__ll2float_rn(r0.B), (float)r1.S, __ll2float_rn(r1.B) * (float)r0.S);
+            const float lb = row_lb(r0.B + r1.B, Dhf, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
+            lbs[r] = lb;
+            bm = fminf(bm, lb);
         }
     } else {
         for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
@@ -1253,7 +1314,7 @@ struct BBArgs {
     const int32_t* ulist_n;     // [grid]
     const unsigned* lbmin;      // [n] smallest row bound of the problem (float bits)
     unsigned* inc;              // [n] global incumbent (float bits)
-    unsigned long long* rows_done;  // [6]: units processed, units with >= 1 swept entry, entries swept, units past
+    unsigned long long* rows_done;  // [6]: units fetched within the band, units with >= 1 swept entry, entries swept, units past
                                     //   the unit bound, units with >= 1 chunk kept, chunks kept
     uint32_t* plist;            // [n * PL_CAP] processed units with a finite minimum
     int32_t* plist_n;
@@ -1559,6 +1620,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             rbase += RSTEP;
             pend = __ballot_sync(0xffffffffu, base + wl < ub);
         }
+        const float bnd_f = bnd;   // the band the fetch-time filters below use (warp-uniform)
         int uT = 0, uTm = 0, uSb = 0, uEa = 0, uNe = 0;
         float uX = 0.0f, uY = 0.0f, uZ = 0.0f;
         uint32_t uCm = 0;
@@ -1566,6 +1628,10 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
         if ((pend >> wl) & 1u) {   // this lane's own unit
             const uint64_t myunit = BB ? ua + (uint64_t)loff : base + (uint64_t)wl;
             uok = unit_consts(myunit, uT, uTm, uSb, uEa, uNe, uX, uY, uZ, uCm, uCh);
+        }
+        if (BB) {   // units fetched within the band; those the fetch-time bounds cleared are not visited below
+            if (wl == 0) ndone += __popc(pend);
+            pend &= __ballot_sync(0xffffffffu, uok);
         }
       while (pend) {
         const int jl = __ffs(pend) - 1;
@@ -1583,7 +1649,6 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 bnd_of = incv;
             }
             if (lbj > bnd) continue;
-            ndone++;
         }
         const int cT = __shfl_sync(0xffffffffu, uT, jl), cTm = __shfl_sync(0xffffffffu, uTm, jl);
         const int sb = __shfl_sync(0xffffffffu, uSb, jl), ea = __shfl_sync(0xffffffffu, uEa, jl);
@@ -1810,8 +1875,9 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                 const int c_lo = ea / P1_CS;
                 chunked = true;
                 const unsigned cm0 = __shfl_sync(0xffffffffu, uCm, jl);
-                // re-checked against the band as it is now (tighter than at fetch time)
-                const bool keep = ((cm0 >> wl) & 1u) && chunk_keep(c_lo + wl, h.T, h.Tm, Xh, Yh, Zh);
+                // re-checked against the band as it is now if it tightened since the fetch (the same test
+                // against the same band would repeat the fetch-time result)
+                const bool keep = ((cm0 >> wl) & 1u) && (bnd == bnd_f || chunk_keep(c_lo + wl, h.T, h.Tm, Xh, Yh, Zh));
                 const unsigned cm = __ballot_sync(0xffffffffu, keep);
                 nch += __popc(cm);
                 nuch += cm != 0u;
@@ -2107,7 +2173,8 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
             return e;
         k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.table_of,
                                                        wk.thull, wk.thull_n);
-        const size_t fsm = (size_t)su.Lmax * (4 * sizeof(float2) + (size_t)(su.W - 2) * sizeof(Lev)) + (size_t)su.rows_max * 4;
+        const size_t fsm = hull_stride(su.Lmax) * sizeof(float2) + (size_t)su.Lmax * (size_t)(su.W - 2) * sizeof(Lev) +
+                           (size_t)su.rows_max * 4;
         if (rowlb_fused_ok(su) && fsm <= 160 * 1024) {
             RowLBF rf = nullptr;
             switch (su.W) {
@@ -2134,7 +2201,10 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         // enough CTAs to fill the GPU (8 per SM), each looping over many rows of its problem
         const long long want = std::max<long long>(1, (148LL * 8 + su.n_problems - 1) / su.n_problems);
         const long long gx = std::min<long long>((su.rows_max + 255) / 256, want);
-        r<<<dim3((unsigned)gx, (unsigned)su.n_problems), 256, (size_t)su.Lmax * 32, st>>>(
+        const size_t rsm = hull_stride(su.Lmax) * sizeof(float2);
+        if ((e = cudaFuncSetAttribute((const void*)r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)) != cudaSuccess)
+            return e;
+        r<<<dim3((unsigned)gx, (unsigned)su.n_problems), 256, rsm, st>>>(
             su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.rowlb, wk.lbmin);
         if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
@@ -2532,7 +2602,7 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
                     const float Ye = fmaf(Sf, invf, Yh), Ze = fmaf(Be, invf, Zh);
                     float lbe = fmaf(Ye, A.preminB[khi], fmaf(Ze, (float)A.ssort[ka], X));
                     if (hull && !(lbe * 0.99998474121f > bound)) {   // the inner hull restricted to the S' range
-                        const float2* hv = hull + ((size_t)P.rep * 2 + 1) * 2 * su.Lmax;
+                        const float2* hv = hull + (size_t)P.rep * hull_stride(su.Lmax) + 2 * (size_t)su.Lmax;
                         lbe = fmaxf(lbe, X + hull_min_in(hv, hv + su.Lmax, rowhdr[P.rep].nh[1], Ye, Ze, (float)A.ssort[ka],
                                                          (float)A.ssort[khi - 1]));
                     }
