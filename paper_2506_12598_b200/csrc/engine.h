@@ -207,12 +207,13 @@ struct AKey {                   // what a problem's step / inner-worker precompu
     u128 hq_step, hq_inner;                // exact QoS thresholds floor(Q D)
 };
 #ifndef BAND_CAP_N
-#define BAND_CAP_N 64
+#define BAND_CAP_N 1024
 #endif
 #ifndef PL_CAP_N
 #define PL_CAP_N 4096
 #endif
 constexpr int BAND_CAP = BAND_CAP_N;   // pass-2 band list capacity per problem
+constexpr int BAND_SORTED = 64;       // band lists up to this length are in index order (pass 2 stops at the first hit)
 constexpr int PL_CAP = PL_CAP_N;       // processed-unit list capacity per problem (tiny values in test builds
                                        // exercise the overflow paths)
 

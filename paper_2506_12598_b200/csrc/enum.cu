@@ -1105,9 +1105,15 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     constexpr int NH = NW - 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Lmax = su.Lmax;
-    float2* sh = reinterpret_cast<float2*>(smem_raw);                  // [2][2][Lmax] hulls + edges, slope tables
-    Lev* hrec = reinterpret_cast<Lev*>(sh + hull_stride(Lmax));         // [NH][Lmax] hi records
-    float* lbs = reinterpret_cast<float*>(hrec + NH * Lmax);            // [rows]
+    // hulls + edges + slope tables; the hi workers' records as separate arrays (lanes read consecutive
+    // levels: one bank per lane); every row's bound; a bit per row with a finite bound
+    float2* sh = reinterpret_cast<float2*>(smem_raw);
+    int64_t* hB = reinterpret_cast<int64_t*>(sh + hull_stride(Lmax));   // [NH][Lmax]
+    int64_t* hBS = hB + NH * Lmax;                                      // [NH][Lmax]
+    int32_t* hS = reinterpret_cast<int32_t*>(hBS + NH * Lmax);          // [NH][Lmax]
+    int32_t* hTx = hS + NH * Lmax;                                      // [NH][Lmax]
+    float* lbs = reinterpret_cast<float*>(hTx + NH * Lmax);             // [rows]
+    uint32_t* fbit = reinterpret_cast<uint32_t*>(lbs + su.rows_max);    // [ceil(rows / 32)]
     __shared__ float red[RLF_THREADS / 32];
     __shared__ int hist[BB_NB], cur[BB_NB];
     const int prob = blockIdx.x;
@@ -1121,7 +1127,10 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     const Lev* base = levs + (size_t)prob * su.lev_stride;
     for (int i = threadIdx.x; i < (int)hull_stride(Lmax); i += blockDim.x) sh[i] = hull[(size_t)rp * hull_stride(Lmax) + i];
     const uint8_t* sht = reinterpret_cast<const uint8_t*>(sh + 4 * Lmax);
-    for (int i = threadIdx.x; i < NH * Lmax; i += blockDim.x) hrec[i] = base[i];
+    for (int i = threadIdx.x; i < NH * Lmax; i += blockDim.x) {
+        const Lev v = base[i];
+        hB[i] = v.B; hBS[i] = v.BS; hS[i] = (int32_t)v.S; hTx[i] = v.Tmax;
+    }
     for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint32_t rows = (uint32_t)P.units;
@@ -1130,15 +1139,14 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
     for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
+    auto feasible = [&](int hT, int hTm) -> bool {
+        if (!QOS) return true;
+        if (H.tn > 0) return ft[hT - H.t0] <= hTm - hT;
+        return !(H.smin_st > min(hTm - hT - H.smin_in, H.umax_in - hT) || H.umax_st < hT + H.smin_in);
+    };
     // Dhf: (float) sum over the hi workers of B_w (hT - S'_w) >= 0 (computed by the caller)
-    auto row_lb = [&](int64_t hB, float Dhf, int hT, int hTm) -> float {
-        bool feas = true;
-        if (QOS) {
-            if (H.tn > 0) feas = ft[hT - H.t0] <= hTm - hT;
-            else feas = !(H.smin_st > min(hTm - hT - H.smin_in, H.umax_in - hT) || H.umax_st < hT + H.smin_in);
-        }
-        if (!feas) return INFINITY;
-        const float hBf = __ll2float_rn(hB), hTf = (float)hT;
+    auto row_lb = [&](int64_t hBv, float Dhf, int hT) -> float {
+        const float hBf = __ll2float_rn(hBv), hTf = (float)hT;
         const float Yh = fmaf(hTf, invf, 1.0f), Zh = hBf * invf;
         const float Xh = fmaf(Dhf, invf, hBf);
         const float Y2 = fmaf(H.Sminf_in, invf, Yh), Z2 = fmaf(H.Bminf_in, invf, Zh);
@@ -1146,44 +1154,53 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
                 hull_min_t(sh + 2 * Lmax, sh + 3 * Lmax, H.nh[1], sht + HT_NB, H.htb[1], Yh, Zh)) *
                0.99998474121f;   // 1 - 2^-16
     };
+    // rows strided over every thread: warp w of pass it handles the 32 consecutive rows of bitmap word
+    // it * (RLF_THREADS / 32) + w
     float bm = INFINITY;
-    if (NH == 2) {
-        // rows = (d0, d1), d1 least significant, strided over every thread (no idle lanes when L1 is not a
-        // multiple of the block); d0 = r / L1 from a float quotient corrected by one step (r < 2^24)
-        const int L1 = (int)Lh[NH - 1];
-        const float rL1 = 1.0f / (float)L1;
-        for (int r = threadIdx.x; r < (int)rows; r += RLF_THREADS) {
-            int d0 = __float2int_rz((float)r * rL1);
-            if (d0 * L1 > r) d0--;
-            else if ((d0 + 1) * L1 <= r) d0++;
-            const int d1 = r - d0 * L1;
-            const Lev& r0 = hrec[d0];
-            const Lev& r1 = hrec[(NH - 1) * Lmax + d1];
-            // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding <= 3u,
-            // inside the bound's 1 - 2^-16 margin)
-            const float Dhf = fmaf(__ll2float_rn(r0.B), (float)r1.S, __ll2float_rn(r1.B) * (float)r0.S);
-            const float lb = row_lb(r0.B + r1.B, Dhf, r0.S + r1.S, min(r0.Tmax, r1.Tmax));
-            lbs[r] = lb;
-            bm = fminf(bm, lb);
-        }
-    } else {
-        for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-            int64_t hB = 0, hBS = 0;
-            int hT = 0, hTm = 1 << 24;
-            uint32_t x = r;
+    const int nwords = (int)((rows + 31) >> 5);
+    const int lane = threadIdx.x & 31;
+    for (int r0 = threadIdx.x - lane; r0 < (int)rows; r0 += RLF_THREADS) {
+        const int r = r0 + lane;
+        float lb = INFINITY;
+        if (r < (int)rows) {
+            if (NH == 2) {
+                // rows = (d0, d1), d1 least significant; d0 = r / L1 from a float quotient corrected by one
+                // step (r < 2^24)
+                const int L1 = (int)Lh[1];
+                int d0 = __float2int_rz((float)r * (1.0f / (float)L1));
+                if (d0 * L1 > r) d0--;
+                else if ((d0 + 1) * L1 <= r) d0++;
+                const int d1 = r - d0 * L1 + Lmax;
+                const int hT = hS[d0] + hS[d1];
+                if (feasible(hT, min(hTx[d0], hTx[d1]))) {
+                    // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding
+                    // <= 3u, inside the bound's 1 - 2^-16 margin)
+                    const int64_t b0 = hB[d0], b1 = hB[d1];
+                    const float Dhf = fmaf(__ll2float_rn(b0), (float)hS[d1], __ll2float_rn(b1) * (float)hS[d0]);
+                    lb = row_lb(b0 + b1, Dhf, hT);
+                }
+            } else {
+                int64_t sB = 0, sBS = 0;
+                int hT = 0, hTm = 1 << 24;
+                uint32_t x = (uint32_t)r;
 #pragma unroll
-            for (int w = NH - 1; w >= 0; w--) {
-                const uint32_t d = x % Lh[w];
-                x /= Lh[w];
-                const Lev& v = hrec[w * Lmax + d];
-                hB += v.B; hBS += v.BS; hT += v.S; hTm = min(hTm, v.Tmax);
+                for (int w = NH - 1; w >= 0; w--) {
+                    const uint32_t d = x % Lh[w];
+                    x /= Lh[w];
+                    const int i = w * Lmax + (int)d;
+                    sB += hB[i]; sBS += hBS[i]; hT += hS[i]; hTm = min(hTm, hTx[i]);
+                }
+                if (feasible(hT, hTm)) {
+                    const u128 Dh = (u128)hT * (u128)sB - (u128)sBS;
+                    const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
+                    lb = row_lb(sB, Dhf, hT);
+                }
             }
-            const u128 Dh = (u128)hT * (u128)hB - (u128)hBS;
-            const float Dhf = (Dh >> 64) ? (float)(double)Dh : __ull2float_rn((unsigned long long)Dh);
-            const float lb = row_lb(hB, Dhf, hT, hTm);
             lbs[r] = lb;
             bm = fminf(bm, lb);
         }
+        const unsigned fb = __ballot_sync(0xffffffffu, lb < INFINITY);
+        if (lane == 0 && r0 < (int)rows) fbit[r0 >> 5] = fb;
     }
     for (int o = 16; o; o >>= 1) bm = fminf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = bm;
@@ -1195,10 +1212,9 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         if (threadIdx.x == 0) ulist_n[prob] = 0;
         return;
     }
-    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-        const float lb = lbs[r];
-        if (lb < INFINITY) atomicAdd(&hist[bb_bucket(lb, bm)], 1);
-    }
+    // bucket histogram and scatter over the rows with a finite bound only (one bitmap word per thread)
+    for (int wd = threadIdx.x; wd < nwords; wd += blockDim.x)
+        for (uint32_t m = fbit[wd]; m; m &= m - 1) atomicAdd(&hist[bb_bucket(lbs[wd * 32 + __ffs(m) - 1], bm)], 1);
     __syncthreads();
     if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
         int v[BB_NB / 32], t = 0;
@@ -1211,10 +1227,12 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     }
     __syncthreads();
     uint2* out = ulist + (size_t)prob * su.upi;
-    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-        const float lb = lbs[r];
-        if (lb < INFINITY) out[atomicAdd(&cur[bb_bucket(lb, bm)], 1)] = make_uint2(r, __float_as_uint(lb));
-    }
+    for (int wd = threadIdx.x; wd < nwords; wd += blockDim.x)
+        for (uint32_t m = fbit[wd]; m; m &= m - 1) {
+            const uint32_t r = (uint32_t)(wd * 32 + __ffs(m) - 1);
+            const float lb = lbs[r];
+            out[atomicAdd(&cur[bb_bucket(lb, bm)], 1)] = make_uint2(r, __float_as_uint(lb));
+        }
 }
 
 __global__ void k_fill_u32(unsigned* p, size_t n, unsigned v) {
@@ -2173,8 +2191,8 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
             return e;
         k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.table_of,
                                                        wk.thull, wk.thull_n);
-        const size_t fsm = hull_stride(su.Lmax) * sizeof(float2) + (size_t)su.Lmax * (size_t)(su.W - 2) * sizeof(Lev) +
-                           (size_t)su.rows_max * 4;
+        const size_t fsm = hull_stride(su.Lmax) * sizeof(float2) + (size_t)su.Lmax * (size_t)(su.W - 2) * 24 +
+                           (size_t)su.rows_max * 4 + (size_t)((su.rows_max + 31) / 32) * 4;
         if (rowlb_fused_ok(su) && fsm <= 160 * 1024) {
             RowLBF rf = nullptr;
             switch (su.W) {
@@ -2259,7 +2277,7 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // one CTA (256 threads) per problem: this shard's minimum over its units' pass-1 minima, then the
 // units pass 2 must rescan (submin within the band of this shard's minimum; the global minimum is
-// never larger, so its band is a subset), sorted into index order; bandn = -1: more than BAND_CAP
+// never larger, so its band is a subset), in index order when at most BAND_SORTED long; bandn = -1: more than BAND_CAP
 __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs, const float* submin,
                                                     const float* submin_sure, float* m32, float* m32_sure,
                                                     int32_t* bandn, uint64_t* bandlist, const uint32_t* plist,
@@ -2326,7 +2344,7 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
     if (tid == 0) {
         const int n = s_cnt;
         if (n <= BAND_CAP) {
-            for (int i = 1; i < n; i++) {   // insertion sort: index order
+            for (int i = 1; i < n && n <= BAND_SORTED; i++) {   // insertion sort: index order (short lists)
                 const uint64_t v = s_list[i];
                 int j = i - 1;
                 while (j >= 0 && s_list[j] > v) { s_list[j + 1] = s_list[j]; j--; }
@@ -2601,11 +2619,8 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
                     if (su.mode == M_PAPER) X += (float)((double)r.BS * invd);
                     const float Ye = fmaf(Sf, invf, Yh), Ze = fmaf(Be, invf, Zh);
                     float lbe = fmaf(Ye, A.preminB[khi], fmaf(Ze, (float)A.ssort[ka], X));
-                    if (hull && !(lbe * 0.99998474121f > bound)) {   // the inner hull restricted to the S' range
-                        const float2* hv = hull + (size_t)P.rep * hull_stride(su.Lmax) + 2 * (size_t)su.Lmax;
-                        lbe = fmaxf(lbe, X + hull_min_in(hv, hv + su.Lmax, rowhdr[P.rep].nh[1], Ye, Ze, (float)A.ssort[ka],
-                                                         (float)A.ssort[khi - 1]));
-                    }
+                    if (!(lbe * 0.99998474121f > bound))   // the inner hull restricted to the S' range (aux block)
+                        lbe = fmaxf(lbe, X + hull_min_pos(A, *A.ihn, Ye, Ze, ka, khi - 1));
                     keep = !(lbe * 0.99998474121f > bound);   // 1 - 2^-16
                 }
                 if (keep) s_elist[atomicAdd(&s_ne, 1)] = (int16_t)e;
@@ -2637,7 +2652,8 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
                 const uint64_t unit = bandlist[(size_t)prob * BAND_CAP + i];
                 if (!(sub_at(su, submin + (size_t)prob * su.units_max, wbits, prob, unit) <= bound)) continue;
                 unit_scan(phase, unit, hs, best, besti);
-                if (phase == 1 && __syncthreads_or(besti != ~0ull)) break;   // first unit with a hit holds the winner
+                // in an index-ordered list the first unit with a hit holds the winner
+                if (phase == 1 && nband <= BAND_SORTED && __syncthreads_or(besti != ~0ull)) break;
             }
             __syncthreads();
             return;
