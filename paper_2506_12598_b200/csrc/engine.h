@@ -24,6 +24,30 @@ constexpr int HT_F2 = 2 * HT_NB / 8;   // the two tables (step, inner) of a prob
 __host__ __device__ __forceinline__ size_t hull_stride(int Lmax) { return (size_t)4 * Lmax + HT_F2; }
 
 enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
+
+// Programmatic dependent launch (sm_90+): kernels of the planner's chain are launched with programmatic
+// stream serialisation (launch_pdl), so a kernel's CTAs are scheduled while its predecessor's last wave
+// still runs.  Every kernel so launched calls pdl_wait() before it reads anything its predecessor wrote
+// (and before it exits, so that its completion implies the predecessor's), then pdl_trigger() to let its
+// own successor be scheduled.  Outside such a launch both are no-ops.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+#endif
 enum Obj { O_SUM = 0, O_MAX = 1, O_ENERGY = 2 };
 
 // ---------------------------------------------------------------------------------------

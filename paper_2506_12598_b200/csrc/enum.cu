@@ -158,6 +158,8 @@ __device__ __forceinline__ void decode_row(uint64_t row, const int* L, int W, in
 // prep
 // ------------------------------------------------------------------------------------------
 __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= su.n_problems) return;
     Prob P;
@@ -277,6 +279,8 @@ __global__ void k_prep_prob(Setup su, Tables tb, PrepIn in, Prob* probs) {
 
 // one thread per (problem, worker, level)
 __global__ void k_prep_lev(Setup su, Tables tb, const Prob* probs, Lev* levs) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
     if (i >= n) return;
@@ -346,6 +350,8 @@ __device__ __forceinline__ bool akey_eq(const AKey& a, const AKey& b) {
 
 __global__ void __launch_bounds__(256) k_akey(Setup su, const Prob* probs, const Lev* levs, AKey* keys,
                                               unsigned long long* slot, int nslots) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     const int p = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (p >= su.n_problems) return;
     const Prob& P = probs[p];
@@ -385,6 +391,8 @@ __global__ void __launch_bounds__(256) k_akey(Setup su, const Prob* probs, const
 }
 
 __global__ void k_arep(Setup su, Prob* probs, const AKey* keys, const unsigned long long* slot, int nslots) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= su.n_problems) return;
     const AKey k = keys[p];
@@ -519,6 +527,8 @@ __device__ __forceinline__ AuxView aux_view(unsigned char* base, int Lmax) {
 template <int MODE>
 __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, Lev* levs, const int32_t* table_of,
                                                   const uint16_t* tord, const uint16_t* thull, const int32_t* thull_n) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     const int prob = blockIdx.x;
     const Prob& P = probs[prob];
     if (P.status != 0 || P.rep != prob) return;   // a representative's block serves this problem
@@ -812,6 +822,8 @@ __global__ void __launch_bounds__(256) k_table_hull(Tables tb, int Lmax, uint16_
 __global__ void __launch_bounds__(256) k_prep_bound(Setup su, const Prob* probs, const Lev* levs, float2* hull,
                                                     int32_t* ftab, RowHdr* hdr, const int32_t* table_of,
                                                     const uint16_t* thull, const int32_t* thull_n) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int* G = reinterpret_cast<int*>(smem_raw);                          // [FT_CAP]
     Lev* sv = reinterpret_cast<Lev*>(G + FT_CAP);                      // [2][Lmax] step, inner records
@@ -1102,6 +1114,8 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
                                                              const float2* hull, const int32_t* ftab,
                                                              const RowHdr* hdr, unsigned* lbmin, uint2* ulist,
                                                              int32_t* ulist_n) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     constexpr int NH = NW - 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Lmax = su.Lmax;
@@ -1236,7 +1250,30 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
 }
 
 __global__ void k_fill_u32(unsigned* p, size_t n, unsigned v) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// up to four fills in one launch (the planner chain: no memset between programmatically serialised kernels)
+struct Fill4 {
+    unsigned* p[4];
+    size_t n[4];
+    unsigned v[4];
+};
+__global__ void k_fill4(Fill4 f) {
+    pdl_wait();
+    pdl_trigger();
+    for (int j = 0; j < 4; j++)
+        for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < f.n[j]; i += (size_t)gridDim.x * blockDim.x)
+            f.p[j][i] = f.v[j];
+}
+static cudaError_t fill4(const Fill4& f, cudaStream_t st) {
+    size_t mx = 0;
+    for (int j = 0; j < 4; j++) mx = std::max(mx, f.p[j] ? f.n[j] : 0);
+    if (mx == 0) return cudaSuccess;
+    const size_t blocks = std::min<size_t>((mx + 255) / 256, 148 * 8);
+    return launch_pdl(k_fill4, dim3((unsigned)blocks), dim3(256), 0, st, f);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1400,6 +1437,8 @@ template <int NW, int MODE, bool QOS, bool BB>
 __global__ void __launch_bounds__(P1_THREADS, (!QOS && !BB && NW >= 2) ? P1_MINB_EXH : P1_MINB)
 k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ levs, float* __restrict__ submin,
              unsigned long long* __restrict__ feasible, BBArgs bb) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     constexpr int NH = NW >= 2 ? NW - 2 : 0;   // hi workers (fixed inside a unit)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
@@ -2180,17 +2219,21 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
         cudaError_t e;
         const size_t n = (size_t)su.n_problems;
         // unwritten units read as +inf through the bitmap (sub_at), so submin itself is not filled
-        if ((e = cudaMemsetAsync(wk.wbits, 0, n * (size_t)((su.units_max + 31) >> 5) * sizeof(uint32_t), st)) != cudaSuccess)
-            return e;
-        if ((e = fill_u32(wk.inc, n, 0x7f800000u, st)) != cudaSuccess) return e;
-        if ((e = fill_u32(wk.lbmin, n, 0x7f800000u, st)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(wk.plist_n, 0, n * sizeof(int32_t), st)) != cudaSuccess) return e;
+        {
+            Fill4 f{};
+            f.p[0] = wk.wbits; f.n[0] = n * (size_t)((su.units_max + 31) >> 5); f.v[0] = 0u;
+            f.p[1] = wk.inc; f.n[1] = n; f.v[1] = 0x7f800000u;
+            f.p[2] = wk.lbmin; f.n[2] = n; f.v[2] = 0x7f800000u;
+            f.p[3] = reinterpret_cast<unsigned*>(wk.plist_n); f.n[3] = n; f.v[3] = 0u;
+            if ((e = fill4(f, st)) != cudaSuccess) return e;
+        }
         const size_t bsm = (size_t)FT_CAP * 4 + (size_t)su.Lmax * 2 * sizeof(Lev);
 
         if ((e = cudaFuncSetAttribute((const void*)k_prep_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)) != cudaSuccess)
             return e;
-        k_prep_bound<<<su.n_problems, 256, bsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.table_of,
-                                                       wk.thull, wk.thull_n);
+        if ((e = launch_pdl(k_prep_bound, dim3(su.n_problems), dim3(256), bsm, st, su, wk.probs, wk.levs, wk.hull, wk.ftab,
+                            wk.rowhdr, wk.table_of, wk.thull, wk.thull_n)) != cudaSuccess)
+            return e;
         const size_t fsm = hull_stride(su.Lmax) * sizeof(float2) + (size_t)su.Lmax * (size_t)(su.W - 2) * 24 +
                            (size_t)su.rows_max * 4 + (size_t)((su.rows_max + 31) / 32) * 4;
         if (rowlb_fused_ok(su) && fsm <= 160 * 1024) {
@@ -2206,13 +2249,16 @@ cudaError_t launch_pass1(const Setup& su, Work& wk, cudaStream_t st) {
             }
             if ((e = cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm)) != cudaSuccess)
                 return e;
-            rf<<<su.n_problems, RLF_THREADS, fsm, st>>>(su, wk.probs, wk.levs, wk.hull, wk.ftab, wk.rowhdr, wk.lbmin,
-                                                       wk.ulist, wk.ulist_n);
+            if ((e = launch_pdl(rf, dim3(su.n_problems), dim3(RLF_THREADS), fsm, st, su, wk.probs, wk.levs, wk.hull, wk.ftab,
+                                wk.rowhdr, wk.lbmin, wk.ulist, wk.ulist_n)) != cudaSuccess)
+                return e;
             if ((e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
                 return e;
             BBArgs bb{wk.ulist, wk.ulist_n, wk.lbmin, wk.inc, wk.rows_done, wk.plist, wk.plist_n, wk.wbits, wk.hull, wk.rowhdr};
             if (wk.kev[0]) cudaEventRecord(wk.kev[0], st);
-            f<<<(unsigned)grid, P1_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.feasible, bb);
+            if ((e = launch_pdl(f, dim3((unsigned)grid), dim3(P1_THREADS), smem, st, su, wk.probs, wk.levs, wk.submin,
+                                wk.feasible, bb)) != cudaSuccess)
+                return e;
             if (wk.kev[1]) cudaEventRecord(wk.kev[1], st);
             return cudaGetLastError();
         }
@@ -2282,6 +2328,8 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
                                                     const float* submin_sure, float* m32, float* m32_sure,
                                                     int32_t* bandn, uint64_t* bandlist, const uint32_t* plist,
                                                     const int32_t* plist_n, const uint32_t* wbits) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     __shared__ float rm[8], rs[8];
     __shared__ int s_cnt;
     __shared__ uint64_t s_list[BAND_CAP];
@@ -2358,9 +2406,10 @@ __global__ void __launch_bounds__(256) k_reduce_min(Setup su, const Prob* probs,
 
 cudaError_t launch_reduce_min(const Setup& su, Work& wk, cudaStream_t st) {
     const bool two = qos_float(su);
-    k_reduce_min<<<su.n_problems, 256, 0, st>>>(su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
+    cudaError_t e = launch_pdl(k_reduce_min, dim3(su.n_problems), dim3(256), 0, st, su, wk.probs, wk.submin, two ? wk.submin_sure : nullptr, wk.m32,
                                                 wk.m32_sure, wk.bandn, wk.bandlist, wk.plist, wk.plist_n,
                                                 pass1_prunable(su) ? wk.wbits : nullptr);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -2479,6 +2528,8 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
                                                const float* m32_sure, U256* hstar, U256* first,
                                                const int32_t* bandn, const uint64_t* bandlist,
                                                const float2* hull, const RowHdr* rowhdr, const uint32_t* wbits) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ U256 red[P2_THREADS];
@@ -2757,10 +2808,10 @@ cudaError_t launch_pass2_both(const Setup& su, Work& wk, cudaStream_t st) {
     size_t smem = (size_t)su.W * su.Lmax * sizeof(Lev);
     cudaError_t e = cudaFuncSetAttribute((const void*)k_pass2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_pass2<2><<<su.n_problems, P2_THREADS, smem, st>>>(su, wk.probs, wk.levs, wk.submin, wk.m32,
-                                                 qos_float(su) ? wk.m32_sure : nullptr,
-                                                 wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
-                                                 pass1_prunable(su) ? wk.wbits : nullptr);
+    e = launch_pdl(k_pass2<2>, dim3(su.n_problems), dim3(P2_THREADS), smem, st, su, wk.probs, wk.levs, wk.submin, wk.m32,
+                   qos_float(su) ? wk.m32_sure : nullptr, wk.hstar, wk.first, wk.bandn, wk.bandlist, wk.hull, wk.rowhdr,
+                   pass1_prunable(su) ? wk.wbits : nullptr);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
@@ -2777,24 +2828,29 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // materialisation (a9): one CTA per problem (thread 0: per-worker scalars; all threads: groups)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs,
-                                                     const U256* hstar, const U256* first, const int32_t* sizes,
-                                                     int C, MatOut o) {
-    const int p = blockIdx.x;
+// one warp per problem (several problems per CTA: the work is a short latency chain, so more problems in
+// flight is what matters)
+constexpr int MZ_MAXPPC = 4;
+__global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs,
+                                                                const U256* hstar, const U256* first,
+                                                                const int32_t* sizes, int C, MatOut o) {
+    pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
+    pdl_trigger();
+    const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = blockIdx.x * (blockDim.x >> 5) + wp;
+    if (p >= su.n_problems) return;   // (whole warps)
     const Prob& P = probs[p];
     const int W = su.W;
-    __shared__ int s_status;
-    __shared__ int lv[MAXW];
-    __shared__ double alpha_w[MAXW];
-    if (threadIdx.x == 0) {
-        int status = P.status;
-        if (status == 0 && (u256_is_max(first[p]) || u256_is_max(hstar[p]))) status = 1;  // infeasible
-        s_status = status;
-        if (o.status) o.status[p] = status;
-    }
-    __syncthreads();
-    if (s_status != 0) {
-        if (threadIdx.x == 0) {
+    __shared__ int lv_s[MZ_MAXPPC][MAXW];
+    __shared__ double alpha_s[MZ_MAXPPC][MAXW];
+    __shared__ int goff_s[MZ_MAXPPC][MAXW + 1];
+    int* lv = lv_s[wp];
+    double* alpha_w = alpha_s[wp];
+    int status = P.status;
+    if (status == 0 && (u256_is_max(first[p]) || u256_is_max(hstar[p]))) status = 1;  // infeasible
+    if (lane == 0 && o.status) o.status[p] = status;
+    if (status != 0) {
+        if (lane == 0) {
             if (o.index) o.index[p] = 0;
             if (o.energy_busy) o.energy_busy[p] = 0.0;
             if (o.objective) o.objective[p] = 0.0;
@@ -2803,16 +2859,16 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             if (o.energy) o.energy[p] = 0.0;
             if (o.thr) o.thr[p] = 0.0;
         }
-        for (int i = threadIdx.x; i < W; i += blockDim.x) {
+        for (int i = lane; i < W; i += 32) {
             if (o.levels) o.levels[(size_t)p * W + i] = -1;
             if (o.latency) o.latency[(size_t)p * W + i] = 0.0;
             if (o.switches) o.switches[(size_t)p * W + i] = 0;
         }
         if (o.group_sm)
-            for (int i = threadIdx.x; i < W * o.group_stride; i += blockDim.x) o.group_sm[(size_t)p * W * o.group_stride + i] = 0;
+            for (int i = lane; i < W * o.group_stride; i += 32) o.group_sm[(size_t)p * W * o.group_stride + i] = 0;
         return;
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         int l[MAXW];
         unpack_tuple(first[p], W, l);
         // mixed-radix candidate index (worker 0 most significant); all-ones if it needs > 64 bits
@@ -2871,9 +2927,9 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
         }
     }
-    __syncthreads();
+    __syncwarp();
     // per worker: switch count; per group: pool size and e_g = beta_g (1 + alpha_w)
-    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    for (int w = lane; w < W; w += 32) {
         const int t = P.table[w], G = tb.G[t];
         const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
         int sw = 0;
@@ -2883,7 +2939,7 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
     for (int w = 0; w < W; w++) {
         const int t = P.table[w], G = tb.G[t];
         const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
-        for (int g = threadIdx.x; g < o.group_stride; g += blockDim.x) {
+        for (int g = lane; g < o.group_stride; g += 32) {
             const size_t at = ((size_t)p * W + w) * o.group_stride + g;
             if (o.group_sm) o.group_sm[at] = g < G ? sizes[wit[g]] : 0;
             if (o.group_lat && g < G) o.group_lat[at] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha_w[w]);
@@ -2893,38 +2949,37 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
     // DESIGN.md R21): every worker starts at 0 and runs its groups back to back; between consecutive group
     // boundaries the power is p_idle + (p_max - p_idle) min(N, sum of the running groups' SMs) / N
     if (o.energy_busy) {
-        // all threads: the workers' group end times (sequential sums, as the run) and pool sizes in shared
-        // memory, the ends ranked into time order, then one elementary interval per rank: its busy SMs from a
-        // binary search of each worker's ends, its energy, and a block sum
+        // the workers' group end times (sequential sums, as the run) and pool sizes in shared memory, the
+        // ends ranked into time order, then one elementary interval per lane: its busy SMs from a binary
+        // search of each worker's ends, its energy, and a warp sum
         extern __shared__ __align__(8) unsigned char msm[];
         const int gs = o.gsum;
-        double* ends = reinterpret_cast<double*>(msm);     // [gs] per worker, groups in order
-        double* srt = ends + gs;                           // [gs] all ends in time order
-        int* csz = reinterpret_cast<int*>(srt + gs);       // [gs] pool size of each group
-        __shared__ int goff[MAXW + 1];
-        __shared__ double red_e[4];
-        if (threadIdx.x == 0) {
+        double* ends = reinterpret_cast<double*>(msm + (size_t)wp * (((size_t)gs * 20 + 7) & ~(size_t)7));   // [gs] per worker
+        double* srt = ends + gs;                                               // [gs] all ends in time order
+        int* csz = reinterpret_cast<int*>(srt + gs);                           // [gs] pool size of each group
+        int* goff = goff_s[wp];
+        if (lane == 0) {
             goff[0] = 0;
             for (int w = 0; w < W; w++) goff[w + 1] = goff[w] + tb.G[P.table[w]];
         }
-        __syncthreads();
+        __syncwarp();
         const int n = goff[W];
         for (int w = 0; w < W; w++) {   // every group's duration and pool size, in parallel
             const int t = P.table[w], G = tb.G[t];
             const uint8_t* wt = tb.wit[t] + (size_t)lv[w] * G;
-            for (int g = threadIdx.x; g < G; g += blockDim.x) {
+            for (int g = lane; g < G; g += 32) {
                 ends[goff[w] + g] = (double)tb.beta[t][g * C + wt[g]] * (1.0 + alpha_w[w]);
                 csz[goff[w] + g] = sizes[wt[g]];
             }
         }
-        __syncthreads();
-        for (int w = threadIdx.x; w < W; w += blockDim.x) {   // one thread per worker: its run, in order
+        __syncwarp();
+        for (int w = lane; w < W; w += 32) {   // one lane per worker: its run, in order
             double e = 0.0;
             for (int i = goff[w]; i < goff[w + 1]; i++) { e += ends[i]; ends[i] = e; }
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {   // rank of end i (ties by position): each worker's
-            const double v = ends[i];                           // ends ascend, so count by binary search
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) {   // rank of end i (ties by position): each worker's ends ascend, so
+            const double v = ends[i];           // count by binary search
             int wi = 0;
             while (goff[wi + 1] <= i) wi++;
             int rk = i - goff[wi];
@@ -2939,10 +2994,10 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             }
             srt[rk] = v;
         }
-        __syncthreads();
+        __syncwarp();
         const double Nd = (double)su.N, pi = (double)P.p_idle, pd = (double)P.p_max - (double)P.p_idle;
         double E = 0.0;
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {   // interval [srt[k-1], srt[k])
+        for (int k = lane; k < n; k += 32) {   // interval [srt[k-1], srt[k])
             const double t0 = k ? srt[k - 1] : 0.0, t1 = srt[k];
             if (!(t1 > t0)) continue;
             int busy = 0;
@@ -2957,24 +3012,23 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
             E += (pi + pd * (double)min(busy, su.N) / Nd) * (t1 - t0);
         }
         for (int off = 16; off; off >>= 1) E += __shfl_xor_sync(0xffffffffu, E, off);
-        if ((threadIdx.x & 31) == 0) red_e[threadIdx.x >> 5] = E;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += red_e[i];
-            o.energy_busy[p] = tot * 1e-9;
-        }
+        if (lane == 0) o.energy_busy[p] = E * 1e-9;
     }
 }
 
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C, MatOut out,
                                cudaStream_t st) {
-    const size_t sm = out.energy_busy ? (size_t)out.gsum * 20 : 0;   // busy-energy staging (k_materialize)
+    const size_t per = out.energy_busy ? (((size_t)out.gsum * 20 + 7) & ~(size_t)7) : 0;   // busy-energy staging per problem
+    int ppc = MZ_MAXPPC;
+    while (ppc > 1 && per * (size_t)ppc > 48 * 1024) ppc--;
+    const size_t sm = per * (size_t)ppc;
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute((const void*)k_materialize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
     }
-    k_materialize<<<su.n_problems, 128, sm, st>>>(su, tb, wk.probs, wk.levs, wk.hstar, wk.first, sizes, C, out);
+    cudaError_t e = launch_pdl(k_materialize, dim3((su.n_problems + ppc - 1) / ppc), dim3(32 * ppc), sm, st, su, tb, wk.probs,
+                               wk.levs, wk.hstar, wk.first, sizes, C, out);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -2991,24 +3045,36 @@ cudaError_t launch_table_hull(const Setup& su, const Tables& tb, Work& wk, cudaS
 cudaError_t launch_prep(const Setup& su, const Tables& tb, const PrepIn& in, Work& wk, int C, const int32_t* sizes,
                         cudaStream_t st, bool table_hull) {
     (void)C; (void)sizes;
-    k_prep_prob<<<(su.n_problems + 31) / 32, 32, 0, st>>>(su, tb, in, wk.probs);   // one warp per block: all SMs
+    cudaError_t e;
+    // one warp per block: all SMs
+    if ((e = launch_pdl(k_prep_prob, dim3((su.n_problems + 31) / 32), dim3(32), 0, st, su, tb, in, wk.probs)) != cudaSuccess)
+        return e;
     size_t n = (size_t)su.n_problems * su.W * su.Lmax;
-    k_prep_lev<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(su, tb, wk.probs, wk.levs);
+    if ((e = launch_pdl(k_prep_lev, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, su, tb, wk.probs, wk.levs)) !=
+        cudaSuccess)
+        return e;
     if (su.aux_bytes > 0) {
-        cudaError_t e;
         if (su.n_problems > 1 && wk.aslots > 0) {   // representatives of the step / inner precomputation
             const size_t ns = (size_t)wk.aslots;
-            if ((e = cudaMemsetAsync(wk.aslot, 0, ns * 8, st)) != cudaSuccess) return e;
-            if ((e = cudaMemsetAsync(wk.aslot + ns, 0xff, ns * 8, st)) != cudaSuccess) return e;
-            k_akey<<<(su.n_problems + 7) / 8, 256, 0, st>>>(su, wk.probs, wk.levs, wk.akey, wk.aslot, wk.aslots);
-            k_arep<<<(su.n_problems + 255) / 256, 256, 0, st>>>(su, wk.probs, wk.akey, wk.aslot, wk.aslots);
+            Fill4 f{};
+            f.p[0] = reinterpret_cast<unsigned*>(wk.aslot); f.n[0] = 2 * ns; f.v[0] = 0u;
+            f.p[1] = reinterpret_cast<unsigned*>(wk.aslot + ns); f.n[1] = 2 * ns; f.v[1] = 0xffffffffu;
+            if ((e = fill4(f, st)) != cudaSuccess) return e;
+            if ((e = launch_pdl(k_akey, dim3((su.n_problems + 7) / 8), dim3(256), 0, st, su, wk.probs, wk.levs, wk.akey,
+                                wk.aslot, wk.aslots)) != cudaSuccess)
+                return e;
+            if ((e = launch_pdl(k_arep, dim3((su.n_problems + 255) / 256), dim3(256), 0, st, su, wk.probs, wk.akey, wk.aslot,
+                                wk.aslots)) != cudaSuccess)
+                return e;
         }
         if (table_hull && (e = launch_table_hull(su, tb, wk, st)) != cudaSuccess) return e;
         const size_t sm = (size_t)2 * su.Lmax * sizeof(Lev) + (size_t)su.aux_bytes;
         auto f = su.mode == M_PAPER ? k_prep_aux<M_PAPER> : k_prep_aux<M_EXCL>;
         e = cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
-        f<<<su.n_problems, 256, sm, st>>>(su, wk.probs, wk.levs, in.table_of, wk.tord, wk.thull, wk.thull_n);
+        if ((e = launch_pdl(f, dim3(su.n_problems), dim3(256), sm, st, su, wk.probs, wk.levs, in.table_of, wk.tord, wk.thull,
+                            wk.thull_n)) != cudaSuccess)
+            return e;
     }
     return cudaGetLastError();
 }
