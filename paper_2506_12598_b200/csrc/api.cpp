@@ -6,6 +6,7 @@
 #include <cerrno>
 #include <cmath>
 #include <cstdarg>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -367,6 +368,7 @@ struct eclip_session {
     const eclip_profiles* prof = nullptr;
     cudaStream_t st = nullptr;
     bool own_stream = false;
+    bool keep_stream = false;            // own_stream shared by the thread's sessions (not destroyed)
     int device = 0;
     DevArena arena;
     // problem description
@@ -393,7 +395,7 @@ struct eclip_session {
             if (e) cudaEventDestroy(e);
         if (own_stream && st) {
             cudaStreamSynchronize(st);
-            cudaStreamDestroy(st);
+            if (!keep_stream) cudaStreamDestroy(st);
         }
     }
 };
@@ -426,6 +428,15 @@ static int setup_device(eclip_session* s, const eclip_options* opt) {
     }
     if (opt && opt->cuda_stream) {
         s->st = (cudaStream_t)opt->cuda_stream;
+    } else if (!s->comm && s->device < 64) {
+        // the library's own stream: one per (host thread, device), created once and kept (a stream per call costs
+        // more than the small plans it serves); sessions of a communicator group get their own (their collectives
+        // must not queue behind each other)
+        static thread_local cudaStream_t cached[64] = {};
+        if (!cached[s->device]) CU(cudaStreamCreateWithFlags(&cached[s->device], cudaStreamNonBlocking));
+        s->st = cached[s->device];
+        s->own_stream = true;
+        s->keep_stream = true;
     } else {
         CU(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
         s->own_stream = true;
@@ -456,6 +467,7 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
         int rc = build_host_table(P, specs[i], &s->tabs[i]);
         if (rc) return rc;
     }
+    host_mark("host tables");
     const int nt = (int)specs.size();
     struct Off { size_t beta, need, V, best, barg, bstar, sidx, wtmp, outS, outB, outW; };
     std::vector<Off> off(nt);
@@ -544,6 +556,7 @@ static int build_tables(eclip_session* s, const std::vector<TableSpec>& specs) {
     int32_t* dL = (int32_t*)at(o_L);
     s->tabL.resize(nt);
     CU(cudaMemcpyAsync(s->tabL.data(), dL, 4 * nt, cudaMemcpyDeviceToHost, s->st));
+    host_mark("K1 launched");
     CU(cudaStreamSynchronize(s->st));   // level counts size the enumeration
     s->tb.n = nt; s->tb.L = dL; s->tb.K = (const int64_t*)at(o_K); s->tb.G = (const int32_t*)at(o_G);
     s->tb.S = (const int64_t* const*)at(o_S); s->tb.B = (const int64_t* const*)at(o_B);
@@ -873,6 +886,7 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
     s->W = W; s->n = 1; s->C = C;
     rc = setup_device(s.get(), opt);
     if (rc) return rc;
+    host_mark("setup_device");
     bool has_qos = false;
     if (pr->qos_ns)
         for (int w = 0; w < W; w++) has_qos |= !std::isinf(pr->qos_ns[w]);
@@ -882,12 +896,14 @@ static int session_from_problem(const eclip_profiles* P, const eclip_problem* pr
     s->su.weighted = unequal ? 1 : 0;
     rc = build_tables(s.get(), specs);
     if (rc) return rc;
+    host_mark("build_tables (K1, synced)");
     s->h_table_of = table_of;
     set_wide(s.get(), table_of);
     rc = plan_geometry(s.get(), opt);
     if (rc) return rc;
     rc = alloc_work(s.get());
     if (rc) return rc;
+    host_mark("geometry + alloc_work");
     // per-problem inputs
     int32_t* dtab; double* dq = nullptr; float* dM = nullptr;
     CU(s->arena.alloc(&dtab, W));
@@ -1528,6 +1544,7 @@ extern "C" int eclip_session_create_problem(const eclip_profiles* prof, const ec
     eclip_session* s = nullptr;
     int rc = session_from_problem(prof, problem, opt, &s);
     if (rc) { delete s; return rc; }
+    host_mark("session_from_problem");
     if (s->engine == ECLIP_ENGINE_SLICE) {
         cudaError_t e = slice_setup(s->slice, s->su, s->tb, s->wk, s->tabL.data(), s->h_table_of.data(), s->st);
         if (e == cudaErrorNotSupported) {
@@ -1545,16 +1562,31 @@ extern "C" int eclip_session_finish_problem(eclip_session* s, const uint64_t* gl
     return plan_one(s, r, global_first_index);
 }
 
+void eclip::host_mark(const char* label) {
+    static const bool on = std::getenv("ECLIP_HOST_TIMING") != nullptr;
+    static thread_local std::chrono::steady_clock::time_point t0;
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    if (!label) { t0 = t; return; }
+    std::fprintf(stderr, "[eclip host] %-28s %9.1f us\n", label,
+                 std::chrono::duration<double, std::micro>(t - t0).count());
+}
+
 extern "C" int eclip_plan(const eclip_profiles* prof, const eclip_problem* problem, const eclip_options* opt,
                           eclip_result* r) {
     if (!r) return fail(ECLIP_E_INVALID_ARG, "null result");
+    host_mark(nullptr);
     eclip_session* s = nullptr;
     int rc = eclip_session_create_problem(prof, problem, opt, &s);
     if (rc) return rc;
+    host_mark("session created");
     std::unique_ptr<eclip_session> guard(s);
     rc = run_all_steps(s);
     if (rc) return rc;
-    return plan_one(s, r, nullptr);
+    host_mark("steps launched");
+    rc = plan_one(s, r, nullptr);
+    host_mark("result on host");
+    return rc;
 }
 
 // ------------------------------------------------------------------------------------------

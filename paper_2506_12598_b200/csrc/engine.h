@@ -8,6 +8,10 @@
 
 namespace eclip {
 
+// host-side checkpoints for diagnosing per-call overhead: with ECLIP_HOST_TIMING set in the environment,
+// host_mark("label") prints the microseconds since the last host_mark(nullptr) reset to stderr
+void host_mark(const char* label);
+
 constexpr int MAXW = 16;        // workers per problem (API limit)
 constexpr int MAXW_ENUM = 8;    // workers per problem on the ENUM engine
 constexpr int P1_THREADS = 256; // pass-1 CTA size

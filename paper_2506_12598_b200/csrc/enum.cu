@@ -2828,17 +2828,19 @@ cudaError_t launch_pass2_first(const Setup& su, Work& wk, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // materialisation (a9): one CTA per problem (thread 0: per-worker scalars; all threads: groups)
 // ------------------------------------------------------------------------------------------
-// one warp per problem (several problems per CTA: the work is a short latency chain, so more problems in
-// flight is what matters)
+// LPP = 32: one warp per problem, several problems per CTA (batches: the work is a short latency chain, so
+// more problems in flight is what matters); LPP = 128: a CTA per problem (few problems with many groups)
 constexpr int MZ_MAXPPC = 4;
-__global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs,
-                                                                const U256* hstar, const U256* first,
-                                                                const int32_t* sizes, int C, MatOut o) {
+template <int LPP>
+__global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const Prob* probs, const Lev* levs,
+                                                     const U256* hstar, const U256* first, const int32_t* sizes, int C,
+                                                     MatOut o) {
     pdl_wait();      // (programmatic dependent launch: the predecessor's results are visible)
     pdl_trigger();
-    const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int p = blockIdx.x * (blockDim.x >> 5) + wp;
-    if (p >= su.n_problems) return;   // (whole warps)
+    const int wp = LPP == 32 ? (int)(threadIdx.x >> 5) : 0, lane = LPP == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    const int p = LPP == 32 ? (int)(blockIdx.x * (blockDim.x >> 5)) + wp : (int)blockIdx.x;
+    auto gsync = [&]() { if (LPP == 32) __syncwarp(); else __syncthreads(); };
+    if (p >= su.n_problems) return;   // (whole warps / CTAs)
     const Prob& P = probs[p];
     const int W = su.W;
     __shared__ int lv_s[MZ_MAXPPC][MAXW];
@@ -2859,13 +2861,13 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
             if (o.energy) o.energy[p] = 0.0;
             if (o.thr) o.thr[p] = 0.0;
         }
-        for (int i = lane; i < W; i += 32) {
+        for (int i = lane; i < W; i += LPP) {
             if (o.levels) o.levels[(size_t)p * W + i] = -1;
             if (o.latency) o.latency[(size_t)p * W + i] = 0.0;
             if (o.switches) o.switches[(size_t)p * W + i] = 0;
         }
         if (o.group_sm)
-            for (int i = lane; i < W * o.group_stride; i += 32) o.group_sm[(size_t)p * W * o.group_stride + i] = 0;
+            for (int i = lane; i < W * o.group_stride; i += LPP) o.group_sm[(size_t)p * W * o.group_stride + i] = 0;
         return;
     }
     if (lane == 0) {
@@ -2927,9 +2929,9 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
             for (int i = 0; i < 4; i++) o.key[(size_t)p * 4 + i] = k.w[i];
         }
     }
-    __syncwarp();
+    gsync();
     // per worker: switch count; per group: pool size and e_g = beta_g (1 + alpha_w)
-    for (int w = lane; w < W; w += 32) {
+    for (int w = lane; w < W; w += LPP) {
         const int t = P.table[w], G = tb.G[t];
         const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
         int sw = 0;
@@ -2939,7 +2941,7 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
     for (int w = 0; w < W; w++) {
         const int t = P.table[w], G = tb.G[t];
         const uint8_t* wit = tb.wit[t] + (size_t)lv[w] * G;
-        for (int g = lane; g < o.group_stride; g += 32) {
+        for (int g = lane; g < o.group_stride; g += LPP) {
             const size_t at = ((size_t)p * W + w) * o.group_stride + g;
             if (o.group_sm) o.group_sm[at] = g < G ? sizes[wit[g]] : 0;
             if (o.group_lat && g < G) o.group_lat[at] = (double)tb.beta[t][g * C + wit[g]] * (1.0 + alpha_w[w]);
@@ -2962,23 +2964,23 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
             goff[0] = 0;
             for (int w = 0; w < W; w++) goff[w + 1] = goff[w] + tb.G[P.table[w]];
         }
-        __syncwarp();
+        gsync();
         const int n = goff[W];
         for (int w = 0; w < W; w++) {   // every group's duration and pool size, in parallel
             const int t = P.table[w], G = tb.G[t];
             const uint8_t* wt = tb.wit[t] + (size_t)lv[w] * G;
-            for (int g = lane; g < G; g += 32) {
+            for (int g = lane; g < G; g += LPP) {
                 ends[goff[w] + g] = (double)tb.beta[t][g * C + wt[g]] * (1.0 + alpha_w[w]);
                 csz[goff[w] + g] = sizes[wt[g]];
             }
         }
-        __syncwarp();
-        for (int w = lane; w < W; w += 32) {   // one lane per worker: its run, in order
+        gsync();
+        for (int w = lane; w < W; w += LPP) {   // one lane per worker: its run, in order
             double e = 0.0;
             for (int i = goff[w]; i < goff[w + 1]; i++) { e += ends[i]; ends[i] = e; }
         }
-        __syncwarp();
-        for (int i = lane; i < n; i += 32) {   // rank of end i (ties by position): each worker's ends ascend, so
+        gsync();
+        for (int i = lane; i < n; i += LPP) {   // rank of end i (ties by position): each worker's ends ascend, so
             const double v = ends[i];           // count by binary search
             int wi = 0;
             while (goff[wi + 1] <= i) wi++;
@@ -2994,10 +2996,10 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
             }
             srt[rk] = v;
         }
-        __syncwarp();
+        gsync();
         const double Nd = (double)su.N, pi = (double)P.p_idle, pd = (double)P.p_max - (double)P.p_idle;
         double E = 0.0;
-        for (int k = lane; k < n; k += 32) {   // interval [srt[k-1], srt[k])
+        for (int k = lane; k < n; k += LPP) {   // interval [srt[k-1], srt[k])
             const double t0 = k ? srt[k - 1] : 0.0, t1 = srt[k];
             if (!(t1 > t0)) continue;
             int busy = 0;
@@ -3012,22 +3014,40 @@ __global__ void __launch_bounds__(32 * MZ_MAXPPC) k_materialize(Setup su, Tables
             E += (pi + pd * (double)min(busy, su.N) / Nd) * (t1 - t0);
         }
         for (int off = 16; off; off >>= 1) E += __shfl_xor_sync(0xffffffffu, E, off);
-        if (lane == 0) o.energy_busy[p] = E * 1e-9;
+        if (LPP == 32) {
+            if (lane == 0) o.energy_busy[p] = E * 1e-9;
+        } else {
+            __shared__ double red_e[4];
+            if ((threadIdx.x & 31) == 0) red_e[threadIdx.x >> 5] = E;
+            __syncthreads();
+            if (threadIdx.x == 0) o.energy_busy[p] = (red_e[0] + red_e[1] + red_e[2] + red_e[3]) * 1e-9;
+        }
     }
 }
 
 cudaError_t launch_materialize(const Setup& su, const Tables& tb, Work& wk, const int32_t* sizes, int C, MatOut out,
                                cudaStream_t st) {
     const size_t per = out.energy_busy ? (((size_t)out.gsum * 20 + 7) & ~(size_t)7) : 0;   // busy-energy staging per problem
+    cudaError_t e;
+    if (su.n_problems < 148 * 4) {   // few problems: a CTA each
+        if (per > 48 * 1024 &&
+            (e = cudaFuncSetAttribute((const void*)k_materialize<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per)) !=
+                cudaSuccess)
+            return e;
+        e = launch_pdl(k_materialize<128>, dim3(su.n_problems), dim3(128), per, st, su, tb, wk.probs, wk.levs, wk.hstar,
+                       wk.first, sizes, C, out);
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
     int ppc = MZ_MAXPPC;
     while (ppc > 1 && per * (size_t)ppc > 48 * 1024) ppc--;
     const size_t sm = per * (size_t)ppc;
     if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute((const void*)k_materialize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        e = cudaFuncSetAttribute((const void*)k_materialize<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
     }
-    cudaError_t e = launch_pdl(k_materialize, dim3((su.n_problems + ppc - 1) / ppc), dim3(32 * ppc), sm, st, su, tb, wk.probs,
-                               wk.levs, wk.hstar, wk.first, sizes, C, out);
+    e = launch_pdl(k_materialize<32>, dim3((su.n_problems + ppc - 1) / ppc), dim3(32 * ppc), sm, st, su, tb, wk.probs,
+                   wk.levs, wk.hstar, wk.first, sizes, C, out);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -4,6 +4,7 @@
 // through (T', S'_w), so with T' fixed the SUM objective separates into per-worker terms.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -483,6 +484,7 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     CK(cudaMemcpyAsync(&P, wk.probs, sizeof(Prob), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lev.data(), wk.levs, lev.size() * sizeof(Lev), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    host_mark("slice_setup: records on host");
     SliceDev& S = s.h;
     S.W = W; S.Lmax = su.Lmax; S.mode = su.mode; S.obj = su.obj;
     S.shard = su.shard; S.n_shards = su.n_shards;
@@ -500,24 +502,35 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     }
     int64_t g = 0;
     for (int w = 0; w < W; w++)
-        for (int l = 0; l < P.L[w]; l++) g = std::gcd(g, (int64_t)lev[(size_t)w * su.Lmax + l].S);
+        for (int l = 0; l < P.L[w]; l++) {
+            const int64_t v = lev[(size_t)w * su.Lmax + l].S;
+            if (g == 0 || v % g != 0) g = std::gcd(g, v);   // (one division for the common multiples)
+        }
     if (g == 0) g = 1;
     S.gS = g;
+    host_mark("slice_setup: gcd");
     std::vector<int16_t> dense;
+    std::vector<int32_t> q((size_t)W * su.Lmax);   // S' / g (exact quotients, one division each)
     for (int w = 0; w < W; w++) {
         int mn = INT32_MAX, mx = 0;
         for (int l = 0; l < P.L[w]; l++) {
-            int v = (int)(lev[(size_t)w * su.Lmax + l].S / g);
+            const int v = (int)(lev[(size_t)w * su.Lmax + l].S / g);
+            q[(size_t)w * su.Lmax + l] = v;
             mn = std::min(mn, v); mx = std::max(mx, v);
         }
         S.smin[w] = mn; S.smax[w] = mx;
         S.doff[w] = (int32_t)dense.size();
         size_t base = dense.size();
         dense.resize(base + (mx - mn + 1), -1);
-        for (int l = 0; l < P.L[w]; l++) dense[base + lev[(size_t)w * su.Lmax + l].S / g - mn] = (int16_t)l;
+        for (int l = 0; l < P.L[w]; l++) dense[base + q[(size_t)w * su.Lmax + l] - mn] = (int16_t)l;
     }
     if (su.Lmax > 32767) return cudaErrorInvalidValue;
     S.gtot = (int32_t)dense.size();
+    host_mark("slice_setup: dense");
+    {
+        static const bool on = std::getenv("ECLIP_HOST_TIMING") != nullptr;
+        if (on) std::fprintf(stderr, "[eclip host] slice W %d Lmax %d gtot %d g %lld\n", W, su.Lmax, S.gtot, (long long)g);
+    }
     S.plo[0] = 0; S.phi[0] = 0;
     for (int w = 0; w < W; w++) { S.plo[w + 1] = S.plo[w] + S.smin[w]; S.phi[w + 1] = S.phi[w] + S.smax[w]; }
     S.slo[W] = 0; S.shi[W] = 0;
@@ -533,13 +546,19 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
                 if (h > lim) return cudaErrorNotSupported;   // -> ECLIP_E_TOO_LARGE (use ENUM)
             }
     }
+    // the widest D range over all slices: per worker, hi(T) - lo(T) + 1 = min(shi, T - plo) - max(slo, T - phi) + 1
+    // is concave and piecewise linear in T, so its maximum over [Tlo, Thi] is at an end or a breakpoint
     int64_t mr = 1;
-    for (int64_t T = S.Tlo; T <= S.Thi; T++)
-        for (int w = 1; w < W; w++) {
+    for (int w = 1; w < W; w++) {
+        const int64_t cand[4] = {S.Tlo, S.Thi, S.shi[w] + S.plo[w], S.slo[w] + S.phi[w]};
+        for (int64_t T : cand) {
+            T = std::min<int64_t>(std::max<int64_t>(T, S.Tlo), S.Thi);
             int64_t lo = std::max(S.slo[w], T - S.phi[w]), hi = std::min(S.shi[w], T - S.plo[w]);
             mr = std::max<int64_t>(mr, hi - lo + 1);
         }
+    }
     S.maxrange = (int32_t)mr;
+    host_mark("slice_setup: ranges");
     int pad = 1;
     for (int w = 0; w < W; w++) pad = std::max(pad, S.smax[w] - S.smin[w] + 1);
     S.pad = pad + RB + KU;
@@ -562,6 +581,7 @@ cudaError_t slice_setup(SliceState& s, const Setup& su, const Tables& tb, Work& 
     s.nband = (int32_t*)(blk + o_nband);
     s.scratch = (uint64_t*)(blk + o_scr);
     CK(cudaMemcpyAsync(s.dense, dense.data(), dense.size() * 2, cudaMemcpyHostToDevice, st));
+    host_mark("slice_setup: done");
     return cudaSuccess;
 }
 
