@@ -23,8 +23,15 @@ metrics = ["gpu__time_duration.sum", "sm__inst_issued.avg.pct_of_peak_sustained_
            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
            "launch__shared_mem_per_block_dynamic", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
-out = subprocess.run(["ncu", "-i", os.path.join(src, "step_full.ncu-rep"), "--page", "raw", "--csv", "--metrics",
-                      ",".join(metrics)], capture_output=True, text=True).stdout
+rep = os.path.join(src, "step_full.ncu-rep")
+if os.path.exists(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(metrics)],
+                         capture_output=True, text=True).stdout
+else:   # summarised on the box (tools/gpu_final.sh): every raw metric of every kernel
+    out = open(os.path.join(src, "step_full_raw.csv")).read()
+for extra in os.listdir(src):   # per-line stall samples and raw CSVs written on the box
+    if extra.startswith("lines_") or extra.endswith("_raw.csv"):
+        shutil.copy(os.path.join(src, extra), os.path.join(dst, f"{rp}_{extra}"))
 rows = list(csv.reader(out.splitlines()))
 h, units = rows[0], rows[1]
 idx = [h.index("Kernel Name")] + [h.index(m) for m in metrics]

@@ -18,4 +18,15 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_
    python tools/profile_driver.py c5 --mixes 4096 --reps 1 > $out/ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_levels|k_slice_f32|k_slice_exact" -c 3 -o $out/c4_full \
    python tools/profile_driver.py c4 --reps 1 > $out/ncu_c4full.log 2>&1
+# summaries on the box (the reports are too large to bring back whole): raw metrics of every kernel and
+# per-line stall samples of the top kernels; only the pass-1 / K3 reports themselves travel back
+ncu -i $out/step_full.ncu-rep --page raw --csv > $out/step_full_raw.csv 2>/dev/null
+ncu -i $out/c4_full.ncu-rep --page raw --csv > $out/c4_full_raw.csv 2>/dev/null
+for k in k_pass1_fast k_rowlb_fused k_pass2 k_prep_aux k_materialize; do
+  python tools/ncu_lines.py $out/step_full.ncu-rep $k 40 > $out/lines_$k.txt 2>&1
+done
+for k in k_levels k_slice_f32 k_slice_exact; do python tools/ncu_lines.py $out/c4_full.ncu-rep $k 40 > $out/lines_c4_$k.txt 2>&1; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_pass1_fast -c 1 -o $out/pass1_full \
+   python tools/profile_driver.py c5 --mixes 4096 --reps 1 > $out/ncu_p1.log 2>&1
+rm -f $out/step_full.ncu-rep $out/c4_full.ncu-rep
 ls -la $out
