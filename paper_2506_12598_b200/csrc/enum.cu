@@ -1746,7 +1746,9 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                     X2[i] = f2pack(X, X); Y2[i] = f2pack(Y, Y); Z2[i] = f2pack(Z, Z);
                 }
                 nfeas += (unsigned long long)nv * (unsigned long long)Lin;
-                for (int p = 0; p < np2; p++) {
+                // pairs p and p + 1 per iteration: accumulator 2i takes even pairs, 2i + 1 odd ones (static register
+                // indices; an index computed from p would put the accumulators in local memory)
+                auto pair = [&](int p, int par) {
                     const float4 r = A.ip[p];
                     const u64 Bp = f2pack(r.x, r.y), Sp = f2pack(r.z, r.w);
                     u64 dd = 0;
@@ -1756,9 +1758,15 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
                         const u64 base = MODE == M_PAPER ? add2(X2[i], dd) : X2[i];
                         float k0, k1;
                         f2unpack(fma2(Bp, Y2[i], fma2(Sp, Z2[i], base)), k0, k1);
-                        acc[2 * i + (p & 1)] = fminf(acc[2 * i + (p & 1)], fminf(k0, k1));
+                        acc[2 * i + par] = fminf(acc[2 * i + par], fminf(k0, k1));
                     }
+                };
+                int p = 0;
+                for (; p + 2 <= np2; p += 2) {
+                    pair(p, 0);
+                    pair(p + 1, 1);
                 }
+                if (p < np2) pair(p, 0);
                 if (Lin & 1) {  // trailing odd element
                     const float4 r = A.ip[Lin >> 1];
                     const float d = MODE == M_PAPER ? A.iD[Lin >> 1].x : 0.0f;
