@@ -499,6 +499,32 @@ def test_planner_every_mix_vs_oracle_golden_host_and_device():
     pl.close()
 
 
+def test_planner_pinned_outputs_written_by_the_kernel():
+    """Host batches whose output arrays are all page-locked: k_materialize writes them directly (mapped
+    memory, no staging copies); every mix against the oracle's stored answers and equal, field by field, to
+    the same batch planned into unpinned host arrays (staging + copies) and into device arrays"""
+    import torch
+    import golden_c5
+    models, ids, qos = synth.make_c5(1000, seed=5)
+    pr = ec.Profiles.from_models(models)
+    pl = ec.Planner(pr, n_models=4, max_problems=1000, total_sms=148, p_idle_w=200.0, p_max_w=1000.0)
+    pinned = ec.alloc_batch_out(1000, 4, 16, pinned=True)
+    plain = ec.alloc_batch_out(1000, 4, 16)
+    dev = ec.alloc_batch_out(1000, 4, 16, device="cuda")
+    for _ in range(2):   # (the second call reuses the planner's buffers)
+        pl.plan(torch.from_numpy(ids).pin_memory().numpy(), torch.from_numpy(qos).pin_memory().numpy(), out=pinned)
+        pl.plan(ids, qos, out=plain)
+        pl.plan(torch.from_numpy(ids).cuda(), torch.from_numpy(qos).cuda(), out=dev)
+        torch.cuda.synchronize()
+        assert golden_c5.check_batch(ids, pinned, sizes=models[0].sizes) == 1000
+        for k, v in pinned.items():
+            if k.startswith("_"):
+                continue
+            assert np.array_equal(np.asarray(v), np.asarray(plain[k])), k
+            assert np.array_equal(np.asarray(v), dev[k].cpu().numpy().view(np.asarray(v).dtype)), k
+    pl.close()
+
+
 def test_planner_other_settings_vs_oracle():
     """planners without QoS, in PAPER mode with masks, and MATRIX (generic kernels) against the oracle"""
     masks = [0xFF, 0xFE, 0x7F, 0xFF, 0x3C, 0xFF, 0xF0]
