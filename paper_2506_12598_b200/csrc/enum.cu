@@ -1095,8 +1095,11 @@ __global__ void __launch_bounds__(256) k_rowlb(Setup su, const Prob* probs, cons
 
 constexpr int BB_NB = 256;
 constexpr float BB_SCALE = 1024.0f;
-__device__ __forceinline__ int bb_bucket(float lb, float lbm) {
-    const float r = __fmul_rn(__fsub_rn(__fdiv_rn(lb, lbm), 1.0f), BB_SCALE);
+// bucket of a bound: floor((lb / lbm - 1) BB_SCALE), the quotient as lb times the correctly rounded reciprocal of
+// lbm (every caller passes inv = __frcp_rn(lbm), so list building and the stop test agree exactly; the product's
+// rounding is far inside bb_edge's one bucket of slack)
+__device__ __forceinline__ int bb_bucket(float lb, float inv) {
+    const float r = __fmul_rn(__fsub_rn(__fmul_rn(lb, inv), 1.0f), BB_SCALE);
     return r <= 0.0f ? 0 : (r >= (float)(BB_NB - 1) ? BB_NB - 1 : (int)r);
 }
 // a value <= every bound in bucket b (one bucket of slack covers the rounding of bb_bucket)
@@ -1226,9 +1229,10 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         if (threadIdx.x == 0) ulist_n[prob] = 0;
         return;
     }
+    const float bminv = __frcp_rn(bm);
     // bucket histogram and scatter over the rows with a finite bound only (one bitmap word per thread)
     for (int wd = threadIdx.x; wd < nwords; wd += blockDim.x)
-        for (uint32_t m = fbit[wd]; m; m &= m - 1) atomicAdd(&hist[bb_bucket(lbs[wd * 32 + __ffs(m) - 1], bm)], 1);
+        for (uint32_t m = fbit[wd]; m; m &= m - 1) atomicAdd(&hist[bb_bucket(lbs[wd * 32 + __ffs(m) - 1], bminv)], 1);
     __syncthreads();
     if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
         int v[BB_NB / 32], t = 0;
@@ -1245,7 +1249,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         for (uint32_t m = fbit[wd]; m; m &= m - 1) {
             const uint32_t r = (uint32_t)(wd * 32 + __ffs(m) - 1);
             const float lb = lbs[r];
-            out[atomicAdd(&cur[bb_bucket(lb, bm)], 1)] = make_uint2(r, __float_as_uint(lb));
+            out[atomicAdd(&cur[bb_bucket(lb, bminv)], 1)] = make_uint2(r, __float_as_uint(lb));
         }
 }
 
@@ -1400,11 +1404,12 @@ __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, con
     const int nseg = P.nseg;
     const float* rlb = rowlb + (size_t)prob * su.rows_max;
     const float lbm = __uint_as_float(lbmin[prob]);
+    const float lbminv = __frcp_rn(lbm);
     for (int i = threadIdx.x; i < BB_NB; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (uint64_t u = ua + threadIdx.x; u < ub; u += blockDim.x) {
         const float lb = rlb[nseg == 1 ? u : u / (uint64_t)nseg];
-        if (lb < INFINITY) atomicAdd(&hist[bb_bucket(lb, lbm)], 1);
+        if (lb < INFINITY) atomicAdd(&hist[bb_bucket(lb, lbminv)], 1);
     }
     __syncthreads();
     if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
@@ -1420,7 +1425,7 @@ __global__ void __launch_bounds__(256) k_bucket(Setup su, const Prob* probs, con
     uint2* out = ulist + (size_t)blockIdx.x * su.upi;
     for (uint64_t u = ua + threadIdx.x; u < ub; u += blockDim.x) {
         const float lb = rlb[nseg == 1 ? u : u / (uint64_t)nseg];
-        if (lb < INFINITY) out[atomicAdd(&cur[bb_bucket(lb, lbm)], 1)] = make_uint2((unsigned)(u - ua), __float_as_uint(lb));
+        if (lb < INFINITY) out[atomicAdd(&cur[bb_bucket(lb, lbminv)], 1)] = make_uint2((unsigned)(u - ua), __float_as_uint(lb));
     }
 }
 
@@ -1668,7 +1673,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (!pend) {   // entries are bucket-ordered: the rest of the list lies above this bucket's edge
                 float mn = lb;
                 for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                if (wl == 0 && bb_edge(bb_bucket(mn, lbm), lbm) > bnd) atomicMax(&s_next, lcnt);   // stop the CTA
+                if (wl == 0 && bb_edge(bb_bucket(mn, __frcp_rn(lbm)), lbm) > bnd) atomicMax(&s_next, lcnt);   // stop the CTA
                 continue;
             }
         } else {
