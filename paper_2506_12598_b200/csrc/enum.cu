@@ -1230,9 +1230,19 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         return;
     }
     const float bminv = __frcp_rn(bm);
-    // bucket histogram and scatter over the rows with a finite bound only (one bitmap word per thread)
-    for (int wd = threadIdx.x; wd < nwords; wd += blockDim.x)
-        for (uint32_t m = fbit[wd]; m; m &= m - 1) atomicAdd(&hist[bb_bucket(lbs[wd * 32 + __ffs(m) - 1], bminv)], 1);
+    // bucket histogram and scatter over the rows with a finite bound, a row per lane (warp w takes bitmap words
+    // w, w + 16, ...); the last bucket -- every bound >= 1.249 x the smallest, most rows -- counted and placed with
+    // one atomic per warp, the others with one per row
+    const int warp = threadIdx.x >> 5;
+    for (int wd = warp; wd < nwords; wd += RLF_THREADS / 32) {
+        const uint32_t fw = fbit[wd];
+        if (!fw) continue;
+        const bool has = (fw >> lane) & 1u;
+        const int b = has ? bb_bucket(lbs[wd * 32 + lane], bminv) : -1;
+        const unsigned top = __ballot_sync(0xffffffffu, b == BB_NB - 1);
+        if (has && b != BB_NB - 1) atomicAdd(&hist[b], 1);
+        if (lane == 0 && top) atomicAdd(&hist[BB_NB - 1], __popc(top));
+    }
     __syncthreads();
     if (threadIdx.x < 32) {   // exclusive scan of the 256 counts (8 per lane)
         int v[BB_NB / 32], t = 0;
@@ -1245,12 +1255,22 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     }
     __syncthreads();
     uint2* out = ulist + (size_t)prob * su.upi;
-    for (int wd = threadIdx.x; wd < nwords; wd += blockDim.x)
-        for (uint32_t m = fbit[wd]; m; m &= m - 1) {
-            const uint32_t r = (uint32_t)(wd * 32 + __ffs(m) - 1);
-            const float lb = lbs[r];
-            out[atomicAdd(&cur[bb_bucket(lb, bminv)], 1)] = make_uint2(r, __float_as_uint(lb));
+    for (int wd = warp; wd < nwords; wd += RLF_THREADS / 32) {
+        const uint32_t fw = fbit[wd];
+        if (!fw) continue;
+        const bool has = (fw >> lane) & 1u;
+        const uint32_t r = (uint32_t)(wd * 32 + lane);
+        const float lb = has ? lbs[r] : INFINITY;
+        const int b = has ? bb_bucket(lb, bminv) : -1;
+        const unsigned top = __ballot_sync(0xffffffffu, b == BB_NB - 1);
+        int p0 = 0;
+        if (lane == 0 && top) p0 = atomicAdd(&cur[BB_NB - 1], __popc(top));
+        p0 = __shfl_sync(0xffffffffu, p0, 0);
+        if (has) {
+            const int pos = b == BB_NB - 1 ? p0 + __popc(top & ((1u << lane) - 1u)) : atomicAdd(&cur[b], 1);
+            out[pos] = make_uint2(r, __float_as_uint(lb));
         }
+    }
 }
 
 __global__ void k_fill_u32(unsigned* p, size_t n, unsigned v) {
