@@ -379,7 +379,7 @@ def main():
             "phases_ms": phase_ms,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_max / a.steps, "api": "eclip_planner_plan (host batch, pinned buffers)"},
-            # per step: k_prep_prob, k_prep_lev, k_akey, k_arep, k_prep_aux, 2 x k_fill_u32, k_prep_bound,
+            # per step: k_prep_prob, k_prep_lev, k_fill4, k_akey, k_arep, k_prep_aux, k_fill4, k_prep_bound,
             # k_rowlb_fused, k_pass1_fast, k_reduce_min, k_pass2, k_materialize (profiles/ launch list)
             "gpu_launches": int(13 * a.steps),
             "roofline": {"bound": "alu", "kernel": "k_pass1_fast<W=4,EXCLUDE_SELF,QoS,pruned>", "achieved": achieved,
