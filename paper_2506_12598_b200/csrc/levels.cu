@@ -160,6 +160,27 @@ __device__ __forceinline__ void rank_level(const LevelJob& J, int l, int L) {
     for (int g = 0; g < J.G; g++) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
 }
 
+// the same with one warp per level: the lanes split the comparisons (L / 32 each) and the witness bytes
+__device__ __forceinline__ void rank_level_warp(const LevelJob& J, int l, int L, int lane) {
+    const int nw = nwords(J);
+    const uint64_t* a = J.wtmp + (size_t)l * nw;
+    int rk = 0;
+    for (int m = lane; m < L; m += 32) {
+        const uint64_t* b = J.wtmp + (size_t)m * nw;
+        for (int q = 0; q < nw; q++) {
+            const uint64_t bq = b[q], aq = a[q];
+            if (bq != aq) { rk += (bq < aq); break; }
+        }
+    }
+    for (int o = 16; o; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+    const int s = J.sidx[l];
+    if (lane == 0) {
+        J.outS[rk] = (int64_t)s * J.u;
+        J.outB[rk] = J.bstar[s];
+    }
+    for (int g = lane; g < J.G; g += 32) J.outW[(size_t)rk * J.G + g] = (uint8_t)(a[g >> 3] >> (8 * (7 - (g & 7))));
+}
+
 // B*(s) = best over j of layer 0 at r = R; compact the attained levels (one CTA per table)
 template <class VT>
 __device__ __forceinline__ void compact_table(const LevelJob& J) {
@@ -280,11 +301,12 @@ __global__ void __launch_bounds__(256) k_levels(const LevelJob* __restrict__ job
     // per table with the table's witness words staged in shared memory (the comparisons are
     // O(L^2); from global memory each thread would walk L dependent L2 loads) ----
     extern __shared__ uint64_t wsm[];
-    if (wsm_words == 0) {   // large tables: one thread per level over the whole grid, from global memory
-        for (int i = gtid; i < nlev; i += gstride) {
+    if (wsm_words == 0) {   // large tables: one warp per level over the whole grid, from global memory (L1-resident)
+        const int lane = threadIdx.x & 31;
+        for (int i = gtid >> 5; i < nlev; i += gstride >> 5) {
             int t = 0;
             while (off[t + 1] <= i) t++;
-            rank_level(sj[t], i - off[t], off[t + 1] - off[t]);
+            rank_level_warp(sj[t], i - off[t], off[t + 1] - off[t], lane);
         }
         return;
     }
