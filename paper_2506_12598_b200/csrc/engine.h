@@ -34,6 +34,21 @@ enum Mode { M_EXCL = 0, M_PAPER = 1, M_EXCESS = 2, M_MATRIX = 3 };
 // still runs.  Every kernel so launched calls pdl_wait() before it reads anything its predecessor wrote
 // (and before it exits, so that its completion implies the predecessor's), then pdl_trigger() to let its
 // own successor be scheduled.  Outside such a launch both are no-ops.
+// ECLIP_CHECK: device-side bounds checks of a test build (-DECLIP_BOUNDS; compute-sanitizer is not available on
+// the GPU pool): a failed check prints its site and traps, so the calling test fails.  Nothing otherwise.
+#ifdef ECLIP_BOUNDS
+#define ECLIP_CHECK(c)                                                                                      \
+    do {                                                                                                    \
+        if (!(c)) {                                                                                         \
+            printf("ECLIP_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__,          \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                      \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define ECLIP_CHECK(c) do { } while (0)
+#endif
+
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(256) k_prep_aux(Setup su, const Prob* probs, L
         }
         if (threadIdx.x == 0) *A.ihn = nh;
         __syncthreads();
+        ECLIP_CHECK((size_t)(A.ht + HT_NB - aux_s) <= su.aux_bytes && nh <= Lmax);
         build_slope_table(A.ie, nh, A.ht, A.htb, threadIdx.x, blockDim.x);
         for (int k = threadIdx.x; k < Lin; k += blockDim.x) {   // last vertex with S' <= S'_k (exact ints)
             const int sk = inner[A.perm[k]].S;
@@ -1156,6 +1157,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     uint32_t Lh[NH > 0 ? NH : 1];
 #pragma unroll
     for (int w = 0; w < NH; w++) Lh[w] = (uint32_t)P.L[w];
+    ECLIP_CHECK(rows <= (uint32_t)su.rows_max && (NH != 2 || rows == Lh[0] * Lh[NH > 1 ? 1 : 0]));
     auto feasible = [&](int hT, int hTm) -> bool {
         if (!QOS) return true;
         if (H.tn > 0) return ft[hT - H.t0] <= hTm - hT;
@@ -1188,6 +1190,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
                 if (d0 * L1 > r) d0--;
                 else if ((d0 + 1) * L1 <= r) d0++;
                 const int d1 = r - d0 * L1 + Lmax;
+                ECLIP_CHECK(d0 >= 0 && d0 < (int)Lh[0] && d1 >= Lmax && d1 < Lmax + L1);
                 const int hT = hS[d0] + hS[d1];
                 if (feasible(hT, min(hTx[d0], hTx[d1]))) {
                     // two hi workers: sum_w B_w (hT - S'_w) = B_0 S'_1 + B_1 S'_0, non-negative terms (rounding
@@ -1239,6 +1242,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         if (!fw) continue;
         const bool has = (fw >> lane) & 1u;
         const int b = has ? bb_bucket(lbs[wd * 32 + lane], bminv) : -1;
+        ECLIP_CHECK(!has || (wd * 32 + lane < (int)rows && b >= 0 && b < BB_NB));
         const unsigned top = __ballot_sync(0xffffffffu, b == BB_NB - 1);
         if (has && b != BB_NB - 1) atomicAdd(&hist[b], 1);
         if (lane == 0 && top) atomicAdd(&hist[BB_NB - 1], __popc(top));
@@ -1268,6 +1272,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
         p0 = __shfl_sync(0xffffffffu, p0, 0);
         if (has) {
             const int pos = b == BB_NB - 1 ? p0 + __popc(top & ((1u << lane) - 1u)) : atomicAdd(&cur[b], 1);
+            ECLIP_CHECK(pos >= 0 && pos < (int)rows && (size_t)pos < (size_t)su.upi);
             out[pos] = make_uint2(r, __float_as_uint(lb));
         }
     }
@@ -1679,6 +1684,7 @@ k_pass1_fast(Setup su, const Prob* __restrict__ probs, const Lev* __restrict__ l
             if (b0 >= lcnt) break;
             const int e = b0 + wl;
             const uint2 en = e < lcnt ? lst[e] : make_uint2(0u, 0x7f800000u);
+            ECLIP_CHECK(lcnt <= su.upi && (e >= lcnt || ua + en.x < ub));
             loff = en.x;
             const float lb = __uint_as_float(en.y);
             lbv = lb;
@@ -2729,6 +2735,7 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
         }
     };
     const int nband = bandn ? bandn[prob] : -1;
+    ECLIP_CHECK(nband <= BAND_CAP);
     auto scan = [&](int phase, U256& best, uint64_t& besti) {
         const U256 hs = s_hs;
         if (nband >= 0) {   // the band's units, listed in index order by k_reduce_min
@@ -3027,6 +3034,7 @@ __global__ void __launch_bounds__(128) k_materialize(Setup su, Tables tb, const 
                 }
                 rk += lo - goff[w];
             }
+            ECLIP_CHECK(rk >= 0 && rk < n && n <= gs);
             srt[rk] = v;
         }
         gsync();
