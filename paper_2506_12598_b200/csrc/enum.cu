@@ -991,7 +991,7 @@ __device__ __forceinline__ float hull_min_in(const float2* v, const float2* ed, 
         if (v[mid].y <= c) a = mid; else b = mid - 1;
     }
     const float2 p = v[a], q = v[a + 1];
-    const float B = fmaf(q.x - p.x, (c - p.y) / (q.y - p.y), p.x);
+    const float B = fmaf(q.x - p.x, __fdividef(c - p.y, q.y - p.y), p.x);   // (2 ulp: inside the bound's margin)
     return fmaf(B, y, c * z);
 }
 
@@ -1012,7 +1012,7 @@ __device__ __forceinline__ float hull_min_pos(const AuxView& A, int n, float y, 
     const int a = A.hpos[below ? ka : kb];
     if (a >= n - 1) return fmaf(v[n - 1].x, y, c * z);
     const float2 p = v[a], q = v[a + 1];
-    const float B = fmaf(q.x - p.x, (c - p.y) / (q.y - p.y), p.x);
+    const float B = fmaf(q.x - p.x, __fdividef(c - p.y, q.y - p.y), p.x);   // (2 ulp: inside the bound's margin)
     return fmaf(fmaxf(B, q.x), y, c * z);
 }
 
