@@ -130,17 +130,34 @@ __host__ __device__ __forceinline__ uint64_t rows_of(const int* L, int W) {
 }
 __host__ __device__ __forceinline__ int lstep_of(const int* L, int W) { return W >= 2 ? L[W - 2] : 1; }
 
+// a / b and a % b for b < 2^31: the 32-bit operations when a fits (the 64-bit ones are a software routine)
+__host__ __device__ __forceinline__ uint64_t udiv_small(uint64_t a, uint32_t b, uint32_t* rem) {
+    if ((a >> 32) == 0) {
+        const uint32_t x = (uint32_t)a, q = x / b;
+        *rem = x - q * b;
+        return q;
+    }
+    const uint64_t q = a / b;
+    *rem = (uint32_t)(a - q * b);
+    return q;
+}
+
 __host__ __device__ __forceinline__ void shard_items(uint64_t n_items, int shard, int n_shards, uint64_t* lo,
                                                      uint64_t* hi) {
+    if (n_shards == 1) {
+        *lo = 0;
+        *hi = n_items;
+        return;
+    }
     *lo = n_items * (uint64_t)shard / (uint64_t)n_shards;
     *hi = n_items * (uint64_t)(shard + 1) / (uint64_t)n_shards;
 }
 
 // unit -> (row, step-digit range [e0, e1))
 __device__ __forceinline__ void unit_range(const Prob& P, uint64_t unit, uint64_t* row, int* e0, int* e1) {
-    *row = unit / (uint64_t)P.nseg;
-    int sg = (int)(unit % (uint64_t)P.nseg);
-    int a = sg * P.seglen, b = a + P.seglen;
+    uint32_t sg;
+    *row = udiv_small(unit, (uint32_t)P.nseg, &sg);
+    int a = (int)sg * P.seglen, b = a + P.seglen;
     if (b > P.Lstep) b = P.Lstep;
     *e0 = a;
     *e1 = b;
@@ -149,8 +166,9 @@ __device__ __forceinline__ void unit_range(const Prob& P, uint64_t unit, uint64_
 // row -> hi digits d[0..W-3] (worker 0 most significant)
 __device__ __forceinline__ void decode_row(uint64_t row, const int* L, int W, int* d) {
     for (int w = W - 3; w >= 0; w--) {
-        d[w] = (int)(row % (uint64_t)L[w]);
-        row /= (uint64_t)L[w];
+        uint32_t r;
+        row = udiv_small(row, (uint32_t)L[w], &r);
+        d[w] = (int)r;
     }
 }
 
@@ -1178,6 +1196,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
     float bm = INFINITY;
     const int nwords = (int)((rows + 31) >> 5);
     const int lane = threadIdx.x & 31;
+    const float rL1 = __frcp_rn((float)Lh[NH > 1 ? 1 : 0]);
     for (int r0 = threadIdx.x - lane; r0 < (int)rows; r0 += RLF_THREADS) {
         const int r = r0 + lane;
         float lb = INFINITY;
@@ -1186,7 +1205,7 @@ __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Pro
                 // rows = (d0, d1), d1 least significant; d0 = r / L1 from a float quotient corrected by one
                 // step (r < 2^24)
                 const int L1 = (int)Lh[1];
-                int d0 = __float2int_rz((float)r * (1.0f / (float)L1));
+                int d0 = __float2int_rz((float)r * rL1);
                 if (d0 * L1 > r) d0--;
                 else if ((d0 + 1) * L1 <= r) d0++;
                 const int d1 = r - d0 * L1 + Lmax;
@@ -2782,7 +2801,11 @@ __global__ void __launch_bounds__(P2_THREADS, P2_MINB) k_pass2(Setup su, Prob* p
         if (idx == ~0ull) first[prob] = u256_max();
         else {
             int lv[MAXW_ENUM];
-            for (int w = W - 1; w >= 0; w--) { lv[w] = (int)(idx % (uint64_t)L[w]); idx /= (uint64_t)L[w]; }
+            for (int w = W - 1; w >= 0; w--) {
+                uint32_t r;
+                idx = udiv_small(idx, (uint32_t)L[w], &r);
+                lv[w] = (int)r;
+            }
             first[prob] = pack_tuple(lv, W);
         }
     };
