@@ -1129,7 +1129,10 @@ __device__ __forceinline__ float bb_edge(int b, float lbm) { return b <= 1 ? 0.0
 // one CTA per problem computes every row's bound into shared memory (hi records and hull staged
 // there), the problem's minimum bound, and the bucket-ordered unit list -- the bounds never go
 // to global memory.  Same arithmetic as k_rowlb + k_bucket.
-constexpr int RLF_THREADS = 512;
+#ifndef RLF_THREADS_N
+#define RLF_THREADS_N 512
+#endif
+constexpr int RLF_THREADS = RLF_THREADS_N;
 constexpr int RLF_ROWS_CAP = 24576;
 template <int NW, bool QOS>
 __global__ void __launch_bounds__(RLF_THREADS) k_rowlb_fused(Setup su, const Prob* probs, const Lev* levs,

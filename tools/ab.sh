@@ -5,4 +5,4 @@ timeout 300 python tools/timeline.py --out $out/tl_default.json > $out/tl_defaul
 for v in "$@"; do
   ECLIP_LIB=$PWD/paper_2506_12598_b200/libeclip_$v.so timeout 300 python tools/timeline.py --out $out/tl_$v.json > $out/tl_$v.txt 2>&1
 done
-for f in $out/tl_*.txt; do echo "== $f"; grep -A40 "step 2" $f | grep "pass1_fast\|rowlb\|busy"; done
+for f in $out/tl_*.txt; do echo "== $f"; grep -A40 "step 2" $f | grep "pass1_fast\|rowlb\|pass2\|busy"; done
